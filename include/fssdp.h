@@ -1,0 +1,303 @@
+/* fssdp.h — C-ABI of libfssdp, the B200-native FSSDP (Hecate, arXiv 2502.02581) hot path.
+ *
+ * Two halves live behind this one header:
+ *
+ *   1. The host placement planner, bit-exact with the reference `moesim` package
+ *      (/root/reference/pkg/src/moesim).  Every planner entry point names the
+ *      reference function it replaces (file:line).  Placements cross the boundary as
+ *      dense chunk-major masks  mask[c * D + d] != 0  <=>  (chunk c, device d) is held.
+ *
+ *   2. The device data plane (sm_100a kernels): gate top-k/load count, counts
+ *      all-gather, SparseAllGather / SparseReduceScatter over peer HBM, token
+ *      dispatch/combine by routing index, and the tcgen05 grouped expert GEMM.
+ *      The reference has no device code; these implement the paper's
+ *      semantics.
+ *
+ * Conventions:
+ *   - plain pointers, sizes and a cudaStream_t (passed as void*); no torch types;
+ *   - every function returns an int status: 0 ok, negative = error class below,
+ *     mapped onto the reference error taxonomy (errors.py:8-53);
+ *   - no allocation inside device entry points: workspaces come from the caller;
+ *   - stream-ordered, one host thread per rank, no host callbacks;
+ *   - peer-visible buffers live in a per-rank "symmetric heap" allocated with
+ *     fssdp_heap_alloc; buffers sit at identical offsets on every rank, so a peer
+ *     address is  peer_bases[rank] + offset  (peer_bases is a DEVICE array of
+ *     world_size uint64 base addresses, own rank included).
+ */
+#ifndef FSSDP_H_
+#define FSSDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ------------------------------------------------------------------ status codes */
+#define FSSDP_OK 0
+#define FSSDP_ERR_DIMENSION (-1)     /* moesim.errors.DimensionError            errors.py:20 */
+#define FSSDP_ERR_INVALID_PAIR (-2)  /* moesim.errors.InvalidPairError          errors.py:28 */
+#define FSSDP_ERR_ORPHAN_EXPERT (-3) /* moesim.errors.OrphanExpertError         errors.py:32 */
+#define FSSDP_ERR_CUDA (-4)          /* CUDA runtime / launch failure (no reference analogue) */
+#define FSSDP_ERR_INTERNAL (-5)      /* moesim.errors.InternalError             errors.py:52 */
+#define FSSDP_ERR_INFEASIBLE (-6)    /* moesim.errors.InfeasibleSlotsError      errors.py:48 */
+#define FSSDP_ERR_EMPTY_HISTORY (-7) /* moesim.errors.EmptyHistoryError         errors.py:36 */
+#define FSSDP_ERR_DIM_MISMATCH (-8)  /* moesim.errors.DimensionMismatchError    errors.py:40 */
+
+/* Verdict reasons (placement.py:26-28) */
+#define FSSDP_VERDICT_OK 0
+#define FSSDP_VERDICT_MISSING_CHUNK 1
+#define FSSDP_VERDICT_DUPLICATE_OWNER 2
+#define FSSDP_VERDICT_DROPPED_ENTRY 3
+
+/* Library version string and the message of the last error on this thread. */
+const char* fssdp_version(void);
+const char* fssdp_last_error(void);
+
+/* ================================================================== planner (host)
+ * Topology = ClusterTopology (topology.py:14-49). */
+typedef struct fssdp_topology {
+  int32_t nodes;
+  int32_t devices_per_node;
+  double intra_bw; /* bytes/s */
+  double inter_bw; /* bytes/s */
+  double alpha;    /* s */
+} fssdp_topology;
+
+/* make_even_partition (placement.py:155-170): owner_out[c] for c in [0, num_chunks). */
+int fssdp_make_even_partition(int32_t num_chunks, int32_t num_devices, int32_t* owner_out);
+
+/* ShardPlan.even (placement.py:260-284): owner_out[l * experts + e]. */
+int fssdp_shard_plan_even(int32_t layers, int32_t experts, int32_t devices, int32_t* owner_out);
+
+/* validate_spag_pair / validate_sprs_pair (placement.py:200-211).
+ * kind 0 = SpAG (pre partition, pre ⊆ post), 1 = SpRS (post partition, post ⊆ pre).
+ * verdict_out[3] = {reason, chunk, device} (chunk/device = -1 when absent). */
+int fssdp_validate_pair(int32_t kind, int32_t num_chunks, int32_t num_devices,
+                        const uint8_t* pre_mask, const uint8_t* post_mask, int32_t* verdict_out);
+
+/* spag_traffic / sprs_traffic (costmodel.py:87-132).  matrix_out is D*D row-major
+ * [src, dst] bytes; report_out[4] = {sparsity, total_interdevice_bytes,
+ * bottleneck_device, bottleneck_bytes} (SparsityReport, costmodel.py:60-84).
+ * Returns FSSDP_ERR_INVALID_PAIR (with the verdict in fssdp_last_error) on bad pairs. */
+int fssdp_spag_traffic(int32_t num_chunks, int32_t num_devices, const uint8_t* pre_mask,
+                       const uint8_t* post_mask, double chunk_bytes, double* matrix_out,
+                       double* report_out);
+int fssdp_sprs_traffic(int32_t num_chunks, int32_t num_devices, const uint8_t* pre_mask,
+                       const uint8_t* post_mask, double chunk_bytes, double* matrix_out,
+                       double* report_out);
+
+/* collective_latency (costmodel.py:149-182). */
+int fssdp_collective_latency(int32_t num_devices, const double* matrix, const fssdp_topology* topo,
+                             double* seconds_out);
+
+/* overlap_degree (costmodel.py:185-194). */
+int fssdp_overlap_degree(double t_nonmoe, const fssdp_topology* topo, double expert_bytes,
+                         int64_t* t_out);
+
+/* build_dispatch (dispatch.py:49-97): counts[D*E] (non-negative integers),
+ * placement mask [E*D] -> route_out[D*E*D] (route[s, e, d]). */
+int fssdp_build_dispatch(int32_t num_devices, int32_t num_experts, const int64_t* counts,
+                         const uint8_t* placement_mask, const fssdp_topology* topo,
+                         int64_t* route_out);
+
+/* estimate_moe_latency (planner.py:205-216) on integral tokens[D*E]. */
+int fssdp_estimate_moe_latency(int32_t num_devices, int32_t num_experts, const uint8_t* placement_mask,
+                               const int64_t* tokens, const fssdp_topology* topo, double token_bytes,
+                               double per_token_expert_time, double* seconds_out);
+
+/* sparse_materialization (planner.py:171-197): base (a partition) + per-expert loads[E]
+ * -> target mask [E*D] and added_per_device[D]. */
+int fssdp_sparse_materialization(int32_t num_experts, int32_t num_devices, const uint8_t* base_mask,
+                                 const double* per_expert_loads, int64_t t, int64_t m,
+                                 const fssdp_topology* topo, uint8_t* target_out,
+                                 int32_t* added_out);
+
+/* calibrate (planner.py:228-276).  plan = (source, target) masks; actual[D*E] (float64).
+ * out: accepted_out, new target mask, added_out[D], doubles_out[3] =
+ * {extra_seconds, estimate_before, estimate_after}. */
+int fssdp_calibrate(int32_t num_experts, int32_t num_devices, const uint8_t* source_mask,
+                    const uint8_t* target_mask, const double* actual, int64_t remaining_m,
+                    double t_remaining, const fssdp_topology* topo, double chunk_bytes,
+                    double token_bytes, double per_token_expert_time, int32_t* accepted_out,
+                    uint8_t* target_out, int32_t* added_out, double* doubles_out);
+
+/* heterogeneous_sharding (planner.py:302-385): profile[L*E] -> owner_out[L*E]. */
+int fssdp_heterogeneous_sharding(int32_t layers, int32_t experts, const double* profile, int64_t t,
+                                 const fssdp_topology* topo, int32_t* owner_out);
+
+/* estimate_loads (planner.py:32-42): mean of the last `window` of `n` stacked D*E
+ * matrices (history is n*D*E row-major, oldest first). */
+int fssdp_estimate_loads(int32_t n, int32_t rows, int32_t cols, const double* history,
+                         int32_t window, double* mean_out);
+
+/* One FSSDP layer-iteration decision, FssdpState.run_iteration per layer
+ * (engine.py:491-553): adoption gate, calibration, fallback, then build_dispatch on the
+ * actual counts.  Inputs: base partition owner[E], estimate est[D*E] (NULL = empty
+ * history), actual counts[D*E] (int64), knobs.  Outputs: final target mask [E*D],
+ * added[D], route[D*E*D], doubles_out[4] = {spag_lat, sprs_lat, remat_lat, calib_time},
+ * flags_out[2] = {adopted_candidate, calibration_accepted}. */
+typedef struct fssdp_layer_knobs {
+  int64_t t;                    /* overlap degree (experts) */
+  int64_t m;                    /* per-device replica capacity (experts) */
+  int32_t calibration;          /* Policy.calibration */
+  int32_t rematerialize;        /* Policy.rematerialize */
+  double expert_bytes;          /* ModelConfig.expert_bytes */
+  double token_bytes;           /* ModelConfig.token_bytes */
+  double attn_fwd_time;         /* ModelConfig.attn_fwd_time */
+  double per_token_expert_time; /* ModelConfig.per_token_expert_time */
+} fssdp_layer_knobs;
+
+int fssdp_plan_layer(int32_t num_experts, const int32_t* base_owner, const double* est,
+                     const int64_t* actual, const fssdp_topology* topo,
+                     const fssdp_layer_knobs* knobs, uint8_t* target_out, int32_t* added_out,
+                     int64_t* route_out, double* doubles_out, int32_t* flags_out);
+
+/* FssdpState._shard_score (engine.py:431-442), numpy summation order included:
+ * score_out[2] = {max node load, max device load}. */
+int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, const double* profile,
+                      const fssdp_topology* topo, double* score_out);
+
+/* ================================================================== device data plane */
+
+/* GEMM group descriptor (one local expert = one group); see gemm_sm100.cu. */
+typedef struct fssdp_gemm_group {
+  int32_t m_tiles;    /* 128-row tiles along M */
+  int32_t tile_start; /* exclusive prefix of m_tiles * n_tiles over groups */
+  int32_t a_m;        /* A tensor-map coordinate of the group's M origin */
+  int32_t a_k;        /* A tensor-map coordinate of the group's K origin */
+  int32_t b_n;        /* B tensor-map coordinate of the group's N origin */
+  int32_t b_k;        /* B tensor-map coordinate of the group's K origin */
+  int32_t k_blocks;   /* number of 64-wide K blocks (0 => C tile written as zeros) */
+  int32_t pad_;
+  int64_t c_off;      /* element offset of the group's C[0, 0] */
+} fssdp_gemm_group;
+
+#define FSSDP_EPI_BF16 0  /* C = bf16(acc) */
+#define FSSDP_EPI_GELU 1  /* C = bf16(acc) (pre-activation), C2 = bf16(gelu(C)) */
+#define FSSDP_EPI_DGELU 2 /* C = bf16(acc * gelu'(aux)) */
+#define FSSDP_EPI_F32 3   /* C = acc (fp32) */
+
+/* Grouped GEMM  C_g = A_g · B_g  on tcgen05 (K5/K7).  A and B are bf16 2-D tensors
+ * described by (inner, outer) element extents (inner contiguous).  a_mn / b_mn select
+ * the operand major-ness: 0 = K-major (A: [M][K], B: [N][K]), 1 = MN-major
+ * (A: [K][M], B: [K][N]).  N (= n_tiles * 256) is shared by every group.
+ * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum. */
+int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
+                       int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
+                       const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
+                       int32_t total_tiles, void* c, void* c2, const void* aux, int64_t ldc,
+                       void* stream);
+
+#define FSSDP_GATE_TILE 64 /* tokens per gate CTA (slot ranks are tile-relative) */
+
+/* K1: logits = x · Wgᵀ (fp32), top-k (ties -> lower expert id), renormalised softmax
+ * weights, tile-relative slot ranks (token-slot order (t, j) ascending) and per-tile
+ * expert histograms.  x [T*d] bf16, wg [E*d] fp32.  logits may be NULL.
+ * tile_counts[ceil(T/64) * E]. */
+int fssdp_gate_topk(const void* x, const float* wg, int64_t T, int32_t d, int32_t E, int32_t k,
+                    float* logits, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
+                    int32_t* tile_counts, void* stream);
+
+/* Top-k / weights / ranks only, from given fp32 logits [T*E] (same semantics as K1's
+ * tail; used to pin K1's selection bit-exactly against the CPU oracle). */
+int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k, int32_t* topk_idx,
+                           float* topk_w, int32_t* slot_rank, int32_t* tile_counts, void* stream);
+
+/* K2: exclusive scan of tile_counts over tiles (tile_prefix, same shape), this rank's
+ * per-expert totals, and the counts all-gather: the row is stored into every peer's
+ * D x E int32 table at heap offset table_off (row = rank), followed by a device
+ * barrier (barrier slot `bar_slot`, value `epoch`). */
+int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
+                               int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
+                               int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
+                               uint32_t epoch, void* stream);
+
+/* Device barrier across the world (system-scope release/acquire on flag pads). */
+int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, int32_t world,
+                  int32_t bar_slot, uint32_t epoch, void* stream);
+
+/* K4: dispatch.  For token-slot (t, j) with expert e and global rank r within
+ * (this source, e) [tile_prefix + slot_rank], the destination d is the first with
+ * route_cum[e*(D+1) + d + 1] > r and the row lands at recv_base[e*D + d] + r - route_cum[..d].
+ * x rows (bf16, d_model wide) are pushed into peer d's receive buffer (heap offset
+ * recv_off).  slot_dest/slot_pos record the destination for the combine.  zero_rows
+ * ([n_zero * 2] {row, count}) lists this rank's own padding rows, zeroed here.
+ * Ends with a device barrier. */
+int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_rank,
+                   const int32_t* tile_prefix, int64_t T, int32_t d_model, int32_t E, int32_t k,
+                   int32_t world, const int32_t* route_cum, const int32_t* recv_base,
+                   int32_t* slot_dest, int32_t* slot_pos, const uint64_t* peer_bases,
+                   int64_t recv_off, const int32_t* zero_rows, int32_t n_zero,
+                   int64_t flags_off, int32_t rank, int32_t bar_slot, uint32_t epoch,
+                   uint32_t* grid_counter, void* stream);
+
+/* K6: combine.  y[t] = sum_j w[t, j] * Y_{dest}[pos]  (fp32, j ascending) -> bf16.
+ * Y rows are pulled from peer heaps (offset y_off). */
+int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float* topk_w,
+                  int64_t T, int32_t d_model, int32_t k, const uint64_t* peer_bases, int64_t y_off,
+                  void* y_out, void* stream);
+
+/* K7 (token side of backward): for every slot, g[t, j] = <dy_t, Y_slot> (fp32) and
+ * bf16(w[t, j] * dy_t) is pushed to the slot's destination dY receive buffer
+ * (heap offset dy_recv_off).  Zeroes own padding rows, ends with a device barrier. */
+int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
+                        const float* topk_w, int64_t T, int32_t d_model, int32_t k,
+                        const uint64_t* peer_bases, int64_t y_off, int64_t dy_recv_off,
+                        float* slot_grad, const int32_t* zero_rows, int32_t n_zero,
+                        int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
+                        uint32_t epoch, uint32_t* grid_counter, void* stream);
+
+/* K7 (gate + combine side of backward):
+ *   dlogit[t, j] = w_j (g_j - sum_i w_i g_i)            (renormalised top-k softmax)
+ *   dx[t] = sum_j dXe_{dest}[pos] + sum_j dlogit[t, j] * Wg[idx_j]     -> bf16
+ * dXe rows are pulled from peer heaps (offset dxe_off).  dlogit_out [T*k] fp32. */
+int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const int32_t* topk_idx,
+                     const float* topk_w, const float* slot_grad, const float* wg, int64_t T,
+                     int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
+                     int64_t dxe_off, float* dlogit_out, void* dx_out, void* stream);
+
+/* Gate weight gradient dWg[e] = sum_t dlogit[t, e] x[t]  (fixed order; fp32 [E*d]).
+ * workspace: fp32 [FSSDP_WG_SPLITS * E * d]. */
+#define FSSDP_WG_SPLITS 16
+int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
+                     int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
+                     void* stream);
+
+/* K3: SparseAllGather.  copies[n * 3] = {src_rank, src_slot, dst_slot}: pull
+ * slot_bytes from peer src_rank's heap (offset param_off + src_slot * slot_bytes) into
+ * this rank's heap (param_off + dst_slot * slot_bytes).  128-bit coalesced loads. */
+int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
+               const int32_t* copies, int32_t n_copies, void* stream);
+
+/* K8: SparseReduceScatter.  jobs[n * 3] = {dst_slot, src_begin, src_count};
+ * srcs[* 2] = {rank, slot} in ascending rank order (owner included):
+ *   own[dst_slot] = sum over srcs (fp32, listed order).  slot_elems fp32 per slot. */
+int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t slot_elems,
+               const int32_t* jobs, int32_t n_jobs, const int32_t* srcs, void* stream);
+
+/* ================================================================== symmetric heap */
+/* cudaMalloc'd, zero-initialised heap (bytes rounded up to 2 MiB). */
+int fssdp_heap_alloc(size_t bytes, void** ptr_out);
+int fssdp_heap_free(void* ptr);
+/* CUDA IPC: 64-byte handle of a heap, and mapping a peer's handle into this process. */
+int fssdp_ipc_handle(void* ptr, uint8_t* handle_out /* 64 bytes */);
+int fssdp_ipc_open(const uint8_t* handle /* 64 bytes */, void** ptr_out);
+int fssdp_ipc_close(void* ptr);
+/* Number of SMs of the current device. */
+int fssdp_num_sms(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSSDP_H_ */

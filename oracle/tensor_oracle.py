@@ -1,0 +1,153 @@
+"""numpy restatement of the FSSDP tensor path — TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+The reference moesim package models tensors as byte counts only, so this
+restates the paper's semantics; parity here is UNPINNED by reference tests:
+
+* gate: logits = x · Wgᵀ, top-k with ties to the lower expert id, GShard-style
+  renormalised softmax over the selected logits;
+  no capacity factor / token dropping.
+* dispatch: token-slot order (t, j) ascending fills the destinations of a
+  (source, expert) cell in ascending device order with the build_dispatch counts
+  route[s, e, d] (dispatch.py:49-97 gives the counts; the per-token order is ours).
+* expert FFN: A = X·W1ᵀ, H = gelu_tanh(A), Y = H·W2ᵀ, bf16 storage,
+  fp32 accumulation.
+* combine: y_t = Σ_j w_tj · Y_tj in fp32, j ascending, then bf16.
+* SpAG: replica = owner copy; SpRS: owner = Σ replicas in ascending device order, fp32
+  (PAPER.md:370-386).
+
+Functions that the kernels reproduce bit-for-bit use explicit float32 operations in
+the kernels' order (selection, ranks, positions, combine, SpAG, SpRS).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+GATE_TILE = 64
+
+
+# ------------------------------------------------------------------ bf16 helpers
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> nearest bf16 (round half to even), returned as float32."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    r = ((u + 0x7FFF + lsb) >> 16) << 16
+    out = r.astype(np.uint32).view(np.float32).copy()
+    nan = np.isnan(a)
+    out[nan] = np.nan
+    return out
+
+
+def bf16_bits_to_f32(bits: np.ndarray) -> np.ndarray:
+    return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+# ------------------------------------------------------------------ gate
+def gate_logits(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
+    """fp32 logits [T, E] (float64 accumulation; compared within tolerance)."""
+    return (x.astype(np.float64) @ wg.astype(np.float64).T).astype(np.float32)
+
+
+def topk_select(logits: np.ndarray, k: int):
+    """Top-k selection, weights, tile-relative slot ranks and per-tile histograms.
+
+    Mirrors K1's tail exactly: selection by repeated scan with strict '>' (ties ->
+    lower expert id); e_j = exp(l_j - l_top1) in float32; s accumulated j ascending;
+    w_j = e_j / s.  Ranks count earlier slots (t, j) of the same expert in the tile."""
+    lg = np.asarray(logits, dtype=np.float32)
+    T, E = lg.shape
+    idx = np.empty((T, k), dtype=np.int32)
+    for t in range(T):
+        row = lg[t]
+        taken = np.zeros(E, dtype=bool)
+        for j in range(k):
+            best, bi = np.float32(0), -1
+            for e in range(E):
+                if taken[e]:
+                    continue
+                if bi < 0 or row[e] > best:
+                    best, bi = row[e], e
+            taken[bi] = True
+            idx[t, j] = bi
+    sel = np.take_along_axis(lg, idx.astype(np.int64), axis=1)
+    m = sel[:, :1]
+    ex = np.exp((sel - m).astype(np.float32)).astype(np.float32)
+    s = np.zeros(T, dtype=np.float32)
+    for j in range(k):
+        s = (s + ex[:, j]).astype(np.float32)
+    w = (ex / s[:, None]).astype(np.float32)
+    tiles = (T + GATE_TILE - 1) // GATE_TILE
+    rank = np.empty((T, k), dtype=np.int32)
+    tile_counts = np.zeros((max(tiles, 1), E), dtype=np.int32)
+    for tile in range(tiles):
+        cnt = np.zeros(E, dtype=np.int64)
+        for t in range(tile * GATE_TILE, min(T, (tile + 1) * GATE_TILE)):
+            for j in range(k):
+                e = idx[t, j]
+                rank[t, j] = cnt[e]
+                cnt[e] += 1
+        tile_counts[tile] = cnt
+    return idx, w, rank, tile_counts
+
+
+def expert_counts(idx: np.ndarray, E: int) -> np.ndarray:
+    return np.bincount(idx.reshape(-1), minlength=E).astype(np.int64)
+
+
+# ------------------------------------------------------------------ activation
+def gelu_tanh(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.float64)
+    return 0.5 * x * (1.0 + np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def gelu_tanh_grad(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.float64)
+    k0, k1 = 0.7978845608028654, 0.044715
+    t = np.tanh(k0 * (x + k1 * x ** 3))
+    return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * k0 * (1.0 + 3.0 * k1 * x * x)
+
+
+# ------------------------------------------------------------------ dispatch / combine
+def slot_positions(idx: np.ndarray, route: np.ndarray, src: int, recv_base: np.ndarray):
+    """Destination device and receive row of every token-slot of source `src`.
+
+    route[s, e, d] (build_dispatch counts); recv_base[e, d] = first receive row of
+    (src, e) on device d.  Slots of one expert are taken in (t, j) order and fill
+    destinations in ascending device order."""
+    T, k = idx.shape
+    D = route.shape[2]
+    dest = np.empty((T, k), dtype=np.int32)
+    pos = np.empty((T, k), dtype=np.int32)
+    seen = np.zeros(route.shape[1], dtype=np.int64)
+    for t in range(T):
+        for j in range(k):
+            e = idx[t, j]
+            r = seen[e]
+            seen[e] += 1
+            cum = np.concatenate([[0], np.cumsum(route[src, e])])
+            d = 0
+            while d + 1 < D and cum[d + 1] <= r:
+                d += 1
+            dest[t, j] = d
+            pos[t, j] = recv_base[e, d] + (r - cum[d])
+    return dest, pos
+
+
+def combine(rows: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """rows [T, k, d] (bf16 values as float32), w [T, k] -> bf16(Σ_j w_j·rows_j), exact
+    float32 order of the kernel (acc += w*y, j ascending, no FMA)."""
+    T, k, d = rows.shape
+    acc = np.zeros((T, d), dtype=np.float32)
+    for j in range(k):
+        prod = (w[:, j:j + 1].astype(np.float32) * rows[:, j, :].astype(np.float32)).astype(np.float32)
+        acc = (acc + prod).astype(np.float32)
+    return bf16_round(acc)
+
+
+def sprs_sum(contribs: list[np.ndarray]) -> np.ndarray:
+    """Owner's reduced gradient: float32 sum in the listed (ascending device) order."""
+    acc = np.zeros_like(contribs[0], dtype=np.float32)
+    for c in contribs:
+        acc = (acc + c.astype(np.float32)).astype(np.float32)
+    return acc

@@ -1,0 +1,149 @@
+"""ctypes binding of libfssdp.so (include/fssdp.h).
+
+The product path has no fallback: if the shared library is missing or a symbol is
+absent, importing this module raises.  `build()` in __graft_entry__.py (or
+`python -m paper_2502_02581_b200.build`) produces the library in-tree.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+from .errors import raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "libfssdp.so"
+HEADER = Path(__file__).resolve().parent.parent / "include" / "fssdp.h"
+
+i32, i64, u32, f64, vp = C.c_int32, C.c_int64, C.c_uint32, C.c_double, C.c_void_p
+P_i32 = C.POINTER(C.c_int32)
+P_i64 = C.POINTER(C.c_int64)
+P_u8 = C.POINTER(C.c_uint8)
+P_f64 = C.POINTER(C.c_double)
+P_f32 = C.POINTER(C.c_float)
+
+
+class Topology(C.Structure):
+    _fields_ = [
+        ("nodes", C.c_int32),
+        ("devices_per_node", C.c_int32),
+        ("intra_bw", C.c_double),
+        ("inter_bw", C.c_double),
+        ("alpha", C.c_double),
+    ]
+
+
+class LayerKnobs(C.Structure):
+    _fields_ = [
+        ("t", C.c_int64),
+        ("m", C.c_int64),
+        ("calibration", C.c_int32),
+        ("rematerialize", C.c_int32),
+        ("expert_bytes", C.c_double),
+        ("token_bytes", C.c_double),
+        ("attn_fwd_time", C.c_double),
+        ("per_token_expert_time", C.c_double),
+    ]
+
+
+class GemmGroup(C.Structure):
+    _fields_ = [
+        ("m_tiles", C.c_int32),
+        ("tile_start", C.c_int32),
+        ("a_m", C.c_int32),
+        ("a_k", C.c_int32),
+        ("b_n", C.c_int32),
+        ("b_k", C.c_int32),
+        ("k_blocks", C.c_int32),
+        ("pad_", C.c_int32),
+        ("c_off", C.c_int64),
+    ]
+
+
+P_topo = C.POINTER(Topology)
+
+# name -> argtypes (every function returns int status unless listed in _RESTYPE)
+_SIGS = {
+    "fssdp_version": [],
+    "fssdp_last_error": [],
+    "fssdp_num_sms": [],
+    # planner
+    "fssdp_make_even_partition": [i32, i32, P_i32],
+    "fssdp_shard_plan_even": [i32, i32, i32, P_i32],
+    "fssdp_validate_pair": [i32, i32, i32, P_u8, P_u8, P_i32],
+    "fssdp_spag_traffic": [i32, i32, P_u8, P_u8, f64, P_f64, P_f64],
+    "fssdp_sprs_traffic": [i32, i32, P_u8, P_u8, f64, P_f64, P_f64],
+    "fssdp_collective_latency": [i32, P_f64, P_topo, P_f64],
+    "fssdp_overlap_degree": [f64, P_topo, f64, P_i64],
+    "fssdp_build_dispatch": [i32, i32, P_i64, P_u8, P_topo, P_i64],
+    "fssdp_estimate_moe_latency": [i32, i32, P_u8, P_i64, P_topo, f64, f64, P_f64],
+    "fssdp_sparse_materialization": [i32, i32, P_u8, P_f64, i64, i64, P_topo, P_u8, P_i32],
+    "fssdp_calibrate": [i32, i32, P_u8, P_u8, P_f64, i64, f64, P_topo, f64, f64, f64, P_i32, P_u8,
+                        P_i32, P_f64],
+    "fssdp_heterogeneous_sharding": [i32, i32, P_f64, i64, P_topo, P_i32],
+    "fssdp_estimate_loads": [i32, i32, i32, P_f64, i32, P_f64],
+    "fssdp_plan_layer": [i32, P_i32, P_f64, P_i64, P_topo, C.POINTER(LayerKnobs), P_u8, P_i32,
+                         P_i64, P_f64, P_i32],
+    "fssdp_shard_score": [i32, i32, P_i32, P_f64, P_topo, P_f64],
+    # device data plane (device pointers as void*)
+    "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
+                           vp, i64, vp],
+    "fssdp_gate_topk": [vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+    "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
+    "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
+    "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
+    "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
+                       i64, i32, i32, u32, vp, vp],
+    "fssdp_combine": [vp, vp, vp, i64, i32, i32, vp, i64, vp, vp],
+    "fssdp_dispatch_grad": [vp, vp, vp, vp, i64, i32, i32, vp, i64, i64, vp, vp, i32, i64, i32,
+                            i32, i32, u32, vp, vp],
+    "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],
+    "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
+    "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
+    "fssdp_sprs": [vp, i32, i64, i64, vp, i32, vp, vp],
+    # symmetric heap
+    "fssdp_heap_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
+    "fssdp_heap_free": [vp],
+    "fssdp_ipc_handle": [vp, P_u8],
+    "fssdp_ipc_open": [P_u8, C.POINTER(C.c_void_p)],
+    "fssdp_ipc_close": [vp],
+}
+_RESTYPE = {"fssdp_version": C.c_char_p, "fssdp_last_error": C.c_char_p}
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares (for the export check)."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(fssdp_\w+)\s*\(", text, re.M)))
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2502_02581_b200.build` "
+            "(there is no CPU fallback for the FSSDP path)"
+        )
+    lib = C.CDLL(str(LIB_PATH))
+    for name, argtypes in _SIGS.items():
+        fn = getattr(lib, name)  # AttributeError if the library lacks an export
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPE.get(name, C.c_int)
+    return lib
+
+
+LIB = _load()
+
+
+def last_error() -> str:
+    msg = LIB.fssdp_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        raise_for_status(status, what, last_error())
+
+
+def call(name: str, *args) -> None:
+    check(getattr(LIB, name)(*args), name)

@@ -1,0 +1,180 @@
+// C-ABI plumbing of libfssdp: error reporting, device queries, TMA descriptor encoding,
+// the grouped-GEMM entry point, and the symmetric heap (cudaMalloc + CUDA IPC).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "fssdp_internal.h"
+
+namespace fssdp {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+int num_sms() {
+  static int cached = -1;
+  if (cached < 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      return 148;
+    cached = n;
+  }
+  return cached;
+}
+
+// cuTensorMapEncodeTiled is fetched through the runtime's driver entry point so the
+// library never links libcuda directly (it must load on GPU-less build hosts).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
+                      int box_inner, int box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return kErrCuda;
+  }
+  if (inner <= 0 || outer <= 0 || (inner * 2) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(base) & 15) != 0) {
+    set_error("tensor map: bad extents or misaligned base");
+    return kErrDimension;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    set_error(buf);
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+}  // namespace fssdp
+
+using namespace fssdp;
+
+extern "C" {
+
+const char* fssdp_version(void) { return "fssdp-b200 0.1.0 (sm_100a)"; }
+
+const char* fssdp_last_error(void) { return g_last_error.c_str(); }
+
+int fssdp_num_sms(void) { return num_sms(); }
+
+int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
+                       int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
+                       const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
+                       int32_t total_tiles, void* c, void* c2, const void* aux, int64_t ldc,
+                       void* stream) {
+  if (num_groups <= 0 || n_tiles <= 0 || total_tiles < 0 || c == nullptr) {
+    set_error("grouped_gemm: bad arguments");
+    return kErrDimension;
+  }
+  if ((epilogue == kEpiGelu && c2 == nullptr) || (epilogue == kEpiDGelu && aux == nullptr)) {
+    set_error("grouped_gemm: epilogue needs c2/aux");
+    return kErrDimension;
+  }
+  GemmLaunch args;
+  args.groups = groups_dev;
+  args.num_groups = num_groups;
+  args.n_tiles = n_tiles;
+  args.total_tiles = total_tiles;
+  args.ldc = ldc;
+  args.c = c;
+  args.c2 = c2;
+  args.aux = static_cast<const __nv_bfloat16*>(aux);
+  int rc = grouped_gemm_launch(a_mn, b_mn, epilogue, a, a_inner, a_outer, b, b_inner, b_outer,
+                               args, reinterpret_cast<cudaStream_t>(stream));
+  if (rc == kErrCuda && g_last_error.empty()) set_error("grouped_gemm launch failed");
+  return rc;
+}
+
+int fssdp_heap_alloc(size_t bytes, void** ptr_out) {
+  const size_t gran = size_t(2) << 20;
+  bytes = (bytes + gran - 1) / gran * gran;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  e = cudaMemset(p, 0, bytes);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  *ptr_out = p;
+  return kOk;
+}
+
+int fssdp_heap_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+int fssdp_ipc_handle(void* ptr, uint8_t* handle_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  memcpy(handle_out, &h, sizeof(h));
+  return kOk;
+}
+
+int fssdp_ipc_open(const uint8_t* handle, void** ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+int fssdp_ipc_close(void* ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+}  // extern "C"

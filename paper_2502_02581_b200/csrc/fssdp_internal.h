@@ -1,0 +1,48 @@
+// Internal declarations shared by the CUDA translation units of libfssdp.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fssdp.h"
+
+namespace fssdp {
+
+constexpr int kOk = FSSDP_OK;
+constexpr int kErrDimension = FSSDP_ERR_DIMENSION;
+constexpr int kErrInvalidPair = FSSDP_ERR_INVALID_PAIR;
+constexpr int kErrOrphan = FSSDP_ERR_ORPHAN_EXPERT;
+constexpr int kErrCuda = FSSDP_ERR_CUDA;
+constexpr int kErrInternal = FSSDP_ERR_INTERNAL;
+constexpr int kErrInfeasible = FSSDP_ERR_INFEASIBLE;
+constexpr int kErrEmptyHistory = FSSDP_ERR_EMPTY_HISTORY;
+
+// GEMM epilogue kinds (mirrors FSSDP_EPI_* in fssdp.h)
+constexpr int kEpiBF16 = FSSDP_EPI_BF16;
+constexpr int kEpiGelu = FSSDP_EPI_GELU;
+constexpr int kEpiDGelu = FSSDP_EPI_DGELU;
+constexpr int kEpiF32 = FSSDP_EPI_F32;
+
+using GemmGroup = fssdp_gemm_group;
+
+struct GemmLaunch {
+  const GemmGroup* groups;  // device array
+  int num_groups;
+  int n_tiles;      // BN tiles along N (same for every group)
+  int total_tiles;  // sum over groups of m_tiles * n_tiles
+  int64_t ldc;      // elements per C row
+  void* c;          // output (bf16 or fp32)
+  void* c2;         // second output (GeLU: post-activation)
+  const __nv_bfloat16* aux;  // DGeLU: pre-activation, same layout as c
+};
+
+int num_sms();
+void set_error(const char* msg);
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
+                      int box_inner, int box_outer);
+int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
+                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
+                        const GemmLaunch& args, cudaStream_t stream);
+
+}  // namespace fssdp

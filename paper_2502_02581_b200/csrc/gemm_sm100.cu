@@ -1,0 +1,337 @@
+// Grouped expert-FFN GEMM for sm_100a (K5 forward, K7 dgrad/wgrad).
+//
+// One persistent, warp-specialised kernel serves all six GEMMs of an FSSDP MoE layer
+// (fwd1, fwd2, dgrad2, dgrad1, wgrad1, wgrad2).  Operands are staged by TMA
+// (cp.async.bulk.tensor, SWIZZLE_128B) into a 4-deep shared-memory ring, multiplied
+// by tcgen05.mma (kind::f16, bf16 in / fp32 accumulate) into a double-buffered TMEM
+// accumulator, and drained by four epilogue warps that fuse the activation
+// (GeLU fwd, GeLU' in dgrad) and the output cast.
+//
+// Grouping: every local expert (owned shard or SpAG replica) is one group.  A group's
+// tokens are a 128-row-aligned segment of the receive buffer, so an M tile never
+// straddles two experts; for wgrad the token axis is K and the segment padding rows
+// are zero, so K blocks never mix experts either.
+//
+// Warp roles (192 threads): w0 = TMA producer, w1 = MMA issuer + TMEM owner,
+// w2..w5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fssdp_internal.h"
+#include "ptx.cuh"
+
+namespace fssdp {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = kStages * kStageBytes;
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
+  static constexpr int kTotal = kBarOffset + (2 * kStages + 4) * 8 + 16;
+  static constexpr int kDynamic = kTotal + 1024;  // slack for 1024-B alignment
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
+  const float k1 = 0.044715f;
+  float u = k0 * (x + k1 * x * x * x);
+  return 0.5f * x * (1.0f + tanhf(u));
+}
+
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f;
+  const float k1 = 0.044715f;
+  float x2 = x * x;
+  float u = k0 * (x + k1 * x2 * x);
+  float t = tanhf(u);
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x2);
+}
+
+struct TileCoord {
+  int group, m_tile, n_tile;
+};
+
+__device__ __forceinline__ TileCoord locate_tile(const GemmGroup* __restrict__ groups,
+                                                 int num_groups, int n_tiles, int tile) {
+  int g = 0;
+  // groups are few (<= experts per device + replica slots); a linear scan is cheapest
+  while (g + 1 < num_groups && groups[g + 1].tile_start <= tile) ++g;
+  int local = tile - groups[g].tile_start;
+  int mt = groups[g].m_tiles;
+  TileCoord tc;
+  tc.group = g;
+  tc.m_tile = local % mt;  // M fastest: neighbouring CTAs share the weight (B) tile in L2
+  tc.n_tile = local / mt;
+  (void)n_tiles;
+  return tc;
+}
+
+template <bool A_MN, bool B_MN, int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, GemmLaunch args) {
+  using S = GemmSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);  // one arrival per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const GemmGroup* __restrict__ groups = args.groups;
+  const int total = args.total_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, tile);
+        const GemmGroup& g = groups[tc.group];
+        const int m0 = g.a_m + tc.m_tile * kBM;
+        const int n0 = g.b_n + tc.n_tile * BN;
+        for (int kb = 0; kb < g.k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          const int ka = g.a_k + kb * kBK;
+          const int kbb = g.b_k + kb * kBK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              tma_load_2d(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
+          } else {
+            tma_load_2d(sa, &map_a, &full_bar[stage], ka, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
+          } else {
+            tma_load_2d(sb, &map_b, &full_bar[stage], kbb, n0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===================== MMA issuer (single thread)
+      constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, tile);
+        const int kblocks = groups[tc.group].k_blocks;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + stage * S::kStageBytes);
+          const uint32_t b_base = a_base + S::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            uint64_t adesc, bdesc;
+            if (A_MN)  // 16 K rows = 2048 B per step; MN chunks of 64 at kBK*128 B
+              adesc = make_sdesc_sw128(a_base + kk * 2048, kBK * 128, 1024);
+            else  // 16 K elements = 32 B inside the 128-B swizzled row
+              adesc = make_sdesc_sw128(a_base + kk * 32, 16, 1024);
+            if (B_MN)
+              bdesc = make_sdesc_sw128(b_base + kk * 2048, kBK * 128, 1024);
+            else
+              bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue: TMEM -> registers -> fused op -> global
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, tile);
+      const GemmGroup& g = groups[tc.group];
+      const int row = tc.m_tile * kBM + q * 32 + lane;  // row inside the group's C
+      const int col0 = tc.n_tile * BN;
+      const int64_t c_row = g.c_off + static_cast<int64_t>(row) * args.ldc + col0;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const bool zero = g.k_blocks == 0;
+#pragma unroll 1
+      for (int chunk = 0; chunk < BN / 32; ++chunk) {
+        uint32_t r[32];
+        if (!zero) {
+          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                 static_cast<uint32_t>(acc * BN + chunk * 32),
+                             r);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        const int64_t off = c_row + chunk * 32;
+        if (EPI == kEpiF32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.c) + off);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        } else {
+          __nv_bfloat162 out[16];
+          if (EPI == kEpiBF16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]),
+                                             __uint_as_float(r[2 * i + 1]));
+          } else if (EPI == kEpiGelu) {
+            __nv_bfloat162 act[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]),
+                                             __uint_as_float(r[2 * i + 1]));
+              float2 pre = __bfloat1622float2(out[i]);
+              act[i] = __floats2bfloat162_rn(gelu_tanh(pre.x), gelu_tanh(pre.y));
+            }
+            int4* dst2 = reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(args.c2) + off);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst2[i] = reinterpret_cast<const int4*>(act)[i];
+          } else {  // kEpiDGelu: out = acc * gelu'(pre-activation)
+            const int4* src = reinterpret_cast<const int4*>(args.aux + off);
+            __nv_bfloat162 pre[16];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(pre)[i] = src[i];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float2 p = __bfloat1622float2(pre[i]);
+              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * gelu_tanh_grad(p.x),
+                                             __uint_as_float(r[2 * i + 1]) * gelu_tanh_grad(p.y));
+            }
+          }
+          int4* dst = reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(args.c) + off);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = reinterpret_cast<const int4*>(out)[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<2 * BN>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+template <bool A_MN, bool B_MN, int BN, int EPI>
+static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const GemmLaunch& args,
+                          int grid, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI>;
+  const int smem = GemmSmem<BN>::kDynamic;
+  static bool configured = false;  // per template instance
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return kErrCuda;
+    configured = true;
+  }
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, args);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+static int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb,
+                        const GemmLaunch& args, int grid, cudaStream_t stream) {
+  switch (epi) {
+    case kEpiBF16: return launch_variant<A_MN, B_MN, BN, kEpiBF16>(ma, mb, args, grid, stream);
+    case kEpiGelu: return launch_variant<A_MN, B_MN, BN, kEpiGelu>(ma, mb, args, grid, stream);
+    case kEpiDGelu: return launch_variant<A_MN, B_MN, BN, kEpiDGelu>(ma, mb, args, grid, stream);
+    case kEpiF32: return launch_variant<A_MN, B_MN, BN, kEpiF32>(ma, mb, args, grid, stream);
+    default: return kErrDimension;
+  }
+}
+
+int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
+                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
+                        const GemmLaunch& args, cudaStream_t stream) {
+  constexpr int BN = 256;
+  if (args.total_tiles <= 0) return kOk;
+  if (args.ldc % 32 != 0) return kErrDimension;
+  CUtensorMap ma, mb;
+  // K-major operand: box = {64 K elems, rows};  MN-major: box = {64 MN elems, 64 K rows}
+  int rc = make_tmap_bf16_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM);
+  if (rc != kOk) return rc;
+  rc = make_tmap_bf16_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN);
+  if (rc != kOk) return rc;
+  int grid = args.total_tiles < num_sms() ? args.total_tiles : num_sms();
+  if (a_mn) {
+    if (b_mn) return dispatch_epi<true, true, BN>(epi, ma, mb, args, grid, stream);
+    return dispatch_epi<true, false, BN>(epi, ma, mb, args, grid, stream);
+  }
+  if (b_mn) return dispatch_epi<false, true, BN>(epi, ma, mb, args, grid, stream);
+  return dispatch_epi<false, false, BN>(epi, ma, mb, args, grid, stream);
+}
+
+}  // namespace fssdp

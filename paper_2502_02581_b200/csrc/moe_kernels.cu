@@ -1,0 +1,784 @@
+// FSSDP token-path and sparse-collective kernels for sm_100a.
+//
+//   K1  gate_topk_kernel        logits (CUDA-core fp32), top-k, renormalised weights,
+//                               tile-relative slot ranks, per-tile expert histograms
+//   K2  route_scan_kernel       tile prefix over the histograms + counts all-gather via
+//                               peer stores + world barrier
+//   K4  dispatch_kernel         push token rows into destination receive segments
+//   K6  combine_kernel          pull expert outputs back, weighted sum (fixed fp32 order)
+//   K7  dispatch_grad_kernel    <dy, Y> for the gate + push w*dy to the experts
+//       combine_dx_kernel       pull dX rows back + gate input gradient
+//       gate_wgrad_kernels      dWg (split-T partials, fixed-order reduce)
+//   K3  spag_kernel             SparseAllGather: pull replica slots from owners
+//   K8  sprs_kernel             SparseReduceScatter: owners pull + reduce replica grads
+//
+// Semantics follow the paper (PAPER.md:234-237 gate/top-k/combine, 370-386 SpAG/SpRS,
+// 615-617 dispatch); the routing counts they execute come from the host planner
+// (moesim build_dispatch, dispatch.py:49-97).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fssdp_internal.h"
+#include "ptx.cuh"
+
+namespace fssdp {
+
+constexpr int kMaxWorld = 32;
+constexpr int kGateTile = FSSDP_GATE_TILE;
+constexpr int kGateThreads = 256;
+constexpr int kGateChunk = 128;
+constexpr int kGateMaxE = 64;
+constexpr int kGateMaxK = 8;
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------------ world barrier
+// Called by one full warp after the caller made its data writes visible
+// (__syncthreads + __threadfence_system).  Epochs only grow, so flags never reset.
+__device__ __forceinline__ void world_barrier_warp(const uint64_t* __restrict__ peer_bases,
+                                                   int64_t flags_off, int rank, int world,
+                                                   int slot, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  if (lane < world) {
+    uint32_t* remote = reinterpret_cast<uint32_t*>(peer_bases[lane] + flags_off) +
+                       slot * kMaxWorld + rank;
+    st_release_sys(remote, epoch);
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(peer_bases[rank] + flags_off) +
+                           slot * kMaxWorld + lane;
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+    }
+  }
+  __syncwarp();
+}
+
+// Grid-wide "all CTAs done" followed by the world barrier, run by the last CTA.
+__device__ __forceinline__ void grid_done_then_barrier(uint32_t* grid_counter,
+                                                       const uint64_t* __restrict__ peer_bases,
+                                                       int64_t flags_off, int rank, int world,
+                                                       int slot, uint32_t epoch) {
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t prev = atomicAdd(grid_counter, 1u);
+    is_last = (prev == gridDim.x * gridDim.y - 1) ? 1 : 0;
+    if (is_last) {
+      __threadfence_system();
+      atomicExch(grid_counter, 0u);
+    }
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x < 32) world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
+}
+
+__global__ void barrier_kernel(const uint64_t* peer_bases, int64_t flags_off, int rank, int world,
+                               int slot, uint32_t epoch) {
+  __threadfence_system();
+  world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
+}
+
+// ------------------------------------------------------------------ K1 gate
+// Selection + weights + tile-relative ranks for the tile's tokens, logits in smem.
+__device__ void gate_select_tile(const float* __restrict__ lg, int lg_stride, int tile, int64_t T,
+                                 int E, int k, int32_t* s_idx, int32_t* s_cnt,
+                                 int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                                 int32_t* __restrict__ slot_rank,
+                                 int32_t* __restrict__ tile_counts) {
+  const int tid = threadIdx.x;
+  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile;
+  const int valid = static_cast<int>(imin64(kGateTile, T - t0));
+  if (tid < valid) {
+    const float* row = lg + tid * lg_stride;
+    uint64_t taken = 0;
+    int sel[kGateMaxK];
+    for (int j = 0; j < k; ++j) {
+      int bi = -1;
+      float best = 0.f;
+      for (int e = 0; e < E; ++e) {
+        if ((taken >> e) & 1ull) continue;
+        float v = row[e];
+        if (bi < 0 || v > best) {  // strict '>' keeps the lower expert id on ties
+          best = v;
+          bi = e;
+        }
+      }
+      taken |= 1ull << bi;
+      sel[j] = bi;
+    }
+    // renormalised softmax over the selected logits (GShard top-k): e_j = exp(l_j - l_0)
+    float ex[kGateMaxK];
+    float m = row[sel[0]];
+    float s = 0.f;
+    for (int j = 0; j < k; ++j) {
+      ex[j] = expf(__fsub_rn(row[sel[j]], m));
+      s = __fadd_rn(s, ex[j]);
+    }
+    const int64_t t = t0 + tid;
+    for (int j = 0; j < k; ++j) {
+      topk_idx[t * k + j] = sel[j];
+      topk_w[t * k + j] = __fdiv_rn(ex[j], s);
+      s_idx[tid * k + j] = sel[j];
+    }
+  }
+  if (tid < E) s_cnt[tid] = 0;
+  __syncthreads();
+  if (tid < 32) {
+    const int nslots = valid * k;
+    const int lane = tid;
+    for (int base = 0; base < nslots; base += 32) {
+      const int slot = base + lane;
+      const bool ok = slot < nslots;
+      const int e = ok ? s_idx[slot] : -1;
+      const uint32_t peers = __match_any_sync(0xffffffffu, e);
+      const uint32_t below = peers & ((1u << lane) - 1u);
+      int r = 0;
+      if (ok) r = s_cnt[e] + __popc(below);
+      __syncwarp();
+      if (ok && (peers >> lane) == 1u) s_cnt[e] += __popc(peers);  // highest lane of the group
+      __syncwarp();
+      if (ok) slot_rank[t0 * k + slot] = r;
+    }
+    for (int e = lane; e < E; e += 32) tile_counts[static_cast<int64_t>(tile) * E + e] = s_cnt[e];
+  }
+}
+
+__global__ void __launch_bounds__(kGateThreads)
+    gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg, int64_t T,
+                     int d, int E, int k, float* __restrict__ logits,
+                     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                     int32_t* __restrict__ slot_rank, int32_t* __restrict__ tile_counts) {
+  // dynamic smem: xs [64][kGateChunk+8] bf16 | ws [E][kGateChunk+4] fp32; the logits
+  // tile lg [64][kGateMaxE+1] fp32 reuses the xs/ws region once the d loop is done.
+  extern __shared__ __align__(16) uint8_t gate_smem[];
+  typedef __nv_bfloat16 XRow[kGateChunk + 8];
+  typedef float WRow[kGateChunk + 4];
+  typedef float LRow[kGateMaxE + 1];
+  XRow* xs = reinterpret_cast<XRow*>(gate_smem);
+  WRow* ws = reinterpret_cast<WRow*>(gate_smem + kGateTile * sizeof(XRow));
+  LRow* lg = reinterpret_cast<LRow*>(gate_smem);
+  __shared__ int32_t s_idx[kGateTile * kGateMaxK];
+  __shared__ int32_t s_cnt[kGateMaxE];
+
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile;
+  const int tok = tid >> 2;
+  const int grp = tid & 3;
+  float acc[kGateMaxE / 4];
+#pragma unroll
+  for (int i = 0; i < kGateMaxE / 4; ++i) acc[i] = 0.f;
+
+  for (int c0 = 0; c0 < d; c0 += kGateChunk) {
+    const int cw = min(kGateChunk, d - c0);  // multiple of 8
+    // x chunk: 64 rows x cw bf16, 16-byte vectors
+    for (int v = tid; v < kGateTile * (kGateChunk / 8); v += kGateThreads) {
+      const int r = v / (kGateChunk / 8);
+      const int c = (v % (kGateChunk / 8)) * 8;
+      int4 val = make_int4(0, 0, 0, 0);
+      if (t0 + r < T && c < cw)
+        val = *reinterpret_cast<const int4*>(x + (t0 + r) * d + c0 + c);
+      *reinterpret_cast<int4*>(&xs[r][c]) = val;
+    }
+    for (int v = tid; v < E * (kGateChunk / 4); v += kGateThreads) {
+      const int e = v / (kGateChunk / 4);
+      const int c = (v % (kGateChunk / 4)) * 4;
+      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < cw) val = *reinterpret_cast<const float4*>(wg + static_cast<int64_t>(e) * d + c0 + c);
+      *reinterpret_cast<float4*>(&ws[e][c]) = val;
+    }
+    __syncthreads();
+    for (int i = 0; i < cw; i += 2) {
+      const float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[tok][i]));
+#pragma unroll
+      for (int q = 0; q < kGateMaxE / 4; ++q) {
+        const int e = grp + 4 * q;
+        if (e < E) {
+          const float2 wv = *reinterpret_cast<const float2*>(&ws[e][i]);
+          acc[q] = fmaf(xv.x, wv.x, acc[q]);
+          acc[q] = fmaf(xv.y, wv.y, acc[q]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kGateMaxE / 4; ++q) {
+    const int e = grp + 4 * q;
+    if (e < E) lg[tok][e] = acc[q];
+  }
+  __syncthreads();
+  if (logits != nullptr) {
+    for (int v = tid; v < kGateTile * E; v += kGateThreads) {
+      const int r = v / E, e = v % E;
+      if (t0 + r < T) logits[(t0 + r) * E + e] = lg[r][e];
+    }
+  }
+  gate_select_tile(&lg[0][0], kGateMaxE + 1, tile, T, E, k, s_idx, s_cnt, topk_idx, topk_w,
+                   slot_rank, tile_counts);
+}
+
+__global__ void __launch_bounds__(kGateThreads)
+    topk_from_logits_kernel(const float* __restrict__ logits, int64_t T, int E, int k,
+                            int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                            int32_t* __restrict__ slot_rank, int32_t* __restrict__ tile_counts) {
+  __shared__ float lg[kGateTile][kGateMaxE + 1];
+  __shared__ int32_t s_idx[kGateTile * kGateMaxK];
+  __shared__ int32_t s_cnt[kGateMaxE];
+  const int tile = blockIdx.x;
+  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile;
+  for (int v = threadIdx.x; v < kGateTile * E; v += blockDim.x) {
+    const int r = v / E, e = v % E;
+    lg[r][e] = (t0 + r < T) ? logits[(t0 + r) * E + e] : 0.f;
+  }
+  __syncthreads();
+  gate_select_tile(&lg[0][0], kGateMaxE + 1, tile, T, E, k, s_idx, s_cnt, topk_idx, topk_w,
+                   slot_rank, tile_counts);
+}
+
+// ------------------------------------------------------------------ K2 scan + counts all-gather
+__global__ void route_scan_kernel(const int32_t* __restrict__ tile_counts, int n_tiles, int E,
+                                  int32_t* __restrict__ tile_prefix,
+                                  const uint64_t* __restrict__ peer_bases, int64_t table_off,
+                                  int64_t flags_off, int rank, int world, int slot, uint32_t epoch) {
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      tile_prefix[static_cast<int64_t>(t) * E + e] = run;
+      run += tile_counts[static_cast<int64_t>(t) * E + e];
+    }
+    for (int p = 0; p < world; ++p)
+      reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncwarp();
+    world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
+  }
+}
+
+// ------------------------------------------------------------------ row copy helpers
+__device__ __forceinline__ void warp_copy_row(int4* __restrict__ dst, const int4* __restrict__ src,
+                                              int n16) {
+  const int lane = threadIdx.x & 31;
+  int i = lane;
+  for (; i + 96 < n16; i += 128) {
+    int4 a = ld_nc_v4(src + i), b = ld_nc_v4(src + i + 32), c = ld_nc_v4(src + i + 64),
+         d = ld_nc_v4(src + i + 96);
+    st_v4(dst + i, a);
+    st_v4(dst + i + 32, b);
+    st_v4(dst + i + 64, c);
+    st_v4(dst + i + 96, d);
+  }
+  for (; i < n16; i += 32) st_v4(dst + i, ld_nc_v4(src + i));
+}
+
+__device__ __forceinline__ void warp_zero_rows(char* base, const int32_t* __restrict__ zero_rows,
+                                               int n_zero, int64_t row_bytes, int warp_global,
+                                               int nwarps) {
+  const int lane = threadIdx.x & 31;
+  const int n16 = static_cast<int>(row_bytes / 16);
+  const int4 z = make_int4(0, 0, 0, 0);
+  for (int r = 0; r < n_zero; ++r) {
+    const int64_t row0 = zero_rows[2 * r];
+    const int cnt = zero_rows[2 * r + 1];
+    for (int i = warp_global; i < cnt; i += nwarps) {
+      int4* dst = reinterpret_cast<int4*>(base + (row0 + i) * row_bytes);
+      for (int c = lane; c < n16; c += 32) st_v4(dst + c, z);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K4 dispatch
+__global__ void __launch_bounds__(256)
+    dispatch_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ topk_idx,
+                    const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ tile_prefix,
+                    int64_t T, int d_model, int E, int k, int world,
+                    const int32_t* __restrict__ route_cum, const int32_t* __restrict__ recv_base,
+                    int32_t* __restrict__ slot_dest, int32_t* __restrict__ slot_pos,
+                    const uint64_t* __restrict__ peer_bases, int64_t recv_off,
+                    const int32_t* __restrict__ zero_rows, int n_zero, int64_t flags_off, int rank,
+                    int bar_slot, uint32_t epoch, uint32_t* grid_counter) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
+  const int n16 = static_cast<int>(row_bytes / 16);
+  const int64_t nslots = T * k;
+  for (int64_t s = warp_global; s < nslots; s += nwarps) {
+    int dst = 0, pos = 0;
+    if (lane == 0) {
+      const int64_t t = s / k;
+      const int e = topk_idx[s];
+      const int r = tile_prefix[(t / kGateTile) * E + e] + slot_rank[s];
+      const int32_t* cum = route_cum + e * (world + 1);
+      int dd = 0;
+      while (dd + 1 < world && cum[dd + 1] <= r) ++dd;
+      dst = dd;
+      pos = recv_base[e * world + dd] + (r - cum[dd]);
+      slot_dest[s] = dst;
+      slot_pos[s] = pos;
+    }
+    dst = __shfl_sync(0xffffffffu, dst, 0);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const int64_t t = s / k;
+    const int4* src = reinterpret_cast<const int4*>(x + t * d_model);
+    int4* out = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[dst] + recv_off) +
+                                        static_cast<int64_t>(pos) * row_bytes);
+    warp_copy_row(out, src, n16);
+  }
+  warp_zero_rows(reinterpret_cast<char*>(peer_bases[rank] + recv_off), zero_rows, n_zero, row_bytes,
+                 warp_global, nwarps);
+  grid_done_then_barrier(grid_counter, peer_bases, flags_off, rank, world, bar_slot, epoch);
+}
+
+// ------------------------------------------------------------------ K6 combine
+__device__ __forceinline__ void bf16x8_to_f32(const int4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 p = __bfloat1622float2(h[i]);
+    f[2 * i] = p.x;
+    f[2 * i + 1] = p.y;
+  }
+}
+__device__ __forceinline__ int4 f32_to_bf16x8(const float (&f)[8]) {
+  int4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+    combine_kernel(const int32_t* __restrict__ slot_dest, const int32_t* __restrict__ slot_pos,
+                   const float* __restrict__ topk_w, int64_t T, int d_model, int k,
+                   const uint64_t* __restrict__ peer_bases, int64_t y_off,
+                   __nv_bfloat16* __restrict__ y_out) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
+  const int n16 = static_cast<int>(row_bytes / 16);
+  for (int64_t t = warp_global; t < T; t += nwarps) {
+    const int4* rows[kGateMaxK];
+    float w[kGateMaxK];
+    for (int j = 0; j < k; ++j) {
+      const int64_t s = t * k + j;
+      rows[j] = reinterpret_cast<const int4*>(
+          reinterpret_cast<const char*>(peer_bases[slot_dest[s]] + y_off) +
+          static_cast<int64_t>(slot_pos[s]) * row_bytes);
+      w[j] = topk_w[s];
+    }
+    int4* out = reinterpret_cast<int4*>(y_out + t * d_model);
+    for (int c = lane; c < n16; c += 32) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        float f[8];
+        bf16x8_to_f32(ld_nc_v4(rows[j] + c), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w[j], f[i]));
+      }
+      out[c] = f32_to_bf16x8(acc);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K7 token-side backward
+__global__ void __launch_bounds__(256)
+    dispatch_grad_kernel(const __nv_bfloat16* __restrict__ dy, const int32_t* __restrict__ slot_dest,
+                         const int32_t* __restrict__ slot_pos, const float* __restrict__ topk_w,
+                         int64_t T, int d_model, int k, const uint64_t* __restrict__ peer_bases,
+                         int64_t y_off, int64_t dy_recv_off, float* __restrict__ slot_grad,
+                         const int32_t* __restrict__ zero_rows, int n_zero, int64_t flags_off,
+                         int rank, int world, int bar_slot, uint32_t epoch,
+                         uint32_t* grid_counter) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
+  const int n16 = static_cast<int>(row_bytes / 16);
+  const int64_t nslots = T * k;
+  for (int64_t s = warp_global; s < nslots; s += nwarps) {
+    const int64_t t = s / k;
+    const int dst = slot_dest[s];
+    const int64_t pos = slot_pos[s];
+    const float w = topk_w[s];
+    const int4* yrow = reinterpret_cast<const int4*>(
+        reinterpret_cast<const char*>(peer_bases[dst] + y_off) + pos * row_bytes);
+    const int4* grow = reinterpret_cast<const int4*>(dy + t * d_model);
+    int4* out = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[dst] + dy_recv_off) +
+                                        pos * row_bytes);
+    float dot = 0.f;
+    for (int c = lane; c < n16; c += 32) {
+      float fy[8], fg[8], o[8];
+      bf16x8_to_f32(ld_nc_v4(yrow + c), fy);
+      bf16x8_to_f32(ld_nc_v4(grow + c), fg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        dot = fmaf(fg[i], fy[i], dot);
+        o[i] = __fmul_rn(w, fg[i]);
+      }
+      st_v4(out + c, f32_to_bf16x8(o));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if (lane == 0) slot_grad[s] = dot;
+  }
+  warp_zero_rows(reinterpret_cast<char*>(peer_bases[rank] + dy_recv_off), zero_rows, n_zero,
+                 row_bytes, warp_global, nwarps);
+  grid_done_then_barrier(grid_counter, peer_bases, flags_off, rank, world, bar_slot, epoch);
+}
+
+__global__ void __launch_bounds__(256)
+    combine_dx_kernel(const int32_t* __restrict__ slot_dest, const int32_t* __restrict__ slot_pos,
+                      const int32_t* __restrict__ topk_idx, const float* __restrict__ topk_w,
+                      const float* __restrict__ slot_grad, const float* __restrict__ wg, int64_t T,
+                      int d_model, int E, int k, const uint64_t* __restrict__ peer_bases,
+                      int64_t dxe_off, float* __restrict__ dlogit_out,
+                      __nv_bfloat16* __restrict__ dx_out) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
+  const int n16 = static_cast<int>(row_bytes / 16);
+  for (int64_t t = warp_global; t < T; t += nwarps) {
+    const int4* rows[kGateMaxK];
+    const float* wrow[kGateMaxK];
+    float dl[kGateMaxK];
+    float sg = 0.f;
+    for (int j = 0; j < k; ++j) sg = fmaf(topk_w[t * k + j], slot_grad[t * k + j], sg);
+    for (int j = 0; j < k; ++j) {
+      const int64_t s = t * k + j;
+      dl[j] = topk_w[s] * (slot_grad[s] - sg);
+      rows[j] = reinterpret_cast<const int4*>(
+          reinterpret_cast<const char*>(peer_bases[slot_dest[s]] + dxe_off) +
+          static_cast<int64_t>(slot_pos[s]) * row_bytes);
+      wrow[j] = wg + static_cast<int64_t>(topk_idx[s]) * d_model;
+    }
+    if (lane < k) dlogit_out[t * k + lane] = dl[lane];
+    int4* out = reinterpret_cast<int4*>(dx_out + t * d_model);
+    for (int c = lane; c < n16; c += 32) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        float f[8];
+        bf16x8_to_f32(ld_nc_v4(rows[j] + c), f);
+        const float4 w0 = *reinterpret_cast<const float4*>(wrow[j] + c * 8);
+        const float4 w1 = *reinterpret_cast<const float4*>(wrow[j] + c * 8 + 4);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += f[i] + dl[j] * wv[i];
+      }
+      out[c] = f32_to_bf16x8(acc);
+    }
+  }
+}
+
+// dWg partials: grid (d/128, SPLITS), 128 threads, one model dim per thread.
+__global__ void __launch_bounds__(128)
+    gate_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
+                              const int32_t* __restrict__ topk_idx,
+                              const float* __restrict__ dlogit, int64_t T, int d_model, int E,
+                              int k, float* __restrict__ workspace) {
+  __shared__ float acc[kGateMaxE][128];
+  const int dim = blockIdx.x * 128 + threadIdx.x;
+  const int split = blockIdx.y;
+  for (int e = 0; e < E; ++e) acc[e][threadIdx.x] = 0.f;
+  const int64_t per = (T + FSSDP_WG_SPLITS - 1) / FSSDP_WG_SPLITS;
+  const int64_t t_begin = split * per;
+  const int64_t t_end = imin64(T, t_begin + per);
+  if (dim < d_model) {
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const float xv = __bfloat162float(x[t * d_model + dim]);
+      for (int j = 0; j < k; ++j) {
+        const int e = topk_idx[t * k + j];
+        acc[e][threadIdx.x] = fmaf(dlogit[t * k + j], xv, acc[e][threadIdx.x]);
+      }
+    }
+    for (int e = 0; e < E; ++e)
+      workspace[(static_cast<int64_t>(split) * E + e) * d_model + dim] = acc[e][threadIdx.x];
+  }
+}
+
+__global__ void gate_wgrad_reduce_kernel(const float* __restrict__ workspace, int d_model, int E,
+                                         float* __restrict__ dwg) {
+  const int64_t n = static_cast<int64_t>(E) * d_model;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < FSSDP_WG_SPLITS; ++p) s += workspace[p * n + i];
+    dwg[i] = s;
+  }
+}
+
+// ------------------------------------------------------------------ K3 SpAG / K8 SpRS
+constexpr int kCollChunk = 64 * 1024;  // bytes per CTA per copy job
+
+__global__ void __launch_bounds__(256)
+    spag_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t param_off,
+                int64_t slot_bytes, const int32_t* __restrict__ copies) {
+  const int job = blockIdx.y;
+  const int src_rank = copies[3 * job];
+  const int64_t src_slot = copies[3 * job + 1];
+  const int64_t dst_slot = copies[3 * job + 2];
+  const int64_t begin = static_cast<int64_t>(blockIdx.x) * kCollChunk;
+  if (begin >= slot_bytes) return;
+  const int64_t bytes = imin64(kCollChunk, slot_bytes - begin);
+  const int4* src = reinterpret_cast<const int4*>(
+      reinterpret_cast<const char*>(peer_bases[src_rank] + param_off) + src_slot * slot_bytes +
+      begin);
+  int4* dst = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[rank] + param_off) +
+                                      dst_slot * slot_bytes + begin);
+  const int n16 = static_cast<int>(bytes / 16);
+  constexpr int U = 8;
+  int i = threadIdx.x;
+  for (; i + (U - 1) * 256 < n16; i += U * 256) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_nc_v4(src + i + u * 256);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_v4(dst + i + u * 256, v[u]);
+  }
+  for (; i < n16; i += 256) st_v4(dst + i, ld_nc_v4(src + i));
+}
+
+__global__ void __launch_bounds__(256)
+    sprs_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
+                int64_t slot_elems, const int32_t* __restrict__ jobs,
+                const int32_t* __restrict__ srcs) {
+  const int job = blockIdx.y;
+  const int64_t dst_slot = jobs[3 * job];
+  const int src_begin = jobs[3 * job + 1];
+  const int src_count = jobs[3 * job + 2];
+  const int64_t chunk_elems = kCollChunk / 4;
+  const int64_t begin = static_cast<int64_t>(blockIdx.x) * chunk_elems;
+  if (begin >= slot_elems) return;
+  const int64_t n = imin64(chunk_elems, slot_elems - begin);
+  const int n4 = static_cast<int>(n / 4);
+  float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(peer_bases[rank] + grad_off) +
+                                          dst_slot * slot_elems + begin);
+  for (int i = threadIdx.x; i < n4; i += 256) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < src_count; ++q) {
+      const int r = srcs[2 * (src_begin + q)];
+      const int64_t sl = srcs[2 * (src_begin + q) + 1];
+      const float4* src = reinterpret_cast<const float4*>(
+          reinterpret_cast<const float*>(peer_bases[r] + grad_off) + sl * slot_elems + begin);
+      int4 raw = ld_nc_v4(reinterpret_cast<const int4*>(src + i));
+      acc.x = __fadd_rn(acc.x, __int_as_float(raw.x));
+      acc.y = __fadd_rn(acc.y, __int_as_float(raw.y));
+      acc.z = __fadd_rn(acc.z, __int_as_float(raw.z));
+      acc.w = __fadd_rn(acc.w, __int_as_float(raw.w));
+    }
+    dst[i] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+static int grid_for_warps(int64_t work_items) {
+  // persistent grid-stride: up to 4 CTAs of 8 warps per SM
+  int64_t blocks = (work_items + 7) / 8;
+  int64_t cap = static_cast<int64_t>(num_sms()) * 4;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+}  // namespace fssdp
+
+using namespace fssdp;
+
+extern "C" {
+
+int fssdp_gate_topk(const void* x, const float* wg, int64_t T, int32_t d, int32_t E, int32_t k,
+                    float* logits, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
+                    int32_t* tile_counts, void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
+      k > E) {
+    set_error("gate: unsupported shape");
+    return kErrDimension;
+  }
+  if (T == 0) return kOk;
+  const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
+  size_t smem = kGateTile * sizeof(__nv_bfloat16) * (kGateChunk + 8) +
+                static_cast<size_t>(E) * sizeof(float) * (kGateChunk + 4);
+  const size_t lg_bytes = kGateTile * sizeof(float) * (kGateMaxE + 1);
+  if (smem < lg_bytes) smem = lg_bytes;
+  static bool configured = false;
+  if (!configured) {
+    const size_t max_smem = kGateTile * sizeof(__nv_bfloat16) * (kGateChunk + 8) +
+                            kGateMaxE * sizeof(float) * (kGateChunk + 4);
+    if (cudaFuncSetAttribute(gate_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(max_smem)) != cudaSuccess)
+      return launch_status();
+    configured = true;
+  }
+  gate_topk_kernel<<<tiles, kGateThreads, smem, as_stream(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, logits, topk_idx, topk_w, slot_rank,
+      tile_counts);
+  return launch_status();
+}
+
+int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k, int32_t* topk_idx,
+                           float* topk_w, int32_t* slot_rank, int32_t* tile_counts, void* stream) {
+  if (T < 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK || k > E) {
+    set_error("topk: unsupported shape");
+    return kErrDimension;
+  }
+  if (T == 0) return kOk;
+  const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
+  topk_from_logits_kernel<<<tiles, kGateThreads, 0, as_stream(stream)>>>(
+      logits, T, E, k, topk_idx, topk_w, slot_rank, tile_counts);
+  return launch_status();
+}
+
+int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
+                               int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
+                               int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
+                               uint32_t epoch, void* stream) {
+  if (world <= 0 || world > kMaxWorld || rank < 0 || rank >= world || E <= 0) {
+    set_error("route_scan: bad world/rank/E");
+    return kErrDimension;
+  }
+  route_scan_kernel<<<1, 256, 0, as_stream(stream)>>>(tile_counts, n_tiles, E, tile_prefix,
+                                                       peer_bases, table_off, flags_off, rank,
+                                                       world, bar_slot, epoch);
+  return launch_status();
+}
+
+int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, int32_t world,
+                  int32_t bar_slot, uint32_t epoch, void* stream) {
+  if (world <= 0 || world > kMaxWorld || rank < 0 || rank >= world) {
+    set_error("barrier: bad world/rank");
+    return kErrDimension;
+  }
+  barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(peer_bases, flags_off, rank, world, bar_slot,
+                                                   epoch);
+  return launch_status();
+}
+
+int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_rank,
+                   const int32_t* tile_prefix, int64_t T, int32_t d_model, int32_t E, int32_t k,
+                   int32_t world, const int32_t* route_cum, const int32_t* recv_base,
+                   int32_t* slot_dest, int32_t* slot_pos, const uint64_t* peer_bases,
+                   int64_t recv_off, const int32_t* zero_rows, int32_t n_zero, int64_t flags_off,
+                   int32_t rank, int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter,
+                   void* stream) {
+  if (d_model % 8 != 0 || world <= 0 || world > kMaxWorld || k > kGateMaxK) {
+    set_error("dispatch: bad shape");
+    return kErrDimension;
+  }
+  const int grid = grid_for_warps(T * k);
+  dispatch_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), topk_idx, slot_rank, tile_prefix, T, d_model, E, k,
+      world, route_cum, recv_base, slot_dest, slot_pos, peer_bases, recv_off, zero_rows, n_zero,
+      flags_off, rank, bar_slot, epoch, grid_counter);
+  return launch_status();
+}
+
+int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float* topk_w, int64_t T,
+                  int32_t d_model, int32_t k, const uint64_t* peer_bases, int64_t y_off,
+                  void* y_out, void* stream) {
+  if (d_model % 8 != 0 || k > kGateMaxK) {
+    set_error("combine: bad shape");
+    return kErrDimension;
+  }
+  if (T == 0) return kOk;
+  combine_kernel<<<grid_for_warps(T), 256, 0, as_stream(stream)>>>(
+      slot_dest, slot_pos, topk_w, T, d_model, k, peer_bases, y_off,
+      static_cast<__nv_bfloat16*>(y_out));
+  return launch_status();
+}
+
+int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
+                        const float* topk_w, int64_t T, int32_t d_model, int32_t k,
+                        const uint64_t* peer_bases, int64_t y_off, int64_t dy_recv_off,
+                        float* slot_grad, const int32_t* zero_rows, int32_t n_zero,
+                        int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
+                        uint32_t epoch, uint32_t* grid_counter, void* stream) {
+  if (d_model % 8 != 0 || world <= 0 || world > kMaxWorld || k > kGateMaxK) {
+    set_error("dispatch_grad: bad shape");
+    return kErrDimension;
+  }
+  dispatch_grad_kernel<<<grid_for_warps(T * k), 256, 0, as_stream(stream)>>>(
+      static_cast<const __nv_bfloat16*>(dy), slot_dest, slot_pos, topk_w, T, d_model, k,
+      peer_bases, y_off, dy_recv_off, slot_grad, zero_rows, n_zero, flags_off, rank, world,
+      bar_slot, epoch, grid_counter);
+  return launch_status();
+}
+
+int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const int32_t* topk_idx,
+                     const float* topk_w, const float* slot_grad, const float* wg, int64_t T,
+                     int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
+                     int64_t dxe_off, float* dlogit_out, void* dx_out, void* stream) {
+  if (d_model % 8 != 0 || k > kGateMaxK || E > kGateMaxE) {
+    set_error("combine_dx: bad shape");
+    return kErrDimension;
+  }
+  if (T == 0) return kOk;
+  combine_dx_kernel<<<grid_for_warps(T), 256, 0, as_stream(stream)>>>(
+      slot_dest, slot_pos, topk_idx, topk_w, slot_grad, wg, T, d_model, E, k, peer_bases, dxe_off,
+      dlogit_out, static_cast<__nv_bfloat16*>(dx_out));
+  return launch_status();
+}
+
+int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
+                     int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
+                     void* stream) {
+  if (E > kGateMaxE || d_model <= 0) {
+    set_error("gate_wgrad: bad shape");
+    return kErrDimension;
+  }
+  dim3 grid((d_model + 127) / 128, FSSDP_WG_SPLITS);
+  gate_wgrad_partial_kernel<<<grid, 128, 0, as_stream(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, workspace);
+  int rc = launch_status();
+  if (rc != kOk) return rc;
+  gate_wgrad_reduce_kernel<<<num_sms(), 256, 0, as_stream(stream)>>>(workspace, d_model, E,
+                                                                      dwg_out);
+  return launch_status();
+}
+
+int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
+               const int32_t* copies, int32_t n_copies, void* stream) {
+  if (slot_bytes % 16 != 0) {
+    set_error("spag: slot_bytes must be a multiple of 16");
+    return kErrDimension;
+  }
+  if (n_copies <= 0) return kOk;
+  dim3 grid(static_cast<unsigned>((slot_bytes + kCollChunk - 1) / kCollChunk), n_copies);
+  spag_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, param_off, slot_bytes, copies);
+  return launch_status();
+}
+
+int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t slot_elems,
+               const int32_t* jobs, int32_t n_jobs, const int32_t* srcs, void* stream) {
+  if (slot_elems % 4 != 0) {
+    set_error("sprs: slot_elems must be a multiple of 4");
+    return kErrDimension;
+  }
+  if (n_jobs <= 0) return kOk;
+  dim3 grid(static_cast<unsigned>((slot_elems * 4 + kCollChunk - 1) / kCollChunk), n_jobs);
+  sprs_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, slot_elems, jobs,
+                                                   srcs);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+"""Torch-facing wrappers of the device entry points in include/fssdp.h.
+
+PyTorch is plumbing here: it owns device memory and streams; every kernel is one of
+libfssdp's sm_100a kernels, reached through the C-ABI with raw pointers.  There is no
+eager fallback — a missing library or a non-CUDA tensor raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import DimensionError
+
+GATE_TILE = 64
+BM, BN, BK = 128, 256, 64
+EPI_BF16, EPI_GELU, EPI_DGELU, EPI_F32 = 0, 1, 2, 3
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(0)
+    if not t.is_cuda:
+        raise DimensionError("FSSDP device ops need CUDA tensors (no CPU fallback)")
+    return C.c_void_p(t.data_ptr())
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if t.dtype != dtype or not t.is_contiguous() or not t.is_cuda:
+        raise DimensionError(f"{name}: expected contiguous CUDA {dtype}, got {t.dtype} "
+                             f"{'contiguous' if t.is_contiguous() else 'strided'} on {t.device}")
+
+
+# ------------------------------------------------------------------ grouped GEMM
+def gemm_groups_tensor(groups: list[tuple], device) -> tuple[torch.Tensor, int, int]:
+    """Pack [(m_tiles, a_m, a_k, b_n, b_k, k_blocks, c_off), ...] into a device array.
+
+    Returns (tensor, num_groups, total_tiles_per_n_tile)."""
+    arr = np.zeros(len(groups), dtype=[("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"),
+                                       ("a_k", "<i4"), ("b_n", "<i4"), ("b_k", "<i4"),
+                                       ("k_blocks", "<i4"), ("pad_", "<i4"), ("c_off", "<i8")])
+    for i, (m_tiles, a_m, a_k, b_n, b_k, k_blocks, c_off) in enumerate(groups):
+        arr[i] = (m_tiles, 0, a_m, a_k, b_n, b_k, k_blocks, 0, c_off)
+    raw = torch.from_numpy(arr.view(np.uint8).copy())
+    return raw.to(device, non_blocking=False), len(groups), int(arr["m_tiles"].sum())
+
+
+def finalize_groups(groups_cpu: np.ndarray, n_tiles: int) -> int:
+    """Fill tile_start in place for a structured group array; return total tiles."""
+    tiles = groups_cpu["m_tiles"].astype(np.int64) * n_tiles
+    starts = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+    groups_cpu["tile_start"] = starts
+    return int(tiles.sum())
+
+
+GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
+                        ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("pad_", "<i4"),
+                        ("c_off", "<i8")])
+
+
+def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, groups_dev: torch.Tensor,
+                 num_groups: int, n_tiles: int, total_tiles: int, c: torch.Tensor, ldc: int,
+                 epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
+                 aux: torch.Tensor | None = None, stream=None) -> None:
+    """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
+
+    a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous)."""
+    for t, nm in ((a, "A"), (b, "B")):
+        _need(t, torch.bfloat16, nm)
+        if t.dim() != 2:
+            raise DimensionError(f"{nm} must be 2-D")
+    N.call("fssdp_grouped_gemm", int(a_mn), int(b_mn), int(epilogue), _ptr(a), a.shape[1],
+           a.shape[0], _ptr(b), b.shape[1], b.shape[0], _ptr(groups_dev), num_groups, n_tiles,
+           total_tiles, _ptr(c), _ptr(c2), _ptr(aux), ldc, _stream(stream))
+
+
+# ------------------------------------------------------------------ gate
+def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, want_logits: bool = False, stream=None):
+    """K1: returns (topk_idx [T,k] i32, topk_w [T,k] f32, slot_rank [T,k] i32,
+    tile_counts [tiles,E] i32, logits [T,E] f32 | None)."""
+    _need(x, torch.bfloat16, "x")
+    _need(wg, torch.float32, "wg")
+    T, d = x.shape
+    E = wg.shape[0]
+    dev = x.device
+    tiles = (T + GATE_TILE - 1) // GATE_TILE
+    idx = torch.empty(T, k, dtype=torch.int32, device=dev)
+    w = torch.empty(T, k, dtype=torch.float32, device=dev)
+    rank = torch.empty(T, k, dtype=torch.int32, device=dev)
+    tc = torch.empty(max(tiles, 1), E, dtype=torch.int32, device=dev)
+    logits = torch.empty(T, E, dtype=torch.float32, device=dev) if want_logits else None
+    N.call("fssdp_gate_topk", _ptr(x), _ptr(wg), T, d, E, k, _ptr(logits), _ptr(idx), _ptr(w),
+           _ptr(rank), _ptr(tc), _stream(stream))
+    return idx, w, rank, tc, logits
+
+
+def topk_from_logits(logits: torch.Tensor, k: int, stream=None):
+    _need(logits, torch.float32, "logits")
+    T, E = logits.shape
+    dev = logits.device
+    tiles = (T + GATE_TILE - 1) // GATE_TILE
+    idx = torch.empty(T, k, dtype=torch.int32, device=dev)
+    w = torch.empty(T, k, dtype=torch.float32, device=dev)
+    rank = torch.empty(T, k, dtype=torch.int32, device=dev)
+    tc = torch.empty(max(tiles, 1), E, dtype=torch.int32, device=dev)
+    N.call("fssdp_topk_from_logits", _ptr(logits), T, E, k, _ptr(idx), _ptr(w), _ptr(rank),
+           _ptr(tc), _stream(stream))
+    return idx, w, rank, tc

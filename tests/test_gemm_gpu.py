@@ -1,0 +1,158 @@
+"""tcgen05 grouped GEMM (K5/K7) against a plain PyTorch fp32 reference.
+
+Tolerance (bf16 operands, fp32 accumulate, bf16 output): |Δ| <= 2e-2·max|ref| + 1e-3
+per tensor.  fp32 outputs (wgrad) use 2e-3·max|ref| + 1e-4.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2502_02581_b200 import ops
+
+    return ops
+
+
+def _groups(ops, rows, n_tiles, dev):
+    g = np.zeros(len(rows), dtype=ops.GROUP_DTYPE)
+    for i, r in enumerate(rows):
+        (g["m_tiles"][i], g["a_m"][i], g["a_k"][i], g["b_n"][i], g["b_k"][i], g["k_blocks"][i],
+         g["c_off"][i]) = r
+    total = ops.finalize_groups(g, n_tiles)
+    return torch.from_numpy(g.view(np.uint8).copy()).to(dev), len(rows), total
+
+
+def _close(out, ref, rel=2e-2, abs_=1e-3):
+    out = out.float()
+    ref = ref.float()
+    err = (out - ref).abs().max().item()
+    bound = rel * ref.abs().max().item() + abs_
+    assert err <= bound, f"max |Δ| {err:.4g} > {bound:.4g}"
+
+
+@pytest.mark.parametrize("epi", ["bf16", "gelu", "dgelu"])
+def test_kmajor_kmajor_grouped(epi):
+    """fwd-style: A [R,K] K-major rows per group, B [G*N, K] K-major per-group weights."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(0)
+    K, N = 320, 512
+    m_tiles = [1, 3, 0, 2]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    A = torch.randn(R, K, device=dev).bfloat16()
+    B = (torch.randn(G * N, K, device=dev) / K ** 0.5).bfloat16()
+    C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    C2 = torch.zeros_like(C)
+    aux = torch.randn(R, N, device=dev).bfloat16()
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, g * N, 0, K // 64, r0 * N))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    e = {"bf16": ops.EPI_BF16, "gelu": ops.EPI_GELU, "dgelu": ops.EPI_DGELU}[epi]
+    ops.grouped_gemm(A, False, B, False, gd, ng, N // 256, total, C, N, epilogue=e, c2=C2,
+                     aux=aux)
+    torch.cuda.synchronize()
+    ref = torch.zeros(R, N, device=dev)
+    r0 = 0
+    for g, mt in enumerate(m_tiles):
+        sl = slice(r0, r0 + mt * 128)
+        ref[sl] = A[sl].float() @ B[g * N:(g + 1) * N].float().T
+        r0 += mt * 128
+    if epi == "bf16":
+        _close(C, ref)
+    elif epi == "gelu":
+        _close(C, ref)
+        pre = C.float()
+        _close(C2, torch.nn.functional.gelu(pre, approximate="tanh"))
+    else:
+        a = aux.float()
+        k0, k1 = 0.7978845608028654, 0.044715
+        t = torch.tanh(k0 * (a + k1 * a ** 3))
+        gp = 0.5 * (1 + t) + 0.5 * a * (1 - t * t) * k0 * (1 + 3 * k1 * a * a)
+        _close(C, ref * gp)
+
+
+def test_kmajor_mnmajor_dgrad_style():
+    """dgrad-style: A [R,K] K-major, B stored [G*K, N] (N contiguous) = MN-major."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(1)
+    K, N = 256, 768
+    m_tiles = [2, 1, 3]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    A = torch.randn(R, K, device=dev).bfloat16()
+    B = (torch.randn(G * K, N, device=dev) / K ** 0.5).bfloat16()
+    C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, 0, g * K, K // 64, r0 * N))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    ops.grouped_gemm(A, False, B, True, gd, ng, N // 256, total, C, N)
+    torch.cuda.synchronize()
+    ref = torch.zeros(R, N, device=dev)
+    r0 = 0
+    for g, mt in enumerate(m_tiles):
+        sl = slice(r0, r0 + mt * 128)
+        ref[sl] = A[sl].float() @ B[g * K:(g + 1) * K].float()
+        r0 += mt * 128
+    _close(C, ref)
+
+
+@pytest.mark.parametrize("a_mn", [True, False])
+def test_wgrad_style_token_k(a_mn):
+    """wgrad-style: K = token segments (incl. an empty one), fp32 output per group."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(2)
+    M, N = 256, 512
+    segs = [128, 0, 384, 64]  # tokens per group (multiples of 64)
+    G = len(segs)
+    Rt = sum(segs)
+    Bt = torch.randn(Rt, N, device=dev).bfloat16()  # [tokens, N]  (MN-major B)
+    if a_mn:
+        At = torch.randn(Rt, M, device=dev).bfloat16()  # [tokens, M]  (MN-major A)
+    else:
+        At = torch.randn(M * G, Rt, device=dev).bfloat16()  # unused layout for K-major A
+    C = torch.full((G * M, N), 7.0, device=dev)
+    rows, k0 = [], 0
+    for g, s in enumerate(segs):
+        if a_mn:
+            rows.append((M // 128, 0, k0, 0, k0, s // 64, g * M * N))
+        else:
+            rows.append((M // 128, g * M, k0, 0, k0, s // 64, g * M * N))
+        k0 += s
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    ops.grouped_gemm(At, a_mn, Bt, True, gd, ng, N // 256, total, C, N, epilogue=ops.EPI_F32)
+    torch.cuda.synchronize()
+    k0 = 0
+    for g, s in enumerate(segs):
+        if a_mn:
+            a = At[k0:k0 + s].float().T
+        else:
+            a = At[g * M:(g + 1) * M, k0:k0 + s].float()
+        ref = a @ Bt[k0:k0 + s].float()
+        _close(C[g * M:(g + 1) * M], ref, rel=2e-3, abs_=1e-4)
+        k0 += s
+
+
+def test_large_square_against_torch():
+    """One big group (the throughput shape family) for a sanity check of the pipeline."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(3)
+    M, K, N = 2048, 1024, 4096
+    A = torch.randn(M, K, device=dev).bfloat16()
+    B = (torch.randn(N, K, device=dev) / K ** 0.5).bfloat16()
+    C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    gd, ng, total = _groups(ops, [(M // 128, 0, 0, 0, 0, K // 64, 0)], N // 256, dev)
+    ops.grouped_gemm(A, False, B, False, gd, ng, N // 256, total, C, N)
+    torch.cuda.synchronize()
+    _close(C, A.float() @ B.float().T)
