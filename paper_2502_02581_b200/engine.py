@@ -1,0 +1,301 @@
+"""FSSDP iteration control — the decision part of moesim's FssdpState (engine.py:386-557).
+
+The reference engine *simulates* a timeline; here the same decisions drive real
+device work: `FssdpPlanner.plan_layer` returns, per MoE layer and iteration, the
+materialized placement (which replicas SpAG fetches and SpRS folds back) and the
+build_dispatch route the dispatch kernel executes.  The per-layer decision chain
+(adoption gate -> calibration -> fallback -> dispatch) runs in one C++ call
+(fssdp_plan_layer).  The simulated timeline, the comparison policies and the CLI are
+out of scope.
+"""
+
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .costmodel import TrafficMatrix, collective_latency, overlap_degree
+from .errors import ConfigError, TraceMismatchError
+from .placement import ChunkPlacement, ShardPlan
+from .planner import GlobalLoadProfile, MaterializationPlan, estimate_loads, heterogeneous_sharding
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Model-side quantities the planner prices (engine.py:54-77)."""
+
+    layers: int
+    experts_per_layer: int
+    expert_bytes: int
+    token_bytes: int
+    attn_fwd_time: float
+    per_token_expert_time: float
+    optimizer_multiplier: float = 6.0
+
+    def __post_init__(self) -> None:
+        if self.layers <= 0 or self.experts_per_layer <= 0:
+            raise ConfigError("layers and experts_per_layer must be positive")
+        if self.expert_bytes <= 0 or self.token_bytes <= 0:
+            raise ConfigError("expert_bytes and token_bytes must be positive")
+        if self.attn_fwd_time < 0 or self.per_token_expert_time < 0:
+            raise ConfigError("times must be non-negative")
+        if self.optimizer_multiplier < 6:
+            raise ConfigError("optimizer_multiplier must be at least 6 (params + moments in "
+                              "full precision plus a full-precision master copy)")
+
+
+class PolicyKind(str, Enum):
+    """EP and FSSDP are executed; the reference's simulated comparators are not (engine.py:80-85)."""
+
+    EP = "ep"
+    FSSDP = "fssdp"
+
+
+@dataclass(frozen=True)
+class Policy:
+    """Placement policy knobs (engine.py:88-121); FSSDP uses all but interval/reserved/top-k."""
+
+    kind: PolicyKind
+    window: int = 5
+    calibration: bool = True
+    rematerialize: bool = False
+    reshard_interval: int = 100
+    interval: int = 25
+    reserved_slots: int = 0
+    replicate_top_k: int = 1
+    free_bytes_per_device: Optional[int] = None
+    overlap_override: Optional[int] = None
+    capacity_override: Optional[int] = None
+
+    def label(self) -> str:
+        return self.kind.value
+
+    def to_json_obj(self) -> dict:
+        return {"kind": self.kind.value, "window": self.window, "calibration": self.calibration,
+                "rematerialize": self.rematerialize, "reshard_interval": self.reshard_interval,
+                "interval": self.interval, "reserved_slots": self.reserved_slots,
+                "replicate_top_k": self.replicate_top_k,
+                "free_bytes_per_device": self.free_bytes_per_device,
+                "overlap_override": self.overlap_override,
+                "capacity_override": self.capacity_override}
+
+
+@dataclass(eq=False)
+class MemoryBreakdown:
+    """Per-device bytes (engine.py:159-177)."""
+
+    param_bytes: np.ndarray
+    grad_bytes: np.ndarray
+    optimizer_bytes: np.ndarray
+    materialized_bytes: np.ndarray
+
+    def total_per_device(self) -> np.ndarray:
+        return self.param_bytes + self.grad_bytes + self.optimizer_bytes + self.materialized_bytes
+
+    def optimizer_total(self) -> float:
+        return float(self.optimizer_bytes.sum())
+
+
+def memory_report(plan: ShardPlan, materializations, config: ModelConfig,
+                  mode: str = "retain") -> MemoryBreakdown:
+    """Expert memory per device; retain = Σ layers' replicas, rematerialize = max
+    (engine.py:188-226).  Sizes the replica buffers of the device layer."""
+    if mode not in ("retain", "rematerialize"):
+        raise ConfigError(f"unknown memory mode {mode!r}")
+    D = plan.num_devices
+    owned = np.zeros(D, dtype=np.float64)
+    for p in plan.per_layer:
+        owned += np.asarray(p.counts_per_device(), dtype=np.float64)
+    param = owned * config.expert_bytes
+    added = np.zeros((plan.num_layers, D), dtype=np.float64)
+    if materializations is not None:
+        for l, mat in enumerate(materializations):
+            if mat is not None:
+                added[l] = np.asarray(mat.added_per_device, dtype=np.float64)
+    added_bytes = added * config.expert_bytes
+    if mode == "retain":
+        materialized = added_bytes.sum(axis=0)
+    else:
+        materialized = added_bytes.max(axis=0) if plan.num_layers else np.zeros(D)
+    return MemoryBreakdown(param_bytes=param, grad_bytes=param + materialized,
+                           optimizer_bytes=param * config.optimizer_multiplier,
+                           materialized_bytes=materialized)
+
+
+@dataclass
+class LayerDecision:
+    """One layer's executed plan for one iteration."""
+
+    base: ChunkPlacement          # ownership partition (SpAG pre / SpRS post)
+    target: ChunkPlacement        # materialized placement (SpAG post / SpRS pre)
+    added_per_device: tuple
+    route: np.ndarray             # (D, E, D) int64, build_dispatch on the actual counts
+    spag_latency: float = 0.0
+    sprs_latency: float = 0.0
+    remat_latency: float = 0.0
+    calib_time: float = 0.0
+    adopted: bool = False
+    calibrated: bool = False
+
+    @property
+    def materialization(self) -> MaterializationPlan:
+        return MaterializationPlan(self.base, self.target, self.added_per_device)
+
+    @property
+    def is_identity(self) -> bool:
+        return self.target == self.base
+
+
+_MOVE_MULTIPLIER = 7  # params + 6x optimizer state move with a re-sharded expert (engine.py:233)
+
+
+class FssdpPlanner:
+    """Per-run FSSDP control state (engine.py:279-292, 386-402).
+
+    Usage per iteration:  begin_iteration();  plan_layer(l, counts_l) for each layer
+    (after that layer's gate);  end_iteration(step_counts)."""
+
+    def __init__(self, config: ModelConfig, topology, policy: Policy) -> None:
+        if policy.kind not in (PolicyKind.FSSDP, PolicyKind.EP):
+            raise ConfigError(f"unknown policy kind {policy.kind!r}")
+        self.config = config
+        self.topo = topology
+        self.policy = policy
+        self.iteration = 0
+        self.history = [deque(maxlen=max(1, policy.window)) for _ in range(config.layers)]
+        self.shards = ShardPlan.even(config.layers, config.experts_per_layer, topology)
+        if policy.overlap_override is not None:
+            self.t = int(policy.overlap_override)
+        else:
+            self.t = overlap_degree(config.attn_fwd_time, topology, config.expert_bytes)
+        if policy.capacity_override is not None:
+            self.m = int(policy.capacity_override)
+        elif policy.free_bytes_per_device is not None:
+            self.m = policy.free_bytes_per_device // config.expert_bytes
+        else:
+            self.m = config.experts_per_layer
+        self._knobs = N.LayerKnobs(
+            self.t, self.m, int(policy.calibration), int(policy.rematerialize),
+            float(config.expert_bytes), float(config.token_bytes), float(config.attn_fwd_time),
+            float(config.per_token_expert_time))
+        self._topo_c = topology.native()
+        self.last_reshard_time = 0.0
+        self.last_reshard_moves: list = []
+
+    # -- helpers ------------------------------------------------------------------
+    def estimate(self, layer: int) -> Optional[np.ndarray]:
+        if not self.history[layer]:
+            return None
+        return estimate_loads(self.history[layer], self.policy.window)
+
+    def _shard_score(self, plan: ShardPlan, profile: GlobalLoadProfile) -> tuple:
+        """(max node load, max device load), numpy order (engine.py:431-442)."""
+        owners = np.ascontiguousarray(plan.owners())
+        prof = np.ascontiguousarray(profile.per_layer, dtype=np.float64)
+        out = np.zeros(2, dtype=np.float64)
+        N.check(N.LIB.fssdp_shard_score(owners.shape[0], owners.shape[1],
+                                        owners.ctypes.data_as(N.P_i32),
+                                        prof.ctypes.data_as(N.P_f64), N.C.byref(self._topo_c),
+                                        out.ctypes.data_as(N.P_f64)), "shard_score")
+        return (float(out[0]), float(out[1]))
+
+    def _reshard_moves(self, candidate: ShardPlan) -> list:
+        moves = []
+        for l, (old, new) in enumerate(zip(self.shards.per_layer, candidate.per_layer)):
+            oo, no = old.owners(), new.owners()
+            for e in range(old.num_chunks):
+                if oo[e] != no[e]:
+                    moves.append((l, e, int(oo[e]), int(no[e])))
+        return moves
+
+    def _move_latency(self, moves: list) -> float:
+        """_move_latency(pairs, 7*expert_bytes) (engine.py:263-276, 444-453)."""
+        if not moves:
+            return 0.0
+        D = self.topo.num_devices
+        mat = np.zeros((D, D))
+        for _, _, src, dst in moves:
+            if src != dst:
+                mat[src, dst] += _MOVE_MULTIPLIER * self.config.expert_bytes
+        return collective_latency(TrafficMatrix(mat), self.topo)
+
+    # -- iteration protocol -------------------------------------------------------
+    def begin_iteration(self) -> float:
+        """Re-shard trigger (engine.py:470-487); returns the modeled re-shard time.
+        The executed data movement is listed in `last_reshard_moves` (layer, expert, src, dst)."""
+        self.last_reshard_time = 0.0
+        self.last_reshard_moves = []
+        if self.policy.kind != PolicyKind.FSSDP or self.t <= 0 or self.m <= 0:
+            return 0.0
+        if (self.iteration > 0 and self.policy.reshard_interval > 0
+                and self.iteration % self.policy.reshard_interval == 0 and all(self.history)):
+            profile = GlobalLoadProfile(np.stack(
+                [self.estimate(l).sum(axis=0) for l in range(self.config.layers)]))
+            candidate = heterogeneous_sharding(profile, self.t, self.topo)
+            if self._shard_score(candidate, profile) < self._shard_score(self.shards, profile):
+                self.last_reshard_moves = self._reshard_moves(candidate)
+                self.last_reshard_time = self._move_latency(self.last_reshard_moves)
+                self.shards = candidate
+        return self.last_reshard_time
+
+    def plan_layer(self, layer: int, actual) -> LayerDecision:
+        """Adoption gate, calibration, fallback, dispatch for one layer (engine.py:491-553)."""
+        base = self.shards.per_layer[layer]
+        E, D = base.num_chunks, base.num_devices
+        act = np.ascontiguousarray(np.asarray(actual, dtype=np.int64))
+        if act.shape != (D, E):
+            raise TraceMismatchError(f"counts {act.shape} do not match {D} devices x {E} experts")
+        owner = np.ascontiguousarray(base.owners())
+        target = np.zeros((E, D), dtype=np.uint8)
+        added = np.zeros(D, dtype=np.int32)
+        route = np.zeros((D, E, D), dtype=np.int64)
+        dbl = np.zeros(4, dtype=np.float64)
+        flags = np.zeros(2, dtype=np.int32)
+        if self.policy.kind == PolicyKind.EP:
+            knobs = N.LayerKnobs(0, 0, 0, 0, self._knobs.expert_bytes, self._knobs.token_bytes,
+                                 self._knobs.attn_fwd_time, self._knobs.per_token_expert_time)
+            est_ptr = None
+        else:
+            knobs = self._knobs
+            est = self.estimate(layer)
+            est_ptr = None if est is None else np.ascontiguousarray(est, dtype=np.float64)
+        N.check(N.LIB.fssdp_plan_layer(
+            E, owner.ctypes.data_as(N.P_i32),
+            None if est_ptr is None else est_ptr.ctypes.data_as(N.P_f64),
+            act.ctypes.data_as(N.P_i64), N.C.byref(self._topo_c), N.C.byref(knobs),
+            target.ctypes.data_as(N.P_u8), added.ctypes.data_as(N.P_i32),
+            route.ctypes.data_as(N.P_i64), dbl.ctypes.data_as(N.P_f64),
+            flags.ctypes.data_as(N.P_i32)), "plan_layer")
+        return LayerDecision(base=base, target=ChunkPlacement.from_mask(target),
+                             added_per_device=tuple(int(a) for a in added), route=route,
+                             spag_latency=float(dbl[0]), sprs_latency=float(dbl[1]),
+                             remat_latency=float(dbl[2]), calib_time=float(dbl[3]),
+                             adopted=bool(flags[0]), calibrated=bool(flags[1]))
+
+    def end_iteration(self, step: Sequence[np.ndarray]) -> None:
+        """Push this iteration's counts into the history window (engine.py:353-356)."""
+        if len(step) != self.config.layers:
+            raise TraceMismatchError(
+                f"step has {len(step)} layers, config declares {self.config.layers}")
+        for l, counts in enumerate(step):
+            self.history[l].append(np.asarray(counts, dtype=np.int64))
+        self.iteration += 1
+
+    def run_iteration(self, step: Sequence[np.ndarray]) -> list:
+        """All layers of one iteration from a recorded step (trace replay)."""
+        if len(step) != self.config.layers:
+            raise TraceMismatchError(
+                f"step has {len(step)} layers, config declares {self.config.layers}")
+        self.begin_iteration()
+        out = [self.plan_layer(l, counts) for l, counts in enumerate(step)]
+        self.end_iteration(step)
+        return out
+
+    def memory(self, decisions) -> MemoryBreakdown:
+        mode = "rematerialize" if self.policy.rematerialize else "retain"
+        return memory_report(self.shards, [d.materialization for d in decisions], self.config, mode)
