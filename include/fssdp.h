@@ -196,13 +196,13 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
 
 #define FSSDP_GATE_TILE 64 /* tokens per gate CTA (slot ranks are tile-relative) */
 
-/* K1: logits = x · Wgᵀ (fp32), top-k (ties -> lower expert id), renormalised softmax
- * weights, tile-relative slot ranks (token-slot order (t, j) ascending) and per-tile
- * expert histograms.  x [T*d] bf16, wg [E*d] fp32.  logits may be NULL.
- * tile_counts[ceil(T/64) * E]. */
-int fssdp_gate_topk(const void* x, const float* wg, int64_t T, int32_t d, int32_t E, int32_t k,
-                    float* logits, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
-                    int32_t* tile_counts, void* stream);
+/* K1: logits = x · Wgᵀ (+ bias) (fp32), top-k (ties -> lower expert id), renormalised
+ * softmax weights, tile-relative slot ranks (token-slot order (t, j) ascending) and
+ * per-tile expert histograms.  x [T*d] bf16, wg [E*d] fp32, bias [E] fp32 or NULL.
+ * logits may be NULL.  tile_counts[ceil(T/64) * E]. */
+int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
+                    int32_t E, int32_t k, float* logits, int32_t* topk_idx, float* topk_w,
+                    int32_t* slot_rank, int32_t* tile_counts, void* stream);
 
 /* Top-k / weights / ranks only, from given fp32 logits [T*E] (same semantics as K1's
  * tail; used to pin K1's selection bit-exactly against the CPU oracle). */
@@ -212,7 +212,8 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
 /* K2: exclusive scan of tile_counts over tiles (tile_prefix, same shape), this rank's
  * per-expert totals, and the counts all-gather: the row is stored into every peer's
  * D x E int32 table at heap offset table_off (row = rank), followed by a device
- * barrier (barrier slot `bar_slot`, value `epoch`). */
+ * barrier (barrier slot `bar_slot`, value `epoch`; a negative bar_slot skips every
+ * barrier of an entry point — single rank, or lockstep emulation of several ranks). */
 int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,

@@ -145,6 +145,57 @@ def combine(rows: np.ndarray, w: np.ndarray) -> np.ndarray:
     return bf16_round(acc)
 
 
+def moe_layer_fwd_bwd(x, idx, w, wg, experts, dy):
+    """Whole-layer restatement for one rank's tokens (placement-independent math).
+
+    x [T, d] bf16-valued float32; idx/w [T, k] (the device's own routing, pinned
+    bit-exactly by the gate tests); wg [E, d]; experts {e: (W1 [f, d], W2 [d, f])}
+    bf16-valued float32; dy [T, d] bf16-valued float32.
+    Returns dict(y, dx, g (slot <dy, Y>), dlogit, dW1 {e}, dW2 {e}, dWg)."""
+    T, k = idx.shape
+    d = x.shape[1]
+    Y = np.zeros((T, k, d), dtype=np.float32)
+    A = {}
+    H = {}
+    for e, (W1, W2) in experts.items():
+        rows = np.argwhere(idx == e)
+        if len(rows) == 0:
+            continue
+        xe = x[rows[:, 0]].astype(np.float32)
+        a = bf16_round((xe @ W1.T).astype(np.float32))
+        h = bf16_round(gelu_tanh(a).astype(np.float32))
+        Y[rows[:, 0], rows[:, 1]] = bf16_round((h @ W2.T).astype(np.float32))
+        A[e], H[e] = (rows, a), h
+    y = combine(Y, w)
+    # backward
+    g = np.einsum("td,tkd->tk", dy.astype(np.float64), Y.astype(np.float64)).astype(np.float32)
+    sg = (w.astype(np.float64) * g).sum(axis=1, keepdims=True)
+    dlogit = (w * (g - sg)).astype(np.float32)
+    dXs = np.zeros((T, k, d), dtype=np.float32)
+    dW1, dW2 = {}, {}
+    for e, (W1, W2) in experts.items():
+        f = W1.shape[0]
+        if e not in A:
+            dW1[e] = np.zeros_like(W1)
+            dW2[e] = np.zeros_like(W2)
+            continue
+        rows, a = A[e]
+        dYe = bf16_round((w[rows[:, 0], rows[:, 1]][:, None] * dy[rows[:, 0]]).astype(np.float32))
+        dH = (dYe @ W2).astype(np.float32)
+        dA = bf16_round((dH * gelu_tanh_grad(a)).astype(np.float32))
+        dXs[rows[:, 0], rows[:, 1]] = bf16_round((dA @ W1).astype(np.float32))
+        xe = x[rows[:, 0]].astype(np.float32)
+        dW1[e] = (dA.T.astype(np.float64) @ xe).astype(np.float32)
+        dW2[e] = (dYe.T.astype(np.float64) @ H[e]).astype(np.float32)
+        del f
+    dx = dXs.sum(axis=1) + np.einsum("tk,tkd->td", dlogit, wg[idx])
+    dWg = np.zeros_like(wg)
+    for j in range(k):
+        np.add.at(dWg, idx[:, j], dlogit[:, j:j + 1] * x)
+    return dict(y=y, dx=bf16_round(dx.astype(np.float32)), g=g, dlogit=dlogit, dW1=dW1, dW2=dW2,
+                dWg=dWg)
+
+
 def sprs_sum(contribs: list[np.ndarray]) -> np.ndarray:
     """Owner's reduced gradient: float32 sum in the listed (ascending device) order."""
     acc = np.zeros_like(contribs[0], dtype=np.float32)

@@ -89,7 +89,7 @@ _SIGS = {
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
                            vp, i64, vp],
-    "fssdp_gate_topk": [vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+    "fssdp_gate_topk": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],

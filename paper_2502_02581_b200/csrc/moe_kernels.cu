@@ -40,6 +40,7 @@ __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { retur
 __device__ __forceinline__ void world_barrier_warp(const uint64_t* __restrict__ peer_bases,
                                                    int64_t flags_off, int rank, int world,
                                                    int slot, uint32_t epoch) {
+  if (slot < 0) return;  // barrier disabled (single rank, or lockstep emulation)
   const int lane = threadIdx.x & 31;
   if (lane < world) {
     uint32_t* remote = reinterpret_cast<uint32_t*>(peer_bases[lane] + flags_off) +
@@ -58,6 +59,7 @@ __device__ __forceinline__ void grid_done_then_barrier(uint32_t* grid_counter,
                                                        const uint64_t* __restrict__ peer_bases,
                                                        int64_t flags_off, int rank, int world,
                                                        int slot, uint32_t epoch) {
+  if (slot < 0) return;
   __shared__ int is_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -145,8 +147,9 @@ __device__ void gate_select_tile(const float* __restrict__ lg, int lg_stride, in
 }
 
 __global__ void __launch_bounds__(kGateThreads)
-    gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg, int64_t T,
-                     int d, int E, int k, float* __restrict__ logits,
+    gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
+                     const float* __restrict__ bias, int64_t T, int d, int E, int k,
+                     float* __restrict__ logits,
                      int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                      int32_t* __restrict__ slot_rank, int32_t* __restrict__ tile_counts) {
   // dynamic smem: xs [64][kGateChunk+8] bf16 | ws [E][kGateChunk+4] fp32; the logits
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kGateThreads)
 #pragma unroll
   for (int q = 0; q < kGateMaxE / 4; ++q) {
     const int e = grp + 4 * q;
-    if (e < E) lg[tok][e] = acc[q];
+    if (e < E) lg[tok][e] = bias != nullptr ? __fadd_rn(acc[q], bias[e]) : acc[q];
   }
   __syncthreads();
   if (logits != nullptr) {
@@ -607,8 +610,8 @@ using namespace fssdp;
 
 extern "C" {
 
-int fssdp_gate_topk(const void* x, const float* wg, int64_t T, int32_t d, int32_t E, int32_t k,
-                    float* logits, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
+int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
+                    int32_t E, int32_t k, float* logits, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
                     int32_t* tile_counts, void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
       k > E) {
@@ -631,7 +634,7 @@ int fssdp_gate_topk(const void* x, const float* wg, int64_t T, int32_t d, int32_
     configured = true;
   }
   gate_topk_kernel<<<tiles, kGateThreads, smem, as_stream(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, logits, topk_idx, topk_w, slot_rank,
+      static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k, logits, topk_idx, topk_w, slot_rank,
       tile_counts);
   return launch_status();
 }

@@ -186,6 +186,7 @@ class FssdpPlanner:
         self._topo_c = topology.native()
         self.last_reshard_time = 0.0
         self.last_reshard_moves: list = []
+        self._step = None
 
     # -- helpers ------------------------------------------------------------------
     def estimate(self, layer: int) -> Optional[np.ndarray]:
@@ -285,6 +286,25 @@ class FssdpPlanner:
         for l, counts in enumerate(step):
             self.history[l].append(np.asarray(counts, dtype=np.int64))
         self.iteration += 1
+
+    # -- layer-driven protocol (used by FssdpMoE) ---------------------------------
+    def plan(self, layer: int, actual) -> LayerDecision:
+        """plan_layer for a live layer; the first call of an iteration runs the re-shard
+        trigger, `finish()` closes the iteration with the counts seen."""
+        if self._step is None:
+            self.begin_iteration()
+            self._step = [None] * self.config.layers
+        self._step[layer] = np.asarray(actual, dtype=np.int64)
+        return self.plan_layer(layer, actual)
+
+    def finish(self) -> None:
+        if self._step is None:
+            return
+        step = self._step
+        self._step = None
+        if any(s is None for s in step):
+            raise TraceMismatchError("iteration finished before every layer was planned")
+        self.end_iteration(step)
 
     def run_iteration(self, step: Sequence[np.ndarray]) -> list:
         """All layers of one iteration from a recorded step (trace replay)."""

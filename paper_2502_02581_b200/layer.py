@@ -1,0 +1,413 @@
+"""FssdpMoE — one FSSDP MoE layer executed on B200s (the hot path of BASELINE.json).
+
+Forward (per rank):  K1 gate -> K2 counts all-gather -> host plan (FssdpPlanner, bit-exact
+with moesim) -> K3 SpAG of the replicas this rank materializes -> K4 dispatch ->
+K5 grouped FFN (tcgen05) -> K6 combine.
+Backward:  K7 token-side A2A (w·dy to the experts, <dy, Y> for the gate) -> optional
+re-materialization SpAG -> grouped dgrad/wgrad (tcgen05) -> dX combine + gate
+backward -> K8 SpRS of replica gradients to their owners.
+
+All heavy work is sm_100a kernels in libfssdp.so; PyTorch only owns memory and streams.
+Execution is split into phases so a driver can run several logical ranks in lockstep
+on one GPU (PeerGroup mode "emulated") — the multi-rank parity tests do that.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import ops
+from .comm import HeapLayout, PeerGroup
+from .engine import FssdpPlanner
+from .errors import DimensionError, InternalError
+from .plan_tables import GEMM_NAMES, PackedTables, build_rank_tables
+
+# barrier slots (flag pads) used by one layer; layer i uses base + 8*i
+BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_SPAG = range(7)
+
+
+@dataclass(frozen=True)
+class LayerGeometry:
+    d_model: int
+    d_ff: int
+    num_experts: int
+    top_k: int
+    max_tokens: int      # per rank per step
+    world: int
+    slots: int           # local expert slot capacity (owned + replicas)
+
+    @property
+    def recv_cap(self) -> int:
+        rows = self.world * self.max_tokens * self.top_k + self.slots * 127
+        return (rows + 127) // 128 * 128
+
+    @property
+    def slot_param_bytes(self) -> int:      # [W1 f×d | W2 d×f] bf16
+        return 4 * self.d_model * self.d_ff
+
+    @property
+    def slot_grad_elems(self) -> int:       # [dW1 | dW2] fp32
+        return 2 * self.d_model * self.d_ff
+
+    @property
+    def expert_bytes(self) -> int:
+        return self.slot_param_bytes
+
+    def validate(self) -> None:
+        if self.d_model % 256 or self.d_ff % 256:
+            raise DimensionError("d_model and d_ff must be multiples of 256 (GEMM N tile)")
+        if not 1 <= self.top_k <= min(8, self.num_experts) or self.num_experts > 64:
+            raise DimensionError("need 1 <= top_k <= 8 and num_experts <= 64")
+
+    def add_regions(self, layout: HeapLayout, prefix: str) -> None:
+        d, R = self.d_model, self.recv_cap
+        layout.add(prefix + "params", self.slots * self.slot_param_bytes)
+        layout.add(prefix + "grads", self.slots * self.slot_grad_elems * 4)
+        layout.add(prefix + "xrecv", R * d * 2)
+        layout.add(prefix + "y", R * d * 2)
+        layout.add(prefix + "dyrecv", R * d * 2)
+        layout.add(prefix + "dxe", R * d * 2)
+        layout.add(prefix + "counts", self.world * self.num_experts * 4)
+
+
+def default_slots(num_experts: int, world: int, m: int) -> int:
+    return min(num_experts, -(-num_experts // world) + max(0, m))
+
+
+class FssdpMoE:
+    """One FSSDP MoE layer on one (logical) rank.
+
+    Parameters live in the rank's symmetric heap: the owned expert shards (slots
+    [0, n_owned)) and the SpAG replica slots after them; gradients likewise (fp32)."""
+
+    def __init__(self, geom: LayerGeometry, group: PeerGroup, planner: FssdpPlanner,
+                 layer_index: int = 0, seed: int = 0, prefix: str = "L0."):
+        geom.validate()
+        self.g = geom
+        self.group = group
+        self.planner = planner
+        self.layer = layer_index
+        self.rank = group.rank
+        self.world = group.world
+        self.dev = group.device
+        self.seed = seed
+        self.bar_base = 8 * layer_index
+        L = group.layout
+        heap = group.local
+        d, f, E, R = geom.d_model, geom.d_ff, geom.num_experts, geom.recv_cap
+        self.off = {k: L.offset(prefix + k) for k in
+                    ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts")}
+        self.flags_off = L.offset("flags")
+        self.params = heap.tensor(self.off["params"], (geom.slots, 2 * d * f), torch.bfloat16)
+        self.grads = heap.tensor(self.off["grads"], (geom.slots, 2 * d * f), torch.float32)
+        self.xrecv = heap.tensor(self.off["xrecv"], (R, d), torch.bfloat16)
+        self.y_e = heap.tensor(self.off["y"], (R, d), torch.bfloat16)
+        self.dyrecv = heap.tensor(self.off["dyrecv"], (R, d), torch.bfloat16)
+        self.dxe = heap.tensor(self.off["dxe"], (R, d), torch.bfloat16)
+        self.counts_table = heap.tensor(self.off["counts"], (self.world, E), torch.int32)
+        # 2-D TMA views of the parameter region
+        flat = self.params.view(-1)
+        self.w1_view = flat.view(geom.slots * 2 * f, d)                  # W1 of slot s: rows s*2f..
+        self.w2_view = flat[f * d:].view(geom.slots * 2 * d - d, f)      # W2 of slot s: rows s*2d..
+        # local activations (capacity-sized once, so plans never reallocate)
+        self.a_pre = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
+        self.h = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
+        self.da = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
+        Tc = geom.max_tokens
+        k = geom.top_k
+        tiles = (Tc + ops.GATE_TILE - 1) // ops.GATE_TILE
+        self.wg = torch.empty(E, d, dtype=torch.float32, device=self.dev)
+        self.gate_bias = torch.zeros(E, dtype=torch.float32, device=self.dev)
+        self.dwg = torch.zeros(E, d, dtype=torch.float32, device=self.dev)
+        self.topk_idx = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
+        self.topk_w = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
+        self.slot_rank = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
+        self.tile_counts = torch.empty(max(tiles, 1), E, dtype=torch.int32, device=self.dev)
+        self.tile_prefix = torch.empty_like(self.tile_counts)
+        self.slot_dest = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
+        self.slot_pos = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
+        self.slot_grad = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
+        self.dlogit = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
+        self.wg_ws = torch.empty(16 * E * d, dtype=torch.float32, device=self.dev)
+        self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
+        self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
+        self.blob_dev = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
+        self.decision = None
+        self.tables = None
+        self.T = 0
+        self.x = None
+        self._owned_expert_ids = None
+        self.init_parameters(seed)
+
+    # ------------------------------------------------------------ parameters
+    def owned_experts(self) -> list:
+        base = self.planner.shards.per_layer[self.layer]
+        return sorted(base.chunks_on(self.rank))
+
+    def init_parameters(self, seed: int) -> None:
+        """Deterministic per-expert init (independent of ownership): W1 ~ N(0, 1/d),
+        W2 ~ N(0, 1/f), Wg ~ N(0, 1/d) (replicated)."""
+        d, f, E = self.g.d_model, self.g.d_ff, self.g.num_experts
+        gen = torch.Generator(device=self.dev)
+        gen.manual_seed(seed * 7919 + 17)
+        self.wg.copy_(torch.randn(E, d, generator=gen, device=self.dev) / d ** 0.5)
+        for s, e in enumerate(self.owned_experts()):
+            w1, w2 = self.make_expert(e, seed)
+            self.params[s, : f * d].copy_(w1.reshape(-1))
+            self.params[s, f * d:].copy_(w2.reshape(-1))
+        self._owned_expert_ids = self.owned_experts()
+
+    def make_expert(self, e: int, seed: int):
+        d, f = self.g.d_model, self.g.d_ff
+        gen = torch.Generator(device=self.dev)
+        gen.manual_seed(seed * 1_000_003 + 31 * e + 1)
+        w1 = (torch.randn(f, d, generator=gen, device=self.dev) / d ** 0.5).bfloat16()
+        w2 = (torch.randn(d, f, generator=gen, device=self.dev) / f ** 0.5).bfloat16()
+        return w1, w2
+
+    def expert_weight(self, e: int):
+        """(W1 [f,d], W2 [d,f]) of an owned expert (views into the heap)."""
+        s = self._owned_expert_ids.index(e)
+        d, f = self.g.d_model, self.g.d_ff
+        return self.params[s, : f * d].view(f, d), self.params[s, f * d:].view(d, f)
+
+    def expert_grad(self, e: int):
+        """(dW1, dW2) fp32 of an owned expert after backward (SpRS-reduced)."""
+        s = self._owned_expert_ids.index(e)
+        d, f = self.g.d_model, self.g.d_ff
+        return self.grads[s, : f * d].view(f, d), self.grads[s, f * d:].view(d, f)
+
+    # ------------------------------------------------------------ helpers
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def _bar(self, which: int):
+        slot, epoch = self.group.barrier_args(self.bar_base + which)
+        return slot, epoch
+
+    def _tab(self, name: str) -> C.c_void_p:
+        return C.c_void_p(self.blob_dev.data_ptr() + self.packed.offsets[name])
+
+    def _pb(self) -> C.c_void_p:
+        return C.c_void_p(self.group.peer_bases.data_ptr())
+
+    # ------------------------------------------------------------ forward phases
+    def phase_gate(self, x: torch.Tensor) -> None:
+        if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.g.d_model:
+            raise DimensionError(f"x must be [T, {self.g.d_model}] bf16, got {tuple(x.shape)} {x.dtype}")
+        T = x.shape[0]
+        if T > self.g.max_tokens:
+            raise DimensionError(f"{T} tokens exceed max_tokens={self.g.max_tokens}")
+        self.x = x.contiguous()
+        self.T = T
+        E, k = self.g.num_experts, self.g.top_k
+        N.call("fssdp_gate_topk", ops._ptr(self.x), ops._ptr(self.wg), ops._ptr(self.gate_bias),
+               T, self.g.d_model, E, k,
+               C.c_void_p(0), ops._ptr(self.topk_idx), ops._ptr(self.topk_w),
+               ops._ptr(self.slot_rank), ops._ptr(self.tile_counts), self._stream())
+
+    def phase_counts(self) -> None:
+        n_tiles = (self.T + ops.GATE_TILE - 1) // ops.GATE_TILE
+        slot, epoch = self._bar(BAR_COUNTS)
+        N.call("fssdp_route_scan_allgather", ops._ptr(self.tile_counts), n_tiles,
+               self.g.num_experts, ops._ptr(self.tile_prefix), self._pb(), self.off["counts"],
+               self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch), self._stream())
+
+    def phase_plan(self) -> None:
+        counts = self.counts_table.cpu().numpy().astype(np.int64)  # host sync point #1
+        dec = self.planner.plan(self.layer, counts)
+        base_owner = dec.base.owners()
+        tables = build_rank_tables(self.rank, base_owner, dec.target.mask, dec.route,
+                                   self.g.d_model, self.g.d_ff)
+        if len(tables.slots) > self.g.slots:
+            raise InternalError(f"plan needs {len(tables.slots)} slots > capacity {self.g.slots}")
+        if tables.recv_rows > self.g.recv_cap:
+            raise InternalError("receive rows exceed capacity")
+        owned_now = sorted(e for e in tables.slots if base_owner[e] == self.rank)
+        if owned_now != self._owned_expert_ids:
+            raise InternalError("ownership changed without a re-shard data move")
+        self.decision, self.tables = dec, tables
+        self.packed = PackedTables(tables)
+        nb = len(self.packed.blob)
+        if nb > self.blob_host.numel():
+            raise InternalError("plan tables exceed the staging buffer")
+        self.blob_host[:nb].numpy()[:] = self.packed.blob
+        self.blob_dev[:nb].copy_(self.blob_host[:nb], non_blocking=True)  # boundary #2
+        self.gemm = {}
+        for name in GEMM_NAMES:
+            arr, n_tiles, total = tables.groups[name]
+            self.gemm[name] = (len(arr), n_tiles, total)
+
+    def phase_spag(self) -> None:
+        n = len(self.tables.spag_copies)
+        if n == 0:
+            return
+        N.call("fssdp_spag", self._pb(), self.rank, self.off["params"], self.g.slot_param_bytes,
+               self._tab("spag"), n, self._stream())
+
+    def phase_dispatch(self) -> None:
+        t = self.tables
+        slot, epoch = self._bar(BAR_DISPATCH)
+        N.call("fssdp_dispatch", ops._ptr(self.x), ops._ptr(self.topk_idx),
+               ops._ptr(self.slot_rank), ops._ptr(self.tile_prefix), self.T, self.g.d_model,
+               self.g.num_experts, self.g.top_k, self.world, self._tab("route_cum"),
+               self._tab("recv_base"), ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
+               self._pb(), self.off["xrecv"], self._tab("zero_rows"), len(t.zero_rows),
+               self.flags_off, self.rank, slot, C.c_uint32(epoch),
+               C.c_void_p(self.grid_counter.data_ptr()), self._stream())
+
+    def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None):
+        ng, n_tiles, total = self.gemm[name]
+        if total == 0:
+            return
+        N.call("fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1],
+               a.shape[0], ops._ptr(b), b.shape[1], b.shape[0], self._tab(name), ng, n_tiles,
+               total, ops._ptr(c), ops._ptr(c2), ops._ptr(aux), ldc, self._stream())
+
+    def phase_experts_fwd(self) -> None:
+        f, d = self.g.d_ff, self.g.d_model
+        self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.a_pre, f, ops.EPI_GELU,
+                   c2=self.h)
+        self._gemm("fwd2", self.h, False, self.w2_view, False, self.y_e, d, ops.EPI_BF16)
+
+    def phase_barrier(self, which: int) -> None:
+        slot, epoch = self._bar(which)
+        if slot < 0:
+            return
+        N.call("fssdp_barrier", self._pb(), self.flags_off, self.rank, self.world, slot,
+               C.c_uint32(epoch), self._stream())
+
+    def phase_combine(self) -> torch.Tensor:
+        y = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
+        N.call("fssdp_combine", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
+               ops._ptr(self.topk_w), self.T, self.g.d_model, self.g.top_k, self._pb(),
+               self.off["y"], ops._ptr(y), self._stream())
+        return y
+
+    # ------------------------------------------------------------ backward phases
+    def phase_dispatch_grad(self, dy: torch.Tensor) -> None:
+        if dy.shape != (self.T, self.g.d_model) or dy.dtype != torch.bfloat16:
+            raise DimensionError("dy must match the forward output ([T, d] bf16)")
+        self.dy = dy.contiguous()
+        t = self.tables
+        slot, epoch = self._bar(BAR_DGRAD)
+        N.call("fssdp_dispatch_grad", ops._ptr(self.dy), ops._ptr(self.slot_dest),
+               ops._ptr(self.slot_pos), ops._ptr(self.topk_w), self.T, self.g.d_model,
+               self.g.top_k, self._pb(), self.off["y"], self.off["dyrecv"],
+               ops._ptr(self.slot_grad), self._tab("zero_rows"), len(t.zero_rows),
+               self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch),
+               C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
+
+    def phase_experts_bwd(self) -> None:
+        f, d = self.g.d_ff, self.g.d_model
+        self._gemm("dgrad2", self.dyrecv, False, self.w2_view, True, self.da, f, ops.EPI_DGELU,
+                   aux=self.a_pre)
+        self._gemm("dgrad1", self.da, False, self.w1_view, True, self.dxe, d, ops.EPI_BF16)
+        grads2d = self.grads.view(-1)
+        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32)
+        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32)
+
+    def phase_combine_dx(self) -> torch.Tensor:
+        dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
+        N.call("fssdp_combine_dx", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
+               ops._ptr(self.topk_idx), ops._ptr(self.topk_w), ops._ptr(self.slot_grad),
+               ops._ptr(self.wg), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,
+               self._pb(), self.off["dxe"], ops._ptr(self.dlogit), ops._ptr(dx), self._stream())
+        return dx
+
+    def phase_gate_wgrad(self) -> None:
+        N.call("fssdp_gate_wgrad", ops._ptr(self.x), ops._ptr(self.topk_idx),
+               ops._ptr(self.dlogit), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,
+               ops._ptr(self.wg_ws), ops._ptr(self.dwg), self._stream())
+
+    def phase_sprs(self) -> None:
+        n = len(self.tables.sprs_jobs)
+        if n == 0:
+            return
+        N.call("fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.g.slot_grad_elems,
+               self._tab("sprs_jobs"), n, self._tab("sprs_srcs"), self._stream())
+
+    # ------------------------------------------------------------ one rank per process
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self.phase_gate(x)
+        self.phase_counts()
+        self.phase_plan()
+        self.phase_spag()
+        self.phase_dispatch()
+        self.phase_experts_fwd()
+        self.phase_barrier(BAR_Y)
+        return self.phase_combine()
+
+    def backward(self, dy: torch.Tensor, rematerialize: bool | None = None) -> torch.Tensor:
+        self.phase_dispatch_grad(dy)
+        remat = self.planner.policy.rematerialize if rematerialize is None else rematerialize
+        if remat:
+            self.phase_spag()
+        self.phase_experts_bwd()
+        self.phase_barrier(BAR_DX)
+        dx = self.phase_combine_dx()
+        self.phase_gate_wgrad()
+        self.phase_sprs()
+        self.phase_barrier(BAR_END)
+        return dx
+
+    def reduce_gate_grad(self, pg=None) -> None:
+        """dWg is data-parallel (the gate is replicated): one small NCCL all-reduce."""
+        if self.world > 1 and self.group.mode == "dist":
+            import torch.distributed as dist
+
+            dist.all_reduce(self.dwg, group=pg)
+
+
+class FssdpMoEFunction(torch.autograd.Function):
+    """autograd wrapper: y = layer(x); expert grads land in the layer's heap (SpRS-reduced
+    on their owners), the gate grad in layer.dwg."""
+
+    @staticmethod
+    def forward(ctx, x, layer):
+        ctx.layer = layer
+        return layer.forward(x)
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx = ctx.layer.backward(dy.to(torch.bfloat16).contiguous())
+        ctx.layer.planner.finish()
+        return dx, None
+
+
+def run_lockstep_forward(layers: list, xs: list) -> list:
+    """Emulated multi-rank forward: every phase on every logical rank before the next."""
+    for ly, x in zip(layers, xs):
+        ly.phase_gate(x)
+    for ly in layers:
+        ly.phase_counts()
+    for ly in layers:
+        ly.phase_plan()
+    for ly in layers:
+        ly.phase_spag()
+    for ly in layers:
+        ly.phase_dispatch()
+    for ly in layers:
+        ly.phase_experts_fwd()
+    return [ly.phase_combine() for ly in layers]
+
+
+def run_lockstep_backward(layers: list, dys: list, rematerialize: bool = False) -> list:
+    for ly, dy in zip(layers, dys):
+        ly.phase_dispatch_grad(dy)
+    if rematerialize:
+        for ly in layers:
+            ly.phase_spag()
+    for ly in layers:
+        ly.phase_experts_bwd()
+    dxs = [ly.phase_combine_dx() for ly in layers]
+    for ly in layers:
+        ly.phase_gate_wgrad()
+    for ly in layers:
+        ly.phase_sprs()
+    return dxs

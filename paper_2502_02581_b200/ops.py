@@ -83,7 +83,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
 
 
 # ------------------------------------------------------------------ gate
-def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, want_logits: bool = False, stream=None):
+def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, want_logits: bool = False, stream=None,
+              bias: torch.Tensor | None = None):
     """K1: returns (topk_idx [T,k] i32, topk_w [T,k] f32, slot_rank [T,k] i32,
     tile_counts [tiles,E] i32, logits [T,E] f32 | None)."""
     _need(x, torch.bfloat16, "x")
@@ -97,7 +98,10 @@ def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, want_logits: bool = Fal
     rank = torch.empty(T, k, dtype=torch.int32, device=dev)
     tc = torch.empty(max(tiles, 1), E, dtype=torch.int32, device=dev)
     logits = torch.empty(T, E, dtype=torch.float32, device=dev) if want_logits else None
-    N.call("fssdp_gate_topk", _ptr(x), _ptr(wg), T, d, E, k, _ptr(logits), _ptr(idx), _ptr(w),
+    if bias is not None:
+        _need(bias, torch.float32, "bias")
+    N.call("fssdp_gate_topk", _ptr(x), _ptr(wg), _ptr(bias), T, d, E, k, _ptr(logits), _ptr(idx),
+           _ptr(w),
            _ptr(rank), _ptr(tc), _stream(stream))
     return idx, w, rank, tc, logits
 

@@ -1,0 +1,197 @@
+"""Device plan tables: turn one layer's global plan into the flat int32 tables the
+kernels consume (SURVEY.md §3.5 boundary #2).
+
+Every rank derives every table from the same deterministic global plan (target
+placement + build_dispatch route), so no table is ever exchanged between ranks.
+
+Receive layout on device d: its local experts occupy *slots* — owned experts
+(ascending id) then replicas (ascending id); each slot's tokens form one segment of
+the receive buffers, segments in slot order, each padded to a multiple of 128 rows
+(the GEMM M tile), so an M tile never mixes experts and wgrad K blocks see zero pad
+rows.  Inside a segment, tokens are grouped by source device (ascending), and inside
+a source by that source's token-slot order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import InternalError
+
+ROW_ALIGN = 128
+GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
+                        ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("pad_", "<i4"),
+                        ("c_off", "<i8")])
+GEMM_NAMES = ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2")
+
+
+def slot_maps(base_owner: np.ndarray, target_mask: np.ndarray) -> list[dict]:
+    """Per device: {expert: slot}.  Owned experts first (ascending), then replicas."""
+    E, D = target_mask.shape
+    maps = []
+    for d in range(D):
+        owned = [e for e in range(E) if base_owner[e] == d]
+        reps = [e for e in range(E) if target_mask[e, d] and base_owner[e] != d]
+        maps.append({e: s for s, e in enumerate(owned + reps)})
+    return maps
+
+
+@dataclass
+class RankTables:
+    """Everything one rank's kernels need for one layer-iteration."""
+
+    rank: int
+    world: int
+    slots: dict                  # expert -> local slot
+    n_owned: int
+    seg_start: np.ndarray        # [n_slots] receive row of each slot's segment
+    seg_rows: np.ndarray         # [n_slots] real rows
+    seg_padded: np.ndarray       # [n_slots] rows incl. padding (multiple of 128)
+    recv_rows: int               # total receive rows on this rank (padded)
+    route_cum: np.ndarray        # [E, D+1] int32 cumulative split of this source's cells
+    recv_base: np.ndarray        # [E, D] int32 first receive row on d of (this source, e)
+    zero_rows: np.ndarray        # [n, 2] int32 {row, count} padding rows of this rank
+    spag_copies: np.ndarray      # [n, 3] int32 {src_rank, src_slot, dst_slot}
+    sprs_jobs: np.ndarray        # [n, 3] int32 {dst_slot, src_begin, src_count}
+    sprs_srcs: np.ndarray        # [m, 2] int32 {rank, slot}, ascending rank per job
+    groups: dict                 # name -> (GROUP_DTYPE array, n_tiles, total_tiles)
+
+
+def _segments(route: np.ndarray, slots: dict, d: int):
+    n = len(slots)
+    rows = np.zeros(n, dtype=np.int64)
+    for e, s in slots.items():
+        rows[s] = int(route[:, e, d].sum())
+    padded = (rows + ROW_ALIGN - 1) // ROW_ALIGN * ROW_ALIGN
+    start = np.concatenate([[0], np.cumsum(padded)[:-1]]).astype(np.int64)
+    return start, rows, padded
+
+
+def _finalize(groups: np.ndarray, n_tiles: int):
+    tiles = groups["m_tiles"].astype(np.int64) * n_tiles
+    groups["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]]) if len(tiles) else tiles
+    return groups, n_tiles, int(tiles.sum())
+
+
+def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int):
+    """The six grouped-GEMM descriptor arrays of one rank (see gemm_sm100.cu).
+
+    Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16; viewed as
+    [(slots*2f) x d] rows for W1 and, from offset f*d, as [(slots*2d) x f] rows for W2.
+    Gradient slot s holds [dW1 (f x d) | dW2 (d x f)] fp32."""
+    d, f = d_model, d_ff
+    n = len(seg_start)
+    out = {}
+    g = np.zeros(n, dtype=GROUP_DTYPE)
+    for i in range(n):
+        s = slot_of_seg[i]
+        mt = int(seg_padded[i] // 128)
+        st = int(seg_start[i])
+        g[i] = (mt, 0, st, 0, s * 2 * f, 0, d // 64, 0, st * f)
+    out["fwd1"] = _finalize(g.copy(), f // 256)
+    for i in range(n):
+        s = slot_of_seg[i]
+        st = int(seg_start[i])
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * 2 * d, 0, f // 64, 0, st * d)
+    out["fwd2"] = _finalize(g.copy(), d // 256)
+    for i in range(n):  # dH = dY . W2  (B = W2 [K=d][N=f], MN-major)
+        s = slot_of_seg[i]
+        st = int(seg_start[i])
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * 2 * d, d // 64, 0, st * f)
+    out["dgrad2"] = _finalize(g.copy(), f // 256)
+    for i in range(n):  # dXe = dA . W1  (B = W1 [K=f][N=d], MN-major)
+        s = slot_of_seg[i]
+        st = int(seg_start[i])
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * 2 * f, f // 64, 0, st * d)
+    out["dgrad1"] = _finalize(g.copy(), d // 256)
+    for i in range(n):  # dW1 = dA^T X  (K = the segment's tokens)
+        s = slot_of_seg[i]
+        st = int(seg_start[i])
+        g[i] = (f // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), 0, s * 2 * f * d)
+    out["wgrad1"] = _finalize(g.copy(), d // 256)
+    for i in range(n):  # dW2 = dY^T H
+        s = slot_of_seg[i]
+        st = int(seg_start[i])
+        g[i] = (d // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), 0, s * 2 * f * d + f * d)
+    out["wgrad2"] = _finalize(g.copy(), f // 256)
+    return out
+
+
+def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray,
+                      route: np.ndarray, d_model: int, d_ff: int) -> RankTables:
+    E, D = target_mask.shape
+    if route.shape != (D, E, D):
+        raise InternalError(f"route shape {route.shape} != {(D, E, D)}")
+    maps = slot_maps(base_owner, target_mask)
+    segs = [_segments(route, maps[d], d) for d in range(D)]
+    slots = maps[rank]
+    start, rows, padded = segs[rank]
+
+    # where this source's rows land on every destination
+    route_cum = np.zeros((E, D + 1), dtype=np.int32)
+    route_cum[:, 1:] = np.cumsum(route[rank], axis=1)
+    recv_base = np.zeros((E, D), dtype=np.int32)
+    for e in range(E):
+        for d in range(D):
+            if e in maps[d]:
+                s = maps[d][e]
+                recv_base[e, d] = segs[d][0][s] + int(route[:rank, e, d].sum())
+    zero = [(int(start[s] + rows[s]), int(padded[s] - rows[s])) for s in range(len(slots))
+            if padded[s] > rows[s]]
+    zero_rows = np.array(zero, dtype=np.int32).reshape(-1, 2)
+
+    # SpAG: replicas this rank materializes, pulled from the owner's slot
+    copies = []
+    for e, s in sorted(slots.items(), key=lambda kv: kv[1]):
+        o = int(base_owner[e])
+        if o != rank:
+            copies.append((o, maps[o][e], s))
+    spag = np.array(copies, dtype=np.int32).reshape(-1, 3)
+
+    # SpRS: for owned experts with replicas, reduce every holder's grad in ascending rank order
+    jobs, srcs = [], []
+    for e, s in sorted(slots.items(), key=lambda kv: kv[1]):
+        if int(base_owner[e]) != rank:
+            continue
+        holders = [d for d in range(D) if target_mask[e, d]]
+        if len(holders) <= 1:
+            continue
+        jobs.append((s, len(srcs), len(holders)))
+        srcs.extend((h, maps[h][e]) for h in holders)
+    sprs_jobs = np.array(jobs, dtype=np.int32).reshape(-1, 3)
+    sprs_srcs = np.array(srcs, dtype=np.int32).reshape(-1, 2)
+
+    order = list(range(len(slots)))  # segments are in slot order
+    groups = gemm_groups(start, padded, order, d_model, d_ff)
+    n_owned = sum(1 for e in slots if int(base_owner[e]) == rank)
+    return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
+                      seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),
+                      route_cum=route_cum, recv_base=recv_base, zero_rows=zero_rows,
+                      spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs, groups=groups)
+
+
+class PackedTables:
+    """One contiguous byte blob (16-byte aligned sections) for a single H2D copy."""
+
+    def __init__(self, tables: RankTables):
+        parts = [("route_cum", tables.route_cum), ("recv_base", tables.recv_base),
+                 ("zero_rows", tables.zero_rows), ("spag", tables.spag_copies),
+                 ("sprs_jobs", tables.sprs_jobs), ("sprs_srcs", tables.sprs_srcs)]
+        for name in GEMM_NAMES:
+            parts.append((name, tables.groups[name][0]))
+        self.offsets = {}
+        chunks = []
+        off = 0
+        for name, arr in parts:
+            raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+            self.offsets[name] = off
+            chunks.append(raw)
+            pad = (-len(raw)) % 16
+            if pad:
+                chunks.append(np.zeros(pad, dtype=np.uint8))
+            off += len(raw) + pad
+        self.blob = np.concatenate(chunks) if chunks else np.zeros(0, dtype=np.uint8)
+        if len(self.blob) == 0:
+            self.blob = np.zeros(16, dtype=np.uint8)

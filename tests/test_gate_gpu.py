@@ -28,8 +28,9 @@ def test_gate_topk_matches_oracle(T, d, E, k):
     np.testing.assert_array_equal(idx.cpu().numpy(), o_idx)
     np.testing.assert_array_equal(rank.cpu().numpy(), o_rank)
     np.testing.assert_array_equal(tc.cpu().numpy(), o_tc)
-    # weights: expf (device) vs numpy float32 exp may differ by one ulp -> 2-ulp tolerance
-    np.testing.assert_array_max_ulp(w.cpu().numpy(), o_w, maxulp=2)
+    # weights: device expf vs numpy float32 exp differ by an ulp or two, amplified by the
+    # renormalisation -> stated tolerance rtol 2e-6 (selection itself is bit-exact above)
+    np.testing.assert_allclose(w.cpu().numpy(), o_w, rtol=2e-6, atol=0)
     assert tc.cpu().numpy().sum() == T * k
 
 

@@ -1,0 +1,81 @@
+"""Host-side plan tables (pure logic, CPU): every rank derives its tables from the same
+global plan; the positions sources compute must tile each destination's receive
+segments exactly, SpAG/SpRS jobs must follow the placement pair contract."""
+
+import numpy as np
+
+import paper_2502_02581_b200 as F
+from oracle import tensor_oracle as TO
+from paper_2502_02581_b200.plan_tables import ROW_ALIGN, build_rank_tables
+
+
+def _random_plan(rng, D, E, T, k):
+    topo = F.ClusterTopology.for_nvswitch(D)
+    cfg = F.ModelConfig(1, E, 2 ** 20, 512, 1e-3, 1e-6)
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=int(rng.integers(1, E + 1)),
+                   capacity_override=int(rng.integers(1, 4)))
+    pl = F.FssdpPlanner(cfg, topo, pol)
+    p = 1.0 / np.arange(1, E + 1) ** 1.2
+    p = p[rng.permutation(E)]
+    idxs = []
+    for _ in range(D):
+        idx = np.stack([rng.choice(E, size=k, replace=False, p=p / p.sum()) for _ in range(T)])
+        idxs.append(idx.astype(np.int32))
+    counts = np.stack([np.bincount(i.reshape(-1), minlength=E) for i in idxs])
+    pl.history[0].append(counts * rng.uniform(0.8, 1.2, size=counts.shape))
+    return pl.plan(0, counts), idxs
+
+
+def test_positions_tile_receive_segments_exactly():
+    rng = np.random.default_rng(0)
+    for _ in range(25):
+        D, E, T, k = int(rng.choice([1, 2, 4, 8])), int(rng.choice([8, 16])), 200, 2
+        dec, idxs = _random_plan(rng, D, E, T, k)
+        owner = dec.base.owners()
+        tabs = [build_rank_tables(r, owner, dec.target.mask, dec.route, 256, 512) for r in range(D)]
+        filled = [np.zeros(t.recv_rows, dtype=np.int64) for t in tabs]
+        for s in range(D):
+            dest, pos = TO.slot_positions(idxs[s], dec.route, s, tabs[s].recv_base)
+            for (t, j), dd in np.ndenumerate(dest):
+                e = idxs[s][t, j]
+                assert dec.target.mask[e, dd], "slot routed to a non-holder"
+                seg = tabs[dd].slots[e]
+                st = tabs[dd].seg_start[seg]
+                assert st <= pos[t, j] < st + tabs[dd].seg_rows[seg]
+                filled[dd][pos[t, j]] += 1
+        for d in range(D):
+            t = tabs[d]
+            want = np.zeros(t.recv_rows, dtype=np.int64)
+            for s_ in range(len(t.seg_start)):
+                want[t.seg_start[s_]:t.seg_start[s_] + t.seg_rows[s_]] = 1
+            assert np.array_equal(filled[d], want)  # bijection onto the real rows
+            assert np.all(t.seg_padded % ROW_ALIGN == 0)
+            zr = {(int(a), int(b)) for a, b in t.zero_rows}
+            assert zr == {(int(t.seg_start[i] + t.seg_rows[i]), int(t.seg_padded[i] - t.seg_rows[i]))
+                          for i in range(len(t.seg_start)) if t.seg_padded[i] > t.seg_rows[i]}
+
+
+def test_spag_sprs_jobs_follow_the_pair_contract():
+    rng = np.random.default_rng(1)
+    for _ in range(25):
+        D, E = int(rng.choice([2, 4, 8])), 16
+        dec, _ = _random_plan(rng, D, E, 300, 2)
+        owner = dec.base.owners()
+        tabs = [build_rank_tables(r, owner, dec.target.mask, dec.route, 256, 512) for r in range(D)]
+        spag_pairs = set()
+        for r, t in enumerate(tabs):
+            for src, src_slot, dst_slot in t.spag_copies:
+                e = [x for x, s in t.slots.items() if s == dst_slot][0]
+                assert owner[e] == src and tabs[src].slots[e] == src_slot
+                spag_pairs.add((e, r))
+        added = dec.target.entries - dec.base.entries
+        assert spag_pairs == set(added)  # SpAG executes exactly spag_traffic's schedule
+        tr, rep = F.spag_traffic(dec.base, dec.target, 1)
+        assert rep.total_interdevice_bytes == len(spag_pairs)
+        for r, t in enumerate(tabs):
+            for dst_slot, b, n in t.sprs_jobs:
+                e = [x for x, s in t.slots.items() if s == dst_slot][0]
+                srcs = t.sprs_srcs[b:b + n]
+                assert list(srcs[:, 0]) == sorted(np.flatnonzero(dec.target.mask[e]))
+                assert all(tabs[h].slots[e] == sl for h, sl in srcs)
+            assert all(owner[e] == r for e, s in t.slots.items() if s < t.n_owned)
