@@ -187,12 +187,16 @@ typedef struct fssdp_gemm_group {
  * described by (inner, outer) element extents (inner contiguous).  a_mn / b_mn select
  * the operand major-ness: 0 = K-major (A: [M][K], B: [N][K]), 1 = MN-major
  * (A: [K][M], B: [K][N]).  N (= n_tiles * 256) is shared by every group.
- * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum. */
+ * C (and C2 / aux) is a row-major [c_rows][ldc] tensor (bf16, or fp32 for
+ * FSSDP_EPI_F32); a group's C origin is element c_off (a multiple of ldc).
+ * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum.
+ * flags: FSSDP_GEMM_N_FASTEST orders a group's tiles N-fastest (A tile shared in L2). */
+#define FSSDP_GEMM_N_FASTEST 1
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
                        int32_t total_tiles, void* c, void* c2, const void* aux, int64_t ldc,
-                       void* stream);
+                       int64_t c_rows, int32_t flags, void* stream);
 
 #define FSSDP_GATE_TILE 64 /* tokens per gate CTA (slot ranks are tile-relative) */
 
@@ -264,8 +268,9 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
                      int64_t dxe_off, float* dlogit_out, void* dx_out, void* stream);
 
 /* Gate weight gradient dWg[e] = sum_t dlogit[t, e] x[t]  (fixed order; fp32 [E*d]).
- * workspace: fp32 [FSSDP_WG_SPLITS * E * d]. */
-#define FSSDP_WG_SPLITS 16
+ * workspace: fp32 [ceil(T / FSSDP_WG_TILE) * E * d] (per-token-tile partials, reduced in
+ * tile order). */
+#define FSSDP_WG_TILE 256
 int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
                      void* stream);

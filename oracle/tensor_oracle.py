@@ -97,15 +97,17 @@ def expert_counts(idx: np.ndarray, E: int) -> np.ndarray:
 
 # ------------------------------------------------------------------ activation
 def gelu_tanh(x: np.ndarray) -> np.ndarray:
-    x = x.astype(np.float64)
-    return 0.5 * x * (1.0 + np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+    x = np.asarray(x, dtype=np.float32)
+    k0, k1 = np.float32(0.7978845608028654), np.float32(0.044715)
+    return np.float32(0.5) * x * (np.float32(1.0) + np.tanh(k0 * (x + k1 * x * x * x)))
 
 
 def gelu_tanh_grad(x: np.ndarray) -> np.ndarray:
-    x = x.astype(np.float64)
-    k0, k1 = 0.7978845608028654, 0.044715
-    t = np.tanh(k0 * (x + k1 * x ** 3))
-    return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * k0 * (1.0 + 3.0 * k1 * x * x)
+    x = np.asarray(x, dtype=np.float32)
+    k0, k1 = np.float32(0.7978845608028654), np.float32(0.044715)
+    t = np.tanh(k0 * (x + k1 * x * x * x))
+    return (np.float32(0.5) * (np.float32(1.0) + t)
+            + np.float32(0.5) * x * (np.float32(1.0) - t * t) * k0 * (np.float32(1.0) + np.float32(3.0) * k1 * x * x))
 
 
 # ------------------------------------------------------------------ dispatch / combine
@@ -168,7 +170,7 @@ def moe_layer_fwd_bwd(x, idx, w, wg, experts, dy):
         A[e], H[e] = (rows, a), h
     y = combine(Y, w)
     # backward
-    g = np.einsum("td,tkd->tk", dy.astype(np.float64), Y.astype(np.float64)).astype(np.float32)
+    g = np.einsum("td,tkd->tk", dy.astype(np.float32), Y, optimize=True).astype(np.float32)
     sg = (w.astype(np.float64) * g).sum(axis=1, keepdims=True)
     dlogit = (w * (g - sg)).astype(np.float32)
     dXs = np.zeros((T, k, d), dtype=np.float32)
@@ -185,8 +187,8 @@ def moe_layer_fwd_bwd(x, idx, w, wg, experts, dy):
         dA = bf16_round((dH * gelu_tanh_grad(a)).astype(np.float32))
         dXs[rows[:, 0], rows[:, 1]] = bf16_round((dA @ W1).astype(np.float32))
         xe = x[rows[:, 0]].astype(np.float32)
-        dW1[e] = (dA.T.astype(np.float64) @ xe).astype(np.float32)
-        dW2[e] = (dYe.T.astype(np.float64) @ H[e]).astype(np.float32)
+        dW1[e] = (dA.T @ xe).astype(np.float32)
+        dW2[e] = (dYe.T @ H[e]).astype(np.float32)
         del f
     dx = dXs.sum(axis=1) + np.einsum("tk,tkd->td", dlogit, wg[idx])
     dWg = np.zeros_like(wg)

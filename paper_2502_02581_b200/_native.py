@@ -88,7 +88,7 @@ _SIGS = {
     "fssdp_shard_score": [i32, i32, P_i32, P_f64, P_topo, P_f64],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
-                           vp, i64, vp],
+                           vp, i64, i64, i32, vp],
     "fssdp_gate_topk": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
@@ -145,5 +145,17 @@ def check(status: int, what: str) -> None:
         raise_for_status(status, what, last_error())
 
 
+# kernels launched per successful call of each device entry point (launch accounting)
+KERNELS_PER_CALL = {
+    "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
+    "fssdp_route_scan_allgather": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1,
+    "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
+    "fssdp_sprs": 1,
+}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     check(getattr(LIB, name)(*args), name)
+    launch_count += KERNELS_PER_CALL.get(name, 0)

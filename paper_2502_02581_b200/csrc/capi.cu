@@ -49,25 +49,32 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
-                      int box_inner, int box_outer) {
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_inner,
+                 int box_outer, int dtype, int swizzle_bytes) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return kErrCuda;
   }
-  if (inner <= 0 || outer <= 0 || (inner * 2) % 16 != 0 ||
+  const int esize = dtype == kDtF32 ? 4 : 2;
+  if (inner <= 0 || outer <= 0 || (inner * esize) % 16 != 0 ||
       (reinterpret_cast<uintptr_t>(base) & 15) != 0) {
     set_error("tensor map: bad extents or misaligned base");
     return kErrDimension;
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * 2)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * esize)};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = fn(map,
+                  dtype == kDtF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[128];
     snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
@@ -93,8 +100,8 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
                        int32_t total_tiles, void* c, void* c2, const void* aux, int64_t ldc,
-                       void* stream) {
-  if (num_groups <= 0 || n_tiles <= 0 || total_tiles < 0 || c == nullptr) {
+                       int64_t c_rows, int32_t flags, void* stream) {
+  if (num_groups <= 0 || n_tiles <= 0 || total_tiles < 0 || c == nullptr || c_rows <= 0) {
     set_error("grouped_gemm: bad arguments");
     return kErrDimension;
   }
@@ -107,12 +114,13 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.num_groups = num_groups;
   args.n_tiles = n_tiles;
   args.total_tiles = total_tiles;
+  args.n_fast = (flags & FSSDP_GEMM_N_FASTEST) ? 1 : 0;
   args.ldc = ldc;
   args.c = c;
   args.c2 = c2;
   args.aux = static_cast<const __nv_bfloat16*>(aux);
   int rc = grouped_gemm_launch(a_mn, b_mn, epilogue, a, a_inner, a_outer, b, b_inner, b_outer,
-                               args, reinterpret_cast<cudaStream_t>(stream));
+                               c_rows, args, reinterpret_cast<cudaStream_t>(stream));
   if (rc == kErrCuda && g_last_error.empty()) set_error("grouped_gemm launch failed");
   return rc;
 }

@@ -31,6 +31,7 @@ struct GemmLaunch {
   int num_groups;
   int n_tiles;      // BN tiles along N (same for every group)
   int total_tiles;  // sum over groups of m_tiles * n_tiles
+  int n_fast;       // tile order: 1 = N fastest (share A in L2), 0 = M fastest (share B)
   int64_t ldc;      // elements per C row
   void* c;          // output (bf16 or fp32)
   void* c2;         // second output (GeLU: post-activation)
@@ -39,10 +40,12 @@ struct GemmLaunch {
 
 int num_sms();
 void set_error(const char* msg);
-int make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
-                      int box_inner, int box_outer);
+constexpr int kDtBF16 = 0;
+constexpr int kDtF32 = 1;
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_inner,
+                 int box_outer, int dtype, int swizzle_bytes);
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
                         int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
-                        const GemmLaunch& args, cudaStream_t stream);
+                        int64_t c_rows, const GemmLaunch& args, cudaStream_t stream);
 
 }  // namespace fssdp

@@ -5,7 +5,8 @@
 // (cp.async.bulk.tensor, SWIZZLE_128B) into a 4-deep shared-memory ring, multiplied
 // by tcgen05.mma (kind::f16, bf16 in / fp32 accumulate) into a double-buffered TMEM
 // accumulator, and drained by four epilogue warps that fuse the activation
-// (GeLU fwd, GeLU' in dgrad) and the output cast.
+// (GeLU fwd, GeLU' in dgrad) and the output cast, then hand 32x32 tiles to TMA bulk
+// stores through double-buffered, bank-conflict-free swizzled staging buffers.
 //
 // Grouping: every local expert (owned shard or SpAG replica) is one group.  A group's
 // tokens are a 128-row-aligned segment of the receive buffer, so an M tile never
@@ -28,32 +29,40 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kStages = 4;
 constexpr int kThreads = 192;
+constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store box)
 
-template <int BN>
+template <int BN, int EPI>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBarOffset = kStages * kStageBytes;
-  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
-  static constexpr int kTotal = kBarOffset + (2 * kStages + 4) * 8 + 16;
+  static constexpr int kOutBytes = (EPI == kEpiF32) ? 4 : 2;
+  static constexpr int kBufBytes = 32 * kEpiCols * kOutBytes;  // one 32x32 staging tile
+  static constexpr int kStreams = (EPI == kEpiGelu || EPI == kEpiDGelu) ? 2 : 1;
+  static constexpr int kEpiWarpBytes = kStreams * 2 * kBufBytes;  // double buffered
+  static constexpr int kEpiOffset = kStages * kStageBytes;
+  static constexpr int kBarOffset = kEpiOffset + 4 * kEpiWarpBytes;
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], aux[4 warps][2], tmem base slot
+  static constexpr int kTotal = kBarOffset + (2 * kStages + 4 + 8) * 8 + 16;
   static constexpr int kDynamic = kTotal + 1024;  // slack for 1024-B alignment
+  static_assert(kDynamic <= 232448, "shared memory budget exceeded");
 };
 
+// tanh.approx (MUFU) is below bf16 output resolution; parity is tolerance-based.
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
   const float k1 = 0.044715f;
-  float u = k0 * (x + k1 * x * x * x);
-  return 0.5f * x * (1.0f + tanhf(u));
+  const float u = k0 * fmaf(k1 * x * x, x, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_approx(u), hx);
 }
 
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f;
   const float k1 = 0.044715f;
-  float x2 = x * x;
-  float u = k0 * (x + k1 * x2 * x);
-  float t = tanhf(u);
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x2);
+  const float x2 = x * x;
+  const float t = tanh_approx(k0 * fmaf(k1 * x2, x, x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f);
 }
 
 struct TileCoord {
@@ -61,25 +70,40 @@ struct TileCoord {
 };
 
 __device__ __forceinline__ TileCoord locate_tile(const GemmGroup* __restrict__ groups,
-                                                 int num_groups, int n_tiles, int tile) {
+                                                 int num_groups, int n_tiles, int n_fast,
+                                                 int tile) {
   int g = 0;
   // groups are few (<= experts per device + replica slots); a linear scan is cheapest
   while (g + 1 < num_groups && groups[g + 1].tile_start <= tile) ++g;
-  int local = tile - groups[g].tile_start;
-  int mt = groups[g].m_tiles;
+  const int local = tile - groups[g].tile_start;
+  const int mt = groups[g].m_tiles;
   TileCoord tc;
   tc.group = g;
-  tc.m_tile = local % mt;  // M fastest: neighbouring CTAs share the weight (B) tile in L2
-  tc.n_tile = local / mt;
-  (void)n_tiles;
+  if (n_fast) {  // neighbouring CTAs share the A tile (activation rows) in L2
+    tc.n_tile = local % n_tiles;
+    tc.m_tile = local / n_tiles;
+  } else {  // neighbouring CTAs share the B tile (weights) in L2
+    tc.m_tile = local % mt;
+    tc.n_tile = local / mt;
+  }
   return tc;
+}
+
+// Swizzled staging addresses: row r of a 32-row tile, 16-byte chunk j.
+__device__ __forceinline__ uint32_t sw64(int r, int j) {  // 64-byte rows, SWIZZLE_64B
+  return static_cast<uint32_t>(r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ uint32_t sw128(int r, int j) {  // 128-byte rows, SWIZZLE_128B
+  return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
 }
 
 template <bool A_MN, bool B_MN, int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, GemmLaunch args) {
-  using S = GemmSmem<BN>;
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c,
+                        const __grid_constant__ CUtensorMap map_x, GemmLaunch args) {
+  using S = GemmSmem<BN, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -87,7 +111,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 8);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -95,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    tma_prefetch_desc(&map_c);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -103,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4);  // one arrival per epilogue warp
     }
+    for (int a = 0; a < 8; ++a) mbar_init(&aux_bar[a], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
@@ -120,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, tile);
+        const TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const GemmGroup& g = groups[tc.group];
         const int m0 = g.a_m + tc.m_tile * kBM;
         const int n0 = g.b_n + tc.n_tile * BN;
@@ -161,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, tile);
+        const TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const int kblocks = groups[tc.group].k_blocks;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -198,38 +225,82 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===================== epilogue: TMEM -> registers -> fused op -> global
+    // ===================== epilogue: TMEM -> registers -> fused op -> smem -> TMA store
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 2;
+    uint8_t* wbase = smem + S::kEpiOffset + ew * S::kEpiWarpBytes;
+    uint8_t* cbuf0 = wbase;                         // C staging, buffers 0/1
+    uint8_t* xbuf0 = wbase + 2 * S::kBufBytes;      // C2 staging (GeLU) or aux tiles (GeLU')
+    uint64_t* abar = aux_bar + 2 * ew;
+    uint32_t aux_phase0 = 0, aux_phase1 = 0;
+    constexpr int kChunks = BN / kEpiCols;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t gchunk = 0;  // running chunk counter (selects the staging buffer)
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, tile);
+      const TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
       const GemmGroup& g = groups[tc.group];
-      const int row = tc.m_tile * kBM + q * 32 + lane;  // row inside the group's C
+      const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * kBM + q * 32;
       const int col0 = tc.n_tile * BN;
-      const int64_t c_row = g.c_off + static_cast<int64_t>(row) * args.ldc + col0;
+      const bool zero = g.k_blocks == 0;
+      if (EPI == kEpiDGelu && lane == 0) {  // prefetch the first aux tile of this tile
+        const int b = gchunk & 1;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&abar[b], S::kBufBytes);
+        tma_load_2d(xbuf0 + b * S::kBufBytes, &map_x, &abar[b], col0, row0);
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const bool zero = g.k_blocks == 0;
 #pragma unroll 1
-      for (int chunk = 0; chunk < BN / 32; ++chunk) {
+      for (int c = 0; c < kChunks; ++c, ++gchunk) {
+        const int b = gchunk & 1;
         uint32_t r[32];
         if (!zero) {
           tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                 static_cast<uint32_t>(acc * BN + chunk * 32),
+                                 static_cast<uint32_t>(acc * BN + c * kEpiCols),
                              r);
           tmem_ld_wait();
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
-        const int64_t off = c_row + chunk * 32;
-        if (EPI == kEpiF32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.c) + off);
+        if (c == kChunks - 1) {  // accumulator fully read: release TMEM to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        }
+        __nv_bfloat162 pre[16];
+        if (EPI == kEpiDGelu) {
+          if (lane == 0 && c + 1 < kChunks) {  // prefetch the next aux tile
+            const int nb = (gchunk + 1) & 1;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&abar[nb], S::kBufBytes);
+            tma_load_2d(xbuf0 + nb * S::kBufBytes, &map_x, &abar[nb], col0 + (c + 1) * kEpiCols,
+                        row0);
+          }
+          if (b == 0) {
+            mbar_wait(&abar[0], aux_phase0);
+            aux_phase0 ^= 1;
+          } else {
+            mbar_wait(&abar[1], aux_phase1);
+            aux_phase1 ^= 1;
+          }
+          const uint8_t* ab = xbuf0 + b * S::kBufBytes;
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<int4*>(&pre[4 * j]) =
+                *reinterpret_cast<const int4*>(ab + sw64(lane, j));
+        }
+        // the staging buffer b was last used two chunks ago: its TMA store must have read it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* cb = cbuf0 + b * S::kBufBytes;
+        if (EPI == kEpiF32) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<int4*>(cb + sw128(lane, j)) =
+                make_int4(static_cast<int>(r[4 * j]), static_cast<int>(r[4 * j + 1]),
+                          static_cast<int>(r[4 * j + 2]), static_cast<int>(r[4 * j + 3]));
         } else {
           __nv_bfloat162 out[16];
           if (EPI == kEpiBF16) {
@@ -243,37 +314,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 16; ++i) {
               out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]),
                                              __uint_as_float(r[2 * i + 1]));
-              float2 pre = __bfloat1622float2(out[i]);
-              act[i] = __floats2bfloat162_rn(gelu_tanh(pre.x), gelu_tanh(pre.y));
+              const float2 p = __bfloat1622float2(out[i]);
+              act[i] = __floats2bfloat162_rn(gelu_tanh(p.x), gelu_tanh(p.y));
             }
-            int4* dst2 = reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(args.c2) + off);
+            uint8_t* xb = xbuf0 + b * S::kBufBytes;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) dst2[i] = reinterpret_cast<const int4*>(act)[i];
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<int4*>(xb + sw64(lane, j)) =
+                  *reinterpret_cast<const int4*>(&act[4 * j]);
           } else {  // kEpiDGelu: out = acc * gelu'(pre-activation)
-            const int4* src = reinterpret_cast<const int4*>(args.aux + off);
-            __nv_bfloat162 pre[16];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(pre)[i] = src[i];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              float2 p = __bfloat1622float2(pre[i]);
+              const float2 p = __bfloat1622float2(pre[i]);
               out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * gelu_tanh_grad(p.x),
                                              __uint_as_float(r[2 * i + 1]) * gelu_tanh_grad(p.y));
             }
           }
-          int4* dst = reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(args.c) + off);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = reinterpret_cast<const int4*>(out)[i];
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<int4*>(cb + sw64(lane, j)) =
+                *reinterpret_cast<const int4*>(&out[4 * j]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, cb, col0 + c * kEpiCols, row0);
+          if (EPI == kEpiGelu) tma_store_2d(&map_x, xbuf0 + b * S::kBufBytes, col0 + c * kEpiCols, row0);
+          bulk_commit();
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait<0>();  // all stores of this warp complete before exit
+    __syncwarp();
   }
 
   __syncthreads();
@@ -286,10 +362,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ host side
 
 template <bool A_MN, bool B_MN, int BN, int EPI>
-static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const GemmLaunch& args,
-                          int grid, cudaStream_t stream) {
+static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                          const CUtensorMap& mx, const GemmLaunch& args, int grid,
+                          cudaStream_t stream) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI>;
-  const int smem = GemmSmem<BN>::kDynamic;
+  const int smem = GemmSmem<BN, EPI>::kDynamic;
   static bool configured = false;  // per template instance
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -297,41 +374,52 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const Ge
       return kErrCuda;
     configured = true;
   }
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, args);
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mx, args);
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 
 template <bool A_MN, bool B_MN, int BN>
 static int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb,
-                        const GemmLaunch& args, int grid, cudaStream_t stream) {
+                        const CUtensorMap& mc, const CUtensorMap& mx, const GemmLaunch& args,
+                        int grid, cudaStream_t stream) {
   switch (epi) {
-    case kEpiBF16: return launch_variant<A_MN, B_MN, BN, kEpiBF16>(ma, mb, args, grid, stream);
-    case kEpiGelu: return launch_variant<A_MN, B_MN, BN, kEpiGelu>(ma, mb, args, grid, stream);
-    case kEpiDGelu: return launch_variant<A_MN, B_MN, BN, kEpiDGelu>(ma, mb, args, grid, stream);
-    case kEpiF32: return launch_variant<A_MN, B_MN, BN, kEpiF32>(ma, mb, args, grid, stream);
+    case kEpiBF16: return launch_variant<A_MN, B_MN, BN, kEpiBF16>(ma, mb, mc, mx, args, grid, stream);
+    case kEpiGelu: return launch_variant<A_MN, B_MN, BN, kEpiGelu>(ma, mb, mc, mx, args, grid, stream);
+    case kEpiDGelu: return launch_variant<A_MN, B_MN, BN, kEpiDGelu>(ma, mb, mc, mx, args, grid, stream);
+    case kEpiF32: return launch_variant<A_MN, B_MN, BN, kEpiF32>(ma, mb, mc, mx, args, grid, stream);
     default: return kErrDimension;
   }
 }
 
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
                         int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
-                        const GemmLaunch& args, cudaStream_t stream) {
+                        int64_t c_rows, const GemmLaunch& args, cudaStream_t stream) {
   constexpr int BN = 256;
   if (args.total_tiles <= 0) return kOk;
   if (args.ldc % 32 != 0) return kErrDimension;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mx;
   // K-major operand: box = {64 K elems, rows};  MN-major: box = {64 MN elems, 64 K rows}
-  int rc = make_tmap_bf16_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM);
+  int rc = make_tmap_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM, kDtBF16, 128);
   if (rc != kOk) return rc;
-  rc = make_tmap_bf16_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN);
+  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN, kDtBF16, 128);
+  if (rc != kOk) return rc;
+  // epilogue tiles: 32 x 32, bf16 rows of 64 B (SWIZZLE_64B) or fp32 rows of 128 B
+  if (epi == kEpiF32)
+    rc = make_tmap_2d(&mc, args.c, args.ldc, c_rows, kEpiCols, 32, kDtF32, 128);
+  else
+    rc = make_tmap_2d(&mc, args.c, args.ldc, c_rows, kEpiCols, 32, kDtBF16, 64);
+  if (rc != kOk) return rc;
+  const void* xptr = epi == kEpiGelu ? args.c2 : (epi == kEpiDGelu ? args.aux : args.c);
+  rc = make_tmap_2d(&mx, xptr, args.ldc, c_rows, kEpiCols, 32, epi == kEpiF32 ? kDtF32 : kDtBF16,
+                    epi == kEpiF32 ? 128 : 64);
   if (rc != kOk) return rc;
   int grid = args.total_tiles < num_sms() ? args.total_tiles : num_sms();
   if (a_mn) {
-    if (b_mn) return dispatch_epi<true, true, BN>(epi, ma, mb, args, grid, stream);
-    return dispatch_epi<true, false, BN>(epi, ma, mb, args, grid, stream);
+    if (b_mn) return dispatch_epi<true, true, BN>(epi, ma, mb, mc, mx, args, grid, stream);
+    return dispatch_epi<true, false, BN>(epi, ma, mb, mc, mx, args, grid, stream);
   }
-  if (b_mn) return dispatch_epi<false, true, BN>(epi, ma, mb, args, grid, stream);
-  return dispatch_epi<false, false, BN>(epi, ma, mb, args, grid, stream);
+  if (b_mn) return dispatch_epi<false, true, BN>(epi, ma, mb, mc, mx, args, grid, stream);
+  return dispatch_epi<false, false, BN>(epi, ma, mb, mc, mx, args, grid, stream);
 }
 
 }  // namespace fssdp

@@ -146,6 +146,9 @@ __device__ void gate_select_tile(const float* __restrict__ lg, int lg_stride, in
   }
 }
 
+// EPT = experts per thread (each thread owns one token and experts grp, grp+4, ...):
+// templated so the inner loop carries no dead iterations for small E.
+template <int EPT>
 __global__ void __launch_bounds__(kGateThreads)
     gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
                      const float* __restrict__ bias, int64_t T, int d, int E, int k,
@@ -169,9 +172,9 @@ __global__ void __launch_bounds__(kGateThreads)
   const int64_t t0 = static_cast<int64_t>(tile) * kGateTile;
   const int tok = tid >> 2;
   const int grp = tid & 3;
-  float acc[kGateMaxE / 4];
+  float acc[EPT];
 #pragma unroll
-  for (int i = 0; i < kGateMaxE / 4; ++i) acc[i] = 0.f;
+  for (int i = 0; i < EPT; ++i) acc[i] = 0.f;
 
   for (int c0 = 0; c0 < d; c0 += kGateChunk) {
     const int cw = min(kGateChunk, d - c0);  // multiple of 8
@@ -192,10 +195,11 @@ __global__ void __launch_bounds__(kGateThreads)
       *reinterpret_cast<float4*>(&ws[e][c]) = val;
     }
     __syncthreads();
+#pragma unroll 4
     for (int i = 0; i < cw; i += 2) {
       const float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[tok][i]));
 #pragma unroll
-      for (int q = 0; q < kGateMaxE / 4; ++q) {
+      for (int q = 0; q < EPT; ++q) {
         const int e = grp + 4 * q;
         if (e < E) {
           const float2 wv = *reinterpret_cast<const float2*>(&ws[e][i]);
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__(kGateThreads)
     __syncthreads();
   }
 #pragma unroll
-  for (int q = 0; q < kGateMaxE / 4; ++q) {
+  for (int q = 0; q < EPT; ++q) {
     const int e = grp + 4 * q;
     if (e < E) lg[tok][e] = bias != nullptr ? __fadd_rn(acc[q], bias[e]) : acc[q];
   }
@@ -241,18 +245,44 @@ __global__ void __launch_bounds__(kGateThreads)
 }
 
 // ------------------------------------------------------------------ K2 scan + counts all-gather
-__global__ void route_scan_kernel(const int32_t* __restrict__ tile_counts, int n_tiles, int E,
-                                  int32_t* __restrict__ tile_prefix,
-                                  const uint64_t* __restrict__ peer_bases, int64_t table_off,
-                                  int64_t flags_off, int rank, int world, int slot, uint32_t epoch) {
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+// One CTA of 1024 threads: thread (chunk c, expert e) owns a contiguous run of tiles,
+// so every load is independent (the old one-thread-per-expert loop was latency bound).
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads)
+    route_scan_kernel(const int32_t* __restrict__ tile_counts, int n_tiles, int E,
+                      int32_t* __restrict__ tile_prefix, const uint64_t* __restrict__ peer_bases,
+                      int64_t table_off, int64_t flags_off, int rank, int world, int slot,
+                      uint32_t epoch) {
+  __shared__ int32_t chunk_sum[kScanThreads];
+  const int chunks = kScanThreads / E;  // E <= 64 -> at least 16 chunks
+  const int per = (n_tiles + chunks - 1) / chunks;
+  const int e = threadIdx.x % E;
+  const int c = threadIdx.x / E;
+  const bool active = c < chunks;
+  const int t0 = c * per;
+  const int t1 = min(n_tiles, t0 + per);
+  int32_t s = 0;
+  if (active)
+    for (int t = t0; t < t1; ++t) s += tile_counts[static_cast<int64_t>(t) * E + e];
+  chunk_sum[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < E) {  // exclusive scan over chunks, expert = threadIdx.x
     int32_t run = 0;
-    for (int t = 0; t < n_tiles; ++t) {
+    for (int q = 0; q < chunks; ++q) {
+      const int32_t v = chunk_sum[q * E + threadIdx.x];
+      chunk_sum[q * E + threadIdx.x] = run;
+      run += v;
+    }
+    for (int p = 0; p < world; ++p)
+      reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + threadIdx.x] = run;
+  }
+  __syncthreads();
+  if (active) {
+    int32_t run = chunk_sum[threadIdx.x];
+    for (int t = t0; t < t1; ++t) {
       tile_prefix[static_cast<int64_t>(t) * E + e] = run;
       run += tile_counts[static_cast<int64_t>(t) * E + e];
     }
-    for (int p = 0; p < world; ++p)
-      reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + e] = run;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -483,39 +513,81 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dWg partials: grid (d/128, SPLITS), 128 threads, one model dim per thread.
+// dWg partials: grid (d/256, ceil(T/FSSDP_WG_TILE)), 128 threads, two model dims per
+// thread (bf16x2 loads, 512 B coalesced per token row), accumulators in smem columns
+// owned by one thread each (no races).  8 token rows are prefetched per iteration so the
+// global loads overlap; the fp32 order per (e, dim) is fixed: tokens ascending, j ascending.
+constexpr int kWgDims = 256;
 __global__ void __launch_bounds__(128)
     gate_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
                               const int32_t* __restrict__ topk_idx,
                               const float* __restrict__ dlogit, int64_t T, int d_model, int E,
                               int k, float* __restrict__ workspace) {
-  __shared__ float acc[kGateMaxE][128];
-  const int dim = blockIdx.x * 128 + threadIdx.x;
-  const int split = blockIdx.y;
-  for (int e = 0; e < E; ++e) acc[e][threadIdx.x] = 0.f;
-  const int64_t per = (T + FSSDP_WG_SPLITS - 1) / FSSDP_WG_SPLITS;
-  const int64_t t_begin = split * per;
-  const int64_t t_end = imin64(T, t_begin + per);
-  if (dim < d_model) {
-    for (int64_t t = t_begin; t < t_end; ++t) {
-      const float xv = __bfloat162float(x[t * d_model + dim]);
+  extern __shared__ __align__(16) float wg_acc[];  // [E][kWgDims]
+  __shared__ int32_t s_e[FSSDP_WG_TILE * kGateMaxK];
+  __shared__ float s_dl[FSSDP_WG_TILE * kGateMaxK];
+  const int c0 = blockIdx.x * kWgDims;
+  const int col = 2 * threadIdx.x;
+  const bool live = c0 + col < d_model;
+  for (int e = 0; e < E; ++e)
+    *reinterpret_cast<float2*>(&wg_acc[e * kWgDims + col]) = make_float2(0.f, 0.f);
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.y) * FSSDP_WG_TILE;
+  const int64_t t_end = imin64(T, t_begin + FSSDP_WG_TILE);
+  // stage the tile's routing (coalesced) so smem addresses never wait on global loads
+  const int nslot = static_cast<int>(t_end - t_begin) * k;
+  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
+    s_e[i] = topk_idx[t_begin * k + i];
+    s_dl[i] = dlogit[t_begin * k + i];
+  }
+  __syncthreads();
+  constexpr int U = 8;
+  for (int64_t t = t_begin; t < t_end; t += U) {
+    float2 xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xv[u] = make_float2(0.f, 0.f);
+      if (live && t + u < t_end)
+        xv[u] = __bfloat1622float2(
+            *reinterpret_cast<const __nv_bfloat162*>(x + (t + u) * d_model + c0 + col));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (t + u >= t_end) break;
+      const int base = static_cast<int>(t + u - t_begin) * k;
       for (int j = 0; j < k; ++j) {
-        const int e = topk_idx[t * k + j];
-        acc[e][threadIdx.x] = fmaf(dlogit[t * k + j], xv, acc[e][threadIdx.x]);
+        const int e = s_e[base + j];
+        const float dl = s_dl[base + j];
+        float2* a = reinterpret_cast<float2*>(&wg_acc[e * kWgDims + col]);
+        float2 v = *a;
+        v.x = fmaf(dl, xv[u].x, v.x);
+        v.y = fmaf(dl, xv[u].y, v.y);
+        *a = v;
       }
     }
+  }
+  if (live) {
+    float* out = workspace + static_cast<int64_t>(blockIdx.y) * E * d_model + c0 + col;
     for (int e = 0; e < E; ++e)
-      workspace[(static_cast<int64_t>(split) * E + e) * d_model + dim] = acc[e][threadIdx.x];
+      *reinterpret_cast<float2*>(out + static_cast<int64_t>(e) * d_model) =
+          *reinterpret_cast<const float2*>(&wg_acc[e * kWgDims + col]);
   }
 }
 
-__global__ void gate_wgrad_reduce_kernel(const float* __restrict__ workspace, int d_model, int E,
-                                         float* __restrict__ dwg) {
+__global__ void gate_wgrad_reduce_kernel(const float* __restrict__ workspace, int n_tiles,
+                                         int d_model, int E, float* __restrict__ dwg) {
   const int64_t n = static_cast<int64_t>(E) * d_model;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float s = 0.f;
-    for (int p = 0; p < FSSDP_WG_SPLITS; ++p) s += workspace[p * n + i];
+    int p = 0;
+    for (; p + 8 <= n_tiles; p += 8) {  // 8 independent loads in flight, summed in order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = workspace[(p + u) * n + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; p < n_tiles; ++p) s += workspace[p * n + i];
     dwg[i] = s;
   }
 }
@@ -624,18 +696,25 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
                 static_cast<size_t>(E) * sizeof(float) * (kGateChunk + 4);
   const size_t lg_bytes = kGateTile * sizeof(float) * (kGateMaxE + 1);
   if (smem < lg_bytes) smem = lg_bytes;
-  static bool configured = false;
-  if (!configured) {
+  const int ept = (E + 3) / 4;
+  auto launch = [&](auto kern) -> int {
     const size_t max_smem = kGateTile * sizeof(__nv_bfloat16) * (kGateChunk + 8) +
                             kGateMaxE * sizeof(float) * (kGateChunk + 4);
-    if (cudaFuncSetAttribute(gate_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(max_smem)) != cudaSuccess)
       return launch_status();
-    configured = true;
-  }
-  gate_topk_kernel<<<tiles, kGateThreads, smem, as_stream(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k, logits, topk_idx, topk_w, slot_rank,
-      tile_counts);
+    kern<<<tiles, kGateThreads, smem, as_stream(stream)>>>(
+        static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k, logits, topk_idx, topk_w,
+        slot_rank, tile_counts);
+    return kOk;
+  };
+  int rc;
+  if (ept <= 1) rc = launch(gate_topk_kernel<1>);
+  else if (ept <= 2) rc = launch(gate_topk_kernel<2>);
+  else if (ept <= 4) rc = launch(gate_topk_kernel<4>);
+  else if (ept <= 8) rc = launch(gate_topk_kernel<8>);
+  else rc = launch(gate_topk_kernel<16>);
+  if (rc != kOk) return rc;
   return launch_status();
 }
 
@@ -656,11 +735,11 @@ int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int3
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
                                uint32_t epoch, void* stream) {
-  if (world <= 0 || world > kMaxWorld || rank < 0 || rank >= world || E <= 0) {
+  if (world <= 0 || world > kMaxWorld || rank < 0 || rank >= world || E <= 0 || E > kGateMaxE) {
     set_error("route_scan: bad world/rank/E");
     return kErrDimension;
   }
-  route_scan_kernel<<<1, 256, 0, as_stream(stream)>>>(tile_counts, n_tiles, E, tile_prefix,
+  route_scan_kernel<<<1, kScanThreads, 0, as_stream(stream)>>>(tile_counts, n_tiles, E, tile_prefix,
                                                        peer_bases, table_off, flags_off, rank,
                                                        world, bar_slot, epoch);
   return launch_status();
@@ -745,17 +824,29 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
 int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
                      void* stream) {
-  if (E > kGateMaxE || d_model <= 0) {
+  if (E > kGateMaxE || d_model <= 0 || d_model % 2 != 0) {
     set_error("gate_wgrad: bad shape");
     return kErrDimension;
   }
-  dim3 grid((d_model + 127) / 128, FSSDP_WG_SPLITS);
-  gate_wgrad_partial_kernel<<<grid, 128, 0, as_stream(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, workspace);
-  int rc = launch_status();
-  if (rc != kOk) return rc;
-  gate_wgrad_reduce_kernel<<<num_sms(), 256, 0, as_stream(stream)>>>(workspace, d_model, E,
-                                                                      dwg_out);
+  const int n_tiles = static_cast<int>((T + FSSDP_WG_TILE - 1) / FSSDP_WG_TILE);
+  if (n_tiles > 0) {
+    const int smem = E * kWgDims * static_cast<int>(sizeof(float));
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(gate_wgrad_partial_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kGateMaxE * kWgDims * static_cast<int>(sizeof(float))) != cudaSuccess)
+        return launch_status();
+      configured = true;
+    }
+    dim3 grid((d_model + kWgDims - 1) / kWgDims, n_tiles);
+    gate_wgrad_partial_kernel<<<grid, 128, smem, as_stream(stream)>>>(
+        static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, workspace);
+    int rc = launch_status();
+    if (rc != kOk) return rc;
+  }
+  gate_wgrad_reduce_kernel<<<num_sms(), 256, 0, as_stream(stream)>>>(workspace, n_tiles, d_model,
+                                                                      E, dwg_out);
   return launch_status();
 }
 

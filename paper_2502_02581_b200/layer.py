@@ -15,6 +15,7 @@ on one GPU (PeerGroup mode "emulated") — the multi-rank parity tests do that.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -26,6 +27,8 @@ from .comm import HeapLayout, PeerGroup
 from .engine import FssdpPlanner
 from .errors import DimensionError, InternalError
 from .plan_tables import GEMM_NAMES, PackedTables, build_rank_tables
+
+WG_TILE = 256  # FSSDP_WG_TILE (include/fssdp.h)
 
 # barrier slots (flag pads) used by one layer; layer i uses base + 8*i
 BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_SPAG = range(7)
@@ -133,7 +136,8 @@ class FssdpMoE:
         self.slot_pos = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
         self.slot_grad = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
         self.dlogit = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
-        self.wg_ws = torch.empty(16 * E * d, dtype=torch.float32, device=self.dev)
+        wg_tiles = max(1, (Tc + WG_TILE - 1) // WG_TILE)
+        self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
         self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
         self.blob_dev = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
@@ -220,6 +224,12 @@ class FssdpMoE:
 
     def phase_plan(self) -> None:
         counts = self.counts_table.cpu().numpy().astype(np.int64)  # host sync point #1
+        t_host = time.perf_counter()
+        self._plan_tables(counts)
+        if self.timers is not None:
+            self.timers.setdefault("host_plan_s", []).append(time.perf_counter() - t_host)
+
+    def _plan_tables(self, counts) -> None:
         dec = self.planner.plan(self.layer, counts)
         base_owner = dec.base.owners()
         tables = build_rank_tables(self.rank, base_owner, dec.target.mask, dec.route,
@@ -247,8 +257,9 @@ class FssdpMoE:
         n = len(self.tables.spag_copies)
         if n == 0:
             return
-        N.call("fssdp_spag", self._pb(), self.rank, self.off["params"], self.g.slot_param_bytes,
-               self._tab("spag"), n, self._stream())
+        self._timed("spag", lambda: N.call(
+            "fssdp_spag", self._pb(), self.rank, self.off["params"], self.g.slot_param_bytes,
+            self._tab("spag"), n, self._stream()))
 
     def phase_dispatch(self) -> None:
         t = self.tables
@@ -261,13 +272,34 @@ class FssdpMoE:
                self.flags_off, self.rank, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr()), self._stream())
 
+    # CUDA-event instrumentation (bench.py): name -> list of (start, end) events recorded on
+    # the launching stream around each kernel launch; None disables it.
+    timers = None
+
+    def _timed(self, key, fn):
+        if self.timers is None:
+            fn()
+            return
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        self.timers.setdefault(key, []).append((s, e))
+
+    # tile order per GEMM: N-fastest where the A operand (activations) is the big,
+    # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
+    N_FASTEST = {"fwd2": True, "dgrad1": True}
+
     def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None):
         ng, n_tiles, total = self.gemm[name]
         if total == 0:
             return
-        N.call("fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1],
-               a.shape[0], ops._ptr(b), b.shape[1], b.shape[0], self._tab(name), ng, n_tiles,
-               total, ops._ptr(c), ops._ptr(c2), ops._ptr(aux), ldc, self._stream())
+        flags = 1 if self.N_FASTEST.get(name, False) else 0
+        self._timed("gemm." + name, lambda: N.call(
+            "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
+            ops._ptr(b), b.shape[1], b.shape[0], self._tab(name), ng, n_tiles, total, ops._ptr(c),
+            ops._ptr(c2), ops._ptr(aux), ldc, c.numel() // ldc, flags, self._stream()))
 
     def phase_experts_fwd(self) -> None:
         f, d = self.g.d_ff, self.g.d_model
@@ -329,8 +361,9 @@ class FssdpMoE:
         n = len(self.tables.sprs_jobs)
         if n == 0:
             return
-        N.call("fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.g.slot_grad_elems,
-               self._tab("sprs_jobs"), n, self._tab("sprs_srcs"), self._stream())
+        self._timed("sprs", lambda: N.call(
+            "fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.g.slot_grad_elems,
+            self._tab("sprs_jobs"), n, self._tab("sprs_srcs"), self._stream()))
 
     # ------------------------------------------------------------ one rank per process
     def forward(self, x: torch.Tensor) -> torch.Tensor:
@@ -362,6 +395,28 @@ class FssdpMoE:
             import torch.distributed as dist
 
             dist.all_reduce(self.dwg, group=pg)
+
+
+def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_tokens: int,
+                 policy, *, rank: int = 0, world: int = 1, device="cuda", seed: int = 0,
+                 peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
+                 per_token_expert_time: float | None = None, pg=None) -> FssdpMoE:
+    """One rank per process: heap layout, IPC peer group (world > 1), planner, layer."""
+    from .engine import ModelConfig
+    from .topology import ClusterTopology
+
+    m = policy.capacity_override if policy.capacity_override is not None else num_experts
+    geom = LayerGeometry(d_model, d_ff, num_experts, top_k, max_tokens, world,
+                         default_slots(num_experts, world, m))
+    layout = HeapLayout()
+    geom.add_regions(layout, "L0.")
+    group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
+    topo = ClusterTopology.for_nvswitch(world, peer_bw)
+    if per_token_expert_time is None:  # fwd expert time per token-slot at the sustained bf16 peak
+        per_token_expert_time = 2.0 * 2 * d_model * d_ff / 1381.7e12
+    cfg = ModelConfig(1, num_experts, geom.expert_bytes, 2 * d_model, attn_fwd_time,
+                      per_token_expert_time)
+    return FssdpMoE(geom, group, FssdpPlanner(cfg, topo, policy), 0, seed)
 
 
 class FssdpMoEFunction(torch.autograd.Function):

@@ -34,8 +34,9 @@ def _close(out, ref, rel=2e-2, abs_=1e-3):
     assert err <= bound, f"max |Δ| {err:.4g} > {bound:.4g}"
 
 
-@pytest.mark.parametrize("epi", ["bf16", "gelu", "dgelu"])
-def test_kmajor_kmajor_grouped(epi):
+@pytest.mark.parametrize("epi,nf", [("bf16", False), ("bf16", True), ("gelu", False),
+                                    ("dgelu", False), ("dgelu", True)])
+def test_kmajor_kmajor_grouped(epi, nf):
     """fwd-style: A [R,K] K-major rows per group, B [G*N, K] K-major per-group weights."""
     ops = _ops()
     dev = "cuda"
@@ -55,7 +56,7 @@ def test_kmajor_kmajor_grouped(epi):
         r0 += mt * 128
     gd, ng, total = _groups(ops, rows, N // 256, dev)
     e = {"bf16": ops.EPI_BF16, "gelu": ops.EPI_GELU, "dgelu": ops.EPI_DGELU}[epi]
-    ops.grouped_gemm(A, False, B, False, gd, ng, N // 256, total, C, N, epilogue=e, c2=C2,
+    ops.grouped_gemm(A, False, B, False, gd, ng, N // 256, total, C, N, epilogue=e, c2=C2, n_fastest=nf,
                      aux=aux)
     torch.cuda.synchronize()
     ref = torch.zeros(R, N, device=dev)
