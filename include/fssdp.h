@@ -163,6 +163,31 @@ int fssdp_plan_layer(int32_t num_experts, const int32_t* base_owner, const doubl
 int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, const double* profile,
                       const fssdp_topology* topo, double* score_out);
 
+/* Device plan tables of one rank for one layer-iteration, derived from the global plan
+ * (base owner[E], target mask [E*D], route[D*E*D]) — every rank derives its own, nothing
+ * is exchanged.  Packed into one blob of 16-byte-aligned sections whose offsets
+ * fssdp_tables_layout returns; header_out[25] = {n_slots, n_owned, recv_rows, n_zero,
+ * n_spag, n_sprs_jobs, n_sprs_srcs, then per GEMM (fwd1, fwd2, dgrad2, dgrad1, wgrad1,
+ * wgrad2): num_groups, n_tiles, total_tiles}.  Layout semantics: plan_tables.py. */
+#define FSSDP_TAB_ROUTE_CUM 0   /* int32 [E][D+1] */
+#define FSSDP_TAB_RECV_BASE 1   /* int32 [E][D]   */
+#define FSSDP_TAB_ZERO_ROWS 2   /* int32 [<=E][2] {row, count} */
+#define FSSDP_TAB_SPAG 3        /* int32 [<=E][3] {src_rank, src_slot, dst_slot} */
+#define FSSDP_TAB_SPRS_JOBS 4   /* int32 [<=E][3] {dst_slot, src_begin, src_count} */
+#define FSSDP_TAB_SPRS_SRCS 5   /* int32 [<=E*D][2] {rank, slot} */
+#define FSSDP_TAB_GEMM0 6       /* 6 x fssdp_gemm_group [<=E] */
+#define FSSDP_TAB_SLOT_EXPERT 12 /* int32 [<=E] expert id of each local slot */
+#define FSSDP_TAB_SEG_START 13
+#define FSSDP_TAB_SEG_ROWS 14
+#define FSSDP_TAB_SEG_PADDED 15
+#define FSSDP_TAB_NSECTIONS 16
+int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offsets_out,
+                        int64_t* total_bytes_out);
+int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_experts,
+                            const int32_t* base_owner, const uint8_t* target_mask,
+                            const int64_t* route, int32_t d_model, int32_t d_ff, uint8_t* blob,
+                            int64_t blob_bytes, int32_t* header_out);
+
 /* ================================================================== device data plane */
 
 /* GEMM group descriptor (one local expert = one group); see gemm_sm100.cu. */

@@ -2,7 +2,7 @@
 
 The product path has no fallback: if the shared library is missing or a symbol is
 absent, importing this module raises.  `build()` in __graft_entry__.py (or
-`python -m paper_2502_02581_b200.build`) produces the library in-tree.
+`python paper_2502_02581_b200/build.py`) produces the library in-tree.
 """
 
 from __future__ import annotations
@@ -86,6 +86,8 @@ _SIGS = {
     "fssdp_plan_layer": [i32, P_i32, P_f64, P_i64, P_topo, C.POINTER(LayerKnobs), P_u8, P_i32,
                          P_i64, P_f64, P_i32],
     "fssdp_shard_score": [i32, i32, P_i32, P_f64, P_topo, P_f64],
+    "fssdp_tables_layout": [i32, i32, P_i64, P_i64],
+    "fssdp_build_rank_tables": [i32, i32, i32, P_i32, P_u8, P_i64, i32, i32, vp, i64, P_i32],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
                            vp, i64, i64, i32, vp],
@@ -121,7 +123,7 @@ def header_symbols() -> list[str]:
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2502_02581_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2502_02581_b200/build.py` "
             "(there is no CPU fallback for the FSSDP path)"
         )
     lib = C.CDLL(str(LIB_PATH))
@@ -133,6 +135,14 @@ def _load() -> C.CDLL:
 
 
 LIB = _load()
+
+# Second handle on the same library for hot host paths: every pointer argument is a
+# plain c_void_p, so callers pass ndarray.ctypes.data (an int) instead of data_as().
+LIB_RAW = C.CDLL(str(LIB_PATH))
+for _name, _args in _SIGS.items():
+    _fn = getattr(LIB_RAW, _name)
+    _fn.argtypes = [vp if a in (P_i32, P_i64, P_u8, P_f64, P_f32) else a for a in _args]
+    _fn.restype = _RESTYPE.get(_name, C.c_int)
 
 
 def last_error() -> str:

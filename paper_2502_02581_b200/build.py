@@ -5,7 +5,8 @@ linked statically and no libcuda link dependency (TMA descriptors are encoded th
 cudaGetDriverEntryPoint), so it loads on GPU-less hosts for the planner and the
 symbol checks, and travels to the GPU box with the repo snapshot.
 
-    python -m paper_2502_02581_b200.build [--force]
+    python paper_2502_02581_b200/build.py [--force]     (run by path: importing the
+                                                         package would load the old .so)
 """
 
 from __future__ import annotations

@@ -48,7 +48,14 @@ __device__ __forceinline__ void world_barrier_warp(const uint64_t* __restrict__ 
     st_release_sys(remote, epoch);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(peer_bases[rank] + flags_off) +
                            slot * kMaxWorld + lane;
+    // bounded spin: a peer that never arrives turns into a loud kernel fault after 30 s
+    // instead of a silently hung GPU
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 30ull * 1000000000ull) __trap();
     }
   }
   __syncwarp();

@@ -998,4 +998,170 @@ int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, con
   return FSSDP_OK;
 }
 
+// ------------------------------------------------------------------ device plan tables
+// Native twin of plan_tables.build_rank_tables (the Python version is the test oracle of
+// this one): one rank's kernel tables for one layer-iteration, packed for a single H2D.
+int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offsets_out,
+                        int64_t* total_bytes_out) {
+  const int64_t E = num_experts, D = num_devices;
+  const int64_t G = E * static_cast<int64_t>(sizeof(fssdp_gemm_group));
+  const int64_t sizes[FSSDP_TAB_NSECTIONS] = {
+      E * (D + 1) * 4, E * D * 4, E * 2 * 4, E * 3 * 4, E * 3 * 4, E * D * 2 * 4,
+      G, G, G, G, G, G,
+      E * 4, E * 4, E * 4, E * 4};
+  int64_t off = 0;
+  for (int i = 0; i < FSSDP_TAB_NSECTIONS; ++i) {
+    offsets_out[i] = off;
+    off += (sizes[i] + 15) / 16 * 16;
+  }
+  *total_bytes_out = off;
+  return FSSDP_OK;
+}
+
+int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* base_owner,
+                            const uint8_t* target_mask, const int64_t* route, int32_t d_model,
+                            int32_t d_ff, uint8_t* blob, int64_t blob_bytes, int32_t* header_out) {
+  int64_t off[FSSDP_TAB_NSECTIONS], total;
+  fssdp_tables_layout(E, D, off, &total);
+  if (blob_bytes < total || rank < 0 || rank >= D || d_model % 256 || d_ff % 256) {
+    set_error("build_rank_tables: bad arguments");
+    return FSSDP_ERR_DIMENSION;
+  }
+  memset(blob, 0, static_cast<size_t>(total));
+  auto R = [&](int s, int e, int d) { return route[(static_cast<int64_t>(s) * E + e) * D + d]; };
+  // slot maps of every device: owned experts (ascending) then replicas (ascending)
+  std::vector<std::vector<int>> slot_of(D, std::vector<int>(E, -1));
+  std::vector<std::vector<int>> slot_expert(D);
+  for (int d = 0; d < D; ++d) {
+    for (int e = 0; e < E; ++e)
+      if (base_owner[e] == d) slot_expert[d].push_back(e);
+    for (int e = 0; e < E; ++e)
+      if (target_mask[static_cast<int64_t>(e) * D + d] && base_owner[e] != d)
+        slot_expert[d].push_back(e);
+    for (size_t s = 0; s < slot_expert[d].size(); ++s) slot_of[d][slot_expert[d][s]] = static_cast<int>(s);
+  }
+  // segments (padded to 128 rows) of every device
+  std::vector<std::vector<int64_t>> seg_start(D), seg_rows(D), seg_pad(D);
+  for (int d = 0; d < D; ++d) {
+    int64_t st = 0;
+    for (int e : slot_expert[d]) {
+      int64_t rows = 0;
+      for (int s = 0; s < D; ++s) rows += R(s, e, d);
+      const int64_t padded = (rows + 127) / 128 * 128;
+      seg_start[d].push_back(st);
+      seg_rows[d].push_back(rows);
+      seg_pad[d].push_back(padded);
+      st += padded;
+    }
+  }
+  int32_t* route_cum = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_ROUTE_CUM]);
+  int32_t* recv_base = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_RECV_BASE]);
+  for (int e = 0; e < E; ++e) {
+    int64_t run = 0;
+    route_cum[e * (D + 1)] = 0;
+    for (int d = 0; d < D; ++d) {
+      run += R(rank, e, d);
+      route_cum[e * (D + 1) + d + 1] = static_cast<int32_t>(run);
+      const int s = slot_of[d][e];
+      if (s >= 0) {
+        int64_t before = 0;
+        for (int src = 0; src < rank; ++src) before += R(src, e, d);
+        recv_base[e * D + d] = static_cast<int32_t>(seg_start[d][s] + before);
+      }
+    }
+  }
+  const int n_slots = static_cast<int>(slot_expert[rank].size());
+  int32_t* zero = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_ZERO_ROWS]);
+  int n_zero = 0;
+  for (int s = 0; s < n_slots; ++s)
+    if (seg_pad[rank][s] > seg_rows[rank][s]) {
+      zero[2 * n_zero] = static_cast<int32_t>(seg_start[rank][s] + seg_rows[rank][s]);
+      zero[2 * n_zero + 1] = static_cast<int32_t>(seg_pad[rank][s] - seg_rows[rank][s]);
+      ++n_zero;
+    }
+  int32_t* spag = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPAG]);
+  int n_spag = 0, n_owned = 0;
+  for (int s = 0; s < n_slots; ++s) {
+    const int e = slot_expert[rank][s];
+    const int o = base_owner[e];
+    if (o == rank) {
+      ++n_owned;
+      continue;
+    }
+    spag[3 * n_spag] = o;
+    spag[3 * n_spag + 1] = slot_of[o][e];
+    spag[3 * n_spag + 2] = s;
+    ++n_spag;
+  }
+  int32_t* jobs = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_JOBS]);
+  int32_t* srcs = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_SRCS]);
+  int n_jobs = 0, n_srcs = 0;
+  for (int s = 0; s < n_slots; ++s) {
+    const int e = slot_expert[rank][s];
+    if (base_owner[e] != rank) continue;
+    int holders = 0;
+    for (int d = 0; d < D; ++d) holders += target_mask[static_cast<int64_t>(e) * D + d] != 0;
+    if (holders <= 1) continue;
+    jobs[3 * n_jobs] = s;
+    jobs[3 * n_jobs + 1] = n_srcs;
+    jobs[3 * n_jobs + 2] = holders;
+    ++n_jobs;
+    for (int d = 0; d < D; ++d)
+      if (target_mask[static_cast<int64_t>(e) * D + d]) {
+        srcs[2 * n_srcs] = d;
+        srcs[2 * n_srcs + 1] = slot_of[d][e];
+        ++n_srcs;
+      }
+  }
+  // the six grouped-GEMM descriptor arrays (see plan_tables.gemm_groups)
+  const int64_t d = d_model, f = d_ff;
+  const int n_tiles[6] = {static_cast<int>(f / 256), static_cast<int>(d / 256),
+                          static_cast<int>(f / 256), static_cast<int>(d / 256),
+                          static_cast<int>(d / 256), static_cast<int>(f / 256)};
+  int ints = 7;
+  for (int gi = 0; gi < 6; ++gi) {
+    fssdp_gemm_group* g = reinterpret_cast<fssdp_gemm_group*>(blob + off[FSSDP_TAB_GEMM0 + gi]);
+    int32_t tile = 0;
+    for (int s = 0; s < n_slots; ++s) {
+      const int32_t st = static_cast<int32_t>(seg_start[rank][s]);
+      const int32_t mt = static_cast<int32_t>(seg_pad[rank][s] / 128);
+      const int32_t kt = static_cast<int32_t>(seg_pad[rank][s] / 64);
+      fssdp_gemm_group& x = g[s];
+      switch (gi) {
+        case 0: x = {mt, 0, st, 0, static_cast<int32_t>(s * 2 * f), 0, static_cast<int32_t>(d / 64), 0, st * f}; break;
+        case 1: x = {mt, 0, st, 0, static_cast<int32_t>(s * 2 * d), 0, static_cast<int32_t>(f / 64), 0, st * d}; break;
+        case 2: x = {mt, 0, st, 0, 0, static_cast<int32_t>(s * 2 * d), static_cast<int32_t>(d / 64), 0, st * f}; break;
+        case 3: x = {mt, 0, st, 0, 0, static_cast<int32_t>(s * 2 * f), static_cast<int32_t>(f / 64), 0, st * d}; break;
+        case 4: x = {static_cast<int32_t>(f / 128), 0, 0, st, 0, st, kt, 0, s * 2 * f * d}; break;
+        default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * 2 * f * d + f * d}; break;
+      }
+      x.tile_start = tile;
+      tile += x.m_tiles * n_tiles[gi];
+    }
+    header_out[ints++] = n_slots;
+    header_out[ints++] = n_tiles[gi];
+    header_out[ints++] = tile;
+  }
+  int32_t* se = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SLOT_EXPERT]);
+  int32_t* ss = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_START]);
+  int32_t* sr = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_ROWS]);
+  int32_t* sp = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_PADDED]);
+  int64_t recv_rows = 0;
+  for (int s = 0; s < n_slots; ++s) {
+    se[s] = slot_expert[rank][s];
+    ss[s] = static_cast<int32_t>(seg_start[rank][s]);
+    sr[s] = static_cast<int32_t>(seg_rows[rank][s]);
+    sp[s] = static_cast<int32_t>(seg_pad[rank][s]);
+    recv_rows += seg_pad[rank][s];
+  }
+  header_out[0] = n_slots;
+  header_out[1] = n_owned;
+  header_out[2] = static_cast<int32_t>(recv_rows);
+  header_out[3] = n_zero;
+  header_out[4] = n_spag;
+  header_out[5] = n_jobs;
+  header_out[6] = n_srcs;
+  return FSSDP_OK;
+}
+
 }  // extern "C"

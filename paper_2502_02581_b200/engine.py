@@ -189,6 +189,13 @@ class FssdpPlanner:
         self._step = None
 
     # -- helpers ------------------------------------------------------------------
+    def _owners(self, layer: int) -> np.ndarray:
+        """Owner table of a layer's current partition (cached per ShardPlan)."""
+        if getattr(self, "_owners_plan", None) is not self.shards:
+            self._owners_cache = np.ascontiguousarray(self.shards.owners(), dtype=np.int32)
+            self._owners_plan = self.shards
+        return self._owners_cache[layer]
+
     def estimate(self, layer: int) -> Optional[np.ndarray]:
         if not self.history[layer]:
             return None
@@ -251,7 +258,7 @@ class FssdpPlanner:
         act = np.ascontiguousarray(np.asarray(actual, dtype=np.int64))
         if act.shape != (D, E):
             raise TraceMismatchError(f"counts {act.shape} do not match {D} devices x {E} experts")
-        owner = np.ascontiguousarray(base.owners())
+        owner = self._owners(layer)
         target = np.zeros((E, D), dtype=np.uint8)
         added = np.zeros(D, dtype=np.int32)
         route = np.zeros((D, E, D), dtype=np.int64)
@@ -265,13 +272,12 @@ class FssdpPlanner:
             knobs = self._knobs
             est = self.estimate(layer)
             est_ptr = None if est is None else np.ascontiguousarray(est, dtype=np.float64)
-        N.check(N.LIB.fssdp_plan_layer(
-            E, owner.ctypes.data_as(N.P_i32),
-            None if est_ptr is None else est_ptr.ctypes.data_as(N.P_f64),
-            act.ctypes.data_as(N.P_i64), N.C.byref(self._topo_c), N.C.byref(knobs),
-            target.ctypes.data_as(N.P_u8), added.ctypes.data_as(N.P_i32),
-            route.ctypes.data_as(N.P_i64), dbl.ctypes.data_as(N.P_f64),
-            flags.ctypes.data_as(N.P_i32)), "plan_layer")
+        # raw addresses (.ctypes.data) — data_as() costs microseconds per argument
+        N.check(N.LIB_RAW.fssdp_plan_layer(
+            E, owner.ctypes.data, None if est_ptr is None else est_ptr.ctypes.data,
+            act.ctypes.data, N.C.byref(self._topo_c), N.C.byref(knobs), target.ctypes.data,
+            added.ctypes.data, route.ctypes.data, dbl.ctypes.data, flags.ctypes.data),
+            "plan_layer")
         return LayerDecision(base=base, target=ChunkPlacement.from_mask(target),
                              added_per_device=tuple(int(a) for a in added), route=route,
                              spag_latency=float(dbl[0]), sprs_latency=float(dbl[1]),

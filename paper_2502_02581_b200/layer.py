@@ -26,7 +26,7 @@ from . import ops
 from .comm import HeapLayout, PeerGroup
 from .engine import FssdpPlanner
 from .errors import DimensionError, InternalError
-from .plan_tables import GEMM_NAMES, PackedTables, build_rank_tables
+from .plan_tables import NativeTables
 
 WG_TILE = 256  # FSSDP_WG_TILE (include/fssdp.h)
 
@@ -140,6 +140,7 @@ class FssdpMoE:
         self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
         self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
+        self.blob_host_np = self.blob_host.numpy()
         self.blob_dev = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
         self.decision = None
         self.tables = None
@@ -232,29 +233,24 @@ class FssdpMoE:
     def _plan_tables(self, counts) -> None:
         dec = self.planner.plan(self.layer, counts)
         base_owner = dec.base.owners()
-        tables = build_rank_tables(self.rank, base_owner, dec.target.mask, dec.route,
-                                   self.g.d_model, self.g.d_ff)
-        if len(tables.slots) > self.g.slots:
-            raise InternalError(f"plan needs {len(tables.slots)} slots > capacity {self.g.slots}")
+        # native table build straight into the pinned staging buffer, one H2D copy
+        tables = NativeTables(self.rank, base_owner, dec.target.mask, dec.route, self.g.d_model,
+                              self.g.d_ff, out_bytes=self.blob_host_np)
+        if tables.n_slots > self.g.slots:
+            raise InternalError(f"plan needs {tables.n_slots} slots > capacity {self.g.slots}")
         if tables.recv_rows > self.g.recv_cap:
             raise InternalError("receive rows exceed capacity")
-        owned_now = sorted(e for e in tables.slots if base_owner[e] == self.rank)
-        if owned_now != self._owned_expert_ids:
+        if tables.n_owned != len(self._owned_expert_ids) or \
+                list(tables.slot_expert[:tables.n_owned]) != self._owned_expert_ids:
             raise InternalError("ownership changed without a re-shard data move")
         self.decision, self.tables = dec, tables
-        self.packed = PackedTables(tables)
-        nb = len(self.packed.blob)
-        if nb > self.blob_host.numel():
-            raise InternalError("plan tables exceed the staging buffer")
-        self.blob_host[:nb].numpy()[:] = self.packed.blob
+        self.packed = tables
+        nb = tables.nbytes
         self.blob_dev[:nb].copy_(self.blob_host[:nb], non_blocking=True)  # boundary #2
-        self.gemm = {}
-        for name in GEMM_NAMES:
-            arr, n_tiles, total = tables.groups[name]
-            self.gemm[name] = (len(arr), n_tiles, total)
+        self.gemm = tables.gemm
 
     def phase_spag(self) -> None:
-        n = len(self.tables.spag_copies)
+        n = self.tables.n_spag
         if n == 0:
             return
         self._timed("spag", lambda: N.call(
@@ -268,7 +264,7 @@ class FssdpMoE:
                ops._ptr(self.slot_rank), ops._ptr(self.tile_prefix), self.T, self.g.d_model,
                self.g.num_experts, self.g.top_k, self.world, self._tab("route_cum"),
                self._tab("recv_base"), ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
-               self._pb(), self.off["xrecv"], self._tab("zero_rows"), len(t.zero_rows),
+               self._pb(), self.off["xrecv"], self._tab("zero_rows"), t.n_zero,
                self.flags_off, self.rank, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr()), self._stream())
 
@@ -331,7 +327,7 @@ class FssdpMoE:
         N.call("fssdp_dispatch_grad", ops._ptr(self.dy), ops._ptr(self.slot_dest),
                ops._ptr(self.slot_pos), ops._ptr(self.topk_w), self.T, self.g.d_model,
                self.g.top_k, self._pb(), self.off["y"], self.off["dyrecv"],
-               ops._ptr(self.slot_grad), self._tab("zero_rows"), len(t.zero_rows),
+               ops._ptr(self.slot_grad), self._tab("zero_rows"), t.n_zero,
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
 
@@ -358,7 +354,7 @@ class FssdpMoE:
                ops._ptr(self.wg_ws), ops._ptr(self.dwg), self._stream())
 
     def phase_sprs(self) -> None:
-        n = len(self.tables.sprs_jobs)
+        n = self.tables.n_sprs_jobs
         if n == 0:
             return
         self._timed("sprs", lambda: N.call(

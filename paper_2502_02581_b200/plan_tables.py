@@ -172,6 +172,104 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
                       spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs, groups=groups)
 
 
+SECTION_NAMES = ("route_cum", "recv_base", "zero_rows", "spag", "sprs_jobs", "sprs_srcs",
+                 *GEMM_NAMES, "slot_expert", "seg_start", "seg_rows", "seg_padded")
+
+
+_LAYOUTS: dict = {}
+
+
+def _layout(E: int, D: int):
+    """Section offsets of the packed tables (fssdp_tables_layout), cached per (E, D)."""
+    key = (E, D)
+    if key not in _LAYOUTS:
+        from . import _native as N
+
+        offs = np.zeros(len(SECTION_NAMES), dtype=np.int64)
+        total = np.zeros(1, dtype=np.int64)
+        N.check(N.LIB_RAW.fssdp_tables_layout(E, D, offs.ctypes.data, total.ctypes.data),
+                "tables_layout")
+        _LAYOUTS[key] = (dict(zip(SECTION_NAMES, offs.tolist())), int(total[0]))
+    return _LAYOUTS[key]
+
+
+class NativeTables:
+    """The same tables built by the C++ twin (fssdp_build_rank_tables) straight into a
+    pinned staging buffer — the product path; build_rank_tables above is its checker."""
+
+    def __init__(self, rank, base_owner, target_mask, route, d_model, d_ff, out_bytes=None):
+        from . import _native as N
+
+        E, D = target_mask.shape
+        self.E, self.D = E, D
+        self.offsets, self.nbytes = _layout(E, D)
+        self.blob = out_bytes if out_bytes is not None else np.zeros(self.nbytes, dtype=np.uint8)
+        if len(self.blob) < self.nbytes:
+            raise InternalError("plan tables exceed the staging buffer")
+        hdr = np.zeros(25, dtype=np.int32)
+        owner = np.ascontiguousarray(base_owner, dtype=np.int32)
+        mask = np.ascontiguousarray(target_mask, dtype=np.uint8)
+        rt = np.ascontiguousarray(route, dtype=np.int64)
+        N.check(N.LIB_RAW.fssdp_build_rank_tables(
+            rank, D, E, owner.ctypes.data, mask.ctypes.data, rt.ctypes.data, d_model, d_ff,
+            self.blob.ctypes.data, self.nbytes, hdr.ctypes.data), "build_rank_tables")
+        (self.n_slots, self.n_owned, self.recv_rows, self.n_zero, self.n_spag, self.n_sprs_jobs,
+         self.n_sprs_srcs) = (int(v) for v in hdr[:7])
+        self.gemm = {name: (int(hdr[7 + 3 * i]), int(hdr[8 + 3 * i]), int(hdr[9 + 3 * i]))
+                     for i, name in enumerate(GEMM_NAMES)}
+
+    def section(self, name, dtype, count):
+        off = self.offsets[name]
+        return self.blob[off:off + count * np.dtype(dtype).itemsize].view(dtype)
+
+    @property
+    def slot_expert(self) -> np.ndarray:
+        return self.section("slot_expert", np.int32, self.n_slots)
+
+    @property
+    def slots(self) -> dict:
+        return {int(e): s for s, e in enumerate(self.slot_expert)}
+
+    @property
+    def seg_start(self):
+        return self.section("seg_start", np.int32, self.n_slots)
+
+    @property
+    def seg_rows(self):
+        return self.section("seg_rows", np.int32, self.n_slots)
+
+    @property
+    def seg_padded(self):
+        return self.section("seg_padded", np.int32, self.n_slots)
+
+    @property
+    def zero_rows(self):
+        return self.section("zero_rows", np.int32, 2 * self.n_zero).reshape(-1, 2)
+
+    @property
+    def spag_copies(self):
+        return self.section("spag", np.int32, 3 * self.n_spag).reshape(-1, 3)
+
+    @property
+    def sprs_jobs(self):
+        return self.section("sprs_jobs", np.int32, 3 * self.n_sprs_jobs).reshape(-1, 3)
+
+    @property
+    def sprs_srcs(self):
+        return self.section("sprs_srcs", np.int32, 2 * self.n_sprs_srcs).reshape(-1, 2)
+
+    @property
+    def route_cum(self):
+        return self.section("route_cum", np.int32, self.E * (self.D + 1)).reshape(self.E, self.D + 1)
+
+    @property
+    def recv_base(self):
+        return self.section("recv_base", np.int32, self.E * self.D).reshape(self.E, self.D)
+
+    def groups(self, name) -> np.ndarray:
+        return self.section(name, GROUP_DTYPE, self.gemm[name][0])
+
+
 class PackedTables:
     """One contiguous byte blob (16-byte aligned sections) for a single H2D copy."""
 

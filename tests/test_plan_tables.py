@@ -55,6 +55,30 @@ def test_positions_tile_receive_segments_exactly():
                           for i in range(len(t.seg_start)) if t.seg_padded[i] > t.seg_rows[i]}
 
 
+def test_native_tables_equal_python_tables():
+    """The C++ twin (product path) builds exactly the tables of plan_tables.py."""
+    from paper_2502_02581_b200.plan_tables import GEMM_NAMES, NativeTables
+
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        D, E = int(rng.choice([1, 2, 4, 8])), int(rng.choice([8, 16, 64]))
+        dec, _ = _random_plan(rng, D, E, 300, 2)
+        owner = dec.base.owners()
+        for r in range(D):
+            py = build_rank_tables(r, owner, dec.target.mask, dec.route, 1024, 4096)
+            nt = NativeTables(r, owner, dec.target.mask, dec.route, 1024, 4096)
+            assert nt.slots == py.slots and nt.n_owned == py.n_owned
+            assert nt.recv_rows == py.recv_rows
+            for name in ("seg_start", "seg_rows", "seg_padded", "route_cum", "recv_base",
+                         "zero_rows", "spag_copies", "sprs_jobs", "sprs_srcs"):
+                assert np.array_equal(np.asarray(getattr(nt, name)),
+                                      np.asarray(getattr(py, name))), name
+            for name in GEMM_NAMES:
+                arr, n_tiles, total = py.groups[name]
+                assert nt.gemm[name] == (len(arr), n_tiles, total), name
+                assert nt.groups(name).tobytes() == arr.tobytes(), name
+
+
 def test_spag_sprs_jobs_follow_the_pair_contract():
     rng = np.random.default_rng(1)
     for _ in range(25):
