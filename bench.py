@@ -279,50 +279,103 @@ def run_ours(args):
         ms_max = float(t.item())
     value = world * T / (ms_max * 1e-3)
 
-    # GEMM roofline (dominant kernel family), from the events of the timed region
+    def gather(vals):
+        """Per-rank float vector -> [world, len] numpy (rank order)."""
+        t = torch.tensor(vals, device=dev, dtype=torch.float64)
+        if world == 1:
+            return t.cpu().numpy()[None, :]
+        out = [torch.empty_like(t) for _ in range(world)]
+        torch.distributed.all_gather(out, t)
+        return torch.stack(out).cpu().numpy()
+
+    # GEMM roofline (dominant kernel family), from the events of the timed region.
+    # Algorithmic FLOPs = this rank's real routed token-slots (no padding) x 3 GEMM passes.
     d, f, k = CFG2["d_model"], CFG2["d_ff"], CFG2["top_k"]
+    dec = layer.decision
     gemm_ms = sum(s.elapsed_time(e) for key, ev in timers.items() if key.startswith("gemm.")
-                  for s, e in ev)
+                  for s, e in ev) / args.steps
     gemm_launches = sum(len(ev) for key, ev in timers.items() if key.startswith("gemm."))
-    flops_step = 3 * 2 * k * T * 2 * d * f   # fwd + dgrad + wgrad, algorithmic (no padding)
+    rows_rank = float(dec.route[:, :, rank].sum())
+    flops_rank = 3 * 2 * rows_rank * 2 * d * f   # fwd + dgrad + wgrad
+    spag_ms = sum(s.elapsed_time(e) for s, e in timers.get("spag", [])) / args.steps
+    sprs_ms = sum(s.elapsed_time(e) for s, e in timers.get("sprs", [])) / args.steps
+    t = layer.tables
+    spag_in = float(t.n_spag * layer.g.slot_param_bytes)
+    sprs_in = float(sum(int(c) - 1 for _, _, c in t.sprs_jobs) * layer.g.slot_grad_elems * 4)
+    host_ms = 1e3 * sum(timers.get("host_plan_s", [])) / args.steps
+    allr = gather([gemm_ms, flops_rank, spag_ms, sprs_ms, spag_in, sprs_in, host_ms, ms])
     peaks, peak_src = load_peaks()
-    achieved = flops_step * args.steps / (gemm_ms * 1e-3) / 1e12
+    achieved = allr[:, 1].sum() / (allr[:, 0].sum() * 1e-3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
                 "kernel": "fssdp grouped_gemm_kernel (tcgen05), all 6 GEMMs of the step",
+                "algorithmic_flops": "3 x 2 x routed_rows x 2 x d_model x d_ff per rank",
                 "peak_source": f"{peak_src}, sustained bf16 (kernels timed inside a long step)",
-                "gemm_ms_per_step": gemm_ms / args.steps,
-                "gemm_share_of_step": gemm_ms / args.steps / ms,
+                "gemm_ms_per_step_per_rank": [round(v, 4) for v in allr[:, 0]],
+                "gemm_share_of_step": float(allr[:, 0].max() / ms_max),
                 "gemm_launches_per_step": gemm_launches / args.steps,
-                "host_plan_ms_per_step": 1e3 * sum(timers.get("host_plan_s", [])) / args.steps}
+                "host_plan_ms_per_step": float(allr[:, 6].max())}
     sparse = None
     if world > 1:
-        dec = layer.decision
         tr, rep = F.spag_traffic(dec.base, dec.target, layer.g.expert_bytes)
-        spag_ms = sum(s.elapsed_time(e) for s, e in timers.get("spag", [])) / args.steps
-        sprs_ms = sum(s.elapsed_time(e) for s, e in timers.get("sprs", [])) / args.steps
-        sparse = {"spag_bottleneck_bytes": rep.bottleneck_bytes,
-                  "spag_total_bytes": rep.total_interdevice_bytes,
-                  "spag_ms_rank": spag_ms, "sprs_ms_rank": sprs_ms,
-                  "replicas": len(dec.target.entries) - E,
-                  "nvlink_peer_gbs_ref": NVLINK_PEER_GBS}
+        spag_max, sprs_max = float(allr[:, 2].max()), float(allr[:, 3].max())
+        gbs = lambda b, m: (b / (m * 1e-3) / 1e9) if m > 0 else None  # noqa: E731
+        sparse = {
+            "replicas": len(dec.target.entries) - E,
+            "spag_total_bytes": rep.total_interdevice_bytes,
+            "spag_bottleneck_bytes": rep.bottleneck_bytes,
+            "spag_ms_max_rank": spag_max, "sprs_ms_max_rank": sprs_max,
+            "spag_bottleneck_gbs": gbs(rep.bottleneck_bytes, spag_max),
+            "spag_inbound_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 4], allr[:, 2])],
+            "sprs_inbound_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 5], allr[:, 3])],
+            "nvlink_peer_gbs_ref": NVLINK_PEER_GBS,
+            "note": "SpRS wire is fp32 (2x the reference's expert_bytes pricing)"}
 
-    # end to end through the public API with host buffers
+    # end to end through the public API with host buffers: inputs are copied H2D on a copy
+    # stream one step ahead (double buffered), dx is copied D2H behind the compute.
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
         dyh = dy.cpu().pin_memory()
-        dxh = torch.empty_like(xh).pin_memory()
-        for _ in range(2):
-            dxh.copy_(step(xh.to(dev, non_blocking=True), dyh.to(dev, non_blocking=True)))
+        dxh = [torch.empty_like(xh).pin_memory() for _ in range(2)]
+        xb = [torch.empty_like(x) for _ in range(2)]
+        dyb = [torch.empty_like(dy) for _ in range(2)]
+        copy_s = torch.cuda.Stream(device=dev)
+        main_s = torch.cuda.current_stream(dev)
+        in_ev = [torch.cuda.Event() for _ in range(2)]
+        done_ev = [torch.cuda.Event() for _ in range(2)]
+
+        def prefetch(i):
+            b = i % 2
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(done_ev[b])  # step i-2 finished with buffer b
+                xb[b].copy_(xh, non_blocking=True)
+                dyb[b].copy_(dyh, non_blocking=True)
+                in_ev[b].record(copy_s)
+
+        def run(n):
+            for ev in done_ev:
+                ev.record(main_s)
+            prefetch(0)
+            for i in range(n):
+                b = i % 2
+                main_s.wait_event(in_ev[b])
+                dx = step(xb[b], dyb[b])
+                done_ev[b].record(main_s)
+                if i + 1 < n:
+                    prefetch(i + 1)
+                with torch.cuda.stream(copy_s):
+                    copy_s.wait_event(done_ev[b])
+                    dxh[b].copy_(dx, non_blocking=True)
+                    dx.record_stream(copy_s)
+            main_s.wait_stream(copy_s)
+
+        run(2)
         barrier()
         s2, e2 = torch.cuda.Event(True), torch.cuda.Event(True)
         s2.record()
-        for _ in range(args.steps):
-            xin = xh.to(dev, non_blocking=True)
-            dyin = dyh.to(dev, non_blocking=True)
-            dxh.copy_(step(xin, dyin), non_blocking=True)
+        run(args.steps)
         e2.record()
         barrier()
         e2e_ms = s2.elapsed_time(e2) / args.steps
@@ -332,7 +385,9 @@ def run_ours(args):
             e2e_ms = float(t.item())
         nb = T * CFG2["d_model"] * 2
         e2e = {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s",
-               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": nb, "ms_per_step": e2e_ms}
+               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": nb, "ms_per_step": e2e_ms,
+               "pipeline": "H2D of step i+1 and D2H of step i on a copy stream, overlapped "
+                           "with step compute (FssdpMoE.forward/backward)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

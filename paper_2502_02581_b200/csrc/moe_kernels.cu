@@ -520,63 +520,69 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dWg partials: grid (d/256, ceil(T/FSSDP_WG_TILE)), 128 threads, two model dims per
-// thread (bf16x2 loads, 512 B coalesced per token row), accumulators in smem columns
-// owned by one thread each (no races).  8 token rows are prefetched per iteration so the
-// global loads overlap; the fp32 order per (e, dim) is fixed: tokens ascending, j ascending.
+// dWg partials: grid (d/256, ceil(T/FSSDP_WG_TILE)), 16 warps.  Warp w owns experts
+// w, w+16, ... (<= 4) and keeps their 256-dim accumulators in registers (8 dims per lane);
+// it walks the tile's tokens and, warp-uniformly, adds dlogit * x[t] for the tokens routed
+// to its experts.  No shared read-modify-write chains; fp32 order per (e, dim) is fixed:
+// tokens ascending.
 constexpr int kWgDims = 256;
-__global__ void __launch_bounds__(128)
+constexpr int kWgWarps = 16;
+constexpr int kWgMaxEpw = kGateMaxE / kWgWarps;
+__global__ void __launch_bounds__(kWgWarps * 32)
     gate_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
                               const int32_t* __restrict__ topk_idx,
                               const float* __restrict__ dlogit, int64_t T, int d_model, int E,
                               int k, float* __restrict__ workspace) {
-  extern __shared__ __align__(16) float wg_acc[];  // [E][kWgDims]
   __shared__ int32_t s_e[FSSDP_WG_TILE * kGateMaxK];
   __shared__ float s_dl[FSSDP_WG_TILE * kGateMaxK];
-  const int c0 = blockIdx.x * kWgDims;
-  const int col = 2 * threadIdx.x;
-  const bool live = c0 + col < d_model;
-  for (int e = 0; e < E; ++e)
-    *reinterpret_cast<float2*>(&wg_acc[e * kWgDims + col]) = make_float2(0.f, 0.f);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c = blockIdx.x * kWgDims + lane * 8;  // this lane's 8 model dims
+  const bool live = c < d_model;
   const int64_t t_begin = static_cast<int64_t>(blockIdx.y) * FSSDP_WG_TILE;
   const int64_t t_end = imin64(T, t_begin + FSSDP_WG_TILE);
-  // stage the tile's routing (coalesced) so smem addresses never wait on global loads
   const int nslot = static_cast<int>(t_end - t_begin) * k;
   for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
     s_e[i] = topk_idx[t_begin * k + i];
     s_dl[i] = dlogit[t_begin * k + i];
   }
   __syncthreads();
-  constexpr int U = 8;
-  for (int64_t t = t_begin; t < t_end; t += U) {
-    float2 xv[U];
+  float acc[kWgMaxEpw][8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      xv[u] = make_float2(0.f, 0.f);
-      if (live && t + u < t_end)
-        xv[u] = __bfloat1622float2(
-            *reinterpret_cast<const __nv_bfloat162*>(x + (t + u) * d_model + c0 + col));
-    }
+  for (int q = 0; q < kWgMaxEpw; ++q)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (t + u >= t_end) break;
-      const int base = static_cast<int>(t + u - t_begin) * k;
-      for (int j = 0; j < k; ++j) {
-        const int e = s_e[base + j];
-        const float dl = s_dl[base + j];
-        float2* a = reinterpret_cast<float2*>(&wg_acc[e * kWgDims + col]);
-        float2 v = *a;
-        v.x = fmaf(dl, xv[u].x, v.x);
-        v.y = fmaf(dl, xv[u].y, v.y);
-        *a = v;
-      }
+    for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
+  const int ntok = static_cast<int>(t_end - t_begin);
+  for (int tt = 0; tt < ntok; ++tt) {
+    float coef[kWgMaxEpw];
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < kWgMaxEpw; ++q) {
+      coef[q] = 0.f;
+      const int e = warp + kWgWarps * q;
+      for (int j = 0; j < k; ++j)
+        if (s_e[tt * k + j] == e) {
+          coef[q] = s_dl[tt * k + j];
+          any = true;
+        }
     }
+    if (!any || !live) continue;  // warp-uniform
+    float xv[8];
+    bf16x8_to_f32(*reinterpret_cast<const int4*>(x + (t_begin + tt) * d_model + c), xv);
+#pragma unroll
+    for (int q = 0; q < kWgMaxEpw; ++q)
+      if (coef[q] != 0.f)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[q][i] = fmaf(coef[q], xv[i], acc[q][i]);
   }
-  if (live) {
-    float* out = workspace + static_cast<int64_t>(blockIdx.y) * E * d_model + c0 + col;
-    for (int e = 0; e < E; ++e)
-      *reinterpret_cast<float2*>(out + static_cast<int64_t>(e) * d_model) =
-          *reinterpret_cast<const float2*>(&wg_acc[e * kWgDims + col]);
+  if (!live) return;
+#pragma unroll
+  for (int q = 0; q < kWgMaxEpw; ++q) {
+    const int e = warp + kWgWarps * q;
+    if (e >= E) break;
+    float4* out = reinterpret_cast<float4*>(
+        workspace + (static_cast<int64_t>(blockIdx.y) * E + e) * d_model + c);
+    out[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+    out[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
   }
 }
 
@@ -831,23 +837,14 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
 int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
                      void* stream) {
-  if (E > kGateMaxE || d_model <= 0 || d_model % 2 != 0) {
+  if (E > kGateMaxE || d_model <= 0 || d_model % 8 != 0 || k > kGateMaxK) {
     set_error("gate_wgrad: bad shape");
     return kErrDimension;
   }
   const int n_tiles = static_cast<int>((T + FSSDP_WG_TILE - 1) / FSSDP_WG_TILE);
   if (n_tiles > 0) {
-    const int smem = E * kWgDims * static_cast<int>(sizeof(float));
-    static bool configured = false;
-    if (!configured) {
-      if (cudaFuncSetAttribute(gate_wgrad_partial_kernel,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kGateMaxE * kWgDims * static_cast<int>(sizeof(float))) != cudaSuccess)
-        return launch_status();
-      configured = true;
-    }
     dim3 grid((d_model + kWgDims - 1) / kWgDims, n_tiles);
-    gate_wgrad_partial_kernel<<<grid, 128, smem, as_stream(stream)>>>(
+    gate_wgrad_partial_kernel<<<grid, kWgWarps * 32, 0, as_stream(stream)>>>(
         static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, workspace);
     int rc = launch_status();
     if (rc != kOk) return rc;
