@@ -233,6 +233,93 @@ __global__ void __launch_bounds__(kGateThreads)
                    slot_rank, tile_counts);
 }
 
+// ------------------------------------------------------------------ K1 on tensor cores
+// Gate logits with mma.sync m16n8k16 (bf16 in, fp32 accumulate): x is exactly bf16 and the
+// fp32 gate weights are split on the fly into hi = bf16(w) and lo = bf16(w - hi) (about 16
+// mantissa bits), logits = x·hi + x·lo.  One warp = 16 tokens x all experts; a CTA = 4
+// warps = one 64-token gate tile, so selection/ranks reuse gate_select_tile.  The HMMA
+// path is ~50x fewer instructions than the CUDA-core kernel and leaves the kernel bound by
+// reading x from HBM.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4],
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, "
+      "{%4, %5, %6, %7}, {%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void split_bf16x2(float2 w, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(w.x, w.y);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(w.x - hf.x, w.y - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+template <int NT>  // NT = E / 8 expert tiles
+__global__ void __launch_bounds__(128)
+    gate_topk_mma_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
+                         const float* __restrict__ bias, int64_t T, int d, int E, int k,
+                         float* __restrict__ logits, int32_t* __restrict__ topk_idx,
+                         float* __restrict__ topk_w, int32_t* __restrict__ slot_rank,
+                         int32_t* __restrict__ tile_counts) {
+  __shared__ float lg[kGateTile][kGateMaxE + 1];
+  __shared__ int32_t s_idx[kGateTile * kGateMaxK];
+  __shared__ int32_t s_cnt[kGateMaxE];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int tile = blockIdx.x;
+  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile + warp * 16;
+  const int64_t r0 = t0 + g, r1 = t0 + g + 8;
+  const bool v0 = r0 < T, v1 = r1 < T;
+  const uint32_t* xr0 = reinterpret_cast<const uint32_t*>(x + (v0 ? r0 : 0) * d);
+  const uint32_t* xr1 = reinterpret_cast<const uint32_t*>(x + (v1 ? r1 : 0) * d);
+  float c[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[n][i] = 0.f;
+#pragma unroll 2
+  for (int k0 = 0; k0 < d; k0 += 16) {
+    uint32_t a[4];
+    const int w0 = (k0 >> 1) + t4;  // 32-bit word of columns k0+2t, k0+2t+1
+    a[0] = v0 ? __ldg(xr0 + w0) : 0u;
+    a[1] = v1 ? __ldg(xr1 + w0) : 0u;
+    a[2] = v0 ? __ldg(xr0 + w0 + 4) : 0u;
+    a[3] = v1 ? __ldg(xr1 + w0 + 4) : 0u;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const float* wr = wg + static_cast<int64_t>(n * 8 + g) * d + k0 + 2 * t4;
+      uint32_t h0, l0, h1, l1;
+      split_bf16x2(__ldg(reinterpret_cast<const float2*>(wr)), h0, l0);
+      split_bf16x2(__ldg(reinterpret_cast<const float2*>(wr + 8)), h1, l1);
+      mma_bf16_16816(c[n], a, h0, h1);
+      mma_bf16_16816(c[n], a, l0, l1);
+    }
+  }
+  const int lr = warp * 16 + g;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int e = n * 8 + 2 * t4;
+    const float b0 = bias ? bias[e] : 0.f, b1 = bias ? bias[e + 1] : 0.f;
+    lg[lr][e] = bias ? __fadd_rn(c[n][0], b0) : c[n][0];
+    lg[lr][e + 1] = bias ? __fadd_rn(c[n][1], b1) : c[n][1];
+    lg[lr + 8][e] = bias ? __fadd_rn(c[n][2], b0) : c[n][2];
+    lg[lr + 8][e + 1] = bias ? __fadd_rn(c[n][3], b1) : c[n][3];
+  }
+  __syncthreads();
+  const int64_t tt0 = static_cast<int64_t>(tile) * kGateTile;
+  if (logits != nullptr) {
+    for (int v = threadIdx.x; v < kGateTile * E; v += blockDim.x) {
+      const int r = v / E, e = v % E;
+      if (tt0 + r < T) logits[(tt0 + r) * E + e] = lg[r][e];
+    }
+  }
+  gate_select_tile(&lg[0][0], kGateMaxE + 1, tile, T, E, k, s_idx, s_cnt, topk_idx, topk_w,
+                   slot_rank, tile_counts);
+}
+
 __global__ void __launch_bounds__(kGateThreads)
     topk_from_logits_kernel(const float* __restrict__ logits, int64_t T, int E, int k,
                             int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
@@ -520,69 +607,91 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dWg partials: grid (d/256, ceil(T/FSSDP_WG_TILE)), 16 warps.  Warp w owns experts
-// w, w+16, ... (<= 4) and keeps their 256-dim accumulators in registers (8 dims per lane);
-// it walks the tile's tokens and, warp-uniformly, adds dlogit * x[t] for the tokens routed
-// to its experts.  No shared read-modify-write chains; fp32 order per (e, dim) is fixed:
-// tokens ascending.
+// dWg partials: grid (d/256, ceil(T/FSSDP_WG_TILE)), 16 warps, one 256-token tile x
+// 256-dim chunk per CTA.  The tile's x rows are staged in shared memory (coalesced), its
+// k*256 token-slots are counting-sorted by expert (warp match_any ranks keep token order),
+// and warp w walks only the slot lists of its experts w, w+16, ... accumulating
+// dlogit * x[t] in registers (8 dims per lane).  fp32 order per (e, dim): tokens ascending.
 constexpr int kWgDims = 256;
 constexpr int kWgWarps = 16;
 constexpr int kWgMaxEpw = kGateMaxE / kWgWarps;
+constexpr int kWgSmemBytes = FSSDP_WG_TILE * kWgDims * 2;  // staged x tile (128 KB)
 __global__ void __launch_bounds__(kWgWarps * 32)
     gate_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
                               const int32_t* __restrict__ topk_idx,
                               const float* __restrict__ dlogit, int64_t T, int d_model, int E,
                               int k, float* __restrict__ workspace) {
-  __shared__ int32_t s_e[FSSDP_WG_TILE * kGateMaxK];
-  __shared__ float s_dl[FSSDP_WG_TILE * kGateMaxK];
+  extern __shared__ __align__(16) int4 s_x[];  // [FSSDP_WG_TILE][kWgDims / 8]
+  __shared__ int32_t s_tok[FSSDP_WG_TILE * kGateMaxK];   // sorted slot -> local token
+  __shared__ float s_coef[FSSDP_WG_TILE * kGateMaxK];    // sorted slot -> dlogit
+  __shared__ int32_t s_rank[FSSDP_WG_TILE * kGateMaxK];  // slot -> rank within its expert
+  __shared__ int32_t s_cnt[kGateMaxE];
+  __shared__ int32_t s_off[kGateMaxE + 1];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c = blockIdx.x * kWgDims + lane * 8;  // this lane's 8 model dims
-  const bool live = c < d_model;
+  const int c0 = blockIdx.x * kWgDims;
   const int64_t t_begin = static_cast<int64_t>(blockIdx.y) * FSSDP_WG_TILE;
-  const int64_t t_end = imin64(T, t_begin + FSSDP_WG_TILE);
-  const int nslot = static_cast<int>(t_end - t_begin) * k;
-  for (int i = threadIdx.x; i < nslot; i += blockDim.x) {
-    s_e[i] = topk_idx[t_begin * k + i];
-    s_dl[i] = dlogit[t_begin * k + i];
+  const int ntok = static_cast<int>(imin64(T, t_begin + FSSDP_WG_TILE) - t_begin);
+  const int nslot = ntok * k;
+  // stage x (all threads, coalesced 16-byte loads)
+  for (int v = threadIdx.x; v < FSSDP_WG_TILE * (kWgDims / 8); v += blockDim.x) {
+    const int r = v / (kWgDims / 8), q = v % (kWgDims / 8);
+    int4 val = make_int4(0, 0, 0, 0);
+    if (r < ntok && c0 + q * 8 < d_model)
+      val = *reinterpret_cast<const int4*>(x + (t_begin + r) * d_model + c0 + q * 8);
+    s_x[v] = val;
+  }
+  // warp 0: stable counting sort of the tile's slots by expert
+  if (warp == 0) {
+    for (int e = lane; e < E; e += 32) s_cnt[e] = 0;
+    __syncwarp();
+    for (int base = 0; base < nslot; base += 32) {
+      const int s = base + lane;
+      const bool ok = s < nslot;
+      const int e = ok ? topk_idx[t_begin * k + s] : -1;
+      const uint32_t peers = __match_any_sync(0xffffffffu, e);
+      const int r = ok ? s_cnt[e] + __popc(peers & ((1u << lane) - 1u)) : 0;
+      __syncwarp();
+      if (ok && (peers >> lane) == 1u) s_cnt[e] += __popc(peers);
+      __syncwarp();
+      if (ok) s_rank[s] = r;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int run = 0;
+      for (int e = 0; e < E; ++e) {
+        s_off[e] = run;
+        run += s_cnt[e];
+      }
+      s_off[E] = run;
+    }
   }
   __syncthreads();
-  float acc[kWgMaxEpw][8];
-#pragma unroll
-  for (int q = 0; q < kWgMaxEpw; ++q)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
-  const int ntok = static_cast<int>(t_end - t_begin);
-  for (int tt = 0; tt < ntok; ++tt) {
-    float coef[kWgMaxEpw];
-    bool any = false;
-#pragma unroll
-    for (int q = 0; q < kWgMaxEpw; ++q) {
-      coef[q] = 0.f;
-      const int e = warp + kWgWarps * q;
-      for (int j = 0; j < k; ++j)
-        if (s_e[tt * k + j] == e) {
-          coef[q] = s_dl[tt * k + j];
-          any = true;
-        }
-    }
-    if (!any || !live) continue;  // warp-uniform
-    float xv[8];
-    bf16x8_to_f32(*reinterpret_cast<const int4*>(x + (t_begin + tt) * d_model + c), xv);
-#pragma unroll
-    for (int q = 0; q < kWgMaxEpw; ++q)
-      if (coef[q] != 0.f)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[q][i] = fmaf(coef[q], xv[i], acc[q][i]);
+  for (int s = threadIdx.x; s < nslot; s += blockDim.x) {
+    const int e = topk_idx[t_begin * k + s];
+    const int dst = s_off[e] + s_rank[s];
+    s_tok[dst] = s / k;
+    s_coef[dst] = dlogit[t_begin * k + s];
   }
-  if (!live) return;
-#pragma unroll
+  __syncthreads();
+  const int c = c0 + lane * 8;
+  if (c >= d_model) return;
   for (int q = 0; q < kWgMaxEpw; ++q) {
     const int e = warp + kWgWarps * q;
     if (e >= E) break;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int p = s_off[e]; p < s_off[e + 1]; ++p) {
+      float xv[8];
+      bf16x8_to_f32(s_x[s_tok[p] * (kWgDims / 8) + lane], xv);
+      const float cf = s_coef[p];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(cf, xv[i], acc[i]);
+    }
     float4* out = reinterpret_cast<float4*>(
         workspace + (static_cast<int64_t>(blockIdx.y) * E + e) * d_model + c);
-    out[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
-    out[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
+    out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
 
@@ -705,6 +814,18 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
   }
   if (T == 0) return kOk;
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
+  if (E % 8 == 0 && d % 16 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
+    auto mma_launch = [&](auto kern) {
+      kern<<<tiles, 128, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(x), wg, bias,
+                                                  T, d, E, k, logits, topk_idx, topk_w, slot_rank,
+                                                  tile_counts);
+    };
+    if (E == 8) mma_launch(gate_topk_mma_kernel<1>);
+    else if (E == 16) mma_launch(gate_topk_mma_kernel<2>);
+    else if (E == 32) mma_launch(gate_topk_mma_kernel<4>);
+    else mma_launch(gate_topk_mma_kernel<8>);
+    return launch_status();
+  }
   size_t smem = kGateTile * sizeof(__nv_bfloat16) * (kGateChunk + 8) +
                 static_cast<size_t>(E) * sizeof(float) * (kGateChunk + 4);
   const size_t lg_bytes = kGateTile * sizeof(float) * (kGateMaxE + 1);
@@ -843,8 +964,16 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
   }
   const int n_tiles = static_cast<int>((T + FSSDP_WG_TILE - 1) / FSSDP_WG_TILE);
   if (n_tiles > 0) {
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(gate_wgrad_partial_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, kWgSmemBytes) !=
+          cudaSuccess)
+        return launch_status();
+      configured = true;
+    }
     dim3 grid((d_model + kWgDims - 1) / kWgDims, n_tiles);
-    gate_wgrad_partial_kernel<<<grid, kWgWarps * 32, 0, as_stream(stream)>>>(
+    gate_wgrad_partial_kernel<<<grid, kWgWarps * 32, kWgSmemBytes, as_stream(stream)>>>(
         static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, workspace);
     int rc = launch_status();
     if (rc != kOk) return rc;
