@@ -217,6 +217,8 @@ typedef struct fssdp_gemm_group {
  * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum.
  * flags: FSSDP_GEMM_N_FASTEST orders a group's tiles N-fastest (A tile shared in L2). */
 #define FSSDP_GEMM_N_FASTEST 1
+/* CTA-pair (tcgen05 cta_group::2) 256 x 256 tiles; requires every group's m_tiles even. */
+#define FSSDP_GEMM_CTA_PAIR 2
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,

@@ -115,6 +115,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.n_tiles = n_tiles;
   args.total_tiles = total_tiles;
   args.n_fast = (flags & FSSDP_GEMM_N_FASTEST) ? 1 : 0;
+  args.cta_group = (flags & FSSDP_GEMM_CTA_PAIR) ? 2 : 1;
   args.ldc = ldc;
   args.c = c;
   args.c2 = c2;

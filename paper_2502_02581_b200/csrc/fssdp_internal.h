@@ -32,6 +32,7 @@ struct GemmLaunch {
   int n_tiles;      // BN tiles along N (same for every group)
   int total_tiles;  // sum over groups of m_tiles * n_tiles
   int n_fast;       // tile order: 1 = N fastest (share A in L2), 0 = M fastest (share B)
+  int cta_group;    // 2 = CTA-pair 256x256 tiles (every group's m_tiles even), 1 = 128x256
   int64_t ldc;      // elements per C row
   void* c;          // output (bf16 or fp32)
   void* c2;         // second output (GeLU: post-activation)

@@ -2,18 +2,26 @@
 //
 // One persistent, warp-specialised kernel serves all six GEMMs of an FSSDP MoE layer
 // (fwd1, fwd2, dgrad2, dgrad1, wgrad1, wgrad2).  Operands are staged by TMA
-// (cp.async.bulk.tensor, SWIZZLE_128B) into a 4-deep shared-memory ring, multiplied
-// by tcgen05.mma (kind::f16, bf16 in / fp32 accumulate) into a double-buffered TMEM
-// accumulator, and drained by four epilogue warps that fuse the activation
-// (GeLU fwd, GeLU' in dgrad) and the output cast, then hand 32x32 tiles to TMA bulk
-// stores through double-buffered, bank-conflict-free swizzled staging buffers.
+// (cp.async.bulk.tensor, SWIZZLE_128B) into a shared-memory ring, multiplied by
+// tcgen05.mma (kind::f16, bf16 in / fp32 accumulate) into a double-buffered TMEM
+// accumulator, and drained by four epilogue warps that fuse the activation (GeLU fwd,
+// GeLU' in dgrad) and the output cast, then hand 32x32 tiles to TMA bulk stores through
+// double-buffered, bank-conflict-free swizzled staging buffers.
+//
+// CG = 2 (default): a CTA pair (cluster of 2) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 issued by the leader; each CTA stages only its 128-row half of
+// A and its 128-column half of B (32 KB per k-block instead of 48 KB for a 128 x 256
+// single-CTA tile), TMA bytes of both CTAs complete on the leader's mbarrier, MMA
+// completion is multicast to both CTAs, and each CTA drains its own 128 TMEM lanes.
+// CG = 1: the single-CTA 128 x 256 variant (used when a GEMM has an odd number of 128-row
+// tiles in some group).
 //
 // Grouping: every local expert (owned shard or SpAG replica) is one group.  A group's
-// tokens are a 128-row-aligned segment of the receive buffer, so an M tile never
-// straddles two experts; for wgrad the token axis is K and the segment padding rows
-// are zero, so K blocks never mix experts either.
+// tokens are a 256-row-aligned segment of the receive buffer, so an M tile never
+// straddles two experts; for wgrad the token axis is K and the segment padding rows are
+// zero, so K blocks never mix experts either.
 //
-// Warp roles (192 threads): w0 = TMA producer, w1 = MMA issuer + TMEM owner,
+// Warp roles (192 threads): w0 = TMA producer, w1 = MMA issuer (leader) + TMEM owner,
 // w2..w5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -25,16 +33,16 @@
 
 namespace fssdp {
 
-constexpr int kBM = 128;
-constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16
-constexpr int kStages = 4;
+constexpr int kBM = 128;  // rows per CTA
+constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
 constexpr int kThreads = 192;
 constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store box)
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 struct GemmSmem {
+  static constexpr int kStages = CG == 2 ? 6 : 4;
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = (EPI == kEpiF32) ? 4 : 2;
   static constexpr int kBufBytes = 32 * kEpiCols * kOutBytes;  // one 32x32 staging tile
@@ -66,17 +74,20 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
 }
 
 struct TileCoord {
-  int group, m_tile, n_tile;
+  int group, m_tile, n_tile;  // m_tile in units of CG * 128 rows
 };
 
+// Tiles are enumerated in units of (CG*128 rows) x BN columns; groups carry m_tiles and
+// tile_start in 128-row units (both even when CG == 2).
+template <int CG>
 __device__ __forceinline__ TileCoord locate_tile(const GemmGroup* __restrict__ groups,
                                                  int num_groups, int n_tiles, int n_fast,
                                                  int tile) {
   int g = 0;
   // groups are few (<= experts per device + replica slots); a linear scan is cheapest
-  while (g + 1 < num_groups && groups[g + 1].tile_start <= tile) ++g;
-  const int local = tile - groups[g].tile_start;
-  const int mt = groups[g].m_tiles;
+  while (g + 1 < num_groups && groups[g + 1].tile_start / CG <= tile) ++g;
+  const int local = tile - groups[g].tile_start / CG;
+  const int mt = groups[g].m_tiles / CG;
   TileCoord tc;
   tc.group = g;
   if (n_fast) {  // neighbouring CTAs share the A tile (activation rows) in L2
@@ -97,13 +108,15 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) {  // 128-byte rows, SWI
   return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
 }
 
-template <bool A_MN, bool B_MN, int BN, int EPI>
+template <bool A_MN, bool B_MN, int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
                         const __grid_constant__ CUtensorMap map_x, GemmLaunch args) {
-  using S = GemmSmem<BN, EPI>;
+  using S = GemmSmem<BN, EPI, CG>;
+  constexpr int kStages = S::kStages;
+  constexpr int kBNc = BN / CG;  // B columns staged by this CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -116,6 +129,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = CG == 2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int units = CG == 2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -127,50 +144,76 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty_bar[a], 4 * CG);  // one arrival per epilogue warp of the pair
     }
     for (int a = 0; a < 8; ++a) mbar_init(&aux_bar[a], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+  if (warp == 1) {
+    if (CG == 2)
+      tmem_alloc_pair<2 * BN>(tmem_slot);
+    else
+      tmem_alloc<2 * BN>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const GemmGroup* __restrict__ groups = args.groups;
-  const int total = args.total_tiles;
+  const int total = args.total_tiles / CG;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===================== TMA producer
+      // ===================== TMA producer (both CTAs stage their own halves)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
+      for (int tile = unit; tile < total; tile += units) {
+        const TileCoord tc =
+            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const GemmGroup& g = groups[tc.group];
-        const int m0 = g.a_m + tc.m_tile * kBM;
-        const int n0 = g.b_n + tc.n_tile * BN;
+        const int m0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * kBM;
+        const int n0 = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * kBNc;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
-          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * S::kStageBytes);
           const int ka = g.a_k + kb * kBK;
           const int kbb = g.b_k + kb * kBK;
-          if (A_MN) {
+          if (CG == 2) {
+            if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < kBM / 64; ++j)
-              tma_load_2d(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
-          } else {
-            tma_load_2d(sa, &map_a, &full_bar[stage], ka, m0);
-          }
-          if (B_MN) {
+              for (int j = 0; j < kBM / 64; ++j)
+                tma_load_2d_pair(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
+            } else {
+              tma_load_2d_pair(sa, &map_a, &full_bar[stage], ka, m0);
+            }
+            if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
+              for (int j = 0; j < kBNc / 64; ++j)
+                tma_load_2d_pair(sb + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
+            } else {
+              tma_load_2d_pair(sb, &map_b, &full_bar[stage], kbb, n0);
+            }
           } else {
-            tma_load_2d(sb, &map_b, &full_bar[stage], kbb, n0);
+            if (A_MN) {
+#pragma unroll
+              for (int j = 0; j < kBM / 64; ++j)
+                tma_load_2d(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
+            } else {
+              tma_load_2d(sa, &map_a, &full_bar[stage], ka, m0);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < kBNc / 64; ++j)
+                tma_load_2d(sb + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
+            } else {
+              tma_load_2d(sb, &map_b, &full_bar[stage], kbb, n0);
+            }
           }
           if (++stage == kStages) {
             stage = 0;
@@ -180,15 +223,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===================== MMA issuer (single thread)
-      constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+    if (lane == 0 && leader) {
+      // ===================== MMA issuer (single thread of the leader CTA)
+      constexpr uint32_t idesc =
+          make_idesc_bf16(CG * kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
+      for (int tile = unit; tile < total; tile += units) {
+        const TileCoord tc =
+            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const int kblocks = groups[tc.group].k_blocks;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -209,15 +254,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               bdesc = make_sdesc_sw128(b_base + kk * 2048, kBK * 128, 1024);
             else
               bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
+            if (CG == 2)
+              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs finish
+          // frees the smem slot (in both CTAs) when these MMAs finish
+          if (CG == 2)
+            umma_commit_pair(&empty_bar[stage]);
+          else
+            umma_commit(&empty_bar[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (CG == 2)  // accumulator ready for both CTAs' epilogues
+          umma_commit_pair(&tfull_bar[acc]);
+        else
+          umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -229,18 +284,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ew = warp - 2;
     uint8_t* wbase = smem + S::kEpiOffset + ew * S::kEpiWarpBytes;
-    uint8_t* cbuf0 = wbase;                         // C staging, buffers 0/1
-    uint8_t* xbuf0 = wbase + 2 * S::kBufBytes;      // C2 staging (GeLU) or aux tiles (GeLU')
+    uint8_t* cbuf0 = wbase;                     // C staging, buffers 0/1
+    uint8_t* xbuf0 = wbase + 2 * S::kBufBytes;  // C2 staging (GeLU) or aux tiles (GeLU')
     uint64_t* abar = aux_bar + 2 * ew;
     uint32_t aux_phase0 = 0, aux_phase1 = 0;
     constexpr int kChunks = BN / kEpiCols;
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t gchunk = 0;  // running chunk counter (selects the staging buffer)
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const TileCoord tc = locate_tile(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
+    for (int tile = unit; tile < total; tile += units) {
+      const TileCoord tc =
+          locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
       const GemmGroup& g = groups[tc.group];
-      const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * kBM + q * 32;
+      const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM) +
+                       static_cast<int>(rank) * kBM + q * 32;
       const int col0 = tc.n_tile * BN;
       const bool zero = g.k_blocks == 0;
       if (EPI == kEpiDGelu && lane == 0) {  // prefetch the first aux tile of this tile
@@ -267,7 +324,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c == kChunks - 1) {  // accumulator fully read: release TMEM to the MMA warp
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          if (lane == 0) {
+            if (CG == 2 && !leader)
+              mbar_arrive_leader(&tempty_bar[acc]);
+            else
+              mbar_arrive(&tempty_bar[acc]);
+          }
         }
         __nv_bfloat162 pre[16];
         if (EPI == kEpiDGelu) {
@@ -339,7 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(&map_c, cb, col0 + c * kEpiCols, row0);
-          if (EPI == kEpiGelu) tma_store_2d(&map_x, xbuf0 + b * S::kBufBytes, col0 + c * kEpiCols, row0);
+          if (EPI == kEpiGelu)
+            tma_store_2d(&map_x, xbuf0 + b * S::kBufBytes, col0 + c * kEpiCols, row0);
           bulk_commit();
         }
       }
@@ -352,21 +415,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
 
-  __syncthreads();
+  tc_fence_before();
+  if (CG == 2)
+    cluster_sync();  // the peer's smem / barriers stay alive until the pair is done
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<2 * BN>(tmem_base);
+    if (CG == 2)
+      tmem_dealloc_pair<2 * BN>(tmem_base);
+    else
+      tmem_dealloc<2 * BN>(tmem_base);
   }
 }
 
 // ------------------------------------------------------------------ host side
 
-template <bool A_MN, bool B_MN, int BN, int EPI>
+template <bool A_MN, bool B_MN, int BN, int EPI, int CG>
 static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                          const CUtensorMap& mx, const GemmLaunch& args, int grid,
-                          cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI>;
-  const int smem = GemmSmem<BN, EPI>::kDynamic;
+                          const CUtensorMap& mx, const GemmLaunch& args, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI, CG>;
+  const int smem = GemmSmem<BN, EPI, CG>::kDynamic;
   static bool configured = false;  // per template instance
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -374,21 +443,48 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
       return kErrCuda;
     configured = true;
   }
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mx, args);
+  const int units = args.total_tiles / CG;  // tiles of CG*128 rows
+  int grid = CG * (units < num_sms() / CG ? units : num_sms() / CG);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, args) != cudaSuccess) return kErrCuda;
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_MN, bool B_MN, int BN, int CG>
 static int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb,
                         const CUtensorMap& mc, const CUtensorMap& mx, const GemmLaunch& args,
-                        int grid, cudaStream_t stream) {
+                        cudaStream_t stream) {
   switch (epi) {
-    case kEpiBF16: return launch_variant<A_MN, B_MN, BN, kEpiBF16>(ma, mb, mc, mx, args, grid, stream);
-    case kEpiGelu: return launch_variant<A_MN, B_MN, BN, kEpiGelu>(ma, mb, mc, mx, args, grid, stream);
-    case kEpiDGelu: return launch_variant<A_MN, B_MN, BN, kEpiDGelu>(ma, mb, mc, mx, args, grid, stream);
-    case kEpiF32: return launch_variant<A_MN, B_MN, BN, kEpiF32>(ma, mb, mc, mx, args, grid, stream);
+    case kEpiBF16: return launch_variant<A_MN, B_MN, BN, kEpiBF16, CG>(ma, mb, mc, mx, args, stream);
+    case kEpiGelu: return launch_variant<A_MN, B_MN, BN, kEpiGelu, CG>(ma, mb, mc, mx, args, stream);
+    case kEpiDGelu: return launch_variant<A_MN, B_MN, BN, kEpiDGelu, CG>(ma, mb, mc, mx, args, stream);
+    case kEpiF32: return launch_variant<A_MN, B_MN, BN, kEpiF32, CG>(ma, mb, mc, mx, args, stream);
     default: return kErrDimension;
   }
+}
+
+template <int CG>
+static int dispatch_major(int a_mn, int b_mn, int epi, const CUtensorMap& ma,
+                          const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
+                          const GemmLaunch& args, cudaStream_t stream) {
+  constexpr int BN = 256;
+  if (a_mn) {
+    if (b_mn) return dispatch_epi<true, true, BN, CG>(epi, ma, mb, mc, mx, args, stream);
+    return dispatch_epi<true, false, BN, CG>(epi, ma, mb, mc, mx, args, stream);
+  }
+  if (b_mn) return dispatch_epi<false, true, BN, CG>(epi, ma, mb, mc, mx, args, stream);
+  return dispatch_epi<false, false, BN, CG>(epi, ma, mb, mc, mx, args, stream);
 }
 
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
@@ -397,11 +493,12 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   constexpr int BN = 256;
   if (args.total_tiles <= 0) return kOk;
   if (args.ldc % 32 != 0) return kErrDimension;
+  const int cg = args.cta_group == 2 ? 2 : 1;
   CUtensorMap ma, mb, mc, mx;
   // K-major operand: box = {64 K elems, rows};  MN-major: box = {64 MN elems, 64 K rows}
   int rc = make_tmap_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM, kDtBF16, 128);
   if (rc != kOk) return rc;
-  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN, kDtBF16, 128);
+  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / cg, kDtBF16, 128);
   if (rc != kOk) return rc;
   // epilogue tiles: 32 x 32, bf16 rows of 64 B (SWIZZLE_64B) or fp32 rows of 128 B
   if (epi == kEpiF32)
@@ -413,13 +510,8 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   rc = make_tmap_2d(&mx, xptr, args.ldc, c_rows, kEpiCols, 32, epi == kEpiF32 ? kDtF32 : kDtBF16,
                     epi == kEpiF32 ? 128 : 64);
   if (rc != kOk) return rc;
-  int grid = args.total_tiles < num_sms() ? args.total_tiles : num_sms();
-  if (a_mn) {
-    if (b_mn) return dispatch_epi<true, true, BN>(epi, ma, mb, mc, mx, args, grid, stream);
-    return dispatch_epi<true, false, BN>(epi, ma, mb, mc, mx, args, grid, stream);
-  }
-  if (b_mn) return dispatch_epi<false, true, BN>(epi, ma, mb, mc, mx, args, grid, stream);
-  return dispatch_epi<false, false, BN>(epi, ma, mb, mc, mx, args, grid, stream);
+  if (cg == 2) return dispatch_major<2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+  return dispatch_major<1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
 }
 
 }  // namespace fssdp

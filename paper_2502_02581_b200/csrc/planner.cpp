@@ -1047,7 +1047,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
     for (int e : slot_expert[d]) {
       int64_t rows = 0;
       for (int s = 0; s < D; ++s) rows += R(s, e, d);
-      const int64_t padded = (rows + 127) / 128 * 128;
+      const int64_t padded = (rows + 255) / 256 * 256;  // CTA-pair GEMM M tile
       seg_start[d].push_back(st);
       seg_rows[d].push_back(rows);
       seg_pad[d].push_back(padded);

@@ -46,7 +46,7 @@ class LayerGeometry:
 
     @property
     def recv_cap(self) -> int:
-        rows = self.world * self.max_tokens * self.top_k + self.slots * 127
+        rows = self.world * self.max_tokens * self.top_k + self.slots * 255  # 256-row padding
         return (rows + 127) // 128 * 128
 
     @property
@@ -286,12 +286,13 @@ class FssdpMoE:
     # tile order per GEMM: N-fastest where the A operand (activations) is the big,
     # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
     N_FASTEST = {"fwd2": True, "dgrad1": True}
+    CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
 
     def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None):
         ng, n_tiles, total = self.gemm[name]
         if total == 0:
             return
-        flags = 1 if self.N_FASTEST.get(name, False) else 0
+        flags = (1 if self.N_FASTEST.get(name, False) else 0) | (2 if self.CTA_PAIR else 0)
         self._timed("gemm." + name, lambda: N.call(
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
             ops._ptr(b), b.shape[1], b.shape[0], self._tab(name), ng, n_tiles, total, ops._ptr(c),

@@ -69,7 +69,8 @@ GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"
 def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, groups_dev: torch.Tensor,
                  num_groups: int, n_tiles: int, total_tiles: int, c: torch.Tensor, ldc: int,
                  epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
-                 aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False) -> None:
+                 aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
+                 cta_pair: bool = False) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
@@ -83,7 +84,7 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
     N.call("fssdp_grouped_gemm", int(a_mn), int(b_mn), int(epilogue), _ptr(a), a.shape[1],
            a.shape[0], _ptr(b), b.shape[1], b.shape[0], _ptr(groups_dev), num_groups, n_tiles,
            total_tiles, _ptr(c), _ptr(c2), _ptr(aux), ldc, c.numel() // ldc,
-           1 if n_fastest else 0, _stream(stream))
+           (1 if n_fastest else 0) | (2 if cta_pair else 0), _stream(stream))
 
 
 # ------------------------------------------------------------------ gate

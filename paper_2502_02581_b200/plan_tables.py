@@ -20,7 +20,7 @@ import numpy as np
 
 from .errors import InternalError
 
-ROW_ALIGN = 128
+ROW_ALIGN = 256  # = the CTA-pair GEMM M tile (two 128-row halves)
 GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
                         ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("pad_", "<i4"),
                         ("c_off", "<i8")])

@@ -144,6 +144,71 @@ def test_wgrad_style_token_k(a_mn):
         k0 += s
 
 
+@pytest.mark.parametrize("a_mn,b_mn,epi", [(False, False, "bf16"), (False, False, "gelu"),
+                                           (False, True, "dgelu"), (False, True, "bf16"),
+                                           (True, True, "f32")])
+@pytest.mark.parametrize("nf", [False, True])
+def test_cta_pair_tiles(a_mn, b_mn, epi, nf):
+    """tcgen05 cta_group::2 (256 x 256 tiles over a CTA pair): every operand major-ness and
+    epilogue the layer uses, groups with even 128-row tile counts (incl. an empty group)."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(7)
+    K, N = 384, 512
+    m_tiles = [2, 4, 0, 2]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    e = {"bf16": ops.EPI_BF16, "gelu": ops.EPI_GELU, "dgelu": ops.EPI_DGELU,
+         "f32": ops.EPI_F32}[epi]
+    if not a_mn:
+        A = torch.randn(R, K, device=dev).bfloat16()                        # [M][K]
+    else:
+        A = torch.randn(K * G, 256, device=dev).bfloat16()                  # [K][M] per group
+    if not b_mn:
+        B = (torch.randn(G * N, K, device=dev) / K ** 0.5).bfloat16()       # [N][K]
+    else:
+        B = (torch.randn(G * K, N, device=dev) / K ** 0.5).bfloat16()       # [K][N]
+    rows, refs, r0 = [], [], 0
+    if a_mn:  # wgrad-like: M = 256 per group, K = per-group token rows
+        C = torch.zeros(G * 256, N, device=dev)
+        for g in range(G):
+            kb = (K // 64) if m_tiles[g] else 0
+            rows.append((2, 0, g * K, 0, g * K, kb, g * 256 * N))
+            ref = A[g * K:(g + 1) * K].float().T @ B[g * K:(g + 1) * K].float()
+            refs.append((slice(g * 256, (g + 1) * 256), ref if kb else torch.zeros_like(ref)))
+    else:
+        C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+        for g, mt in enumerate(m_tiles):
+            if b_mn:
+                rows.append((mt, r0, 0, 0, g * K, K // 64, r0 * N))
+                ref = A[r0:r0 + mt * 128].float() @ B[g * K:(g + 1) * K].float()
+            else:
+                rows.append((mt, r0, 0, g * N, 0, K // 64, r0 * N))
+                ref = A[r0:r0 + mt * 128].float() @ B[g * N:(g + 1) * N].float().T
+            refs.append((slice(r0, r0 + mt * 128), ref))
+            r0 += mt * 128
+    C2 = torch.zeros_like(C)
+    aux = torch.randn(C.shape, device=dev).bfloat16() if epi == "dgelu" else None
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    ops.grouped_gemm(A, a_mn, B, b_mn, gd, ng, N // 256, total, C, N, epilogue=e,
+                     c2=C2 if epi == "gelu" else None, aux=aux, n_fastest=nf, cta_pair=True)
+    torch.cuda.synchronize()
+    for sl, ref in refs:
+        if ref.numel() == 0:
+            continue
+        if epi == "f32":
+            _close(C[sl], ref, rel=2e-3, abs_=1e-4)
+        elif epi == "dgelu":
+            a = aux[sl].float()
+            k0, k1 = 0.7978845608028654, 0.044715
+            t = torch.tanh(k0 * (a + k1 * a ** 3))
+            _close(C[sl], ref * (0.5 * (1 + t) + 0.5 * a * (1 - t * t) * k0 * (1 + 3 * k1 * a * a)))
+        else:
+            _close(C[sl], ref)
+            if epi == "gelu":
+                _close(C2[sl], torch.nn.functional.gelu(C[sl].float(), approximate="tanh"))
+
+
 def test_large_square_against_torch():
     """One big group (the throughput shape family) for a sanity check of the pipeline."""
     ops = _ops()
