@@ -204,8 +204,8 @@ typedef struct fssdp_gemm_group {
 } fssdp_gemm_group;
 
 #define FSSDP_EPI_BF16 0  /* C = bf16(acc) */
-#define FSSDP_EPI_GELU 1  /* C = bf16(acc) (pre-activation), C2 = bf16(gelu(C)) */
-#define FSSDP_EPI_DGELU 2 /* C = bf16(acc * gelu'(aux)) */
+#define FSSDP_EPI_GELU 1  /* C = bf16(gelu'(acc)) (saved for backward), C2 = bf16(gelu(acc)) */
+#define FSSDP_EPI_DGELU 2 /* C = bf16(acc * aux)  (aux = the saved gelu'(pre-activation)) */
 #define FSSDP_EPI_F32 3   /* C = acc (fp32) */
 
 /* Grouped GEMM  C_g = A_g · B_g  on tcgen05 (K5/K7).  A and B are bf16 2-D tensors

@@ -9,8 +9,8 @@ restates the paper's semantics; parity here is UNPINNED by reference tests:
 * dispatch: token-slot order (t, j) ascending fills the destinations of a
   (source, expert) cell in ascending device order with the build_dispatch counts
   route[s, e, d] (dispatch.py:49-97 gives the counts; the per-token order is ours).
-* expert FFN: A = X·W1ᵀ, H = gelu_tanh(A), Y = H·W2ᵀ, bf16 storage,
-  fp32 accumulation.
+* expert FFN: A = X·W1ᵀ (fp32), H = bf16(gelu_tanh(A)), Y = H·W2ᵀ; the
+  backward uses the saved G' = bf16(gelu_tanh'(A)): dA = bf16((dY·W2)·G').
 * combine: y_t = Σ_j w_tj · Y_tj in fp32, j ascending, then bf16.
 * SpAG: replica = owner copy; SpRS: owner = Σ replicas in ascending device order, fp32
   (PAPER.md:370-386).
@@ -164,7 +164,7 @@ def moe_layer_fwd_bwd(x, idx, w, wg, experts, dy):
         if len(rows) == 0:
             continue
         xe = x[rows[:, 0]].astype(np.float32)
-        a = bf16_round((xe @ W1.T).astype(np.float32))
+        a = (xe @ W1.T).astype(np.float32)  # fp32 pre-activation (never stored)
         h = bf16_round(gelu_tanh(a).astype(np.float32))
         Y[rows[:, 0], rows[:, 1]] = bf16_round((h @ W2.T).astype(np.float32))
         A[e], H[e] = (rows, a), h
@@ -184,7 +184,8 @@ def moe_layer_fwd_bwd(x, idx, w, wg, experts, dy):
         rows, a = A[e]
         dYe = bf16_round((w[rows[:, 0], rows[:, 1]][:, None] * dy[rows[:, 0]]).astype(np.float32))
         dH = (dYe @ W2).astype(np.float32)
-        dA = bf16_round((dH * gelu_tanh_grad(a)).astype(np.float32))
+        gp = bf16_round(gelu_tanh_grad(a).astype(np.float32))  # saved gelu'(a), bf16
+        dA = bf16_round((dH * gp).astype(np.float32))
         dXs[rows[:, 0], rows[:, 1]] = bf16_round((dA @ W1).astype(np.float32))
         xe = x[rows[:, 0]].astype(np.float32)
         dW1[e] = (dA.T @ xe).astype(np.float32)

@@ -35,23 +35,31 @@ namespace fssdp {
 
 constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
-constexpr int kThreads = 192;
+// 4 epilogue warps (one per TMEM lane quarter).  8 (two per quarter, column halves) is
+// supported by the code but measured slower: the smem it needs costs a mainloop stage.
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store box)
 
 template <int BN, int EPI, int CG>
 struct GemmSmem {
-  static constexpr int kStages = CG == 2 ? 6 : 4;
+  // GeLU' (dgrad2) trades a mainloop stage for a deeper aux-tile prefetch ring
+  static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : 0;
+  static constexpr int kStages =
+      kEpiWarps == 4 ? (CG == 2 ? (EPI == kEpiDGelu ? 5 : 6) : 4)
+                     : (CG == 2 ? (EPI == kEpiDGelu ? 4 : 5) : 3);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = (EPI == kEpiF32) ? 4 : 2;
   static constexpr int kBufBytes = 32 * kEpiCols * kOutBytes;  // one 32x32 staging tile
-  static constexpr int kStreams = (EPI == kEpiGelu || EPI == kEpiDGelu) ? 2 : 1;
-  static constexpr int kEpiWarpBytes = kStreams * 2 * kBufBytes;  // double buffered
+  // per warp: C staging x2, plus C2 staging x2 (GeLU) or the aux ring (GeLU')
+  static constexpr int kXBufs = EPI == kEpiGelu ? 2 : kAuxBufs;
+  static constexpr int kEpiWarpBytes = (2 + kXBufs) * kBufBytes;
   static constexpr int kEpiOffset = kStages * kStageBytes;
-  static constexpr int kBarOffset = kEpiOffset + 4 * kEpiWarpBytes;
-  // full[S], empty[S], tmem_full[2], tmem_empty[2], aux[4 warps][2], tmem base slot
-  static constexpr int kTotal = kBarOffset + (2 * kStages + 4 + 8) * 8 + 16;
+  static constexpr int kBarOffset = kEpiOffset + kEpiWarps * kEpiWarpBytes;
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], aux[kEpiWarps][4], tmem base slot
+  static constexpr int kTotal = kBarOffset + (2 * kStages + 4 + 4 * kEpiWarps) * 8 + 16;
   static constexpr int kDynamic = kTotal + 1024;  // slack for 1024-B alignment
   static_assert(kDynamic <= 232448, "shared memory budget exceeded");
 };
@@ -65,12 +73,15 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return fmaf(hx, tanh_approx(u), hx);
 }
 
-__device__ __forceinline__ float gelu_tanh_grad(float x) {
+// GeLU and its derivative from one tanh (fwd1 saves gelu'(a) for dgrad2's epilogue).
+__device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
   const float k0 = 0.7978845608028654f;
   const float k1 = 0.044715f;
   const float x2 = x * x;
   const float t = tanh_approx(k0 * fmaf(k1 * x2, x, x));
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f);
+  const float hx = 0.5f * x;
+  g = fmaf(hx, t, hx);
+  dg = fmaf(0.5f, 1.0f + t, hx * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f));
 }
 
 struct TileCoord {
@@ -125,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* aux_bar = tempty_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4 * kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -144,9 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4 * CG);  // one arrival per epilogue warp of the pair
+      mbar_init(&tempty_bar[a], kEpiWarps * CG);  // one arrival per epilogue warp of the pair
     }
-    for (int a = 0; a < 8; ++a) mbar_init(&aux_bar[a], 1);
+    for (int a = 0; a < 4 * kEpiWarps; ++a) mbar_init(&aux_bar[a], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -286,12 +297,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* wbase = smem + S::kEpiOffset + ew * S::kEpiWarpBytes;
     uint8_t* cbuf0 = wbase;                     // C staging, buffers 0/1
     uint8_t* xbuf0 = wbase + 2 * S::kBufBytes;  // C2 staging (GeLU) or aux tiles (GeLU')
-    uint64_t* abar = aux_bar + 2 * ew;
-    uint32_t aux_phase0 = 0, aux_phase1 = 0;
+    // aux ring (GeLU'): kAuxBufs tiles, prefetched kAuxBufs-1 chunks ahead
+    constexpr int kAB = S::kAuxBufs > 0 ? S::kAuxBufs : 1;
+    uint64_t* abar = aux_bar + 4 * ew;
+    uint32_t aux_phase = 0;  // bit i = phase of aux buffer i
     constexpr int kChunks = BN / kEpiCols;
+    constexpr int kCW = kChunks / (kEpiWarps / 4);  // chunks drained by this warp
+    const int cbase = (ew / 4) * kCW;                // warps 2-5: left half, 6-9: right half
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t gchunk = 0;  // running chunk counter (selects the staging buffer)
+    uint32_t gchunk = 0;  // running chunk counter (selects the staging buffers)
     for (int tile = unit; tile < total; tile += units) {
       const TileCoord tc =
           locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
@@ -300,16 +315,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                        static_cast<int>(rank) * kBM + q * 32;
       const int col0 = tc.n_tile * BN;
       const bool zero = g.k_blocks == 0;
-      if (EPI == kEpiDGelu && lane == 0) {  // prefetch the first aux tile of this tile
-        const int b = gchunk & 1;
+      if (EPI == kEpiDGelu && lane == 0) {  // prefetch the first aux tiles of this tile
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&abar[b], S::kBufBytes);
-        tma_load_2d(xbuf0 + b * S::kBufBytes, &map_x, &abar[b], col0, row0);
+        for (int p = 0; p < kAB - 1 && p < kCW; ++p) {
+          const int ab = (gchunk + p) % kAB;
+          mbar_arrive_expect_tx(&abar[ab], S::kBufBytes);
+          tma_load_2d(xbuf0 + ab * S::kBufBytes, &map_x, &abar[ab], col0 + (cbase + p) * kEpiCols,
+                      row0);
+        }
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < kChunks; ++c, ++gchunk) {
+      for (int ci = 0; ci < kCW; ++ci, ++gchunk) {
+        const int c = cbase + ci;
         const int b = gchunk & 1;
         uint32_t r[32];
         if (!zero) {
@@ -321,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
-        if (c == kChunks - 1) {  // accumulator fully read: release TMEM to the MMA warp
+        if (ci == kCW - 1) {  // this warp's share of the accumulator read: release TMEM
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -333,21 +352,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __nv_bfloat162 pre[16];
         if (EPI == kEpiDGelu) {
-          if (lane == 0 && c + 1 < kChunks) {  // prefetch the next aux tile
-            const int nb = (gchunk + 1) & 1;
+          if (lane == 0 && ci + kAB - 1 < kCW) {  // keep kAB-1 aux tiles in flight
+            const int nb = (gchunk + kAB - 1) % kAB;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&abar[nb], S::kBufBytes);
-            tma_load_2d(xbuf0 + nb * S::kBufBytes, &map_x, &abar[nb], col0 + (c + 1) * kEpiCols,
-                        row0);
+            tma_load_2d(xbuf0 + nb * S::kBufBytes, &map_x, &abar[nb],
+                        col0 + (c + kAB - 1) * kEpiCols, row0);
           }
-          if (b == 0) {
-            mbar_wait(&abar[0], aux_phase0);
-            aux_phase0 ^= 1;
-          } else {
-            mbar_wait(&abar[1], aux_phase1);
-            aux_phase1 ^= 1;
-          }
-          const uint8_t* ab = xbuf0 + b * S::kBufBytes;
+          const int cur = gchunk % kAB;
+          mbar_wait(&abar[cur], (aux_phase >> cur) & 1u);
+          aux_phase ^= 1u << cur;
+          const uint8_t* ab = xbuf0 + cur * S::kBufBytes;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<int4*>(&pre[4 * j]) =
@@ -373,23 +388,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (EPI == kEpiGelu) {
             __nv_bfloat162 act[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]),
-                                             __uint_as_float(r[2 * i + 1]));
-              const float2 p = __bfloat1622float2(out[i]);
-              act[i] = __floats2bfloat162_rn(gelu_tanh(p.x), gelu_tanh(p.y));
+            for (int i = 0; i < 16; ++i) {  // one tanh feeds both GeLU and GeLU'
+              float g0, d0, g1, d1;
+              gelu_and_grad(__uint_as_float(r[2 * i]), g0, d0);
+              gelu_and_grad(__uint_as_float(r[2 * i + 1]), g1, d1);
+              act[i] = __floats2bfloat162_rn(g0, g1);
+              out[i] = __floats2bfloat162_rn(d0, d1);
             }
             uint8_t* xb = xbuf0 + b * S::kBufBytes;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               *reinterpret_cast<int4*>(xb + sw64(lane, j)) =
                   *reinterpret_cast<const int4*>(&act[4 * j]);
-          } else {  // kEpiDGelu: out = acc * gelu'(pre-activation)
+          } else {  // kEpiDGelu: out = acc * gelu'(pre-activation), gelu' saved by fwd1
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float2 p = __bfloat1622float2(pre[i]);
-              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * gelu_tanh_grad(p.x),
-                                             __uint_as_float(r[2 * i + 1]) * gelu_tanh_grad(p.y));
+              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * p.x,
+                                             __uint_as_float(r[2 * i + 1]) * p.y);
             }
           }
 #pragma unroll

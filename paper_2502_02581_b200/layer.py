@@ -118,7 +118,7 @@ class FssdpMoE:
         self.w1_view = flat.view(geom.slots * 2 * f, d)                  # W1 of slot s: rows s*2f..
         self.w2_view = flat[f * d:].view(geom.slots * 2 * d - d, f)      # W2 of slot s: rows s*2d..
         # local activations (capacity-sized once, so plans never reallocate)
-        self.a_pre = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
+        self.gprime = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)  # gelu'(X W1^T)
         self.h = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
         self.da = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
         Tc = geom.max_tokens
@@ -300,7 +300,7 @@ class FssdpMoE:
 
     def phase_experts_fwd(self) -> None:
         f, d = self.g.d_ff, self.g.d_model
-        self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.a_pre, f, ops.EPI_GELU,
+        self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.gprime, f, ops.EPI_GELU,
                    c2=self.h)
         self._gemm("fwd2", self.h, False, self.w2_view, False, self.y_e, d, ops.EPI_BF16)
 
@@ -335,7 +335,7 @@ class FssdpMoE:
     def phase_experts_bwd(self) -> None:
         f, d = self.g.d_ff, self.g.d_model
         self._gemm("dgrad2", self.dyrecv, False, self.w2_view, True, self.da, f, ops.EPI_DGELU,
-                   aux=self.a_pre)
+                   aux=self.gprime)
         self._gemm("dgrad1", self.da, False, self.w1_view, True, self.dxe, d, ops.EPI_BF16)
         grads2d = self.grads.view(-1)
         self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32)

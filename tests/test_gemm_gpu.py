@@ -67,16 +67,17 @@ def test_kmajor_kmajor_grouped(epi, nf):
         r0 += mt * 128
     if epi == "bf16":
         _close(C, ref)
-    elif epi == "gelu":
-        _close(C, ref)
-        pre = C.float()
-        _close(C2, torch.nn.functional.gelu(pre, approximate="tanh"))
-    else:
-        a = aux.float()
-        k0, k1 = 0.7978845608028654, 0.044715
-        t = torch.tanh(k0 * (a + k1 * a ** 3))
-        gp = 0.5 * (1 + t) + 0.5 * a * (1 - t * t) * k0 * (1 + 3 * k1 * a * a)
-        _close(C, ref * gp)
+    elif epi == "gelu":  # C = gelu'(acc) (saved for backward), C2 = gelu(acc)
+        _close(C, gelu_grad(ref))
+        _close(C2, torch.nn.functional.gelu(ref, approximate="tanh"))
+    else:  # C = acc * aux
+        _close(C, ref * aux.float())
+
+
+def gelu_grad(a):
+    k0, k1 = 0.7978845608028654, 0.044715
+    t = torch.tanh(k0 * (a + k1 * a ** 3))
+    return 0.5 * (1 + t) + 0.5 * a * (1 - t * t) * k0 * (1 + 3 * k1 * a * a)
 
 
 def test_kmajor_mnmajor_dgrad_style():
@@ -199,14 +200,12 @@ def test_cta_pair_tiles(a_mn, b_mn, epi, nf):
         if epi == "f32":
             _close(C[sl], ref, rel=2e-3, abs_=1e-4)
         elif epi == "dgelu":
-            a = aux[sl].float()
-            k0, k1 = 0.7978845608028654, 0.044715
-            t = torch.tanh(k0 * (a + k1 * a ** 3))
-            _close(C[sl], ref * (0.5 * (1 + t) + 0.5 * a * (1 - t * t) * k0 * (1 + 3 * k1 * a * a)))
+            _close(C[sl], ref * aux[sl].float())
+        elif epi == "gelu":
+            _close(C[sl], gelu_grad(ref))
+            _close(C2[sl], torch.nn.functional.gelu(ref, approximate="tanh"))
         else:
             _close(C[sl], ref)
-            if epi == "gelu":
-                _close(C2[sl], torch.nn.functional.gelu(C[sl].float(), approximate="tanh"))
 
 
 def test_large_square_against_torch():
