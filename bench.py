@@ -316,6 +316,13 @@ def run_ours(args):
                 "gemm_share_of_step": float(allr[:, 0].max() / ms_max),
                 "gemm_launches_per_step": gemm_launches / args.steps,
                 "host_plan_ms_per_step": float(allr[:, 6].max())}
+    # per-phase device time (CUDA events around every kernel of the timed steps), max over ranks
+    keys = sorted(k for k in timers if k != "host_plan_s")
+    phase_ms = [sum(s.elapsed_time(e) for s, e in timers[k]) / args.steps for k in keys]
+    allp = gather(phase_ms) if keys else None
+    breakdown = {k: round(float(allp[:, i].max()), 4) for i, k in enumerate(keys)} if keys else {}
+    breakdown["host_plan"] = round(float(allr[:, 6].max()), 4)
+    breakdown["sum_of_kernels_max_rank"] = round(float(allp.sum(axis=1).max()), 4) if keys else 0.0
     sparse = None
     if world > 1:
         tr, rep = F.spag_traffic(dec.base, dec.target, layer.g.expert_bytes)
@@ -401,7 +408,8 @@ def run_ours(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded N(0,1) tokens, random-init experts, Zipf gate bias)",
                 "config": _config(args, world), "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary()}
+                "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+                "phase_ms_per_step": breakdown}
         if sparse:
             line["sparse_collectives"] = sparse
         print(json.dumps(line), flush=True)

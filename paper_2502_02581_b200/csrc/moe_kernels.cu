@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "fssdp_internal.h"
 #include "ptx.cuh"
@@ -715,18 +717,26 @@ __global__ void gate_wgrad_reduce_kernel(const float* __restrict__ workspace, in
 }
 
 // ------------------------------------------------------------------ K3 SpAG / K8 SpRS
-constexpr int kCollChunk = 64 * 1024;  // bytes per CTA per copy job
+// Chunk size per CTA is chosen by the launcher so every launch spreads over ~4 CTAs per
+// SM whatever the expert size (small experts are otherwise latency/parallelism bound).
+static int64_t coll_chunk_bytes(int64_t total_bytes, int sms) {
+  int64_t c = total_bytes / (4 * static_cast<int64_t>(sms));
+  c = (c + 4095) / 4096 * 4096;
+  if (c < 8192) c = 8192;
+  if (c > 256 * 1024) c = 256 * 1024;
+  return c;
+}
 
 __global__ void __launch_bounds__(256)
     spag_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t param_off,
-                int64_t slot_bytes, const int32_t* __restrict__ copies) {
+                int64_t slot_bytes, const int32_t* __restrict__ copies, int64_t chunk) {
   const int job = blockIdx.y;
   const int src_rank = copies[3 * job];
   const int64_t src_slot = copies[3 * job + 1];
   const int64_t dst_slot = copies[3 * job + 2];
-  const int64_t begin = static_cast<int64_t>(blockIdx.x) * kCollChunk;
+  const int64_t begin = static_cast<int64_t>(blockIdx.x) * chunk;
   if (begin >= slot_bytes) return;
-  const int64_t bytes = imin64(kCollChunk, slot_bytes - begin);
+  const int64_t bytes = imin64(chunk, slot_bytes - begin);
   const int4* src = reinterpret_cast<const int4*>(
       reinterpret_cast<const char*>(peer_bases[src_rank] + param_off) + src_slot * slot_bytes +
       begin);
@@ -745,35 +755,98 @@ __global__ void __launch_bounds__(256)
   for (; i < n16; i += 256) st_v4(dst + i, ld_nc_v4(src + i));
 }
 
+// TMA-staged SpAG: one warp per CTA, its elected lane streams the CTA's chunk of a replica
+// copy through a kTmaRing-deep ring of kTmaSub-byte smem buffers: bulk load from the owner's
+// (peer) HBM, bulk store to the local replica slot.  Few SM resources per byte in flight.
+constexpr int kTmaSub = 8 * 1024;
+constexpr int kTmaRing = 4;  // 32 KB of static smem per CTA -> several CTAs per SM
+__global__ void __launch_bounds__(32)
+    spag_tma_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t param_off,
+                    int64_t slot_bytes, const int32_t* __restrict__ copies, int64_t chunk) {
+  __shared__ __align__(128) uint8_t ring[kTmaRing][kTmaSub];
+  __shared__ __align__(8) uint64_t bar[kTmaRing];
+  const int job = blockIdx.y;
+  const int64_t begin = static_cast<int64_t>(blockIdx.x) * chunk;
+  if (begin >= slot_bytes || threadIdx.x != 0) return;
+  const int src_rank = copies[3 * job];
+  const int64_t src_slot = copies[3 * job + 1];
+  const int64_t dst_slot = copies[3 * job + 2];
+  const int64_t bytes = imin64(chunk, slot_bytes - begin);
+  const char* src = reinterpret_cast<const char*>(peer_bases[src_rank] + param_off) +
+                    src_slot * slot_bytes + begin;
+  char* dst = reinterpret_cast<char*>(peer_bases[rank] + param_off) + dst_slot * slot_bytes + begin;
+  for (int i = 0; i < kTmaRing; ++i) mbar_init(&bar[i], 1);
+  fence_barrier_init();
+  const int nsub = static_cast<int>((bytes + kTmaSub - 1) / kTmaSub);
+  auto issue = [&](int s) {
+    const int slot = s % kTmaRing;
+    const uint32_t n = static_cast<uint32_t>(imin64(kTmaSub, bytes - int64_t(s) * kTmaSub));
+    mbar_arrive_expect_tx(&bar[slot], n);
+    bulk_load_g2s(ring[slot], src + int64_t(s) * kTmaSub, n, &bar[slot]);
+  };
+  for (int s = 0; s < kTmaRing && s < nsub; ++s) issue(s);
+  uint32_t phase = 0;  // bit per ring slot
+  for (int s = 0; s < nsub; ++s) {
+    const int slot = s % kTmaRing;
+    mbar_wait(&bar[slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    const uint32_t n = static_cast<uint32_t>(imin64(kTmaSub, bytes - int64_t(s) * kTmaSub));
+    bulk_store_s2g(dst + int64_t(s) * kTmaSub, ring[slot], n);
+    bulk_commit();
+    if (s + kTmaRing < nsub) {
+      bulk_wait_read<0>();  // this slot's store has read the buffer: reuse it
+      issue(s + kTmaRing);
+    }
+  }
+  bulk_wait<0>();
+}
+
 __global__ void __launch_bounds__(256)
     sprs_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
                 int64_t slot_elems, const int32_t* __restrict__ jobs,
-                const int32_t* __restrict__ srcs) {
+                const int32_t* __restrict__ srcs, int64_t chunk) {
+  __shared__ const int4* s_src[kMaxWorld];
   const int job = blockIdx.y;
   const int64_t dst_slot = jobs[3 * job];
   const int src_begin = jobs[3 * job + 1];
   const int src_count = jobs[3 * job + 2];
-  const int64_t chunk_elems = kCollChunk / 4;
+  const int64_t chunk_elems = chunk / 4;
   const int64_t begin = static_cast<int64_t>(blockIdx.x) * chunk_elems;
   if (begin >= slot_elems) return;
+  if (threadIdx.x < src_count) {
+    const int r = srcs[2 * (src_begin + threadIdx.x)];
+    const int64_t sl = srcs[2 * (src_begin + threadIdx.x) + 1];
+    s_src[threadIdx.x] = reinterpret_cast<const int4*>(
+        reinterpret_cast<const float*>(peer_bases[r] + grad_off) + sl * slot_elems + begin);
+  }
+  __syncthreads();
   const int64_t n = imin64(chunk_elems, slot_elems - begin);
   const int n4 = static_cast<int>(n / 4);
   float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(peer_bases[rank] + grad_off) +
                                           dst_slot * slot_elems + begin);
-  for (int i = threadIdx.x; i < n4; i += 256) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  // U float4 per thread per pass: U * src_count 128-bit loads in flight; each element is
+  // still summed over the holders in ascending-rank order (bit-exact vs the oracle).
+  constexpr int U = 4;
+  for (int i0 = threadIdx.x; i0 < n4; i0 += U * 256) {
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int q = 0; q < src_count; ++q) {
-      const int r = srcs[2 * (src_begin + q)];
-      const int64_t sl = srcs[2 * (src_begin + q) + 1];
-      const float4* src = reinterpret_cast<const float4*>(
-          reinterpret_cast<const float*>(peer_bases[r] + grad_off) + sl * slot_elems + begin);
-      int4 raw = ld_nc_v4(reinterpret_cast<const int4*>(src + i));
-      acc.x = __fadd_rn(acc.x, __int_as_float(raw.x));
-      acc.y = __fadd_rn(acc.y, __int_as_float(raw.y));
-      acc.z = __fadd_rn(acc.z, __int_as_float(raw.z));
-      acc.w = __fadd_rn(acc.w, __int_as_float(raw.w));
+      int4 raw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        raw[u] = (i0 + u * 256 < n4) ? ld_nc_v4(s_src[q] + i0 + u * 256) : make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u].x = __fadd_rn(acc[u].x, __int_as_float(raw[u].x));
+        acc[u].y = __fadd_rn(acc[u].y, __int_as_float(raw[u].y));
+        acc[u].z = __fadd_rn(acc[u].z, __int_as_float(raw[u].z));
+        acc[u].w = __fadd_rn(acc[u].w, __int_as_float(raw[u].w));
+      }
     }
-    dst[i] = acc;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * 256 < n4) dst[i0 + u * 256] = acc[u];
   }
 }
 
@@ -990,8 +1063,24 @@ int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int6
     return kErrDimension;
   }
   if (n_copies <= 0) return kOk;
-  dim3 grid(static_cast<unsigned>((slot_bytes + kCollChunk - 1) / kCollChunk), n_copies);
-  spag_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, param_off, slot_bytes, copies);
+  static const int impl = [] {
+    const char* v = getenv("FSSDP_SPAG_IMPL");
+    return (v && strcmp(v, "ldg") == 0) ? 0 : 1;  // default: TMA-staged bulk copies
+  }();
+  if (impl == 1) {
+    int64_t chunk = slot_bytes * n_copies / (2 * static_cast<int64_t>(num_sms()));
+    chunk = (chunk + kTmaSub - 1) / kTmaSub * kTmaSub;
+    if (chunk < 4 * kTmaSub) chunk = 4 * kTmaSub;
+    if (chunk > (1 << 20)) chunk = 1 << 20;
+    dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
+    spag_tma_kernel<<<grid, 32, 0, as_stream(stream)>>>(peer_bases, rank, param_off, slot_bytes,
+                                                        copies, chunk);
+    return launch_status();
+  }
+  const int64_t chunk = coll_chunk_bytes(slot_bytes * n_copies, num_sms());
+  dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
+  spag_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, param_off, slot_bytes, copies,
+                                                   chunk);
   return launch_status();
 }
 
@@ -1002,9 +1091,10 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
     return kErrDimension;
   }
   if (n_jobs <= 0) return kOk;
-  dim3 grid(static_cast<unsigned>((slot_elems * 4 + kCollChunk - 1) / kCollChunk), n_jobs);
+  const int64_t chunk = coll_chunk_bytes(slot_elems * 4 * n_jobs, num_sms());
+  dim3 grid(static_cast<unsigned>((slot_elems * 4 + chunk - 1) / chunk), n_jobs);
   sprs_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, slot_elems, jobs,
-                                                   srcs);
+                                                   srcs, chunk);
   return launch_status();
 }
 

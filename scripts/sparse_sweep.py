@@ -1,0 +1,116 @@
+"""SparseAllGather / SparseReduceScatter bandwidth sweep (BASELINE.json config 5).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/sparse_sweep.py [--quick]
+
+E = N experts, even single-owner partition; the post-placement adds expert e to devices
+(e+1 .. e+r-1) mod N (balanced ring: every GPU pulls (r-1)·S in SpAG and its owner pulls
+(r-1)·S_grad in SpRS).  A "hot" variant materializes expert 0 on r devices only.  Times are
+CUDA events around the kernel, max over ranks; GB/s = per-GPU inbound bytes / time
+(SpAG) and the reference's bottleneck bytes / time (costmodel.py:75-84).  SpRS reduces
+fp32 gradients (S_grad = 2·S).  Prints one JSON line per case on rank 0.
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2502_02581_b200 as F  # noqa: E402
+from paper_2502_02581_b200 import _native as N  # noqa: E402
+from paper_2502_02581_b200.comm import HeapLayout, PeerGroup  # noqa: E402
+from paper_2502_02581_b200.plan_tables import NativeTables  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--iters", type=int, default=10)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    sizes_mb = [1, 4, 16, 64, 256] if args.quick else [1, 2, 4, 8, 16, 32, 64, 128, 256]
+    smax = max(sizes_mb) << 20
+    slots = world  # owned slot + up to world-1 replicas
+    layout = HeapLayout()
+    layout.add("params", slots * smax)
+    layout.add("grads", slots * 2 * smax)
+    group = PeerGroup(layout, rank, world, dev, "dist")
+    poff, goff = layout.offset("params"), layout.offset("grads")
+    heap = group.local
+    heap.tensor(poff, (slots * smax // 2,), torch.bfloat16).normal_()
+    heap.tensor(goff, (slots * smax // 2,), torch.float32).normal_()
+    topo = F.ClusterTopology.for_nvswitch(world)
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    pb = C.c_void_p(group.peer_bases.data_ptr())
+    E = world
+    base = F.make_even_partition(E, topo)
+    for variant in ("ring", "hot"):
+        for r in range(2, world + 1):
+            if variant == "ring":
+                extra = [(e, (e + i) % world) for e in range(E) for i in range(1, r)]
+            else:
+                extra = [(0, i) for i in range(1, r)]
+            post = base.union(extra)
+            owner = base.owners()
+            route = np.zeros((world, E, world), dtype=np.int64)
+            for mb in sizes_mb:
+                S = mb << 20
+                tab = NativeTables(rank, owner, post.mask, route, 256, 256)
+                blob = torch.from_numpy(tab.blob[:tab.nbytes].copy()).to(dev)
+                spag_t = C.c_void_p(blob.data_ptr() + tab.offsets["spag"])
+                jobs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_jobs"])
+                srcs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_srcs"])
+                res = {}
+                for kind in ("spag", "sprs"):
+                    times = []
+                    for it in range(args.iters + 2):
+                        dist.barrier()
+                        torch.cuda.synchronize()
+                        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+                        s.record()
+                        if kind == "spag" and tab.n_spag:
+                            N.call("fssdp_spag", pb, rank, poff, S, spag_t, tab.n_spag, sp)
+                        if kind == "sprs" and tab.n_sprs_jobs:
+                            N.call("fssdp_sprs", pb, rank, goff, S // 2, jobs_t, tab.n_sprs_jobs,
+                                   srcs_t, sp)
+                        e.record()
+                        torch.cuda.synchronize()
+                        if it >= 2:
+                            times.append(s.elapsed_time(e))
+                    t = torch.tensor([float(np.median(times))], device=dev, dtype=torch.float64)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    res[kind] = float(t.item())
+                tr, rep = F.spag_traffic(base, post, S)
+                inbound_spag = float(tr.data[:, rank].sum())
+                g = torch.tensor([inbound_spag], device=dev, dtype=torch.float64)
+                dist.all_reduce(g, op=dist.ReduceOp.MAX)
+                max_in = float(g.item())
+                if rank == 0:
+                    line = {
+                        "n_gpus": world, "variant": variant, "replicas": r, "expert_mib": mb,
+                        "spag_ms": res["spag"], "sprs_ms": res["sprs"],
+                        "spag_bottleneck_bytes": rep.bottleneck_bytes,
+                        "spag_gbs_bottleneck": rep.bottleneck_bytes / (res["spag"] * 1e-3) / 1e9,
+                        "spag_gbs_inbound_max": max_in / (res["spag"] * 1e-3) / 1e9,
+                        "sprs_gbs_bottleneck_fp32": 2 * rep.bottleneck_bytes / (res["sprs"] * 1e-3) / 1e9,
+                        "nvlink_peer_gbs_ref": 770.0,
+                    }
+                    print("SWEEP " + json.dumps(line), flush=True)
+    dist.barrier()
+    group.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

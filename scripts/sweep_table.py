@@ -1,0 +1,11 @@
+"""Pretty-print SWEEP lines from scripts/sparse_sweep.py output."""
+import json
+import sys
+
+print(f"{'N':>2} {'variant':7} {'r':>2} {'MiB':>4} {'spag_ms':>8} {'spag_GB/s':>9} {'sprs_ms':>8} {'sprs_GB/s(fp32)':>15}")
+for line in open(sys.argv[1]):
+    if not line.startswith("SWEEP "):
+        continue
+    d = json.loads(line[6:])
+    print(f"{d['n_gpus']:>2} {d['variant']:7} {d['replicas']:>2} {d['expert_mib']:>4} {d['spag_ms']:8.3f} "
+          f"{d['spag_gbs_bottleneck']:9.0f} {d['sprs_ms']:8.3f} {d['sprs_gbs_bottleneck_fp32']:15.0f}")
