@@ -6,9 +6,9 @@
 
 Workload (configs[1], "cfg2"): a GPT-MoE layer — 16 experts, top-2, d_model 1024,
 d_ff 4096 (GeLU), 16384 tokens per GPU, bf16 — under seeded Zipf(1.2)-skewed gate
-loads, FSSDP policy (t=4 replicas budget, m=2 slots, calibration on).  A step is one
-FSSDP layer fwd+bwd: gate, counts all-gather, host plan (bit-exact moesim planner),
-SpAG, token dispatch, grouped FFN (tcgen05), combine; backward A2A, dgrad/wgrad,
+loads, FSSDP policy (t=8 replicable experts, m=4 replica slots, calibration on).  A step
+is one FSSDP layer fwd+bwd: early SpAG of the history-based candidate (side stream), gate,
+counts all-gather, host plan (bit-exact moesim planner), SpAG of the rest, token dispatch, grouped FFN (tcgen05), combine; backward A2A, dgrad/wgrad,
 dX combine + gate backward, SpRS.  Weak scaling: tokens per GPU are fixed.
 
 Prints ONE JSON line (rank 0).  `value` = all ranks' tokens / max-over-ranks device
@@ -34,7 +34,9 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "MoE fwd+bwd tokens/s at 1/2/4/8 B200; sparse AG/RS GB/s vs NVLink peak"
 CFG2 = dict(num_experts=16, top_k=2, d_model=1024, d_ff=4096, tokens_per_gpu=16384)
-POLICY = dict(overlap_override=4, capacity_override=2, calibration=True, rematerialize=False,
+# FSSDP knobs (engine.py:88-121): t = 8 replicable experts, m = 4 replica slots per GPU —
+# chosen offline with the bit-exact planner for the lowest max/mean device load at N = 4/8.
+POLICY = dict(overlap_override=8, capacity_override=4, calibration=True, rematerialize=False,
               reshard_interval=0)
 ZIPF_S = 1.2
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -77,28 +79,42 @@ class ClockSampler:
         self.max_mhz = None
         self.err = None
 
+    def _sample(self):
+        nv = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        self.samples.append((sm, reasons))
+
     def _run(self):
         try:
-            import pynvml as nv
-
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.idx)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, reasons))
-                self._stop.wait(0.01)
-        except Exception as exc:  # pragma: no cover - NVML missing
+            while not self._stop.wait(0.01):
+                self._sample()
+        except Exception as exc:  # pragma: no cover - NVML failure mid-run
             self.err = repr(exc)
 
     def __enter__(self):
-        self._t.start()
+        try:  # NVML opened and sampled once synchronously: every region gets >= 2 samples
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._sample()
+            self._t.start()
+        except Exception as exc:  # pragma: no cover - NVML missing
+            self.err = repr(exc)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t.is_alive():
+            self._t.join(timeout=10)
+        if self.err is None and self.max_mhz is not None:
+            try:
+                self._sample()
+            except Exception as exc:  # pragma: no cover
+                self.err = repr(exc)
 
     def summary(self):
         if not self.samples:
@@ -271,6 +287,18 @@ def run_ours(args):
     launches = NAT.launch_count
     ms = start.elapsed_time(end) / args.steps
     timers = layer.timers
+    if os.environ.get("FSSDP_TIMELINE"):
+        # last timed step's kernels as (start, end) ms from the step's first kernel, per rank
+        last = []
+        for key, ev in timers.items():
+            if key == "host_plan_s":
+                continue
+            per = len(ev) // args.steps
+            last += [(key, s_, e_) for s_, e_ in ev[len(ev) - per:]]
+        s0 = min(last, key=lambda t: start.elapsed_time(t[1]))[1]
+        rows = sorted((round(s0.elapsed_time(s_), 4), round(s0.elapsed_time(e_), 4), key)
+                      for key, s_, e_ in last)
+        print("TIMELINE", rank, json.dumps(rows), file=sys.stderr, flush=True)
     layer.timers = None
     ms_max = ms
     if world > 1:
@@ -297,10 +325,12 @@ def run_ours(args):
     gemm_launches = sum(len(ev) for key, ev in timers.items() if key.startswith("gemm."))
     rows_rank = float(dec.route[:, :, rank].sum())
     flops_rank = 3 * 2 * rows_rank * 2 * d * f   # fwd + dgrad + wgrad
-    spag_ms = sum(s.elapsed_time(e) for s, e in timers.get("spag", [])) / args.steps
+    spag_ms = sum(s.elapsed_time(e) for key in ("spag", "spag_pre")
+                  for s, e in timers.get(key, [])) / args.steps
     sprs_ms = sum(s.elapsed_time(e) for s, e in timers.get("sprs", [])) / args.steps
     t = layer.tables
-    spag_in = float(t.n_spag * layer.g.slot_param_bytes)
+    n_pre = layer.pre_tables.n_spag if layer.pre_tables is not None else 0
+    spag_in = float((t.n_spag + n_pre) * layer.g.slot_param_bytes)
     sprs_in = float(sum(int(c) - 1 for _, _, c in t.sprs_jobs) * layer.g.slot_grad_elems * 4)
     host_ms = 1e3 * sum(timers.get("host_plan_s", [])) / args.steps
     allr = gather([gemm_ms, flops_rank, spag_ms, sprs_ms, spag_in, sprs_in, host_ms, ms])
@@ -318,7 +348,11 @@ def run_ours(args):
                 "host_plan_ms_per_step": float(allr[:, 6].max())}
     # per-phase device time (CUDA events around every kernel of the timed steps), max over ranks
     keys = sorted(k for k in timers if k != "host_plan_s")
-    phase_ms = [sum(s.elapsed_time(e) for s, e in timers[k]) / args.steps for k in keys]
+    if world > 1:  # ranks may launch different phases (e.g. no SpAG copies): use the union
+        allk = [None] * world
+        torch.distributed.all_gather_object(allk, keys)
+        keys = sorted(set().union(*allk))
+    phase_ms = [sum(s.elapsed_time(e) for s, e in timers.get(k, [])) / args.steps for k in keys]
     allp = gather(phase_ms) if keys else None
     breakdown = {k: round(float(allp[:, i].max()), 4) for i, k in enumerate(keys)} if keys else {}
     breakdown["host_plan"] = round(float(allr[:, 6].max()), 4)
@@ -332,6 +366,7 @@ def run_ours(args):
             "replicas": len(dec.target.entries) - E,
             "spag_total_bytes": rep.total_interdevice_bytes,
             "spag_bottleneck_bytes": rep.bottleneck_bytes,
+            "spag_early_copies_rank0": n_pre, "spag_late_copies_rank0": t.n_spag,
             "spag_ms_max_rank": spag_max, "sprs_ms_max_rank": sprs_max,
             "spag_bottleneck_gbs": gbs(rep.bottleneck_bytes, spag_max),
             "spag_inbound_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 4], allr[:, 2])],

@@ -166,9 +166,15 @@ int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, con
 /* Device plan tables of one rank for one layer-iteration, derived from the global plan
  * (base owner[E], target mask [E*D], route[D*E*D]) — every rank derives its own, nothing
  * is exchanged.  Packed into one blob of 16-byte-aligned sections whose offsets
- * fssdp_tables_layout returns; header_out[25] = {n_slots, n_owned, recv_rows, n_zero,
- * n_spag, n_sprs_jobs, n_sprs_srcs, then per GEMM (fwd1, fwd2, dgrad2, dgrad1, wgrad1,
- * wgrad2): num_groups, n_tiles, total_tiles}.  Layout semantics: plan_tables.py. */
+ * fssdp_tables_layout returns; header_out[FSSDP_TAB_HEADER_INTS] = {n_slots, n_owned,
+ * recv_rows, n_zero, n_spag, n_sprs_jobs, n_sprs_srcs, then per GEMM (fwd1, fwd2, dgrad2,
+ * dgrad1, wgrad1, wgrad2): num_groups, n_tiles, total_tiles, then n_shared,
+ * wgrad1_shared_tiles, wgrad2_shared_tiles}.  The wgrad group arrays list the n_shared
+ * slots whose expert has other holders (the SpRS inputs) first, as a separately launchable
+ * prefix; the remaining groups restart tile_start at 0, so a wgrad runs as two launches
+ * (shared prefix, then the rest) and SpRS can start between them.
+ * Layout semantics: plan_tables.py. */
+#define FSSDP_TAB_HEADER_INTS 28
 #define FSSDP_TAB_ROUTE_CUM 0   /* int32 [E][D+1] */
 #define FSSDP_TAB_RECV_BASE 1   /* int32 [E][D]   */
 #define FSSDP_TAB_ZERO_ROWS 2   /* int32 [<=E][2] {row, count} */
@@ -185,8 +191,16 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
                         int64_t* total_bytes_out);
 int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_experts,
                             const int32_t* base_owner, const uint8_t* target_mask,
-                            const int64_t* route, int32_t d_model, int32_t d_ff, uint8_t* blob,
-                            int64_t blob_bytes, int32_t* header_out);
+                            const uint8_t* pre_mask, const int64_t* route, int32_t d_model,
+                            int32_t d_ff, uint8_t* blob, int64_t blob_bytes, int32_t* header_out);
+
+/* The estimate-based, adoption-gated materialization alone (engine.py:497-501 with
+ * _adopt_materialization engine.py:406-429): depends only on the load history, so its
+ * SparseAllGather can start before the gate.  fssdp_plan_layer's final target is either
+ * a superset (calibration only extends) or the bare base partition (fallback). */
+int fssdp_plan_candidate(int32_t num_experts, const int32_t* base_owner, const double* est,
+                         const fssdp_topology* topo, const fssdp_layer_knobs* knobs,
+                         uint8_t* target_out, int32_t* adopted_out);
 
 /* ================================================================== device data plane */
 

@@ -801,52 +801,56 @@ __global__ void __launch_bounds__(32)
   bulk_wait<0>();
 }
 
+// Persistent over (chunk, job) units so the launcher can bound the SMs it occupies: SpRS
+// runs beside the backward GEMMs (side stream) and must not crowd them out.
 __global__ void __launch_bounds__(256)
     sprs_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
                 int64_t slot_elems, const int32_t* __restrict__ jobs,
-                const int32_t* __restrict__ srcs, int64_t chunk) {
+                const int32_t* __restrict__ srcs, int64_t chunk, int n_chunks, int n_units) {
   __shared__ const int4* s_src[kMaxWorld];
-  const int job = blockIdx.y;
-  const int64_t dst_slot = jobs[3 * job];
-  const int src_begin = jobs[3 * job + 1];
-  const int src_count = jobs[3 * job + 2];
   const int64_t chunk_elems = chunk / 4;
-  const int64_t begin = static_cast<int64_t>(blockIdx.x) * chunk_elems;
-  if (begin >= slot_elems) return;
-  if (threadIdx.x < src_count) {
-    const int r = srcs[2 * (src_begin + threadIdx.x)];
-    const int64_t sl = srcs[2 * (src_begin + threadIdx.x) + 1];
-    s_src[threadIdx.x] = reinterpret_cast<const int4*>(
-        reinterpret_cast<const float*>(peer_bases[r] + grad_off) + sl * slot_elems + begin);
-  }
-  __syncthreads();
-  const int64_t n = imin64(chunk_elems, slot_elems - begin);
-  const int n4 = static_cast<int>(n / 4);
-  float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(peer_bases[rank] + grad_off) +
-                                          dst_slot * slot_elems + begin);
-  // U float4 per thread per pass: U * src_count 128-bit loads in flight; each element is
-  // still summed over the holders in ascending-rank order (bit-exact vs the oracle).
-  constexpr int U = 4;
-  for (int i0 = threadIdx.x; i0 < n4; i0 += U * 256) {
-    float4 acc[U];
+  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    const int job = unit / n_chunks;
+    const int64_t dst_slot = jobs[3 * job];
+    const int src_begin = jobs[3 * job + 1];
+    const int src_count = jobs[3 * job + 2];
+    const int64_t begin = static_cast<int64_t>(unit % n_chunks) * chunk_elems;
+    __syncthreads();  // previous unit's readers of s_src are done
+    if (threadIdx.x < src_count) {
+      const int r = srcs[2 * (src_begin + threadIdx.x)];
+      const int64_t sl = srcs[2 * (src_begin + threadIdx.x) + 1];
+      s_src[threadIdx.x] = reinterpret_cast<const int4*>(
+          reinterpret_cast<const float*>(peer_bases[r] + grad_off) + sl * slot_elems + begin);
+    }
+    __syncthreads();
+    const int64_t n = imin64(chunk_elems, slot_elems - begin);
+    const int n4 = static_cast<int>(n / 4);
+    float4* dst = reinterpret_cast<float4*>(
+        reinterpret_cast<float*>(peer_bases[rank] + grad_off) + dst_slot * slot_elems + begin);
+    // U float4 per thread per pass: U * src_count 128-bit loads in flight; each element is
+    // still summed over the holders in ascending-rank order (bit-exact vs the oracle).
+    constexpr int U = 4;
+    for (int i0 = threadIdx.x; i0 < n4; i0 += U * 256) {
+      float4 acc[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int q = 0; q < src_count; ++q) {
-      int4 raw[U];
+      for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < src_count; ++q) {
+        int4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          raw[u] = (i0 + u * 256 < n4) ? ld_nc_v4(s_src[q] + i0 + u * 256) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          acc[u].x = __fadd_rn(acc[u].x, __int_as_float(raw[u].x));
+          acc[u].y = __fadd_rn(acc[u].y, __int_as_float(raw[u].y));
+          acc[u].z = __fadd_rn(acc[u].z, __int_as_float(raw[u].z));
+          acc[u].w = __fadd_rn(acc[u].w, __int_as_float(raw[u].w));
+        }
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        raw[u] = (i0 + u * 256 < n4) ? ld_nc_v4(s_src[q] + i0 + u * 256) : make_int4(0, 0, 0, 0);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        acc[u].x = __fadd_rn(acc[u].x, __int_as_float(raw[u].x));
-        acc[u].y = __fadd_rn(acc[u].y, __int_as_float(raw[u].y));
-        acc[u].z = __fadd_rn(acc[u].z, __int_as_float(raw[u].z));
-        acc[u].w = __fadd_rn(acc[u].w, __int_as_float(raw[u].w));
-      }
+        if (i0 + u * 256 < n4) dst[i0 + u * 256] = acc[u];
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i0 + u * 256 < n4) dst[i0 + u * 256] = acc[u];
   }
 }
 
@@ -1091,10 +1095,18 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
     return kErrDimension;
   }
   if (n_jobs <= 0) return kOk;
+  // CTA budget (FSSDP_SPRS_CTAS, default one per SM): SpRS runs beside the backward GEMMs
+  // and a full 4-per-SM grid slows them more than it speeds the reduction (measured, N=4)
+  static const int budget = [] {
+    const char* v = getenv("FSSDP_SPRS_CTAS");
+    return v ? atoi(v) : num_sms();
+  }();
   const int64_t chunk = coll_chunk_bytes(slot_elems * 4 * n_jobs, num_sms());
-  dim3 grid(static_cast<unsigned>((slot_elems * 4 + chunk - 1) / chunk), n_jobs);
-  sprs_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, slot_elems, jobs,
-                                                   srcs, chunk);
+  const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
+  const int n_units = n_chunks * n_jobs;
+  const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
+  sprs_kernel<<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, slot_elems, jobs,
+                                                   srcs, chunk, n_chunks, n_units);
   return launch_status();
 }
 

@@ -313,44 +313,43 @@ bool build_dispatch(const int64_t* counts, const Placement& p, const Topo& t, Ro
   out->D = D;
   out->E = E;
   out->r.assign(static_cast<size_t>(D) * E * D, 0);
-  std::vector<int64_t> assigned(D, 0);
-  std::vector<int> targets;
-  targets.reserve(D);
+  // scratch reused across (source, expert) cells: this runs several times per plan on the
+  // planning critical path
+  std::vector<int64_t> assigned(D, 0), share(D);
+  std::vector<int> targets(D), order(D);
   for (int src = 0; src < D; ++src) {
     const int node = t.node_of(src);
     for (int e = 0; e < E; ++e) {
       const int64_t n = counts[static_cast<size_t>(src) * E + e];
       if (n == 0) continue;
-      if (p.holders_count(e) == 0) {
-        err->code = FSSDP_ERR_ORPHAN_EXPERT;
-        err->msg = "expert " + std::to_string(e) + " has tokens but is materialized nowhere";
-        return false;
-      }
       if (p.has(e, src)) {
         out->at(src, e, src) += n;
         assigned[src] += n;
         continue;
       }
-      targets.clear();
+      int k = 0;
       for (int d = 0; d < D; ++d)
-        if (p.has(e, d) && t.node_of(d) == node) targets.push_back(d);
-      if (targets.empty())
+        if (p.has(e, d) && t.node_of(d) == node) targets[k++] = d;
+      if (k == 0)
         for (int d = 0; d < D; ++d)
-          if (p.has(e, d)) targets.push_back(d);
-      const int64_t k = static_cast<int64_t>(targets.size());
+          if (p.has(e, d)) targets[k++] = d;
+      if (k == 0) {
+        err->code = FSSDP_ERR_ORPHAN_EXPERT;
+        err->msg = "expert " + std::to_string(e) + " has tokens but is materialized nowhere";
+        return false;
+      }
       const int64_t base = n / k, rem = n % k;
-      std::vector<int64_t> share(targets.size(), base);
+      for (int i = 0; i < k; ++i) share[i] = base;
       if (rem) {
-        std::vector<int> order(targets.size());
-        for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
-        std::sort(order.begin(), order.end(), [&](int a, int b) {
+        for (int i = 0; i < k; ++i) order[i] = i;
+        std::sort(order.begin(), order.begin() + k, [&](int a, int b) {
           const int da = targets[a], db = targets[b];
           if (assigned[da] != assigned[db]) return assigned[da] < assigned[db];
           return da < db;
         });
         for (int64_t i = 0; i < rem; ++i) share[order[i]] += 1;
       }
-      for (size_t i = 0; i < targets.size(); ++i) {
+      for (int i = 0; i < k; ++i) {
         out->at(src, e, targets[i]) += share[i];
         assigned[targets[i]] += share[i];
       }
@@ -664,6 +663,83 @@ int fail(const Err& e) {
   return e.code;
 }
 
+// Estimate-based candidate + adoption gate (engine.py:497-501, _adopt_materialization
+// engine.py:406-429).  Depends only on the load history, so it is known before the gate.
+bool adopted_candidate_uncached(const Placement& base, const double* est, const Topo& t,
+                       const fssdp_layer_knobs* knobs, Placement* target, int* adopted, Err* err) {
+  const int D = base.D, E = base.C;
+  *target = base;
+  *adopted = 0;
+  Placement cand = extend_placement(base, column_sums(est, D, E), knobs->t, knobs->m, t);
+  if (cand == base) return true;
+  std::vector<int64_t> tokens(static_cast<size_t>(D) * E);
+  for (size_t i = 0; i < tokens.size(); ++i) {
+    double r = nearbyint(est[i]);  // np.rint: half to even
+    tokens[i] = r > 0 ? static_cast<int64_t>(r) : 0;
+  }
+  double before, after;
+  if (!estimate_moe_latency(base, tokens.data(), t, knobs->token_bytes,
+                            knobs->per_token_expert_time, &before, err) ||
+      !estimate_moe_latency(cand, tokens.data(), t, knobs->token_bytes,
+                            knobs->per_token_expert_time, &after, err))
+    return false;
+  std::vector<double> mat;
+  if (!spag_traffic(base, cand, knobs->expert_bytes, &mat, nullptr, err)) return false;
+  const double s_lat = collective_latency(mat, D, t);
+  if (!sprs_traffic(cand, base, knobs->expert_bytes, &mat, nullptr, err)) return false;
+  const double r_lat = collective_latency(mat, D, t);
+  const double remat = knobs->rematerialize ? s_lat : 0.0;
+  if (after + s_lat + r_lat + remat < before) {
+    *target = cand;
+    *adopted = 1;
+  }
+  return true;
+}
+
+// The candidate is computed twice per layer-iteration with identical inputs (early SpAG
+// before the gate, then fssdp_plan_layer after it): memoize the last few by exact inputs.
+struct CandidateMemo {
+  std::vector<uint8_t> key;
+  Placement target{0, 1};
+  int adopted = 0;
+};
+
+bool adopted_candidate(const Placement& base, const double* est, const Topo& t,
+                       const fssdp_layer_knobs* knobs, Placement* target, int* adopted, Err* err) {
+  static thread_local std::vector<CandidateMemo> memo;
+  static thread_local size_t next = 0;
+  // key: every input, as exact bytes
+  std::vector<uint8_t> key;
+  auto put = [&key](const void* p, size_t n) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    key.insert(key.end(), b, b + n);
+  };
+  const size_t est_bytes = static_cast<size_t>(base.C) * base.D * sizeof(double);
+  key.reserve(6 * 8 + 7 * 8 + 8 + base.m.size() + est_bytes);
+  const int64_t ints[6] = {base.C, base.D, t.nodes, t.dpn, knobs->t, knobs->m};
+  const double dbls[7] = {t.intra, t.inter, t.alpha, knobs->expert_bytes, knobs->token_bytes,
+                          knobs->attn_fwd_time, knobs->per_token_expert_time};
+  const int32_t flags[2] = {knobs->calibration, knobs->rematerialize};
+  put(ints, sizeof(ints));
+  put(dbls, sizeof(dbls));
+  put(flags, sizeof(flags));
+  put(base.m.data(), base.m.size());
+  put(est, est_bytes);
+  for (const CandidateMemo& c : memo)
+    if (c.key == key) {
+      *target = c.target;
+      *adopted = c.adopted;
+      return true;
+    }
+  if (!adopted_candidate_uncached(base, est, t, knobs, target, adopted, err)) return false;
+  if (memo.size() < 16) memo.emplace_back();
+  CandidateMemo& slot = memo[next++ % memo.size()];
+  slot.key = std::move(key);
+  slot.target = *target;
+  slot.adopted = *adopted;
+  return true;
+}
+
 void copy_mask(const Placement& p, uint8_t* out) { memcpy(out, p.m.data(), p.m.size()); }
 
 }  // namespace
@@ -867,6 +943,25 @@ int fssdp_estimate_loads(int32_t n, int32_t rows, int32_t cols, const double* hi
   return FSSDP_OK;
 }
 
+int fssdp_plan_candidate(int32_t E, const int32_t* base_owner, const double* est,
+                         const fssdp_topology* topo, const fssdp_layer_knobs* knobs,
+                         uint8_t* target_out, int32_t* adopted_out) {
+  if (int rc = check_topo(topo)) return rc;
+  const Topo t = to_topo(topo);
+  const int D = t.devices();
+  Placement base(E, D);
+  for (int e = 0; e < E; ++e) base.set(e, base_owner[e]);
+  Placement target = base;
+  int adopted = 0;
+  Err err;
+  if (est != nullptr && knobs->t > 0 && knobs->m > 0 &&
+      !adopted_candidate(base, est, t, knobs, &target, &adopted, &err))
+    return fail(err);
+  copy_mask(target, target_out);
+  *adopted_out = adopted;
+  return FSSDP_OK;
+}
+
 int fssdp_plan_layer(int32_t E, const int32_t* base_owner, const double* est,
                      const int64_t* actual, const fssdp_topology* topo,
                      const fssdp_layer_knobs* knobs, uint8_t* target_out, int32_t* added_out,
@@ -892,30 +987,7 @@ int fssdp_plan_layer(int32_t E, const int32_t* base_owner, const double* est,
   const bool degenerate = knobs->t <= 0 || knobs->m <= 0;
   if (!degenerate) {
     if (est != nullptr) {  // engine.py:497-501
-      Placement cand = extend_placement(base, column_sums(est, D, E), knobs->t, knobs->m, t);
-      if (!(cand == base)) {
-        // _adopt_materialization (engine.py:406-429)
-        std::vector<int64_t> tokens(static_cast<size_t>(D) * E);
-        for (size_t i = 0; i < tokens.size(); ++i) {
-          double r = nearbyint(est[i]);  // np.rint: half to even
-          tokens[i] = r > 0 ? static_cast<int64_t>(r) : 0;
-        }
-        double before, after;
-        if (!estimate_moe_latency(base, tokens.data(), t, knobs->token_bytes,
-                                  knobs->per_token_expert_time, &before, &err) ||
-            !estimate_moe_latency(cand, tokens.data(), t, knobs->token_bytes,
-                                  knobs->per_token_expert_time, &after, &err))
-          return fail(err);
-        if (!spag_traffic(base, cand, knobs->expert_bytes, &mat, nullptr, &err)) return fail(err);
-        const double s_lat = collective_latency(mat, D, t);
-        if (!sprs_traffic(cand, base, knobs->expert_bytes, &mat, nullptr, &err)) return fail(err);
-        const double r_lat = collective_latency(mat, D, t);
-        const double remat = knobs->rematerialize ? s_lat : 0.0;
-        if (after + s_lat + r_lat + remat < before) {
-          target = cand;
-          adopted = 1;
-        }
-      }
+      if (!adopted_candidate(base, est, t, knobs, &target, &adopted, &err)) return fail(err);
     }
     if (!(target == base)) {  // engine.py:502-506
       if (!spag_traffic(base, target, knobs->expert_bytes, &mat, nullptr, &err)) return fail(err);
@@ -939,10 +1011,10 @@ int fssdp_plan_layer(int32_t E, const int32_t* base_owner, const double* est,
         accepted = 1;
       }
       if (!(target == base)) {
-        double kept, bare;
-        if (!estimate_moe_latency(target, actual, t, knobs->token_bytes,
-                                  knobs->per_token_expert_time, &kept, &err) ||
-            !estimate_moe_latency(base, actual, t, knobs->token_bytes,
+        // kept = estimate_moe_latency(target, actual): calibrate already priced exactly
+        // this placement on these counts (after if accepted, before otherwise)
+        double kept = out.accepted ? out.after : out.before, bare;
+        if (!estimate_moe_latency(base, actual, t, knobs->token_bytes,
                                   knobs->per_token_expert_time, &bare, &err))
           return fail(err);
         kept += calib_time;
@@ -1019,8 +1091,14 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
 }
 
 int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* base_owner,
-                            const uint8_t* target_mask, const int64_t* route, int32_t d_model,
-                            int32_t d_ff, uint8_t* blob, int64_t blob_bytes, int32_t* header_out) {
+                            const uint8_t* target_mask, const uint8_t* pre_mask,
+                            const int64_t* route, int32_t d_model, int32_t d_ff, uint8_t* blob,
+                            int64_t blob_bytes, int32_t* header_out) {
+  // pre_mask (nullable): replicas already fetched by the early, estimate-based SpAG.  They
+  // take the first replica slots (ascending expert id) and get no SpAG copy here.
+  auto pre = [&](int e, int d) {
+    return pre_mask != nullptr && pre_mask[static_cast<int64_t>(e) * D + d] != 0;
+  };
   int64_t off[FSSDP_TAB_NSECTIONS], total;
   fssdp_tables_layout(E, D, off, &total);
   if (blob_bytes < total || rank < 0 || rank >= D || d_model % 256 || d_ff % 256) {
@@ -1035,12 +1113,14 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   for (int d = 0; d < D; ++d) {
     for (int e = 0; e < E; ++e)
       if (base_owner[e] == d) slot_expert[d].push_back(e);
-    for (int e = 0; e < E; ++e)
-      if (target_mask[static_cast<int64_t>(e) * D + d] && base_owner[e] != d)
-        slot_expert[d].push_back(e);
+    for (int pass = 0; pass < 2; ++pass)  // prefetched replicas first, then the rest
+      for (int e = 0; e < E; ++e)
+        if (target_mask[static_cast<int64_t>(e) * D + d] && base_owner[e] != d &&
+            pre(e, d) == (pass == 0))
+          slot_expert[d].push_back(e);
     for (size_t s = 0; s < slot_expert[d].size(); ++s) slot_of[d][slot_expert[d][s]] = static_cast<int>(s);
   }
-  // segments (padded to 128 rows) of every device
+  // segments (padded to 256 rows) of every device
   std::vector<std::vector<int64_t>> seg_start(D), seg_rows(D), seg_pad(D);
   for (int d = 0; d < D; ++d) {
     int64_t st = 0;
@@ -1088,6 +1168,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       ++n_owned;
       continue;
     }
+    if (pre(e, rank)) continue;  // fetched early
     spag[3 * n_spag] = o;
     spag[3 * n_spag + 1] = slot_of[o][e];
     spag[3 * n_spag + 2] = s;
@@ -1113,20 +1194,40 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
         ++n_srcs;
       }
   }
-  // the six grouped-GEMM descriptor arrays (see plan_tables.gemm_groups)
+  // the six grouped-GEMM descriptor arrays (see plan_tables.gemm_groups); the wgrads list
+  // the slots shared with other holders first (their SpRS can start before the rest runs)
+  auto shared = [&](int s) {
+    const int e = slot_expert[rank][s];
+    int holders = 0;
+    for (int dd = 0; dd < D; ++dd) holders += target_mask[static_cast<int64_t>(e) * D + dd] != 0;
+    return holders > 1;
+  };
+  std::vector<int> wg_order;
+  for (int s = 0; s < n_slots; ++s)
+    if (shared(s)) wg_order.push_back(s);
+  const int n_shared = static_cast<int>(wg_order.size());
+  for (int s = 0; s < n_slots; ++s)
+    if (!shared(s)) wg_order.push_back(s);
   const int64_t d = d_model, f = d_ff;
   const int n_tiles[6] = {static_cast<int>(f / 256), static_cast<int>(d / 256),
                           static_cast<int>(f / 256), static_cast<int>(d / 256),
                           static_cast<int>(d / 256), static_cast<int>(f / 256)};
   int ints = 7;
+  int32_t shared_tiles[2] = {0, 0};
   for (int gi = 0; gi < 6; ++gi) {
     fssdp_gemm_group* g = reinterpret_cast<fssdp_gemm_group*>(blob + off[FSSDP_TAB_GEMM0 + gi]);
-    int32_t tile = 0;
-    for (int s = 0; s < n_slots; ++s) {
+    const bool wgrad = gi >= 4;
+    int32_t tile = 0, total = 0;
+    for (int i = 0; i < n_slots; ++i) {
+      const int s = wgrad ? wg_order[i] : i;
+      if (wgrad && i == n_shared) {  // the rest restarts at tile 0
+        shared_tiles[gi - 4] = tile;
+        tile = 0;
+      }
       const int32_t st = static_cast<int32_t>(seg_start[rank][s]);
       const int32_t mt = static_cast<int32_t>(seg_pad[rank][s] / 128);
       const int32_t kt = static_cast<int32_t>(seg_pad[rank][s] / 64);
-      fssdp_gemm_group& x = g[s];
+      fssdp_gemm_group& x = g[i];
       switch (gi) {
         case 0: x = {mt, 0, st, 0, static_cast<int32_t>(s * 2 * f), 0, static_cast<int32_t>(d / 64), 0, st * f}; break;
         case 1: x = {mt, 0, st, 0, static_cast<int32_t>(s * 2 * d), 0, static_cast<int32_t>(f / 64), 0, st * d}; break;
@@ -1137,11 +1238,16 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       }
       x.tile_start = tile;
       tile += x.m_tiles * n_tiles[gi];
+      total += x.m_tiles * n_tiles[gi];
     }
+    if (wgrad && n_shared == n_slots) shared_tiles[gi - 4] = tile;
     header_out[ints++] = n_slots;
     header_out[ints++] = n_tiles[gi];
-    header_out[ints++] = tile;
+    header_out[ints++] = total;
   }
+  header_out[25] = n_shared;
+  header_out[26] = shared_tiles[0];
+  header_out[27] = shared_tiles[1];
   int32_t* se = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SLOT_EXPERT]);
   int32_t* ss = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_START]);
   int32_t* sr = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_ROWS]);

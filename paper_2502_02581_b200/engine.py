@@ -151,6 +151,27 @@ class LayerDecision:
         return self.target == self.base
 
 
+class _PlanScratch:
+    """Persistent fssdp_plan_layer buffers of one layer with their addresses resolved once
+    (numpy's .ctypes.data costs microseconds per access on the planning critical path)."""
+
+    def __init__(self, E: int, D: int) -> None:
+        self.act = np.zeros((D, E), dtype=np.int64)
+        self.target = np.zeros((E, D), dtype=np.uint8)
+        self.added = np.zeros(D, dtype=np.int32)
+        self.route = np.zeros((D, E, D), dtype=np.int64)
+        self.dbl = np.zeros(4, dtype=np.float64)
+        self.flags = np.zeros(2, dtype=np.int32)
+        for k in ("act", "target", "added", "route", "dbl", "flags"):
+            setattr(self, "p_" + k, getattr(self, k).ctypes.data)
+        self._topo = None
+
+    def topo_ref(self, topo_c):
+        if self._topo is None or self._topo[0] is not topo_c:
+            self._topo = (topo_c, N.C.byref(topo_c))
+        return self._topo[1]
+
+
 _MOVE_MULTIPLIER = 7  # params + 6x optimizer state move with a re-sharded expert (engine.py:233)
 
 
@@ -197,9 +218,20 @@ class FssdpPlanner:
         return self._owners_cache[layer]
 
     def estimate(self, layer: int) -> Optional[np.ndarray]:
-        if not self.history[layer]:
+        """Window mean of the layer's history (cached until the history changes: the early
+        candidate and the plan of one iteration share it)."""
+        h = self.history[layer]
+        if not h:
             return None
-        return estimate_loads(self.history[layer], self.policy.window)
+        key = (len(h), h[-1], h[0])  # the arrays themselves (kept alive, compared by identity)
+        cache = self.__dict__.setdefault("_est_cache", {})
+        hit = cache.get(layer)
+        if hit is not None and hit[0][0] == key[0] and hit[0][1] is key[1] and hit[0][2] is key[2]:
+            return hit[1]
+        est = np.ascontiguousarray(estimate_loads(h, self.policy.window), dtype=np.float64)
+        est.flags.writeable = False
+        cache[layer] = (key, est, est.ctypes.data)
+        return est
 
     def _shard_score(self, plan: ShardPlan, profile: GlobalLoadProfile) -> tuple:
         """(max node load, max device load), numpy order (engine.py:431-442)."""
@@ -251,38 +283,59 @@ class FssdpPlanner:
                 self.shards = candidate
         return self.last_reshard_time
 
+    def _scratch(self, layer: int) -> "_PlanScratch":
+        sc = self.__dict__.setdefault("_scratches", {}).get(layer)
+        if sc is None:
+            base = self.shards.per_layer[layer]
+            sc = self._scratches[layer] = _PlanScratch(base.num_chunks, base.num_devices)
+        return sc
+
     def plan_layer(self, layer: int, actual) -> LayerDecision:
-        """Adoption gate, calibration, fallback, dispatch for one layer (engine.py:491-553)."""
+        """Adoption gate, calibration, fallback, dispatch for one layer (engine.py:491-553).
+
+        On the planning critical path (between the count all-gather and the dispatch): the
+        C++ call works on persistent buffers whose addresses are resolved once; the
+        decision holds copies.  `last_target_ptr` / `last_route_ptr` address the scratch
+        copies for an immediate NativeTables.from_pointers."""
         base = self.shards.per_layer[layer]
         E, D = base.num_chunks, base.num_devices
-        act = np.ascontiguousarray(np.asarray(actual, dtype=np.int64))
+        sc = self._scratch(layer)
+        act = np.asarray(actual)
         if act.shape != (D, E):
             raise TraceMismatchError(f"counts {act.shape} do not match {D} devices x {E} experts")
-        owner = self._owners(layer)
-        target = np.zeros((E, D), dtype=np.uint8)
-        added = np.zeros(D, dtype=np.int32)
-        route = np.zeros((D, E, D), dtype=np.int64)
-        dbl = np.zeros(4, dtype=np.float64)
-        flags = np.zeros(2, dtype=np.int32)
+        np.copyto(sc.act, act, casting="unsafe")
+        owner_ptr = self._owners_ptr(layer)
         if self.policy.kind == PolicyKind.EP:
-            knobs = N.LayerKnobs(0, 0, 0, 0, self._knobs.expert_bytes, self._knobs.token_bytes,
-                                 self._knobs.attn_fwd_time, self._knobs.per_token_expert_time)
+            knobs = self.__dict__.get("_ep_knobs")
+            if knobs is None:
+                knobs = self._ep_knobs = N.LayerKnobs(
+                    0, 0, 0, 0, self._knobs.expert_bytes, self._knobs.token_bytes,
+                    self._knobs.attn_fwd_time, self._knobs.per_token_expert_time)
             est_ptr = None
         else:
             knobs = self._knobs
-            est = self.estimate(layer)
-            est_ptr = None if est is None else np.ascontiguousarray(est, dtype=np.float64)
-        # raw addresses (.ctypes.data) — data_as() costs microseconds per argument
+            est_ptr = self._estimate_ptr(layer)
         N.check(N.LIB_RAW.fssdp_plan_layer(
-            E, owner.ctypes.data, None if est_ptr is None else est_ptr.ctypes.data,
-            act.ctypes.data, N.C.byref(self._topo_c), N.C.byref(knobs), target.ctypes.data,
-            added.ctypes.data, route.ctypes.data, dbl.ctypes.data, flags.ctypes.data),
-            "plan_layer")
-        return LayerDecision(base=base, target=ChunkPlacement.from_mask(target),
-                             added_per_device=tuple(int(a) for a in added), route=route,
-                             spag_latency=float(dbl[0]), sprs_latency=float(dbl[1]),
-                             remat_latency=float(dbl[2]), calib_time=float(dbl[3]),
-                             adopted=bool(flags[0]), calibrated=bool(flags[1]))
+            E, owner_ptr, est_ptr, sc.p_act, sc.topo_ref(self._topo_c), N.C.byref(knobs),
+            sc.p_target, sc.p_added, sc.p_route, sc.p_dbl, sc.p_flags), "plan_layer")
+        self.last_target_ptr, self.last_route_ptr = sc.p_target, sc.p_route
+        dbl, flags = sc.dbl.tolist(), sc.flags.tolist()
+        return LayerDecision(base=base, target=ChunkPlacement.from_mask(sc.target.copy(), copy=False),
+                             added_per_device=tuple(sc.added.tolist()), route=sc.route.copy(),
+                             spag_latency=dbl[0], sprs_latency=dbl[1], remat_latency=dbl[2],
+                             calib_time=dbl[3], adopted=bool(flags[0]), calibrated=bool(flags[1]))
+
+    def _owners_ptr(self, layer: int) -> int:
+        self._owners(layer)  # refreshes the cache for the current ShardPlan
+        if getattr(self, "_owners_ptrs_plan", None) is not self.shards:
+            self._owners_ptrs = [row.ctypes.data for row in self._owners_cache]
+            self._owners_ptrs_plan = self.shards
+        return self._owners_ptrs[layer]
+
+    def _estimate_ptr(self, layer: int):
+        if self.estimate(layer) is None:
+            return None
+        return self._est_cache[layer][2]
 
     def end_iteration(self, step: Sequence[np.ndarray]) -> None:
         """Push this iteration's counts into the history window (engine.py:353-356)."""
@@ -292,6 +345,31 @@ class FssdpPlanner:
         for l, counts in enumerate(step):
             self.history[l].append(np.asarray(counts, dtype=np.int64))
         self.iteration += 1
+
+    def candidate(self, layer: int) -> Optional[np.ndarray]:
+        """The estimate-based, adoption-gated target mask (E, D) of the coming iteration, or
+        None when it is the bare partition — known BEFORE the gate, so its SpAG can start
+        early (engine.py:497-501; calibration may only extend it, fallback drops it)."""
+        if self.policy.kind != PolicyKind.FSSDP:
+            return None
+        if self._step is None and self._reshard_pending():
+            return None  # the re-shard decision of this iteration comes first
+        est_ptr = self._estimate_ptr(layer)
+        if est_ptr is None:
+            return None
+        base = self.shards.per_layer[layer]
+        E, D = base.num_chunks, base.num_devices
+        target = np.zeros((E, D), dtype=np.uint8)
+        adopted = np.zeros(1, dtype=np.int32)
+        N.check(N.LIB_RAW.fssdp_plan_candidate(E, self._owners_ptr(layer), est_ptr,
+                                               N.C.byref(self._topo_c), N.C.byref(self._knobs),
+                                               target.ctypes.data, adopted.ctypes.data),
+                "plan_candidate")
+        return target if adopted[0] else None
+
+    def _reshard_pending(self) -> bool:
+        return (self.iteration > 0 and self.policy.reshard_interval > 0
+                and self.iteration % self.policy.reshard_interval == 0 and all(self.history))
 
     # -- layer-driven protocol (used by FssdpMoE) ---------------------------------
     def plan(self, layer: int, actual) -> LayerDecision:

@@ -29,9 +29,10 @@ from .errors import DimensionError, InternalError
 from .plan_tables import NativeTables
 
 WG_TILE = 256  # FSSDP_WG_TILE (include/fssdp.h)
+GROUP_BYTES = N.C.sizeof(N.GemmGroup)  # fssdp_gemm_group
 
 # barrier slots (flag pads) used by one layer; layer i uses base + 8*i
-BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_SPAG = range(7)
+BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_SPAG, BAR_SPRS = range(8)
 
 
 @dataclass(frozen=True)
@@ -113,6 +114,9 @@ class FssdpMoE:
         self.dyrecv = heap.tensor(self.off["dyrecv"], (R, d), torch.bfloat16)
         self.dxe = heap.tensor(self.off["dxe"], (R, d), torch.bfloat16)
         self.counts_table = heap.tensor(self.off["counts"], (self.world, E), torch.int32)
+        self.counts_host = torch.empty(self.world, E, dtype=torch.int32, pin_memory=True)
+        self.counts_host_np = self.counts_host.numpy()
+        self._counts_ev = torch.cuda.Event()
         # 2-D TMA views of the parameter region
         flat = self.params.view(-1)
         self.w1_view = flat.view(geom.slots * 2 * f, d)                  # W1 of slot s: rows s*2f..
@@ -141,7 +145,17 @@ class FssdpMoE:
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
         self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
         self.blob_host_np = self.blob_host.numpy()
+        self.blob_host_ptr = self.blob_host_np.ctypes.data
         self.blob_dev = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
+        # tables of the early (estimate-based) SpAG, staged separately from the final ones
+        self.pre_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
+        self.pre_host_np = self.pre_host.numpy()
+        self.pre_dev = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
+        self.pre_mask = None      # (E, D) replicas fetched early this iteration, or None
+        self.pre_mask_ptr = None
+        self.pre_tables = None
+        self._pre_done = None     # event on the side stream after the early SpAG
+        self._pre_staged = None   # event after the H2D of pre_host (before it is rewritten)
         self.decision = None
         self.tables = None
         self.T = 0
@@ -202,6 +216,63 @@ class FssdpMoE:
         return C.c_void_p(self.group.peer_bases.data_ptr())
 
     # ------------------------------------------------------------ forward phases
+    # Early SpAG: the estimate-based candidate (engine.py:497-501) depends only on the
+    # load history, so its replicas are pulled on a side stream while the gate, the
+    # count all-gather and the host planner run; the final plan (a superset after
+    # calibration, or the bare partition after fallback) then copies only the rest.
+    # Owned shards must not change between the end of backward and the next forward
+    # (peers read them early) — put a barrier after an optimizer step that updates them.
+    PREFETCH = True
+
+    def phase_prefetch(self) -> None:
+        self.pre_mask, self.pre_mask_ptr, self.pre_tables, self._pre_done = None, None, None, None
+        self._pre_launch = False
+        if not self.PREFETCH:
+            return
+        pre = self.planner.candidate(self.layer)
+        if pre is None:
+            return
+        if self._pre_staged is not None:
+            self._pre_staged.synchronize()  # last iteration's H2D of pre_host has landed
+        base_owner = self.planner._owners(self.layer)
+        E, D = pre.shape
+        tables = NativeTables(self.rank, base_owner, pre, np.zeros((D, E, D), dtype=np.int64),
+                              self.g.d_model, self.g.d_ff, out_bytes=self.pre_host_np)
+        if tables.n_slots > self.g.slots:
+            raise InternalError(f"early plan needs {tables.n_slots} slots > capacity {self.g.slots}")
+        self.pre_mask, self.pre_mask_ptr, self.pre_tables = pre, pre.ctypes.data, tables
+        if tables.n_spag == 0:
+            return
+        main = torch.cuda.current_stream(self.dev)
+        side = self._side_stream()
+        side.wait_stream(main)  # previous users of the replica slots are done
+        with torch.cuda.stream(side):
+            nb = tables.nbytes
+            self.pre_dev[:nb].copy_(self.pre_host[:nb], non_blocking=True)
+            self._pre_staged = torch.cuda.Event()
+            self._pre_staged.record(side)
+        self._pre_launch = True  # the copies themselves start after the count all-gather
+
+    def _launch_prefetch(self) -> None:
+        """Early SpAG on the side stream, ordered after the gate and the count all-gather:
+        it then runs in the host-planning gap instead of slowing the gate (measured)."""
+        if not getattr(self, "_pre_launch", False):
+            return
+        self._pre_launch = False
+        main = torch.cuda.current_stream(self.dev)
+        side = self._side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side)
+            self._pre_done = torch.cuda.Event()
+            self._pre_done.record(side)
+
+    def _spag_launch(self, key, blob_dev, tables, stream) -> None:
+        spag = C.c_void_p(blob_dev.data_ptr() + tables.offsets["spag"])
+        self._timed(key, lambda: N.call(
+            "fssdp_spag", self._pb(), self.rank, self.off["params"], self.g.slot_param_bytes,
+            spag, tables.n_spag, C.c_void_p(stream.cuda_stream)))
+
     def phase_gate(self, x: torch.Tensor) -> None:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.g.d_model:
             raise DimensionError(f"x must be [T, {self.g.d_model}] bf16, got {tuple(x.shape)} {x.dtype}")
@@ -222,9 +293,14 @@ class FssdpMoE:
         self._call("fssdp_route_scan_allgather", ops._ptr(self.tile_counts), n_tiles,
                self.g.num_experts, ops._ptr(self.tile_prefix), self._pb(), self.off["counts"],
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch), self._stream())
+        self._launch_prefetch()
 
     def phase_plan(self) -> None:
-        counts = self.counts_table.cpu().numpy().astype(np.int64)  # host sync point #1
+        # host sync point #1: pinned copy of the all-gathered counts
+        self.counts_host.copy_(self.counts_table, non_blocking=True)
+        self._counts_ev.record()
+        self._counts_ev.synchronize()
+        counts = self.counts_host_np
         t_host = time.perf_counter()
         self._plan_tables(counts)
         if self.timers is not None:
@@ -232,10 +308,21 @@ class FssdpMoE:
 
     def _plan_tables(self, counts) -> None:
         dec = self.planner.plan(self.layer, counts)
-        base_owner = dec.base.owners()
-        # native table build straight into the pinned staging buffer, one H2D copy
-        tables = NativeTables(self.rank, base_owner, dec.target.mask, dec.route, self.g.d_model,
-                              self.g.d_ff, out_bytes=self.blob_host_np)
+        target = dec.target.mask  # 0/1 uint8, like pre_mask
+        pre = self.pre_mask
+        if pre is not None and np.any(pre > target):
+            # the final plan dropped a prefetched replica: it can only be the bare
+            # partition (fallback), which has no replica slots — keep the layout check honest
+            if np.any(target > dec.base.mask):
+                raise InternalError("final placement is neither a superset of the early one "
+                                    "nor the bare partition")
+        # native table build from the planner's scratch copies of target/route, straight into
+        # the pinned staging buffer, one H2D copy
+        pl = self.planner
+        tables = NativeTables.from_pointers(
+            self.rank, target.shape[0], target.shape[1], pl._owners_ptr(self.layer),
+            pl.last_target_ptr, self.pre_mask_ptr, pl.last_route_ptr, self.g.d_model,
+            self.g.d_ff, self.blob_host_np, self.blob_host_ptr)
         if tables.n_slots > self.g.slots:
             raise InternalError(f"plan needs {tables.n_slots} slots > capacity {self.g.slots}")
         if tables.recv_rows > self.g.recv_cap:
@@ -249,13 +336,18 @@ class FssdpMoE:
         self.blob_dev[:nb].copy_(self.blob_host[:nb], non_blocking=True)  # boundary #2
         self.gemm = tables.gemm
 
-    def phase_spag(self) -> None:
-        n = self.tables.n_spag
-        if n == 0:
-            return
-        self._timed("spag", lambda: N.call(
-            "fssdp_spag", self._pb(), self.rank, self.off["params"], self.g.slot_param_bytes,
-            self._tab("spag"), n, self._stream()))
+    def phase_spag(self, refetch_early: bool = False) -> None:
+        """The SpAG of the final plan's replicas not fetched early; the main stream then
+        waits for the early SpAG.  `refetch_early` (rematerialization in backward) also
+        re-pulls the early replicas."""
+        main = torch.cuda.current_stream(self.dev)
+        if self._pre_done is not None:
+            main.wait_event(self._pre_done)
+            self._pre_done = None
+        if refetch_early and self.pre_tables is not None and self.pre_tables.n_spag:
+            self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, main)
+        if self.tables.n_spag:
+            self._spag_launch("spag", self.blob_dev, self.tables, main)
 
     def phase_dispatch(self) -> None:
         t = self.tables
@@ -292,14 +384,25 @@ class FssdpMoE:
         """One device entry point, CUDA-event-timed under its own name when profiling."""
         self._timed(name[6:], lambda: N.call(name, *args))
 
-    def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None):
+    def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None, part=None):
+        """One grouped GEMM of the plan; `part` "shared" / "rest" launches the wgrad prefix
+        of SpRS-input slots / the remaining groups (tables: wgrad_split)."""
         ng, n_tiles, total = self.gemm[name]
+        tab = self._tab(name)
+        if part is not None:
+            n_sh = self.tables.wgrad_split[0]
+            t_sh = self.tables.wgrad_split[1 if name == "wgrad1" else 2]
+            if part == "shared":
+                ng, total = n_sh, t_sh
+            else:
+                ng, total = ng - n_sh, total - t_sh
+                tab = C.c_void_p(tab.value + n_sh * GROUP_BYTES)
         if total == 0:
             return
         flags = (1 if self.N_FASTEST.get(name, False) else 0) | (2 if self.CTA_PAIR else 0)
         self._timed("gemm." + name, lambda: N.call(
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
-            ops._ptr(b), b.shape[1], b.shape[0], self._tab(name), ng, n_tiles, total, ops._ptr(c),
+            ops._ptr(b), b.shape[1], b.shape[0], tab, ng, n_tiles, total, ops._ptr(c),
             ops._ptr(c2), ops._ptr(aux), ldc, c.numel() // ldc, flags, self._stream()))
 
     def phase_experts_fwd(self) -> None:
@@ -337,13 +440,26 @@ class FssdpMoE:
                C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
 
     def phase_experts_bwd(self) -> None:
+        self.phase_bwd_shared()
+        self.phase_bwd_rest()
+
+    def phase_bwd_shared(self) -> None:
+        """dH -> dA (all slots), then the weight grads of the slots SpRS reduces."""
         f, d = self.g.d_ff, self.g.d_model
         self._gemm("dgrad2", self.dyrecv, False, self.w2_view, True, self.da, f, ops.EPI_DGELU,
                    aux=self.gprime)
+        grads2d = self.grads.view(-1)
+        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32, part="shared")
+        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32,
+                   part="shared")
+
+    def phase_bwd_rest(self) -> None:
+        """dXe and the weight grads of the slots no other rank holds."""
+        f, d = self.g.d_ff, self.g.d_model
         self._gemm("dgrad1", self.da, False, self.w1_view, True, self.dxe, d, ops.EPI_BF16)
         grads2d = self.grads.view(-1)
-        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32)
-        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32)
+        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32, part="rest")
+        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32, part="rest")
 
     def phase_combine_dx(self) -> torch.Tensor:
         dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
@@ -368,6 +484,7 @@ class FssdpMoE:
 
     # ------------------------------------------------------------ one rank per process
     def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self.phase_prefetch()
         self.phase_gate(x)
         self.phase_counts()
         self.phase_plan()
@@ -381,14 +498,36 @@ class FssdpMoE:
         self.phase_dispatch_grad(dy)
         remat = self.planner.policy.rematerialize if rematerialize is None else rematerialize
         if remat:
-            self.phase_spag()
-        self.phase_experts_bwd()
-        self.phase_barrier(BAR_DX)
-        dx = self.phase_combine_dx()
-        self.phase_gate_wgrad()
-        self.phase_sprs()
+            self.phase_spag(refetch_early=True)
+        if self.decision.target == self.decision.base:  # no replicas anywhere: no SpRS
+            self.phase_experts_bwd()
+            self.phase_barrier(BAR_DX)
+            dx = self.phase_combine_dx()
+            self.phase_gate_wgrad()
+        else:
+            # SpRS (replica grads -> owners over NVLink) starts as soon as every rank has the
+            # weight grads of its shared slots, on a side stream, and overlaps dXe, the
+            # remaining wgrads, the dX combine and the gate backward (disjoint buffers).
+            # The decision is global (same plan on every rank), so all ranks join BAR_SPRS.
+            self.phase_bwd_shared()
+            main = torch.cuda.current_stream(self.dev)
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.phase_barrier(BAR_SPRS)
+                self.phase_sprs()
+            self.phase_bwd_rest()
+            self.phase_barrier(BAR_DX)
+            dx = self.phase_combine_dx()
+            self.phase_gate_wgrad()
+            main.wait_stream(side)
         self.phase_barrier(BAR_END)
         return dx
+
+    def _side_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.dev)
+        return self._side
 
     def reduce_gate_grad(self, pg=None) -> None:
         """dWg is data-parallel (the gate is replicated): one small NCCL all-reduce."""
@@ -438,6 +577,8 @@ class FssdpMoEFunction(torch.autograd.Function):
 
 def run_lockstep_forward(layers: list, xs: list) -> list:
     """Emulated multi-rank forward: every phase on every logical rank before the next."""
+    for ly in layers:
+        ly.phase_prefetch()
     for ly, x in zip(layers, xs):
         ly.phase_gate(x)
     for ly in layers:
@@ -458,9 +599,11 @@ def run_lockstep_backward(layers: list, dys: list, rematerialize: bool = False) 
         ly.phase_dispatch_grad(dy)
     if rematerialize:
         for ly in layers:
-            ly.phase_spag()
+            ly.phase_spag(refetch_early=True)
     for ly in layers:
-        ly.phase_experts_bwd()
+        ly.phase_bwd_shared()
+    for ly in layers:
+        ly.phase_bwd_rest()
     dxs = [ly.phase_combine_dx() for ly in layers]
     for ly in layers:
         ly.phase_gate_wgrad()

@@ -80,12 +80,19 @@ class ChunkPlacement:
         return cls(num_chunks, num_devices, pairs)
 
     @classmethod
-    def from_mask(cls, mask: np.ndarray) -> "ChunkPlacement":
-        m = np.ascontiguousarray(np.asarray(mask) != 0, dtype=np.uint8)
+    def from_mask(cls, mask: np.ndarray, copy: bool = True) -> "ChunkPlacement":
+        """`copy=False` adopts a fresh 0/1 uint8 array the caller will not touch again."""
+        if copy or not (isinstance(mask, np.ndarray) and mask.dtype == np.uint8
+                        and mask.flags.c_contiguous):
+            m = np.ascontiguousarray(np.asarray(mask) != 0, dtype=np.uint8)
+            if copy:
+                m = m.copy()
+        else:
+            m = mask
         if m.ndim != 2 or m.shape[1] <= 0:
             raise DimensionError(f"placement mask must be (chunks, devices), got {m.shape}")
         obj = cls.__new__(cls)
-        obj._init(m.shape[0], m.shape[1], m.copy())
+        obj._init(m.shape[0], m.shape[1], m)
         return obj
 
     @classmethod

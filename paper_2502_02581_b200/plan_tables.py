@@ -5,9 +5,9 @@ Every rank derives every table from the same deterministic global plan (target
 placement + build_dispatch route), so no table is ever exchanged between ranks.
 
 Receive layout on device d: its local experts occupy *slots* — owned experts
-(ascending id) then replicas (ascending id); each slot's tokens form one segment of
-the receive buffers, segments in slot order, each padded to a multiple of 128 rows
-(the GEMM M tile), so an M tile never mixes experts and wgrad K blocks see zero pad
+(ascending id) then replicas (ascending id; replicas fetched early first); each slot's tokens form one segment of
+the receive buffers, segments in slot order, each padded to a multiple of ROW_ALIGN =
+256 rows (the CTA-pair GEMM M tile), so an M tile never mixes experts and wgrad K blocks see zero pad
 rows.  Inside a segment, tokens are grouped by source device (ascending), and inside
 a source by that source's token-slot order.
 """
@@ -27,13 +27,16 @@ GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"
 GEMM_NAMES = ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2")
 
 
-def slot_maps(base_owner: np.ndarray, target_mask: np.ndarray) -> list[dict]:
-    """Per device: {expert: slot}.  Owned experts first (ascending), then replicas."""
+def slot_maps(base_owner: np.ndarray, target_mask: np.ndarray, pre_mask=None) -> list[dict]:
+    """Per device: {expert: slot}.  Owned experts first (ascending), then the replicas
+    fetched early (in `pre_mask`, ascending), then the other replicas (ascending)."""
     E, D = target_mask.shape
+    pre = np.zeros((E, D), dtype=bool) if pre_mask is None else np.asarray(pre_mask, dtype=bool)
     maps = []
     for d in range(D):
         owned = [e for e in range(E) if base_owner[e] == d]
         reps = [e for e in range(E) if target_mask[e, d] and base_owner[e] != d]
+        reps = [e for e in reps if pre[e, d]] + [e for e in reps if not pre[e, d]]
         maps.append({e: s for s, e in enumerate(owned + reps)})
     return maps
 
@@ -48,7 +51,7 @@ class RankTables:
     n_owned: int
     seg_start: np.ndarray        # [n_slots] receive row of each slot's segment
     seg_rows: np.ndarray         # [n_slots] real rows
-    seg_padded: np.ndarray       # [n_slots] rows incl. padding (multiple of 128)
+    seg_padded: np.ndarray       # [n_slots] rows incl. padding (multiple of ROW_ALIGN)
     recv_rows: int               # total receive rows on this rank (padded)
     route_cum: np.ndarray        # [E, D+1] int32 cumulative split of this source's cells
     recv_base: np.ndarray        # [E, D] int32 first receive row on d of (this source, e)
@@ -57,6 +60,7 @@ class RankTables:
     sprs_jobs: np.ndarray        # [n, 3] int32 {dst_slot, src_begin, src_count}
     sprs_srcs: np.ndarray        # [m, 2] int32 {rank, slot}, ascending rank per job
     groups: dict                 # name -> (GROUP_DTYPE array, n_tiles, total_tiles)
+    wgrad_split: tuple = (0, 0, 0)  # (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles)
 
 
 def _segments(route: np.ndarray, slots: dict, d: int):
@@ -75,14 +79,20 @@ def _finalize(groups: np.ndarray, n_tiles: int):
     return groups, n_tiles, int(tiles.sum())
 
 
-def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int):
+def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None):
     """The six grouped-GEMM descriptor arrays of one rank (see gemm_sm100.cu).
 
     Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16; viewed as
     [(slots*2f) x d] rows for W1 and, from offset f*d, as [(slots*2d) x f] rows for W2.
-    Gradient slot s holds [dW1 (f x d) | dW2 (d x f)] fp32."""
+    Gradient slot s holds [dW1 (f x d) | dW2 (d x f)] fp32.
+
+    `shared` (bool per segment): the wgrads list shared segments (experts with other
+    holders — the SpRS inputs) first; the rest restart tile_start at 0 and run as a second
+    launch, so SpRS can start in between.  Returns (groups, wgrad_split) with wgrad_split =
+    (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles)."""
     d, f = d_model, d_ff
     n = len(seg_start)
+    shared = [False] * n if shared is None else [bool(x) for x in shared]
     out = {}
     g = np.zeros(n, dtype=GROUP_DTYPE)
     for i in range(n):
@@ -106,25 +116,30 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int):
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * 2 * f, f // 64, 0, st * d)
     out["dgrad1"] = _finalize(g.copy(), d // 256)
-    for i in range(n):  # dW1 = dA^T X  (K = the segment's tokens)
-        s = slot_of_seg[i]
-        st = int(seg_start[i])
-        g[i] = (f // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), 0, s * 2 * f * d)
-    out["wgrad1"] = _finalize(g.copy(), d // 256)
-    for i in range(n):  # dW2 = dY^T H
-        s = slot_of_seg[i]
-        st = int(seg_start[i])
-        g[i] = (d // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), 0, s * 2 * f * d + f * d)
-    out["wgrad2"] = _finalize(g.copy(), f // 256)
-    return out
+    order = [i for i in range(n) if shared[i]] + [i for i in range(n) if not shared[i]]
+    n_sh = sum(shared)
+    split = [n_sh]
+    for name, rows, n_t, extra in (("wgrad1", f, d // 256, 0), ("wgrad2", d, f // 256, f * d)):
+        gw = np.zeros(n, dtype=GROUP_DTYPE)
+        for j, i in enumerate(order):  # dW1 = dA^T X, dW2 = dY^T H (K = the segment's tokens)
+            s = slot_of_seg[i]
+            st = int(seg_start[i])
+            gw[j] = (rows // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), 0,
+                     s * 2 * f * d + extra)
+        head, _, t_sh = _finalize(gw[:n_sh], n_t)
+        tail, _, t_rest = _finalize(gw[n_sh:], n_t)
+        out[name] = (np.concatenate([head, tail]), n_t, t_sh + t_rest)
+        split.append(t_sh)
+    return out, tuple(split)
 
 
 def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray,
-                      route: np.ndarray, d_model: int, d_ff: int) -> RankTables:
+                      route: np.ndarray, d_model: int, d_ff: int, pre_mask=None) -> RankTables:
+    """`pre_mask` (E, D): replicas already fetched by an earlier SpAG (same slots, no copy)."""
     E, D = target_mask.shape
     if route.shape != (D, E, D):
         raise InternalError(f"route shape {route.shape} != {(D, E, D)}")
-    maps = slot_maps(base_owner, target_mask)
+    maps = slot_maps(base_owner, target_mask, pre_mask)
     segs = [_segments(route, maps[d], d) for d in range(D)]
     slots = maps[rank]
     start, rows, padded = segs[rank]
@@ -146,7 +161,7 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
     copies = []
     for e, s in sorted(slots.items(), key=lambda kv: kv[1]):
         o = int(base_owner[e])
-        if o != rank:
+        if o != rank and not (pre_mask is not None and pre_mask[e, rank]):
             copies.append((o, maps[o][e], s))
     spag = np.array(copies, dtype=np.int32).reshape(-1, 3)
 
@@ -164,12 +179,15 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
     sprs_srcs = np.array(srcs, dtype=np.int32).reshape(-1, 2)
 
     order = list(range(len(slots)))  # segments are in slot order
-    groups = gemm_groups(start, padded, order, d_model, d_ff)
+    by_slot = {s: e for e, s in slots.items()}
+    shared = [int(np.count_nonzero(target_mask[by_slot[s]])) > 1 for s in order]
+    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared)
     n_owned = sum(1 for e in slots if int(base_owner[e]) == rank)
     return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
                       seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),
                       route_cum=route_cum, recv_base=recv_base, zero_rows=zero_rows,
-                      spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs, groups=groups)
+                      spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs, groups=groups,
+                      wgrad_split=wgrad_split)
 
 
 SECTION_NAMES = ("route_cum", "recv_base", "zero_rows", "spag", "sprs_jobs", "sprs_srcs",
@@ -197,26 +215,50 @@ class NativeTables:
     """The same tables built by the C++ twin (fssdp_build_rank_tables) straight into a
     pinned staging buffer — the product path; build_rank_tables above is its checker."""
 
-    def __init__(self, rank, base_owner, target_mask, route, d_model, d_ff, out_bytes=None):
-        from . import _native as N
+    _hdr = np.zeros(28, dtype=np.int32)  # FSSDP_TAB_HEADER_INTS
+    _hdr_ptr = _hdr.ctypes.data
 
+    def __init__(self, rank, base_owner, target_mask, route, d_model, d_ff, out_bytes=None,
+                 pre_mask=None):
         E, D = target_mask.shape
-        self.E, self.D = E, D
-        self.offsets, self.nbytes = _layout(E, D)
-        self.blob = out_bytes if out_bytes is not None else np.zeros(self.nbytes, dtype=np.uint8)
-        if len(self.blob) < self.nbytes:
-            raise InternalError("plan tables exceed the staging buffer")
-        hdr = np.zeros(25, dtype=np.int32)
+        _, nbytes = _layout(E, D)
+        blob = out_bytes if out_bytes is not None else np.zeros(nbytes, dtype=np.uint8)
         owner = np.ascontiguousarray(base_owner, dtype=np.int32)
         mask = np.ascontiguousarray(target_mask, dtype=np.uint8)
         rt = np.ascontiguousarray(route, dtype=np.int64)
-        N.check(N.LIB_RAW.fssdp_build_rank_tables(
-            rank, D, E, owner.ctypes.data, mask.ctypes.data, rt.ctypes.data, d_model, d_ff,
-            self.blob.ctypes.data, self.nbytes, hdr.ctypes.data), "build_rank_tables")
+        pre = None if pre_mask is None else np.ascontiguousarray(pre_mask, dtype=np.uint8)
+        self._build(rank, E, D, owner.ctypes.data, mask.ctypes.data,
+                    None if pre is None else pre.ctypes.data, rt.ctypes.data, d_model, d_ff,
+                    blob, blob.ctypes.data)
+
+    @classmethod
+    def from_pointers(cls, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff,
+                      blob, blob_ptr) -> "NativeTables":
+        """Planning critical path: inputs already in place (FssdpPlanner scratch buffers),
+        addresses resolved by the caller."""
+        obj = cls.__new__(cls)
+        obj._build(rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
+                   blob_ptr)
+        return obj
+
+    def _build(self, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
+               blob_ptr) -> None:
+        from . import _native as N
+
+        self.E, self.D = E, D
+        self.offsets, self.nbytes = _layout(E, D)
+        self.blob = blob
+        if len(blob) < self.nbytes:
+            raise InternalError("plan tables exceed the staging buffer")
+        N.check(N.LIB_RAW.fssdp_build_rank_tables(rank, D, E, owner_ptr, mask_ptr, pre_ptr,
+                                                  route_ptr, d_model, d_ff, blob_ptr, self.nbytes,
+                                                  self._hdr_ptr), "build_rank_tables")
+        h = self._hdr.tolist()
         (self.n_slots, self.n_owned, self.recv_rows, self.n_zero, self.n_spag, self.n_sprs_jobs,
-         self.n_sprs_srcs) = (int(v) for v in hdr[:7])
-        self.gemm = {name: (int(hdr[7 + 3 * i]), int(hdr[8 + 3 * i]), int(hdr[9 + 3 * i]))
+         self.n_sprs_srcs) = h[:7]
+        self.gemm = {name: (h[7 + 3 * i], h[8 + 3 * i], h[9 + 3 * i])
                      for i, name in enumerate(GEMM_NAMES)}
+        self.wgrad_split = (h[25], h[26], h[27])
 
     def section(self, name, dtype, count):
         off = self.offsets[name]

@@ -106,7 +106,7 @@ def test_multi_rank_equals_single_rank(world, E, policy_kw):
     multi = build(world, E, d, f, k, Tr, pol, seed=7, bias=bias)
     single = build(1, E, d, f, k, Tr * world, F.Policy(F.PolicyKind.EP), seed=7, bias=bias)[0]
     g = torch.Generator(device="cuda").manual_seed(11)
-    replicas_seen = 0
+    replicas_seen = prefetched = 0
     for it in range(3):
         x = torch.randn(world * Tr, d, device="cuda", generator=g).bfloat16()
         dy = (torch.randn(world * Tr, d, device="cuda", generator=g) * 0.05).bfloat16()
@@ -122,6 +122,7 @@ def test_multi_rank_equals_single_rank(world, E, policy_kw):
         torch.cuda.synchronize()
         dec = multi[0].decision
         replicas_seen += len(dec.target.entries) - E
+        prefetched += sum(ly.pre_tables.n_spag for ly in multi if ly.pre_tables is not None)
         # every rank computed the same plan
         for ly in multi[1:]:
             assert ly.decision.target == dec.target
@@ -148,5 +149,6 @@ def test_multi_rank_equals_single_rank(world, E, policy_kw):
                 assert torch.equal(ly.params[s], multi[o].params[os_])
     if kind == F.PolicyKind.FSSDP:
         assert replicas_seen > 0, "the skewed loads should have produced replicas"
+        assert prefetched > 0, "history-driven replicas should have been fetched early"
     else:
-        assert replicas_seen == 0
+        assert replicas_seen == 0 and prefetched == 0

@@ -77,6 +77,92 @@ def test_native_tables_equal_python_tables():
                 arr, n_tiles, total = py.groups[name]
                 assert nt.gemm[name] == (len(arr), n_tiles, total), name
                 assert nt.groups(name).tobytes() == arr.tobytes(), name
+            assert nt.wgrad_split == py.wgrad_split
+
+
+def test_early_spag_tables_compose_with_the_final_plan():
+    """The estimate-based candidate (known before the gate) is contained in the final
+    placement unless the final one fell back to the bare partition; its early tables put
+    every prefetched replica in the slot the final tables use, and early + late SpAG
+    copies are exactly the full SpAG schedule (native == python for both)."""
+    from paper_2502_02581_b200.plan_tables import NativeTables
+
+    rng = np.random.default_rng(5)
+    checked = 0
+    for _ in range(60):
+        D, E = int(rng.choice([2, 4, 8])), int(rng.choice([8, 16]))
+        topo = F.ClusterTopology.for_nvswitch(D)
+        cfg = F.ModelConfig(1, E, 2 ** 20, 512, 1e-3, 1e-6)
+        pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=int(rng.integers(1, E + 1)),
+                       capacity_override=int(rng.integers(1, 4)))
+        pl = F.FssdpPlanner(cfg, topo, pol)
+        p = 1.0 / np.arange(1, E + 1) ** 1.2
+        p = p[rng.permutation(E)]
+        hist = rng.multinomial(600, p / p.sum(), size=D)
+        pl.history[0].append(hist.astype(np.float64))
+        pre = pl.candidate(0)
+        counts = rng.multinomial(600, p / p.sum(), size=D)
+        dec = pl.plan(0, counts)
+        target, base = dec.target.mask.astype(bool), dec.base.mask.astype(bool)
+        if pre is None:
+            assert not dec.adopted
+            continue
+        assert dec.adopted
+        if np.any(pre.astype(bool) & ~target):
+            assert np.array_equal(target, base), "final plan must be a superset or the partition"
+            continue
+        checked += 1
+        owner = dec.base.owners()
+        zero = np.zeros((D, E, D), dtype=np.int64)
+        for r in range(D):
+            early = build_rank_tables(r, owner, pre, zero, 256, 512)
+            late = build_rank_tables(r, owner, dec.target.mask, dec.route, 256, 512, pre_mask=pre)
+            full = build_rank_tables(r, owner, dec.target.mask, dec.route, 256, 512)
+            for e, s in early.slots.items():
+                assert late.slots[e] == s
+            for py, args in ((early, (pre, zero, None)), (late, (dec.target.mask, dec.route, pre))):
+                nt = NativeTables(r, owner, args[0], args[1], 256, 512, pre_mask=args[2])
+                assert nt.slots == py.slots
+                assert np.array_equal(np.asarray(nt.spag_copies), py.spag_copies)
+            def copied(t):
+                by_slot = {s: e for e, s in t.slots.items()}
+                return [by_slot[int(s)] for _, _, s in t.spag_copies]
+
+            ce, cl = copied(early), copied(late)
+            assert not set(ce) & set(cl)
+            assert sorted(ce + cl) == sorted(copied(full))
+    assert checked > 5
+
+
+def test_wgrad_shared_prefix_covers_every_sprs_input():
+    """The wgrad groups list, first, exactly the slots SpRS reads or writes (experts with
+    more than one holder); both launches together tile every slot once."""
+    rng = np.random.default_rng(9)
+    for _ in range(30):
+        D, E = int(rng.choice([2, 4, 8])), 16
+        dec, _ = _random_plan(rng, D, E, 300, 2)
+        owner = dec.base.owners()
+        for r in range(D):
+            t = build_rank_tables(r, owner, dec.target.mask, dec.route, 256, 512)
+            n_sh, t1, t2 = t.wgrad_split
+            by_slot = {s: e for e, s in t.slots.items()}
+            for name, t_sh in (("wgrad1", t1), ("wgrad2", t2)):
+                arr, n_tiles, total = t.groups[name]
+                assert len(arr) == len(t.slots)
+                slots = [int(c_off) // (2 * 256 * 512) for c_off in arr["c_off"]]
+                assert sorted(slots) == list(range(len(t.slots)))
+                head = {by_slot[s] for s in slots[:n_sh]}
+                want = {e for e in t.slots if np.count_nonzero(dec.target.mask[e]) > 1}
+                assert head == want
+                for part in (arr[:n_sh], arr[n_sh:]):  # each launch starts at tile 0
+                    if len(part):
+                        assert part["tile_start"][0] == 0
+                        assert np.all(np.diff(part["tile_start"]) ==
+                                      (part["m_tiles"][:-1] * n_tiles))
+                assert t_sh == int((arr[:n_sh]["m_tiles"] * n_tiles).sum())
+                assert total == int((arr["m_tiles"] * n_tiles).sum())
+            sprs_slots = {int(s) for s, _, _ in t.sprs_jobs}
+            assert sprs_slots <= {t.slots[e] for e in head}
 
 
 def test_spag_sprs_jobs_follow_the_pair_contract():
