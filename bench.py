@@ -288,7 +288,8 @@ def run_ours(args):
     ms = start.elapsed_time(end) / args.steps
     timers = layer.timers
     if os.environ.get("FSSDP_TIMELINE"):
-        # last timed step's kernels as (start, end) ms from the step's first kernel, per rank
+        # last timed step's kernels as (start, end) ms from the step's first kernel, one
+        # file per rank: $FSSDP_TIMELINE_n{world}_r{rank}.json
         last = []
         for key, ev in timers.items():
             if key == "host_plan_s":
@@ -298,7 +299,7 @@ def run_ours(args):
         s0 = min(last, key=lambda t: start.elapsed_time(t[1]))[1]
         rows = sorted((round(s0.elapsed_time(s_), 4), round(s0.elapsed_time(e_), 4), key)
                       for key, s_, e_ in last)
-        print("TIMELINE", rank, json.dumps(rows), file=sys.stderr, flush=True)
+        Path(f"{os.environ['FSSDP_TIMELINE']}_n{world}_r{rank}.json").write_text(json.dumps(rows))
     layer.timers = None
     ms_max = ms
     if world > 1:

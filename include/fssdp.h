@@ -169,12 +169,13 @@ int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, con
  * fssdp_tables_layout returns; header_out[FSSDP_TAB_HEADER_INTS] = {n_slots, n_owned,
  * recv_rows, n_zero, n_spag, n_sprs_jobs, n_sprs_srcs, then per GEMM (fwd1, fwd2, dgrad2,
  * dgrad1, wgrad1, wgrad2): num_groups, n_tiles, total_tiles, then n_shared,
- * wgrad1_shared_tiles, wgrad2_shared_tiles}.  The wgrad group arrays list the n_shared
+ * wgrad1_shared_tiles, wgrad2_shared_tiles, n_stage}.  n_stage = staging slots this rank
+ * receives partial gradients in (see fssdp_sprs).  The wgrad group arrays list the n_shared
  * slots whose expert has other holders (the SpRS inputs) first, as a separately launchable
  * prefix; the remaining groups restart tile_start at 0, so a wgrad runs as two launches
  * (shared prefix, then the rest) and SpRS can start between them.
  * Layout semantics: plan_tables.py. */
-#define FSSDP_TAB_HEADER_INTS 28
+#define FSSDP_TAB_HEADER_INTS 29
 #define FSSDP_TAB_ROUTE_CUM 0   /* int32 [E][D+1] */
 #define FSSDP_TAB_RECV_BASE 1   /* int32 [E][D]   */
 #define FSSDP_TAB_ZERO_ROWS 2   /* int32 [<=E][2] {row, count} */
@@ -213,8 +214,8 @@ typedef struct fssdp_gemm_group {
   int32_t b_n;        /* B tensor-map coordinate of the group's N origin */
   int32_t b_k;        /* B tensor-map coordinate of the group's K origin */
   int32_t k_blocks;   /* number of 64-wide K blocks (0 => C tile written as zeros) */
-  int32_t pad_;
-  int64_t c_off;      /* element offset of the group's C[0, 0] */
+  int32_t c_dest;     /* 0: C;  r + 1: the tensor c_dest_maps[r] (e.g. a peer's staging) */
+  int64_t c_off;      /* element offset of the group's C[0, 0] in its destination */
 } fssdp_gemm_group;
 
 #define FSSDP_EPI_BF16 0  /* C = bf16(acc) */
@@ -229,6 +230,9 @@ typedef struct fssdp_gemm_group {
  * C (and C2 / aux) is a row-major [c_rows][ldc] tensor (bf16, or fp32 for
  * FSSDP_EPI_F32); a group's C origin is element c_off (a multiple of ldc).
  * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum.
+ * c_dest_maps (nullable): device array of 128-byte tensor maps made by
+ * fssdp_epilogue_tmap, the destinations of groups with c_dest > 0 — a wgrad pushes a
+ * replica's partial gradient into its owner's staging slot over NVLink this way.
  * flags: FSSDP_GEMM_N_FASTEST orders a group's tiles N-fastest (A tile shared in L2). */
 #define FSSDP_GEMM_N_FASTEST 1
 /* CTA-pair (tcgen05 cta_group::2) 256 x 256 tiles; requires every group's m_tiles even. */
@@ -236,8 +240,13 @@ typedef struct fssdp_gemm_group {
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
-                       int32_t total_tiles, void* c, void* c2, const void* aux, int64_t ldc,
-                       int64_t c_rows, int32_t flags, void* stream);
+                       int32_t total_tiles, void* c, void* c2, const void* aux,
+                       const void* c_dest_maps, int64_t ldc, int64_t c_rows, int32_t flags,
+                       void* stream);
+/* The epilogue tensor map fssdp_grouped_gemm builds for C = [rows][ldc] at `base` with
+ * this epilogue (128 bytes into map_out, host memory); upload it for c_dest_maps. */
+int fssdp_epilogue_tmap(int32_t epilogue, const void* base, int64_t ldc, int64_t rows,
+                        void* map_out);
 
 #define FSSDP_GATE_TILE 64 /* tokens per gate CTA (slot ranks are tile-relative) */
 
@@ -322,11 +331,15 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
 int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
                const int32_t* copies, int32_t n_copies, void* stream);
 
-/* K8: SparseReduceScatter.  jobs[n * 3] = {dst_slot, src_begin, src_count};
- * srcs[* 2] = {rank, slot} in ascending rank order (owner included):
- *   own[dst_slot] = sum over srcs (fp32, listed order).  slot_elems fp32 per slot. */
-int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t slot_elems,
-               const int32_t* jobs, int32_t n_jobs, const int32_t* srcs, void* stream);
+/* K8: SparseReduceScatter, owner side.  The holders' wgrads already pushed their partial
+ * gradients into this rank's staging slots (c_dest groups); here, per job
+ * jobs[n * 3] = {dst_slot, src_begin, src_count} with srcs[* 2] = {rank, idx} in ascending
+ * rank order (owner included):  grads[dst_slot] = sum over srcs (fp32, listed order) of
+ * (rank == this rank ? grads[idx] : stage[idx]).  Local memory only; slot_elems fp32 per
+ * slot; grads / stage at heap offsets grad_off / stage_off. */
+int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,
+               int64_t slot_elems, const int32_t* jobs, int32_t n_jobs, const int32_t* srcs,
+               void* stream);
 
 /* ================================================================== symmetric heap */
 /* cudaMalloc'd, zero-initialised heap (bytes rounded up to 2 MiB). */
@@ -338,6 +351,10 @@ int fssdp_ipc_open(const uint8_t* handle /* 64 bytes */, void** ptr_out);
 int fssdp_ipc_close(void* ptr);
 /* Number of SMs of the current device. */
 int fssdp_num_sms(void);
+/* Plan-boundary copies (counts readback, plan-table upload): cudaMemcpyAsync of `bytes`
+ * on `stream` (direction inferred from the pointers), then, if `synchronize`, wait for
+ * the stream.  Host buffers should be pinned. */
+int fssdp_copy(void* dst, const void* src, int64_t bytes, void* stream, int32_t synchronize);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -56,7 +56,7 @@ class GemmGroup(C.Structure):
         ("b_n", C.c_int32),
         ("b_k", C.c_int32),
         ("k_blocks", C.c_int32),
-        ("pad_", C.c_int32),
+        ("c_dest", C.c_int32),
         ("c_off", C.c_int64),
     ]
 
@@ -91,7 +91,8 @@ _SIGS = {
     "fssdp_plan_candidate": [i32, P_i32, P_f64, P_topo, C.POINTER(LayerKnobs), P_u8, P_i32],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
-                           vp, i64, i64, i32, vp],
+                           vp, vp, i64, i64, i32, vp],
+    "fssdp_epilogue_tmap": [i32, vp, i64, i64, vp],
     "fssdp_gate_topk": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
@@ -104,13 +105,14 @@ _SIGS = {
     "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],
     "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
-    "fssdp_sprs": [vp, i32, i64, i64, vp, i32, vp, vp],
+    "fssdp_sprs": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
     # symmetric heap
     "fssdp_heap_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "fssdp_heap_free": [vp],
     "fssdp_ipc_handle": [vp, P_u8],
     "fssdp_ipc_open": [P_u8, C.POINTER(C.c_void_p)],
     "fssdp_ipc_close": [vp],
+    "fssdp_copy": [vp, vp, i64, vp, i32],
 }
 _RESTYPE = {"fssdp_version": C.c_char_p, "fssdp_last_error": C.c_char_p}
 

@@ -96,11 +96,28 @@ const char* fssdp_last_error(void) { return g_last_error.c_str(); }
 
 int fssdp_num_sms(void) { return num_sms(); }
 
+int fssdp_copy(void* dst, const void* src, int64_t bytes, void* stream, int32_t synchronize) {
+  if (bytes < 0 || (bytes > 0 && (dst == nullptr || src == nullptr))) {
+    set_error("copy: bad arguments");
+    return kErrDimension;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = bytes ? cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, s)
+                        : cudaSuccess;
+  if (e == cudaSuccess && synchronize) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
-                       int32_t total_tiles, void* c, void* c2, const void* aux, int64_t ldc,
-                       int64_t c_rows, int32_t flags, void* stream) {
+                       int32_t total_tiles, void* c, void* c2, const void* aux,
+                       const void* c_dest_maps, int64_t ldc, int64_t c_rows, int32_t flags,
+                       void* stream) {
   if (num_groups <= 0 || n_tiles <= 0 || total_tiles < 0 || c == nullptr || c_rows <= 0) {
     set_error("grouped_gemm: bad arguments");
     return kErrDimension;
@@ -120,10 +137,27 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.c = c;
   args.c2 = c2;
   args.aux = static_cast<const __nv_bfloat16*>(aux);
+  args.c_dest_maps = c_dest_maps;
   int rc = grouped_gemm_launch(a_mn, b_mn, epilogue, a, a_inner, a_outer, b, b_inner, b_outer,
                                c_rows, args, reinterpret_cast<cudaStream_t>(stream));
   if (rc == kErrCuda && g_last_error.empty()) set_error("grouped_gemm launch failed");
   return rc;
+}
+
+int fssdp_epilogue_tmap(int32_t epilogue, const void* base, int64_t ldc, int64_t rows,
+                        void* map_out) {
+  if (epilogue < kEpiBF16 || epilogue > kEpiF32 || map_out == nullptr) {
+    set_error("epilogue_tmap: bad arguments");
+    return kErrDimension;
+  }
+  CUtensorMap m;
+  const int rc = epilogue_tmap(epilogue, base, ldc, rows, &m);
+  if (rc != kOk) {
+    if (g_last_error.empty()) set_error("epilogue_tmap: cannot encode the tensor map");
+    return rc;
+  }
+  memcpy(map_out, &m, sizeof(m));
+  return kOk;
 }
 
 int fssdp_heap_alloc(size_t bytes, void** ptr_out) {

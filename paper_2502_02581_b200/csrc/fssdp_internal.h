@@ -37,12 +37,14 @@ struct GemmLaunch {
   void* c;          // output (bf16 or fp32)
   void* c2;         // second output (GeLU: post-activation)
   const __nv_bfloat16* aux;  // DGeLU: pre-activation, same layout as c
+  const void* c_dest_maps;   // device CUtensorMap[] for groups with c_dest > 0 (nullable)
 };
 
 int num_sms();
 void set_error(const char* msg);
 constexpr int kDtBF16 = 0;
 constexpr int kDtF32 = 1;
+int epilogue_tmap(int epi, const void* base, int64_t ldc, int64_t rows, CUtensorMap* map);
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_inner,
                  int box_outer, int dtype, int swizzle_bytes);
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,

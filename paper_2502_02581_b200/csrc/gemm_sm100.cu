@@ -315,6 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                        static_cast<int>(rank) * kBM + q * 32;
       const int col0 = tc.n_tile * BN;
       const bool zero = g.k_blocks == 0;
+      // destination: C, or (c_dest > 0) a tensor map in global memory — e.g. a peer's
+      // staging slot, so the store itself is the NVLink transfer
+      const CUtensorMap* cmap =
+          g.c_dest > 0 ? static_cast<const CUtensorMap*>(args.c_dest_maps) + (g.c_dest - 1) : &map_c;
       if (EPI == kEpiDGelu && lane == 0) {  // prefetch the first aux tiles of this tile
         fence_proxy_async_smem();
         for (int p = 0; p < kAB - 1 && p < kCW; ++p) {
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&map_c, cb, col0 + c * kEpiCols, row0);
+          tma_store_2d(cmap, cb, col0 + c * kEpiCols, row0);
           if (EPI == kEpiGelu)
             tma_store_2d(&map_x, xbuf0 + b * S::kBufBytes, col0 + c * kEpiCols, row0);
           bulk_commit();
@@ -503,6 +507,13 @@ static int dispatch_major(int a_mn, int b_mn, int epi, const CUtensorMap& ma,
   return dispatch_epi<false, false, BN, CG>(epi, ma, mb, mc, mx, args, stream);
 }
 
+// epilogue tiles: 32 x 32, bf16 rows of 64 B (SWIZZLE_64B) or fp32 rows of 128 B
+int epilogue_tmap(int epi, const void* base, int64_t ldc, int64_t rows, CUtensorMap* map) {
+  if (ldc % 32 != 0 || rows <= 0 || base == nullptr) return kErrDimension;
+  if (epi == kEpiF32) return make_tmap_2d(map, base, ldc, rows, kEpiCols, 32, kDtF32, 128);
+  return make_tmap_2d(map, base, ldc, rows, kEpiCols, 32, kDtBF16, 64);
+}
+
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
                         int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                         int64_t c_rows, const GemmLaunch& args, cudaStream_t stream) {
@@ -516,11 +527,7 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   if (rc != kOk) return rc;
   rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / cg, kDtBF16, 128);
   if (rc != kOk) return rc;
-  // epilogue tiles: 32 x 32, bf16 rows of 64 B (SWIZZLE_64B) or fp32 rows of 128 B
-  if (epi == kEpiF32)
-    rc = make_tmap_2d(&mc, args.c, args.ldc, c_rows, kEpiCols, 32, kDtF32, 128);
-  else
-    rc = make_tmap_2d(&mc, args.c, args.ldc, c_rows, kEpiCols, 32, kDtBF16, 64);
+  rc = epilogue_tmap(epi, args.c, args.ldc, c_rows, &mc);
   if (rc != kOk) return rc;
   const void* xptr = epi == kEpiGelu ? args.c2 : (epi == kEpiDGelu ? args.aux : args.c);
   rc = make_tmap_2d(&mx, xptr, args.ldc, c_rows, kEpiCols, 32, epi == kEpiF32 ? kDtF32 : kDtBF16,

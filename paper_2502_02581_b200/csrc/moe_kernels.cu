@@ -801,11 +801,12 @@ __global__ void __launch_bounds__(32)
   bulk_wait<0>();
 }
 
-// Persistent over (chunk, job) units so the launcher can bound the SMs it occupies: SpRS
-// runs beside the backward GEMMs (side stream) and must not crowd them out.
+// Owner-side SpRS reduction (the holders' partials were pushed into the local staging
+// slots by their wgrad epilogues): local HBM reads only.  Persistent over (chunk, job)
+// units so the launcher can bound the SMs it occupies beside the backward GEMMs.
 __global__ void __launch_bounds__(256)
     sprs_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
-                int64_t slot_elems, const int32_t* __restrict__ jobs,
+                int64_t stage_off, int64_t slot_elems, const int32_t* __restrict__ jobs,
                 const int32_t* __restrict__ srcs, int64_t chunk, int n_chunks, int n_units) {
   __shared__ const int4* s_src[kMaxWorld];
   const int64_t chunk_elems = chunk / 4;
@@ -816,11 +817,12 @@ __global__ void __launch_bounds__(256)
     const int src_count = jobs[3 * job + 2];
     const int64_t begin = static_cast<int64_t>(unit % n_chunks) * chunk_elems;
     __syncthreads();  // previous unit's readers of s_src are done
-    if (threadIdx.x < src_count) {
+    if (threadIdx.x < src_count) {  // own grads slot, or the staging slot a holder pushed
       const int r = srcs[2 * (src_begin + threadIdx.x)];
-      const int64_t sl = srcs[2 * (src_begin + threadIdx.x) + 1];
+      const int64_t idx = srcs[2 * (src_begin + threadIdx.x) + 1];
+      const int64_t off = r == rank ? grad_off : stage_off;
       s_src[threadIdx.x] = reinterpret_cast<const int4*>(
-          reinterpret_cast<const float*>(peer_bases[r] + grad_off) + sl * slot_elems + begin);
+          reinterpret_cast<const float*>(peer_bases[rank] + off) + idx * slot_elems + begin);
     }
     __syncthreads();
     const int64_t n = imin64(chunk_elems, slot_elems - begin);
@@ -1088,8 +1090,9 @@ int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int6
   return launch_status();
 }
 
-int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t slot_elems,
-               const int32_t* jobs, int32_t n_jobs, const int32_t* srcs, void* stream) {
+int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,
+               int64_t slot_elems, const int32_t* jobs, int32_t n_jobs, const int32_t* srcs,
+               void* stream) {
   if (slot_elems % 4 != 0) {
     set_error("sprs: slot_elems must be a multiple of 4");
     return kErrDimension;
@@ -1105,8 +1108,9 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
   const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
   const int n_units = n_chunks * n_jobs;
   const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
-  sprs_kernel<<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, slot_elems, jobs,
-                                                   srcs, chunk, n_chunks, n_units);
+  sprs_kernel<<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, stage_off,
+                                                   slot_elems, jobs, srcs, chunk, n_chunks,
+                                                   n_units);
   return launch_status();
 }
 

@@ -1174,6 +1174,22 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
     spag[3 * n_spag + 2] = s;
     ++n_spag;
   }
+  // SpRS by push: a holder's wgrad epilogue writes its partial of a replica straight into
+  // the owner's staging slot (NVLink); the owner then sums locally, ascending rank.
+  // Staging index on owner o: its owned experts with other holders in slot order, each
+  // followed by its non-owner holders ascending.  Every rank derives the same indices.
+  auto holds = [&](int e, int dd) { return target_mask[static_cast<int64_t>(e) * D + dd] != 0; };
+  std::vector<int> stage_idx(static_cast<size_t>(E) * D, -1);  // [e][holder]
+  int n_stage = 0;
+  for (int o = 0; o < D; ++o) {
+    int j = 0;
+    for (int e : slot_expert[o]) {
+      if (base_owner[e] != o) continue;
+      for (int h = 0; h < D; ++h)
+        if (h != o && holds(e, h)) stage_idx[static_cast<size_t>(e) * D + h] = j++;
+    }
+    if (o == rank) n_stage = j;
+  }
   int32_t* jobs = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_JOBS]);
   int32_t* srcs = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_SRCS]);
   int n_jobs = 0, n_srcs = 0;
@@ -1181,16 +1197,16 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
     const int e = slot_expert[rank][s];
     if (base_owner[e] != rank) continue;
     int holders = 0;
-    for (int d = 0; d < D; ++d) holders += target_mask[static_cast<int64_t>(e) * D + d] != 0;
+    for (int dd = 0; dd < D; ++dd) holders += holds(e, dd);
     if (holders <= 1) continue;
     jobs[3 * n_jobs] = s;
     jobs[3 * n_jobs + 1] = n_srcs;
     jobs[3 * n_jobs + 2] = holders;
     ++n_jobs;
-    for (int d = 0; d < D; ++d)
-      if (target_mask[static_cast<int64_t>(e) * D + d]) {
-        srcs[2 * n_srcs] = d;
-        srcs[2 * n_srcs + 1] = slot_of[d][e];
+    for (int dd = 0; dd < D; ++dd)
+      if (holds(e, dd)) {  // {rank, own grads slot | staging slot}
+        srcs[2 * n_srcs] = dd;
+        srcs[2 * n_srcs + 1] = dd == rank ? s : stage_idx[static_cast<size_t>(e) * D + dd];
         ++n_srcs;
       }
   }
@@ -1199,7 +1215,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   auto shared = [&](int s) {
     const int e = slot_expert[rank][s];
     int holders = 0;
-    for (int dd = 0; dd < D; ++dd) holders += target_mask[static_cast<int64_t>(e) * D + dd] != 0;
+    for (int dd = 0; dd < D; ++dd) holders += holds(e, dd);
     return holders > 1;
   };
   std::vector<int> wg_order;
@@ -1236,6 +1252,15 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
         case 4: x = {static_cast<int32_t>(f / 128), 0, 0, st, 0, st, kt, 0, s * 2 * f * d}; break;
         default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * 2 * f * d + f * d}; break;
       }
+      if (wgrad) {  // a replica's partial goes to its owner's staging slot
+        const int e = slot_expert[rank][s];
+        const int o = base_owner[e];
+        if (o != rank) {
+          x.c_dest = o + 1;
+          x.c_off = static_cast<int64_t>(stage_idx[static_cast<size_t>(e) * D + rank]) * 2 * f * d +
+                    (gi == 5 ? f * d : 0);
+        }
+      }
       x.tile_start = tile;
       tile += x.m_tiles * n_tiles[gi];
       total += x.m_tiles * n_tiles[gi];
@@ -1248,6 +1273,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   header_out[25] = n_shared;
   header_out[26] = shared_tiles[0];
   header_out[27] = shared_tiles[1];
+  header_out[28] = n_stage;
   int32_t* se = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SLOT_EXPERT]);
   int32_t* ss = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_START]);
   int32_t* sr = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SEG_ROWS]);

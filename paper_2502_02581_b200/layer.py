@@ -62,6 +62,18 @@ class LayerGeometry:
     def expert_bytes(self) -> int:
         return self.slot_param_bytes
 
+    @property
+    def stage_slots(self) -> int:
+        """Staging slots for replica partial gradients pushed to this rank as an owner:
+        at most (world-1) holders per owned expert, and at most every other rank's replica
+        slots in total."""
+        if self.world <= 1:
+            return 0
+        owned_max = -(-self.num_experts // self.world)
+        owned_min = self.num_experts // self.world
+        return min((self.world - 1) * owned_max,
+                   (self.world - 1) * max(0, self.slots - owned_min))
+
     def validate(self) -> None:
         if self.d_model % 256 or self.d_ff % 256:
             raise DimensionError("d_model and d_ff must be multiples of 256 (GEMM N tile)")
@@ -77,6 +89,7 @@ class LayerGeometry:
         layout.add(prefix + "dyrecv", R * d * 2)
         layout.add(prefix + "dxe", R * d * 2)
         layout.add(prefix + "counts", self.world * self.num_experts * 4)
+        layout.add(prefix + "stage", max(1, self.stage_slots) * self.slot_grad_elems * 4)
 
 
 def default_slots(num_experts: int, world: int, m: int) -> int:
@@ -105,7 +118,7 @@ class FssdpMoE:
         heap = group.local
         d, f, E, R = geom.d_model, geom.d_ff, geom.num_experts, geom.recv_cap
         self.off = {k: L.offset(prefix + k) for k in
-                    ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts")}
+                    ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage")}
         self.flags_off = L.offset("flags")
         self.params = heap.tensor(self.off["params"], (geom.slots, 2 * d * f), torch.bfloat16)
         self.grads = heap.tensor(self.off["grads"], (geom.slots, 2 * d * f), torch.float32)
@@ -116,7 +129,17 @@ class FssdpMoE:
         self.counts_table = heap.tensor(self.off["counts"], (self.world, E), torch.int32)
         self.counts_host = torch.empty(self.world, E, dtype=torch.int32, pin_memory=True)
         self.counts_host_np = self.counts_host.numpy()
-        self._counts_ev = torch.cuda.Event()
+        self.counts_host_ptr = self.counts_host.data_ptr()
+        self.counts_dev_ptr = self.counts_table.data_ptr()
+        self.counts_nbytes = self.counts_table.numel() * 4
+        # wgrad destinations for replica partials: every rank's staging region, as the
+        # epilogue tensor maps of wgrad1 (ldc d) and wgrad2 (ldc f); built once
+        stage_elems = max(1, geom.stage_slots) * geom.slot_grad_elems
+        self.dest_maps = {}
+        for name, ldc in (("wgrad1", d), ("wgrad2", f)):
+            blob = b"".join(ops.epilogue_tmap(ops.EPI_F32, base + self.off["stage"], ldc,
+                                              stage_elems // ldc) for base in group.bases)
+            self.dest_maps[name] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.dev)
         # 2-D TMA views of the parameter region
         flat = self.params.view(-1)
         self.w1_view = flat.view(geom.slots * 2 * f, d)                  # W1 of slot s: rows s*2f..
@@ -147,6 +170,7 @@ class FssdpMoE:
         self.blob_host_np = self.blob_host.numpy()
         self.blob_host_ptr = self.blob_host_np.ctypes.data
         self.blob_dev = torch.empty(1 << 20, dtype=torch.uint8, device=self.dev)
+        self.blob_dev_ptr = self.blob_dev.data_ptr()
         # tables of the early (estimate-based) SpAG, staged separately from the final ones
         self.pre_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
         self.pre_host_np = self.pre_host.numpy()
@@ -296,13 +320,12 @@ class FssdpMoE:
         self._launch_prefetch()
 
     def phase_plan(self) -> None:
-        # host sync point #1: pinned copy of the all-gathered counts
-        self.counts_host.copy_(self.counts_table, non_blocking=True)
-        self._counts_ev.record()
-        self._counts_ev.synchronize()
-        counts = self.counts_host_np
+        # host sync point #1: pinned copy of the all-gathered counts (raw cudaMemcpyAsync +
+        # stream sync: the torch copy/event path costs tens of microseconds here)
+        N.check(N.LIB_RAW.fssdp_copy(self.counts_host_ptr, self.counts_dev_ptr,
+                                     self.counts_nbytes, self._stream(), 1), "counts readback")
         t_host = time.perf_counter()
-        self._plan_tables(counts)
+        self._plan_tables(self.counts_host_np)
         if self.timers is not None:
             self.timers.setdefault("host_plan_s", []).append(time.perf_counter() - t_host)
 
@@ -327,13 +350,15 @@ class FssdpMoE:
             raise InternalError(f"plan needs {tables.n_slots} slots > capacity {self.g.slots}")
         if tables.recv_rows > self.g.recv_cap:
             raise InternalError("receive rows exceed capacity")
+        if tables.n_stage > self.g.stage_slots:
+            raise InternalError(f"plan needs {tables.n_stage} staging slots > {self.g.stage_slots}")
         if tables.n_owned != len(self._owned_expert_ids) or \
                 list(tables.slot_expert[:tables.n_owned]) != self._owned_expert_ids:
             raise InternalError("ownership changed without a re-shard data move")
         self.decision, self.tables = dec, tables
         self.packed = tables
-        nb = tables.nbytes
-        self.blob_dev[:nb].copy_(self.blob_host[:nb], non_blocking=True)  # boundary #2
+        N.check(N.LIB_RAW.fssdp_copy(self.blob_dev_ptr, self.blob_host_ptr, tables.nbytes,
+                                     self._stream(), 0), "plan tables upload")  # boundary #2
         self.gemm = tables.gemm
 
     def phase_spag(self, refetch_early: bool = False) -> None:
@@ -400,10 +425,11 @@ class FssdpMoE:
         if total == 0:
             return
         flags = (1 if self.N_FASTEST.get(name, False) else 0) | (2 if self.CTA_PAIR else 0)
+        maps = ops._ptr(self.dest_maps.get(name))
         self._timed("gemm." + name, lambda: N.call(
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
             ops._ptr(b), b.shape[1], b.shape[0], tab, ng, n_tiles, total, ops._ptr(c),
-            ops._ptr(c2), ops._ptr(aux), ldc, c.numel() // ldc, flags, self._stream()))
+            ops._ptr(c2), ops._ptr(aux), maps, ldc, c.numel() // ldc, flags, self._stream()))
 
     def phase_experts_fwd(self) -> None:
         f, d = self.g.d_ff, self.g.d_model
@@ -479,8 +505,9 @@ class FssdpMoE:
         if n == 0:
             return
         self._timed("sprs", lambda: N.call(
-            "fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.g.slot_grad_elems,
-            self._tab("sprs_jobs"), n, self._tab("sprs_srcs"), self._stream()))
+            "fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.off["stage"],
+            self.g.slot_grad_elems, self._tab("sprs_jobs"), n, self._tab("sprs_srcs"),
+            self._stream()))
 
     # ------------------------------------------------------------ one rank per process
     def forward(self, x: torch.Tensor) -> torch.Tensor:

@@ -40,13 +40,17 @@ def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
 
 
 # ------------------------------------------------------------------ grouped GEMM
+# fssdp_gemm_group (include/fssdp.h): c_dest 0 = C, r + 1 = c_dest_maps[r]
+GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
+                        ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("c_dest", "<i4"),
+                        ("c_off", "<i8")])
+
+
 def gemm_groups_tensor(groups: list[tuple], device) -> tuple[torch.Tensor, int, int]:
     """Pack [(m_tiles, a_m, a_k, b_n, b_k, k_blocks, c_off), ...] into a device array.
 
     Returns (tensor, num_groups, total_tiles_per_n_tile)."""
-    arr = np.zeros(len(groups), dtype=[("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"),
-                                       ("a_k", "<i4"), ("b_n", "<i4"), ("b_k", "<i4"),
-                                       ("k_blocks", "<i4"), ("pad_", "<i4"), ("c_off", "<i8")])
+    arr = np.zeros(len(groups), dtype=GROUP_DTYPE)
     for i, (m_tiles, a_m, a_k, b_n, b_k, k_blocks, c_off) in enumerate(groups):
         arr[i] = (m_tiles, 0, a_m, a_k, b_n, b_k, k_blocks, 0, c_off)
     raw = torch.from_numpy(arr.view(np.uint8).copy())
@@ -61,20 +65,16 @@ def finalize_groups(groups_cpu: np.ndarray, n_tiles: int) -> int:
     return int(tiles.sum())
 
 
-GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
-                        ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("pad_", "<i4"),
-                        ("c_off", "<i8")])
-
-
 def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, groups_dev: torch.Tensor,
                  num_groups: int, n_tiles: int, total_tiles: int, c: torch.Tensor, ldc: int,
                  epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
                  aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
-                 cta_pair: bool = False) -> None:
+                 cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
-    aux) the whole output tensor, viewed as [numel // ldc, ldc]."""
+    aux) the whole output tensor, viewed as [numel // ldc, ldc].  c_dest_maps: device
+    uint8 tensor of 128-byte tensor maps (epilogue_tmap) for groups with c_dest > 0."""
     for t, nm in ((a, "A"), (b, "B")):
         _need(t, torch.bfloat16, nm)
         if t.dim() != 2:
@@ -83,8 +83,15 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
         raise DimensionError("C must hold whole rows of ldc elements")
     N.call("fssdp_grouped_gemm", int(a_mn), int(b_mn), int(epilogue), _ptr(a), a.shape[1],
            a.shape[0], _ptr(b), b.shape[1], b.shape[0], _ptr(groups_dev), num_groups, n_tiles,
-           total_tiles, _ptr(c), _ptr(c2), _ptr(aux), ldc, c.numel() // ldc,
+           total_tiles, _ptr(c), _ptr(c2), _ptr(aux), _ptr(c_dest_maps), ldc, c.numel() // ldc,
            (1 if n_fastest else 0) | (2 if cta_pair else 0), _stream(stream))
+
+
+def epilogue_tmap(epilogue: int, base_ptr: int, ldc: int, rows: int) -> bytes:
+    """The 128-byte epilogue tensor map of C = [rows][ldc] at device address base_ptr."""
+    out = (C.c_uint8 * 128)()
+    N.call("fssdp_epilogue_tmap", int(epilogue), C.c_void_p(base_ptr), ldc, rows, out)
+    return bytes(out)
 
 
 # ------------------------------------------------------------------ gate

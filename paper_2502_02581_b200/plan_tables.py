@@ -22,7 +22,7 @@ from .errors import InternalError
 
 ROW_ALIGN = 256  # = the CTA-pair GEMM M tile (two 128-row halves)
 GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
-                        ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("pad_", "<i4"),
+                        ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("c_dest", "<i4"),
                         ("c_off", "<i8")])
 GEMM_NAMES = ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2")
 
@@ -58,9 +58,10 @@ class RankTables:
     zero_rows: np.ndarray        # [n, 2] int32 {row, count} padding rows of this rank
     spag_copies: np.ndarray      # [n, 3] int32 {src_rank, src_slot, dst_slot}
     sprs_jobs: np.ndarray        # [n, 3] int32 {dst_slot, src_begin, src_count}
-    sprs_srcs: np.ndarray        # [m, 2] int32 {rank, slot}, ascending rank per job
+    sprs_srcs: np.ndarray        # [m, 2] int32 {rank, own slot | staging slot}, ascending rank
     groups: dict                 # name -> (GROUP_DTYPE array, n_tiles, total_tiles)
     wgrad_split: tuple = (0, 0, 0)  # (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles)
+    n_stage: int = 0             # staging slots this rank receives replica partials in
 
 
 def _segments(route: np.ndarray, slots: dict, d: int):
@@ -79,7 +80,8 @@ def _finalize(groups: np.ndarray, n_tiles: int):
     return groups, n_tiles, int(tiles.sum())
 
 
-def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None):
+def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None,
+                push=None):
     """The six grouped-GEMM descriptor arrays of one rank (see gemm_sm100.cu).
 
     Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16; viewed as
@@ -89,10 +91,14 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     `shared` (bool per segment): the wgrads list shared segments (experts with other
     holders — the SpRS inputs) first; the rest restart tile_start at 0 and run as a second
     launch, so SpRS can start in between.  Returns (groups, wgrad_split) with wgrad_split =
-    (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles)."""
+    (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles).
+
+    `push` (per segment: None, or (owner, staging index)): a replica's wgrad writes its
+    partial gradient into the owner's staging slot (c_dest = owner + 1) — the SpRS wire."""
     d, f = d_model, d_ff
     n = len(seg_start)
     shared = [False] * n if shared is None else [bool(x) for x in shared]
+    push = [None] * n if push is None else list(push)
     out = {}
     g = np.zeros(n, dtype=GROUP_DTYPE)
     for i in range(n):
@@ -124,8 +130,9 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
         for j, i in enumerate(order):  # dW1 = dA^T X, dW2 = dY^T H (K = the segment's tokens)
             s = slot_of_seg[i]
             st = int(seg_start[i])
-            gw[j] = (rows // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), 0,
-                     s * 2 * f * d + extra)
+            dest, slot = (0, s) if push[i] is None else (push[i][0] + 1, push[i][1])
+            gw[j] = (rows // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), dest,
+                     slot * 2 * f * d + extra)
         head, _, t_sh = _finalize(gw[:n_sh], n_t)
         tail, _, t_rest = _finalize(gw[n_sh:], n_t)
         out[name] = (np.concatenate([head, tail]), n_t, t_sh + t_rest)
@@ -165,7 +172,21 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
             copies.append((o, maps[o][e], s))
     spag = np.array(copies, dtype=np.int32).reshape(-1, 3)
 
-    # SpRS: for owned experts with replicas, reduce every holder's grad in ascending rank order
+    # SpRS by push: staging index of (expert, holder) on the expert's owner — the owner's
+    # experts with other holders in slot order, each followed by those holders ascending
+    stage, n_stage = {}, 0
+    for o in range(D):
+        j = 0
+        for e, s in sorted(maps[o].items(), key=lambda kv: kv[1]):
+            if int(base_owner[e]) != o:
+                continue
+            for h in range(D):
+                if h != o and target_mask[e, h]:
+                    stage[(e, h)] = j
+                    j += 1
+        if o == rank:
+            n_stage = j
+    # owner side: grads[s] = sum over holders ascending of (own slot | staging slot)
     jobs, srcs = [], []
     for e, s in sorted(slots.items(), key=lambda kv: kv[1]):
         if int(base_owner[e]) != rank:
@@ -174,20 +195,22 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
         if len(holders) <= 1:
             continue
         jobs.append((s, len(srcs), len(holders)))
-        srcs.extend((h, maps[h][e]) for h in holders)
+        srcs.extend((h, s if h == rank else stage[(e, h)]) for h in holders)
     sprs_jobs = np.array(jobs, dtype=np.int32).reshape(-1, 3)
     sprs_srcs = np.array(srcs, dtype=np.int32).reshape(-1, 2)
 
     order = list(range(len(slots)))  # segments are in slot order
     by_slot = {s: e for e, s in slots.items()}
     shared = [int(np.count_nonzero(target_mask[by_slot[s]])) > 1 for s in order]
-    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared)
+    push = [None if int(base_owner[by_slot[s]]) == rank else
+            (int(base_owner[by_slot[s]]), stage[(by_slot[s], rank)]) for s in order]
+    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared, push)
     n_owned = sum(1 for e in slots if int(base_owner[e]) == rank)
     return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
                       seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),
                       route_cum=route_cum, recv_base=recv_base, zero_rows=zero_rows,
                       spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs, groups=groups,
-                      wgrad_split=wgrad_split)
+                      wgrad_split=wgrad_split, n_stage=n_stage)
 
 
 SECTION_NAMES = ("route_cum", "recv_base", "zero_rows", "spag", "sprs_jobs", "sprs_srcs",
@@ -215,7 +238,7 @@ class NativeTables:
     """The same tables built by the C++ twin (fssdp_build_rank_tables) straight into a
     pinned staging buffer — the product path; build_rank_tables above is its checker."""
 
-    _hdr = np.zeros(28, dtype=np.int32)  # FSSDP_TAB_HEADER_INTS
+    _hdr = np.zeros(29, dtype=np.int32)  # FSSDP_TAB_HEADER_INTS
     _hdr_ptr = _hdr.ctypes.data
 
     def __init__(self, rank, base_owner, target_mask, route, d_model, d_ff, out_bytes=None,
@@ -259,6 +282,7 @@ class NativeTables:
         self.gemm = {name: (h[7 + 3 * i], h[8 + 3 * i], h[9 + 3 * i])
                      for i, name in enumerate(GEMM_NAMES)}
         self.wgrad_split = (h[25], h[26], h[27])
+        self.n_stage = h[28]
 
     def section(self, name, dtype, count):
         off = self.offsets[name]

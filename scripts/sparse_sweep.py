@@ -6,8 +6,11 @@ E = N experts, even single-owner partition; the post-placement adds expert e to 
 (e+1 .. e+r-1) mod N (balanced ring: every GPU pulls (r-1)·S in SpAG and its owner pulls
 (r-1)·S_grad in SpRS).  A "hot" variant materializes expert 0 on r devices only.  Times are
 CUDA events around the kernel, max over ranks; GB/s = per-GPU inbound bytes / time
-(SpAG) and the reference's bottleneck bytes / time (costmodel.py:75-84).  SpRS reduces
-fp32 gradients (S_grad = 2·S).  Prints one JSON line per case on rank 0.
+(SpAG) and the reference's bottleneck bytes / time (costmodel.py:75-84).  SpRS moves fp32
+gradients (S_grad = 2·S) the way the layer does: the shared-prefix wgrad launches push each
+holder's partial into its owner's staging slot through the epilogue's TMA stores (run
+here with K = 0, i.e. the store path alone), then a barrier and the owner's local
+reduction.  Prints one JSON line per case on rank 0.
 """
 
 import argparse
@@ -24,6 +27,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2502_02581_b200 as F  # noqa: E402
 from paper_2502_02581_b200 import _native as N  # noqa: E402
+from paper_2502_02581_b200 import ops  # noqa: E402
 from paper_2502_02581_b200.comm import HeapLayout, PeerGroup  # noqa: E402
 from paper_2502_02581_b200.plan_tables import NativeTables  # noqa: E402
 
@@ -44,14 +48,34 @@ def main():
     layout = HeapLayout()
     layout.add("params", slots * smax)
     layout.add("grads", slots * 2 * smax)
+    layout.add("stage", (world - 1) * 2 * smax)
     group = PeerGroup(layout, rank, world, dev, "dist")
     poff, goff = layout.offset("params"), layout.offset("grads")
+    soff = layout.offset("stage")
+    dummy = torch.zeros(64, 1 << 18, dtype=torch.bfloat16, device=dev)  # never read (K = 0)
+    bar_epoch = [0]
     heap = group.local
     heap.tensor(poff, (slots * smax // 2,), torch.bfloat16).normal_()
     heap.tensor(goff, (slots * smax // 2,), torch.float32).normal_()
     topo = F.ClusterTopology.for_nvswitch(world)
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)
+    flags_off = layout.offset("flags")
+    grads = heap.tensor(goff, (slots * smax // 2,), torch.float32)
+
+    def push(tab, blob, maps, d_, f_):
+        """The shared-prefix wgrad launches with K = 0: replica partials (zeros) stored
+        into the owners' staging slots, owned shared slots locally."""
+        n_sh, t1, t2 = tab.wgrad_split
+        for name, ldc, tiles, a_w, b_w in (("wgrad1", d_, t1, f_, d_), ("wgrad2", f_, t2, d_, f_)):
+            if tiles == 0:
+                continue
+            a = dummy[:, :a_w]
+            b = dummy[:, :b_w]
+            N.call("fssdp_grouped_gemm", 1, 1, ops.EPI_F32, ops._ptr(a), a_w, 64, ops._ptr(b),
+                   b_w, 64, C.c_void_p(blob.data_ptr() + tab.offsets[name]), n_sh,
+                   tab.gemm[name][1], tiles, ops._ptr(grads), None, None, ops._ptr(maps[name]),
+                   ldc, grads.numel() // ldc, 2, sp)
     pb = C.c_void_p(group.peer_bases.data_ptr())
     E = world
     base = F.make_even_partition(E, topo)
@@ -66,8 +90,15 @@ def main():
             route = np.zeros((world, E, world), dtype=np.int64)
             for mb in sizes_mb:
                 S = mb << 20
-                tab = NativeTables(rank, owner, post.mask, route, 256, 256)
+                d_, f_ = 256, mb * 1024   # one slot = [W1 | W2] = 4 d f bytes = S
+                tab = NativeTables(rank, owner, post.mask, route, d_, f_)
                 blob = torch.from_numpy(tab.blob[:tab.nbytes].copy()).to(dev)
+                maps = {}
+                for name, ldc in (("wgrad1", d_), ("wgrad2", f_)):
+                    raw = b"".join(ops.epilogue_tmap(ops.EPI_F32, b + soff, ldc,
+                                                     (world - 1) * 2 * d_ * f_ // ldc)
+                                   for b in group.bases)
+                    maps[name] = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
                 spag_t = C.c_void_p(blob.data_ptr() + tab.offsets["spag"])
                 jobs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_jobs"])
                 srcs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_srcs"])
@@ -81,9 +112,14 @@ def main():
                         s.record()
                         if kind == "spag" and tab.n_spag:
                             N.call("fssdp_spag", pb, rank, poff, S, spag_t, tab.n_spag, sp)
-                        if kind == "sprs" and tab.n_sprs_jobs:
-                            N.call("fssdp_sprs", pb, rank, goff, S // 2, jobs_t, tab.n_sprs_jobs,
-                                   srcs_t, sp)
+                        if kind == "sprs":
+                            push(tab, blob, maps, d_, f_)
+                            bar_epoch[0] += 1
+                            N.call("fssdp_barrier", pb, flags_off, rank, world, 0,
+                                   C.c_uint32(bar_epoch[0]), sp)
+                            if tab.n_sprs_jobs:
+                                N.call("fssdp_sprs", pb, rank, goff, soff, S // 2, jobs_t,
+                                       tab.n_sprs_jobs, srcs_t, sp)
                         e.record()
                         torch.cuda.synchronize()
                         if it >= 2:
@@ -104,6 +140,7 @@ def main():
                         "spag_gbs_bottleneck": rep.bottleneck_bytes / (res["spag"] * 1e-3) / 1e9,
                         "spag_gbs_inbound_max": max_in / (res["spag"] * 1e-3) / 1e9,
                         "sprs_gbs_bottleneck_fp32": 2 * rep.bottleneck_bytes / (res["sprs"] * 1e-3) / 1e9,
+                        "sprs_path": "wgrad epilogue TMA-store push (K=0) + barrier + local reduce",
                         "nvlink_peer_gbs_ref": 770.0,
                     }
                     print("SWEEP " + json.dumps(line), flush=True)

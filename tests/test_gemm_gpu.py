@@ -221,3 +221,42 @@ def test_large_square_against_torch():
     ops.grouped_gemm(A, False, B, False, gd, ng, N // 256, total, C, N)
     torch.cuda.synchronize()
     _close(C, A.float() @ B.float().T)
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_wgrad_c_dest_scatter(pair):
+    """Groups with c_dest > 0 store through the given tensor maps (the push-SpRS wire):
+    here two extra fp32 buffers stand in for two owners' staging regions."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(4)
+    M, N = 256, 512
+    segs = [256, 128, 384]
+    dests = [0, 2, 1]          # group 0 -> C, group 1 -> buffer #2 slot 1, group 2 -> #1 slot 0
+    slots = [0, 1, 0]
+    Rt = sum(segs)
+    At = torch.randn(Rt, M, device=dev).bfloat16()
+    Bt = torch.randn(Rt, N, device=dev).bfloat16()
+    C = torch.zeros(2 * M, N, device=dev)
+    stage = [torch.full((2 * M, N), 5.0, device=dev) for _ in range(2)]
+    maps = b"".join(ops.epilogue_tmap(ops.EPI_F32, s.data_ptr(), N, 2 * M) for s in stage)
+    maps_dev = torch.frombuffer(bytearray(maps), dtype=torch.uint8).to(dev)
+    g = np.zeros(len(segs), dtype=ops.GROUP_DTYPE)
+    k0 = 0
+    for i, s in enumerate(segs):
+        g[i] = (M // 128, 0, 0, k0, 0, k0, s // 64, dests[i], slots[i] * M * N)
+        k0 += s
+    total = ops.finalize_groups(g, N // 256)
+    gd = torch.from_numpy(g.view(np.uint8).copy()).to(dev)
+    ops.grouped_gemm(At, True, Bt, True, gd, len(segs), N // 256, total, C, N,
+                     epilogue=ops.EPI_F32, cta_pair=pair, c_dest_maps=maps_dev)
+    torch.cuda.synchronize()
+    k0 = 0
+    for i, s in enumerate(segs):
+        ref = At[k0:k0 + s].float().T @ Bt[k0:k0 + s].float()
+        out = C if dests[i] == 0 else stage[dests[i] - 1]
+        _close(out[slots[i] * M:(slots[i] + 1) * M], ref, rel=2e-3, abs_=1e-4)
+        k0 += s
+    assert torch.all(stage[1][:M] == 5.0)  # untouched staging slots stay
+    assert torch.all(stage[0][M:] == 5.0)
+    assert torch.all(C[M:] == 0.0)

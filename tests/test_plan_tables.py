@@ -77,7 +77,7 @@ def test_native_tables_equal_python_tables():
                 arr, n_tiles, total = py.groups[name]
                 assert nt.gemm[name] == (len(arr), n_tiles, total), name
                 assert nt.groups(name).tobytes() == arr.tobytes(), name
-            assert nt.wgrad_split == py.wgrad_split
+            assert nt.wgrad_split == py.wgrad_split and nt.n_stage == py.n_stage
 
 
 def test_early_spag_tables_compose_with_the_final_plan():
@@ -136,24 +136,38 @@ def test_early_spag_tables_compose_with_the_final_plan():
 
 def test_wgrad_shared_prefix_covers_every_sprs_input():
     """The wgrad groups list, first, exactly the slots SpRS reads or writes (experts with
-    more than one holder); both launches together tile every slot once."""
+    more than one holder), each launch starting at tile 0; a replica's groups write into
+    its owner's staging slot (c_dest = owner + 1), the one the owner's SpRS job reads."""
     rng = np.random.default_rng(9)
+    f_, d_ = 512, 256
     for _ in range(30):
         D, E = int(rng.choice([2, 4, 8])), 16
         dec, _ = _random_plan(rng, D, E, 300, 2)
         owner = dec.base.owners()
-        for r in range(D):
-            t = build_rank_tables(r, owner, dec.target.mask, dec.route, 256, 512)
+        tabs = [build_rank_tables(r, owner, dec.target.mask, dec.route, d_, f_) for r in range(D)]
+        for r, t in enumerate(tabs):
             n_sh, t1, t2 = t.wgrad_split
             by_slot = {s: e for e, s in t.slots.items()}
-            for name, t_sh in (("wgrad1", t1), ("wgrad2", t2)):
+            shared = [s for s in range(len(t.slots))
+                      if np.count_nonzero(dec.target.mask[by_slot[s]]) > 1]
+            order = shared + [s for s in range(len(t.slots)) if s not in shared]
+            assert n_sh == len(shared)
+            for name, t_sh, extra in (("wgrad1", t1, 0), ("wgrad2", t2, f_ * d_)):
                 arr, n_tiles, total = t.groups[name]
                 assert len(arr) == len(t.slots)
-                slots = [int(c_off) // (2 * 256 * 512) for c_off in arr["c_off"]]
-                assert sorted(slots) == list(range(len(t.slots)))
-                head = {by_slot[s] for s in slots[:n_sh]}
-                want = {e for e in t.slots if np.count_nonzero(dec.target.mask[e]) > 1}
-                assert head == want
+                for g, s in zip(arr, order):
+                    e = by_slot[s]
+                    o = int(owner[e])
+                    if o == r:
+                        assert g["c_dest"] == 0 and g["c_off"] == s * 2 * f_ * d_ + extra
+                        continue
+                    assert g["c_dest"] == o + 1
+                    j, rem = divmod(int(g["c_off"]) - extra, 2 * f_ * d_)
+                    assert rem == 0 and 0 <= j < tabs[o].n_stage
+                    jobs = {int(js): (b, c) for js, b, c in tabs[o].sprs_jobs}
+                    b, c = jobs[tabs[o].slots[e]]
+                    assert [int(x) for x in tabs[o].sprs_srcs[b:b + c][:, 1][
+                        list(tabs[o].sprs_srcs[b:b + c][:, 0]).index(r)].reshape(-1)] == [j]
                 for part in (arr[:n_sh], arr[n_sh:]):  # each launch starts at tile 0
                     if len(part):
                         assert part["tile_start"][0] == 0
@@ -161,8 +175,10 @@ def test_wgrad_shared_prefix_covers_every_sprs_input():
                                       (part["m_tiles"][:-1] * n_tiles))
                 assert t_sh == int((arr[:n_sh]["m_tiles"] * n_tiles).sum())
                 assert total == int((arr["m_tiles"] * n_tiles).sum())
-            sprs_slots = {int(s) for s, _, _ in t.sprs_jobs}
-            assert sprs_slots <= {t.slots[e] for e in head}
+        # staging slots on every owner are used exactly once
+        for o, t in enumerate(tabs):
+            got = sorted(int(i) for h, i in t.sprs_srcs if h != o)
+            assert got == list(range(t.n_stage))
 
 
 def test_spag_sprs_jobs_follow_the_pair_contract():
@@ -187,5 +203,8 @@ def test_spag_sprs_jobs_follow_the_pair_contract():
                 e = [x for x, s in t.slots.items() if s == dst_slot][0]
                 srcs = t.sprs_srcs[b:b + n]
                 assert list(srcs[:, 0]) == sorted(np.flatnonzero(dec.target.mask[e]))
-                assert all(tabs[h].slots[e] == sl for h, sl in srcs)
+                assert all(sl == dst_slot for h, sl in srcs if h == r)  # own partial in place
             assert all(owner[e] == r for e, s in t.slots.items() if s < t.n_owned)
+        # SpRS moves exactly sprs_traffic's schedule: one staging slot per (replica, holder)
+        tr, rep = F.sprs_traffic(dec.target, dec.base, 1)
+        assert rep.total_interdevice_bytes == sum(t.n_stage for t in tabs)
