@@ -320,7 +320,7 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
 /* Gate weight gradient dWg[e] = sum_t dlogit[t, e] x[t]  (fixed order; fp32 [E*d]).
  * workspace: fp32 [ceil(T / FSSDP_WG_TILE) * E * d] (per-token-tile partials, reduced in
  * tile order). */
-#define FSSDP_WG_TILE 256
+#define FSSDP_WG_TILE 64
 int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
                      void* stream);

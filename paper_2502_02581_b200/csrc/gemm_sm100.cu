@@ -35,14 +35,25 @@ namespace fssdp {
 
 constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
-// 4 epilogue warps (one per TMEM lane quarter).  8 (two per quarter, column halves) is
-// supported by the code but measured slower: the smem it needs costs a mainloop stage.
-constexpr int kEpiWarps = 4;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+// Epilogue warps: 4 (one per TMEM lane quarter), or 8 (two per quarter, column halves)
+// for the GeLU epilogue, whose per-element math otherwise outlasts a K = d_model mainloop
+// (the extra staging smem costs one mainloop stage).
+#ifndef FSSDP_GELU_EPI_WARPS
+#define FSSDP_GELU_EPI_WARPS 4
+#endif
+template <int EPI>
+constexpr int epi_warps() {
+  return EPI == FSSDP_EPI_GELU ? FSSDP_GELU_EPI_WARPS : 4;
+}
+template <int EPI>
+constexpr int gemm_threads() {
+  return 64 + 32 * epi_warps<EPI>();
+}
 constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store box)
 
 template <int BN, int EPI, int CG>
 struct GemmSmem {
+  static constexpr int kEpiWarps = epi_warps<EPI>();
   // GeLU' (dgrad2) trades a mainloop stage for a deeper aux-tile prefetch ring
   static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : 0;
   static constexpr int kStages =
@@ -84,6 +95,13 @@ __device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
   dg = fmaf(0.5f, 1.0f + t, hx * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f));
 }
 
+// Work order of a persistent CTA (pair): round r takes tile r*units + unit, in reverse
+// CTA order on odd rounds ("snake").  With groups listed by descending cost (wgrad: K =
+// segment rows), this deals the tiles out close to longest-processing-time-first.
+__device__ __forceinline__ int snake_tile(int round, int unit, int units) {
+  return round * units + ((round & 1) ? units - 1 - unit : unit);
+}
+
 struct TileCoord {
   int group, m_tile, n_tile;  // m_tile in units of CG * 128 rows
 };
@@ -120,7 +138,7 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) {  // 128-byte rows, SWI
 }
 
 template <bool A_MN, bool B_MN, int BN, int EPI, int CG>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
@@ -136,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* aux_bar = tempty_bar + 2;
+  constexpr int kEpiWarps = S::kEpiWarps;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4 * kEpiWarps);
 
   const int warp = threadIdx.x / 32;
@@ -182,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===================== TMA producer (both CTAs stage their own halves)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < total; tile += units) {
+      for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
         const TileCoord tc =
             locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const GemmGroup& g = groups[tc.group];
@@ -242,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = unit; tile < total; tile += units) {
+      for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
         const TileCoord tc =
             locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const int kblocks = groups[tc.group].k_blocks;
@@ -307,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t gchunk = 0;  // running chunk counter (selects the staging buffers)
-    for (int tile = unit; tile < total; tile += units) {
+    for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
       const TileCoord tc =
           locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
       const GemmGroup& g = groups[tc.group];
@@ -467,7 +486,7 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   int grid = CG * (units < num_sms() / CG ? units : num_sms() / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(gemm_threads<EPI>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

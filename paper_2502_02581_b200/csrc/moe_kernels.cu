@@ -275,29 +275,49 @@ __global__ void __launch_bounds__(128)
   const int64_t t0 = static_cast<int64_t>(tile) * kGateTile + warp * 16;
   const int64_t r0 = t0 + g, r1 = t0 + g + 8;
   const bool v0 = r0 < T, v1 = r1 < T;
-  const uint32_t* xr0 = reinterpret_cast<const uint32_t*>(x + (v0 ? r0 : 0) * d);
-  const uint32_t* xr1 = reinterpret_cast<const uint32_t*>(x + (v1 ? r1 : 0) * d);
+  const int4* xr0 = reinterpret_cast<const int4*>(x + (v0 ? r0 : 0) * d);
+  const int4* xr1 = reinterpret_cast<const int4*>(x + (v1 ? r1 : 0) * d);
   float c[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n)
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[n][i] = 0.f;
-#pragma unroll 2
-  for (int k0 = 0; k0 < d; k0 += 16) {
-    uint32_t a[4];
-    const int w0 = (k0 >> 1) + t4;  // 32-bit word of columns k0+2t, k0+2t+1
-    a[0] = v0 ? __ldg(xr0 + w0) : 0u;
-    a[1] = v1 ? __ldg(xr1 + w0) : 0u;
-    a[2] = v0 ? __ldg(xr0 + w0 + 4) : 0u;
-    a[3] = v1 ? __ldg(xr1 + w0 + 4) : 0u;
+  // K in 64-column blocks: lane t4 loads 16-byte vectors at columns 8*t4 and 32 + 8*t4 of
+  // rows g and g+8 (each load instruction covers 64 contiguous bytes per row).  The MMA's
+  // k index is a fixed permutation of the block's columns, applied to x and Wg alike: the
+  // logits are the same dot products, summed in another order.  KB blocks in flight.
+  constexpr int KB = 4;
+  for (int kb = 0; kb < d; kb += 64 * KB) {
+    int4 va[KB][2], vb[KB][2];
 #pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const float* wr = wg + static_cast<int64_t>(n * 8 + g) * d + k0 + 2 * t4;
-      uint32_t h0, l0, h1, l1;
-      split_bf16x2(__ldg(reinterpret_cast<const float2*>(wr)), h0, l0);
-      split_bf16x2(__ldg(reinterpret_cast<const float2*>(wr + 8)), h1, l1);
-      mma_bf16_16816(c[n], a, h0, h1);
-      mma_bf16_16816(c[n], a, l0, l1);
+    for (int u = 0; u < KB; ++u) {
+      const int col = kb + 64 * u + 8 * t4;
+      const bool in = kb + 64 * u < d;
+      va[u][0] = (in && v0) ? __ldg(xr0 + col / 8) : make_int4(0, 0, 0, 0);
+      va[u][1] = (in && v0) ? __ldg(xr0 + col / 8 + 4) : make_int4(0, 0, 0, 0);
+      vb[u][0] = (in && v1) ? __ldg(xr1 + col / 8) : make_int4(0, 0, 0, 0);
+      vb[u][1] = (in && v1) ? __ldg(xr1 + col / 8 + 4) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < KB; ++u) {
+      if (kb + 64 * u >= d) break;
+      const uint32_t* pa = reinterpret_cast<const uint32_t*>(&va[u][0]);  // 8 column pairs
+      const uint32_t* pb = reinterpret_cast<const uint32_t*>(&vb[u][0]);
+#pragma unroll
+      for (int st = 0; st < 4; ++st) {
+        const uint32_t a[4] = {pa[2 * st], pb[2 * st], pa[2 * st + 1], pb[2 * st + 1]};
+        const int wcol = kb + 64 * u + (st < 2 ? 8 * t4 + 4 * st : 32 + 8 * t4 + 4 * (st - 2));
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const float4 wv =
+              __ldg(reinterpret_cast<const float4*>(wg + static_cast<int64_t>(n * 8 + g) * d + wcol));
+          uint32_t h0, l0, h1, l1;
+          split_bf16x2(make_float2(wv.x, wv.y), h0, l0);
+          split_bf16x2(make_float2(wv.z, wv.w), h1, l1);
+          mma_bf16_16816(c[n], a, h0, h1);
+          mma_bf16_16816(c[n], a, l0, l1);
+        }
+      }
     }
   }
   const int lr = warp * 16 + g;
@@ -404,6 +424,36 @@ __device__ __forceinline__ void warp_copy_row(int4* __restrict__ dst, const int4
   for (; i < n16; i += 32) st_v4(dst + i, ld_nc_v4(src + i));
 }
 
+// Two rows at once: 8 x 16 B loads in flight per lane before the stores.
+__device__ __forceinline__ void warp_copy_rows2(int4* __restrict__ d0, const int4* __restrict__ s0,
+                                                int4* __restrict__ d1, const int4* __restrict__ s1,
+                                                int n16) {
+  const int lane = threadIdx.x & 31;
+  int i = lane;
+  for (; i + 96 < n16; i += 128) {
+    int4 a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = ld_nc_v4(s0 + i + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] = ld_nc_v4(s1 + i + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) st_v4(d0 + i + 32 * u, a[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) st_v4(d1 + i + 32 * u, b[u]);
+  }
+  for (; i < n16; i += 32) {
+    const int4 a = ld_nc_v4(s0 + i), b = ld_nc_v4(s1 + i);
+    st_v4(d0 + i, a);
+    st_v4(d1 + i, b);
+  }
+}
+
+// The token-side kernels work in warp batches: the lanes first load / derive the index
+// data of a batch of slots (or tokens) in parallel — one latency instead of one per item —
+// then the warp streams the batch's rows with that data broadcast by shuffles.
+constexpr int kBatch = 4;     // slots per warp batch (dispatch, dispatch_grad)
+constexpr int kTokBatch = 4;  // tokens per warp batch (combine, combine_dx): 4 * K <= 32
+
 __device__ __forceinline__ void warp_zero_rows(char* base, const int32_t* __restrict__ zero_rows,
                                                int n_zero, int64_t row_bytes, int warp_global,
                                                int nwarps) {
@@ -436,27 +486,41 @@ __global__ void __launch_bounds__(256)
   const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
   const int n16 = static_cast<int>(row_bytes / 16);
   const int64_t nslots = T * k;
-  for (int64_t s = warp_global; s < nslots; s += nwarps) {
+  for (int64_t base = static_cast<int64_t>(warp_global) * kBatch; base < nslots;
+       base += static_cast<int64_t>(nwarps) * kBatch) {
     int dst = 0, pos = 0;
-    if (lane == 0) {
-      const int64_t t = s / k;
-      const int e = topk_idx[s];
-      const int r = tile_prefix[(t / kGateTile) * E + e] + slot_rank[s];
+    const int64_t sl = base + lane;
+    if (lane < kBatch && sl < nslots) {
+      const int64_t t = sl / k;
+      const int e = topk_idx[sl];
+      const int r = tile_prefix[(t / kGateTile) * E + e] + slot_rank[sl];
       const int32_t* cum = route_cum + e * (world + 1);
       int dd = 0;
       while (dd + 1 < world && cum[dd + 1] <= r) ++dd;
       dst = dd;
       pos = recv_base[e * world + dd] + (r - cum[dd]);
-      slot_dest[s] = dst;
-      slot_pos[s] = pos;
+      slot_dest[sl] = dst;
+      slot_pos[sl] = pos;
     }
-    dst = __shfl_sync(0xffffffffu, dst, 0);
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    const int64_t t = s / k;
-    const int4* src = reinterpret_cast<const int4*>(x + t * d_model);
-    int4* out = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[dst] + recv_off) +
-                                        static_cast<int64_t>(pos) * row_bytes);
-    warp_copy_row(out, src, n16);
+    const int cnt = static_cast<int>(imin64(kBatch, nslots - base));
+    auto out_row = [&](int i) {
+      const int di = __shfl_sync(0xffffffffu, dst, i), pi = __shfl_sync(0xffffffffu, pos, i);
+      return reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[di] + recv_off) +
+                                     static_cast<int64_t>(pi) * row_bytes);
+    };
+    auto in_row = [&](int i) {
+      return reinterpret_cast<const int4*>(x + ((base + i) / k) * d_model);
+    };
+    int i = 0;
+    for (; i + 1 < cnt; i += 2) {
+      int4* o0 = out_row(i);
+      int4* o1 = out_row(i + 1);
+      warp_copy_rows2(o0, in_row(i), o1, in_row(i + 1), n16);
+    }
+    if (i < cnt) {
+      int4* o0 = out_row(i);
+      warp_copy_row(o0, in_row(i), n16);
+    }
   }
   warp_zero_rows(reinterpret_cast<char*>(peer_bases[rank] + recv_off), zero_rows, n_zero, row_bytes,
                  warp_global, nwarps);
@@ -481,38 +545,71 @@ __device__ __forceinline__ int4 f32_to_bf16x8(const float (&f)[8]) {
   return v;
 }
 
+// Row chunks: a warp walks a row in blocks of 128 x 16 B; a lane holds 4 of them, and the
+// loads of all K rows of a token are issued before any use (one memory latency per token).
+constexpr int kRowBlk = 128;
+
+template <int K>
 __global__ void __launch_bounds__(256)
     combine_kernel(const int32_t* __restrict__ slot_dest, const int32_t* __restrict__ slot_pos,
-                   const float* __restrict__ topk_w, int64_t T, int d_model, int k,
+                   const float* __restrict__ topk_w, int64_t T, int d_model,
                    const uint64_t* __restrict__ peer_bases, int64_t y_off,
                    __nv_bfloat16* __restrict__ y_out) {
+  constexpr int TB = kTokBatch;  // tokens per warp batch (TB * K <= 32)
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
   const int n16 = static_cast<int>(row_bytes / 16);
-  for (int64_t t = warp_global; t < T; t += nwarps) {
-    const int4* rows[kGateMaxK];
-    float w[kGateMaxK];
-    for (int j = 0; j < k; ++j) {
-      const int64_t s = t * k + j;
-      rows[j] = reinterpret_cast<const int4*>(
-          reinterpret_cast<const char*>(peer_bases[slot_dest[s]] + y_off) +
-          static_cast<int64_t>(slot_pos[s]) * row_bytes);
-      w[j] = topk_w[s];
+  for (int64_t base = static_cast<int64_t>(warp_global) * TB; base < T;
+       base += static_cast<int64_t>(nwarps) * TB) {
+    const int64_t sl = base * K + lane;
+    int sd = 0, sp = 0;
+    float sw = 0.f;
+    if (lane < TB * K && sl < T * K) {
+      sd = slot_dest[sl];
+      sp = slot_pos[sl];
+      sw = topk_w[sl];
     }
-    int4* out = reinterpret_cast<int4*>(y_out + t * d_model);
-    for (int c = lane; c < n16; c += 32) {
-      float acc[8];
+    const int cnt = static_cast<int>(imin64(TB, T - base));
+    for (int i = 0; i < cnt; ++i) {
+      const int4* rows[K];
+      float w[K];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-      for (int j = 0; j < k; ++j) {
-        float f[8];
-        bf16x8_to_f32(ld_nc_v4(rows[j] + c), f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w[j], f[i]));
+      for (int j = 0; j < K; ++j) {
+        const int src = i * K + j;
+        rows[j] = reinterpret_cast<const int4*>(
+            reinterpret_cast<const char*>(peer_bases[__shfl_sync(0xffffffffu, sd, src)] + y_off) +
+            static_cast<int64_t>(__shfl_sync(0xffffffffu, sp, src)) * row_bytes);
+        w[j] = __shfl_sync(0xffffffffu, sw, src);
       }
-      out[c] = f32_to_bf16x8(acc);
+      int4* out = reinterpret_cast<int4*>(y_out + (base + i) * d_model);
+      for (int c0 = 0; c0 < n16; c0 += kRowBlk) {
+        int4 v[K][4];
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + lane + 32 * u;
+            v[j][u] = c < n16 ? ld_nc_v4(rows[j] + c) : make_int4(0, 0, 0, 0);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane + 32 * u;
+          if (c >= n16) break;
+          float acc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            float f[8];
+            bf16x8_to_f32(v[j][u], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(w[j], f[q]));
+          }
+          out[c] = f32_to_bf16x8(acc);
+        }
+      }
     }
   }
 }
@@ -532,187 +629,244 @@ __global__ void __launch_bounds__(256)
   const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
   const int n16 = static_cast<int>(row_bytes / 16);
   const int64_t nslots = T * k;
-  for (int64_t s = warp_global; s < nslots; s += nwarps) {
-    const int64_t t = s / k;
-    const int dst = slot_dest[s];
-    const int64_t pos = slot_pos[s];
-    const float w = topk_w[s];
-    const int4* yrow = reinterpret_cast<const int4*>(
-        reinterpret_cast<const char*>(peer_bases[dst] + y_off) + pos * row_bytes);
-    const int4* grow = reinterpret_cast<const int4*>(dy + t * d_model);
-    int4* out = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[dst] + dy_recv_off) +
-                                        pos * row_bytes);
-    float dot = 0.f;
-    for (int c = lane; c < n16; c += 32) {
-      float fy[8], fg[8], o[8];
-      bf16x8_to_f32(ld_nc_v4(yrow + c), fy);
-      bf16x8_to_f32(ld_nc_v4(grow + c), fg);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        dot = fmaf(fg[i], fy[i], dot);
-        o[i] = __fmul_rn(w, fg[i]);
-      }
-      st_v4(out + c, f32_to_bf16x8(o));
+  for (int64_t base = static_cast<int64_t>(warp_global) * kBatch; base < nslots;
+       base += static_cast<int64_t>(nwarps) * kBatch) {
+    const int64_t sl = base + lane;
+    int sd = 0, sp = 0;
+    float sw = 0.f;
+    if (lane < kBatch && sl < nslots) {
+      sd = slot_dest[sl];
+      sp = slot_pos[sl];
+      sw = topk_w[sl];
     }
+    float my_dot = 0.f;  // lane i keeps item i's <dy, Y>
+    const int cnt = static_cast<int>(imin64(kBatch, nslots - base));
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t t = (base + i) / k;
+      const int dst = __shfl_sync(0xffffffffu, sd, i);
+      const int64_t pos = __shfl_sync(0xffffffffu, sp, i);
+      const float w = __shfl_sync(0xffffffffu, sw, i);
+      const int4* yrow = reinterpret_cast<const int4*>(
+          reinterpret_cast<const char*>(peer_bases[dst] + y_off) + pos * row_bytes);
+      const int4* grow = reinterpret_cast<const int4*>(dy + t * d_model);
+      int4* out = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[dst] + dy_recv_off) +
+                                          pos * row_bytes);
+      float dot = 0.f;
+      for (int c0 = 0; c0 < n16; c0 += kRowBlk) {
+        int4 vy[4], vg[4];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-    if (lane == 0) slot_grad[s] = dot;
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane + 32 * u;
+          vy[u] = c < n16 ? ld_nc_v4(yrow + c) : make_int4(0, 0, 0, 0);
+          vg[u] = c < n16 ? ld_nc_v4(grow + c) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane + 32 * u;
+          if (c >= n16) break;
+          float fy[8], fg[8], o[8];
+          bf16x8_to_f32(vy[u], fy);
+          bf16x8_to_f32(vg[u], fg);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            dot = fmaf(fg[q], fy[q], dot);
+            o[q] = __fmul_rn(w, fg[q]);
+          }
+          st_v4(out + c, f32_to_bf16x8(o));
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+      if (lane == i) my_dot = dot;
+    }
+    if (lane < cnt) slot_grad[sl] = my_dot;
   }
   warp_zero_rows(reinterpret_cast<char*>(peer_bases[rank] + dy_recv_off), zero_rows, n_zero,
                  row_bytes, warp_global, nwarps);
   grid_done_then_barrier(grid_counter, peer_bases, flags_off, rank, world, bar_slot, epoch);
 }
 
+template <int K>
 __global__ void __launch_bounds__(256)
     combine_dx_kernel(const int32_t* __restrict__ slot_dest, const int32_t* __restrict__ slot_pos,
                       const int32_t* __restrict__ topk_idx, const float* __restrict__ topk_w,
                       const float* __restrict__ slot_grad, const float* __restrict__ wg, int64_t T,
-                      int d_model, int E, int k, const uint64_t* __restrict__ peer_bases,
-                      int64_t dxe_off, float* __restrict__ dlogit_out,
-                      __nv_bfloat16* __restrict__ dx_out) {
+                      int d_model, const uint64_t* __restrict__ peer_bases, int64_t dxe_off,
+                      float* __restrict__ dlogit_out, __nv_bfloat16* __restrict__ dx_out) {
+  constexpr int TB = kTokBatch;
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int64_t row_bytes = static_cast<int64_t>(d_model) * 2;
   const int n16 = static_cast<int>(row_bytes / 16);
-  for (int64_t t = warp_global; t < T; t += nwarps) {
-    const int4* rows[kGateMaxK];
-    const float* wrow[kGateMaxK];
-    float dl[kGateMaxK];
-    float sg = 0.f;
-    for (int j = 0; j < k; ++j) sg = fmaf(topk_w[t * k + j], slot_grad[t * k + j], sg);
-    for (int j = 0; j < k; ++j) {
-      const int64_t s = t * k + j;
-      dl[j] = topk_w[s] * (slot_grad[s] - sg);
-      rows[j] = reinterpret_cast<const int4*>(
-          reinterpret_cast<const char*>(peer_bases[slot_dest[s]] + dxe_off) +
-          static_cast<int64_t>(slot_pos[s]) * row_bytes);
-      wrow[j] = wg + static_cast<int64_t>(topk_idx[s]) * d_model;
+  for (int64_t base = static_cast<int64_t>(warp_global) * TB; base < T;
+       base += static_cast<int64_t>(nwarps) * TB) {
+    const int64_t sl = base * K + lane;
+    const bool own = lane < TB * K && sl < T * K;
+    int sd = 0, sp = 0, se = 0;
+    float sw = 0.f, sgr = 0.f;
+    if (own) {
+      sd = slot_dest[sl];
+      sp = slot_pos[sl];
+      se = topk_idx[sl];
+      sw = topk_w[sl];
+      sgr = slot_grad[sl];
     }
-    if (lane < k) dlogit_out[t * k + lane] = dl[lane];
-    int4* out = reinterpret_cast<int4*>(dx_out + t * d_model);
-    for (int c = lane; c < n16; c += 32) {
-      float acc[8];
+    // dlogit of this lane's slot: w_j (g_j - sum_i w_i g_i), the sum over its token's slots
+    const int first = (lane / K) * K;
+    float sg = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-      for (int j = 0; j < k; ++j) {
-        float f[8];
-        bf16x8_to_f32(ld_nc_v4(rows[j] + c), f);
-        const float4 w0 = *reinterpret_cast<const float4*>(wrow[j] + c * 8);
-        const float4 w1 = *reinterpret_cast<const float4*>(wrow[j] + c * 8 + 4);
-        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    for (int j = 0; j < K; ++j)
+      sg = fmaf(__shfl_sync(0xffffffffu, sw, (first + j) & 31),
+                __shfl_sync(0xffffffffu, sgr, (first + j) & 31), sg);
+    const float dlv = sw * (sgr - sg);
+    if (own) dlogit_out[sl] = dlv;
+    const int cnt = static_cast<int>(imin64(TB, T - base));
+    for (int i = 0; i < cnt; ++i) {
+      const int4* rows[K];
+      const float* wrow[K];
+      float dl[K];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += f[i] + dl[j] * wv[i];
+      for (int j = 0; j < K; ++j) {
+        const int src = i * K + j;
+        dl[j] = __shfl_sync(0xffffffffu, dlv, src);
+        rows[j] = reinterpret_cast<const int4*>(
+            reinterpret_cast<const char*>(peer_bases[__shfl_sync(0xffffffffu, sd, src)] +
+                                          dxe_off) +
+            static_cast<int64_t>(__shfl_sync(0xffffffffu, sp, src)) * row_bytes);
+        wrow[j] = wg + static_cast<int64_t>(__shfl_sync(0xffffffffu, se, src)) * d_model;
       }
-      out[c] = f32_to_bf16x8(acc);
+      int4* out = reinterpret_cast<int4*>(dx_out + (base + i) * d_model);
+      for (int c0 = 0; c0 < n16; c0 += kRowBlk) {
+        int4 v[K][4];
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + lane + 32 * u;
+            v[j][u] = c < n16 ? ld_nc_v4(rows[j] + c) : make_int4(0, 0, 0, 0);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane + 32 * u;
+          if (c >= n16) break;
+          float acc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            float f[8];
+            bf16x8_to_f32(v[j][u], f);
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(wrow[j] + c * 8));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(wrow[j] + c * 8 + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] += f[q] + dl[j] * wv[q];
+          }
+          out[c] = f32_to_bf16x8(acc);
+        }
+      }
     }
   }
 }
 
-// dWg partials: grid (d/256, ceil(T/FSSDP_WG_TILE)), 16 warps, one 256-token tile x
-// 256-dim chunk per CTA.  The tile's x rows are staged in shared memory (coalesced), its
-// k*256 token-slots are counting-sorted by expert (warp match_any ranks keep token order),
-// and warp w walks only the slot lists of its experts w, w+16, ... accumulating
-// dlogit * x[t] in registers (8 dims per lane).  fp32 order per (e, dim): tokens ascending.
-constexpr int kWgDims = 256;
-constexpr int kWgWarps = 16;
-constexpr int kWgMaxEpw = kGateMaxE / kWgWarps;
-constexpr int kWgSmemBytes = FSSDP_WG_TILE * kWgDims * 2;  // staged x tile (128 KB)
-__global__ void __launch_bounds__(kWgWarps * 32)
+// Streaming partials: a CTA owns kWgCols columns of dWg for a contiguous run of tokens;
+// each thread owns 4 columns and keeps their E accumulators in shared memory (only it
+// touches them: no synchronisation, conflict-free float4 accesses).  x is read once,
+// kWgU tokens of 8-byte loads in flight per thread; the expert of a slot is uniform
+// across the CTA, so the update is one smem read-modify-write per slot and thread.
+constexpr int kWgCols = 512;
+constexpr int kWgThreads = kWgCols / 4;
+constexpr int kWgU = 8;
+__global__ void __launch_bounds__(kWgThreads)
     gate_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
                               const int32_t* __restrict__ topk_idx,
                               const float* __restrict__ dlogit, int64_t T, int d_model, int E,
-                              int k, float* __restrict__ workspace) {
-  extern __shared__ __align__(16) int4 s_x[];  // [FSSDP_WG_TILE][kWgDims / 8]
-  __shared__ int32_t s_tok[FSSDP_WG_TILE * kGateMaxK];   // sorted slot -> local token
-  __shared__ float s_coef[FSSDP_WG_TILE * kGateMaxK];    // sorted slot -> dlogit
-  __shared__ int32_t s_rank[FSSDP_WG_TILE * kGateMaxK];  // slot -> rank within its expert
-  __shared__ int32_t s_cnt[kGateMaxE];
-  __shared__ int32_t s_off[kGateMaxE + 1];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c0 = blockIdx.x * kWgDims;
-  const int64_t t_begin = static_cast<int64_t>(blockIdx.y) * FSSDP_WG_TILE;
-  const int ntok = static_cast<int>(imin64(T, t_begin + FSSDP_WG_TILE) - t_begin);
-  const int nslot = ntok * k;
-  // stage x (all threads, coalesced 16-byte loads)
-  for (int v = threadIdx.x; v < FSSDP_WG_TILE * (kWgDims / 8); v += blockDim.x) {
-    const int r = v / (kWgDims / 8), q = v % (kWgDims / 8);
-    int4 val = make_int4(0, 0, 0, 0);
-    if (r < ntok && c0 + q * 8 < d_model)
-      val = *reinterpret_cast<const int4*>(x + (t_begin + r) * d_model + c0 + q * 8);
-    s_x[v] = val;
+                              int k, int64_t tok_per_cta, float* __restrict__ workspace) {
+  extern __shared__ __align__(16) float4 s_acc[];  // [E][kWgThreads]
+  __shared__ int32_t s_e[FSSDP_WG_TILE * kGateMaxK];
+  __shared__ float s_w[FSSDP_WG_TILE * kGateMaxK];
+  const int c = blockIdx.x * kWgCols + threadIdx.x * 4;
+  const bool col_ok = c < d_model;
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.y) * tok_per_cta;
+  const int ntok = static_cast<int>(imin64(T, t_begin + tok_per_cta) - t_begin);
+  // the run's slots (expert, dlogit) once into smem: broadcast reads in the loop below
+  for (int i = threadIdx.x; i < ntok * k; i += blockDim.x) {
+    s_e[i] = topk_idx[t_begin * k + i];
+    s_w[i] = dlogit[t_begin * k + i];
   }
-  // warp 0: stable counting sort of the tile's slots by expert
-  if (warp == 0) {
-    for (int e = lane; e < E; e += 32) s_cnt[e] = 0;
-    __syncwarp();
-    for (int base = 0; base < nslot; base += 32) {
-      const int s = base + lane;
-      const bool ok = s < nslot;
-      const int e = ok ? topk_idx[t_begin * k + s] : -1;
-      const uint32_t peers = __match_any_sync(0xffffffffu, e);
-      const int r = ok ? s_cnt[e] + __popc(peers & ((1u << lane) - 1u)) : 0;
-      __syncwarp();
-      if (ok && (peers >> lane) == 1u) s_cnt[e] += __popc(peers);
-      __syncwarp();
-      if (ok) s_rank[s] = r;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      int run = 0;
-      for (int e = 0; e < E; ++e) {
-        s_off[e] = run;
-        run += s_cnt[e];
+  float4* my = s_acc + threadIdx.x;
+  for (int e = 0; e < E; ++e) my[e * kWgThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const __nv_bfloat16* xc = x + t_begin * d_model + c;
+  auto load = [&](int t0, uint2 (&v)[kWgU]) {
+#pragma unroll
+    for (int u = 0; u < kWgU; ++u)
+      v[u] = (col_ok && t0 + u < ntok)
+                 ? __ldg(reinterpret_cast<const uint2*>(xc + static_cast<int64_t>(t0 + u) * d_model))
+                 : make_uint2(0u, 0u);
+  };
+  uint2 cur[kWgU], nxt[kWgU];
+  load(0, cur);
+  __syncthreads();
+  for (int t0 = 0; t0 < ntok; t0 += kWgU) {
+    load(t0 + kWgU, nxt);  // next group in flight while this one is accumulated
+#pragma unroll
+    for (int u = 0; u < kWgU; ++u) {
+      if (t0 + u >= ntok) break;
+      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cur[u].x));
+      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cur[u].y));
+      for (int j = 0; j < k; ++j) {
+        const int sl = (t0 + u) * k + j;
+        const int e = s_e[sl];
+        const float w = s_w[sl];
+        float4 a = my[e * kWgThreads];
+        a.x = fmaf(w, lo.x, a.x);
+        a.y = fmaf(w, lo.y, a.y);
+        a.z = fmaf(w, hi.x, a.z);
+        a.w = fmaf(w, hi.y, a.w);
+        my[e * kWgThreads] = a;
       }
-      s_off[E] = run;
     }
-  }
-  __syncthreads();
-  for (int s = threadIdx.x; s < nslot; s += blockDim.x) {
-    const int e = topk_idx[t_begin * k + s];
-    const int dst = s_off[e] + s_rank[s];
-    s_tok[dst] = s / k;
-    s_coef[dst] = dlogit[t_begin * k + s];
-  }
-  __syncthreads();
-  const int c = c0 + lane * 8;
-  if (c >= d_model) return;
-  for (int q = 0; q < kWgMaxEpw; ++q) {
-    const int e = warp + kWgWarps * q;
-    if (e >= E) break;
-    float acc[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-    for (int p = s_off[e]; p < s_off[e + 1]; ++p) {
-      float xv[8];
-      bf16x8_to_f32(s_x[s_tok[p] * (kWgDims / 8) + lane], xv);
-      const float cf = s_coef[p];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = fmaf(cf, xv[i], acc[i]);
-    }
-    float4* out = reinterpret_cast<float4*>(
-        workspace + (static_cast<int64_t>(blockIdx.y) * E + e) * d_model + c);
-    out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    for (int u = 0; u < kWgU; ++u) cur[u] = nxt[u];
   }
+  if (!col_ok) return;
+  for (int e = 0; e < E; ++e)
+    *reinterpret_cast<float4*>(workspace + (static_cast<int64_t>(blockIdx.y) * E + e) * d_model +
+                               c) = my[e * kWgThreads];
 }
 
-__global__ void gate_wgrad_reduce_kernel(const float* __restrict__ workspace, int n_tiles,
-                                         int d_model, int E, float* __restrict__ dwg) {
+// dWg = sum over runs in run order: a CTA owns 32 consecutive outputs (one per lane); its
+// 8 warps sum contiguous eighths of the runs (8 loads in flight each), then warp 0 adds the
+// eight partial sums in warp order.  Deterministic for a given T.
+__global__ void __launch_bounds__(256)
+    gate_wgrad_reduce_kernel(const float* __restrict__ workspace, int n_tiles, int d_model, int E,
+                             float* __restrict__ dwg) {
+  __shared__ float part[8][32];
   const int64_t n = static_cast<int64_t>(E) * d_model;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float s = 0.f;
-    int p = 0;
-    for (; p + 8 <= n_tiles; p += 8) {  // 8 independent loads in flight, summed in order
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const int per = (n_tiles + 7) / 8;
+  const int p0 = warp * per, p1 = min(n_tiles, p0 + per);
+  float s = 0.f;
+  if (i < n) {
+    int p = p0;
+    for (; p + 8 <= p1; p += 8) {
       float v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = workspace[(p + u) * n + i];
 #pragma unroll
       for (int u = 0; u < 8; ++u) s += v[u];
     }
-    for (; p < n_tiles; ++p) s += workspace[p * n + i];
-    dwg[i] = s;
+    for (; p < p1; ++p) s += workspace[p * n + i];
+  }
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && i < n) {
+    float t = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t += part[w][lane];
+    dwg[i] = t;
   }
 }
 
@@ -868,6 +1022,19 @@ static int launch_status() {
   return kOk;
 }
 
+// K-templated launch for the token gathers (K = top-k <= kGateMaxK = 8)
+#define FSSDP_DISPATCH_K(k, KERNEL, GRID, STREAM, ...)               \
+  switch (k) {                                                        \
+    case 1: KERNEL<1><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 2: KERNEL<2><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 3: KERNEL<3><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 4: KERNEL<4><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 5: KERNEL<5><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 6: KERNEL<6><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 7: KERNEL<7><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
+    default: KERNEL<8><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break; \
+  }
+
 static int grid_for_warps(int64_t work_items) {
   // persistent grid-stride: up to 4 CTAs of 8 warps per SM
   int64_t blocks = (work_items + 7) / 8;
@@ -893,7 +1060,7 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
   }
   if (T == 0) return kOk;
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
-  if (E % 8 == 0 && d % 16 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
+  if (E % 8 == 0 && d % 64 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
     auto mma_launch = [&](auto kern) {
       kern<<<tiles, 128, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(x), wg, bias,
                                                   T, d, E, k, logits, topk_idx, topk_w, slot_rank,
@@ -980,7 +1147,7 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
     set_error("dispatch: bad shape");
     return kErrDimension;
   }
-  const int grid = grid_for_warps(T * k);
+  const int grid = grid_for_warps((T * k + kBatch - 1) / kBatch);  // one warp per batch
   dispatch_kernel<<<grid, 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(x), topk_idx, slot_rank, tile_prefix, T, d_model, E, k,
       world, route_cum, recv_base, slot_dest, slot_pos, peer_bases, recv_off, zero_rows, n_zero,
@@ -991,14 +1158,14 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
 int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float* topk_w, int64_t T,
                   int32_t d_model, int32_t k, const uint64_t* peer_bases, int64_t y_off,
                   void* y_out, void* stream) {
-  if (d_model % 8 != 0 || k > kGateMaxK) {
+  if (d_model % 8 != 0 || k <= 0 || k > kGateMaxK) {
     set_error("combine: bad shape");
     return kErrDimension;
   }
   if (T == 0) return kOk;
-  combine_kernel<<<grid_for_warps(T), 256, 0, as_stream(stream)>>>(
-      slot_dest, slot_pos, topk_w, T, d_model, k, peer_bases, y_off,
-      static_cast<__nv_bfloat16*>(y_out));
+  const int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
+  FSSDP_DISPATCH_K(k, combine_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_w, T,
+                   d_model, peer_bases, y_off, static_cast<__nv_bfloat16*>(y_out));
   return launch_status();
 }
 
@@ -1012,7 +1179,7 @@ int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t*
     set_error("dispatch_grad: bad shape");
     return kErrDimension;
   }
-  dispatch_grad_kernel<<<grid_for_warps(T * k), 256, 0, as_stream(stream)>>>(
+  dispatch_grad_kernel<<<grid_for_warps((T * k + kBatch - 1) / kBatch), 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(dy), slot_dest, slot_pos, topk_w, T, d_model, k,
       peer_bases, y_off, dy_recv_off, slot_grad, zero_rows, n_zero, flags_off, rank, world,
       bar_slot, epoch, grid_counter);
@@ -1023,42 +1190,49 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
                      const float* topk_w, const float* slot_grad, const float* wg, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
                      int64_t dxe_off, float* dlogit_out, void* dx_out, void* stream) {
-  if (d_model % 8 != 0 || k > kGateMaxK || E > kGateMaxE) {
+  if (d_model % 8 != 0 || k <= 0 || k > kGateMaxK || E > kGateMaxE) {
     set_error("combine_dx: bad shape");
     return kErrDimension;
   }
   if (T == 0) return kOk;
-  combine_dx_kernel<<<grid_for_warps(T), 256, 0, as_stream(stream)>>>(
-      slot_dest, slot_pos, topk_idx, topk_w, slot_grad, wg, T, d_model, E, k, peer_bases, dxe_off,
-      dlogit_out, static_cast<__nv_bfloat16*>(dx_out));
+  const int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
+  FSSDP_DISPATCH_K(k, combine_dx_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_idx,
+                   topk_w, slot_grad, wg, T, d_model, peer_bases, dxe_off, dlogit_out,
+                   static_cast<__nv_bfloat16*>(dx_out));
   return launch_status();
 }
 
 int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
                      void* stream) {
-  if (E > kGateMaxE || d_model <= 0 || d_model % 8 != 0 || k > kGateMaxK) {
+  if (E > kGateMaxE || d_model <= 0 || d_model % 4 != 0 || k > kGateMaxK) {
     set_error("gate_wgrad: bad shape");
     return kErrDimension;
   }
-  const int n_tiles = static_cast<int>((T + FSSDP_WG_TILE - 1) / FSSDP_WG_TILE);
+  // fixed FSSDP_WG_TILE-token runs (the partition, hence the fp32 grouping, depends only on
+  // the token index), reduced in run order
+  const int col_blocks = (d_model + kWgCols - 1) / kWgCols;
+  const int64_t tok_per_cta = FSSDP_WG_TILE;
+  const int n_tiles = static_cast<int>((T + tok_per_cta - 1) / tok_per_cta);
   if (n_tiles > 0) {
-    static bool configured = false;
-    if (!configured) {
+    const int smem = E * kWgThreads * static_cast<int>(sizeof(float4));
+    static int configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
       if (cudaFuncSetAttribute(gate_wgrad_partial_kernel,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, kWgSmemBytes) !=
-          cudaSuccess)
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return launch_status();
-      configured = true;
+      configured = smem;
     }
-    dim3 grid((d_model + kWgDims - 1) / kWgDims, n_tiles);
-    gate_wgrad_partial_kernel<<<grid, kWgWarps * 32, kWgSmemBytes, as_stream(stream)>>>(
-        static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, workspace);
+    dim3 grid(col_blocks, n_tiles);
+    gate_wgrad_partial_kernel<<<grid, kWgThreads, smem, as_stream(stream)>>>(
+        static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, tok_per_cta,
+        workspace);
     int rc = launch_status();
     if (rc != kOk) return rc;
   }
-  gate_wgrad_reduce_kernel<<<num_sms(), 256, 0, as_stream(stream)>>>(workspace, n_tiles, d_model,
-                                                                      E, dwg_out);
+  const int64_t n_out = static_cast<int64_t>(E) * d_model;
+  gate_wgrad_reduce_kernel<<<static_cast<unsigned>((n_out + 31) / 32), 256, 0, as_stream(stream)>>>(
+      workspace, n_tiles, d_model, E, dwg_out);
   return launch_status();
 }
 

@@ -1218,12 +1218,17 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
     for (int dd = 0; dd < D; ++dd) holders += holds(e, dd);
     return holders > 1;
   };
+  // each part longest-first (K = segment rows): the GEMM's snake tile order then deals
+  // the tiles out close to LPT
   std::vector<int> wg_order;
   for (int s = 0; s < n_slots; ++s)
     if (shared(s)) wg_order.push_back(s);
   const int n_shared = static_cast<int>(wg_order.size());
   for (int s = 0; s < n_slots; ++s)
     if (!shared(s)) wg_order.push_back(s);
+  auto longer = [&](int a, int b) { return seg_pad[rank][a] > seg_pad[rank][b]; };
+  std::stable_sort(wg_order.begin(), wg_order.begin() + n_shared, longer);
+  std::stable_sort(wg_order.begin() + n_shared, wg_order.end(), longer);
   const int64_t d = d_model, f = d_ff;
   const int n_tiles[6] = {static_cast<int>(f / 256), static_cast<int>(d / 256),
                           static_cast<int>(f / 256), static_cast<int>(d / 256),

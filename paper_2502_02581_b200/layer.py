@@ -28,7 +28,7 @@ from .engine import FssdpPlanner
 from .errors import DimensionError, InternalError
 from .plan_tables import NativeTables
 
-WG_TILE = 256  # FSSDP_WG_TILE (include/fssdp.h)
+WG_TILE = 64  # FSSDP_WG_TILE (include/fssdp.h)
 GROUP_BYTES = N.C.sizeof(N.GemmGroup)  # fssdp_gemm_group
 
 # barrier slots (flag pads) used by one layer; layer i uses base + 8*i

@@ -122,7 +122,9 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * 2 * f, f // 64, 0, st * d)
     out["dgrad1"] = _finalize(g.copy(), d // 256)
-    order = [i for i in range(n) if shared[i]] + [i for i in range(n) if not shared[i]]
+    # each part longest-first (stable): the GEMM's snake tile order is then close to LPT
+    order = (sorted([i for i in range(n) if shared[i]], key=lambda i: -int(seg_padded[i])) +
+             sorted([i for i in range(n) if not shared[i]], key=lambda i: -int(seg_padded[i])))
     n_sh = sum(shared)
     split = [n_sh]
     for name, rows, n_t, extra in (("wgrad1", f, d // 256, 0), ("wgrad2", d, f // 256, f * d)):

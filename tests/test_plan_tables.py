@@ -150,7 +150,9 @@ def test_wgrad_shared_prefix_covers_every_sprs_input():
             by_slot = {s: e for e, s in t.slots.items()}
             shared = [s for s in range(len(t.slots))
                       if np.count_nonzero(dec.target.mask[by_slot[s]]) > 1]
-            order = shared + [s for s in range(len(t.slots)) if s not in shared]
+            rest = [s for s in range(len(t.slots)) if s not in shared]
+            order = (sorted(shared, key=lambda s: -int(t.seg_padded[s])) +
+                     sorted(rest, key=lambda s: -int(t.seg_padded[s])))
             assert n_sh == len(shared)
             for name, t_sh, extra in (("wgrad1", t1, 0), ("wgrad2", t2, f_ * d_)):
                 arr, n_tiles, total = t.groups[name]
