@@ -274,7 +274,7 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         step(x, dy)
     barrier()
-    layer.timers = {}
+    layer.timers = None  # the timed region runs uninstrumented
     NAT.launch_count = 0
     start, end = torch.cuda.Event(True), torch.cuda.Event(True)
     with ClockSampler(local) as clocks:
@@ -286,7 +286,15 @@ def run_ours(args):
         barrier()
     launches = NAT.launch_count
     ms = start.elapsed_time(end) / args.steps
+    # a second, instrumented pass of the same K steps: CUDA events around every kernel
+    # (phase breakdown, the GEMM roofline) and host timestamps on the planning path
+    layer.timers = {}
+    barrier()
+    for _ in range(args.steps):
+        step(x, dy)
+    barrier()
     timers = layer.timers
+    marks = timers.pop("marks", [])
     if os.environ.get("FSSDP_TIMELINE"):
         # last timed step's kernels as (start, end) ms from the step's first kernel, one
         # file per rank: $FSSDP_TIMELINE_n{world}_r{rank}.json
@@ -348,6 +356,13 @@ def run_ours(args):
                 "gemm_launches_per_step": gemm_launches / args.steps,
                 "host_plan_ms_per_step": float(allr[:, 6].max())}
     # per-phase device time (CUDA events around every kernel of the timed steps), max over ranks
+    # host planning path: mean microseconds between consecutive marks of a step
+    host_us = {}
+    for (n0, t0), (n1, t1) in zip(marks, marks[1:]):
+        if n1 == "readback":
+            continue  # next step
+        key = f"{n0}->{n1}"
+        host_us[key] = host_us.get(key, 0.0) + (t1 - t0) * 1e6 / args.steps
     keys = sorted(k for k in timers if k != "host_plan_s")
     if world > 1:  # ranks may launch different phases (e.g. no SpAG copies): use the union
         allk = [None] * world
@@ -384,7 +399,8 @@ def run_ours(args):
         dxh = [torch.empty_like(xh).pin_memory() for _ in range(2)]
         xb = [torch.empty_like(x) for _ in range(2)]
         dyb = [torch.empty_like(dy) for _ in range(2)]
-        copy_s = torch.cuda.Stream(device=dev)
+        copy_s = torch.cuda.Stream(device=dev)   # H2D
+        d2h_s = torch.cuda.Stream(device=dev)    # D2H: PCIe is full duplex
         main_s = torch.cuda.current_stream(dev)
         in_ev = [torch.cuda.Event() for _ in range(2)]
         done_ev = [torch.cuda.Event() for _ in range(2)]
@@ -408,11 +424,12 @@ def run_ours(args):
                 done_ev[b].record(main_s)
                 if i + 1 < n:
                     prefetch(i + 1)
-                with torch.cuda.stream(copy_s):
-                    copy_s.wait_event(done_ev[b])
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(done_ev[b])
                     dxh[b].copy_(dx, non_blocking=True)
-                    dx.record_stream(copy_s)
+                    dx.record_stream(d2h_s)
             main_s.wait_stream(copy_s)
+            main_s.wait_stream(d2h_s)
 
         run(2)
         barrier()
@@ -429,8 +446,8 @@ def run_ours(args):
         nb = T * CFG2["d_model"] * 2
         e2e = {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": nb, "ms_per_step": e2e_ms,
-               "pipeline": "H2D of step i+1 and D2H of step i on a copy stream, overlapped "
-                           "with step compute (FssdpMoE.forward/backward)"}
+               "pipeline": "H2D of step i+1 and D2H of step i on two copy streams (PCIe full "
+                           "duplex), overlapped with step compute (FssdpMoE.forward/backward)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -445,7 +462,8 @@ def run_ours(args):
                 "data": "synthetic (seeded N(0,1) tokens, random-init experts, Zipf gate bias)",
                 "config": _config(args, world), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
-                "phase_ms_per_step": breakdown}
+                "phase_ms_per_step": breakdown,
+                "host_plan_path_us": {k: round(v, 1) for k, v in host_us.items()}}
         if sparse:
             line["sparse_collectives"] = sparse
         print(json.dumps(line), flush=True)

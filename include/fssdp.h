@@ -195,6 +195,17 @@ int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_exper
                             const uint8_t* pre_mask, const int64_t* route, int32_t d_model,
                             int32_t d_ff, uint8_t* blob, int64_t blob_bytes, int32_t* header_out);
 
+/* The planning critical path in one call: fssdp_plan_layer on this rank's all-gathered
+ * int32 counts [D*E], then fssdp_build_rank_tables for `rank` into the pinned `blob`, then
+ * (if blob_dev) its upload on `stream`.  Outputs as the two calls'. */
+int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
+                            const int32_t* counts, const fssdp_topology* topo,
+                            const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
+                            int32_t d_model, int32_t d_ff, uint8_t* target_out, int32_t* added_out,
+                            int64_t* route_out, double* doubles_out, int32_t* flags_out,
+                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out, void* blob_dev,
+                            void* stream);
+
 /* The estimate-based, adoption-gated materialization alone (engine.py:497-501 with
  * _adopt_materialization engine.py:406-429): depends only on the load history, so its
  * SparseAllGather can start before the gate.  fssdp_plan_layer's final target is either

@@ -96,6 +96,35 @@ const char* fssdp_last_error(void) { return g_last_error.c_str(); }
 
 int fssdp_num_sms(void) { return num_sms(); }
 
+int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
+                            const int32_t* counts, const fssdp_topology* topo,
+                            const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
+                            int32_t d_model, int32_t d_ff, uint8_t* target_out, int32_t* added_out,
+                            int64_t* route_out, double* doubles_out, int32_t* flags_out,
+                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out, void* blob_dev,
+                            void* stream) {
+  if (topo == nullptr || counts == nullptr || num_experts <= 0) {
+    set_error("plan_layer_tables: bad arguments");
+    return kErrDimension;
+  }
+  const int64_t D = static_cast<int64_t>(topo->nodes) * topo->devices_per_node;
+  int64_t actual[64 * 64];  // D <= kMaxWorld (32), E <= 64
+  if (D <= 0 || D * num_experts > 64 * 64) {
+    set_error("plan_layer_tables: too many devices x experts");
+    return kErrDimension;
+  }
+  for (int64_t i = 0; i < D * num_experts; ++i) actual[i] = counts[i];
+  int rc = fssdp_plan_layer(num_experts, base_owner, est, actual, topo, knobs, target_out,
+                            added_out, route_out, doubles_out, flags_out);
+  if (rc != kOk) return rc;
+  rc = fssdp_build_rank_tables(rank, static_cast<int32_t>(D), num_experts, base_owner, target_out,
+                               pre_mask, route_out, d_model, d_ff, blob, blob_bytes, header_out);
+  if (rc != kOk || blob_dev == nullptr) return rc;
+  int64_t offs[FSSDP_TAB_NSECTIONS], total = 0;
+  fssdp_tables_layout(num_experts, static_cast<int32_t>(D), offs, &total);
+  return fssdp_copy(blob_dev, blob, total, stream, 0);
+}
+
 int fssdp_copy(void* dst, const void* src, int64_t bytes, void* stream, int32_t synchronize) {
   if (bytes < 0 || (bytes > 0 && (dst == nullptr || src == nullptr))) {
     set_error("copy: bad arguments");

@@ -305,25 +305,54 @@ class FssdpPlanner:
             raise TraceMismatchError(f"counts {act.shape} do not match {D} devices x {E} experts")
         np.copyto(sc.act, act, casting="unsafe")
         owner_ptr = self._owners_ptr(layer)
+        knobs, est_ptr = self._layer_knobs(layer)
+        N.check(N.LIB_RAW.fssdp_plan_layer(
+            E, owner_ptr, est_ptr, sc.p_act, sc.topo_ref(self._topo_c), N.C.byref(knobs),
+            sc.p_target, sc.p_added, sc.p_route, sc.p_dbl, sc.p_flags), "plan_layer")
+        self.last_target_ptr, self.last_route_ptr = sc.p_target, sc.p_route
+        return self._decision(base, sc)
+
+    def _layer_knobs(self, layer: int):
         if self.policy.kind == PolicyKind.EP:
             knobs = self.__dict__.get("_ep_knobs")
             if knobs is None:
                 knobs = self._ep_knobs = N.LayerKnobs(
                     0, 0, 0, 0, self._knobs.expert_bytes, self._knobs.token_bytes,
                     self._knobs.attn_fwd_time, self._knobs.per_token_expert_time)
-            est_ptr = None
-        else:
-            knobs = self._knobs
-            est_ptr = self._estimate_ptr(layer)
-        N.check(N.LIB_RAW.fssdp_plan_layer(
-            E, owner_ptr, est_ptr, sc.p_act, sc.topo_ref(self._topo_c), N.C.byref(knobs),
-            sc.p_target, sc.p_added, sc.p_route, sc.p_dbl, sc.p_flags), "plan_layer")
-        self.last_target_ptr, self.last_route_ptr = sc.p_target, sc.p_route
+            return knobs, None
+        return self._knobs, self._estimate_ptr(layer)
+
+    @staticmethod
+    def _decision(base, sc) -> LayerDecision:
         dbl, flags = sc.dbl.tolist(), sc.flags.tolist()
         return LayerDecision(base=base, target=ChunkPlacement.from_mask(sc.target.copy(), copy=False),
                              added_per_device=tuple(sc.added.tolist()), route=sc.route.copy(),
                              spag_latency=dbl[0], sprs_latency=dbl[1], remat_latency=dbl[2],
                              calib_time=dbl[3], adopted=bool(flags[0]), calibrated=bool(flags[1]))
+
+    def plan_with_tables(self, layer: int, counts, counts_ptr: int, rank: int, pre_ptr,
+                         d_model: int, d_ff: int, blob, blob_ptr: int, header_ptr: int,
+                         blob_dev_ptr, stream) -> LayerDecision:
+        """plan() fused with this rank's device tables and their upload: one native call on
+        the planning critical path (fssdp_plan_layer_tables).  `counts` is the (D, E) int32
+        host array at counts_ptr."""
+        if self._step is None:
+            self.begin_iteration()
+            self._step = [None] * self.config.layers
+        base = self.shards.per_layer[layer]
+        E, D = base.num_chunks, base.num_devices
+        if counts.shape != (D, E):
+            raise TraceMismatchError(f"counts {counts.shape} do not match {D} devices x {E} experts")
+        self._step[layer] = counts.astype(np.int64)
+        sc = self._scratch(layer)
+        knobs, est_ptr = self._layer_knobs(layer)
+        N.check(N.LIB_RAW.fssdp_plan_layer_tables(
+            E, self._owners_ptr(layer), est_ptr, counts_ptr, sc.topo_ref(self._topo_c),
+            N.C.byref(knobs), rank, pre_ptr, d_model, d_ff, sc.p_target, sc.p_added, sc.p_route,
+            sc.p_dbl, sc.p_flags, blob_ptr, len(blob), header_ptr, blob_dev_ptr, stream),
+            "plan_layer_tables")
+        self.last_target_ptr, self.last_route_ptr = sc.p_target, sc.p_route
+        return self._decision(base, sc)
 
     def _owners_ptr(self, layer: int) -> int:
         self._owners(layer)  # refreshes the cache for the current ShardPlan

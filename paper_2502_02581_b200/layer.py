@@ -14,6 +14,7 @@ on one GPU (PeerGroup mode "emulated") — the multi-rank parity tests do that.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import time
 from dataclasses import dataclass
@@ -182,6 +183,9 @@ class FssdpMoE:
         self._pre_staged = None   # event after the H2D of pre_host (before it is rewritten)
         self.decision = None
         self.tables = None
+        self._cs = None  # launching stream during forward()/backward()
+        self._tab_ptrs = None
+        self._pb_c = C.c_void_p(self.group.peer_bases.data_ptr())
         self.T = 0
         self.x = None
         self._owned_expert_ids = None
@@ -204,6 +208,7 @@ class FssdpMoE:
             self.params[s, : f * d].copy_(w1.reshape(-1))
             self.params[s, f * d:].copy_(w2.reshape(-1))
         self._owned_expert_ids = self.owned_experts()
+        self._n_owned = len(self._owned_expert_ids)
 
     def make_expert(self, e: int, seed: int):
         d, f = self.g.d_model, self.g.d_ff
@@ -227,17 +232,27 @@ class FssdpMoE:
 
     # ------------------------------------------------------------ helpers
     def _stream(self):
-        return C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+        """The launching stream (resolved once per forward / backward call: looking up
+        torch's current stream costs microseconds on the planning critical path)."""
+        cs = self._cs
+        if cs is None:
+            cs = C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+        return cs
 
     def _bar(self, which: int):
         slot, epoch = self.group.barrier_args(self.bar_base + which)
         return slot, epoch
 
     def _tab(self, name: str) -> C.c_void_p:
-        return C.c_void_p(self.blob_dev.data_ptr() + self.packed.offsets[name])
+        ptrs = self._tab_ptrs
+        if ptrs is None or ptrs[0] is not self.packed.offsets:  # layout is per (E, D)
+            offs = self.packed.offsets
+            ptrs = self._tab_ptrs = (offs, {k: C.c_void_p(self.blob_dev_ptr + v)
+                                            for k, v in offs.items()})
+        return ptrs[1][name]
 
     def _pb(self) -> C.c_void_p:
-        return C.c_void_p(self.group.peer_bases.data_ptr())
+        return self._pb_c
 
     # ------------------------------------------------------------ forward phases
     # Early SpAG: the estimate-based candidate (engine.py:497-501) depends only on the
@@ -322,15 +337,24 @@ class FssdpMoE:
     def phase_plan(self) -> None:
         # host sync point #1: pinned copy of the all-gathered counts (raw cudaMemcpyAsync +
         # stream sync: the torch copy/event path costs tens of microseconds here)
+        self._mark("readback")
         N.check(N.LIB_RAW.fssdp_copy(self.counts_host_ptr, self.counts_dev_ptr,
                                      self.counts_nbytes, self._stream(), 1), "counts readback")
         t_host = time.perf_counter()
+        self._mark("synced")
         self._plan_tables(self.counts_host_np)
         if self.timers is not None:
             self.timers.setdefault("host_plan_s", []).append(time.perf_counter() - t_host)
 
     def _plan_tables(self, counts) -> None:
-        dec = self.planner.plan(self.layer, counts)
+        # plan + this rank's tables + their upload (boundary #2): one native call
+        E, D = self.g.num_experts, self.world
+        dec = self.planner.plan_with_tables(
+            self.layer, counts, self.counts_host_ptr, self.rank, self.pre_mask_ptr,
+            self.g.d_model, self.g.d_ff, self.blob_host_np, self.blob_host_ptr,
+            NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream())
+        self._mark("planned")
+        tables = NativeTables.from_header(E, D, self.blob_host_np)
         target = dec.target.mask  # 0/1 uint8, like pre_mask
         pre = self.pre_mask
         if pre is not None and np.any(pre > target):
@@ -339,32 +363,27 @@ class FssdpMoE:
             if np.any(target > dec.base.mask):
                 raise InternalError("final placement is neither a superset of the early one "
                                     "nor the bare partition")
-        # native table build from the planner's scratch copies of target/route, straight into
-        # the pinned staging buffer, one H2D copy
-        pl = self.planner
-        tables = NativeTables.from_pointers(
-            self.rank, target.shape[0], target.shape[1], pl._owners_ptr(self.layer),
-            pl.last_target_ptr, self.pre_mask_ptr, pl.last_route_ptr, self.g.d_model,
-            self.g.d_ff, self.blob_host_np, self.blob_host_ptr)
         if tables.n_slots > self.g.slots:
             raise InternalError(f"plan needs {tables.n_slots} slots > capacity {self.g.slots}")
         if tables.recv_rows > self.g.recv_cap:
             raise InternalError("receive rows exceed capacity")
         if tables.n_stage > self.g.stage_slots:
             raise InternalError(f"plan needs {tables.n_stage} staging slots > {self.g.stage_slots}")
-        if tables.n_owned != len(self._owned_expert_ids) or \
-                list(tables.slot_expert[:tables.n_owned]) != self._owned_expert_ids:
+        if tables.n_owned != self._n_owned or (
+                self.planner.last_reshard_moves and
+                list(tables.slot_expert[:tables.n_owned]) != self._owned_expert_ids):
             raise InternalError("ownership changed without a re-shard data move")
         self.decision, self.tables = dec, tables
         self.packed = tables
-        N.check(N.LIB_RAW.fssdp_copy(self.blob_dev_ptr, self.blob_host_ptr, tables.nbytes,
-                                     self._stream(), 0), "plan tables upload")  # boundary #2
         self.gemm = tables.gemm
+        self._mark("tables")
 
     def phase_spag(self, refetch_early: bool = False) -> None:
         """The SpAG of the final plan's replicas not fetched early; the main stream then
         waits for the early SpAG.  `refetch_early` (rematerialization in backward) also
         re-pulls the early replicas."""
+        if self._pre_done is None and not self.tables.n_spag and not refetch_early:
+            return
         main = torch.cuda.current_stream(self.dev)
         if self._pre_done is not None:
             main.wait_event(self._pre_done)
@@ -389,6 +408,11 @@ class FssdpMoE:
     # the launching stream around each kernel launch; None disables it.
     timers = None
 
+    def _mark(self, name: str) -> None:
+        """Host timestamp of a planning-path point (bench.py's host breakdown)."""
+        if self.timers is not None:
+            self.timers.setdefault("marks", []).append((name, time.perf_counter()))
+
     def _timed(self, key, fn):
         if self.timers is None:
             fn()
@@ -407,7 +431,10 @@ class FssdpMoE:
 
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
-        self._timed(name[6:], lambda: N.call(name, *args))
+        if self.timers is None:
+            N.call(name, *args)
+        else:
+            self._timed(name[6:], lambda: N.call(name, *args))
 
     def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None, part=None):
         """One grouped GEMM of the plan; `part` "shared" / "rest" launches the wgrad prefix
@@ -511,17 +538,32 @@ class FssdpMoE:
 
     # ------------------------------------------------------------ one rank per process
     def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self._cs = C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+        try:
+            return self._forward(x)
+        finally:
+            self._cs = None
+
+    def _forward(self, x: torch.Tensor) -> torch.Tensor:
         self.phase_prefetch()
         self.phase_gate(x)
         self.phase_counts()
         self.phase_plan()
         self.phase_spag()
         self.phase_dispatch()
+        self._mark("dispatch_launched")
         self.phase_experts_fwd()
         self.phase_barrier(BAR_Y)
         return self.phase_combine()
 
     def backward(self, dy: torch.Tensor, rematerialize: bool | None = None) -> torch.Tensor:
+        self._cs = C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+        try:
+            return self._backward(dy, rematerialize)
+        finally:
+            self._cs = None
+
+    def _backward(self, dy: torch.Tensor, rematerialize: bool | None) -> torch.Tensor:
         self.phase_dispatch_grad(dy)
         remat = self.planner.policy.rematerialize if rematerialize is None else rematerialize
         if remat:
@@ -540,7 +582,7 @@ class FssdpMoE:
             main = torch.cuda.current_stream(self.dev)
             side = self._side_stream()
             side.wait_stream(main)
-            with torch.cuda.stream(side):
+            with self._on(side):
                 self.phase_barrier(BAR_SPRS)
                 self.phase_sprs()
             self.phase_bwd_rest()
@@ -550,6 +592,17 @@ class FssdpMoE:
             main.wait_stream(side)
         self.phase_barrier(BAR_END)
         return dx
+
+    @contextlib.contextmanager
+    def _on(self, stream: torch.cuda.Stream):
+        """Launch the enclosed phases on `stream` (torch's current stream and _stream())."""
+        prev = self._cs
+        self._cs = C.c_void_p(stream.cuda_stream)
+        try:
+            with torch.cuda.stream(stream):
+                yield
+        finally:
+            self._cs = prev
 
     def _side_stream(self) -> torch.cuda.Stream:
         if getattr(self, "_side", None) is None:

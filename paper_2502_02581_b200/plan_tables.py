@@ -266,6 +266,26 @@ class NativeTables:
                    blob_ptr)
         return obj
 
+    @classmethod
+    def from_header(cls, E, D, blob) -> "NativeTables":
+        """Tables a fused native call (fssdp_plan_layer_tables) already wrote into `blob`,
+        its header in NativeTables._hdr."""
+        obj = cls.__new__(cls)
+        obj.E, obj.D = E, D
+        obj.offsets, obj.nbytes = _layout(E, D)
+        obj.blob = blob
+        obj._parse_header()
+        return obj
+
+    def _parse_header(self) -> None:
+        h = self._hdr.tolist()
+        (self.n_slots, self.n_owned, self.recv_rows, self.n_zero, self.n_spag, self.n_sprs_jobs,
+         self.n_sprs_srcs) = h[:7]
+        self.gemm = {name: (h[7 + 3 * i], h[8 + 3 * i], h[9 + 3 * i])
+                     for i, name in enumerate(GEMM_NAMES)}
+        self.wgrad_split = (h[25], h[26], h[27])
+        self.n_stage = h[28]
+
     def _build(self, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
                blob_ptr) -> None:
         from . import _native as N
@@ -278,13 +298,7 @@ class NativeTables:
         N.check(N.LIB_RAW.fssdp_build_rank_tables(rank, D, E, owner_ptr, mask_ptr, pre_ptr,
                                                   route_ptr, d_model, d_ff, blob_ptr, self.nbytes,
                                                   self._hdr_ptr), "build_rank_tables")
-        h = self._hdr.tolist()
-        (self.n_slots, self.n_owned, self.recv_rows, self.n_zero, self.n_spag, self.n_sprs_jobs,
-         self.n_sprs_srcs) = h[:7]
-        self.gemm = {name: (h[7 + 3 * i], h[8 + 3 * i], h[9 + 3 * i])
-                     for i, name in enumerate(GEMM_NAMES)}
-        self.wgrad_split = (h[25], h[26], h[27])
-        self.n_stage = h[28]
+        self._parse_header()
 
     def section(self, name, dtype, count):
         off = self.offsets[name]
