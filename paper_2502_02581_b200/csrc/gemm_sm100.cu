@@ -76,30 +76,58 @@ struct GemmSmem {
 };
 
 // tanh.approx (MUFU) is below bf16 output resolution; parity is tolerance-based.
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
-  const float k1 = 0.044715f;
-  const float u = k0 * fmaf(k1 * x * x, x, x);
-  const float hx = 0.5f * x;
-  return fmaf(hx, tanh_approx(u), hx);
-}
-
-// GeLU and its derivative from one tanh (fwd1 saves gelu'(a) for dgrad2's epilogue).
-__device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
-  const float k0 = 0.7978845608028654f;
-  const float k1 = 0.044715f;
-  const float x2 = x * x;
-  const float t = tanh_approx(k0 * fmaf(k1 * x2, x, x));
-  const float hx = 0.5f * x;
-  g = fmaf(hx, t, hx);
-  dg = fmaf(0.5f, 1.0f + t, hx * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f));
-}
 
 // Work order of a persistent CTA (pair): round r takes tile r*units + unit, in reverse
 // CTA order on odd rounds ("snake").  With groups listed by descending cost (wgrad: K =
 // segment rows), this deals the tiles out close to longest-processing-time-first.
 __device__ __forceinline__ int snake_tile(int round, int unit, int units) {
   return round * units + ((round & 1) ? units - 1 - unit : unit);
+}
+
+// Packed fp32x2 (FFMA2 / FMUL2 on sm_100): the GeLU epilogue works on element pairs, which
+// halves its FP instruction count — it is the limiter of the fwd1 tile loop.
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t r) {
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(r));
+  return f;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// gelu and gelu' of an element pair from one tanh each:
+//   t = tanh(k0 (x + k1 x^3)),  gelu = hx (1 + t),
+//   gelu' = 0.5 (1 + t) + hx (1 - t^2) (k0 + 3 k0 k1 x^2)
+__device__ __forceinline__ void gelu_and_grad2(uint64_t x, uint64_t& g, uint64_t& dg) {
+  constexpr float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const uint64_t one = f2_pack(1.f, 1.f), half = f2_pack(0.5f, 0.5f);
+  const uint64_t x2 = f2_mul(x, x);
+  const uint64_t v = f2_fma(f2_mul(f2_pack(k1, k1), x2), x, x);
+  const float2 a = f2_unpack(f2_mul(f2_pack(k0, k0), v));
+  const uint64_t t = f2_pack(tanh_approx(a.x), tanh_approx(a.y));
+  const uint64_t hx = f2_mul(half, x);
+  g = f2_fma(hx, t, hx);
+  const uint64_t q = f2_fma(f2_mul(t, f2_pack(-1.f, -1.f)), t, one);  // 1 - t^2
+  const uint64_t w = f2_fma(f2_pack(3.f * k1 * k0, 3.f * k1 * k0), x2, f2_pack(k0, k0));
+  dg = f2_fma(half, f2_add(one, t), f2_mul(f2_mul(hx, q), w));
 }
 
 struct TileCoord {
@@ -412,11 +440,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             __nv_bfloat162 act[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {  // one tanh feeds both GeLU and GeLU'
-              float g0, d0, g1, d1;
-              gelu_and_grad(__uint_as_float(r[2 * i]), g0, d0);
-              gelu_and_grad(__uint_as_float(r[2 * i + 1]), g1, d1);
-              act[i] = __floats2bfloat162_rn(g0, g1);
-              out[i] = __floats2bfloat162_rn(d0, d1);
+              uint64_t g2, d2;
+              gelu_and_grad2(f2_pack(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                             g2, d2);
+              const float2 gf = f2_unpack(g2), df = f2_unpack(d2);
+              act[i] = __floats2bfloat162_rn(gf.x, gf.y);
+              out[i] = __floats2bfloat162_rn(df.x, df.y);
             }
             uint8_t* xb = xbuf0 + b * S::kBufBytes;
 #pragma unroll
@@ -427,8 +456,10 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float2 p = __bfloat1622float2(pre[i]);
-              out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * p.x,
-                                             __uint_as_float(r[2 * i + 1]) * p.y);
+              const float2 o = f2_unpack(f2_mul(
+                  f2_pack(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                  f2_pack(p.x, p.y)));
+              out[i] = __floats2bfloat162_rn(o.x, o.y);
             }
           }
 #pragma unroll

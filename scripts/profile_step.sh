@@ -1,12 +1,14 @@
 # One-GPU profile pass: tests, a clean bench line, then the ncu launch list and a full
-# capture of one step's kernels (each only after the same command exited 0 without ncu).
+# capture of one step's 14 kernels (each only after the same command exited 0 without ncu).
 set -e
 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-FSSDP_TIMELINE=gpurun_out/tl python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/n1.json 2> gpurun_out/n1.err
+FSSDP_TIMELINE=gpurun_out/tl python bench.py --steps 20 --warmup 5 > gpurun_out/n1.json 2> gpurun_out/n1.err
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"dispatch|combine|gate|route_scan|grouped_gemm" \
-    --launch-skip 45 -c 15 -f -o gpurun_out/step_full \
+# warm-up 3 steps + timed 1 step = 4 x 14 launches skipped: the capture is the instrumented step
+ncu --set full --clock-control none --import-source on \
+    -k regex:"dispatch|combine|gate|route_scan|grouped_gemm" --launch-skip 56 -c 14 \
+    -f -o gpurun_out/step_full \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 echo PROFILE_DONE
