@@ -346,8 +346,14 @@ def run_ours(args):
     peaks, peak_src = load_peaks()
     achieved = allr[:, 1].sum() / (allr[:, 0].sum() * 1e-3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
+    traffic, traffic_src = None, None
+    tfiles = sorted((ROOT / "profiles").glob("*gemm_traffic.json"))
+    if tfiles:  # DRAM bytes of the step's GEMM launches from the committed ncu --set full capture
+        traffic = json.loads(tfiles[-1].read_text())["gemm_dram_bytes_per_step"]
+        traffic_src = f"{tfiles[-1].name}: dram__bytes_read.sum + dram__bytes_write.sum"
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step "
+                "(the N=1 step's GEMM launches)", "traffic_source": traffic_src,
                 "kernel": "fssdp grouped_gemm_kernel (tcgen05), all 6 GEMMs of the step",
                 "algorithmic_flops": "3 x 2 x routed_rows x 2 x d_model x d_ff per rank",
                 "peak_source": f"{peak_src}, sustained bf16 (kernels timed inside a long step)",

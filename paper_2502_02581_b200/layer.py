@@ -1,11 +1,15 @@
 """FssdpMoE — one FSSDP MoE layer executed on B200s (the hot path of BASELINE.json).
 
 Forward (per rank):  K1 gate -> K2 counts all-gather -> host plan (FssdpPlanner, bit-exact
-with moesim) -> K3 SpAG of the replicas this rank materializes -> K4 dispatch ->
-K5 grouped FFN (tcgen05) -> K6 combine.
+with moesim; plan + device tables + upload in one native call) -> K4 dispatch -> K3 SpAG of
+the replicas this rank materializes (those the history-based candidate already implied
+were pulled early, on a side stream, from the count all-gather on) -> K5 grouped FFN
+(tcgen05) -> K6 combine.
 Backward:  K7 token-side A2A (w·dy to the experts, <dy, Y> for the gate) -> optional
-re-materialization SpAG -> grouped dgrad/wgrad (tcgen05) -> dX combine + gate
-backward -> K8 SpRS of replica gradients to their owners.
+re-materialization SpAG -> dgrad2 and the weight grads of the SpRS-input slots (replica
+partials are stored straight into their owners' staging slots by the GEMM epilogue) ->
+K8 SpRS owner-side reduction on a side stream, beside dgrad1 and the remaining wgrads ->
+dX combine + gate backward.
 
 All heavy work is sm_100a kernels in libfssdp.so; PyTorch only owns memory and streams.
 Execution is split into phases so a driver can run several logical ranks in lockstep
@@ -549,9 +553,9 @@ class FssdpMoE:
         self.phase_gate(x)
         self.phase_counts()
         self.phase_plan()
-        self.phase_spag()
         self.phase_dispatch()
         self._mark("dispatch_launched")
+        self.phase_spag()  # only fwd1 reads the replicas: the dispatch overlaps the early SpAG
         self.phase_experts_fwd()
         self.phase_barrier(BAR_Y)
         return self.phase_combine()
@@ -666,9 +670,9 @@ def run_lockstep_forward(layers: list, xs: list) -> list:
     for ly in layers:
         ly.phase_plan()
     for ly in layers:
-        ly.phase_spag()
-    for ly in layers:
         ly.phase_dispatch()
+    for ly in layers:
+        ly.phase_spag()
     for ly in layers:
         ly.phase_experts_fwd()
     return [ly.phase_combine() for ly in layers]

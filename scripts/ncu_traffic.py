@@ -18,7 +18,7 @@ def main(path, out_path):
     rd, wr, t = (hdr.index(m) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum",
                                         "gpu__time_duration.sum"))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
     kernels = []
     for r in data:
         kernels.append({
