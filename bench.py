@@ -340,9 +340,15 @@ def run_ours(args):
     t = layer.tables
     n_pre = layer.pre_tables.n_spag if layer.pre_tables is not None else 0
     spag_in = float((t.n_spag + n_pre) * layer.g.slot_param_bytes)
-    sprs_in = float(sum(int(c) - 1 for _, _, c in t.sprs_jobs) * layer.g.slot_grad_elems * 4)
+    # SpRS: partials pushed into this rank's staging slots by the holders' wgrad epilogues
+    # (NVLink, inside the GEMMs); the "sprs" kernel is the owner-side local reduction, which
+    # reads every holder's partial (own slot + staging) and writes the sum
+    sprs_in = float(t.n_stage * layer.g.slot_grad_elems * 4)
+    sprs_reduce_bytes = float(sum(int(c) + 1 for _, _, c in t.sprs_jobs) *
+                              layer.g.slot_grad_elems * 4)
     host_ms = 1e3 * sum(timers.get("host_plan_s", [])) / args.steps
-    allr = gather([gemm_ms, flops_rank, spag_ms, sprs_ms, spag_in, sprs_in, host_ms, ms])
+    allr = gather([gemm_ms, flops_rank, spag_ms, sprs_ms, spag_in, sprs_in, host_ms, ms,
+                   sprs_reduce_bytes])
     peaks, peak_src = load_peaks()
     achieved = allr[:, 1].sum() / (allr[:, 0].sum() * 1e-3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
@@ -392,9 +398,11 @@ def run_ours(args):
             "spag_ms_max_rank": spag_max, "sprs_ms_max_rank": sprs_max,
             "spag_bottleneck_gbs": gbs(rep.bottleneck_bytes, spag_max),
             "spag_inbound_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 4], allr[:, 2])],
-            "sprs_inbound_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 5], allr[:, 3])],
+            "sprs_pushed_in_bytes_per_rank": [float(b) for b in allr[:, 5]],
+            "sprs_local_reduce_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 8], allr[:, 3])],
             "nvlink_peer_gbs_ref": NVLINK_PEER_GBS,
-            "note": "SpRS wire is fp32 (2x the reference's expert_bytes pricing)"}
+            "note": "SpRS wire is fp32 partials pushed by the wgrad epilogue's TMA stores "
+                    "(2x the reference's expert_bytes pricing); sprs_ms is the local reduce"}
 
     # end to end through the public API with host buffers: inputs are copied H2D on a copy
     # stream one step ahead (double buffered), dx is copied D2H behind the compute.
