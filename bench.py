@@ -433,11 +433,11 @@ def run_ours(args):
             prefetch(0)
             for i in range(n):
                 b = i % 2
+                if i + 1 < n:  # next inputs stream in while this step computes
+                    prefetch(i + 1)
                 main_s.wait_event(in_ev[b])
                 dx = step(xb[b], dyb[b])
                 done_ev[b].record(main_s)
-                if i + 1 < n:
-                    prefetch(i + 1)
                 with torch.cuda.stream(d2h_s):
                     d2h_s.wait_event(done_ev[b])
                     dxh[b].copy_(dx, non_blocking=True)

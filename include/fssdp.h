@@ -197,14 +197,16 @@ int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_exper
 
 /* The planning critical path in one call: fssdp_plan_layer on this rank's all-gathered
  * int32 counts [D*E], then fssdp_build_rank_tables for `rank` into the pinned `blob`, then
- * (if blob_dev) its upload on `stream`.  Outputs as the two calls'. */
+ * (if blob_dev) its upload on `stream`.  Outputs as the two calls'.  limits (nullable):
+ * {slot capacity, receive-row capacity, staging-slot capacity} of this rank's buffers; a
+ * plan exceeding one returns FSSDP_ERR_INFEASIBLE before anything is uploaded. */
 int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
                             const int32_t* counts, const fssdp_topology* topo,
                             const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
-                            int32_t d_model, int32_t d_ff, uint8_t* target_out, int32_t* added_out,
-                            int64_t* route_out, double* doubles_out, int32_t* flags_out,
-                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out, void* blob_dev,
-                            void* stream);
+                            int32_t d_model, int32_t d_ff, const int64_t* limits,
+                            uint8_t* target_out, int32_t* added_out, int64_t* route_out,
+                            double* doubles_out, int32_t* flags_out, uint8_t* blob,
+                            int64_t blob_bytes, int32_t* header_out, void* blob_dev, void* stream);
 
 /* The estimate-based, adoption-gated materialization alone (engine.py:497-501 with
  * _adopt_materialization engine.py:406-429): depends only on the load history, so its
@@ -362,6 +364,16 @@ int fssdp_ipc_open(const uint8_t* handle /* 64 bytes */, void** ptr_out);
 int fssdp_ipc_close(void* ptr);
 /* Number of SMs of the current device. */
 int fssdp_num_sms(void);
+/* Plan-boundary transfers without the copy engines (which may be busy with the caller's
+ * bulk input/output copies): fssdp_push_host copies `bytes` (multiple of 16, <= 16 MiB) of
+ * device memory into pinned host memory with the SMs, then stores flag_value into
+ * *flag_host (pinned, nullable) with system-scope release; fssdp_host_wait spins on the
+ * host until *flag_host == value (or timeout_s); fssdp_pull_host copies pinned host memory
+ * into device memory with the SMs. */
+int fssdp_push_host(const void* src_dev, void* dst_host, int64_t bytes, uint32_t* flag_host,
+                    uint32_t flag_value, void* stream);
+int fssdp_host_wait(const uint32_t* flag_host, uint32_t value, double timeout_s);
+int fssdp_pull_host(void* dst_dev, const void* src_host, int64_t bytes, void* stream);
 /* Plan-boundary copies (counts readback, plan-table upload): cudaMemcpyAsync of `bytes`
  * on `stream` (direction inferred from the pointers), then, if `synchronize`, wait for
  * the stream.  Host buffers should be pinned. */

@@ -90,8 +90,8 @@ _SIGS = {
     "fssdp_build_rank_tables": [i32, i32, i32, P_i32, P_u8, P_u8, P_i64, i32, i32, vp, i64, P_i32],
     "fssdp_plan_candidate": [i32, P_i32, P_f64, P_topo, C.POINTER(LayerKnobs), P_u8, P_i32],
     "fssdp_plan_layer_tables": [i32, P_i32, P_f64, P_i32, P_topo, C.POINTER(LayerKnobs), i32,
-                                P_u8, i32, i32, P_u8, P_i32, P_i64, P_f64, P_i32, vp, i64, P_i32,
-                                vp, vp],
+                                P_u8, i32, i32, P_i64, P_u8, P_i32, P_i64, P_f64, P_i32, vp, i64,
+                                P_i32, vp, vp],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
                            vp, vp, i64, i64, i32, vp],
@@ -116,6 +116,9 @@ _SIGS = {
     "fssdp_ipc_open": [P_u8, C.POINTER(C.c_void_p)],
     "fssdp_ipc_close": [vp],
     "fssdp_copy": [vp, vp, i64, vp, i32],
+    "fssdp_push_host": [vp, vp, i64, vp, u32, vp],
+    "fssdp_host_wait": [vp, u32, f64],
+    "fssdp_pull_host": [vp, vp, i64, vp],
 }
 _RESTYPE = {"fssdp_version": C.c_char_p, "fssdp_last_error": C.c_char_p}
 
@@ -166,7 +169,7 @@ KERNELS_PER_CALL = {
     "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
     "fssdp_route_scan_allgather": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
-    "fssdp_sprs": 1,
+    "fssdp_sprs": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
 }
 launch_count = 0
 

@@ -99,10 +99,10 @@ int fssdp_num_sms(void) { return num_sms(); }
 int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
                             const int32_t* counts, const fssdp_topology* topo,
                             const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
-                            int32_t d_model, int32_t d_ff, uint8_t* target_out, int32_t* added_out,
-                            int64_t* route_out, double* doubles_out, int32_t* flags_out,
-                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out, void* blob_dev,
-                            void* stream) {
+                            int32_t d_model, int32_t d_ff, const int64_t* limits,
+                            uint8_t* target_out, int32_t* added_out, int64_t* route_out,
+                            double* doubles_out, int32_t* flags_out, uint8_t* blob,
+                            int64_t blob_bytes, int32_t* header_out, void* blob_dev, void* stream) {
   if (topo == nullptr || counts == nullptr || num_experts <= 0) {
     set_error("plan_layer_tables: bad arguments");
     return kErrDimension;
@@ -119,10 +119,24 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
   if (rc != kOk) return rc;
   rc = fssdp_build_rank_tables(rank, static_cast<int32_t>(D), num_experts, base_owner, target_out,
                                pre_mask, route_out, d_model, d_ff, blob, blob_bytes, header_out);
-  if (rc != kOk || blob_dev == nullptr) return rc;
+  if (rc != kOk) return rc;
+  if (limits != nullptr) {  // header: [0] slots, [2] receive rows, [28] staging slots
+    const int64_t need[3] = {header_out[0], header_out[2], header_out[28]};
+    static const char* what[3] = {"expert slots", "receive rows", "staging slots"};
+    for (int i = 0; i < 3; ++i)
+      if (need[i] > limits[i]) {
+        char msg[160];
+        snprintf(msg, sizeof(msg), "plan needs %lld %s > capacity %lld", (long long)need[i],
+                 what[i], (long long)limits[i]);
+        set_error(msg);
+        return FSSDP_ERR_INFEASIBLE;
+      }
+  }
+  if (blob_dev == nullptr) return rc;
   int64_t offs[FSSDP_TAB_NSECTIONS], total = 0;
   fssdp_tables_layout(num_experts, static_cast<int32_t>(D), offs, &total);
-  return fssdp_copy(blob_dev, blob, total, stream, 0);
+  // SM-driven pull from the pinned blob: not queued behind the caller's bulk H2D copies
+  return fssdp_pull_host(blob_dev, blob, (total + 15) / 16 * 16, stream);
 }
 
 int fssdp_copy(void* dst, const void* src, int64_t bytes, void* stream, int32_t synchronize) {

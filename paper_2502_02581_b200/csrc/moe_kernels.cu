@@ -22,6 +22,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+#include <chrono>
+
 #include "fssdp_internal.h"
 #include "ptx.cuh"
 
@@ -1010,6 +1013,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------------ plan-boundary transfers
+// Small host<->device transfers on the planning critical path done by the SMs through
+// mapped pinned memory: a copy-engine transfer would queue behind bulk H2D/D2H traffic of
+// the caller (e.g. the next step's inputs, the previous step's outputs).
+__global__ void __launch_bounds__(256)
+    push_host_kernel(const int4* __restrict__ src, int4* dst_host, int n16, uint32_t* flag_host,
+                     uint32_t flag_value) {
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst_host[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0 && flag_host != nullptr) {
+    __threadfence_system();
+    st_release_sys(flag_host, flag_value);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    pull_host_kernel(const int4* src_host, int4* __restrict__ dst, int n16) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
+    dst[i] = src_host[i];
+}
+
 // ------------------------------------------------------------------ launchers
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -1286,6 +1310,48 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
                                                    slot_elems, jobs, srcs, chunk, n_chunks,
                                                    n_units);
   return launch_status();
+}
+
+int fssdp_push_host(const void* src_dev, void* dst_host, int64_t bytes, uint32_t* flag_host,
+                    uint32_t flag_value, void* stream) {
+  if (bytes < 0 || bytes % 16 != 0 || bytes > (int64_t(1) << 24)) {
+    set_error("push_host: bytes must be a multiple of 16 and at most 16 MiB");
+    return kErrDimension;
+  }
+  push_host_kernel<<<1, 256, 0, as_stream(stream)>>>(static_cast<const int4*>(src_dev),
+                                                    static_cast<int4*>(dst_host),
+                                                    static_cast<int>(bytes / 16), flag_host,
+                                                    flag_value);
+  return launch_status();
+}
+
+int fssdp_pull_host(void* dst_dev, const void* src_host, int64_t bytes, void* stream) {
+  if (bytes < 0 || bytes % 16 != 0 || bytes > (int64_t(1) << 24)) {
+    set_error("pull_host: bytes must be a multiple of 16 and at most 16 MiB");
+    return kErrDimension;
+  }
+  if (bytes == 0) return kOk;
+  const int n16 = static_cast<int>(bytes / 16);
+  const int grid = (n16 + 255) / 256 < 16 ? (n16 + 255) / 256 : 16;
+  pull_host_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int4*>(src_host),
+                                                       static_cast<int4*>(dst_dev), n16);
+  return launch_status();
+}
+
+int fssdp_host_wait(const uint32_t* flag_host, uint32_t value, double timeout_s) {
+  const volatile uint32_t* f = flag_host;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t spins = 0;; ++spins) {
+    if (*f == value) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      return kOk;
+    }
+    if ((spins & 1023) == 0 &&
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+      set_error("host_wait: timed out waiting for the device");
+      return kErrCuda;
+    }
+  }
 }
 
 }  // extern "C"

@@ -93,7 +93,7 @@ class LayerGeometry:
         layout.add(prefix + "y", R * d * 2)
         layout.add(prefix + "dyrecv", R * d * 2)
         layout.add(prefix + "dxe", R * d * 2)
-        layout.add(prefix + "counts", self.world * self.num_experts * 4)
+        layout.add(prefix + "counts", (self.world * self.num_experts * 4 + 15) // 16 * 16)
         layout.add(prefix + "stage", max(1, self.stage_slots) * self.slot_grad_elems * 4)
 
 
@@ -132,11 +132,17 @@ class FssdpMoE:
         self.dyrecv = heap.tensor(self.off["dyrecv"], (R, d), torch.bfloat16)
         self.dxe = heap.tensor(self.off["dxe"], (R, d), torch.bfloat16)
         self.counts_table = heap.tensor(self.off["counts"], (self.world, E), torch.int32)
-        self.counts_host = torch.empty(self.world, E, dtype=torch.int32, pin_memory=True)
+        # counts readback through mapped pinned memory (SM-pushed, flag-signalled): the copy
+        # engines may be busy with the caller's bulk input/output transfers
+        self.counts_nbytes = (self.world * E * 4 + 15) // 16 * 16
+        self.counts_host_raw = torch.zeros(self.counts_nbytes // 4 + 4, dtype=torch.int32,
+                                           pin_memory=True)
+        self.counts_host = self.counts_host_raw[:self.world * E].view(self.world, E)
         self.counts_host_np = self.counts_host.numpy()
         self.counts_host_ptr = self.counts_host.data_ptr()
+        self.counts_flag_ptr = self.counts_host_raw.data_ptr() + self.counts_nbytes
         self.counts_dev_ptr = self.counts_table.data_ptr()
-        self.counts_nbytes = self.counts_table.numel() * 4
+        self._counts_epoch = 0
         # wgrad destinations for replica partials: every rank's staging region, as the
         # epilogue tensor maps of wgrad1 (ldc d) and wgrad2 (ldc f); built once
         stage_elems = max(1, geom.stage_slots) * geom.slot_grad_elems
@@ -188,6 +194,9 @@ class FssdpMoE:
         self.decision = None
         self.tables = None
         self._cs = None  # launching stream during forward()/backward()
+        self._plan_pending = False
+        self._limits = np.array([geom.slots, geom.recv_cap, geom.stage_slots], dtype=np.int64)
+        self._limits_ptr = self._limits.ctypes.data
         self._tab_ptrs = None
         self._pb_c = C.c_void_p(self.group.peer_bases.data_ptr())
         self.T = 0
@@ -342,8 +351,12 @@ class FssdpMoE:
         # host sync point #1: pinned copy of the all-gathered counts (raw cudaMemcpyAsync +
         # stream sync: the torch copy/event path costs tens of microseconds here)
         self._mark("readback")
-        N.check(N.LIB_RAW.fssdp_copy(self.counts_host_ptr, self.counts_dev_ptr,
-                                     self.counts_nbytes, self._stream(), 1), "counts readback")
+        self._counts_epoch = (self._counts_epoch + 1) & 0xFFFFFFFF
+        N.check(N.LIB_RAW.fssdp_push_host(self.counts_dev_ptr, self.counts_host_ptr,
+                                          self.counts_nbytes, self.counts_flag_ptr,
+                                          self._counts_epoch, self._stream()), "counts readback")
+        N.check(N.LIB_RAW.fssdp_host_wait(self.counts_flag_ptr, self._counts_epoch, 60.0),
+                "counts readback")
         t_host = time.perf_counter()
         self._mark("synced")
         self._plan_tables(self.counts_host_np)
@@ -351,14 +364,27 @@ class FssdpMoE:
             self.timers.setdefault("host_plan_s", []).append(time.perf_counter() - t_host)
 
     def _plan_tables(self, counts) -> None:
-        # plan + this rank's tables + their upload (boundary #2): one native call
+        # plan + this rank's tables + their upload (boundary #2), capacity-checked: one native
+        # call; the Python-side decision object is built after the dispatch is launched
         E, D = self.g.num_experts, self.world
-        dec = self.planner.plan_with_tables(
+        self.planner.plan_with_tables(
             self.layer, counts, self.counts_host_ptr, self.rank, self.pre_mask_ptr,
             self.g.d_model, self.g.d_ff, self.blob_host_np, self.blob_host_ptr,
-            NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream())
+            NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
+            decide=False)
         self._mark("planned")
         tables = NativeTables.from_header(E, D, self.blob_host_np)
+        self.tables = self.packed = tables
+        self.gemm = tables.gemm
+        self._plan_pending = True
+
+    def _finish_plan(self) -> None:
+        """Decision object and consistency checks, off the planning critical path."""
+        if not self._plan_pending:
+            return
+        self._plan_pending = False
+        dec = self.planner.last_decision(self.layer)
+        tables = self.tables
         target = dec.target.mask  # 0/1 uint8, like pre_mask
         pre = self.pre_mask
         if pre is not None and np.any(pre > target):
@@ -367,20 +393,11 @@ class FssdpMoE:
             if np.any(target > dec.base.mask):
                 raise InternalError("final placement is neither a superset of the early one "
                                     "nor the bare partition")
-        if tables.n_slots > self.g.slots:
-            raise InternalError(f"plan needs {tables.n_slots} slots > capacity {self.g.slots}")
-        if tables.recv_rows > self.g.recv_cap:
-            raise InternalError("receive rows exceed capacity")
-        if tables.n_stage > self.g.stage_slots:
-            raise InternalError(f"plan needs {tables.n_stage} staging slots > {self.g.stage_slots}")
         if tables.n_owned != self._n_owned or (
                 self.planner.last_reshard_moves and
                 list(tables.slot_expert[:tables.n_owned]) != self._owned_expert_ids):
             raise InternalError("ownership changed without a re-shard data move")
-        self.decision, self.tables = dec, tables
-        self.packed = tables
-        self.gemm = tables.gemm
-        self._mark("tables")
+        self.decision = dec
 
     def phase_spag(self, refetch_early: bool = False) -> None:
         """The SpAG of the final plan's replicas not fetched early; the main stream then
@@ -407,6 +424,7 @@ class FssdpMoE:
                self._pb(), self.off["xrecv"], self._tab("zero_rows"), t.n_zero,
                self.flags_off, self.rank, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr()), self._stream())
+        self._finish_plan()
 
     # CUDA-event instrumentation (bench.py): name -> list of (start, end) events recorded on
     # the launching stream around each kernel launch; None disables it.
