@@ -228,6 +228,25 @@ def _config(args, world):
             "l2": "per-step working set > 1 GB exceeds the 126 MB L2 (no explicit flush)"}
 
 
+def a2a_stats(dec, allp, keys, world):
+    """Token A2A against its roofline: bytes = dispatch_traffic(route, B),
+    the max over devices of in/out bytes, per kernel launch (dispatch and dispatch_grad
+    push rows, combine and combine_dx pull them back), ÷ the max-rank kernel time."""
+    import numpy as np
+
+    B = 2 * CFG2["d_model"]
+    r = np.asarray(dec.route, dtype=np.float64)  # [src, e, dst]
+    mat = r.sum(axis=1) * B
+    np.fill_diagonal(mat, 0.0)
+    worst = float(max(mat.sum(axis=1).max(), mat.sum(axis=0).max()))
+    out = {"bottleneck_bytes_per_pass": worst, "total_remote_bytes_per_pass": float(mat.sum())}
+    for k in ("dispatch", "combine", "dispatch_grad", "combine_dx"):
+        if k in keys:
+            ms = float(allp[:, keys.index(k)].max())
+            out[k + "_gbs"] = worst / (ms * 1e-3) / 1e9 if ms > 0 else None
+    return out
+
+
 # ----------------------------------------------------------------- our arm
 def run_ours(args):
     import numpy as np
@@ -401,6 +420,7 @@ def run_ours(args):
             "sprs_pushed_in_bytes_per_rank": [float(b) for b in allr[:, 5]],
             "sprs_local_reduce_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 8], allr[:, 3])],
             "nvlink_peer_gbs_ref": NVLINK_PEER_GBS,
+            "a2a": a2a_stats(dec, allp, keys, world),
             "note": "SpRS wire is fp32 partials pushed by the wgrad epilogue's TMA stores "
                     "(2x the reference's expert_bytes pricing); sprs_ms is the local reduce"}
 
