@@ -163,7 +163,9 @@ int fssdp_plan_layer(int32_t num_experts, const int32_t* base_owner, const doubl
 int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, const double* profile,
                       const fssdp_topology* topo, double* score_out);
 
-/* Device plan tables of one rank for one layer-iteration, derived from the global plan
+/* n_mats: expert matrices per slot — 2 = GeLU [W1 | W2], 3 = SwiGLU [W13 | W2] (W13 =
+ * block-interleaved W1/W3, see FSSDP_EPI_SWIGLU).  d_model % 256 == 0, d_ff % 128 == 0.
+ * Device plan tables of one rank for one layer-iteration, derived from the global plan
  * (base owner[E], target mask [E*D], route[D*E*D]) — every rank derives its own, nothing
  * is exchanged.  Packed into one blob of 16-byte-aligned sections whose offsets
  * fssdp_tables_layout returns; header_out[FSSDP_TAB_HEADER_INTS] = {n_slots, n_owned,
@@ -193,7 +195,8 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
 int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_experts,
                             const int32_t* base_owner, const uint8_t* target_mask,
                             const uint8_t* pre_mask, const int64_t* route, int32_t d_model,
-                            int32_t d_ff, uint8_t* blob, int64_t blob_bytes, int32_t* header_out);
+                            int32_t d_ff, int32_t n_mats, uint8_t* blob, int64_t blob_bytes,
+                            int32_t* header_out);
 
 /* The planning critical path in one call: fssdp_plan_layer on this rank's all-gathered
  * int32 counts [D*E], then fssdp_build_rank_tables for `rank` into the pinned `blob`, then
@@ -203,7 +206,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_exper
 int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
                             const int32_t* counts, const fssdp_topology* topo,
                             const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
-                            int32_t d_model, int32_t d_ff, const int64_t* limits,
+                            int32_t d_model, int32_t d_ff, int32_t n_mats, const int64_t* limits,
                             uint8_t* target_out, int32_t* added_out, int64_t* route_out,
                             double* doubles_out, int32_t* flags_out, uint8_t* blob,
                             int64_t blob_bytes, int32_t* header_out, void* blob_dev, void* stream);
@@ -235,6 +238,13 @@ typedef struct fssdp_gemm_group {
 #define FSSDP_EPI_GELU 1  /* C = bf16(gelu'(acc)) (saved for backward), C2 = bf16(gelu(acc)) */
 #define FSSDP_EPI_DGELU 2 /* C = bf16(acc * aux)  (aux = the saved gelu'(pre-activation)) */
 #define FSSDP_EPI_F32 3   /* C = acc (fp32) */
+/* SwiGLU experts.  W13 = [W1; W3] stored block-interleaved: rows [256b, 256b+128) are
+ * W1 rows [128b, 128b+128) and rows [256b+128, 256b+256) are W3's, so a 256-wide output
+ * tile of x·W13ᵀ holds a1 and a3 of the same 128 hidden units. */
+#define FSSDP_EPI_SWIGLU 4  /* N = 2f, 256-wide tiles: C = bf16([a1|a3]) (saved, ldc = 2f),
+                               C2 = bf16(silu(a1)·a3) (width ldc/2 = f) */
+#define FSSDP_EPI_DSWIGLU 5 /* N = f (acc = dH): aux = the saved [a1|a3] (ldc = 2f);
+                               C = bf16([dH·a3·silu'(a1) | dH·silu(a1)]) (ldc = 2f) */
 
 /* Grouped GEMM  C_g = A_g · B_g  on tcgen05 (K5/K7).  A and B are bf16 2-D tensors
  * described by (inner, outer) element extents (inner contiguous).  a_mn / b_mn select
@@ -250,6 +260,8 @@ typedef struct fssdp_gemm_group {
 #define FSSDP_GEMM_N_FASTEST 1
 /* CTA-pair (tcgen05 cta_group::2) 256 x 256 tiles; requires every group's m_tiles even. */
 #define FSSDP_GEMM_CTA_PAIR 2
+/* 128-wide N tiles (N % 256 != 0, e.g. d_ff = 1408); not with FSSDP_EPI_SWIGLU. */
+#define FSSDP_GEMM_BN128 4
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,

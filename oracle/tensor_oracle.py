@@ -10,7 +10,9 @@ restates the paper's semantics; parity here is UNPINNED by reference tests:
   (source, expert) cell in ascending device order with the build_dispatch counts
   route[s, e, d] (dispatch.py:49-97 gives the counts; the per-token order is ours).
 * expert FFN: A = X·W1ᵀ (fp32), H = bf16(gelu_tanh(A)), Y = H·W2ᵀ; the
-  backward uses the saved G' = bf16(gelu_tanh'(A)): dA = bf16((dY·W2)·G').
+  backward uses the saved G' = bf16(gelu_tanh'(A)): dA = bf16((dY·W2)·G').  SwiGLU experts
+  (configs 3-4): H = bf16(silu(A1)·A3) from fp32 A1 = X·W1ᵀ, A3 = X·W3ᵀ; the backward uses
+  the saved bf16 A1, A3: dA1 = bf16(dH·A3·silu'(A1)), dA3 = bf16(dH·silu(A1)).
 * combine: y_t = Σ_j w_tj · Y_tj in fp32, j ascending, then bf16.
 * SpAG: replica = owner copy; SpRS: owner = Σ replicas in ascending device order, fp32
   (PAPER.md:370-386).
@@ -147,56 +149,87 @@ def combine(rows: np.ndarray, w: np.ndarray) -> np.ndarray:
     return bf16_round(acc)
 
 
+def silu(a):
+    return (a / (1.0 + np.exp(-a.astype(np.float64)))).astype(np.float32)
+
+
 def moe_layer_fwd_bwd(x, idx, w, wg, experts, dy):
     """Whole-layer restatement for one rank's tokens (placement-independent math).
 
     x [T, d] bf16-valued float32; idx/w [T, k] (the device's own routing, pinned
-    bit-exactly by the gate tests); wg [E, d]; experts {e: (W1 [f, d], W2 [d, f])}
-    bf16-valued float32; dy [T, d] bf16-valued float32.
-    Returns dict(y, dx, g (slot <dy, Y>), dlogit, dW1 {e}, dW2 {e}, dWg)."""
+    bit-exactly by the gate tests); wg [E, d]; experts {e: (W1 [f, d], W2 [d, f])} (GeLU,
+    PAPER.md:645) or {e: (W1, W3 [f, d], W2)} (SwiGLU: h = silu(x W1ᵀ) ⊙ (x W3ᵀ), the
+    Mixtral / DeepSeek expert of configs 3-4), bf16-valued float32; dy [T, d].
+    Rounding points mirror the device: fwd keeps fp32 pre-activations for h, saves bf16
+    (gelu'(a) | a1, a3) for backward; dgrad2 multiplies the fp32 dH by the saved values.
+    Returns dict(y, dx, g (slot <dy, Y>), dlogit, dW1 {e}, dW2 {e}, [dW3 {e}], dWg)."""
     T, k = idx.shape
     d = x.shape[1]
+    swiglu = len(next(iter(experts.values()))) == 3
     Y = np.zeros((T, k, d), dtype=np.float32)
     A = {}
     H = {}
-    for e, (W1, W2) in experts.items():
+    for e, mats in experts.items():
         rows = np.argwhere(idx == e)
         if len(rows) == 0:
             continue
         xe = x[rows[:, 0]].astype(np.float32)
-        a = (xe @ W1.T).astype(np.float32)  # fp32 pre-activation (never stored)
-        h = bf16_round(gelu_tanh(a).astype(np.float32))
+        W2 = mats[-1]
+        if swiglu:
+            a1 = (xe @ mats[0].T).astype(np.float32)
+            a3 = (xe @ mats[1].T).astype(np.float32)
+            h = bf16_round((silu(a1) * a3).astype(np.float32))
+            A[e] = (rows, (bf16_round(a1), bf16_round(a3)))  # saved bf16 pre-activations
+        else:
+            a = (xe @ mats[0].T).astype(np.float32)  # fp32 pre-activation (never stored)
+            h = bf16_round(gelu_tanh(a).astype(np.float32))
+            A[e] = (rows, a)
         Y[rows[:, 0], rows[:, 1]] = bf16_round((h @ W2.T).astype(np.float32))
-        A[e], H[e] = (rows, a), h
+        H[e] = h
     y = combine(Y, w)
     # backward
     g = np.einsum("td,tkd->tk", dy.astype(np.float32), Y, optimize=True).astype(np.float32)
     sg = (w.astype(np.float64) * g).sum(axis=1, keepdims=True)
     dlogit = (w * (g - sg)).astype(np.float32)
     dXs = np.zeros((T, k, d), dtype=np.float32)
-    dW1, dW2 = {}, {}
-    for e, (W1, W2) in experts.items():
-        f = W1.shape[0]
+    dW1, dW2, dW3 = {}, {}, {}
+    for e, mats in experts.items():
+        W2 = mats[-1]
         if e not in A:
-            dW1[e] = np.zeros_like(W1)
+            dW1[e] = np.zeros_like(mats[0])
             dW2[e] = np.zeros_like(W2)
+            if swiglu:
+                dW3[e] = np.zeros_like(mats[1])
             continue
-        rows, a = A[e]
+        rows, saved = A[e]
         dYe = bf16_round((w[rows[:, 0], rows[:, 1]][:, None] * dy[rows[:, 0]]).astype(np.float32))
         dH = (dYe @ W2).astype(np.float32)
-        gp = bf16_round(gelu_tanh_grad(a).astype(np.float32))  # saved gelu'(a), bf16
-        dA = bf16_round((dH * gp).astype(np.float32))
-        dXs[rows[:, 0], rows[:, 1]] = bf16_round((dA @ W1).astype(np.float32))
         xe = x[rows[:, 0]].astype(np.float32)
-        dW1[e] = (dA.T @ xe).astype(np.float32)
+        if swiglu:
+            a1, a3 = saved
+            sg1 = (1.0 / (1.0 + np.exp(-a1.astype(np.float64)))).astype(np.float32)
+            dsilu = (sg1 * (1.0 + a1 * (1.0 - sg1))).astype(np.float32)
+            dA1 = bf16_round((dH * a3 * dsilu).astype(np.float32))
+            dA3 = bf16_round((dH * a1 * sg1).astype(np.float32))
+            dXs[rows[:, 0], rows[:, 1]] = bf16_round(
+                (dA1 @ mats[0] + dA3 @ mats[1]).astype(np.float32))
+            dW1[e] = (dA1.T @ xe).astype(np.float32)
+            dW3[e] = (dA3.T @ xe).astype(np.float32)
+        else:
+            gp = bf16_round(gelu_tanh_grad(saved).astype(np.float32))  # saved gelu'(a), bf16
+            dA = bf16_round((dH * gp).astype(np.float32))
+            dXs[rows[:, 0], rows[:, 1]] = bf16_round((dA @ mats[0]).astype(np.float32))
+            dW1[e] = (dA.T @ xe).astype(np.float32)
         dW2[e] = (dYe.T @ H[e]).astype(np.float32)
-        del f
     dx = dXs.sum(axis=1) + np.einsum("tk,tkd->td", dlogit, wg[idx])
     dWg = np.zeros_like(wg)
     for j in range(k):
         np.add.at(dWg, idx[:, j], dlogit[:, j:j + 1] * x)
-    return dict(y=y, dx=bf16_round(dx.astype(np.float32)), g=g, dlogit=dlogit, dW1=dW1, dW2=dW2,
-                dWg=dWg)
+    out = dict(y=y, dx=bf16_round(dx.astype(np.float32)), g=g, dlogit=dlogit, dW1=dW1, dW2=dW2,
+               dWg=dWg)
+    if swiglu:
+        out["dW3"] = dW3
+    return out
 
 
 def sprs_sum(contribs: list[np.ndarray]) -> np.ndarray:

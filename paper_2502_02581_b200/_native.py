@@ -87,11 +87,12 @@ _SIGS = {
                          P_i64, P_f64, P_i32],
     "fssdp_shard_score": [i32, i32, P_i32, P_f64, P_topo, P_f64],
     "fssdp_tables_layout": [i32, i32, P_i64, P_i64],
-    "fssdp_build_rank_tables": [i32, i32, i32, P_i32, P_u8, P_u8, P_i64, i32, i32, vp, i64, P_i32],
+    "fssdp_build_rank_tables": [i32, i32, i32, P_i32, P_u8, P_u8, P_i64, i32, i32, i32, vp, i64,
+                                P_i32],
     "fssdp_plan_candidate": [i32, P_i32, P_f64, P_topo, C.POINTER(LayerKnobs), P_u8, P_i32],
     "fssdp_plan_layer_tables": [i32, P_i32, P_f64, P_i32, P_topo, C.POINTER(LayerKnobs), i32,
-                                P_u8, i32, i32, P_i64, P_u8, P_i32, P_i64, P_f64, P_i32, vp, i64,
-                                P_i32, vp, vp],
+                                P_u8, i32, i32, i32, P_i64, P_u8, P_i32, P_i64, P_f64, P_i32, vp,
+                                i64, P_i32, vp, vp],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
                            vp, vp, i64, i64, i32, vp],

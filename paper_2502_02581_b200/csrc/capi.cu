@@ -99,7 +99,7 @@ int fssdp_num_sms(void) { return num_sms(); }
 int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
                             const int32_t* counts, const fssdp_topology* topo,
                             const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
-                            int32_t d_model, int32_t d_ff, const int64_t* limits,
+                            int32_t d_model, int32_t d_ff, int32_t n_mats, const int64_t* limits,
                             uint8_t* target_out, int32_t* added_out, int64_t* route_out,
                             double* doubles_out, int32_t* flags_out, uint8_t* blob,
                             int64_t blob_bytes, int32_t* header_out, void* blob_dev, void* stream) {
@@ -118,7 +118,8 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
                             added_out, route_out, doubles_out, flags_out);
   if (rc != kOk) return rc;
   rc = fssdp_build_rank_tables(rank, static_cast<int32_t>(D), num_experts, base_owner, target_out,
-                               pre_mask, route_out, d_model, d_ff, blob, blob_bytes, header_out);
+                               pre_mask, route_out, d_model, d_ff, n_mats, blob, blob_bytes,
+                               header_out);
   if (rc != kOk) return rc;
   if (limits != nullptr) {  // header: [0] slots, [2] receive rows, [28] staging slots
     const int64_t need[3] = {header_out[0], header_out[2], header_out[28]};
@@ -165,7 +166,9 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
     set_error("grouped_gemm: bad arguments");
     return kErrDimension;
   }
-  if ((epilogue == kEpiGelu && c2 == nullptr) || (epilogue == kEpiDGelu && aux == nullptr)) {
+  if (((epilogue == kEpiGelu || epilogue == kEpiSwiglu) && c2 == nullptr) ||
+      ((epilogue == kEpiDGelu || epilogue == kEpiDSwiglu) && aux == nullptr) || epilogue < 0 ||
+      epilogue > kEpiDSwiglu) {
     set_error("grouped_gemm: epilogue needs c2/aux");
     return kErrDimension;
   }
@@ -176,6 +179,11 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.total_tiles = total_tiles;
   args.n_fast = (flags & FSSDP_GEMM_N_FASTEST) ? 1 : 0;
   args.cta_group = (flags & FSSDP_GEMM_CTA_PAIR) ? 2 : 1;
+  args.bn = (flags & FSSDP_GEMM_BN128) ? 128 : 256;
+  if (args.bn == 128 && epilogue == kEpiSwiglu) {
+    set_error("grouped_gemm: the SwiGLU epilogue needs 256-wide N tiles");
+    return kErrDimension;
+  }
   args.ldc = ldc;
   args.c = c;
   args.c2 = c2;

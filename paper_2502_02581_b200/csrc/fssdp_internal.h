@@ -23,6 +23,8 @@ constexpr int kEpiBF16 = FSSDP_EPI_BF16;
 constexpr int kEpiGelu = FSSDP_EPI_GELU;
 constexpr int kEpiDGelu = FSSDP_EPI_DGELU;
 constexpr int kEpiF32 = FSSDP_EPI_F32;
+constexpr int kEpiSwiglu = FSSDP_EPI_SWIGLU;
+constexpr int kEpiDSwiglu = FSSDP_EPI_DSWIGLU;
 
 using GemmGroup = fssdp_gemm_group;
 
@@ -33,6 +35,7 @@ struct GemmLaunch {
   int total_tiles;  // sum over groups of m_tiles * n_tiles
   int n_fast;       // tile order: 1 = N fastest (share A in L2), 0 = M fastest (share B)
   int cta_group;    // 2 = CTA-pair 256x256 tiles (every group's m_tiles even), 1 = 128x256
+  int bn;           // N tile: 256, or 128 (FSSDP_GEMM_BN128)
   int64_t ldc;      // elements per C row
   void* c;          // output (bf16 or fp32)
   void* c2;         // second output (GeLU: post-activation)

@@ -54,21 +54,28 @@ constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store
 template <int BN, int EPI, int CG>
 struct GemmSmem {
   static constexpr int kEpiWarps = epi_warps<EPI>();
-  // GeLU' (dgrad2) trades a mainloop stage for a deeper aux-tile prefetch ring
-  static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : 0;
-  static constexpr int kStages =
-      kEpiWarps == 4 ? (CG == 2 ? (EPI == kEpiDGelu ? 5 : 6) : 4)
-                     : (CG == 2 ? (EPI == kEpiDGelu ? 4 : 5) : 3);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = (EPI == kEpiF32) ? 4 : 2;
   static constexpr int kBufBytes = 32 * kEpiCols * kOutBytes;  // one 32x32 staging tile
-  // per warp: C staging x2, plus C2 staging x2 (GeLU) or the aux ring (GeLU')
-  static constexpr int kXBufs = EPI == kEpiGelu ? 2 : kAuxBufs;
-  static constexpr int kEpiWarpBytes = (2 + kXBufs) * kBufBytes;
+  // output staging tiles per warp (two sets, so a store can drain while the next chunk is
+  // staged): C; C + C2 (GeLU); a1 + a3 + h (SwiGLU); da1 + da3 (SwiGLU backward)
+  static constexpr int kOutTiles = EPI == kEpiGelu ? 2 : EPI == kEpiSwiglu ? 3
+                                   : EPI == kEpiDSwiglu ? 2 : 1;
+  static constexpr int kCBufs = 2 * kOutTiles;
+  // aux-tile prefetch ring (dgrad2): entries of one tile (GeLU') or two (a1, a3)
+  static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : EPI == kEpiDSwiglu ? 2 : 0;
+  static constexpr int kAuxTiles = EPI == kEpiDSwiglu ? 2 : 1;
+  static constexpr int kEpiWarpBytes = (kCBufs + kAuxBufs * kAuxTiles) * kBufBytes;
+  // as many mainloop stages (up to 6) as the 227 KB budget leaves
+  static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
+  static constexpr int kBarBytes = (2 * 6 + 4 + 4 * kEpiWarps) * 8 + 16;
+  static constexpr int kFit = (232448 - 1024 - kBarBytes - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kFit < 6 ? kFit : 6;
+  static_assert(kStages >= 2, "shared memory budget exceeded");
   static constexpr int kEpiOffset = kStages * kStageBytes;
-  static constexpr int kBarOffset = kEpiOffset + kEpiWarps * kEpiWarpBytes;
+  static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], aux[kEpiWarps][4], tmem base slot
   static constexpr int kTotal = kBarOffset + (2 * kStages + 4 + 4 * kEpiWarps) * 8 + 16;
   static constexpr int kDynamic = kTotal + 1024;  // slack for 1024-B alignment
@@ -342,18 +349,23 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ew = warp - 2;
     uint8_t* wbase = smem + S::kEpiOffset + ew * S::kEpiWarpBytes;
-    uint8_t* cbuf0 = wbase;                     // C staging, buffers 0/1
-    uint8_t* xbuf0 = wbase + 2 * S::kBufBytes;  // C2 staging (GeLU) or aux tiles (GeLU')
-    // aux ring (GeLU'): kAuxBufs tiles, prefetched kAuxBufs-1 chunks ahead
+    uint8_t* cbuf0 = wbase;                               // output staging, 2 sets
+    uint8_t* abuf0 = wbase + S::kCBufs * S::kBufBytes;    // aux ring (dgrad2)
     constexpr int kAB = S::kAuxBufs > 0 ? S::kAuxBufs : 1;
+    constexpr int kAT = S::kAuxTiles;
+    constexpr int kOT = S::kOutTiles;
+    constexpr bool kAux = EPI == kEpiDGelu || EPI == kEpiDSwiglu;
     uint64_t* abar = aux_bar + 4 * ew;
-    uint32_t aux_phase = 0;  // bit i = phase of aux buffer i
-    constexpr int kChunks = BN / kEpiCols;
+    uint32_t aux_phase = 0;  // bit i = phase of aux entry i
+    // SwiGLU drains column PAIRS (a1 chunk c, a3 chunk c + 4): BN/64 steps of 32 hidden units
+    constexpr int kChunks = EPI == kEpiSwiglu ? BN / (2 * kEpiCols) : BN / kEpiCols;
     constexpr int kCW = kChunks / (kEpiWarps / 4);  // chunks drained by this warp
     const int cbase = (ew / 4) * kCW;                // warps 2-5: left half, 6-9: right half
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t gchunk = 0;  // running chunk counter (selects the staging buffers)
+    uint32_t gchunk = 0;  // running chunk counter (selects the staging set)
+    // aux / output column of f-space column j in the interleaved [a1|a3] layout (SwiGLU)
+    auto a13_col = [](int j) { return 256 * (j >> 7) + (j & 127); };
     for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
       const TileCoord tc =
           locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
@@ -366,14 +378,20 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       // staging slot, so the store itself is the NVLink transfer
       const CUtensorMap* cmap =
           g.c_dest > 0 ? static_cast<const CUtensorMap*>(args.c_dest_maps) + (g.c_dest - 1) : &map_c;
-      if (EPI == kEpiDGelu && lane == 0) {  // prefetch the first aux tiles of this tile
-        fence_proxy_async_smem();
-        for (int p = 0; p < kAB - 1 && p < kCW; ++p) {
-          const int ab = (gchunk + p) % kAB;
-          mbar_arrive_expect_tx(&abar[ab], S::kBufBytes);
-          tma_load_2d(xbuf0 + ab * S::kBufBytes, &map_x, &abar[ab], col0 + (cbase + p) * kEpiCols,
-                      row0);
+      auto aux_load = [&](int entry, int c) {  // the aux tile(s) of chunk c into an entry
+        uint8_t* dst = abuf0 + entry * kAT * S::kBufBytes;
+        mbar_arrive_expect_tx(&abar[entry], kAT * S::kBufBytes);
+        if (EPI == kEpiDSwiglu) {
+          const int a1 = a13_col(col0 + c * kEpiCols);
+          tma_load_2d(dst, &map_x, &abar[entry], a1, row0);
+          tma_load_2d(dst + S::kBufBytes, &map_x, &abar[entry], a1 + 128, row0);
+        } else {
+          tma_load_2d(dst, &map_x, &abar[entry], col0 + c * kEpiCols, row0);
         }
+      };
+      if (kAux && lane == 0) {  // prefetch the first aux tiles of this tile
+        fence_proxy_async_smem();
+        for (int p = 0; p < kAB - 1 && p < kCW; ++p) aux_load((gchunk + p) % kAB, cbase + p);
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -381,15 +399,16 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       for (int ci = 0; ci < kCW; ++ci, ++gchunk) {
         const int c = cbase + ci;
         const int b = gchunk & 1;
-        uint32_t r[32];
+        uint32_t r[32], r3[32];
+        const uint32_t tm = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                            static_cast<uint32_t>(acc * BN + c * kEpiCols);
         if (!zero) {
-          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                 static_cast<uint32_t>(acc * BN + c * kEpiCols),
-                             r);
+          tmem_ld_32x32b_x32(tm, r);
+          if (EPI == kEpiSwiglu) tmem_ld_32x32b_x32(tm + BN / 2, r3);  // the a3 half
           tmem_ld_wait();
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0u;
+          for (int i = 0; i < 32; ++i) r[i] = r3[i] = 0u;
         }
         if (ci == kCW - 1) {  // this warp's share of the accumulator read: release TMEM
           tc_fence_before();
@@ -401,34 +420,68 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               mbar_arrive(&tempty_bar[acc]);
           }
         }
-        __nv_bfloat162 pre[16];
-        if (EPI == kEpiDGelu) {
-          if (lane == 0 && ci + kAB - 1 < kCW) {  // keep kAB-1 aux tiles in flight
-            const int nb = (gchunk + kAB - 1) % kAB;
+        __nv_bfloat162 pre[16], pre3[16];
+        if (kAux) {
+          if (lane == 0 && ci + kAB - 1 < kCW) {  // keep kAB-1 aux entries in flight
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&abar[nb], S::kBufBytes);
-            tma_load_2d(xbuf0 + nb * S::kBufBytes, &map_x, &abar[nb],
-                        col0 + (c + kAB - 1) * kEpiCols, row0);
+            aux_load((gchunk + kAB - 1) % kAB, c + kAB - 1);
           }
           const int cur = gchunk % kAB;
           mbar_wait(&abar[cur], (aux_phase >> cur) & 1u);
           aux_phase ^= 1u << cur;
-          const uint8_t* ab = xbuf0 + cur * S::kBufBytes;
+          const uint8_t* ab = abuf0 + cur * kAT * S::kBufBytes;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 4; ++j) {
             *reinterpret_cast<int4*>(&pre[4 * j]) =
                 *reinterpret_cast<const int4*>(ab + sw64(lane, j));
+            if (EPI == kEpiDSwiglu)
+              *reinterpret_cast<int4*>(&pre3[4 * j]) =
+                  *reinterpret_cast<const int4*>(ab + S::kBufBytes + sw64(lane, j));
+          }
         }
-        // the staging buffer b was last used two chunks ago: its TMA store must have read it
+        // the staging set b was last used two chunks ago: its TMA stores must have read it
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
-        uint8_t* cb = cbuf0 + b * S::kBufBytes;
+        uint8_t* cb = cbuf0 + b * kOT * S::kBufBytes;
+        auto stage_bf16 = [&](uint8_t* dst, const __nv_bfloat162 (&v)[16]) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<int4*>(dst + sw64(lane, j)) = *reinterpret_cast<const int4*>(&v[4 * j]);
+        };
         if (EPI == kEpiF32) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *reinterpret_cast<int4*>(cb + sw128(lane, j)) =
                 make_int4(static_cast<int>(r[4 * j]), static_cast<int>(r[4 * j + 1]),
                           static_cast<int>(r[4 * j + 2]), static_cast<int>(r[4 * j + 3]));
+        } else if (EPI == kEpiSwiglu) {
+          __nv_bfloat162 o1[16], o3[16], oh[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 a1 = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+            const float2 a3 = make_float2(__uint_as_float(r3[2 * i]), __uint_as_float(r3[2 * i + 1]));
+            o1[i] = __floats2bfloat162_rn(a1.x, a1.y);
+            o3[i] = __floats2bfloat162_rn(a3.x, a3.y);
+            // h = silu(a1) a3 from the fp32 accumulators
+            oh[i] = __floats2bfloat162_rn(__fdividef(a1.x, 1.f + __expf(-a1.x)) * a3.x,
+                                          __fdividef(a1.y, 1.f + __expf(-a1.y)) * a3.y);
+          }
+          stage_bf16(cb, o1);
+          stage_bf16(cb + S::kBufBytes, o3);
+          stage_bf16(cb + 2 * S::kBufBytes, oh);
+        } else if (EPI == kEpiDSwiglu) {
+          __nv_bfloat162 d1[16], d3[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {  // dH (fp32) with the saved bf16 a1, a3
+            const float2 a1 = __bfloat1622float2(pre[i]), a3 = __bfloat1622float2(pre3[i]);
+            const float dh0 = __uint_as_float(r[2 * i]), dh1 = __uint_as_float(r[2 * i + 1]);
+            const float s0 = __frcp_rn(1.f + __expf(-a1.x)), s1 = __frcp_rn(1.f + __expf(-a1.y));
+            const float ds0 = s0 * (1.f + a1.x * (1.f - s0)), ds1 = s1 * (1.f + a1.y * (1.f - s1));
+            d1[i] = __floats2bfloat162_rn(dh0 * a3.x * ds0, dh1 * a3.y * ds1);
+            d3[i] = __floats2bfloat162_rn(dh0 * a1.x * s0, dh1 * a1.y * s1);
+          }
+          stage_bf16(cb, d1);
+          stage_bf16(cb + S::kBufBytes, d3);
         } else {
           __nv_bfloat162 out[16];
           if (EPI == kEpiBF16) {
@@ -447,11 +500,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               act[i] = __floats2bfloat162_rn(gf.x, gf.y);
               out[i] = __floats2bfloat162_rn(df.x, df.y);
             }
-            uint8_t* xb = xbuf0 + b * S::kBufBytes;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              *reinterpret_cast<int4*>(xb + sw64(lane, j)) =
-                  *reinterpret_cast<const int4*>(&act[4 * j]);
+            stage_bf16(cb + S::kBufBytes, act);
           } else {  // kEpiDGelu: out = acc * gelu'(pre-activation), gelu' saved by fwd1
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -462,17 +511,25 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               out[i] = __floats2bfloat162_rn(o.x, o.y);
             }
           }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<int4*>(cb + sw64(lane, j)) =
-                *reinterpret_cast<const int4*>(&out[4 * j]);
+          stage_bf16(cb, out);
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(cmap, cb, col0 + c * kEpiCols, row0);
-          if (EPI == kEpiGelu)
-            tma_store_2d(&map_x, xbuf0 + b * S::kBufBytes, col0 + c * kEpiCols, row0);
+          if (EPI == kEpiSwiglu) {
+            const int j = col0 + c * kEpiCols;  // a1 column in the interleaved 2f layout
+            tma_store_2d(cmap, cb, j, row0);
+            tma_store_2d(cmap, cb + S::kBufBytes, j + BN / 2, row0);
+            tma_store_2d(&map_x, cb + 2 * S::kBufBytes, col0 / 2 + c * kEpiCols, row0);
+          } else if (EPI == kEpiDSwiglu) {
+            const int a1 = a13_col(col0 + c * kEpiCols);
+            tma_store_2d(cmap, cb, a1, row0);
+            tma_store_2d(cmap, cb + S::kBufBytes, a1 + 128, row0);
+          } else {
+            tma_store_2d(cmap, cb, col0 + c * kEpiCols, row0);
+            if (EPI == kEpiGelu)
+              tma_store_2d(&map_x, cb + S::kBufBytes, col0 + c * kEpiCols, row0);
+          }
           bulk_commit();
         }
       }
@@ -531,24 +588,49 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 
+// Instantiated (A major, B major, epilogue) combinations.  BN = 256: every combination
+// the tests use; BN = 128 only the layer's own (N = d_ff not a multiple of 256).
 template <bool A_MN, bool B_MN, int BN, int CG>
 static int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb,
                         const CUtensorMap& mc, const CUtensorMap& mx, const GemmLaunch& args,
                         cudaStream_t stream) {
+  constexpr bool kFull = BN == 256;
   switch (epi) {
-    case kEpiBF16: return launch_variant<A_MN, B_MN, BN, kEpiBF16, CG>(ma, mb, mc, mx, args, stream);
-    case kEpiGelu: return launch_variant<A_MN, B_MN, BN, kEpiGelu, CG>(ma, mb, mc, mx, args, stream);
-    case kEpiDGelu: return launch_variant<A_MN, B_MN, BN, kEpiDGelu, CG>(ma, mb, mc, mx, args, stream);
-    case kEpiF32: return launch_variant<A_MN, B_MN, BN, kEpiF32, CG>(ma, mb, mc, mx, args, stream);
-    default: return kErrDimension;
+    case kEpiBF16:
+      if constexpr (kFull || !A_MN)
+        return launch_variant<A_MN, B_MN, BN, kEpiBF16, CG>(ma, mb, mc, mx, args, stream);
+      break;
+    case kEpiGelu:
+      if constexpr (kFull || (!A_MN && !B_MN))
+        return launch_variant<A_MN, B_MN, BN, kEpiGelu, CG>(ma, mb, mc, mx, args, stream);
+      break;
+    case kEpiDGelu:
+      if constexpr (kFull || (!A_MN && B_MN))
+        return launch_variant<A_MN, B_MN, BN, kEpiDGelu, CG>(ma, mb, mc, mx, args, stream);
+      break;
+    case kEpiF32:
+      if constexpr (kFull || (A_MN && B_MN))
+        return launch_variant<A_MN, B_MN, BN, kEpiF32, CG>(ma, mb, mc, mx, args, stream);
+      break;
+    case kEpiSwiglu:
+      if constexpr (kFull && !A_MN && !B_MN)
+        return launch_variant<A_MN, B_MN, BN, kEpiSwiglu, CG>(ma, mb, mc, mx, args, stream);
+      break;
+    case kEpiDSwiglu:
+      if constexpr (!A_MN && B_MN)
+        return launch_variant<A_MN, B_MN, BN, kEpiDSwiglu, CG>(ma, mb, mc, mx, args, stream);
+      break;
+    default:
+      break;
   }
+  set_error("grouped_gemm: operand majors / epilogue / N tile combination not instantiated");
+  return kErrDimension;
 }
 
-template <int CG>
+template <int BN, int CG>
 static int dispatch_major(int a_mn, int b_mn, int epi, const CUtensorMap& ma,
                           const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                           const GemmLaunch& args, cudaStream_t stream) {
-  constexpr int BN = 256;
   if (a_mn) {
     if (b_mn) return dispatch_epi<true, true, BN, CG>(epi, ma, mb, mc, mx, args, stream);
     return dispatch_epi<true, false, BN, CG>(epi, ma, mb, mc, mx, args, stream);
@@ -567,7 +649,7 @@ int epilogue_tmap(int epi, const void* base, int64_t ldc, int64_t rows, CUtensor
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,
                         int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                         int64_t c_rows, const GemmLaunch& args, cudaStream_t stream) {
-  constexpr int BN = 256;
+  const int BN = args.bn == 128 ? 128 : 256;
   if (args.total_tiles <= 0) return kOk;
   if (args.ldc % 32 != 0) return kErrDimension;
   const int cg = args.cta_group == 2 ? 2 : 1;
@@ -579,12 +661,20 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   if (rc != kOk) return rc;
   rc = epilogue_tmap(epi, args.c, args.ldc, c_rows, &mc);
   if (rc != kOk) return rc;
-  const void* xptr = epi == kEpiGelu ? args.c2 : (epi == kEpiDGelu ? args.aux : args.c);
-  rc = make_tmap_2d(&mx, xptr, args.ldc, c_rows, kEpiCols, 32, epi == kEpiF32 ? kDtF32 : kDtBF16,
+  // second tensor: GeLU's post-activation (same shape as C), SwiGLU's h (half the width of
+  // C), dgrad2's saved aux (same shape as C), else unused (C again)
+  const void* xptr = (epi == kEpiGelu || epi == kEpiSwiglu) ? args.c2
+                     : (epi == kEpiDGelu || epi == kEpiDSwiglu) ? args.aux : args.c;
+  const int64_t xld = epi == kEpiSwiglu ? args.ldc / 2 : args.ldc;
+  rc = make_tmap_2d(&mx, xptr, xld, c_rows, kEpiCols, 32, epi == kEpiF32 ? kDtF32 : kDtBF16,
                     epi == kEpiF32 ? 128 : 64);
   if (rc != kOk) return rc;
-  if (cg == 2) return dispatch_major<2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
-  return dispatch_major<1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+  if (BN == 128) {
+    if (cg == 2) return dispatch_major<128, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+    return dispatch_major<128, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+  }
+  if (cg == 2) return dispatch_major<256, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+  return dispatch_major<256, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
 }
 
 }  // namespace fssdp

@@ -1092,8 +1092,8 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
 
 int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* base_owner,
                             const uint8_t* target_mask, const uint8_t* pre_mask,
-                            const int64_t* route, int32_t d_model, int32_t d_ff, uint8_t* blob,
-                            int64_t blob_bytes, int32_t* header_out) {
+                            const int64_t* route, int32_t d_model, int32_t d_ff, int32_t n_mats,
+                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out) {
   // pre_mask (nullable): replicas already fetched by the early, estimate-based SpAG.  They
   // take the first replica slots (ascending expert id) and get no SpAG copy here.
   auto pre = [&](int e, int d) {
@@ -1101,7 +1101,8 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   };
   int64_t off[FSSDP_TAB_NSECTIONS], total;
   fssdp_tables_layout(E, D, off, &total);
-  if (blob_bytes < total || rank < 0 || rank >= D || d_model % 256 || d_ff % 256) {
+  if (blob_bytes < total || rank < 0 || rank >= D || d_model % 256 || d_ff % 128 ||
+      (n_mats != 2 && n_mats != 3)) {
     set_error("build_rank_tables: bad arguments");
     return FSSDP_ERR_DIMENSION;
   }
@@ -1229,10 +1230,14 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   auto longer = [&](int a, int b) { return seg_pad[rank][a] > seg_pad[rank][b]; };
   std::stable_sort(wg_order.begin(), wg_order.begin() + n_shared, longer);
   std::stable_sort(wg_order.begin() + n_shared, wg_order.end(), longer);
-  const int64_t d = d_model, f = d_ff;
-  const int n_tiles[6] = {static_cast<int>(f / 256), static_cast<int>(d / 256),
-                          static_cast<int>(f / 256), static_cast<int>(d / 256),
-                          static_cast<int>(d / 256), static_cast<int>(f / 256)};
+  // slot = [W1 (f x d) | W2 (d x f)] (GeLU, n_mats 2) or [W13 (2f x d) | W2] (SwiGLU, 3);
+  // n1 = fwd1's N.  N tiles of width f use 128 columns when f % 256 != 0; SwiGLU's fwd1
+  // always uses 256 (an a1|a3 block pair per tile)
+  const int64_t d = d_model, f = d_ff, nm = n_mats, n1 = (nm - 1) * f;
+  const int64_t bnf = f % 256 == 0 ? 256 : 128, bn1 = nm == 3 ? 256 : bnf;
+  const int n_tiles[6] = {static_cast<int>(n1 / bn1), static_cast<int>(d / 256),
+                          static_cast<int>(f / bnf), static_cast<int>(d / 256),
+                          static_cast<int>(d / 256), static_cast<int>(f / bnf)};
   int ints = 7;
   int32_t shared_tiles[2] = {0, 0};
   for (int gi = 0; gi < 6; ++gi) {
@@ -1249,21 +1254,22 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       const int32_t mt = static_cast<int32_t>(seg_pad[rank][s] / 128);
       const int32_t kt = static_cast<int32_t>(seg_pad[rank][s] / 64);
       fssdp_gemm_group& x = g[i];
+      const int32_t w1r = static_cast<int32_t>(s * nm * f), w2r = static_cast<int32_t>(s * nm * d);
       switch (gi) {
-        case 0: x = {mt, 0, st, 0, static_cast<int32_t>(s * 2 * f), 0, static_cast<int32_t>(d / 64), 0, st * f}; break;
-        case 1: x = {mt, 0, st, 0, static_cast<int32_t>(s * 2 * d), 0, static_cast<int32_t>(f / 64), 0, st * d}; break;
-        case 2: x = {mt, 0, st, 0, 0, static_cast<int32_t>(s * 2 * d), static_cast<int32_t>(d / 64), 0, st * f}; break;
-        case 3: x = {mt, 0, st, 0, 0, static_cast<int32_t>(s * 2 * f), static_cast<int32_t>(f / 64), 0, st * d}; break;
-        case 4: x = {static_cast<int32_t>(f / 128), 0, 0, st, 0, st, kt, 0, s * 2 * f * d}; break;
-        default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * 2 * f * d + f * d}; break;
+        case 0: x = {mt, 0, st, 0, w1r, 0, static_cast<int32_t>(d / 64), 0, st * n1}; break;
+        case 1: x = {mt, 0, st, 0, w2r, 0, static_cast<int32_t>(f / 64), 0, st * d}; break;
+        case 2: x = {mt, 0, st, 0, 0, w2r, static_cast<int32_t>(d / 64), 0, st * n1}; break;
+        case 3: x = {mt, 0, st, 0, 0, w1r, static_cast<int32_t>(n1 / 64), 0, st * d}; break;
+        case 4: x = {static_cast<int32_t>(n1 / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d}; break;
+        default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d + n1 * d}; break;
       }
       if (wgrad) {  // a replica's partial goes to its owner's staging slot
         const int e = slot_expert[rank][s];
         const int o = base_owner[e];
         if (o != rank) {
           x.c_dest = o + 1;
-          x.c_off = static_cast<int64_t>(stage_idx[static_cast<size_t>(e) * D + rank]) * 2 * f * d +
-                    (gi == 5 ? f * d : 0);
+          x.c_off = static_cast<int64_t>(stage_idx[static_cast<size_t>(e) * D + rank]) * nm * f * d +
+                    (gi == 5 ? n1 * d : 0);
         }
       }
       x.tile_start = tile;

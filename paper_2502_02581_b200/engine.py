@@ -332,8 +332,8 @@ class FssdpPlanner:
 
     def plan_with_tables(self, layer: int, counts, counts_ptr: int, rank: int, pre_ptr,
                          d_model: int, d_ff: int, blob, blob_ptr: int, header_ptr: int,
-                         blob_dev_ptr, stream, limits_ptr=None,
-                         decide: bool = True) -> Optional[LayerDecision]:
+                         blob_dev_ptr, stream, limits_ptr=None, decide: bool = True,
+                         n_mats: int = 2) -> Optional[LayerDecision]:
         """plan() fused with this rank's device tables and their upload: one native call on
         the planning critical path (fssdp_plan_layer_tables).  `counts` is the (D, E) int32
         host array at counts_ptr.  decide=False defers the LayerDecision to
@@ -350,7 +350,8 @@ class FssdpPlanner:
         knobs, est_ptr = self._layer_knobs(layer)
         N.check(N.LIB_RAW.fssdp_plan_layer_tables(
             E, self._owners_ptr(layer), est_ptr, counts_ptr, sc.topo_ref(self._topo_c),
-            N.C.byref(knobs), rank, pre_ptr, d_model, d_ff, limits_ptr, sc.p_target, sc.p_added,
+            N.C.byref(knobs), rank, pre_ptr, d_model, d_ff, n_mats, limits_ptr, sc.p_target,
+            sc.p_added,
             sc.p_route, sc.p_dbl, sc.p_flags, blob_ptr, len(blob), header_ptr, blob_dev_ptr,
             stream), "plan_layer_tables")
         self.last_target_ptr, self.last_route_ptr = sc.p_target, sc.p_route

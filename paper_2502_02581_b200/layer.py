@@ -31,7 +31,7 @@ from . import ops
 from .comm import HeapLayout, PeerGroup
 from .engine import FssdpPlanner
 from .errors import DimensionError, InternalError
-from .plan_tables import NativeTables
+from .plan_tables import NativeTables, n_tile_widths
 
 WG_TILE = 64  # FSSDP_WG_TILE (include/fssdp.h)
 GROUP_BYTES = N.C.sizeof(N.GemmGroup)  # fssdp_gemm_group
@@ -49,6 +49,15 @@ class LayerGeometry:
     max_tokens: int      # per rank per step
     world: int
     slots: int           # local expert slot capacity (owned + replicas)
+    activation: str = "gelu"  # "gelu": [W1 | W2];  "swiglu": [W13 | W2] (Mixtral/DeepSeek)
+
+    @property
+    def n_mats(self) -> int:  # expert matrices per slot
+        return 3 if self.activation == "swiglu" else 2
+
+    @property
+    def n1(self) -> int:  # fwd1's output width: a (GeLU) or the interleaved [a1|a3] (SwiGLU)
+        return (self.n_mats - 1) * self.d_ff
 
     @property
     def recv_cap(self) -> int:
@@ -56,12 +65,12 @@ class LayerGeometry:
         return (rows + 127) // 128 * 128
 
     @property
-    def slot_param_bytes(self) -> int:      # [W1 f×d | W2 d×f] bf16
-        return 4 * self.d_model * self.d_ff
+    def slot_param_bytes(self) -> int:      # [W1 f×d | W2 d×f] or [W13 2f×d | W2] bf16
+        return 2 * self.n_mats * self.d_model * self.d_ff
 
     @property
-    def slot_grad_elems(self) -> int:       # [dW1 | dW2] fp32
-        return 2 * self.d_model * self.d_ff
+    def slot_grad_elems(self) -> int:       # the same matrices in fp32
+        return self.n_mats * self.d_model * self.d_ff
 
     @property
     def expert_bytes(self) -> int:
@@ -80,8 +89,10 @@ class LayerGeometry:
                    (self.world - 1) * max(0, self.slots - owned_min))
 
     def validate(self) -> None:
-        if self.d_model % 256 or self.d_ff % 256:
-            raise DimensionError("d_model and d_ff must be multiples of 256 (GEMM N tile)")
+        if self.d_model % 256 or self.d_ff % 128:
+            raise DimensionError("d_model must be a multiple of 256 and d_ff of 128 (GEMM tiles)")
+        if self.activation not in ("gelu", "swiglu"):
+            raise DimensionError(f"unknown expert activation {self.activation!r}")
         if not 1 <= self.top_k <= min(8, self.num_experts) or self.num_experts > 64:
             raise DimensionError("need 1 <= top_k <= 8 and num_experts <= 64")
 
@@ -125,8 +136,10 @@ class FssdpMoE:
         self.off = {k: L.offset(prefix + k) for k in
                     ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage")}
         self.flags_off = L.offset("flags")
-        self.params = heap.tensor(self.off["params"], (geom.slots, 2 * d * f), torch.bfloat16)
-        self.grads = heap.tensor(self.off["grads"], (geom.slots, 2 * d * f), torch.float32)
+        self.params = heap.tensor(self.off["params"], (geom.slots, geom.n_mats * d * f),
+                                  torch.bfloat16)
+        self.grads = heap.tensor(self.off["grads"], (geom.slots, geom.n_mats * d * f),
+                                 torch.float32)
         self.xrecv = heap.tensor(self.off["xrecv"], (R, d), torch.bfloat16)
         self.y_e = heap.tensor(self.off["y"], (R, d), torch.bfloat16)
         self.dyrecv = heap.tensor(self.off["dyrecv"], (R, d), torch.bfloat16)
@@ -151,14 +164,27 @@ class FssdpMoE:
             blob = b"".join(ops.epilogue_tmap(ops.EPI_F32, base + self.off["stage"], ldc,
                                               stage_elems // ldc) for base in group.bases)
             self.dest_maps[name] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.dev)
-        # 2-D TMA views of the parameter region
+        # 2-D TMA views of the parameter region (nm = matrices per slot, n1 = (nm-1) f)
+        nm, n1 = geom.n_mats, geom.n1
         flat = self.params.view(-1)
-        self.w1_view = flat.view(geom.slots * 2 * f, d)                  # W1 of slot s: rows s*2f..
-        self.w2_view = flat[f * d:].view(geom.slots * 2 * d - d, f)      # W2 of slot s: rows s*2d..
-        # local activations (capacity-sized once, so plans never reallocate)
-        self.gprime = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)  # gelu'(X W1^T)
+        self.w1_view = flat.view(geom.slots * nm * f, d)              # W1/W13 of slot s: rows s*nm*f..
+        self.w2_view = flat[n1 * d:].view(geom.slots * nm * d - (nm - 1) * d, f)  # W2: rows s*nm*d..
+        # local activations (capacity-sized once, so plans never reallocate): fwd1 saves
+        # gelu'(a) (GeLU) or the pre-activations [a1|a3] (SwiGLU) for dgrad2's epilogue
+        self.gprime = torch.empty(R, n1, dtype=torch.bfloat16, device=self.dev)
         self.h = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
-        self.da = torch.empty(R, f, dtype=torch.bfloat16, device=self.dev)
+        self.da = torch.empty(R, n1, dtype=torch.bfloat16, device=self.dev)
+        self.epi_fwd1 = ops.EPI_SWIGLU if geom.activation == "swiglu" else ops.EPI_GELU
+        self.epi_dgrad2 = ops.EPI_DSWIGLU if geom.activation == "swiglu" else ops.EPI_DGELU
+        # per GEMM: 128-wide N tiles where N = d_ff is not a multiple of 256; CTA pairs where
+        # every group has an even number of 128-row tiles (wgrad1: M = n1)
+        bn1, bnf = n_tile_widths(f, nm)
+        bn = {"fwd1": bn1, "fwd2": 256, "dgrad2": bnf, "dgrad1": 256, "wgrad1": 256,
+              "wgrad2": bnf}
+        pair = {k: self.CTA_PAIR for k in bn}
+        pair["wgrad1"] = self.CTA_PAIR and (n1 // 128) % 2 == 0
+        self._gemm_flags = {k: (ops.GEMM_BN128 if bn[k] == 128 else 0) |
+                               (ops.GEMM_CTA_PAIR if pair[k] else 0) for k in bn}
         Tc = geom.max_tokens
         k = geom.top_k
         tiles = (Tc + ops.GATE_TILE - 1) // ops.GATE_TILE
@@ -210,38 +236,66 @@ class FssdpMoE:
         return sorted(base.chunks_on(self.rank))
 
     def init_parameters(self, seed: int) -> None:
-        """Deterministic per-expert init (independent of ownership): W1 ~ N(0, 1/d),
+        """Deterministic per-expert init (independent of ownership): W1 (W3) ~ N(0, 1/d),
         W2 ~ N(0, 1/f), Wg ~ N(0, 1/d) (replicated)."""
         d, f, E = self.g.d_model, self.g.d_ff, self.g.num_experts
         gen = torch.Generator(device=self.dev)
         gen.manual_seed(seed * 7919 + 17)
         self.wg.copy_(torch.randn(E, d, generator=gen, device=self.dev) / d ** 0.5)
+        n1 = self.g.n1
         for s, e in enumerate(self.owned_experts()):
-            w1, w2 = self.make_expert(e, seed)
-            self.params[s, : f * d].copy_(w1.reshape(-1))
-            self.params[s, f * d:].copy_(w2.reshape(-1))
+            mats = self.make_expert(e, seed)
+            self.params[s, : n1 * d].copy_(self.pack_w13(mats[:-1]).reshape(-1))
+            self.params[s, n1 * d:].copy_(mats[-1].reshape(-1))
         self._owned_expert_ids = self.owned_experts()
         self._n_owned = len(self._owned_expert_ids)
 
     def make_expert(self, e: int, seed: int):
+        """(W1 [f,d], W2 [d,f]) or, for SwiGLU, (W1, W3 [f,d], W2) — bf16, seeded per expert."""
         d, f = self.g.d_model, self.g.d_ff
         gen = torch.Generator(device=self.dev)
         gen.manual_seed(seed * 1_000_003 + 31 * e + 1)
         w1 = (torch.randn(f, d, generator=gen, device=self.dev) / d ** 0.5).bfloat16()
         w2 = (torch.randn(d, f, generator=gen, device=self.dev) / f ** 0.5).bfloat16()
-        return w1, w2
+        if self.g.activation != "swiglu":
+            return w1, w2
+        w3 = (torch.randn(f, d, generator=gen, device=self.dev) / d ** 0.5).bfloat16()
+        return w1, w3, w2
+
+    @staticmethod
+    def pack_w13(mats):
+        """[W1] or the block-interleaved [W1; W3] (128-row blocks, FSSDP_EPI_SWIGLU)."""
+        if len(mats) == 1:
+            return mats[0]
+        w1, w3 = mats
+        f, d = w1.shape
+        return torch.stack([w1.view(f // 128, 128, d), w3.view(f // 128, 128, d)], 1).reshape(2 * f, d)
+
+    @staticmethod
+    def unpack_w13(w13):
+        """Inverse of pack_w13 for an interleaved [2f, d] tensor: (W1, W3)."""
+        f2, d = w13.shape
+        v = w13.reshape(f2 // 256, 2, 128, d)
+        return v[:, 0].reshape(f2 // 2, d), v[:, 1].reshape(f2 // 2, d)
+
+    def _slot_mats(self, buf, e):
+        s = self._owned_expert_ids.index(e)
+        d, f, n1 = self.g.d_model, self.g.d_ff, self.g.n1
+        w2 = buf[s, n1 * d:].view(d, f)
+        if self.g.activation != "swiglu":
+            return buf[s, : f * d].view(f, d), w2
+        w1, w3 = self.unpack_w13(buf[s, : n1 * d].view(n1, d))
+        return w1, w3, w2
 
     def expert_weight(self, e: int):
-        """(W1 [f,d], W2 [d,f]) of an owned expert (views into the heap)."""
-        s = self._owned_expert_ids.index(e)
-        d, f = self.g.d_model, self.g.d_ff
-        return self.params[s, : f * d].view(f, d), self.params[s, f * d:].view(d, f)
+        """(W1 [f,d], W2 [d,f]) of an owned expert (views into the heap); SwiGLU: (W1, W3,
+        W2), W1/W3 de-interleaved copies."""
+        return self._slot_mats(self.params, e)
 
     def expert_grad(self, e: int):
-        """(dW1, dW2) fp32 of an owned expert after backward (SpRS-reduced)."""
-        s = self._owned_expert_ids.index(e)
-        d, f = self.g.d_model, self.g.d_ff
-        return self.grads[s, : f * d].view(f, d), self.grads[s, f * d:].view(d, f)
+        """(dW1, dW2) [SwiGLU: (dW1, dW3, dW2)] fp32 of an owned expert after backward
+        (SpRS-reduced)."""
+        return self._slot_mats(self.grads, e)
 
     # ------------------------------------------------------------ helpers
     def _stream(self):
@@ -289,7 +343,8 @@ class FssdpMoE:
         base_owner = self.planner._owners(self.layer)
         E, D = pre.shape
         tables = NativeTables(self.rank, base_owner, pre, np.zeros((D, E, D), dtype=np.int64),
-                              self.g.d_model, self.g.d_ff, out_bytes=self.pre_host_np)
+                              self.g.d_model, self.g.d_ff, out_bytes=self.pre_host_np,
+                              n_mats=self.g.n_mats)
         if tables.n_slots > self.g.slots:
             raise InternalError(f"early plan needs {tables.n_slots} slots > capacity {self.g.slots}")
         self.pre_mask, self.pre_mask_ptr, self.pre_tables = pre, pre.ctypes.data, tables
@@ -371,7 +426,7 @@ class FssdpMoE:
             self.layer, counts, self.counts_host_ptr, self.rank, self.pre_mask_ptr,
             self.g.d_model, self.g.d_ff, self.blob_host_np, self.blob_host_ptr,
             NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
-            decide=False)
+            decide=False, n_mats=self.g.n_mats)
         self._mark("planned")
         tables = NativeTables.from_header(E, D, self.blob_host_np)
         self.tables = self.packed = tables
@@ -473,7 +528,7 @@ class FssdpMoE:
                 tab = C.c_void_p(tab.value + n_sh * GROUP_BYTES)
         if total == 0:
             return
-        flags = (1 if self.N_FASTEST.get(name, False) else 0) | (2 if self.CTA_PAIR else 0)
+        flags = (1 if self.N_FASTEST.get(name, False) else 0) | self._gemm_flags[name]
         maps = ops._ptr(self.dest_maps.get(name))
         self._timed("gemm." + name, lambda: N.call(
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
@@ -481,8 +536,8 @@ class FssdpMoE:
             ops._ptr(c2), ops._ptr(aux), maps, ldc, c.numel() // ldc, flags, self._stream()))
 
     def phase_experts_fwd(self) -> None:
-        f, d = self.g.d_ff, self.g.d_model
-        self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.gprime, f, ops.EPI_GELU,
+        f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1
+        self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.gprime, n1, self.epi_fwd1,
                    c2=self.h)
         self._gemm("fwd2", self.h, False, self.w2_view, False, self.y_e, d, ops.EPI_BF16)
 
@@ -520,8 +575,8 @@ class FssdpMoE:
 
     def phase_bwd_shared(self) -> None:
         """dH -> dA (all slots), then the weight grads of the slots SpRS reduces."""
-        f, d = self.g.d_ff, self.g.d_model
-        self._gemm("dgrad2", self.dyrecv, False, self.w2_view, True, self.da, f, ops.EPI_DGELU,
+        f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1
+        self._gemm("dgrad2", self.dyrecv, False, self.w2_view, True, self.da, n1, self.epi_dgrad2,
                    aux=self.gprime)
         grads2d = self.grads.view(-1)
         self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32, part="shared")
@@ -642,20 +697,21 @@ class FssdpMoE:
 def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_tokens: int,
                  policy, *, rank: int = 0, world: int = 1, device="cuda", seed: int = 0,
                  peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
-                 per_token_expert_time: float | None = None, pg=None) -> FssdpMoE:
+                 per_token_expert_time: float | None = None, pg=None,
+                 activation: str = "gelu") -> FssdpMoE:
     """One rank per process: heap layout, IPC peer group (world > 1), planner, layer."""
     from .engine import ModelConfig
     from .topology import ClusterTopology
 
     m = policy.capacity_override if policy.capacity_override is not None else num_experts
     geom = LayerGeometry(d_model, d_ff, num_experts, top_k, max_tokens, world,
-                         default_slots(num_experts, world, m))
+                         default_slots(num_experts, world, m), activation)
     layout = HeapLayout()
     geom.add_regions(layout, "L0.")
     group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
     topo = ClusterTopology.for_nvswitch(world, peer_bw)
     if per_token_expert_time is None:  # fwd expert time per token-slot at the sustained bf16 peak
-        per_token_expert_time = 2.0 * 2 * d_model * d_ff / 1381.7e12
+        per_token_expert_time = 2.0 * geom.n_mats * d_model * d_ff / 1381.7e12
     cfg = ModelConfig(1, num_experts, geom.expert_bytes, 2 * d_model, attn_fwd_time,
                       per_token_expert_time)
     return FssdpMoE(geom, group, FssdpPlanner(cfg, topo, policy), 0, seed)

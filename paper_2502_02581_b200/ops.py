@@ -17,7 +17,8 @@ from .errors import DimensionError
 
 GATE_TILE = 64
 BM, BN, BK = 128, 256, 64
-EPI_BF16, EPI_GELU, EPI_DGELU, EPI_F32 = 0, 1, 2, 3
+EPI_BF16, EPI_GELU, EPI_DGELU, EPI_F32, EPI_SWIGLU, EPI_DSWIGLU = 0, 1, 2, 3, 4, 5
+GEMM_N_FASTEST, GEMM_CTA_PAIR, GEMM_BN128 = 1, 2, 4  # fssdp_grouped_gemm flags
 
 
 def _stream(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
@@ -69,7 +70,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
                  num_groups: int, n_tiles: int, total_tiles: int, c: torch.Tensor, ldc: int,
                  epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
                  aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
-                 cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None) -> None:
+                 cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None,
+                 bn128: bool = False) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
@@ -84,7 +86,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
     N.call("fssdp_grouped_gemm", int(a_mn), int(b_mn), int(epilogue), _ptr(a), a.shape[1],
            a.shape[0], _ptr(b), b.shape[1], b.shape[0], _ptr(groups_dev), num_groups, n_tiles,
            total_tiles, _ptr(c), _ptr(c2), _ptr(aux), _ptr(c_dest_maps), ldc, c.numel() // ldc,
-           (1 if n_fastest else 0) | (2 if cta_pair else 0), _stream(stream))
+           (GEMM_N_FASTEST if n_fastest else 0) | (GEMM_CTA_PAIR if cta_pair else 0) |
+           (GEMM_BN128 if bn128 else 0), _stream(stream))
 
 
 def epilogue_tmap(epilogue: int, base_ptr: int, ldc: int, rows: int) -> bytes:

@@ -80,13 +80,21 @@ def _finalize(groups: np.ndarray, n_tiles: int):
     return groups, n_tiles, int(tiles.sum())
 
 
+def n_tile_widths(d_ff: int, n_mats: int) -> tuple:
+    """(N tile of fwd1, N tile of the GEMMs whose N = d_ff): 128 when d_ff % 256 != 0;
+    SwiGLU's fwd1 always 256 (an a1|a3 block pair per tile) — fssdp_gemm_group docs."""
+    bnf = 256 if d_ff % 256 == 0 else 128
+    return (256 if n_mats == 3 else bnf), bnf
+
+
 def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None,
-                push=None):
+                push=None, n_mats: int = 2):
     """The six grouped-GEMM descriptor arrays of one rank (see gemm_sm100.cu).
 
-    Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16; viewed as
-    [(slots*2f) x d] rows for W1 and, from offset f*d, as [(slots*2d) x f] rows for W2.
-    Gradient slot s holds [dW1 (f x d) | dW2 (d x f)] fp32.
+    Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16 (GeLU, n_mats 2) or
+    [W13 (2f x d) | W2] (SwiGLU, n_mats 3, W13 block-interleaved); viewed as
+    [(slots*n_mats*f) x d] rows for W1/W13 and, from offset n1*d, as [(slots*n_mats*d) x f]
+    rows for W2 (n1 = (n_mats-1)*f, fwd1's N).  Gradient slots mirror it in fp32.
 
     `shared` (bool per segment): the wgrads list shared segments (experts with other
     holders — the SpRS inputs) first; the rest restart tile_start at 0 and run as a second
@@ -95,7 +103,9 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
 
     `push` (per segment: None, or (owner, staging index)): a replica's wgrad writes its
     partial gradient into the owner's staging slot (c_dest = owner + 1) — the SpRS wire."""
-    d, f = d_model, d_ff
+    d, f, nm = d_model, d_ff, n_mats
+    n1 = (nm - 1) * f
+    bn1, bnf = n_tile_widths(f, nm)
     n = len(seg_start)
     shared = [False] * n if shared is None else [bool(x) for x in shared]
     push = [None] * n if push is None else list(push)
@@ -103,38 +113,37 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     g = np.zeros(n, dtype=GROUP_DTYPE)
     for i in range(n):
         s = slot_of_seg[i]
-        mt = int(seg_padded[i] // 128)
         st = int(seg_start[i])
-        g[i] = (mt, 0, st, 0, s * 2 * f, 0, d // 64, 0, st * f)
-    out["fwd1"] = _finalize(g.copy(), f // 256)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * f, 0, d // 64, 0, st * n1)
+    out["fwd1"] = _finalize(g.copy(), n1 // bn1)
     for i in range(n):
         s = slot_of_seg[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * 2 * d, 0, f // 64, 0, st * d)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * d, 0, f // 64, 0, st * d)
     out["fwd2"] = _finalize(g.copy(), d // 256)
     for i in range(n):  # dH = dY . W2  (B = W2 [K=d][N=f], MN-major)
         s = slot_of_seg[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * 2 * d, d // 64, 0, st * f)
-    out["dgrad2"] = _finalize(g.copy(), f // 256)
-    for i in range(n):  # dXe = dA . W1  (B = W1 [K=f][N=d], MN-major)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * d, d // 64, 0, st * n1)
+    out["dgrad2"] = _finalize(g.copy(), f // bnf)
+    for i in range(n):  # dXe = dA . W1  (B = W1 / W13 [K=n1][N=d], MN-major)
         s = slot_of_seg[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * 2 * f, f // 64, 0, st * d)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * f, n1 // 64, 0, st * d)
     out["dgrad1"] = _finalize(g.copy(), d // 256)
     # each part longest-first (stable): the GEMM's snake tile order is then close to LPT
     order = (sorted([i for i in range(n) if shared[i]], key=lambda i: -int(seg_padded[i])) +
              sorted([i for i in range(n) if not shared[i]], key=lambda i: -int(seg_padded[i])))
     n_sh = sum(shared)
     split = [n_sh]
-    for name, rows, n_t, extra in (("wgrad1", f, d // 256, 0), ("wgrad2", d, f // 256, f * d)):
+    for name, rows, n_t, extra in (("wgrad1", n1, d // 256, 0), ("wgrad2", d, f // bnf, n1 * d)):
         gw = np.zeros(n, dtype=GROUP_DTYPE)
         for j, i in enumerate(order):  # dW1 = dA^T X, dW2 = dY^T H (K = the segment's tokens)
             s = slot_of_seg[i]
             st = int(seg_start[i])
             dest, slot = (0, s) if push[i] is None else (push[i][0] + 1, push[i][1])
             gw[j] = (rows // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), dest,
-                     slot * 2 * f * d + extra)
+                     slot * nm * f * d + extra)
         head, _, t_sh = _finalize(gw[:n_sh], n_t)
         tail, _, t_rest = _finalize(gw[n_sh:], n_t)
         out[name] = (np.concatenate([head, tail]), n_t, t_sh + t_rest)
@@ -143,7 +152,8 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
 
 
 def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray,
-                      route: np.ndarray, d_model: int, d_ff: int, pre_mask=None) -> RankTables:
+                      route: np.ndarray, d_model: int, d_ff: int, pre_mask=None,
+                      n_mats: int = 2) -> RankTables:
     """`pre_mask` (E, D): replicas already fetched by an earlier SpAG (same slots, no copy)."""
     E, D = target_mask.shape
     if route.shape != (D, E, D):
@@ -206,7 +216,7 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
     shared = [int(np.count_nonzero(target_mask[by_slot[s]])) > 1 for s in order]
     push = [None if int(base_owner[by_slot[s]]) == rank else
             (int(base_owner[by_slot[s]]), stage[(by_slot[s], rank)]) for s in order]
-    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared, push)
+    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared, push, n_mats)
     n_owned = sum(1 for e in slots if int(base_owner[e]) == rank)
     return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
                       seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),
@@ -244,7 +254,7 @@ class NativeTables:
     _hdr_ptr = _hdr.ctypes.data
 
     def __init__(self, rank, base_owner, target_mask, route, d_model, d_ff, out_bytes=None,
-                 pre_mask=None):
+                 pre_mask=None, n_mats=2):
         E, D = target_mask.shape
         _, nbytes = _layout(E, D)
         blob = out_bytes if out_bytes is not None else np.zeros(nbytes, dtype=np.uint8)
@@ -254,16 +264,16 @@ class NativeTables:
         pre = None if pre_mask is None else np.ascontiguousarray(pre_mask, dtype=np.uint8)
         self._build(rank, E, D, owner.ctypes.data, mask.ctypes.data,
                     None if pre is None else pre.ctypes.data, rt.ctypes.data, d_model, d_ff,
-                    blob, blob.ctypes.data)
+                    blob, blob.ctypes.data, n_mats)
 
     @classmethod
     def from_pointers(cls, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff,
-                      blob, blob_ptr) -> "NativeTables":
+                      blob, blob_ptr, n_mats=2) -> "NativeTables":
         """Planning critical path: inputs already in place (FssdpPlanner scratch buffers),
         addresses resolved by the caller."""
         obj = cls.__new__(cls)
         obj._build(rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
-                   blob_ptr)
+                   blob_ptr, n_mats)
         return obj
 
     @classmethod
@@ -287,7 +297,7 @@ class NativeTables:
         self.n_stage = h[28]
 
     def _build(self, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
-               blob_ptr) -> None:
+               blob_ptr, n_mats=2) -> None:
         from . import _native as N
 
         self.E, self.D = E, D
@@ -296,8 +306,8 @@ class NativeTables:
         if len(blob) < self.nbytes:
             raise InternalError("plan tables exceed the staging buffer")
         N.check(N.LIB_RAW.fssdp_build_rank_tables(rank, D, E, owner_ptr, mask_ptr, pre_ptr,
-                                                  route_ptr, d_model, d_ff, blob_ptr, self.nbytes,
-                                                  self._hdr_ptr), "build_rank_tables")
+                                                  route_ptr, d_model, d_ff, n_mats, blob_ptr,
+                                                  self.nbytes, self._hdr_ptr), "build_rank_tables")
         self._parse_header()
 
     def section(self, name, dtype, count):

@@ -260,3 +260,158 @@ def test_wgrad_c_dest_scatter(pair):
     assert torch.all(stage[1][:M] == 5.0)  # untouched staging slots stay
     assert torch.all(stage[0][M:] == 5.0)
     assert torch.all(C[M:] == 0.0)
+
+
+def _interleave(w1, w3):
+    f, k = w1.shape
+    return torch.stack([w1.view(f // 128, 128, k), w3.view(f // 128, 128, k)], 1).reshape(2 * f, k)
+
+
+def _deinterleave(m):
+    r, f2 = m.shape
+    v = m.reshape(r, f2 // 256, 2, 128)
+    return v[:, :, 0].reshape(r, f2 // 2), v[:, :, 1].reshape(r, f2 // 2)
+
+
+@pytest.mark.parametrize("f,pair", [(256, True), (384, True), (384, False)])
+def test_swiglu_fwd1_epilogue(f, pair):
+    """fwd1 of SwiGLU experts: C = bf16([a1|a3]) (block-interleaved), C2 = bf16(silu(a1)·a3)."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(5)
+    K = 256
+    m_tiles = [2, 4, 2]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    A = torch.randn(R, K, device=dev).bfloat16()
+    W1 = (torch.randn(G, f, K, device=dev) / K ** 0.5).bfloat16()
+    W3 = (torch.randn(G, f, K, device=dev) / K ** 0.5).bfloat16()
+    B = torch.cat([_interleave(W1[g], W3[g]) for g in range(G)])  # [G*2f, K]
+    C = torch.zeros(R, 2 * f, device=dev, dtype=torch.bfloat16)
+    H = torch.zeros(R, f, device=dev, dtype=torch.bfloat16)
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, g * 2 * f, 0, K // 64, r0 * 2 * f))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, 2 * f // 256, dev)
+    ops.grouped_gemm(A, False, B, False, gd, ng, 2 * f // 256, total, C, 2 * f,
+                     epilogue=ops.EPI_SWIGLU, c2=H, cta_pair=pair)
+    torch.cuda.synchronize()
+    r0 = 0
+    for g, mt in enumerate(m_tiles):
+        sl = slice(r0, r0 + mt * 128)
+        a1 = A[sl].float() @ W1[g].float().T
+        a3 = A[sl].float() @ W3[g].float().T
+        c1, c3 = _deinterleave(C[sl])
+        _close(c1, a1)
+        _close(c3, a3)
+        _close(H[sl], torch.nn.functional.silu(a1) * a3)
+        r0 += mt * 128
+
+
+@pytest.mark.parametrize("f,bn128", [(256, False), (512, False), (384, True), (512, True)])
+def test_swiglu_dgrad2_epilogue(f, bn128):
+    """dgrad2 of SwiGLU experts: acc = dH = dY·W2; with the saved [a1|a3]:
+    C = bf16([dH·a3·silu'(a1) | dH·silu(a1)]) (block-interleaved)."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(6)
+    d = 256
+    m_tiles = [2, 2]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    dY = torch.randn(R, d, device=dev).bfloat16()
+    W2 = (torch.randn(G * d, f, device=dev) / f ** 0.5).bfloat16()  # [K=d][N=f] per group
+    aux = torch.randn(R, 2 * f, device=dev).bfloat16()
+    C = torch.zeros(R, 2 * f, device=dev, dtype=torch.bfloat16)
+    bn = 128 if bn128 else 256
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, 0, g * d, d // 64, r0 * 2 * f))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, f // bn, dev)
+    ops.grouped_gemm(dY, False, W2, True, gd, ng, f // bn, total, C, 2 * f,
+                     epilogue=ops.EPI_DSWIGLU, aux=aux, cta_pair=True, bn128=bn128)
+    torch.cuda.synchronize()
+    r0 = 0
+    for g, mt in enumerate(m_tiles):
+        sl = slice(r0, r0 + mt * 128)
+        dh = dY[sl].float() @ W2[g * d:(g + 1) * d].float()
+        a1, a3 = (t.float() for t in _deinterleave(aux[sl]))
+        s = torch.sigmoid(a1)
+        d1, d3 = _deinterleave(C[sl])
+        _close(d1, dh * a3 * s * (1 + a1 * (1 - s)))
+        _close(d3, dh * a1 * s)
+        r0 += mt * 128
+
+
+@pytest.mark.parametrize("epi", ["bf16", "gelu", "dgelu"])
+def test_bn128_kmajor(epi):
+    """N = 384 (not a multiple of 256): 128-wide N tiles."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(7)
+    K, N = 256, 384
+    m_tiles = [2, 2, 4]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    A = torch.randn(R, K, device=dev).bfloat16()
+    b_mn = epi == "dgelu"
+    B = ((torch.randn(G * K, N, device=dev) if b_mn else torch.randn(G * N, K, device=dev))
+         / K ** 0.5).bfloat16()
+    C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    C2 = torch.zeros_like(C)
+    aux = torch.randn(R, N, device=dev).bfloat16()
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        if b_mn:
+            rows.append((mt, r0, 0, 0, g * K, K // 64, r0 * N))
+        else:
+            rows.append((mt, r0, 0, g * N, 0, K // 64, r0 * N))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N // 128, dev)
+    e = {"bf16": ops.EPI_BF16, "gelu": ops.EPI_GELU, "dgelu": ops.EPI_DGELU}[epi]
+    ops.grouped_gemm(A, False, B, b_mn, gd, ng, N // 128, total, C, N, epilogue=e, c2=C2,
+                     aux=aux, cta_pair=True, bn128=True)
+    torch.cuda.synchronize()
+    r0 = 0
+    for g, mt in enumerate(m_tiles):
+        sl = slice(r0, r0 + mt * 128)
+        if b_mn:
+            acc = A[sl].float() @ B[g * K:(g + 1) * K].float()
+        else:
+            acc = A[sl].float() @ B[g * N:(g + 1) * N].float().T
+        if epi == "bf16":
+            _close(C[sl], acc)
+        elif epi == "gelu":
+            _close(C2[sl], torch.nn.functional.gelu(acc, approximate="tanh"))
+        else:
+            _close(C[sl], acc * aux[sl].float())
+        r0 += mt * 128
+
+
+def test_bn128_wgrad_fp32():
+    """wgrad2-style fp32 output with N = 384 (128-wide N tiles), MN-major A and B."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(8)
+    M, N = 256, 384
+    segs = [256, 0, 512]
+    G = len(segs)
+    Rt = sum(segs)
+    At = torch.randn(Rt, M, device=dev).bfloat16()
+    Bt = torch.randn(Rt, N, device=dev).bfloat16()
+    C = torch.full((G * M, N), 3.0, device=dev)
+    rows, k0 = [], 0
+    for g, s_ in enumerate(segs):
+        rows.append((M // 128, 0, k0, 0, k0, s_ // 64, g * M * N))
+        k0 += s_
+    gd, ng, total = _groups(ops, rows, N // 128, dev)
+    ops.grouped_gemm(At, True, Bt, True, gd, ng, N // 128, total, C, N, epilogue=ops.EPI_F32,
+                     cta_pair=True, bn128=True)
+    torch.cuda.synchronize()
+    k0 = 0
+    for g, s_ in enumerate(segs):
+        ref = At[k0:k0 + s_].float().T @ Bt[k0:k0 + s_].float()
+        _close(C[g * M:(g + 1) * M], ref, rel=2e-3, abs_=1e-4)
+        k0 += s_

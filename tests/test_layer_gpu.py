@@ -23,9 +23,9 @@ from paper_2502_02581_b200.layer import (FssdpMoE, LayerGeometry, default_slots,
 pytestmark = pytest.mark.gpu
 
 
-def build(world, E, d, f, k, T, policy, seed=0, bias=None):
+def build(world, E, d, f, k, T, policy, seed=0, bias=None, activation="gelu"):
     m = policy.capacity_override if policy.capacity_override is not None else E
-    geom = LayerGeometry(d, f, E, k, T, world, default_slots(E, world, m))
+    geom = LayerGeometry(d, f, E, k, T, world, default_slots(E, world, m), activation)
     layout = HeapLayout()
     geom.add_regions(layout, "L0.")
     groups = emulated_group(layout, world)
@@ -58,10 +58,14 @@ def zipf_bias(E, s=1.2, seed=0):
     return torch.tensor(np.log(p / p.sum()), dtype=torch.float32, device="cuda")
 
 
-def test_single_rank_matches_oracle():
-    E, d, f, k, T = 8, 256, 1024, 2, 1000
+@pytest.mark.parametrize("f,activation", [(1024, "gelu"), (384, "gelu"), (384, "swiglu"),
+                                          (512, "swiglu")])
+def test_single_rank_matches_oracle(f, activation):
+    """GeLU and SwiGLU experts; d_ff = 384 exercises 128-wide N tiles (and, for GeLU, the
+    single-CTA wgrad1: d_ff / 128 is odd)."""
+    E, d, k, T = 8, 256, 2, 1000
     pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2)
-    (ly,) = build(1, E, d, f, k, T, pol, seed=3, bias=zipf_bias(E))
+    (ly,) = build(1, E, d, f, k, T, pol, seed=3, bias=zipf_bias(E), activation=activation)
     g = torch.Generator(device="cuda").manual_seed(5)
     x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
     dy = (torch.randn(T, d, device="cuda", generator=g) * 0.1).bfloat16()
@@ -73,13 +77,21 @@ def test_single_rank_matches_oracle():
     experts = {e: tuple(f32(t) for t in ly.expert_weight(e)) for e in range(E)}
     ref = TO.moe_layer_fwd_bwd(f32(x), idx, w, ly.wg.cpu().numpy(), experts, f32(dy))
     close(f32(y), ref["y"], what="y")
-    close(ly.slot_grad[:T].cpu().numpy(), ref["g"], rel=1e-3, abs_=1e-4, what="g")
-    close(ly.dlogit[:T].cpu().numpy(), ref["dlogit"], rel=1e-3, abs_=1e-5, what="dlogit")
+    # g = <dy, Y_slot>: tight against the device's own expert rows (the kernel's dot
+    # product), loose against the oracle (bf16 rows differ by an ulp here and there)
+    pos = ly.slot_pos[:T].long().cpu()
+    y_rows = ly.y_e.float().cpu()[pos]                                    # [T, k, d]
+    g_dev = torch.einsum("td,tkd->tk", dy.float().cpu(), y_rows).numpy()
+    close(ly.slot_grad[:T].cpu().numpy(), g_dev, rel=1e-5, abs_=1e-5, what="g (own rows)")
+    close(ly.slot_grad[:T].cpu().numpy(), ref["g"], rel=5e-3, abs_=1e-4, what="g")
+    close(ly.dlogit[:T].cpu().numpy(), ref["dlogit"], rel=5e-3, abs_=1e-5, what="dlogit")
     close(f32(dx), ref["dx"], what="dx")
     for e in range(E):
-        gw1, gw2 = ly.expert_grad(e)
-        close(f32(gw1), ref["dW1"][e], abs_=1e-5, what=f"dW1[{e}]")
-        close(f32(gw2), ref["dW2"][e], abs_=1e-5, what=f"dW2[{e}]")
+        grads = ly.expert_grad(e)
+        close(f32(grads[0]), ref["dW1"][e], abs_=1e-5, what=f"dW1[{e}]")
+        close(f32(grads[-1]), ref["dW2"][e], abs_=1e-5, what=f"dW2[{e}]")
+        if activation == "swiglu":
+            close(f32(grads[1]), ref["dW3"][e], abs_=1e-5, what=f"dW3[{e}]")
     close(ly.dwg.cpu().numpy(), ref["dWg"], rel=1e-3, abs_=1e-5, what="dWg")
     # padding rows of the receive buffers are zero (wgrad K blocks rely on it)
     t = ly.tables
@@ -89,22 +101,25 @@ def test_single_rank_matches_oracle():
         assert not xr[a:b].any()
 
 
-@pytest.mark.parametrize("world,E,policy_kw", [
-    (4, 8, dict(overlap_override=8, capacity_override=2)),
-    (2, 16, dict(overlap_override=4, capacity_override=3, rematerialize=True)),
-    (8, 16, dict(overlap_override=6, capacity_override=2)),
-    (4, 8, dict(kind=F.PolicyKind.EP)),
+@pytest.mark.parametrize("world,E,policy_kw,f,activation", [
+    (4, 8, dict(overlap_override=8, capacity_override=2), 512, "gelu"),
+    (2, 16, dict(overlap_override=4, capacity_override=3, rematerialize=True), 512, "gelu"),
+    (8, 16, dict(overlap_override=6, capacity_override=2), 512, "gelu"),
+    (4, 8, dict(kind=F.PolicyKind.EP), 512, "gelu"),
+    (4, 8, dict(overlap_override=8, capacity_override=2, rematerialize=True), 384, "swiglu"),
+    (8, 16, dict(overlap_override=6, capacity_override=2), 384, "gelu"),
 ])
-def test_multi_rank_equals_single_rank(world, E, policy_kw):
+def test_multi_rank_equals_single_rank(world, E, policy_kw, f, activation):
     """FSSDP over N emulated ranks == the same tokens on one rank (y, dx bit-exact;
     SpRS-reduced owner grads within fp32 tolerance), over 3 iterations so history-driven
     adoption and calibration both act."""
-    d, f, k, Tr = 256, 512, 2, 384
+    d, k, Tr = 256, 2, 384
     kind = policy_kw.pop("kind", F.PolicyKind.FSSDP)
     pol = F.Policy(kind, **policy_kw)
     bias = zipf_bias(E, 1.3, seed=world)
-    multi = build(world, E, d, f, k, Tr, pol, seed=7, bias=bias)
-    single = build(1, E, d, f, k, Tr * world, F.Policy(F.PolicyKind.EP), seed=7, bias=bias)[0]
+    multi = build(world, E, d, f, k, Tr, pol, seed=7, bias=bias, activation=activation)
+    single = build(1, E, d, f, k, Tr * world, F.Policy(F.PolicyKind.EP), seed=7, bias=bias,
+                   activation=activation)[0]
     g = torch.Generator(device="cuda").manual_seed(11)
     replicas_seen = prefetched = 0
     for it in range(3):
@@ -132,10 +147,8 @@ def test_multi_rank_equals_single_rank(world, E, policy_kw):
         # owners hold the SpRS-reduced gradient of every expert
         for e in range(E):
             owner = dec.base.owner(e)
-            gm1, gm2 = multi[owner].expert_grad(e)
-            gs1, gs2 = single.expert_grad(e)
-            close(f32(gm1), f32(gs1), rel=1e-4, abs_=1e-6, what=f"dW1[{e}] it{it}")
-            close(f32(gm2), f32(gs2), rel=1e-4, abs_=1e-6, what=f"dW2[{e}] it{it}")
+            for j, (gm, gs) in enumerate(zip(multi[owner].expert_grad(e), single.expert_grad(e))):
+                close(f32(gm), f32(gs), rel=1e-4, abs_=1e-6, what=f"grad{j}[{e}] it{it}")
         dwg = sum(ly.dwg.double() for ly in multi)
         close(dwg.cpu().numpy(), single.dwg.double().cpu().numpy(), rel=1e-4, abs_=1e-6,
               what="dWg")

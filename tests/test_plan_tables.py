@@ -60,13 +60,15 @@ def test_native_tables_equal_python_tables():
     from paper_2502_02581_b200.plan_tables import GEMM_NAMES, NativeTables
 
     rng = np.random.default_rng(3)
-    for _ in range(40):
+    shapes = [(1024, 4096, 2), (256, 384, 2), (256, 384, 3), (2048, 1408, 3), (4096, 14336, 3)]
+    for it in range(40):
         D, E = int(rng.choice([1, 2, 4, 8])), int(rng.choice([8, 16, 64]))
+        d, f, nm = shapes[it % len(shapes)]
         dec, _ = _random_plan(rng, D, E, 300, 2)
         owner = dec.base.owners()
         for r in range(D):
-            py = build_rank_tables(r, owner, dec.target.mask, dec.route, 1024, 4096)
-            nt = NativeTables(r, owner, dec.target.mask, dec.route, 1024, 4096)
+            py = build_rank_tables(r, owner, dec.target.mask, dec.route, d, f, n_mats=nm)
+            nt = NativeTables(r, owner, dec.target.mask, dec.route, d, f, n_mats=nm)
             assert nt.slots == py.slots and nt.n_owned == py.n_owned
             assert nt.recv_rows == py.recv_rows
             for name in ("seg_start", "seg_rows", "seg_padded", "route_cum", "recv_base",
