@@ -50,6 +50,7 @@ class LayerGeometry:
     world: int
     slots: int           # local expert slot capacity (owned + replicas)
     activation: str = "gelu"  # "gelu": [W1 | W2];  "swiglu": [W13 | W2] (Mixtral/DeepSeek)
+    owned_max: int = 0        # max experts of this layer a rank owns (0: ceil(E / world))
 
     @property
     def n_mats(self) -> int:  # expert matrices per slot
@@ -83,6 +84,8 @@ class LayerGeometry:
         slots in total."""
         if self.world <= 1:
             return 0
+        if self.owned_max:  # heterogeneous sharding: per-rank ownership varies
+            return (self.world - 1) * self.owned_max
         owned_max = -(-self.num_experts // self.world)
         owned_min = self.num_experts // self.world
         return min((self.world - 1) * owned_max,
@@ -240,7 +243,7 @@ class FssdpMoE:
         W2 ~ N(0, 1/f), Wg ~ N(0, 1/d) (replicated)."""
         d, f, E = self.g.d_model, self.g.d_ff, self.g.num_experts
         gen = torch.Generator(device=self.dev)
-        gen.manual_seed(seed * 7919 + 17)
+        gen.manual_seed(seed * 7919 + 17 + 1_000_033 * self.layer)
         self.wg.copy_(torch.randn(E, d, generator=gen, device=self.dev) / d ** 0.5)
         n1 = self.g.n1
         for s, e in enumerate(self.owned_experts()):
@@ -254,7 +257,7 @@ class FssdpMoE:
         """(W1 [f,d], W2 [d,f]) or, for SwiGLU, (W1, W3 [f,d], W2) — bf16, seeded per expert."""
         d, f = self.g.d_model, self.g.d_ff
         gen = torch.Generator(device=self.dev)
-        gen.manual_seed(seed * 1_000_003 + 31 * e + 1)
+        gen.manual_seed(seed * 1_000_003 + 31 * e + 1 + 100_003 * self.layer)
         w1 = (torch.randn(f, d, generator=gen, device=self.dev) / d ** 0.5).bfloat16()
         w2 = (torch.randn(d, f, generator=gen, device=self.dev) / f ** 0.5).bfloat16()
         if self.g.activation != "swiglu":
@@ -715,6 +718,54 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
     cfg = ModelConfig(1, num_experts, geom.expert_bytes, 2 * d_model, attn_fwd_time,
                       per_token_expert_time)
     return FssdpMoE(geom, group, FssdpPlanner(cfg, topo, policy), 0, seed)
+
+
+def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
+                     max_tokens: int, m: int, activation: str = "gelu") -> list:
+    """Per-layer geometry under the planner's current ShardPlan (even or heterogeneous):
+    slot capacity = the most experts any rank owns in that layer + m replica slots."""
+    geoms = []
+    for base in planner.shards.per_layer:
+        D, E = base.num_devices, base.num_chunks
+        owned_max = max(len(base.chunks_on(d)) for d in range(D))
+        geoms.append(LayerGeometry(d_model, d_ff, E, top_k, max_tokens, D,
+                                   min(E, owned_max + max(0, m)), activation, owned_max))
+    return geoms
+
+
+def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top_k: int,
+                 max_tokens: int, policy, *, rank: int = 0, world: int = 1, device="cuda",
+                 seed: int = 0, peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
+                 per_token_expert_time: float | None = None, pg=None,
+                 activation: str = "gelu", load_profile=None) -> list:
+    """num_layers FSSDP MoE layers sharing one planner (one iteration = every layer's
+    forward, then backward in reverse, then planner.finish()) and one symmetric heap.
+    load_profile [L, E] (expected per-expert loads): the initial ShardPlan comes from
+    heterogeneous_sharding (Alg. 2, planner.py:302-385) instead of the even split."""
+    from .engine import ModelConfig
+    from .planner import GlobalLoadProfile, heterogeneous_sharding
+    from .topology import ClusterTopology
+
+    nm = 3 if activation == "swiglu" else 2
+    m = policy.capacity_override if policy.capacity_override is not None else num_experts
+    topo = ClusterTopology.for_nvswitch(world, peer_bw)
+    if per_token_expert_time is None:
+        per_token_expert_time = 2.0 * nm * d_model * d_ff / 1381.7e12
+    cfg = ModelConfig(num_layers, num_experts, 2 * nm * d_model * d_ff, 2 * d_model,
+                      attn_fwd_time, per_token_expert_time)
+    if not 1 <= num_layers <= 8:
+        raise DimensionError("1 <= num_layers <= 8 (8 barrier slots per layer in the flag pad)")
+    planner = FssdpPlanner(cfg, topo, policy)
+    if load_profile is not None:
+        planner.shards = heterogeneous_sharding(
+            GlobalLoadProfile(np.asarray(load_profile, dtype=np.float64)), planner.t, topo)
+    geoms = layer_geometries(planner, d_model, d_ff, top_k, max_tokens, m, activation)
+    layout = HeapLayout()
+    for li, geom in enumerate(geoms):
+        geom.add_regions(layout, f"L{li}.")
+    group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
+    return [FssdpMoE(geom, group, planner, li, seed, prefix=f"L{li}.")
+            for li, geom in enumerate(geoms)]
 
 
 class FssdpMoEFunction(torch.autograd.Function):

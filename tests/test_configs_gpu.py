@@ -1,0 +1,142 @@
+"""BASELINE.json configurations as parity cases (configs 1, 3, 4; config 2 is the bench
+line, config 5 the sparse sweep), at reduced token counts, with N logical ranks in
+lockstep on one GPU (PeerGroup "emulated").  Bit-exact multi-rank == single-rank for y and
+dx of every layer; the single-rank run against the numpy oracle where it is affordable.
+
+* cfg1: 8 experts, top-2, d_model 256, d_ff 1024 (GeLU), 4 devices, 4096 tokens.
+* cfg3 (Mixtral-shaped, scaled 1/8 in d_model / d_ff): SwiGLU experts, 8 experts, 4 layers
+  with heterogeneous sharding (Alg. 2) from a skewed load profile on 8 devices.
+* cfg4 (DeepSeek-style fine-grained, d_model scaled 1/8): 64 SwiGLU experts, d_ff 1408
+  (128-wide N tiles), Zipf-skewed gate, re-materialization on.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_02581_b200 as F
+from oracle import tensor_oracle as TO
+from paper_2502_02581_b200.comm import HeapLayout, emulated_group
+from paper_2502_02581_b200.layer import (FssdpMoE, layer_geometries, run_lockstep_backward,
+                                         run_lockstep_forward)
+
+pytestmark = pytest.mark.gpu
+
+
+def zipf_bias(E, s, seed):
+    p = 1.0 / np.arange(1, E + 1) ** s
+    p = p[np.random.default_rng(seed).permutation(E)]
+    return torch.tensor(np.log(p / p.sum()), dtype=torch.float32, device="cuda")
+
+
+def build_model(world, L, E, d, f, k, T, policy, activation, profile=None, bias=None, seed=3):
+    """L layers x `world` emulated ranks: layers[l][r]."""
+    nm = 3 if activation == "swiglu" else 2
+    topo = F.ClusterTopology.for_nvswitch(world)
+    cfg = F.ModelConfig(L, E, 2 * nm * d * f, 2 * d, 1e-3, 1e-6)
+    planners = [F.FssdpPlanner(cfg, topo, policy) for _ in range(world)]
+    if profile is not None:
+        shards = F.heterogeneous_sharding(F.GlobalLoadProfile(profile), planners[0].t, topo)
+        for p in planners:
+            p.shards = shards
+    m = policy.capacity_override if policy.capacity_override is not None else E
+    geoms = layer_geometries(planners[0], d, f, k, T, m, activation)
+    layout = HeapLayout()
+    for li, g in enumerate(geoms):
+        g.add_regions(layout, f"L{li}.")
+    groups = emulated_group(layout, world)
+    layers = [[FssdpMoE(geoms[li], groups[r], planners[r], li, seed, prefix=f"L{li}.")
+               for r in range(world)] for li in range(L)]
+    if bias is not None:
+        for row in layers:
+            for ly in row:
+                ly.gate_bias.copy_(bias)
+    return layers
+
+
+def run_step(layers, xs, dys, remat):
+    """Forward through every layer, backward in reverse; returns per-layer (ys, dxs)."""
+    outs = []
+    h = xs
+    for row in layers:
+        h = run_lockstep_forward(row, h)
+        outs.append(h)
+    g = dys
+    grads = []
+    for row in reversed(layers):
+        g = run_lockstep_backward(row, g, rematerialize=remat)
+        grads.append(g)
+    for ly in layers[0]:
+        ly.planner.finish()
+    return outs, grads[::-1]
+
+
+def compare(world, L, E, d, f, k, Tr, policy, activation, profile=None, bias=None, iters=2,
+            oracle=False):
+    multi = build_model(world, L, E, d, f, k, Tr, policy, activation, profile, bias)
+    single = build_model(1, L, E, d, f, k, Tr * world, F.Policy(F.PolicyKind.EP), activation,
+                         bias=bias)
+    g = torch.Generator(device="cuda").manual_seed(17)
+    replicas = 0
+    for it in range(iters):
+        x = torch.randn(world * Tr, d, device="cuda", generator=g).bfloat16()
+        dy = (torch.randn(world * Tr, d, device="cuda", generator=g) * 0.05).bfloat16()
+        ym, dxm = run_step(multi, list(x.split(Tr)), list(dy.split(Tr)), policy.rematerialize)
+        ys, dxs = run_step(single, [x], [dy], False)
+        torch.cuda.synchronize()
+        for li in range(L):
+            assert torch.equal(torch.cat(ym[li]), ys[li][0]), f"layer {li} y differs (it {it})"
+            assert torch.equal(torch.cat(dxm[li]), dxs[li][0]), f"layer {li} dx differs (it {it})"
+            dec = multi[li][0].decision
+            replicas += len(dec.target.entries) - E
+            for e in range(E):  # owners hold the SpRS-reduced gradients
+                o = dec.base.owner(e)
+                for gm, gs in zip(multi[li][o].expert_grad(e), single[li][0].expert_grad(e)):
+                    gm, gs = gm.double(), gs.double()
+                    assert (gm - gs).abs().max() <= 1e-4 * gs.abs().max() + 1e-6
+    if oracle:  # the single-rank run of the first layer against the numpy restatement
+        ly = single[0][0]
+        T = world * Tr
+        x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+        dy = (torch.randn(T, d, device="cuda", generator=g) * 0.05).bfloat16()
+        y = ly.forward(x)
+        dx = ly.backward(dy)
+        torch.cuda.synchronize()
+        idx = ly.topk_idx[:T].cpu().numpy()
+        w = ly.topk_w[:T].cpu().numpy()
+        experts = {e: tuple(t.float().cpu().numpy() for t in ly.expert_weight(e))
+                   for e in range(E)}
+        ref = TO.moe_layer_fwd_bwd(x.float().cpu().numpy(), idx, w, ly.wg.cpu().numpy(),
+                                   experts, dy.float().cpu().numpy())
+        for name, out in (("y", y), ("dx", dx)):
+            o, r = out.float().cpu().numpy(), ref[name]
+            assert np.abs(o - r).max() <= 2e-2 * np.abs(r).max() + 1e-3, name
+    return replicas
+
+
+def test_cfg1_toy_layer():
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2)
+    replicas = compare(4, 1, 8, 256, 1024, 2, 1024, pol, "gelu", bias=zipf_bias(8, 1.2, 1),
+                       oracle=True)
+    assert replicas > 0
+
+
+def test_cfg3_mixtral_shaped_heterogeneous_sharding():
+    L, E, D = 4, 8, 8
+    rng = np.random.default_rng(0)
+    profile = rng.dirichlet(np.full(E, 0.3), size=L) * 1e4  # skewed per-layer loads
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=2, capacity_override=1)
+    topo = F.ClusterTopology.for_nvswitch(D)
+    shards = F.heterogeneous_sharding(F.GlobalLoadProfile(profile), 2, topo)
+    per_layer = [[len(shards.per_layer[li].chunks_on(d)) for d in range(D)] for li in range(L)]
+    assert any(max(c) > 1 for c in per_layer), "heterogeneous sharding should be uneven per layer"
+    compare(D, L, E, 512, 1792, 2, 128, pol, "swiglu", profile=profile,
+            bias=zipf_bias(E, 1.0, 3))
+
+
+def test_cfg4_fine_grained_swiglu_remat():
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=16, capacity_override=4,
+                   rematerialize=True)
+    replicas = compare(4, 1, 64, 256, 1408, 2, 512, pol, "swiglu", bias=zipf_bias(64, 1.2, 4),
+                       oracle=True)
+    assert replicas > 0
