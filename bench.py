@@ -33,12 +33,41 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "MoE fwd+bwd tokens/s at 1/2/4/8 B200; sparse AG/RS GB/s vs NVLink peak"
-CFG2 = dict(num_experts=16, top_k=2, d_model=1024, d_ff=4096, tokens_per_gpu=16384)
-# FSSDP knobs (engine.py:88-121): t = 8 replicable experts, m = 4 replica slots per GPU —
-# chosen offline with the bit-exact planner for the lowest max/mean device load at N = 4/8.
-POLICY = dict(overlap_override=8, capacity_override=4, calibration=True, rematerialize=False,
-              reshard_interval=0)
-ZIPF_S = 1.2
+# BASELINE.json configs.  cfg2 is the metric's configuration (the default bench line); the
+# others are available with --config for reference measurements (one MoE layer of that
+# shape; cfg3's heterogeneous sharding over 4 layers is covered by tests/test_configs_gpu.py).
+# FSSDP knobs (engine.py:88-121) for cfg2: t = 8 replicable experts, m = 4 replica slots per
+# GPU — chosen offline with the bit-exact planner for the lowest max/mean device load at N = 4/8.
+CONFIGS = {
+    "cfg1": dict(num_experts=8, top_k=2, d_model=256, d_ff=1024, tokens_per_gpu=1024,
+                 activation="gelu", zipf_s=1.2,
+                 policy=dict(overlap_override=4, capacity_override=2, calibration=True,
+                             rematerialize=False, reshard_interval=0),
+                 workload="cfg1: toy MoE layer, 8 experts top-2, d_model 256, d_ff 1024 GeLU, "
+                          "1024 tokens/GPU"),
+    "cfg2": dict(num_experts=16, top_k=2, d_model=1024, d_ff=4096, tokens_per_gpu=16384,
+                 activation="gelu", zipf_s=1.2,
+                 policy=dict(overlap_override=8, capacity_override=4, calibration=True,
+                             rematerialize=False, reshard_interval=0),
+                 workload="cfg2: single GPT-MoE layer fwd+bwd (FSSDP), 16 experts top-2, "
+                          "d_model 1024, d_ff 4096 GeLU, 16K tokens/GPU, Zipf(1.2) gate skew"),
+    "cfg3": dict(num_experts=8, top_k=2, d_model=4096, d_ff=14336, tokens_per_gpu=8192,
+                 activation="swiglu", zipf_s=1.0,
+                 policy=dict(overlap_override=2, capacity_override=1, calibration=True,
+                             rematerialize=False, reshard_interval=0),
+                 workload="cfg3: Mixtral-8x7B-shaped MoE layer, 8 SwiGLU experts top-2, "
+                          "d_model 4096, d_ff 14336, 8K tokens/GPU"),
+    "cfg4": dict(num_experts=64, top_k=2, d_model=2048, d_ff=1408, tokens_per_gpu=16384,
+                 activation="swiglu", zipf_s=1.2,
+                 policy=dict(overlap_override=16, capacity_override=4, calibration=True,
+                             rematerialize=True, reshard_interval=0),
+                 workload="cfg4: 64 fine-grained SwiGLU experts top-2, d_model 2048, d_ff 1408, "
+                          "16K tokens/GPU, Zipf(1.2), re-materialization"),
+}
+CFG = CONFIGS["cfg2"]
+CFG2 = CFG  # the metric's configuration
+POLICY = CFG["policy"]
+ZIPF_S = CFG["zipf_s"]
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 
@@ -49,7 +78,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tokens", type=int, default=CFG2["tokens_per_gpu"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default: config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -147,15 +177,18 @@ class OracleWorkload:
         self.wg = (rng.standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
         p = 1.0 / np.arange(1, E + 1) ** ZIPF_S
         self.bias = np.log(p[rng.permutation(E)] / p.sum()).astype(np.float32)
-        self.experts = {
-            e: (TO.bf16_round((rng.standard_normal((f, d)) / np.sqrt(d)).astype(np.float32)),
-                TO.bf16_round((rng.standard_normal((d, f)) / np.sqrt(f)).astype(np.float32)))
-            for e in range(E)}
+        nm = 3 if CFG["activation"] == "swiglu" else 2
+
+        def mat(rows, cols, fan_in):
+            return TO.bf16_round((rng.standard_normal((rows, cols)) / np.sqrt(fan_in))
+                                 .astype(np.float32))
+        self.experts = {e: tuple([mat(f, d, d) for _ in range(nm - 1)] + [mat(d, f, f)])
+                        for e in range(E)}
         self.dy = TO.bf16_round((0.05 * rng.standard_normal((sample_tokens, d))).astype(np.float32))
         self.topo = PO.Topo(1, 1, NVLINK_PEER_GBS * 1e9, NVLINK_PEER_GBS * 1e9)
         self.knobs = dict(t=POLICY["overlap_override"], m=POLICY["capacity_override"],
-                          calibration=True, rematerialize=False, expert_bytes=4 * d * f,
-                          token_bytes=2 * d, attn_fwd_time=1e-3, ptt=2.0 * 2 * d * f / 1381.7e12)
+                          calibration=True, rematerialize=False, expert_bytes=2 * nm * d * f,
+                          token_bytes=2 * d, attn_fwd_time=1e-3, ptt=2.0 * nm * d * f / 1381.7e12)
 
     def step(self) -> float:
         np, PO, TO = self.np, self.PO, self.TO
@@ -180,6 +213,13 @@ class OracleWorkload:
         return n
 
 
+def cpu_sample_tokens(at_cfg2: int) -> int:
+    """The CPU sample, scaled so a step costs about what `at_cfg2` tokens cost at cfg2."""
+    nm = 3 if CFG["activation"] == "swiglu" else 2
+    scale = (2 * 1024 * 4096) / (nm * CFG["d_model"] * CFG["d_ff"])
+    return int(max(64, min(at_cfg2 * scale, CFG["tokens_per_gpu"])))
+
+
 def cpu_oracle_rate(sample_tokens: int, budget_s: float):
     wl = OracleWorkload(sample_tokens)
     wl.step()  # warm-up
@@ -195,7 +235,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sample = 2048
+    sample = cpu_sample_tokens(2048)
     wl = OracleWorkload(sample)
     for _ in range(args.warmup):
         wl.step()
@@ -210,7 +250,7 @@ def run_reference(args):
         "config": _config(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": det["threads"],
                          "kind": "port",
-                         "sample": f"{sample} tokens of cfg2 per step through oracle/ (numpy "
+                         "sample": f"{sample} tokens of {args.config} per step through oracle/ (numpy "
                                    f"fwd+bwd restatement + planner port), scaled to tokens/s"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -219,8 +259,7 @@ def run_reference(args):
 
 
 def _config(args, world):
-    return {"workload": "cfg2: single GPT-MoE layer fwd+bwd (FSSDP), 16 experts top-2, "
-                        "d_model 1024, d_ff 4096 GeLU, 16K tokens/GPU, Zipf(1.2) gate skew",
+    return {"workload": CFG["workload"], "activation": CFG["activation"],
             "experts": CFG2["num_experts"], "top_k": CFG2["top_k"], "d_model": CFG2["d_model"],
             "d_ff": CFG2["d_ff"], "tokens_per_gpu": args.tokens,
             "global_batch_tokens": args.tokens * world, "parallelism": f"fssdp{world}",
@@ -269,7 +308,8 @@ def run_ours(args):
     T = args.tokens
     pol = F.Policy(F.PolicyKind.FSSDP, **POLICY)
     layer = create_layer(CFG2["d_model"], CFG2["d_ff"], CFG2["num_experts"], CFG2["top_k"], T,
-                         pol, rank=rank, world=world, device=dev, seed=1234)
+                         pol, rank=rank, world=world, device=dev, seed=1234,
+                         activation=CFG["activation"])
     E = CFG2["num_experts"]
     p = 1.0 / np.arange(1, E + 1) ** ZIPF_S
     p = p[np.random.default_rng(42).permutation(E)]
@@ -352,7 +392,8 @@ def run_ours(args):
                   for s, e in ev) / args.steps
     gemm_launches = sum(len(ev) for key, ev in timers.items() if key.startswith("gemm."))
     rows_rank = float(dec.route[:, :, rank].sum())
-    flops_rank = 3 * 2 * rows_rank * 2 * d * f   # fwd + dgrad + wgrad
+    nmats = 3 if CFG["activation"] == "swiglu" else 2
+    flops_rank = 3 * 2 * rows_rank * nmats * d * f   # fwd + dgrad + wgrad
     spag_ms = sum(s.elapsed_time(e) for key in ("spag", "spag_pre")
                   for s, e in timers.get(key, [])) / args.steps
     sprs_ms = sum(s.elapsed_time(e) for s, e in timers.get("sprs", [])) / args.steps
@@ -380,7 +421,8 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step "
                 "(the N=1 step's GEMM launches)", "traffic_source": traffic_src,
                 "kernel": "fssdp grouped_gemm_kernel (tcgen05), all 6 GEMMs of the step",
-                "algorithmic_flops": "3 x 2 x routed_rows x 2 x d_model x d_ff per rank",
+                "algorithmic_flops": "3 x 2 x routed_rows x n_mats x d_model x d_ff per rank "
+                                     "(n_mats 2 GeLU, 3 SwiGLU)",
                 "peak_source": f"{peak_src}, sustained bf16 (kernels timed inside a long step)",
                 "gemm_ms_per_step_per_rank": [round(v, 4) for v in allr[:, 0]],
                 "gemm_share_of_step": float(allr[:, 0].max() / ms_max),
@@ -485,9 +527,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, det = cpu_oracle_rate(1024, 8.0)
+        sample = cpu_sample_tokens(1024)
+        rate, det = cpu_oracle_rate(sample, 8.0)
         cpu = {"value": rate, "unit": "tokens/s", "cores": det["threads"], "kind": "port",
-               "sample": f"1024-token batches of cfg2 through oracle/ (numpy fwd+bwd + planner "
+               "sample": f"{sample}-token batches of {args.config} through oracle/ (numpy fwd+bwd + planner "
                          f"port), {det['steps']} batches in {det['seconds']:.1f} s"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -506,8 +549,18 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def select_config(name: str) -> None:
+    global CFG, CFG2, POLICY, ZIPF_S
+    CFG = CFG2 = CONFIGS[name]
+    POLICY = CFG["policy"]
+    ZIPF_S = CFG["zipf_s"]
+
+
 def main():
     args = parse()
+    select_config(args.config)
+    if args.tokens is None:
+        args.tokens = CFG["tokens_per_gpu"]
     if args.impl == "reference":
         run_reference(args)
     else:
