@@ -23,6 +23,7 @@ from .costmodel import TrafficMatrix, collective_latency, overlap_degree
 from .errors import ConfigError, TraceMismatchError
 from .placement import ChunkPlacement, ShardPlan
 from .planner import GlobalLoadProfile, MaterializationPlan, estimate_loads, heterogeneous_sharding
+from .traces import TraceRecorder
 
 
 @dataclass(frozen=True)
@@ -181,7 +182,8 @@ class FssdpPlanner:
     Usage per iteration:  begin_iteration();  plan_layer(l, counts_l) for each layer
     (after that layer's gate);  end_iteration(step_counts)."""
 
-    def __init__(self, config: ModelConfig, topology, policy: Policy) -> None:
+    def __init__(self, config: ModelConfig, topology, policy: Policy,
+                 record_trace: bool = False) -> None:
         if policy.kind not in (PolicyKind.FSSDP, PolicyKind.EP):
             raise ConfigError(f"unknown policy kind {policy.kind!r}")
         self.config = config
@@ -208,6 +210,8 @@ class FssdpPlanner:
         self.last_reshard_time = 0.0
         self.last_reshard_moves: list = []
         self._step = None
+        # the gate counts of every finished iteration, as a moesim trace (traces.py)
+        self.recorder = TraceRecorder() if record_trace else None
 
     # -- helpers ------------------------------------------------------------------
     def _owners(self, layer: int) -> np.ndarray:
@@ -380,6 +384,8 @@ class FssdpPlanner:
                 f"step has {len(step)} layers, config declares {self.config.layers}")
         for l, counts in enumerate(step):
             self.history[l].append(np.asarray(counts, dtype=np.int64))
+        if self.recorder is not None:
+            self.recorder.push(step)
         self.iteration += 1
 
     def candidate(self, layer: int) -> Optional[np.ndarray]:

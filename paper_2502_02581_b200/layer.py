@@ -701,7 +701,7 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
                  policy, *, rank: int = 0, world: int = 1, device="cuda", seed: int = 0,
                  peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
                  per_token_expert_time: float | None = None, pg=None,
-                 activation: str = "gelu") -> FssdpMoE:
+                 activation: str = "gelu", record_trace: bool = False) -> FssdpMoE:
     """One rank per process: heap layout, IPC peer group (world > 1), planner, layer."""
     from .engine import ModelConfig
     from .topology import ClusterTopology
@@ -717,7 +717,7 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
         per_token_expert_time = 2.0 * geom.n_mats * d_model * d_ff / 1381.7e12
     cfg = ModelConfig(1, num_experts, geom.expert_bytes, 2 * d_model, attn_fwd_time,
                       per_token_expert_time)
-    return FssdpMoE(geom, group, FssdpPlanner(cfg, topo, policy), 0, seed)
+    return FssdpMoE(geom, group, FssdpPlanner(cfg, topo, policy, record_trace), 0, seed)
 
 
 def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
@@ -737,7 +737,7 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
                  max_tokens: int, policy, *, rank: int = 0, world: int = 1, device="cuda",
                  seed: int = 0, peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
                  per_token_expert_time: float | None = None, pg=None,
-                 activation: str = "gelu", load_profile=None) -> list:
+                 activation: str = "gelu", load_profile=None, record_trace: bool = False) -> list:
     """num_layers FSSDP MoE layers sharing one planner (one iteration = every layer's
     forward, then backward in reverse, then planner.finish()) and one symmetric heap.
     load_profile [L, E] (expected per-expert loads): the initial ShardPlan comes from
@@ -755,7 +755,7 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
                       attn_fwd_time, per_token_expert_time)
     if not 1 <= num_layers <= 8:
         raise DimensionError("1 <= num_layers <= 8 (8 barrier slots per layer in the flag pad)")
-    planner = FssdpPlanner(cfg, topo, policy)
+    planner = FssdpPlanner(cfg, topo, policy, record_trace)
     if load_profile is not None:
         planner.shards = heterogeneous_sharding(
             GlobalLoadProfile(np.asarray(load_profile, dtype=np.float64)), planner.t, topo)

@@ -263,6 +263,25 @@ def gen_shard_score(rng, n):
     return out
 
 
+def gen_traces(rng, n):
+    """traces.py: the reference's own JSONL text of seeded synthetic traces."""
+    import tempfile
+
+    out = []
+    for _ in range(n):
+        meta = moesim.TraceMeta(int(rng.integers(1, 7)), int(rng.integers(1, 4)),
+                                int(rng.choice([4, 8, 16, 64])), int(rng.choice([1, 2, 4, 8])),
+                                int(rng.choice([1, 7, 128, 1000, 4096])))
+        skew = float(rng.choice([0.25, 0.5, 1.0, 2.0]))
+        drift = float(rng.choice([0.0, 0.02, 0.05, 0.3]))
+        seed = int(rng.integers(0, 10_000))
+        path = tempfile.mktemp(suffix=".jsonl")
+        moesim.save_trace(moesim.gen_synthetic_trace(meta, skew=skew, drift=drift, seed=seed), path)
+        out.append(dict(meta=meta.to_json_obj(), skew=skew, drift=drift, seed=seed,
+                        jsonl=open(path).read()))
+    return out
+
+
 def main():
     rng = np.random.default_rng(20250204)
     data = dict(
@@ -276,6 +295,7 @@ def main():
         shard_score=gen_shard_score(rng, 120),
         replays=gen_replays(rng),
     )
+    data["traces"] = gen_traces(rng, 24)
     data["_meta"] = dict(generator="tests/golden/make_goldens.py", reference="/root/reference/pkg/src (moesim 0.1.0)",
                          numpy=np.__version__, seed=20250204)
     text = json.dumps(data, separators=(",", ":"))
