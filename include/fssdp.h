@@ -355,6 +355,10 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
  * this rank's heap (param_off + dst_slot * slot_bytes).  128-bit coalesced loads. */
 int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
                const int32_t* copies, int32_t n_copies, void* stream);
+/* The same pull with separate heap offsets for the source slots (on src_rank) and the
+ * destination slots (here) — re-sharding moves owned shards through a staging region. */
+int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off, int64_t dst_off,
+                       int64_t slot_bytes, const int32_t* copies, int32_t n_copies, void* stream);
 
 /* K8: SparseReduceScatter, owner side.  The holders' wgrads already pushed their partial
  * gradients into this rank's staging slots (c_dest groups); here, per job

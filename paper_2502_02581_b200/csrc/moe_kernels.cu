@@ -918,8 +918,9 @@ __global__ void __launch_bounds__(256)
 constexpr int kTmaSub = 8 * 1024;
 constexpr int kTmaRing = 4;  // 32 KB of static smem per CTA -> several CTAs per SM
 __global__ void __launch_bounds__(32)
-    spag_tma_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t param_off,
-                    int64_t slot_bytes, const int32_t* __restrict__ copies, int64_t chunk) {
+    spag_tma_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t src_off,
+                    int64_t dst_off, int64_t slot_bytes, const int32_t* __restrict__ copies,
+                    int64_t chunk) {
   __shared__ __align__(128) uint8_t ring[kTmaRing][kTmaSub];
   __shared__ __align__(8) uint64_t bar[kTmaRing];
   const int job = blockIdx.y;
@@ -929,9 +930,9 @@ __global__ void __launch_bounds__(32)
   const int64_t src_slot = copies[3 * job + 1];
   const int64_t dst_slot = copies[3 * job + 2];
   const int64_t bytes = imin64(chunk, slot_bytes - begin);
-  const char* src = reinterpret_cast<const char*>(peer_bases[src_rank] + param_off) +
+  const char* src = reinterpret_cast<const char*>(peer_bases[src_rank] + src_off) +
                     src_slot * slot_bytes + begin;
-  char* dst = reinterpret_cast<char*>(peer_bases[rank] + param_off) + dst_slot * slot_bytes + begin;
+  char* dst = reinterpret_cast<char*>(peer_bases[rank] + dst_off) + dst_slot * slot_bytes + begin;
   for (int i = 0; i < kTmaRing; ++i) mbar_init(&bar[i], 1);
   fence_barrier_init();
   const int nsub = static_cast<int>((bytes + kTmaSub - 1) / kTmaSub);
@@ -1260,10 +1261,10 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
   return launch_status();
 }
 
-int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
-               const int32_t* copies, int32_t n_copies, void* stream) {
+int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off, int64_t dst_off,
+                       int64_t slot_bytes, const int32_t* copies, int32_t n_copies, void* stream) {
   if (slot_bytes % 16 != 0) {
-    set_error("spag: slot_bytes must be a multiple of 16");
+    set_error("gather_slots: slot_bytes must be a multiple of 16");
     return kErrDimension;
   }
   if (n_copies <= 0) return kOk;
@@ -1271,21 +1272,27 @@ int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int6
     const char* v = getenv("FSSDP_SPAG_IMPL");
     return (v && strcmp(v, "ldg") == 0) ? 0 : 1;  // default: TMA-staged bulk copies
   }();
-  if (impl == 1) {
+  if (impl == 1 || src_off != dst_off) {
     int64_t chunk = slot_bytes * n_copies / (2 * static_cast<int64_t>(num_sms()));
     chunk = (chunk + kTmaSub - 1) / kTmaSub * kTmaSub;
     if (chunk < 4 * kTmaSub) chunk = 4 * kTmaSub;
     if (chunk > (1 << 20)) chunk = 1 << 20;
     dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
-    spag_tma_kernel<<<grid, 32, 0, as_stream(stream)>>>(peer_bases, rank, param_off, slot_bytes,
-                                                        copies, chunk);
+    spag_tma_kernel<<<grid, 32, 0, as_stream(stream)>>>(peer_bases, rank, src_off, dst_off,
+                                                        slot_bytes, copies, chunk);
     return launch_status();
   }
   const int64_t chunk = coll_chunk_bytes(slot_bytes * n_copies, num_sms());
   dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
-  spag_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, param_off, slot_bytes, copies,
+  spag_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, src_off, slot_bytes, copies,
                                                    chunk);
   return launch_status();
+}
+
+int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
+               const int32_t* copies, int32_t n_copies, void* stream) {
+  return fssdp_gather_slots(peer_bases, rank, param_off, param_off, slot_bytes, copies, n_copies,
+                            stream);
 }
 
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,

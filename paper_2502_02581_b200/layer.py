@@ -37,7 +37,7 @@ WG_TILE = 64  # FSSDP_WG_TILE (include/fssdp.h)
 GROUP_BYTES = N.C.sizeof(N.GemmGroup)  # fssdp_gemm_group
 
 # barrier slots (flag pads) used by one layer; layer i uses base + 8*i
-BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_SPAG, BAR_SPRS = range(8)
+BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_RESHARD, BAR_SPRS = range(8)
 
 
 @dataclass(frozen=True)
@@ -51,6 +51,7 @@ class LayerGeometry:
     slots: int           # local expert slot capacity (owned + replicas)
     activation: str = "gelu"  # "gelu": [W1 | W2];  "swiglu": [W13 | W2] (Mixtral/DeepSeek)
     owned_max: int = 0        # max experts of this layer a rank owns (0: ceil(E / world))
+    reshard: bool = False     # heterogeneous re-sharding enabled: a staging region for moves
 
     @property
     def n_mats(self) -> int:  # expert matrices per slot
@@ -109,6 +110,8 @@ class LayerGeometry:
         layout.add(prefix + "dxe", R * d * 2)
         layout.add(prefix + "counts", (self.world * self.num_experts * 4 + 15) // 16 * 16)
         layout.add(prefix + "stage", max(1, self.stage_slots) * self.slot_grad_elems * 4)
+        # re-shard staging: the old owned shards, pulled by their new owners
+        layout.add(prefix + "reshard", (self.slots if self.reshard else 1) * self.slot_param_bytes)
 
 
 def default_slots(num_experts: int, world: int, m: int) -> int:
@@ -137,7 +140,8 @@ class FssdpMoE:
         heap = group.local
         d, f, E, R = geom.d_model, geom.d_ff, geom.num_experts, geom.recv_cap
         self.off = {k: L.offset(prefix + k) for k in
-                    ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage")}
+                    ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage",
+                     "reshard")}
         self.flags_off = L.offset("flags")
         self.params = heap.tensor(self.off["params"], (geom.slots, geom.n_mats * d * f),
                                   torch.bfloat16)
@@ -231,6 +235,8 @@ class FssdpMoE:
         self.T = 0
         self.x = None
         self._owned_expert_ids = None
+        self._base_owner = None      # owner per expert of the partition the params follow
+        self._reshard_pending = None  # device copy list of a re-shard gather, or None
         self.init_parameters(seed)
 
     # ------------------------------------------------------------ parameters
@@ -252,6 +258,7 @@ class FssdpMoE:
             self.params[s, n1 * d:].copy_(mats[-1].reshape(-1))
         self._owned_expert_ids = self.owned_experts()
         self._n_owned = len(self._owned_expert_ids)
+        self._base_owner = np.asarray(self.planner.shards.per_layer[self.layer].owners())
 
     def make_expert(self, e: int, seed: int):
         """(W1 [f,d], W2 [d,f]) or, for SwiGLU, (W1, W3 [f,d], W2) — bf16, seeded per expert."""
@@ -338,6 +345,9 @@ class FssdpMoE:
         self._pre_launch = False
         if not self.PREFETCH:
             return
+        if self._base_owner is not None and not np.array_equal(
+                self._base_owner, self.planner._owners(self.layer)):
+            return  # a re-shard of this layer is pending: its owners' slots are not in place
         pre = self.planner.candidate(self.layer)
         if pre is None:
             return
@@ -431,6 +441,8 @@ class FssdpMoE:
             NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
             decide=False, n_mats=self.g.n_mats)
         self._mark("planned")
+        if self.planner.last_reshard_moves:
+            self._reshard_stage()
         tables = NativeTables.from_header(E, D, self.blob_host_np)
         self.tables = self.packed = tables
         self.gemm = tables.gemm
@@ -472,7 +484,48 @@ class FssdpMoE:
         if self.tables.n_spag:
             self._spag_launch("spag", self.blob_dev, self.tables, main)
 
+    # ------------------------------------------------------------ re-sharding
+    # When the planner's re-shard trigger (engine.py:470-487) adopts a new ShardPlan, the
+    # owned shards follow it: every rank copies its old owned slots into its staging region
+    # (planning phase), then — after a device barrier — every rank pulls its new owned
+    # experts, in slot order, from their old owners' staging (dispatch phase, before the
+    # dispatch's own barrier, so no replica is pulled from a shard still in flight).  Only
+    # parameters move: this layer keeps no optimizer state (the reference prices 7×S per
+    # moved expert, engine.py:233, for parameters + Adam state).
+    def _reshard_stage(self) -> None:
+        new_owner = np.asarray(self.planner.shards.per_layer[self.layer].owners())
+        if np.array_equal(new_owner, self._base_owner):
+            return  # this layer's partition did not change
+        if not self.g.reshard:
+            raise InternalError("re-sharding needs a layer built with reshard=True "
+                                "(policy.reshard_interval > 0)")
+        nb = self._n_owned * self.g.slot_param_bytes
+        if nb:
+            stage = self.group.local.tensor(self.off["reshard"], (nb,), torch.uint8)
+            stage.copy_(self.params.view(torch.uint8).view(-1)[:nb])
+        old_owner = self._base_owner
+        old_slots = {r: sorted(int(e) for e in np.flatnonzero(old_owner == r))
+                     for r in range(self.world)}
+        new_owned = sorted(int(e) for e in np.flatnonzero(new_owner == self.rank))
+        copies = np.array([(int(old_owner[e]), old_slots[int(old_owner[e])].index(e), s)
+                           for s, e in enumerate(new_owned)], dtype=np.int32).reshape(-1, 3)
+        self._reshard_pending = torch.from_numpy(copies).to(self.dev)
+        self._owned_expert_ids = new_owned
+        self._n_owned = len(new_owned)
+        self._base_owner = new_owner
+
+    def _reshard_gather(self) -> None:
+        copies = self._reshard_pending
+        if copies is None:
+            return
+        self._reshard_pending = None
+        self.phase_barrier(BAR_RESHARD)  # every old owner has staged its shards
+        self._call("fssdp_gather_slots", self._pb(), self.rank, self.off["reshard"],
+                   self.off["params"], self.g.slot_param_bytes, ops._ptr(copies),
+                   copies.shape[0], self._stream())
+
     def phase_dispatch(self) -> None:
+        self._reshard_gather()
         t = self.tables
         slot, epoch = self._bar(BAR_DISPATCH)
         self._call("fssdp_dispatch", ops._ptr(self.x), ops._ptr(self.topk_idx),
@@ -708,7 +761,8 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
 
     m = policy.capacity_override if policy.capacity_override is not None else num_experts
     geom = LayerGeometry(d_model, d_ff, num_experts, top_k, max_tokens, world,
-                         default_slots(num_experts, world, m), activation)
+                         default_slots(num_experts, world, m), activation, 0,
+                         policy.reshard_interval > 0)
     layout = HeapLayout()
     geom.add_regions(layout, "L0.")
     group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
@@ -723,13 +777,18 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
 def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
                      max_tokens: int, m: int, activation: str = "gelu") -> list:
     """Per-layer geometry under the planner's current ShardPlan (even or heterogeneous):
-    slot capacity = the most experts any rank owns in that layer + m replica slots."""
+    slot capacity = the most experts any rank owns in that layer + m replica slots.  With
+    re-sharding on, a layer may later own up to a device's whole share across layers
+    (ShardPlan slot totals, placement.py:240-250): the capacity covers that."""
     geoms = []
+    reshard = planner.policy.reshard_interval > 0
     for base in planner.shards.per_layer:
         D, E = base.num_devices, base.num_chunks
         owned_max = max(len(base.chunks_on(d)) for d in range(D))
+        if reshard:
+            owned_max = min(E, max(owned_max, -(-(E * len(planner.shards.per_layer)) // D)))
         geoms.append(LayerGeometry(d_model, d_ff, E, top_k, max_tokens, D,
-                                   min(E, owned_max + max(0, m)), activation, owned_max))
+                                   min(E, owned_max + max(0, m)), activation, owned_max, reshard))
     return geoms
 
 

@@ -140,3 +140,32 @@ def test_cfg4_fine_grained_swiglu_remat():
     replicas = compare(4, 1, 64, 256, 1408, 2, 512, pol, "swiglu", bias=zipf_bias(64, 1.2, 4),
                        oracle=True)
     assert replicas > 0
+
+
+def test_resharding_moves_owned_shards():
+    """reshard_interval = 2 over a 2-layer model whose expert loads differ per layer:
+    heterogeneous_sharding moves ownership (engine.py:470-487); the owned shards move with
+    it (staging + gather), so every later step still equals the single-rank run bit-exactly."""
+    L, E, D, Tr = 2, 8, 4, 256
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2,
+                   reshard_interval=2)
+    bias = zipf_bias(E, 1.5, 9)
+    multi = build_model(D, L, E, 256, 512, 2, Tr, pol, "gelu", bias=bias)
+    single = build_model(1, L, E, 256, 512, 2, Tr * D, F.Policy(F.PolicyKind.EP), "gelu",
+                         bias=bias)
+    before = [np.asarray(multi[li][0].planner.shards.per_layer[li].owners()) for li in range(L)]
+    g = torch.Generator(device="cuda").manual_seed(23)
+    moved = 0
+    for it in range(5):
+        x = torch.randn(D * Tr, 256, device="cuda", generator=g).bfloat16()
+        dy = (torch.randn(D * Tr, 256, device="cuda", generator=g) * 0.05).bfloat16()
+        ym, dxm = run_step(multi, list(x.split(Tr)), list(dy.split(Tr)), False)
+        ys, dxs = run_step(single, [x], [dy], False)
+        torch.cuda.synchronize()
+        moved += len(multi[0][0].planner.last_reshard_moves)
+        for li in range(L):
+            assert torch.equal(torch.cat(ym[li]), ys[li][0]), f"layer {li} y differs (it {it})"
+            assert torch.equal(torch.cat(dxm[li]), dxs[li][0]), f"layer {li} dx differs (it {it})"
+    after = [np.asarray(multi[li][0].planner.shards.per_layer[li].owners()) for li in range(L)]
+    assert moved > 0 and any(not np.array_equal(a, b) for a, b in zip(before, after)), \
+        "the skewed loads should have triggered a re-shard"
