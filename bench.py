@@ -345,6 +345,15 @@ def run_ours(args):
         barrier()
     launches = NAT.launch_count
     ms = start.elapsed_time(end) / args.steps
+    # the GPU-side planning gap (count all-gather done -> tables uploaded, dispatch next),
+    # probed with just two events per step
+    layer.gap_events = []
+    barrier()
+    for _ in range(args.steps):
+        step(x, dy)
+    barrier()
+    plan_gap_ms = sum(a.elapsed_time(b) for a, b in layer.gap_events) / max(1, len(layer.gap_events))
+    layer.gap_events = None
     # a second, instrumented pass of the same K steps: CUDA events around every kernel
     # (phase breakdown, the GEMM roofline) and host timestamps on the planning path
     layer.timers = {}
@@ -445,6 +454,7 @@ def run_ours(args):
     allp = gather(phase_ms) if keys else None
     breakdown = {k: round(float(allp[:, i].max()), 4) for i, k in enumerate(keys)} if keys else {}
     breakdown["host_plan"] = round(float(allr[:, 6].max()), 4)
+    breakdown["planning_gap_gpu"] = round(float(gather([plan_gap_ms])[:, 0].max()), 4)
     breakdown["sum_of_kernels_max_rank"] = round(float(allp.sum(axis=1).max()), 4) if keys else 0.0
     sparse = None
     if world > 1:

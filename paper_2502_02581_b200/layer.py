@@ -677,11 +677,22 @@ class FssdpMoE:
         finally:
             self._cs = None
 
+    # planning-gap probe (bench.py): two CUDA events per step around the host planning
+    # gap, from the end of the count all-gather to the start of the dispatch
+    gap_events = None
+
     def _forward(self, x: torch.Tensor) -> torch.Tensor:
         self.phase_prefetch()
         self.phase_gate(x)
         self.phase_counts()
+        if self.gap_events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         self.phase_plan()
+        if self.gap_events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self.gap_events.append((e0, e1))
         self.phase_dispatch()
         self._mark("dispatch_launched")
         self.phase_spag()  # only fwd1 reads the replicas: the dispatch overlaps the early SpAG
