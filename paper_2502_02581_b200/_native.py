@@ -13,7 +13,11 @@ from pathlib import Path
 
 from .errors import raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "libfssdp.so"
+import os
+
+# FSSDP_LIB: an alternative build of the same library (diagnostics only, e.g. the GEMM
+# role-wait counter variant of build.py --gemm-profile)
+LIB_PATH = Path(os.environ.get("FSSDP_LIB", Path(__file__).resolve().parent / "libfssdp.so"))
 HEADER = Path(__file__).resolve().parent.parent / "include" / "fssdp.h"
 
 i32, i64, u32, f64, vp = C.c_int32, C.c_int64, C.c_uint32, C.c_double, C.c_void_p

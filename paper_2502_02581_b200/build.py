@@ -24,6 +24,9 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "fssdp"
 LIB = PKG / "libfssdp.so"
+# diagnostic variant (--gemm-profile): GEMM role-wait cycle counters, loaded with
+# FSSDP_LIB=<path> by scripts/gemm_profile.py only
+LIB_PROF = ROOT / "build" / "libfssdp_gemm_profile.so"
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -53,10 +56,10 @@ def _deps() -> list[Path]:
     ]
 
 
-def _compile(src: Path, verbose: bool) -> Path:
-    obj = BUILD / (src.name + ".o")
+def _compile(src: Path, verbose: bool, out_dir: Path = BUILD, defines=()) -> Path:
+    obj = out_dir / (src.name + ".o")
     if src.suffix == ".cu":
-        cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *NVCC_FLAGS, *defines, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
     else:
@@ -92,12 +95,30 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_gemm_profile() -> Path:
+    out = ROOT / "build" / "fssdp_prof"
+    out.mkdir(parents=True, exist_ok=True)
+    srcs = _sources()
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
+        objs = list(pool.map(lambda s: _compile(s, False, out, ("-DFSSDP_GEMM_PROFILE",)), srcs))
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB_PROF), *map(str, objs),
+           "-lstdc++"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    return LIB_PROF
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true", help="print ptxas resource usage")
+    ap.add_argument("--gemm-profile", action="store_true",
+                    help="also build the diagnostic GEMM role-wait counter variant")
     args = ap.parse_args()
     print(build(force=args.force, verbose=args.verbose))
+    if args.gemm_profile:
+        print(build_gemm_profile())
 
 
 if __name__ == "__main__":

@@ -33,6 +33,20 @@
 
 namespace fssdp {
 
+// Diagnostic build only (build.py --gemm-profile): per-CTA cycle counters of the roles'
+// waits — producer waiting for a free stage, MMA waiting for data / for the epilogue,
+// epilogue waiting for the accumulator — read back with fssdp_gemm_profile_read.
+#ifdef FSSDP_GEMM_PROFILE
+__device__ unsigned long long g_gemm_prof[1024][8];
+#define PROF_T0(v) const long long v = clock64()
+#define PROF_ADD(slot, v) atomicAdd(&g_gemm_prof[blockIdx.x][slot], (unsigned long long)(clock64() - (v)))
+#define PROF_INC(slot) atomicAdd(&g_gemm_prof[blockIdx.x][slot], 1ull)
+#else
+#define PROF_T0(v)
+#define PROF_ADD(slot, v)
+#define PROF_INC(slot)
+#endif
+
 constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
 // Epilogue warps: 4 (one per TMEM lane quarter), or 8 (two per quarter, column halves)
@@ -234,6 +248,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===================== TMA producer (both CTAs stage their own halves)
+      PROF_T0(tp0);
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
@@ -243,7 +258,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         const int m0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * kBM;
         const int n0 = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * kBNc;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
+          PROF_T0(tw);
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          PROF_ADD(1, tw);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * S::kStageBytes);
@@ -286,10 +303,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           }
         }
       }
+      PROF_ADD(0, tp0);
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ===================== MMA issuer (single thread of the leader CTA)
+      PROF_T0(tm0);
       constexpr uint32_t idesc =
           make_idesc_bf16(CG * kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
       int stage = 0;
@@ -300,11 +319,16 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         const TileCoord tc =
             locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const int kblocks = groups[tc.group].k_blocks;
+        PROF_T0(te);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        PROF_ADD(3, te);
+        PROF_INC(7);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < kblocks; ++kb) {
+          PROF_T0(tf);
           mbar_wait(&full_bar[stage], phase);
+          PROF_ADD(2, tf);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * S::kStageBytes);
           const uint32_t b_base = a_base + S::kABytes;
@@ -343,6 +367,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           acc_phase ^= 1;
         }
       }
+      PROF_ADD(4, tm0);
     }
   } else {
     // ===================== epilogue: TMEM -> registers -> fused op -> smem -> TMA store
@@ -364,6 +389,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t gchunk = 0;  // running chunk counter (selects the staging set)
+    PROF_T0(tep0);
     // aux / output column of f-space column j in the interleaved [a1|a3] layout (SwiGLU)
     auto a13_col = [](int j) { return 256 * (j >> 7) + (j & 127); };
     for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
@@ -393,7 +419,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         fence_proxy_async_smem();
         for (int p = 0; p < kAB - 1 && p < kCW; ++p) aux_load((gchunk + p) % kAB, cbase + p);
       }
+      PROF_T0(ta);
       mbar_wait(&tfull_bar[acc], acc_phase);
+      if (ew == 0 && lane == 0) PROF_ADD(5, ta);
       tc_fence_after();
 #pragma unroll 1
       for (int ci = 0; ci < kCW; ++ci, ++gchunk) {
@@ -540,6 +568,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     }
     if (lane == 0) bulk_wait<0>();  // all stores of this warp complete before exit
     __syncwarp();
+    if (ew == 0 && lane == 0) PROF_ADD(6, tep0);
   }
 
   tc_fence_before();
@@ -676,5 +705,17 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   if (cg == 2) return dispatch_major<256, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
   return dispatch_major<256, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
 }
+
+#ifdef FSSDP_GEMM_PROFILE
+extern "C" __attribute__((visibility("default"))) int fssdp_gemm_profile_read(
+    unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_gemm_prof, sizeof(g_gemm_prof)) != cudaSuccess) return -4;
+  if (reset) {
+    static unsigned long long zeros[1024][8];
+    if (cudaMemcpyToSymbol(g_gemm_prof, zeros, sizeof(zeros)) != cudaSuccess) return -4;
+  }
+  return 0;
+}
+#endif
 
 }  // namespace fssdp
