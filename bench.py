@@ -569,6 +569,9 @@ def select_config(name: str) -> None:
 def main():
     args = parse()
     select_config(args.config)
+    if os.environ.get("FSSDP_POLICY"):  # experiments: "t,m" overrides the config's knobs
+        t, m = (int(v) for v in os.environ["FSSDP_POLICY"].split(","))
+        POLICY.update(overlap_override=t, capacity_override=m)
     if args.tokens is None:
         args.tokens = CFG["tokens_per_gpu"]
     if args.impl == "reference":
