@@ -213,6 +213,47 @@ class OracleWorkload:
         return n
 
 
+def planner_compare(devices: int = 8, reps: int = 20) -> dict:
+    """One layer-iteration of FSSDP decisions (adoption gate, calibration, fallback,
+    build_dispatch; engine.py:491-553) at `devices` GPUs on this config's skewed counts:
+    the Python restatement (oracle/, the reference's own algorithm) vs the native planner."""
+    import numpy as np
+
+    import paper_2502_02581_b200 as F
+    from oracle import planner_oracle as PO
+
+    E, T, k = CFG["num_experts"], CFG["tokens_per_gpu"], CFG["top_k"]
+    nm = 3 if CFG["activation"] == "swiglu" else 2
+    rng = np.random.default_rng(7)
+    p = 1.0 / np.arange(1, E + 1) ** ZIPF_S
+    p = p[rng.permutation(E)] / p.sum()
+    hist = [rng.multinomial(T * k, p, size=devices).astype(np.int64) for _ in range(5)]
+    actual = rng.multinomial(T * k, p, size=devices).astype(np.int64)
+    est = np.mean(np.stack(hist), axis=0)
+    d, f = CFG["d_model"], CFG["d_ff"]
+    knobs = dict(t=POLICY["overlap_override"], m=POLICY["capacity_override"], calibration=True,
+                 rematerialize=False, expert_bytes=2 * nm * d * f, token_bytes=2 * d,
+                 attn_fwd_time=1e-3, ptt=2.0 * nm * d * f / 1381.7e12)
+    topo = PO.Topo(1, devices, NVLINK_PEER_GBS * 1e9, NVLINK_PEER_GBS * 1e9)
+    owner = [e * devices // E for e in range(E)]
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        PO.plan_layer(owner, est, actual, topo, knobs)
+    oracle_ms = (time.perf_counter() - t0) * 1e3 / reps
+    cfg = F.ModelConfig(1, E, knobs["expert_bytes"], 2 * d, 1e-3, knobs["ptt"])
+    pl = F.FssdpPlanner(cfg, F.ClusterTopology.for_nvswitch(devices, NVLINK_PEER_GBS * 1e9),
+                        F.Policy(F.PolicyKind.FSSDP, **POLICY))
+    for h in hist:
+        pl.history[0].append(h)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        pl.plan_layer(0, actual)
+    native_ms = (time.perf_counter() - t0) * 1e3 / reps
+    return {"devices": devices, "oracle_port_python": round(oracle_ms, 3),
+            "native_cpp_via_python": round(native_ms, 4),
+            "note": "planning decisions only; bit-identical outputs (tests/test_planner_native.py)"}
+
+
 def cpu_sample_tokens(at_cfg2: int) -> int:
     """The CPU sample, scaled so a step costs about what `at_cfg2` tokens cost at cfg2."""
     nm = 3 if CFG["activation"] == "swiglu" else 2
@@ -541,7 +582,8 @@ def run_ours(args):
         rate, det = cpu_oracle_rate(sample, 8.0)
         cpu = {"value": rate, "unit": "tokens/s", "cores": det["threads"], "kind": "port",
                "sample": f"{sample}-token batches of {args.config} through oracle/ (numpy fwd+bwd + planner "
-                         f"port), {det['steps']} batches in {det['seconds']:.1f} s"}
+                         f"port), {det['steps']} batches in {det['seconds']:.1f} s",
+               "planner_ms_per_layer_iteration": planner_compare()}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max,
