@@ -390,11 +390,6 @@ int fssdp_push_host(const void* src_dev, void* dst_host, int64_t bytes, uint32_t
                     uint32_t flag_value, void* stream);
 int fssdp_host_wait(const uint32_t* flag_host, uint32_t value, double timeout_s);
 int fssdp_pull_host(void* dst_dev, const void* src_host, int64_t bytes, void* stream);
-/* Plan-boundary copies (counts readback, plan-table upload): cudaMemcpyAsync of `bytes`
- * on `stream` (direction inferred from the pointers), then, if `synchronize`, wait for
- * the stream.  Host buffers should be pinned. */
-int fssdp_copy(void* dst, const void* src, int64_t bytes, void* stream, int32_t synchronize);
-
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -121,7 +121,6 @@ _SIGS = {
     "fssdp_ipc_handle": [vp, P_u8],
     "fssdp_ipc_open": [P_u8, C.POINTER(C.c_void_p)],
     "fssdp_ipc_close": [vp],
-    "fssdp_copy": [vp, vp, i64, vp, i32],
     "fssdp_push_host": [vp, vp, i64, vp, u32, vp],
     "fssdp_host_wait": [vp, u32, f64],
     "fssdp_pull_host": [vp, vp, i64, vp],

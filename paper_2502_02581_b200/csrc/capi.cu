@@ -140,21 +140,6 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
   return fssdp_pull_host(blob_dev, blob, (total + 15) / 16 * 16, stream);
 }
 
-int fssdp_copy(void* dst, const void* src, int64_t bytes, void* stream, int32_t synchronize) {
-  if (bytes < 0 || (bytes > 0 && (dst == nullptr || src == nullptr))) {
-    set_error("copy: bad arguments");
-    return kErrDimension;
-  }
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = bytes ? cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, s)
-                        : cudaSuccess;
-  if (e == cudaSuccess && synchronize) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) {
-    set_error(cudaGetErrorString(e));
-    return kErrCuda;
-  }
-  return kOk;
-}
 
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,

@@ -47,17 +47,6 @@ GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"
                         ("c_off", "<i8")])
 
 
-def gemm_groups_tensor(groups: list[tuple], device) -> tuple[torch.Tensor, int, int]:
-    """Pack [(m_tiles, a_m, a_k, b_n, b_k, k_blocks, c_off), ...] into a device array.
-
-    Returns (tensor, num_groups, total_tiles_per_n_tile)."""
-    arr = np.zeros(len(groups), dtype=GROUP_DTYPE)
-    for i, (m_tiles, a_m, a_k, b_n, b_k, k_blocks, c_off) in enumerate(groups):
-        arr[i] = (m_tiles, 0, a_m, a_k, b_n, b_k, k_blocks, 0, c_off)
-    raw = torch.from_numpy(arr.view(np.uint8).copy())
-    return raw.to(device, non_blocking=False), len(groups), int(arr["m_tiles"].sum())
-
-
 def finalize_groups(groups_cpu: np.ndarray, n_tiles: int) -> int:
     """Fill tile_start in place for a structured group array; return total tiles."""
     tiles = groups_cpu["m_tiles"].astype(np.int64) * n_tiles

@@ -360,28 +360,3 @@ class NativeTables:
 
     def groups(self, name) -> np.ndarray:
         return self.section(name, GROUP_DTYPE, self.gemm[name][0])
-
-
-class PackedTables:
-    """One contiguous byte blob (16-byte aligned sections) for a single H2D copy."""
-
-    def __init__(self, tables: RankTables):
-        parts = [("route_cum", tables.route_cum), ("recv_base", tables.recv_base),
-                 ("zero_rows", tables.zero_rows), ("spag", tables.spag_copies),
-                 ("sprs_jobs", tables.sprs_jobs), ("sprs_srcs", tables.sprs_srcs)]
-        for name in GEMM_NAMES:
-            parts.append((name, tables.groups[name][0]))
-        self.offsets = {}
-        chunks = []
-        off = 0
-        for name, arr in parts:
-            raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
-            self.offsets[name] = off
-            chunks.append(raw)
-            pad = (-len(raw)) % 16
-            if pad:
-                chunks.append(np.zeros(pad, dtype=np.uint8))
-            off += len(raw) + pad
-        self.blob = np.concatenate(chunks) if chunks else np.zeros(0, dtype=np.uint8)
-        if len(self.blob) == 0:
-            self.blob = np.zeros(16, dtype=np.uint8)
