@@ -369,6 +369,16 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,
                int64_t slot_elems, const int32_t* jobs, int32_t n_jobs, const int32_t* srcs,
                void* stream);
+/* K8, pull variant (the standalone SparseReduceScatter, costmodel.py:111-132 schedule): the
+ * holders wrote their partials into THEIR OWN staging slots at the index the owner assigned
+ * (the same srcs table; c_dest maps pointing at the local staging region), and the owner
+ * pulls them over NVLink through a TMA ring, summing in listed order:
+ * grads[dst_slot] = sum over srcs of (rank == this rank ? grads[idx] : peer rank's stage[idx]).
+ * The caller orders it after every holder's partials are complete (device barrier) and
+ * keeps the holders' staging slots intact until it has finished. */
+int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
+                    int64_t stage_off, int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
+                    const int32_t* srcs, void* stream);
 
 /* ================================================================== symmetric heap */
 /* cudaMalloc'd, zero-initialised heap (bytes rounded up to 2 MiB). */

@@ -115,6 +115,7 @@ _SIGS = {
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
     "fssdp_gather_slots": [vp, i32, i64, i64, i64, vp, i32, vp],
     "fssdp_sprs": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
+    "fssdp_sprs_pull": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
     # symmetric heap
     "fssdp_heap_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "fssdp_heap_free": [vp],
@@ -174,7 +175,7 @@ KERNELS_PER_CALL = {
     "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
     "fssdp_route_scan_allgather": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
-    "fssdp_sprs": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
+    "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
     "fssdp_gather_slots": 1,
 }
 launch_count = 0

@@ -1014,6 +1014,100 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// SpRS by pull: each holder's partial sits in ITS OWN staging slot (the index its owner
+// assigned), the owner streams every source of a chunk through a TMA ring — remote partials
+// straight from the holders' HBM over NVLink, its own from local HBM — and sums them in
+// listed (ascending-rank) order into its grads slot.  One pass, no staging round trip on
+// the owner.  Warp 0 (one lane) produces, kPullWarps warps consume: each consumer thread
+// owns 4 float4 of every kPullSub-byte sub-chunk, so a sub-chunk's sum stays in registers
+// while its sources arrive one ring stage each.
+constexpr int kPullSub = 8 * 1024;
+constexpr int kPullRing = 8;   // 64 KB of dynamic smem per CTA: 3 CTAs per SM
+constexpr int kPullWarps = 4;  // 128 consumer threads x 4 float4 = one sub-chunk
+__global__ void __launch_bounds__(32 * (kPullWarps + 1))
+    sprs_pull_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
+                     int64_t stage_off, int64_t slot_elems, const int32_t* __restrict__ jobs,
+                     const int32_t* __restrict__ srcs, int64_t chunk, int n_chunks, int n_units) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kPullRing], empty[kPullRing];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPullRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kPullWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t slot_bytes = slot_elems * 4;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) {
+    if (threadIdx.x != 0) return;
+    uint32_t it = 0;
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      const int job = unit / n_chunks;
+      const int src_begin = jobs[3 * job + 1], src_count = jobs[3 * job + 2];
+      const int64_t begin = static_cast<int64_t>(unit % n_chunks) * chunk;
+      const int64_t bytes = imin64(chunk, slot_bytes - begin);
+      for (int64_t c = 0; c < bytes; c += kPullSub) {
+        const uint32_t n = static_cast<uint32_t>(imin64(kPullSub, bytes - c));
+        for (int q = 0; q < src_count; ++q, ++it) {
+          const int r = srcs[2 * (src_begin + q)];
+          const int64_t idx = srcs[2 * (src_begin + q) + 1];
+          const char* src = reinterpret_cast<const char*>(
+                                peer_bases[r] + (r == rank ? grad_off : stage_off)) +
+                            idx * slot_bytes + begin + c;
+          const uint32_t st = it % kPullRing;
+          if (it >= kPullRing) mbar_wait(&empty[st], ((it / kPullRing) - 1) & 1u);
+          mbar_arrive_expect_tx(&full[st], n);
+          bulk_load_g2s(ring + st * kPullSub, src, n, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  const int t = threadIdx.x - 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t it = 0;
+  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    const int job = unit / n_chunks;
+    const int64_t dst_slot = jobs[3 * job];
+    const int src_count = jobs[3 * job + 2];
+    const int64_t begin = static_cast<int64_t>(unit % n_chunks) * chunk;
+    const int64_t bytes = imin64(chunk, slot_bytes - begin);
+    char* dst = reinterpret_cast<char*>(peer_bases[rank] + grad_off) + dst_slot * slot_bytes + begin;
+    for (int64_t c = 0; c < bytes; c += kPullSub) {
+      const int n16 = static_cast<int>(imin64(kPullSub, bytes - c) / 16);
+      float4 acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < src_count; ++q, ++it) {
+        const uint32_t st = it % kPullRing;
+        mbar_wait(&full[st], (it / kPullRing) & 1u);
+        const float4* buf = reinterpret_cast<const float4*>(ring + st * kPullSub);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = t + u * 32 * kPullWarps;
+          if (i < n16) {
+            const float4 v = buf[i];
+            acc[u].x = __fadd_rn(acc[u].x, v.x);
+            acc[u].y = __fadd_rn(acc[u].y, v.y);
+            acc[u].z = __fadd_rn(acc[u].z, v.z);
+            acc[u].w = __fadd_rn(acc[u].w, v.w);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      float4* out = reinterpret_cast<float4*>(dst + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = t + u * 32 * kPullWarps;
+        if (i < n16) out[i] = acc[u];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ plan-boundary transfers
 // Small host<->device transfers on the planning critical path done by the SMs through
 // mapped pinned memory: a copy-engine transfer would queue behind bulk H2D/D2H traffic of
@@ -1316,6 +1410,40 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
   sprs_kernel<<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, stage_off,
                                                    slot_elems, jobs, srcs, chunk, n_chunks,
                                                    n_units);
+  return launch_status();
+}
+
+int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
+                    int64_t stage_off, int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
+                    const int32_t* srcs, void* stream) {
+  if (slot_elems % 4 != 0) {
+    set_error("sprs_pull: slot_elems must be a multiple of 4");
+    return kErrDimension;
+  }
+  if (n_jobs <= 0) return kOk;
+  constexpr int kSmem = kPullRing * kPullSub;
+  static const bool attr_ok = cudaFuncSetAttribute(sprs_pull_kernel,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kSmem) == cudaSuccess;
+  if (!attr_ok) {
+    set_error("sprs_pull: cannot reserve the TMA ring");
+    return kErrCuda;
+  }
+  // CTA budget (FSSDP_SPRS_PULL_CTAS, default 3 per SM): beside the backward GEMMs the
+  // caller may want fewer
+  static const int budget = [] {
+    const char* v = getenv("FSSDP_SPRS_PULL_CTAS");
+    return v ? atoi(v) : 3 * num_sms();
+  }();
+  int64_t chunk = slot_elems * 4 * n_jobs / (3 * static_cast<int64_t>(num_sms()));
+  chunk = (chunk + kPullSub - 1) / kPullSub * kPullSub;
+  if (chunk < 4 * kPullSub) chunk = 4 * kPullSub;
+  if (chunk > (1 << 20)) chunk = 1 << 20;
+  const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
+  const int n_units = n_chunks * n_jobs;
+  const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
+  sprs_pull_kernel<<<ctas, 32 * (kPullWarps + 1), kSmem, as_stream(stream)>>>(
+      peer_bases, rank, grad_off, stage_off, slot_elems, jobs, srcs, chunk, n_chunks, n_units);
   return launch_status();
 }
 

@@ -10,7 +10,9 @@ CUDA events around the kernel, max over ranks; GB/s = per-GPU inbound bytes / ti
 gradients (S_grad = 2·S) the way the layer does: the shared-prefix wgrad launches push each
 holder's partial into its owner's staging slot through the epilogue's TMA stores (run
 here with K = 0, i.e. the store path alone), then a barrier and the owner's local
-reduction.  Prints one JSON line per case on rank 0.
+reduction.  "sprs_pull" times the pull transport alone: the partials already sit in the
+holders' own staging slots and each owner pulls them over NVLink and sums them in one
+pass (fssdp_sprs_pull).  Prints one JSON line per case on rank 0.
 """
 
 import argparse
@@ -103,7 +105,7 @@ def main():
                 jobs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_jobs"])
                 srcs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_srcs"])
                 res = {}
-                for kind in ("spag", "sprs"):
+                for kind in ("spag", "sprs", "sprs_pull"):
                     times = []
                     for it in range(args.iters + 2):
                         dist.barrier()
@@ -120,6 +122,11 @@ def main():
                             if tab.n_sprs_jobs:
                                 N.call("fssdp_sprs", pb, rank, goff, soff, S // 2, jobs_t,
                                        tab.n_sprs_jobs, srcs_t, sp)
+                        if kind == "sprs_pull" and tab.n_sprs_jobs:
+                            # partials already in the holders' own staging slots (the wgrad
+                            # wrote them locally): the owners' pull + sum alone
+                            N.call("fssdp_sprs_pull", pb, rank, goff, soff, S // 2, jobs_t,
+                                   tab.n_sprs_jobs, srcs_t, sp)
                         e.record()
                         torch.cuda.synchronize()
                         if it >= 2:
@@ -141,6 +148,10 @@ def main():
                         "spag_gbs_inbound_max": max_in / (res["spag"] * 1e-3) / 1e9,
                         "sprs_gbs_bottleneck_fp32": 2 * rep.bottleneck_bytes / (res["sprs"] * 1e-3) / 1e9,
                         "sprs_path": "wgrad epilogue TMA-store push (K=0) + barrier + local reduce",
+                        "sprs_pull_ms": res["sprs_pull"],
+                        "sprs_pull_gbs_bottleneck_fp32":
+                            2 * rep.bottleneck_bytes / (res["sprs_pull"] * 1e-3) / 1e9,
+                        "sprs_pull_gbs_inbound_max_fp32": 2 * max_in / (res["sprs_pull"] * 1e-3) / 1e9,
                         "nvlink_peer_gbs_ref": 770.0,
                     }
                     print("SWEEP " + json.dumps(line), flush=True)

@@ -1,0 +1,126 @@
+"""SparseAllGather / SparseReduceScatter kernels on their own (K3, K8), N logical ranks
+emulated on one GPU (separate symmetric heaps, real cross-heap addressing).
+
+SpAG: every replica slot becomes a bit-exact copy of its owner's shard.  SpRS (push's
+owner-local reduce and the pull kernel): each owned slot becomes the fp32 sum, in listed
+(ascending-rank) order, of the holders' partials — checked BIT-EXACTLY against a numpy
+float32 sequential sum.  Schedules come from the product tables (build_rank_tables) of
+ring and hot-expert placements (sparse sweep shapes) and random ones; slot sizes include
+ragged ones (not a multiple of the kernels' 8 KB sub-chunks).
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_02581_b200 as F
+from paper_2502_02581_b200 import _native as N
+from paper_2502_02581_b200.comm import HeapLayout, emulated_group
+from paper_2502_02581_b200.plan_tables import NativeTables
+
+pytestmark = pytest.mark.gpu
+
+
+def placements(world, E, kind, seed=0):
+    topo = F.ClusterTopology.for_nvswitch(world)
+    base = F.make_even_partition(E, topo)
+    if kind == "ring":
+        extra = [(e, (base.owner(e) + i) % world) for e in range(E) for i in range(1, world)]
+    elif kind == "hot":
+        extra = [(0, d) for d in range(world)]
+    else:
+        rng = np.random.default_rng(seed)
+        extra = [(e, d) for e in range(E) for d in range(world) if rng.random() < 0.4]
+    return base, base.union(extra)
+
+
+def setup(world, E, slot_elems, kind, seed=0):
+    base, post = placements(world, E, kind, seed)
+    owner = np.asarray(base.owners(), dtype=np.int32)
+    route = np.zeros((world, E, world), dtype=np.int64)
+    tabs = [NativeTables(r, owner, post.mask, route, 256, 256) for r in range(world)]
+    slots = max(t.n_slots for t in tabs)
+    n_stage = max(1, max(t.n_stage for t in tabs))
+    layout = HeapLayout()
+    layout.add("params", slots * slot_elems * 2)
+    layout.add("grads", slots * slot_elems * 4)
+    layout.add("stage", n_stage * slot_elems * 4)
+    groups = emulated_group(layout, world)
+    return base, post, tabs, layout, groups, slots, n_stage
+
+
+@pytest.mark.parametrize("world,E,kind,slot_elems", [
+    (2, 2, "ring", 1 << 20), (4, 4, "ring", 3 * 4096 + 1000), (4, 8, "hot", 1 << 18),
+    (8, 8, "ring", 12344 * 4), (8, 16, "random", 77776 * 4)])
+def test_spag_copies_owner_shards(world, E, kind, slot_elems):
+    base, post, tabs, layout, groups, slots, _ = setup(world, E, slot_elems, kind)
+    poff = layout.offset("params")
+    g = torch.Generator(device="cuda").manual_seed(1)
+    params = [grp.local.tensor(poff, (slots, slot_elems), torch.bfloat16) for grp in groups]
+    for p in params:
+        p.copy_(torch.randn(slots, slot_elems, generator=g, device="cuda"))
+    for r, t in enumerate(tabs):
+        blob = torch.from_numpy(t.blob[:t.nbytes].copy()).cuda()
+        if t.n_spag:
+            N.call("fssdp_spag", C.c_void_p(groups[r].peer_bases.data_ptr()), r, poff,
+                   slot_elems * 2, C.c_void_p(blob.data_ptr() + t.offsets["spag"]), t.n_spag,
+                   C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    for r, t in enumerate(tabs):
+        for e, s in t.slots.items():
+            o = base.owner(e)
+            assert torch.equal(params[r][s], params[o][tabs[o].slots[e]]), (r, e)
+
+
+@pytest.mark.parametrize("pull", [False, True])
+@pytest.mark.parametrize("world,E,kind,slot_elems", [
+    (2, 2, "ring", 1 << 20), (4, 4, "ring", 3 * 2048 + 500), (4, 8, "hot", 1 << 18),
+    (8, 8, "ring", 12345 * 4), (8, 16, "random", 77777 * 4)])
+def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull):
+    """Partials sit where the transport puts them — push: the owner's staging slot; pull:
+    the holder's own staging slot at the same index — and the owner's grads slot ends up
+    holding the ascending-rank fp32 sum (bit-exact)."""
+    base, post, tabs, layout, groups, slots, n_stage = setup(world, E, slot_elems, kind, seed=3)
+    goff, soff = layout.offset("grads"), layout.offset("stage")
+    g = torch.Generator(device="cuda").manual_seed(2)
+    grads = [grp.local.tensor(goff, (slots, slot_elems), torch.float32) for grp in groups]
+    stage = [grp.local.tensor(soff, (n_stage, slot_elems), torch.float32) for grp in groups]
+    partial = {}  # (expert, holder) -> its partial
+    for r, t in enumerate(tabs):
+        grads[r].copy_(torch.randn(slots, slot_elems, generator=g, device="cuda"))
+        for e, s in t.slots.items():
+            partial[(e, r)] = grads[r][s].clone()
+    # place the replicas' partials the way the wgrad epilogue would (c_dest)
+    for r, t in enumerate(tabs):
+        for dst_slot, b, n in t.sprs_jobs:
+            for h, idx in t.sprs_srcs[b:b + n]:
+                if h != r:
+                    e = [x for x, s in t.slots.items() if s == dst_slot][0]
+                    (stage[h] if pull else stage[r])[idx].copy_(partial[(e, int(h))])
+    torch.cuda.synchronize()
+    for r, t in enumerate(tabs):
+        blob = torch.from_numpy(t.blob[:t.nbytes].copy()).cuda()
+        N.call("fssdp_sprs_pull" if pull else "fssdp_sprs",
+               C.c_void_p(groups[r].peer_bases.data_ptr()), r, goff, soff, slot_elems,
+               C.c_void_p(blob.data_ptr() + t.offsets["sprs_jobs"]), t.n_sprs_jobs,
+               C.c_void_p(blob.data_ptr() + t.offsets["sprs_srcs"]),
+               C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    reduced = 0
+    for r, t in enumerate(tabs):
+        for e, s in t.slots.items():
+            if base.owner(e) != r:
+                continue
+            holders = [d for d in range(world) if post.mask[e, d]]
+            want = np.zeros(slot_elems, dtype=np.float32)
+            for h in holders:
+                want = want + partial[(e, h)].cpu().numpy()   # float32, ascending rank
+            got = grads[r][s].cpu().numpy()
+            if len(holders) > 1:
+                reduced += 1
+                assert np.array_equal(got, want), (r, e)
+            else:
+                assert np.array_equal(got, partial[(e, r)].cpu().numpy())
+    assert reduced > 0
