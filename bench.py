@@ -399,6 +399,8 @@ def run_ours(args):
     # (phase breakdown, the GEMM roofline) and host timestamps on the planning path
     layer.timers = {}
     barrier()
+    ref = NAT.NativeEvent()  # timeline origin for the per-kernel launch-timing windows
+    ref.record(torch.cuda.current_stream(dev))
     for _ in range(args.steps):
         step(x, dy)
     barrier()
@@ -413,7 +415,7 @@ def run_ours(args):
                 continue
             per = len(ev) // args.steps
             last += [(key, s_, e_) for s_, e_ in ev[len(ev) - per:]]
-        s0 = min(last, key=lambda t: start.elapsed_time(t[1]))[1]
+        s0 = min(last, key=lambda t: ref.elapsed_time(t[1]))[1]
         rows = sorted((round(s0.elapsed_time(s_), 4), round(s0.elapsed_time(e_), 4), key)
                       for key, s_, e_ in last)
         Path(f"{os.environ['FSSDP_TIMELINE']}_n{world}_r{rank}.json").write_text(json.dumps(rows))

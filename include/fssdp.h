@@ -189,7 +189,9 @@ int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, con
 #define FSSDP_TAB_SEG_START 13
 #define FSSDP_TAB_SEG_ROWS 14
 #define FSSDP_TAB_SEG_PADDED 15
-#define FSSDP_TAB_NSECTIONS 16
+#define FSSDP_TAB_SPRS_PULL 16  /* int32 [<=E*D][2] {rank, grads slot on that rank}, parallel
+                                   to SPRS_SRCS (fssdp_sprs_pull) */
+#define FSSDP_TAB_NSECTIONS 17
 int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offsets_out,
                         int64_t* total_bytes_out);
 int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_experts,
@@ -369,16 +371,16 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,
                int64_t slot_elems, const int32_t* jobs, int32_t n_jobs, const int32_t* srcs,
                void* stream);
-/* K8, pull variant (the standalone SparseReduceScatter, costmodel.py:111-132 schedule): the
- * holders wrote their partials into THEIR OWN staging slots at the index the owner assigned
- * (the same srcs table; c_dest maps pointing at the local staging region), and the owner
- * pulls them over NVLink through a TMA ring, summing in listed order:
- * grads[dst_slot] = sum over srcs of (rank == this rank ? grads[idx] : peer rank's stage[idx]).
- * The caller orders it after every holder's partials are complete (device barrier) and
- * keeps the holders' staging slots intact until it has finished. */
+/* K8, pull variant — the standalone SparseReduceScatter (sprs_traffic's schedule,
+ * costmodel.py:111-132): every holder's partial stays in its own grads slot and the owner
+ * pulls them over NVLink through a TMA ring, summing in listed (ascending-rank) order:
+ * grads[dst_slot] = sum over pull_srcs {r, slot} of rank r's grads[slot] (the
+ * FSSDP_TAB_SPRS_PULL section; the owner's own entry is local).  The caller orders it after
+ * every holder's partials are complete (device barrier) and keeps the holders' replica
+ * grads intact until it has finished. */
 int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
-                    int64_t stage_off, int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
-                    const int32_t* srcs, void* stream);
+                    int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
+                    const int32_t* pull_srcs, void* stream);
 
 /* ================================================================== symmetric heap */
 /* cudaMalloc'd, zero-initialised heap (bytes rounded up to 2 MiB). */
@@ -390,6 +392,20 @@ int fssdp_ipc_open(const uint8_t* handle /* 64 bytes */, void** ptr_out);
 int fssdp_ipc_close(void* ptr);
 /* Number of SMs of the current device. */
 int fssdp_num_sms(void);
+
+/* Launch timing (measurement only).  fssdp_timing_arm(start, end) arms two CUDA events
+ * (cudaEvent_t, timing enabled, e.g. from fssdp_event_create); the next device entry point
+ * called on this host thread records `start` right before its first kernel launch — after
+ * its host-side setup — and `end` right after its last, on the launching stream.
+ * fssdp_timing_done() disarms and returns 1 if both were recorded (0: no kernel ran).
+ * Unlike events recorded by the caller around the call, the window holds no host time
+ * when the GPU is waiting for the launch. */
+int fssdp_event_create(void** event_out);
+int fssdp_event_destroy(void* event);
+int fssdp_event_record(void* event, void* stream);
+int fssdp_event_elapsed(void* start, void* end, float* ms_out);
+int fssdp_timing_arm(void* start, void* end);
+int fssdp_timing_done(void);
 /* Plan-boundary transfers without the copy engines (which may be busy with the caller's
  * bulk input/output copies): fssdp_push_host copies `bytes` (multiple of 16, <= 16 MiB) of
  * device memory into pinned host memory with the SMs, then stores flag_value into

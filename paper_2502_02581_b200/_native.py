@@ -115,7 +115,14 @@ _SIGS = {
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
     "fssdp_gather_slots": [vp, i32, i64, i64, i64, vp, i32, vp],
     "fssdp_sprs": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
-    "fssdp_sprs_pull": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
+    "fssdp_sprs_pull": [vp, i32, i64, i64, vp, i32, vp, vp],
+    # launch timing (measurement)
+    "fssdp_event_create": [C.POINTER(C.c_void_p)],
+    "fssdp_event_destroy": [vp],
+    "fssdp_event_record": [vp, vp],
+    "fssdp_event_elapsed": [vp, vp, C.POINTER(C.c_float)],
+    "fssdp_timing_arm": [vp, vp],
+    "fssdp_timing_done": [],
     # symmetric heap
     "fssdp_heap_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "fssdp_heap_free": [vp],
@@ -185,3 +192,41 @@ def call(name: str, *args) -> None:
     global launch_count
     check(getattr(LIB, name)(*args), name)
     launch_count += KERNELS_PER_CALL.get(name, 0)
+
+
+class NativeEvent:
+    """A CUDA event owned by libfssdp (timing enabled), with torch.cuda.Event's
+    elapsed_time() so phase timers can mix with the torch-side code that reads them."""
+
+    __slots__ = ("handle",)
+
+    def __init__(self) -> None:
+        h = C.c_void_p()
+        check(LIB.fssdp_event_create(C.byref(h)), "event_create")
+        self.handle = h
+
+    def record(self, stream) -> None:
+        check(LIB_RAW.fssdp_event_record(self.handle, C.c_void_p(stream.cuda_stream)),
+              "event_record")
+
+    def elapsed_time(self, end: "NativeEvent") -> float:
+        ms = C.c_float()
+        check(LIB_RAW.fssdp_event_elapsed(self.handle, end.handle, C.byref(ms)), "event_elapsed")
+        return float(ms.value)
+
+    def __del__(self) -> None:
+        if LIB_RAW is not None and self.handle:
+            LIB_RAW.fssdp_event_destroy(self.handle)
+
+
+def timed_launch(timers: dict, key: str, fn) -> None:
+    """Run fn (one device entry point) inside an armed launch-timing window
+    (fssdp_timing_arm): timers[key] gets the (start, end) NativeEvent pair recorded right
+    around its kernel launches, or nothing if it launched none."""
+    s, e = NativeEvent(), NativeEvent()
+    LIB_RAW.fssdp_timing_arm(s.handle, e.handle)
+    try:
+        fn()
+    finally:
+        if LIB_RAW.fssdp_timing_done():
+            timers.setdefault(key, []).append((s, e))

@@ -16,6 +16,11 @@ static thread_local std::string g_last_error;
 
 void set_error(const char* msg) { g_last_error = msg ? msg : ""; }
 
+LaunchTiming& launch_timing() {
+  static thread_local LaunchTiming t;
+  return t;
+}
+
 int num_sms() {
   static int cached = -1;
   if (cached < 0) {
@@ -95,6 +100,52 @@ const char* fssdp_version(void) { return "fssdp-b200 0.1.0 (sm_100a)"; }
 const char* fssdp_last_error(void) { return g_last_error.c_str(); }
 
 int fssdp_num_sms(void) { return num_sms(); }
+
+int fssdp_event_create(void** event_out) {
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    set_error("event_create: cudaEventCreate failed");
+    return kErrCuda;
+  }
+  *event_out = e;
+  return kOk;
+}
+
+int fssdp_event_destroy(void* event) {
+  return cudaEventDestroy(static_cast<cudaEvent_t>(event)) == cudaSuccess ? kOk : kErrCuda;
+}
+
+int fssdp_event_record(void* event, void* stream) {
+  return cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? kOk
+             : kErrCuda;
+}
+
+int fssdp_event_elapsed(void* start, void* end, float* ms_out) {
+  if (cudaEventElapsedTime(ms_out, static_cast<cudaEvent_t>(start),
+                           static_cast<cudaEvent_t>(end)) != cudaSuccess) {
+    set_error("event_elapsed: events not both completed");
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+int fssdp_timing_arm(void* start, void* end) {
+  LaunchTiming& t = launch_timing();
+  t.start = static_cast<cudaEvent_t>(start);
+  t.end = static_cast<cudaEvent_t>(end);
+  t.state = start && end ? 1 : 0;
+  return kOk;
+}
+
+int fssdp_timing_done(void) {
+  LaunchTiming& t = launch_timing();
+  timing_end();  // an entry point that returned between its launches
+  const int fired = t.state == 3;
+  t.state = 0;
+  return fired;
+}
 
 int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
                             const int32_t* counts, const fssdp_topology* topo,

@@ -45,6 +45,31 @@ struct GemmLaunch {
 
 int num_sms();
 void set_error(const char* msg);
+
+// Launch timing windows (fssdp_timing_arm): the events a caller armed are recorded right
+// around the next entry point's kernel launches — after its host-side setup — so the
+// window holds no host time even when the GPU is waiting for the launch.
+struct LaunchTiming {
+  cudaEvent_t start = nullptr, end = nullptr;
+  cudaStream_t stream = nullptr;
+  int state = 0;  // 0 idle, 1 armed, 2 start recorded, 3 both recorded
+};
+LaunchTiming& launch_timing();  // per host thread
+inline void timing_begin(cudaStream_t s) {
+  LaunchTiming& t = launch_timing();
+  if (t.state == 1) {
+    cudaEventRecord(t.start, s);
+    t.stream = s;
+    t.state = 2;
+  }
+}
+inline void timing_end() {
+  LaunchTiming& t = launch_timing();
+  if (t.state == 2) {
+    cudaEventRecord(t.end, t.stream);
+    t.state = 3;
+  }
+}
 constexpr int kDtBF16 = 0;
 constexpr int kDtF32 = 1;
 int epilogue_tmap(int epi, const void* base, int64_t ldc, int64_t rows, CUtensorMap* map);

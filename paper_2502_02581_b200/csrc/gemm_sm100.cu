@@ -613,7 +613,10 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, args) != cudaSuccess) return kErrCuda;
+  timing_begin(stream);
+  const cudaError_t launched = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, args);
+  timing_end();
+  if (launched != cudaSuccess) return kErrCuda;
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 

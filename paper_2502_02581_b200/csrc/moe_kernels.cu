@@ -1014,19 +1014,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// SpRS by pull: each holder's partial sits in ITS OWN staging slot (the index its owner
-// assigned), the owner streams every source of a chunk through a TMA ring — remote partials
-// straight from the holders' HBM over NVLink, its own from local HBM — and sums them in
-// listed (ascending-rank) order into its grads slot.  One pass, no staging round trip on
-// the owner.  Warp 0 (one lane) produces, kPullWarps warps consume: each consumer thread
-// owns 4 float4 of every kPullSub-byte sub-chunk, so a sub-chunk's sum stays in registers
-// while its sources arrive one ring stage each.
+// SpRS by pull (the standalone SparseReduceScatter): each holder's partial stays in its
+// own grads slot; the owner streams every source of a chunk through a TMA ring — remote
+// partials straight from the holders' HBM over NVLink, its own from local HBM — and sums
+// them in listed (ascending-rank) order into its grads slot.  One pass, no staging round
+// trip.  Warp 0 (one lane) produces, kPullWarps warps consume: each consumer thread owns 4
+// float4 of every kPullSub-byte sub-chunk, so a sub-chunk's sum stays in registers while
+// its sources arrive one ring stage each.
 constexpr int kPullSub = 8 * 1024;
 constexpr int kPullRing = 8;   // 64 KB of dynamic smem per CTA: 3 CTAs per SM
 constexpr int kPullWarps = 4;  // 128 consumer threads x 4 float4 = one sub-chunk
 __global__ void __launch_bounds__(32 * (kPullWarps + 1))
     sprs_pull_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
-                     int64_t stage_off, int64_t slot_elems, const int32_t* __restrict__ jobs,
+                     int64_t slot_elems, const int32_t* __restrict__ jobs,
                      const int32_t* __restrict__ srcs, int64_t chunk, int n_chunks, int n_units) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kPullRing], empty[kPullRing];
@@ -1053,8 +1053,7 @@ __global__ void __launch_bounds__(32 * (kPullWarps + 1))
         for (int q = 0; q < src_count; ++q, ++it) {
           const int r = srcs[2 * (src_begin + q)];
           const int64_t idx = srcs[2 * (src_begin + q) + 1];
-          const char* src = reinterpret_cast<const char*>(
-                                peer_bases[r] + (r == rank ? grad_off : stage_off)) +
+          const char* src = reinterpret_cast<const char*>(peer_bases[r] + grad_off) +
                             idx * slot_bytes + begin + c;
           const uint32_t st = it % kPullRing;
           if (it >= kPullRing) mbar_wait(&empty[st], ((it / kPullRing) - 1) & 1u);
@@ -1132,13 +1131,19 @@ __global__ void __launch_bounds__(256)
 // ------------------------------------------------------------------ launchers
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-static int launch_status() {
+static int launch_check() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));
     return kErrCuda;
   }
   return kOk;
+}
+
+// end of an entry point's launches: closes an armed timing window (fssdp_timing_arm)
+static int launch_status() {
+  timing_end();
+  return launch_check();
 }
 
 // K-templated launch for the token gathers (K = top-k <= kGateMaxK = 8)
@@ -1181,6 +1186,7 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
   if (E % 8 == 0 && d % 64 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
     auto mma_launch = [&](auto kern) {
+      timing_begin(as_stream(stream));
       kern<<<tiles, 128, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(x), wg, bias,
                                                   T, d, E, k, logits, topk_idx, topk_w, slot_rank,
                                                   tile_counts);
@@ -1202,6 +1208,7 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(max_smem)) != cudaSuccess)
       return launch_status();
+    timing_begin(as_stream(stream));
     kern<<<tiles, kGateThreads, smem, as_stream(stream)>>>(
         static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k, logits, topk_idx, topk_w,
         slot_rank, tile_counts);
@@ -1225,6 +1232,7 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
   }
   if (T == 0) return kOk;
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
+  timing_begin(as_stream(stream));
   topk_from_logits_kernel<<<tiles, kGateThreads, 0, as_stream(stream)>>>(
       logits, T, E, k, topk_idx, topk_w, slot_rank, tile_counts);
   return launch_status();
@@ -1238,6 +1246,7 @@ int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int3
     set_error("route_scan: bad world/rank/E");
     return kErrDimension;
   }
+  timing_begin(as_stream(stream));
   route_scan_kernel<<<1, kScanThreads, 0, as_stream(stream)>>>(tile_counts, n_tiles, E, tile_prefix,
                                                        peer_bases, table_off, flags_off, rank,
                                                        world, bar_slot, epoch);
@@ -1250,6 +1259,7 @@ int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, i
     set_error("barrier: bad world/rank");
     return kErrDimension;
   }
+  timing_begin(as_stream(stream));
   barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(peer_bases, flags_off, rank, world, bar_slot,
                                                    epoch);
   return launch_status();
@@ -1267,6 +1277,7 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
     return kErrDimension;
   }
   const int grid = grid_for_warps((T * k + kBatch - 1) / kBatch);  // one warp per batch
+  timing_begin(as_stream(stream));
   dispatch_kernel<<<grid, 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(x), topk_idx, slot_rank, tile_prefix, T, d_model, E, k,
       world, route_cum, recv_base, slot_dest, slot_pos, peer_bases, recv_off, zero_rows, n_zero,
@@ -1283,6 +1294,7 @@ int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float
   }
   if (T == 0) return kOk;
   const int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
+  timing_begin(as_stream(stream));
   FSSDP_DISPATCH_K(k, combine_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_w, T,
                    d_model, peer_bases, y_off, static_cast<__nv_bfloat16*>(y_out));
   return launch_status();
@@ -1298,6 +1310,7 @@ int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t*
     set_error("dispatch_grad: bad shape");
     return kErrDimension;
   }
+  timing_begin(as_stream(stream));
   dispatch_grad_kernel<<<grid_for_warps((T * k + kBatch - 1) / kBatch), 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(dy), slot_dest, slot_pos, topk_w, T, d_model, k,
       peer_bases, y_off, dy_recv_off, slot_grad, zero_rows, n_zero, flags_off, rank, world,
@@ -1315,6 +1328,7 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
   }
   if (T == 0) return kOk;
   const int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
+  timing_begin(as_stream(stream));
   FSSDP_DISPATCH_K(k, combine_dx_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_idx,
                    topk_w, slot_grad, wg, T, d_model, peer_bases, dxe_off, dlogit_out,
                    static_cast<__nv_bfloat16*>(dx_out));
@@ -1343,13 +1357,15 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
       configured = smem;
     }
     dim3 grid(col_blocks, n_tiles);
+    timing_begin(as_stream(stream));
     gate_wgrad_partial_kernel<<<grid, kWgThreads, smem, as_stream(stream)>>>(
         static_cast<const __nv_bfloat16*>(x), topk_idx, dlogit, T, d_model, E, k, tok_per_cta,
         workspace);
-    int rc = launch_status();
+    int rc = launch_check();
     if (rc != kOk) return rc;
   }
   const int64_t n_out = static_cast<int64_t>(E) * d_model;
+  timing_begin(as_stream(stream));
   gate_wgrad_reduce_kernel<<<static_cast<unsigned>((n_out + 31) / 32), 256, 0, as_stream(stream)>>>(
       workspace, n_tiles, d_model, E, dwg_out);
   return launch_status();
@@ -1372,12 +1388,14 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
     if (chunk < 4 * kTmaSub) chunk = 4 * kTmaSub;
     if (chunk > (1 << 20)) chunk = 1 << 20;
     dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
+    timing_begin(as_stream(stream));
     spag_tma_kernel<<<grid, 32, 0, as_stream(stream)>>>(peer_bases, rank, src_off, dst_off,
                                                         slot_bytes, copies, chunk);
     return launch_status();
   }
   const int64_t chunk = coll_chunk_bytes(slot_bytes * n_copies, num_sms());
   dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
+  timing_begin(as_stream(stream));
   spag_kernel<<<grid, 256, 0, as_stream(stream)>>>(peer_bases, rank, src_off, slot_bytes, copies,
                                                    chunk);
   return launch_status();
@@ -1407,6 +1425,7 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
   const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
   const int n_units = n_chunks * n_jobs;
   const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
+  timing_begin(as_stream(stream));
   sprs_kernel<<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, stage_off,
                                                    slot_elems, jobs, srcs, chunk, n_chunks,
                                                    n_units);
@@ -1414,8 +1433,8 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
 }
 
 int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
-                    int64_t stage_off, int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
-                    const int32_t* srcs, void* stream) {
+                    int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
+                    const int32_t* pull_srcs, void* stream) {
   if (slot_elems % 4 != 0) {
     set_error("sprs_pull: slot_elems must be a multiple of 4");
     return kErrDimension;
@@ -1442,8 +1461,9 @@ int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
   const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
   const int n_units = n_chunks * n_jobs;
   const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
+  timing_begin(as_stream(stream));
   sprs_pull_kernel<<<ctas, 32 * (kPullWarps + 1), kSmem, as_stream(stream)>>>(
-      peer_bases, rank, grad_off, stage_off, slot_elems, jobs, srcs, chunk, n_chunks, n_units);
+      peer_bases, rank, grad_off, slot_elems, jobs, pull_srcs, chunk, n_chunks, n_units);
   return launch_status();
 }
 
@@ -1453,6 +1473,7 @@ int fssdp_push_host(const void* src_dev, void* dst_host, int64_t bytes, uint32_t
     set_error("push_host: bytes must be a multiple of 16 and at most 16 MiB");
     return kErrDimension;
   }
+  timing_begin(as_stream(stream));
   push_host_kernel<<<1, 256, 0, as_stream(stream)>>>(static_cast<const int4*>(src_dev),
                                                     static_cast<int4*>(dst_host),
                                                     static_cast<int>(bytes / 16), flag_host,
@@ -1468,6 +1489,7 @@ int fssdp_pull_host(void* dst_dev, const void* src_host, int64_t bytes, void* st
   if (bytes == 0) return kOk;
   const int n16 = static_cast<int>(bytes / 16);
   const int grid = (n16 + 255) / 256 < 16 ? (n16 + 255) / 256 : 16;
+  timing_begin(as_stream(stream));
   pull_host_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int4*>(src_host),
                                                        static_cast<int4*>(dst_dev), n16);
   return launch_status();

@@ -1080,7 +1080,7 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
   const int64_t sizes[FSSDP_TAB_NSECTIONS] = {
       E * (D + 1) * 4, E * D * 4, E * 2 * 4, E * 3 * 4, E * 3 * 4, E * D * 2 * 4,
       G, G, G, G, G, G,
-      E * 4, E * 4, E * 4, E * 4};
+      E * 4, E * 4, E * 4, E * 4, E * D * 2 * 4};
   int64_t off = 0;
   for (int i = 0; i < FSSDP_TAB_NSECTIONS; ++i) {
     offsets_out[i] = off;
@@ -1193,6 +1193,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   }
   int32_t* jobs = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_JOBS]);
   int32_t* srcs = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_SRCS]);
+  int32_t* pull = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPRS_PULL]);
   int n_jobs = 0, n_srcs = 0;
   for (int s = 0; s < n_slots; ++s) {
     const int e = slot_expert[rank][s];
@@ -1208,6 +1209,8 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       if (holds(e, dd)) {  // {rank, own grads slot | staging slot}
         srcs[2 * n_srcs] = dd;
         srcs[2 * n_srcs + 1] = dd == rank ? s : stage_idx[static_cast<size_t>(e) * D + dd];
+        pull[2 * n_srcs] = dd;  // the standalone pull transport: the holder's grads slot
+        pull[2 * n_srcs + 1] = slot_of[dd][e];
         ++n_srcs;
       }
   }

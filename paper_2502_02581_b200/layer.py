@@ -19,7 +19,6 @@ on one GPU (PeerGroup mode "emulated") — the multi-rank parity tests do that.
 from __future__ import annotations
 
 import contextlib
-import os
 import ctypes as C
 import time
 from dataclasses import dataclass
@@ -164,17 +163,13 @@ class FssdpMoE:
         self.counts_flag_ptr = self.counts_host_raw.data_ptr() + self.counts_nbytes
         self.counts_dev_ptr = self.counts_table.data_ptr()
         self._counts_epoch = 0
-        # wgrad destinations for replica partials, as the epilogue tensor maps of wgrad1
-        # (ldc d) and wgrad2 (ldc f); built once.  SpRS by push: every owner's staging region
-        # (the partial crosses NVLink inside the GEMM).  By pull: this rank's own staging
-        # region for every owner (the owner fetches it, fssdp_sprs_pull)
+        # wgrad destinations for replica partials: every rank's staging region, as the
+        # epilogue tensor maps of wgrad1 (ldc d) and wgrad2 (ldc f); built once
         stage_elems = max(1, geom.stage_slots) * geom.slot_grad_elems
-        self.sprs_pull = self.SPRS_PULL
-        dest_bases = ([group.bases[self.rank]] * self.world if self.sprs_pull else group.bases)
         self.dest_maps = {}
         for name, ldc in (("wgrad1", d), ("wgrad2", f)):
             blob = b"".join(ops.epilogue_tmap(ops.EPI_F32, base + self.off["stage"], ldc,
-                                              stage_elems // ldc) for base in dest_bases)
+                                              stage_elems // ldc) for base in group.bases)
             self.dest_maps[name] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.dev)
         # 2-D TMA views of the parameter region (nm = matrices per slot, n1 = (nm-1) f)
         nm, n1 = geom.n_mats, geom.n1
@@ -552,24 +547,19 @@ class FssdpMoE:
             self.timers.setdefault("marks", []).append((name, time.perf_counter()))
 
     def _timed(self, key, fn):
+        """fn (one device entry point), inside a native launch-timing window when profiling:
+        the events sit right around its kernels, so host time spent issuing the launch
+        never counts as kernel time (torch events around the call would hold it whenever
+        the GPU is waiting for this launch)."""
         if self.timers is None:
             fn()
-            return
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
-        s.record()
-        fn()
-        e.record()
-        self.timers.setdefault(key, []).append((s, e))
+        else:
+            N.timed_launch(self.timers, key, fn)
 
     # tile order per GEMM: N-fastest where the A operand (activations) is the big,
     # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
     N_FASTEST = {"fwd2": True, "dgrad1": True}
     CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
-    # SpRS transport: push (replica partials stored into the owners' staging by the wgrad
-    # epilogue, then an owner-local sum) or pull (partials stored locally, owners fetch and
-    # sum them in one pass, fssdp_sprs_pull).  FSSDP_SPRS=push|pull
-    SPRS_PULL = os.environ.get("FSSDP_SPRS", "push") == "pull"
 
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
@@ -674,8 +664,7 @@ class FssdpMoE:
         if n == 0:
             return
         self._timed("sprs", lambda: N.call(
-            "fssdp_sprs_pull" if self.sprs_pull else "fssdp_sprs", self._pb(), self.rank,
-            self.off["grads"], self.off["stage"],
+            "fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.off["stage"],
             self.g.slot_grad_elems, self._tab("sprs_jobs"), n, self._tab("sprs_srcs"),
             self._stream()))
 

@@ -59,6 +59,7 @@ class RankTables:
     spag_copies: np.ndarray      # [n, 3] int32 {src_rank, src_slot, dst_slot}
     sprs_jobs: np.ndarray        # [n, 3] int32 {dst_slot, src_begin, src_count}
     sprs_srcs: np.ndarray        # [m, 2] int32 {rank, own slot | staging slot}, ascending rank
+    sprs_pull: np.ndarray        # [m, 2] int32 {rank, grads slot on that rank} (pull transport)
     groups: dict                 # name -> (GROUP_DTYPE array, n_tiles, total_tiles)
     wgrad_split: tuple = (0, 0, 0)  # (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles)
     n_stage: int = 0             # staging slots this rank receives replica partials in
@@ -198,8 +199,9 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
                     j += 1
         if o == rank:
             n_stage = j
-    # owner side: grads[s] = sum over holders ascending of (own slot | staging slot)
-    jobs, srcs = [], []
+    # owner side: grads[s] = sum over holders ascending of (own slot | staging slot); the
+    # pull transport (fssdp_sprs_pull) reads each holder's own grads slot instead
+    jobs, srcs, pull = [], [], []
     for e, s in sorted(slots.items(), key=lambda kv: kv[1]):
         if int(base_owner[e]) != rank:
             continue
@@ -208,8 +210,10 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
             continue
         jobs.append((s, len(srcs), len(holders)))
         srcs.extend((h, s if h == rank else stage[(e, h)]) for h in holders)
+        pull.extend((h, maps[h][e]) for h in holders)
     sprs_jobs = np.array(jobs, dtype=np.int32).reshape(-1, 3)
     sprs_srcs = np.array(srcs, dtype=np.int32).reshape(-1, 2)
+    sprs_pull = np.array(pull, dtype=np.int32).reshape(-1, 2)
 
     order = list(range(len(slots)))  # segments are in slot order
     by_slot = {s: e for e, s in slots.items()}
@@ -221,12 +225,13 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
     return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
                       seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),
                       route_cum=route_cum, recv_base=recv_base, zero_rows=zero_rows,
-                      spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs, groups=groups,
+                      spag_copies=spag, sprs_jobs=sprs_jobs, sprs_srcs=sprs_srcs,
+                      sprs_pull=sprs_pull, groups=groups,
                       wgrad_split=wgrad_split, n_stage=n_stage)
 
 
 SECTION_NAMES = ("route_cum", "recv_base", "zero_rows", "spag", "sprs_jobs", "sprs_srcs",
-                 *GEMM_NAMES, "slot_expert", "seg_start", "seg_rows", "seg_padded")
+                 *GEMM_NAMES, "slot_expert", "seg_start", "seg_rows", "seg_padded", "sprs_pull")
 
 
 _LAYOUTS: dict = {}
@@ -349,6 +354,10 @@ class NativeTables:
     @property
     def sprs_srcs(self):
         return self.section("sprs_srcs", np.int32, 2 * self.n_sprs_srcs).reshape(-1, 2)
+
+    @property
+    def sprs_pull(self):
+        return self.section("sprs_pull", np.int32, 2 * self.n_sprs_srcs).reshape(-1, 2)
 
     @property
     def route_cum(self):

@@ -11,7 +11,7 @@ gradients (S_grad = 2·S) the way the layer does: the shared-prefix wgrad launch
 holder's partial into its owner's staging slot through the epilogue's TMA stores (run
 here with K = 0, i.e. the store path alone), then a barrier and the owner's local
 reduction.  "sprs_pull" times the pull transport alone: the partials already sit in the
-holders' own staging slots and each owner pulls them over NVLink and sums them in one
+holders' own grads slots and each owner pulls them over NVLink and sums them in one
 pass (fssdp_sprs_pull).  Prints one JSON line per case on rank 0.
 """
 
@@ -104,6 +104,7 @@ def main():
                 spag_t = C.c_void_p(blob.data_ptr() + tab.offsets["spag"])
                 jobs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_jobs"])
                 srcs_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_srcs"])
+                pull_t = C.c_void_p(blob.data_ptr() + tab.offsets["sprs_pull"])
                 res = {}
                 for kind in ("spag", "sprs", "sprs_pull"):
                     times = []
@@ -123,10 +124,10 @@ def main():
                                 N.call("fssdp_sprs", pb, rank, goff, soff, S // 2, jobs_t,
                                        tab.n_sprs_jobs, srcs_t, sp)
                         if kind == "sprs_pull" and tab.n_sprs_jobs:
-                            # partials already in the holders' own staging slots (the wgrad
-                            # wrote them locally): the owners' pull + sum alone
-                            N.call("fssdp_sprs_pull", pb, rank, goff, soff, S // 2, jobs_t,
-                                   tab.n_sprs_jobs, srcs_t, sp)
+                            # partials already in the holders' own grads slots (a wgrad
+                            # without c_dest writes them there): the owners' pull + sum alone
+                            N.call("fssdp_sprs_pull", pb, rank, goff, S // 2, jobs_t,
+                                   tab.n_sprs_jobs, pull_t, sp)
                         e.record()
                         torch.cuda.synchronize()
                         if it >= 2:

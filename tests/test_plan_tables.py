@@ -72,7 +72,7 @@ def test_native_tables_equal_python_tables():
             assert nt.slots == py.slots and nt.n_owned == py.n_owned
             assert nt.recv_rows == py.recv_rows
             for name in ("seg_start", "seg_rows", "seg_padded", "route_cum", "recv_base",
-                         "zero_rows", "spag_copies", "sprs_jobs", "sprs_srcs"):
+                         "zero_rows", "spag_copies", "sprs_jobs", "sprs_srcs", "sprs_pull"):
                 assert np.array_equal(np.asarray(getattr(nt, name)),
                                       np.asarray(getattr(py, name))), name
             for name in GEMM_NAMES:

@@ -79,9 +79,9 @@ def test_spag_copies_owner_shards(world, E, kind, slot_elems):
     (2, 2, "ring", 1 << 20), (4, 4, "ring", 3 * 2048 + 500), (4, 8, "hot", 1 << 18),
     (8, 8, "ring", 12345 * 4), (8, 16, "random", 77777 * 4)])
 def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull):
-    """Partials sit where the transport puts them — push: the owner's staging slot; pull:
-    the holder's own staging slot at the same index — and the owner's grads slot ends up
-    holding the ascending-rank fp32 sum (bit-exact)."""
+    """Partials sit where the transport expects them — push: the owner's staging slots;
+    pull: the holders' own grads slots — and the owner's grads slot ends up holding the
+    ascending-rank fp32 sum (bit-exact)."""
     base, post, tabs, layout, groups, slots, n_stage = setup(world, E, slot_elems, kind, seed=3)
     goff, soff = layout.offset("grads"), layout.offset("stage")
     g = torch.Generator(device="cuda").manual_seed(2)
@@ -92,21 +92,28 @@ def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull):
         grads[r].copy_(torch.randn(slots, slot_elems, generator=g, device="cuda"))
         for e, s in t.slots.items():
             partial[(e, r)] = grads[r][s].clone()
-    # place the replicas' partials the way the wgrad epilogue would (c_dest)
-    for r, t in enumerate(tabs):
-        for dst_slot, b, n in t.sprs_jobs:
-            for h, idx in t.sprs_srcs[b:b + n]:
-                if h != r:
-                    e = [x for x, s in t.slots.items() if s == dst_slot][0]
-                    (stage[h] if pull else stage[r])[idx].copy_(partial[(e, int(h))])
+    # push: place the replicas' partials where the wgrad epilogue stores them (c_dest, the
+    # owner's staging slots); pull: they stay in the holders' own grads slots
+    if not pull:
+        for r, t in enumerate(tabs):
+            for dst_slot, b, n in t.sprs_jobs:
+                for h, idx in t.sprs_srcs[b:b + n]:
+                    if h != r:
+                        e = [x for x, s in t.slots.items() if s == dst_slot][0]
+                        stage[r][idx].copy_(partial[(e, int(h))])
     torch.cuda.synchronize()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    blobs = [torch.from_numpy(t.blob[:t.nbytes].copy()).cuda() for t in tabs]
     for r, t in enumerate(tabs):
-        blob = torch.from_numpy(t.blob[:t.nbytes].copy()).cuda()
-        N.call("fssdp_sprs_pull" if pull else "fssdp_sprs",
-               C.c_void_p(groups[r].peer_bases.data_ptr()), r, goff, soff, slot_elems,
-               C.c_void_p(blob.data_ptr() + t.offsets["sprs_jobs"]), t.n_sprs_jobs,
-               C.c_void_p(blob.data_ptr() + t.offsets["sprs_srcs"]),
-               C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        pb, jobs = C.c_void_p(groups[r].peer_bases.data_ptr()), t.offsets["sprs_jobs"]
+        if pull:
+            N.call("fssdp_sprs_pull", pb, r, goff, slot_elems,
+                   C.c_void_p(blobs[r].data_ptr() + jobs), t.n_sprs_jobs,
+                   C.c_void_p(blobs[r].data_ptr() + t.offsets["sprs_pull"]), stream)
+        else:
+            N.call("fssdp_sprs", pb, r, goff, soff, slot_elems,
+                   C.c_void_p(blobs[r].data_ptr() + jobs), t.n_sprs_jobs,
+                   C.c_void_p(blobs[r].data_ptr() + t.offsets["sprs_srcs"]), stream)
     torch.cuda.synchronize()
     reduced = 0
     for r, t in enumerate(tabs):
