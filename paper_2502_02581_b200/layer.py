@@ -640,14 +640,22 @@ class FssdpMoE:
 
     def phase_bwd_rest(self) -> None:
         """dXe and the weight grads of the slots no other rank holds."""
+        self.phase_dgrad1()
+        self.phase_wgrad_rest()
+
+    def phase_dgrad1(self) -> None:
+        self._gemm("dgrad1", self.da, False, self.w1_view, True, self.dxe, self.g.d_model,
+                   ops.EPI_BF16)
+
+    def phase_wgrad_rest(self) -> None:
         f, d = self.g.d_ff, self.g.d_model
-        self._gemm("dgrad1", self.da, False, self.w1_view, True, self.dxe, d, ops.EPI_BF16)
         grads2d = self.grads.view(-1)
         self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32, part="rest")
         self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32, part="rest")
 
-    def phase_combine_dx(self) -> torch.Tensor:
-        dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
+    def phase_combine_dx(self, dx: torch.Tensor | None = None) -> torch.Tensor:
+        if dx is None:
+            dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
         self._call("fssdp_combine_dx", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
                ops._ptr(self.topk_idx), ops._ptr(self.topk_w), ops._ptr(self.slot_grad),
                ops._ptr(self.wg), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,
@@ -711,27 +719,32 @@ class FssdpMoE:
         remat = self.planner.policy.rematerialize if rematerialize is None else rematerialize
         if remat:
             self.phase_spag(refetch_early=True)
-        if self.decision.target == self.decision.base:  # no replicas anywhere: no SpRS
-            self.phase_experts_bwd()
-            self.phase_barrier(BAR_DX)
-            dx = self.phase_combine_dx()
-            self.phase_gate_wgrad()
-        else:
-            # SpRS (replica grads -> owners over NVLink) starts as soon as every rank has the
-            # weight grads of its shared slots, on a side stream, and overlaps dXe, the
-            # remaining wgrads, the dX combine and the gate backward (disjoint buffers).
-            # The decision is global (same plan on every rank), so all ranks join BAR_SPRS.
-            self.phase_bwd_shared()
-            main = torch.cuda.current_stream(self.dev)
+        # Three streams.  main: dgrad2, the shared-slot wgrads, dgrad1, the remaining
+        # wgrads.  side (replicas only): SpRS as soon as every rank has the weight grads of
+        # its shared slots.  dx: the dX combine and the gate backward as soon as every rank
+        # has its dXe rows — both HBM/NVLink-bound, they run beside the tensor-bound wgrads
+        # (disjoint buffers).  The decision is global (same plan on every rank), so every
+        # rank joins the same barriers.
+        replicas = self.decision.target != self.decision.base
+        main = torch.cuda.current_stream(self.dev)
+        self.phase_bwd_shared()
+        if replicas:
             side = self._side_stream()
             side.wait_stream(main)
             with self._on(side):
                 self.phase_barrier(BAR_SPRS)
                 self.phase_sprs()
-            self.phase_bwd_rest()
+        self.phase_dgrad1()
+        dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
+        dxs = self._dx_stream()
+        dxs.wait_stream(main)
+        with self._on(dxs):
             self.phase_barrier(BAR_DX)
-            dx = self.phase_combine_dx()
+            self.phase_combine_dx(dx)
             self.phase_gate_wgrad()
+        self.phase_wgrad_rest()
+        main.wait_stream(dxs)
+        if replicas:
             main.wait_stream(side)
         self.phase_barrier(BAR_END)
         return dx
@@ -746,6 +759,11 @@ class FssdpMoE:
                 yield
         finally:
             self._cs = prev
+
+    def _dx_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_dxs", None) is None:
+            self._dxs = torch.cuda.Stream(device=self.dev)
+        return self._dxs
 
     def _side_stream(self) -> torch.cuda.Stream:
         if getattr(self, "_side", None) is None:
