@@ -1372,7 +1372,8 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
 }
 
 int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off, int64_t dst_off,
-                       int64_t slot_bytes, const int32_t* copies, int32_t n_copies, void* stream) {
+                       int64_t slot_bytes, const int32_t* copies, int32_t n_copies,
+                       int32_t max_ctas, void* stream) {
   if (slot_bytes % 16 != 0) {
     set_error("gather_slots: slot_bytes must be a multiple of 16");
     return kErrDimension;
@@ -1387,6 +1388,11 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
     chunk = (chunk + kTmaSub - 1) / kTmaSub * kTmaSub;
     if (chunk < 4 * kTmaSub) chunk = 4 * kTmaSub;
     if (chunk > (1 << 20)) chunk = 1 << 20;
+    // a bounded footprint (max_ctas > 0): a copy running beside other kernels must leave
+    // them SM slots — small latency-bound transfers stall behind a full-width copy
+    while (max_ctas > 0 && chunk < slot_bytes &&
+           ((slot_bytes + chunk - 1) / chunk) * n_copies > max_ctas)
+      chunk *= 2;
     dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
     timing_begin(as_stream(stream));
     spag_tma_kernel<<<grid, 32, 0, as_stream(stream)>>>(peer_bases, rank, src_off, dst_off,
@@ -1404,7 +1410,7 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
 int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
                const int32_t* copies, int32_t n_copies, void* stream) {
   return fssdp_gather_slots(peer_bases, rank, param_off, param_off, slot_bytes, copies, n_copies,
-                            stream);
+                            0, stream);
 }
 
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,

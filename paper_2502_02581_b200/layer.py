@@ -19,6 +19,7 @@ on one GPU (PeerGroup mode "emulated") — the multi-rank parity tests do that.
 from __future__ import annotations
 
 import contextlib
+import os
 import ctypes as C
 import time
 from dataclasses import dataclass
@@ -338,7 +339,7 @@ class FssdpMoE:
     # calibration, or the bare partition after fallback) then copies only the rest.
     # Owned shards must not change between the end of backward and the next forward
     # (peers read them early) — put a barrier after an optimizer step that updates them.
-    PREFETCH = True
+    PREFETCH = os.environ.get("FSSDP_PREFETCH", "1") != "0"
 
     def phase_prefetch(self) -> None:
         self.pre_mask, self.pre_mask_ptr, self.pre_tables, self._pre_done = None, None, None, None
@@ -371,7 +372,9 @@ class FssdpMoE:
             self.pre_dev[:nb].copy_(self.pre_host[:nb], non_blocking=True)
             self._pre_staged = torch.cuda.Event()
             self._pre_staged.record(side)
-        self._pre_launch = True  # the copies themselves start after the count all-gather
+        self._pre_launch = True  # the copies themselves start at PREFETCH_AT
+        if self.PREFETCH_AT == "gate":
+            self._launch_prefetch()
 
     def _launch_prefetch(self) -> None:
         """Early SpAG on the side stream, ordered after the gate and the count all-gather:
@@ -387,11 +390,21 @@ class FssdpMoE:
             self._pre_done = torch.cuda.Event()
             self._pre_done.record(side)
 
+    # the early SpAG runs beside the count readback, the host planning and the table upload:
+    # a bounded grid (one CTA per SM by default, FSSDP_SPAG_PRE_CTAS; 0 = full width) keeps
+    # those small transfers from stalling behind it (N=4: the table upload went from ~90 to
+    # ~20 us, the step from 1.874 to 1.844 ms; N=2 unchanged — profiles/r1_spag_pre_ctas.txt)
+    SPAG_PRE_CTAS = int(os.environ.get("FSSDP_SPAG_PRE_CTAS", "-1"))
+
     def _spag_launch(self, key, blob_dev, tables, stream) -> None:
         spag = C.c_void_p(blob_dev.data_ptr() + tables.offsets["spag"])
+        off = self.off["params"]
+        cap = 0
+        if key == "spag_pre":
+            cap = self.SPAG_PRE_CTAS if self.SPAG_PRE_CTAS >= 0 else N.LIB.fssdp_num_sms()
         self._timed(key, lambda: N.call(
-            "fssdp_spag", self._pb(), self.rank, self.off["params"], self.g.slot_param_bytes,
-            spag, tables.n_spag, C.c_void_p(stream.cuda_stream)))
+            "fssdp_gather_slots", self._pb(), self.rank, off, off, self.g.slot_param_bytes,
+            spag, tables.n_spag, cap, C.c_void_p(stream.cuda_stream)))
 
     def phase_gate(self, x: torch.Tensor) -> None:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.g.d_model:
@@ -413,16 +426,23 @@ class FssdpMoE:
         self._call("fssdp_route_scan_allgather", ops._ptr(self.tile_counts), n_tiles,
                self.g.num_experts, ops._ptr(self.tile_prefix), self._pb(), self.off["counts"],
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch), self._stream())
-        self._launch_prefetch()
+        if self.PREFETCH_AT == "counts":
+            self._launch_prefetch()
+
+    # where the early SpAG starts: with the gate ("gate"), after the count all-gather
+    # ("counts"), or once the counts readback has left ("push")
+    PREFETCH_AT = os.environ.get("FSSDP_PREFETCH_AT", "counts")
 
     def phase_plan(self) -> None:
         # host sync point #1: pinned copy of the all-gathered counts (raw cudaMemcpyAsync +
         # stream sync: the torch copy/event path costs tens of microseconds here)
         self._mark("readback")
         self._counts_epoch = (self._counts_epoch + 1) & 0xFFFFFFFF
-        N.check(N.LIB_RAW.fssdp_push_host(self.counts_dev_ptr, self.counts_host_ptr,
-                                          self.counts_nbytes, self.counts_flag_ptr,
-                                          self._counts_epoch, self._stream()), "counts readback")
+        self._timed("push_host", lambda: N.check(N.LIB_RAW.fssdp_push_host(
+            self.counts_dev_ptr, self.counts_host_ptr, self.counts_nbytes, self.counts_flag_ptr,
+            self._counts_epoch, self._stream()), "counts readback"))
+        if self.PREFETCH_AT == "push":
+            self._launch_prefetch()
         N.check(N.LIB_RAW.fssdp_host_wait(self.counts_flag_ptr, self._counts_epoch, 60.0),
                 "counts readback")
         t_host = time.perf_counter()
@@ -435,11 +455,12 @@ class FssdpMoE:
         # plan + this rank's tables + their upload (boundary #2), capacity-checked: one native
         # call; the Python-side decision object is built after the dispatch is launched
         E, D = self.g.num_experts, self.world
-        self.planner.plan_with_tables(
+        # (timed as "pull_host": the native window covers only the table upload kernel)
+        self._timed("pull_host", lambda: self.planner.plan_with_tables(
             self.layer, counts, self.counts_host_ptr, self.rank, self.pre_mask_ptr,
             self.g.d_model, self.g.d_ff, self.blob_host_np, self.blob_host_ptr,
             NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
-            decide=False, n_mats=self.g.n_mats)
+            decide=False, n_mats=self.g.n_mats))
         self._mark("planned")
         if self.planner.last_reshard_moves:
             self._reshard_stage()
@@ -522,7 +543,7 @@ class FssdpMoE:
         self.phase_barrier(BAR_RESHARD)  # every old owner has staged its shards
         self._call("fssdp_gather_slots", self._pb(), self.rank, self.off["reshard"],
                    self.off["params"], self.g.slot_param_bytes, ops._ptr(copies),
-                   copies.shape[0], self._stream())
+                   copies.shape[0], 0, self._stream())
 
     def phase_dispatch(self) -> None:
         self._reshard_gather()
