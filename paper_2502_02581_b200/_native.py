@@ -194,6 +194,22 @@ def call(name: str, *args) -> None:
     launch_count += KERNELS_PER_CALL.get(name, 0)
 
 
+_RAW_FNS: dict = {}
+
+
+def call_raw(name: str, *args) -> None:
+    """call() through LIB_RAW (pointer arguments as c_void_p / ints): cheaper argument
+    conversion on the launch path."""
+    global launch_count
+    fn = _RAW_FNS.get(name)
+    if fn is None:
+        fn = _RAW_FNS[name] = getattr(LIB_RAW, name)
+    status = fn(*args)
+    if status != 0:
+        raise_for_status(status, name, last_error())
+    launch_count += KERNELS_PER_CALL.get(name, 0)
+
+
 class NativeEvent:
     """A CUDA event owned by libfssdp (timing enabled), with torch.cuda.Event's
     elapsed_time() so phase timers can mix with the torch-side code that reads them."""

@@ -232,6 +232,7 @@ class FssdpMoE:
         self._limits = np.array([geom.slots, geom.recv_cap, geom.stage_slots], dtype=np.int64)
         self._limits_ptr = self._limits.ctypes.data
         self._tab_ptrs = None
+        self._dispatch_args = None
         self._pb_c = C.c_void_p(self.group.peer_bases.data_ptr())
         self.T = 0
         self.x = None
@@ -546,16 +547,23 @@ class FssdpMoE:
                    copies.shape[0], 0, self._stream())
 
     def phase_dispatch(self) -> None:
+        """K4 — first launch after the host plan: its arguments are mostly prebuilt (the
+        Python between the table upload and this launch is GPU idle time)."""
         self._reshard_gather()
-        t = self.tables
         slot, epoch = self._bar(BAR_DISPATCH)
-        self._call("fssdp_dispatch", ops._ptr(self.x), ops._ptr(self.topk_idx),
-               ops._ptr(self.slot_rank), ops._ptr(self.tile_prefix), self.T, self.g.d_model,
-               self.g.num_experts, self.g.top_k, self.world, self._tab("route_cum"),
-               self._tab("recv_base"), ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
-               self._pb(), self.off["xrecv"], self._tab("zero_rows"), t.n_zero,
-               self.flags_off, self.rank, slot, C.c_uint32(epoch),
-               C.c_void_p(self.grid_counter.data_ptr()), self._stream())
+        a = self._dispatch_args
+        if a is None:
+            a = self._dispatch_args = (
+                ops._ptr(self.topk_idx), ops._ptr(self.slot_rank), ops._ptr(self.tile_prefix),
+                ops._ptr(self.slot_dest), ops._ptr(self.slot_pos), self._pb(),
+                C.c_void_p(self.grid_counter.data_ptr()))
+        idx, rank_, prefix, dest, pos, pb, counter = a
+        self._call("fssdp_dispatch", C.c_void_p(self.x.data_ptr()), idx, rank_, prefix, self.T,
+                   self.g.d_model, self.g.num_experts, self.g.top_k, self.world,
+                   self._tab("route_cum"), self._tab("recv_base"), dest, pos, pb,
+                   self.off["xrecv"], self._tab("zero_rows"), self.tables.n_zero,
+                   self.flags_off, self.rank, slot, epoch, counter, self._stream())
+        self._mark("dispatch_issued")
         self._finish_plan()
 
     # CUDA-event instrumentation (bench.py): name -> list of (start, end) events recorded on
@@ -585,9 +593,9 @@ class FssdpMoE:
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
         if self.timers is None:
-            N.call(name, *args)
+            N.call_raw(name, *args)
         else:
-            self._timed(name[6:], lambda: N.call(name, *args))
+            self._timed(name[6:], lambda: N.call_raw(name, *args))
 
     def _gemm(self, name, a, a_mn, b, b_mn, c, ldc, epi, c2=None, aux=None, part=None):
         """One grouped GEMM of the plan; `part` "shared" / "rest" launches the wgrad prefix
