@@ -295,6 +295,16 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
  * D x E int32 table at heap offset table_off (row = rank), followed by a device
  * barrier (barrier slot `bar_slot`, value `epoch`; a negative bar_slot skips every
  * barrier of an entry point — single rank, or lockstep emulation of several ranks). */
+/* K1 + K2 in one launch (the layer's path): the tensor-core gate, whose last CTA to finish
+ * then does fssdp_route_scan_allgather's work (tile_prefix, this rank's totals into every
+ * rank's count table, world barrier on bar_slot / epoch).  ws: int32[1 + E] device
+ * workspace, zero before the first call (left zero after each).  Shapes the tensor-core
+ * gate does not take (d % 64 or E not in {8, 16, 32, 64}) run the two kernels. */
+int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
+                     int32_t E, int32_t k, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
+                     int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
+                     const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
+                     int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch, void* stream);
 int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,

@@ -103,6 +103,8 @@ _SIGS = {
     "fssdp_epilogue_tmap": [i32, vp, i64, i64, vp],
     "fssdp_gate_topk": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
+    "fssdp_gate_route": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i64,
+                         i32, i32, i32, C.c_uint32, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
     "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
@@ -180,7 +182,7 @@ def check(status: int, what: str) -> None:
 # kernels launched per successful call of each device entry point (launch accounting)
 KERNELS_PER_CALL = {
     "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
-    "fssdp_route_scan_allgather": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1,
+    "fssdp_route_scan_allgather": 1, "fssdp_gate_route": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
     "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
     "fssdp_gather_slots": 1,

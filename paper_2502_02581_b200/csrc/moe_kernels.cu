@@ -262,20 +262,85 @@ __device__ __forceinline__ void split_bf16x2(float2 w, uint32_t& hi, uint32_t& l
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-template <int NT>  // NT = E / 8 expert tiles
-__global__ void __launch_bounds__(128)
+// Count scan + all-gather tail of the fused gate (fssdp_gate_route), run by the gate's LAST
+// CTA to finish (ticket in ws[0]; per-expert totals accumulated in ws[1..E] by atomics):
+// tile_prefix[t][e] = sum of tile_counts[t'][e] over t' < t, this rank's totals written into
+// every rank's count table, then the world barrier.  The other CTAs' tile counts are read
+// through L2 (__ldcg): they were published with a fence before taking their ticket.
+__device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ tile_counts,
+                                int32_t* __restrict__ tile_prefix, int32_t* __restrict__ ws,
+                                const uint64_t* __restrict__ peer_bases, int64_t table_off,
+                                int64_t flags_off, int rank, int world, int slot, uint32_t epoch) {
+  __shared__ int32_t csum[512];
+  const int nthr = blockDim.x;
+  const int chunks = (nthr < 512 ? nthr : 512) / E;
+  const int per = (n_tiles + chunks - 1) / chunks;
+  const int e = threadIdx.x % E;
+  const int c = threadIdx.x / E;
+  const bool active = c < chunks;
+  const int t0 = c * per, t1 = min(n_tiles, t0 + per);
+  int32_t sum = 0;
+  if (active) {
+#pragma unroll 8
+    for (int t = t0; t < t1; ++t) sum += __ldcg(tile_counts + static_cast<int64_t>(t) * E + e);
+    csum[threadIdx.x] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x < E) {  // exclusive scan over the chunks of expert threadIdx.x
+    int32_t run = 0;
+    for (int q = 0; q < chunks; ++q) {
+      const int32_t v = csum[q * E + threadIdx.x];
+      csum[q * E + threadIdx.x] = run;
+      run += v;
+    }
+    const int32_t total = __ldcg(ws + 1 + threadIdx.x);
+    for (int p = 0; p < world; ++p)
+      reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + threadIdx.x] = total;
+    ws[1 + threadIdx.x] = 0;  // ready for the next call (stream order)
+  }
+  __syncthreads();
+  if (active) {
+    int32_t run = csum[threadIdx.x];
+    for (int t = t0; t < t1; ++t) {
+      tile_prefix[static_cast<int64_t>(t) * E + e] = run;
+      run += __ldcg(tile_counts + static_cast<int64_t>(t) * E + e);
+    }
+  }
+  if (threadIdx.x == 0) ws[0] = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncwarp();
+    world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
+  }
+}
+
+// NT = E / 8 expert tiles; KS = warps splitting d (the CTA is 4 x KS warps: 4 groups of 16
+// tokens, each group's columns split KS ways, partial logits summed in smem in ks order) —
+// more warps per SM for a kernel that is bound by the latency of reading x.  SW: the split
+// gate weights are staged once per CTA in shared memory (one 16-byte record {hi, hi, lo,
+// lo} per 4 columns, rows padded by 16 B) instead of re-read and re-split from L1/L2 by
+// every warp inside the MMA loop.
+template <int NT, int KS, bool SW>
+__global__ void __launch_bounds__(128 * KS)
     gate_topk_mma_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
                          const float* __restrict__ bias, int64_t T, int d, int E, int k,
                          float* __restrict__ logits, int32_t* __restrict__ topk_idx,
                          float* __restrict__ topk_w, int32_t* __restrict__ slot_rank,
-                         int32_t* __restrict__ tile_counts) {
+                         int32_t* __restrict__ tile_counts, int32_t* __restrict__ tile_prefix,
+                         int32_t* __restrict__ ws, const uint64_t* __restrict__ peer_bases,
+                         int64_t table_off, int64_t flags_off, int rank, int world, int slot,
+                         uint32_t epoch) {
   __shared__ float lg[kGateTile][kGateMaxE + 1];
+  __shared__ float part[KS > 1 ? KS - 1 : 1][kGateTile][8 * NT + 1];
   __shared__ int32_t s_idx[kGateTile * kGateMaxK];
   __shared__ int32_t s_cnt[kGateMaxE];
+  __shared__ int is_last;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tg = warp % 4, ks = warp / 4;
   const int g = lane >> 2, t4 = lane & 3;
   const int tile = blockIdx.x;
-  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile + warp * 16;
+  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile + tg * 16;
   const int64_t r0 = t0 + g, r1 = t0 + g + 8;
   const bool v0 = r0 < T, v1 = r1 < T;
   const int4* xr0 = reinterpret_cast<const int4*>(x + (v0 ? r0 : 0) * d);
@@ -289,13 +354,28 @@ __global__ void __launch_bounds__(128)
   // rows g and g+8 (each load instruction covers 64 contiguous bytes per row).  The MMA's
   // k index is a fixed permutation of the block's columns, applied to x and Wg alike: the
   // logits are the same dot products, summed in another order.  KB blocks in flight.
+  extern __shared__ __align__(16) uint8_t gate_wsm[];
+  const int wrow = 4 * d + 16;  // bytes per staged expert row
+  if (SW) {
+    const int per_row = d / 4;
+    for (int i = threadIdx.x; i < E * per_row; i += blockDim.x) {
+      const int e = i / per_row, c4 = i % per_row;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(wg + static_cast<int64_t>(e) * d) + c4);
+      uint4 rec;
+      split_bf16x2(make_float2(v.x, v.y), rec.x, rec.z);
+      split_bf16x2(make_float2(v.z, v.w), rec.y, rec.w);
+      *reinterpret_cast<uint4*>(gate_wsm + e * wrow + c4 * 16) = rec;
+    }
+    __syncthreads();
+  }
   constexpr int KB = 4;
-  for (int kb = 0; kb < d; kb += 64 * KB) {
+  const int dk = d / KS, kbeg = ks * dk, kend = kbeg + dk;
+  for (int kb = kbeg; kb < kend; kb += 64 * KB) {
     int4 va[KB][2], vb[KB][2];
 #pragma unroll
     for (int u = 0; u < KB; ++u) {
       const int col = kb + 64 * u + 8 * t4;
-      const bool in = kb + 64 * u < d;
+      const bool in = kb + 64 * u < kend;
       va[u][0] = (in && v0) ? __ldg(xr0 + col / 8) : make_int4(0, 0, 0, 0);
       va[u][1] = (in && v0) ? __ldg(xr0 + col / 8 + 4) : make_int4(0, 0, 0, 0);
       vb[u][0] = (in && v1) ? __ldg(xr1 + col / 8) : make_int4(0, 0, 0, 0);
@@ -303,7 +383,7 @@ __global__ void __launch_bounds__(128)
     }
 #pragma unroll
     for (int u = 0; u < KB; ++u) {
-      if (kb + 64 * u >= d) break;
+      if (kb + 64 * u >= kend) break;
       const uint32_t* pa = reinterpret_cast<const uint32_t*>(&va[u][0]);  // 8 column pairs
       const uint32_t* pb = reinterpret_cast<const uint32_t*>(&vb[u][0]);
 #pragma unroll
@@ -312,26 +392,60 @@ __global__ void __launch_bounds__(128)
         const int wcol = kb + 64 * u + (st < 2 ? 8 * t4 + 4 * st : 32 + 8 * t4 + 4 * (st - 2));
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-          const float4 wv =
-              __ldg(reinterpret_cast<const float4*>(wg + static_cast<int64_t>(n * 8 + g) * d + wcol));
-          uint32_t h0, l0, h1, l1;
-          split_bf16x2(make_float2(wv.x, wv.y), h0, l0);
-          split_bf16x2(make_float2(wv.z, wv.w), h1, l1);
-          mma_bf16_16816(c[n], a, h0, h1);
-          mma_bf16_16816(c[n], a, l0, l1);
+          if (SW) {
+            const uint4 r =
+                *reinterpret_cast<const uint4*>(gate_wsm + (n * 8 + g) * wrow + (wcol / 4) * 16);
+            mma_bf16_16816(c[n], a, r.x, r.y);
+            mma_bf16_16816(c[n], a, r.z, r.w);
+          } else {
+            const float4 wv = __ldg(
+                reinterpret_cast<const float4*>(wg + static_cast<int64_t>(n * 8 + g) * d + wcol));
+            uint32_t h0, l0, h1, l1;
+            split_bf16x2(make_float2(wv.x, wv.y), h0, l0);
+            split_bf16x2(make_float2(wv.z, wv.w), h1, l1);
+            mma_bf16_16816(c[n], a, h0, h1);
+            mma_bf16_16816(c[n], a, l0, l1);
+          }
         }
       }
     }
   }
-  const int lr = warp * 16 + g;
+  const int lr = tg * 16 + g;
+  if (KS > 1) {
+    if (ks > 0) {
 #pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    const int e = n * 8 + 2 * t4;
-    const float b0 = bias ? bias[e] : 0.f, b1 = bias ? bias[e + 1] : 0.f;
-    lg[lr][e] = bias ? __fadd_rn(c[n][0], b0) : c[n][0];
-    lg[lr][e + 1] = bias ? __fadd_rn(c[n][1], b1) : c[n][1];
-    lg[lr + 8][e] = bias ? __fadd_rn(c[n][2], b0) : c[n][2];
-    lg[lr + 8][e + 1] = bias ? __fadd_rn(c[n][3], b1) : c[n][3];
+      for (int n = 0; n < NT; ++n) {
+        const int e = n * 8 + 2 * t4;
+        part[ks - 1][lr][e] = c[n][0];
+        part[ks - 1][lr][e + 1] = c[n][1];
+        part[ks - 1][lr + 8][e] = c[n][2];
+        part[ks - 1][lr + 8][e + 1] = c[n][3];
+      }
+    }
+    __syncthreads();
+    if (ks == 0) {
+#pragma unroll
+      for (int q = 0; q < KS - 1; ++q)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int e = n * 8 + 2 * t4;
+          c[n][0] = __fadd_rn(c[n][0], part[q][lr][e]);
+          c[n][1] = __fadd_rn(c[n][1], part[q][lr][e + 1]);
+          c[n][2] = __fadd_rn(c[n][2], part[q][lr + 8][e]);
+          c[n][3] = __fadd_rn(c[n][3], part[q][lr + 8][e + 1]);
+        }
+    }
+  }
+  if (ks == 0) {
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int e = n * 8 + 2 * t4;
+      const float b0 = bias ? bias[e] : 0.f, b1 = bias ? bias[e + 1] : 0.f;
+      lg[lr][e] = bias ? __fadd_rn(c[n][0], b0) : c[n][0];
+      lg[lr][e + 1] = bias ? __fadd_rn(c[n][1], b1) : c[n][1];
+      lg[lr + 8][e] = bias ? __fadd_rn(c[n][2], b0) : c[n][2];
+      lg[lr + 8][e + 1] = bias ? __fadd_rn(c[n][3], b1) : c[n][3];
+    }
   }
   __syncthreads();
   const int64_t tt0 = static_cast<int64_t>(tile) * kGateTile;
@@ -343,6 +457,21 @@ __global__ void __launch_bounds__(128)
   }
   gate_select_tile(&lg[0][0], kGateMaxE + 1, tile, T, E, k, s_idx, s_cnt, topk_idx, topk_w,
                    slot_rank, tile_counts);
+  if (ws == nullptr) return;
+  // fused K2: publish this tile's counts, and the last CTA scans / all-gathers them
+  __syncthreads();
+  if (threadIdx.x < E) atomicAdd(ws + 1 + threadIdx.x, s_cnt[threadIdx.x]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int ticket = atomicAdd(ws, 1);
+    is_last = ticket == static_cast<int>(gridDim.x) - 1;
+    if (is_last) __threadfence();
+  }
+  __syncthreads();
+  if (!is_last) return;
+  gate_route_tail(gridDim.x, E, tile_counts, tile_prefix, ws, peer_bases, table_off, flags_off,
+                  rank, world, slot, epoch);
 }
 
 __global__ void __launch_bounds__(kGateThreads)
@@ -1168,6 +1297,59 @@ static int grid_for_warps(int64_t work_items) {
   return static_cast<int>(blocks);
 }
 
+static bool gate_mma_ok(int d, int E) {
+  return E % 8 == 0 && d % 64 == 0 && (E == 8 || E == 16 || E == 32 || E == 64);
+}
+
+// The tensor-core gate, K split over 2 warps per token group when d allows it.
+static int gate_mma_launch(const __nv_bfloat16* x, const float* wg, const float* bias, int64_t T,
+                           int d, int E, int k, float* logits, int32_t* topk_idx, float* topk_w,
+                           int32_t* slot_rank, int32_t* tile_counts, int32_t* tile_prefix,
+                           int32_t* ws, const uint64_t* peer_bases, int64_t table_off,
+                           int64_t flags_off, int rank, int world, int slot, uint32_t epoch,
+                           cudaStream_t stream) {
+  const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
+  const bool split = d % 128 == 0;
+  // staged split weights when they fit beside two CTAs per SM
+  const size_t wsm = static_cast<size_t>(E) * (4 * static_cast<size_t>(d) + 16);
+  const bool sw = wsm <= 80 * 1024;
+  auto go = [&](auto kern, int threads) {
+    const size_t dyn = sw ? wsm : 0;
+    // static + dynamic above 48 KB needs the opt-in; raised once per kernel (all the
+    // instantiations share one function-pointer type, so key by address)
+    static const void* fn_seen[32];
+    static size_t fn_opted[32];
+    int slot_i = 0;
+    while (slot_i < 31 && fn_seen[slot_i] != nullptr &&
+           fn_seen[slot_i] != reinterpret_cast<const void*>(kern))
+      ++slot_i;
+    fn_seen[slot_i] = reinterpret_cast<const void*>(kern);
+    if (dyn > fn_opted[slot_i]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(dyn)) != cudaSuccess)
+        return;  // reported by launch_status()
+      fn_opted[slot_i] = dyn;
+    }
+    timing_begin(stream);
+    kern<<<tiles, threads, dyn, stream>>>(x, wg, bias, T, d, E, k, logits, topk_idx, topk_w,
+                                          slot_rank, tile_counts, tile_prefix, ws, peer_bases,
+                                          table_off, flags_off, rank, world, slot, epoch);
+  };
+#define FSSDP_GATE_GO(KS, SW, THREADS)                              \
+  do {                                                              \
+    if (E == 8) go(gate_topk_mma_kernel<1, KS, SW>, THREADS);       \
+    else if (E == 16) go(gate_topk_mma_kernel<2, KS, SW>, THREADS); \
+    else if (E == 32) go(gate_topk_mma_kernel<4, KS, SW>, THREADS); \
+    else go(gate_topk_mma_kernel<8, KS, SW>, THREADS);              \
+  } while (0)
+  if (split && sw) FSSDP_GATE_GO(2, true, 256);
+  else if (split) FSSDP_GATE_GO(2, false, 256);
+  else if (sw) FSSDP_GATE_GO(1, true, 128);
+  else FSSDP_GATE_GO(1, false, 128);
+#undef FSSDP_GATE_GO
+  return kOk;
+}
+
 }  // namespace fssdp
 
 using namespace fssdp;
@@ -1184,17 +1366,11 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
   }
   if (T == 0) return kOk;
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
-  if (E % 8 == 0 && d % 64 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
-    auto mma_launch = [&](auto kern) {
-      timing_begin(as_stream(stream));
-      kern<<<tiles, 128, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(x), wg, bias,
-                                                  T, d, E, k, logits, topk_idx, topk_w, slot_rank,
-                                                  tile_counts);
-    };
-    if (E == 8) mma_launch(gate_topk_mma_kernel<1>);
-    else if (E == 16) mma_launch(gate_topk_mma_kernel<2>);
-    else if (E == 32) mma_launch(gate_topk_mma_kernel<4>);
-    else mma_launch(gate_topk_mma_kernel<8>);
+  if (gate_mma_ok(d, E)) {
+    const int rc = gate_mma_launch(static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k,
+                                   logits, topk_idx, topk_w, slot_rank, tile_counts, nullptr,
+                                   nullptr, nullptr, 0, 0, 0, 1, -1, 0, as_stream(stream));
+    if (rc != kOk) return rc;
     return launch_status();
   }
   size_t smem = kGateTile * sizeof(__nv_bfloat16) * (kGateChunk + 8) +
@@ -1235,6 +1411,32 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
   timing_begin(as_stream(stream));
   topk_from_logits_kernel<<<tiles, kGateThreads, 0, as_stream(stream)>>>(
       logits, T, E, k, topk_idx, topk_w, slot_rank, tile_counts);
+  return launch_status();
+}
+
+int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
+                     int32_t E, int32_t k, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
+                     int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
+                     const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
+                     int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch, void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
+      k > E || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world) {
+    set_error("gate_route: unsupported shape");
+    return kErrDimension;
+  }
+  const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
+  if (!gate_mma_ok(d, E) || tiles == 0) {  // the two-kernel path
+    int rc = fssdp_gate_topk(x, wg, bias, T, d, E, k, nullptr, topk_idx, topk_w, slot_rank,
+                             tile_counts, stream);
+    if (rc != kOk) return rc;
+    return fssdp_route_scan_allgather(tile_counts, tiles, E, tile_prefix, peer_bases, table_off,
+                                      flags_off, rank, world, bar_slot, epoch, stream);
+  }
+  const int rc = gate_mma_launch(static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k,
+                                 nullptr, topk_idx, topk_w, slot_rank, tile_counts, tile_prefix,
+                                 ws, peer_bases, table_off, flags_off, rank, world, bar_slot,
+                                 epoch, as_stream(stream));
+  if (rc != kOk) return rc;
   return launch_status();
 }
 

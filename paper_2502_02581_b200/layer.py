@@ -32,7 +32,7 @@ from . import ops
 from .comm import HeapLayout, PeerGroup
 from .engine import FssdpPlanner
 from .errors import DimensionError, InternalError
-from .plan_tables import NativeTables, n_tile_widths
+from .plan_tables import NativeTables, _layout, n_tile_widths
 
 WG_TILE = 64  # FSSDP_WG_TILE (include/fssdp.h)
 GROUP_BYTES = N.C.sizeof(N.GemmGroup)  # fssdp_gemm_group
@@ -211,6 +211,7 @@ class FssdpMoE:
         wg_tiles = max(1, (Tc + WG_TILE - 1) // WG_TILE)
         self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
+        self.gate_ws = torch.zeros(1 + E, dtype=torch.int32, device=self.dev)  # ticket, totals
         self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
         self.blob_host_np = self.blob_host.numpy()
         self.blob_host_ptr = self.blob_host_np.ctypes.data
@@ -233,6 +234,7 @@ class FssdpMoE:
         self._limits_ptr = self._limits.ctypes.data
         self._tab_ptrs = None
         self._dispatch_args = None
+        self._dispatched = False
         self._pb_c = C.c_void_p(self.group.peer_bases.data_ptr())
         self.T = 0
         self.x = None
@@ -323,12 +325,12 @@ class FssdpMoE:
         return slot, epoch
 
     def _tab(self, name: str) -> C.c_void_p:
+        """Device address of a table section (the layout is fixed per (E, D))."""
         ptrs = self._tab_ptrs
-        if ptrs is None or ptrs[0] is not self.packed.offsets:  # layout is per (E, D)
-            offs = self.packed.offsets
-            ptrs = self._tab_ptrs = (offs, {k: C.c_void_p(self.blob_dev_ptr + v)
-                                            for k, v in offs.items()})
-        return ptrs[1][name]
+        if ptrs is None:
+            offs, _ = _layout(self.g.num_experts, self.world)
+            ptrs = self._tab_ptrs = {k: C.c_void_p(self.blob_dev_ptr + v) for k, v in offs.items()}
+        return ptrs[name]
 
     def _pb(self) -> C.c_void_p:
         return self._pb_c
@@ -416,17 +418,18 @@ class FssdpMoE:
         self.x = x.contiguous()
         self.T = T
         E, k = self.g.num_experts, self.g.top_k
-        self._call("fssdp_gate_topk", ops._ptr(self.x), ops._ptr(self.wg), ops._ptr(self.gate_bias),
-               T, self.g.d_model, E, k,
-               C.c_void_p(0), ops._ptr(self.topk_idx), ops._ptr(self.topk_w),
-               ops._ptr(self.slot_rank), ops._ptr(self.tile_counts), self._stream())
+        # K1 + K2 fused: the gate's last CTA scans the tile counts, all-gathers this rank's
+        # totals and joins the count barrier
+        slot, epoch = self._bar(BAR_COUNTS)
+        self._call("fssdp_gate_route", ops._ptr(self.x), ops._ptr(self.wg),
+                   ops._ptr(self.gate_bias), T, self.g.d_model, E, k, ops._ptr(self.topk_idx),
+                   ops._ptr(self.topk_w), ops._ptr(self.slot_rank), ops._ptr(self.tile_counts),
+                   ops._ptr(self.tile_prefix), ops._ptr(self.gate_ws), self._pb(),
+                   self.off["counts"], self.flags_off, self.rank, self.world, slot, epoch,
+                   self._stream())
 
     def phase_counts(self) -> None:
-        n_tiles = (self.T + ops.GATE_TILE - 1) // ops.GATE_TILE
-        slot, epoch = self._bar(BAR_COUNTS)
-        self._call("fssdp_route_scan_allgather", ops._ptr(self.tile_counts), n_tiles,
-               self.g.num_experts, ops._ptr(self.tile_prefix), self._pb(), self.off["counts"],
-               self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch), self._stream())
+        """The counts are all-gathered by the gate launch; the early SpAG may start now."""
         if self.PREFETCH_AT == "counts":
             self._launch_prefetch()
 
@@ -434,7 +437,9 @@ class FssdpMoE:
     # ("counts"), or once the counts readback has left ("push")
     PREFETCH_AT = os.environ.get("FSSDP_PREFETCH_AT", "counts")
 
-    def phase_plan(self) -> None:
+    def phase_plan(self, dispatch: bool = False) -> None:
+        """Counts readback, host plan, table upload; with dispatch=True the dispatch is
+        launched right after the upload, before any Python bookkeeping of the plan."""
         # host sync point #1: pinned copy of the all-gathered counts (raw cudaMemcpyAsync +
         # stream sync: the torch copy/event path costs tens of microseconds here)
         self._mark("readback")
@@ -448,11 +453,11 @@ class FssdpMoE:
                 "counts readback")
         t_host = time.perf_counter()
         self._mark("synced")
-        self._plan_tables(self.counts_host_np)
+        self._plan_tables(self.counts_host_np, dispatch)
         if self.timers is not None:
             self.timers.setdefault("host_plan_s", []).append(time.perf_counter() - t_host)
 
-    def _plan_tables(self, counts) -> None:
+    def _plan_tables(self, counts, dispatch: bool = False) -> None:
         # plan + this rank's tables + their upload (boundary #2), capacity-checked: one native
         # call; the Python-side decision object is built after the dispatch is launched
         E, D = self.g.num_experts, self.world
@@ -463,6 +468,14 @@ class FssdpMoE:
             NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
             decide=False, n_mats=self.g.n_mats))
         self._mark("planned")
+        if self.gap_events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self.gap_events[-1] = (self.gap_events[-1][0], e1)
+        self._dispatched = False
+        if dispatch and not self.planner.last_reshard_moves:
+            self.phase_dispatch(n_zero=int(NativeTables._hdr[3]))  # header: n_zero
+            self._dispatched = True
         if self.planner.last_reshard_moves:
             self._reshard_stage()
         tables = NativeTables.from_header(E, D, self.blob_host_np)
@@ -546,7 +559,7 @@ class FssdpMoE:
                    self.off["params"], self.g.slot_param_bytes, ops._ptr(copies),
                    copies.shape[0], 0, self._stream())
 
-    def phase_dispatch(self) -> None:
+    def phase_dispatch(self, n_zero: int | None = None) -> None:
         """K4 — first launch after the host plan: its arguments are mostly prebuilt (the
         Python between the table upload and this launch is GPU idle time)."""
         self._reshard_gather()
@@ -561,10 +574,10 @@ class FssdpMoE:
         self._call("fssdp_dispatch", C.c_void_p(self.x.data_ptr()), idx, rank_, prefix, self.T,
                    self.g.d_model, self.g.num_experts, self.g.top_k, self.world,
                    self._tab("route_cum"), self._tab("recv_base"), dest, pos, pb,
-                   self.off["xrecv"], self._tab("zero_rows"), self.tables.n_zero,
+                   self.off["xrecv"], self._tab("zero_rows"),
+                   self.tables.n_zero if n_zero is None else n_zero,
                    self.flags_off, self.rank, slot, epoch, counter, self._stream())
         self._mark("dispatch_issued")
-        self._finish_plan()
 
     # CUDA-event instrumentation (bench.py): name -> list of (start, end) events recorded on
     # the launching stream around each kernel launch; None disables it.
@@ -724,12 +737,11 @@ class FssdpMoE:
         if self.gap_events is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        self.phase_plan()
-        if self.gap_events is not None:
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record()
-            self.gap_events.append((e0, e1))
-        self.phase_dispatch()
+            self.gap_events.append((e0, None))  # closed after the table upload
+        self.phase_plan(dispatch=True)
+        if not self._dispatched:
+            self.phase_dispatch()
+        self._finish_plan()
         self._mark("dispatch_launched")
         self.phase_spag()  # only fwd1 reads the replicas: the dispatch overlaps the early SpAG
         self.phase_experts_fwd()
@@ -912,6 +924,7 @@ def run_lockstep_forward(layers: list, xs: list) -> list:
         ly.phase_plan()
     for ly in layers:
         ly.phase_dispatch()
+        ly._finish_plan()
     for ly in layers:
         ly.phase_spag()
     for ly in layers:

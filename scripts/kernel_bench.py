@@ -20,15 +20,15 @@ from paper_2502_02581_b200 import ops  # noqa: E402
 
 
 def timeit(fn, reps=30):
+    """Median µs of one entry point's kernels (native launch-timing window: no host time)."""
     for _ in range(5):
         fn()
     ts = []
     for _ in range(reps):
-        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
-        s.record()
-        fn()
-        e.record()
+        timers = {}
+        N.timed_launch(timers, "k", fn)
         torch.cuda.synchronize()
+        s, e = timers["k"][0]
         ts.append(s.elapsed_time(e) * 1e3)
     return float(np.median(ts))
 

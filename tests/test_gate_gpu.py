@@ -49,3 +49,44 @@ def test_topk_ties_pick_lower_expert():
     assert (idx.cpu().numpy()[1::2] == [5, 0]).all()
     np.testing.assert_array_equal(rank.cpu().numpy(), o_rank)
     np.testing.assert_array_equal(tc.cpu().numpy(), o_tc)
+
+
+@pytest.mark.parametrize("T,d,E,k", [(16384, 1024, 16, 2), (1000, 256, 8, 2), (777, 2048, 64, 2),
+                                     (130, 192, 16, 4)])
+def test_gate_route_fused_equals_two_kernels(T, d, E, k):
+    """fssdp_gate_route (gate + last-CTA scan / count all-gather) == fssdp_gate_topk followed
+    by fssdp_route_scan_allgather, bit for bit, and leaves its workspace zeroed (twice)."""
+    import ctypes as C
+
+    from paper_2502_02581_b200 import _native as N
+    from paper_2502_02581_b200 import ops
+    from paper_2502_02581_b200.comm import HeapLayout, emulated_group
+
+    g = torch.Generator().manual_seed(T + d)
+    x = torch.randn(T, d, generator=g).bfloat16().cuda()
+    wg = (torch.randn(E, d, generator=g) / d ** 0.5).cuda()
+    bias = torch.linspace(-1, 1, E).cuda()
+    layout = HeapLayout()
+    layout.add("counts", 4 * E * 4)
+    (grp,) = emulated_group(layout, 1)
+    pb, off, flags = C.c_void_p(grp.peer_bases.data_ptr()), layout.offset("counts"), layout.offset("flags")
+    table = grp.local.tensor(off, (E,), torch.int32)
+    tiles = (T + ops.GATE_TILE - 1) // ops.GATE_TILE
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    idx, w, rank, tc, _ = ops.gate_topk(x, wg, k, bias=bias)
+    prefix = torch.empty(tiles, E, dtype=torch.int32, device="cuda")
+    N.call("fssdp_route_scan_allgather", ops._ptr(tc), tiles, E, ops._ptr(prefix), pb, off, flags,
+           0, 1, -1, 0, s)
+    torch.cuda.synchronize()
+    want = [t.cpu().clone() for t in (idx, w, rank, tc, prefix, table)]
+    ws = torch.zeros(1 + E, dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        out = [torch.empty_like(t) for t in (idx, w, rank, tc, prefix)]
+        table.zero_()
+        N.call("fssdp_gate_route", ops._ptr(x), ops._ptr(wg), ops._ptr(bias), T, d, E, k,
+               *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0, s)
+        torch.cuda.synchronize()
+        for a, b in zip(want, [t.cpu() for t in out] + [table.cpu()]):
+            assert torch.equal(a, b)
+        assert not ws.any()
+    assert int(want[5].sum()) == T * k
