@@ -460,7 +460,7 @@ def run_ours(args):
                               layer.g.slot_grad_elems * 4)
     host_ms = 1e3 * sum(timers.get("host_plan_s", [])) / args.steps
     allr = gather([gemm_ms, flops_rank, spag_ms, sprs_ms, spag_in, sprs_in, host_ms, ms,
-                   sprs_reduce_bytes])
+                   sprs_reduce_bytes, rows_rank, float(t.recv_rows), float(t.n_slots)])
     peaks, peak_src = load_peaks()
     achieved = allr[:, 1].sum() / (allr[:, 0].sum() * 1e-3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
@@ -477,6 +477,11 @@ def run_ours(args):
                                      "(n_mats 2 GeLU, 3 SwiGLU)",
                 "peak_source": f"{peak_src}, sustained bf16 (kernels timed inside a long step)",
                 "gemm_ms_per_step_per_rank": [round(v, 4) for v in allr[:, 0]],
+                "gemm_tflops_per_rank": [round(f / (g * 1e-3) / 1e12, 1)
+                                         for g, f in zip(allr[:, 0], allr[:, 1])],
+                "routed_rows_per_rank": [int(v) for v in allr[:, 9]],
+                "padded_rows_per_rank": [int(v) for v in allr[:, 10]],
+                "expert_slots_per_rank": [int(v) for v in allr[:, 11]],
                 "gemm_share_of_step": float(allr[:, 0].max() / ms_max),
                 "gemm_launches_per_step": gemm_launches / args.steps,
                 "host_plan_ms_per_step": float(allr[:, 6].max())}
