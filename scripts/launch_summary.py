@@ -2,7 +2,7 @@
 kernels (namespace fssdp) of the last `steps` steps, `per_step` launches each.  ncu times
 are cold-cache and serialised: compare SHARES of the step, not absolute step times.
 
-    python scripts/launch_summary.py gpurun_out/launches.csv [steps=2] [per_step=14]
+    python scripts/launch_summary.py gpurun_out/launches.csv [steps=2] [per_step=15]
 """
 import collections
 import csv
@@ -10,7 +10,7 @@ import sys
 
 path = sys.argv[1]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-per_step = int(sys.argv[3]) if len(sys.argv) > 3 else 14
+per_step = int(sys.argv[3]) if len(sys.argv) > 3 else 15
 rows = list(csv.reader(open(path)))
 hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 h = rows[hdr]

@@ -6,9 +6,10 @@ FSSDP_TIMELINE=gpurun_out/tl python bench.py --steps 20 --warmup 5 > gpurun_out/
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-# warm-up 3 steps + timed 1 step = 4 x 14 launches skipped: the capture is the instrumented step
+# warm-up 3 + timed 1 + gap-probe 1 steps: 4 x 13 matching launches skipped (gate, dispatch,
+# 6 GEMMs, combine, dispatch_grad, combine_dx, gate_wgrad x2), then one step captured
 ncu --set full --clock-control none --import-source on \
-    -k regex:"dispatch|combine|gate|route_scan|grouped_gemm" --launch-skip 56 -c 14 \
+    -k regex:"dispatch|combine|gate|route_scan|grouped_gemm" --launch-skip 52 -c 13 \
     -f -o gpurun_out/step_full \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 echo PROFILE_DONE
