@@ -299,12 +299,18 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
  * then does fssdp_route_scan_allgather's work (tile_prefix, this rank's totals into every
  * rank's count table, world barrier on bar_slot / epoch).  ws: int32[1 + E] device
  * workspace, zero before the first call (left zero after each).  Shapes the tensor-core
- * gate does not take (d % 64 or E not in {8, 16, 32, 64}) run the two kernels. */
+ * gate does not take (d % 64 or E not in {8, 16, 32, 64}) run the two kernels.
+ * local_tables (nullable; world must be 1): a device table blob of fssdp_tables_layout(E, 1)
+ * whose dispatch sections are filled from the counts — route_cum, recv_base and zero_rows
+ * with one {row, count >= 0} entry per expert (pass n_zero = E to fssdp_dispatch) — equal to
+ * what fssdp_build_rank_tables derives for a single device, so the dispatch can be
+ * launched before the host plan. */
 int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
                      int32_t E, int32_t k, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
                      int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
                      const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
-                     int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch, void* stream);
+                     int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
+                     int32_t* local_tables, void* stream);
 int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,

@@ -267,11 +267,46 @@ __device__ __forceinline__ void split_bf16x2(float2 w, uint32_t& hi, uint32_t& l
 // tile_prefix[t][e] = sum of tile_counts[t'][e] over t' < t, this rank's totals written into
 // every rank's count table, then the world barrier.  The other CTAs' tile counts are read
 // through L2 (__ldcg): they were published with a fence before taking their ticket.
+//
+// local != nullptr (a single-rank layer): the placement cannot change (one device holds every
+// expert, the route is the counts), so the dispatch tables are a function of the counts and
+// are written here — route_cum [E][2], recv_base [E][1], zero_rows [E][2] (every expert,
+// count 0 where the segment has no padding) in the fssdp_build_rank_tables layout — and the
+// dispatch can run while the host plans.
+struct GateLocalTables {
+  int32_t* route_cum;
+  int32_t* recv_base;
+  int32_t* zero_rows;
+};
+
+__device__ void write_local_tables(const int32_t* totals, int E, GateLocalTables local) {
+  int32_t row = 0;
+  for (int e = 0; e < E; ++e) {
+    const int32_t c = totals[e], pad = (c + 255) / 256 * 256;  // CTA-pair GEMM M tile
+    local.route_cum[2 * e] = 0;
+    local.route_cum[2 * e + 1] = c;
+    local.recv_base[e] = row;
+    local.zero_rows[2 * e] = row + c;
+    local.zero_rows[2 * e + 1] = pad - c;
+    row += pad;
+  }
+}
+
+// the two-kernel path's version (after fssdp_route_scan_allgather wrote the counts row)
+__global__ void gate_local_tables_kernel(const uint64_t* peer_bases, int rank, int64_t table_off,
+                                         int E, GateLocalTables local) {
+  if (threadIdx.x == 0)
+    write_local_tables(reinterpret_cast<const int32_t*>(peer_bases[rank] + table_off) + rank * E,
+                       E, local);
+}
+
 __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ tile_counts,
                                 int32_t* __restrict__ tile_prefix, int32_t* __restrict__ ws,
                                 const uint64_t* __restrict__ peer_bases, int64_t table_off,
-                                int64_t flags_off, int rank, int world, int slot, uint32_t epoch) {
+                                int64_t flags_off, int rank, int world, int slot, uint32_t epoch,
+                                GateLocalTables local) {
   __shared__ int32_t csum[512];
+  __shared__ int32_t s_tot[kGateMaxE];
   const int nthr = blockDim.x;
   const int chunks = (nthr < 512 ? nthr : 512) / E;
   const int per = (n_tiles + chunks - 1) / chunks;
@@ -297,8 +332,10 @@ __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ 
     for (int p = 0; p < world; ++p)
       reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + threadIdx.x] = total;
     ws[1 + threadIdx.x] = 0;  // ready for the next call (stream order)
+    s_tot[threadIdx.x] = total;
   }
   __syncthreads();
+  if (local.route_cum != nullptr && threadIdx.x == 0) write_local_tables(s_tot, E, local);
   if (active) {
     int32_t run = csum[threadIdx.x];
     for (int t = t0; t < t1; ++t) {
@@ -330,7 +367,7 @@ __global__ void __launch_bounds__(128 * KS)
                          int32_t* __restrict__ tile_counts, int32_t* __restrict__ tile_prefix,
                          int32_t* __restrict__ ws, const uint64_t* __restrict__ peer_bases,
                          int64_t table_off, int64_t flags_off, int rank, int world, int slot,
-                         uint32_t epoch) {
+                         uint32_t epoch, GateLocalTables local) {
   __shared__ float lg[kGateTile][kGateMaxE + 1];
   __shared__ float part[KS > 1 ? KS - 1 : 1][kGateTile][8 * NT + 1];
   __shared__ int32_t s_idx[kGateTile * kGateMaxK];
@@ -471,7 +508,7 @@ __global__ void __launch_bounds__(128 * KS)
   __syncthreads();
   if (!is_last) return;
   gate_route_tail(gridDim.x, E, tile_counts, tile_prefix, ws, peer_bases, table_off, flags_off,
-                  rank, world, slot, epoch);
+                  rank, world, slot, epoch, local);
 }
 
 __global__ void __launch_bounds__(kGateThreads)
@@ -1307,7 +1344,7 @@ static int gate_mma_launch(const __nv_bfloat16* x, const float* wg, const float*
                            int32_t* slot_rank, int32_t* tile_counts, int32_t* tile_prefix,
                            int32_t* ws, const uint64_t* peer_bases, int64_t table_off,
                            int64_t flags_off, int rank, int world, int slot, uint32_t epoch,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, GateLocalTables local = {}) {
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
   const bool split = d % 128 == 0;
   // staged split weights when they fit beside two CTAs per SM
@@ -1333,7 +1370,7 @@ static int gate_mma_launch(const __nv_bfloat16* x, const float* wg, const float*
     timing_begin(stream);
     kern<<<tiles, threads, dyn, stream>>>(x, wg, bias, T, d, E, k, logits, topk_idx, topk_w,
                                           slot_rank, tile_counts, tile_prefix, ws, peer_bases,
-                                          table_off, flags_off, rank, world, slot, epoch);
+                                          table_off, flags_off, rank, world, slot, epoch, local);
   };
 #define FSSDP_GATE_GO(KS, SW, THREADS)                              \
   do {                                                              \
@@ -1418,24 +1455,39 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
                      int32_t E, int32_t k, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
                      int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
                      const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
-                     int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch, void* stream) {
+                     int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
+                     int32_t* local_tables, void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
-      k > E || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world) {
-    set_error("gate_route: unsupported shape");
+      k > E || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world ||
+      (local_tables != nullptr && world != 1)) {
+    set_error("gate_route: unsupported shape (local tables need world == 1)");
     return kErrDimension;
   }
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
-  if (!gate_mma_ok(d, E) || tiles == 0) {  // the two-kernel path
+  GateLocalTables local = {};
+  if (local_tables != nullptr) {  // the fssdp_tables_layout sections of a (E, 1) blob
+    int64_t off[FSSDP_TAB_NSECTIONS], total = 0;
+    fssdp_tables_layout(E, 1, off, &total);
+    auto sec = [&](int i) {
+      return reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(local_tables) + off[i]);
+    };
+    local = {sec(FSSDP_TAB_ROUTE_CUM), sec(FSSDP_TAB_RECV_BASE), sec(FSSDP_TAB_ZERO_ROWS)};
+  }
+  if (!gate_mma_ok(d, E) || tiles == 0) {  // the two-kernel path (+ the local tables)
     int rc = fssdp_gate_topk(x, wg, bias, T, d, E, k, nullptr, topk_idx, topk_w, slot_rank,
                              tile_counts, stream);
     if (rc != kOk) return rc;
-    return fssdp_route_scan_allgather(tile_counts, tiles, E, tile_prefix, peer_bases, table_off,
-                                      flags_off, rank, world, bar_slot, epoch, stream);
+    rc = fssdp_route_scan_allgather(tile_counts, tiles, E, tile_prefix, peer_bases, table_off,
+                                    flags_off, rank, world, bar_slot, epoch, stream);
+    if (rc != kOk || local_tables == nullptr) return rc;
+    gate_local_tables_kernel<<<1, 32, 0, as_stream(stream)>>>(peer_bases, rank, table_off, E,
+                                                             local);
+    return launch_status();
   }
   const int rc = gate_mma_launch(static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k,
                                  nullptr, topk_idx, topk_w, slot_rank, tile_counts, tile_prefix,
                                  ws, peer_bases, table_off, flags_off, rank, world, bar_slot,
-                                 epoch, as_stream(stream));
+                                 epoch, as_stream(stream), local);
   if (rc != kOk) return rc;
   return launch_status();
 }

@@ -426,7 +426,8 @@ class FssdpMoE:
                    ops._ptr(self.topk_w), ops._ptr(self.slot_rank), ops._ptr(self.tile_counts),
                    ops._ptr(self.tile_prefix), ops._ptr(self.gate_ws), self._pb(),
                    self.off["counts"], self.flags_off, self.rank, self.world, slot, epoch,
-                   self._stream())
+                   C.c_void_p(self.blob_dev_ptr) if self.LOCAL_DISPATCH and self.world == 1
+                   else None, self._stream())
 
     def phase_counts(self) -> None:
         """The counts are all-gathered by the gate launch; the early SpAG may start now."""
@@ -437,11 +438,9 @@ class FssdpMoE:
     # ("counts"), or once the counts readback has left ("push")
     PREFETCH_AT = os.environ.get("FSSDP_PREFETCH_AT", "counts")
 
-    def phase_plan(self, dispatch: bool = False) -> None:
-        """Counts readback, host plan, table upload; with dispatch=True the dispatch is
-        launched right after the upload, before any Python bookkeeping of the plan."""
-        # host sync point #1: pinned copy of the all-gathered counts (raw cudaMemcpyAsync +
-        # stream sync: the torch copy/event path costs tens of microseconds here)
+    def _push_counts(self) -> None:
+        """Host boundary #1: the all-gathered counts to mapped pinned memory + a flag, by the
+        SMs (a copy-engine transfer would queue behind the caller's bulk copies)."""
         self._mark("readback")
         self._counts_epoch = (self._counts_epoch + 1) & 0xFFFFFFFF
         self._timed("push_host", lambda: N.check(N.LIB_RAW.fssdp_push_host(
@@ -449,6 +448,12 @@ class FssdpMoE:
             self._counts_epoch, self._stream()), "counts readback"))
         if self.PREFETCH_AT == "push":
             self._launch_prefetch()
+
+    def phase_plan(self, dispatch: bool = False, pushed: bool = False) -> None:
+        """Counts readback, host plan, table upload; with dispatch=True the dispatch is
+        launched right after the upload, before any Python bookkeeping of the plan."""
+        if not pushed:
+            self._push_counts()
         N.check(N.LIB_RAW.fssdp_host_wait(self.counts_flag_ptr, self._counts_epoch, 60.0),
                 "counts readback")
         t_host = time.perf_counter()
@@ -730,6 +735,10 @@ class FssdpMoE:
     # gap, from the end of the count all-gather to the start of the dispatch
     gap_events = None
 
+    # single rank: the gate writes the dispatch tables itself (the placement cannot change),
+    # so the dispatch runs while the host plans (FSSDP_LOCAL_DISPATCH=0 disables)
+    LOCAL_DISPATCH = os.environ.get("FSSDP_LOCAL_DISPATCH", "1") != "0"
+
     def _forward(self, x: torch.Tensor) -> torch.Tensor:
         self.phase_prefetch()
         self.phase_gate(x)
@@ -738,13 +747,18 @@ class FssdpMoE:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
             self.gap_events.append((e0, None))  # closed after the table upload
-        self.phase_plan(dispatch=True)
-        if not self._dispatched:
-            self.phase_dispatch()
-        self._finish_plan()
+        if self.LOCAL_DISPATCH and self.world == 1:
+            self._push_counts()
+            self.phase_dispatch(n_zero=self.g.num_experts)  # one {row, count} per expert
+            self.phase_plan(pushed=True)
+        else:
+            self.phase_plan(dispatch=True)
+            if not self._dispatched:
+                self.phase_dispatch()
         self._mark("dispatch_launched")
         self.phase_spag()  # only fwd1 reads the replicas: the dispatch overlaps the early SpAG
         self.phase_experts_fwd()
+        self._finish_plan()  # Python bookkeeping of the plan, once the GEMMs are queued
         self.phase_barrier(BAR_Y)
         return self.phase_combine()
 

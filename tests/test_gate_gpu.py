@@ -61,6 +61,7 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
     from paper_2502_02581_b200 import _native as N
     from paper_2502_02581_b200 import ops
     from paper_2502_02581_b200.comm import HeapLayout, emulated_group
+    from paper_2502_02581_b200.plan_tables import NativeTables, _layout
 
     g = torch.Generator().manual_seed(T + d)
     x = torch.randn(T, d, generator=g).bfloat16().cuda()
@@ -80,13 +81,29 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
     torch.cuda.synchronize()
     want = [t.cpu().clone() for t in (idx, w, rank, tc, prefix, table)]
     ws = torch.zeros(1 + E, dtype=torch.int32, device="cuda")
-    for _ in range(2):
+    offs, nbytes = _layout(E, 1)
+    blob = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    for local in (False, True):
         out = [torch.empty_like(t) for t in (idx, w, rank, tc, prefix)]
         table.zero_()
         N.call("fssdp_gate_route", ops._ptr(x), ops._ptr(wg), ops._ptr(bias), T, d, E, k,
-               *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0, s)
+               *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0,
+               ops._ptr(blob) if local else None, s)
         torch.cuda.synchronize()
         for a, b in zip(want, [t.cpu() for t in out] + [table.cpu()]):
             assert torch.equal(a, b)
         assert not ws.any()
     assert int(want[5].sum()) == T * k
+    # the single-rank dispatch tables the gate wrote == the host builder's for one device
+    counts = want[5].numpy().astype(np.int64)
+    host = NativeTables(0, np.zeros(E, np.int32), np.ones((E, 1), np.uint8), counts[None, :, None],
+                        256, 256)
+    dev = blob.cpu().numpy()
+
+    def sec(name, n):
+        return dev[offs[name]:offs[name] + 4 * n].view(np.int32)
+
+    assert np.array_equal(sec("route_cum", 2 * E).reshape(E, 2), host.route_cum)
+    assert np.array_equal(sec("recv_base", E).reshape(E, 1), host.recv_base)
+    zr = sec("zero_rows", 2 * E).reshape(E, 2)
+    assert np.array_equal(zr[zr[:, 1] > 0], host.zero_rows)
