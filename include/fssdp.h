@@ -375,12 +375,14 @@ int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int6
                const int32_t* copies, int32_t n_copies, void* stream);
 /* The same pull with separate heap offsets for the source slots (on src_rank) and the
  * destination slots (here) — re-sharding moves owned shards through a staging region —
- * and an optional bound on its footprint: max_ctas > 0 caps the grid (larger chunks per
- * CTA), for a copy that runs beside other kernels (the early SpAG of the planning gap:
- * small latency-bound transfers stall behind a full-width copy); 0 = full width. */
+ * copying copy_bytes (0 = slot_bytes) of each slot from its start (callers shift the
+ * offsets to copy a later part, e.g. W2 of [W1 | W2]), with an optional bound on its
+ * footprint: max_ctas > 0 caps the grid (larger chunks per CTA), for a copy that runs
+ * beside other kernels (the early SpAG of the planning gap: small latency-bound transfers
+ * stall behind a full-width copy); 0 = full width. */
 int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off, int64_t dst_off,
-                       int64_t slot_bytes, const int32_t* copies, int32_t n_copies,
-                       int32_t max_ctas, void* stream);
+                       int64_t slot_bytes, int64_t copy_bytes, const int32_t* copies,
+                       int32_t n_copies, int32_t max_ctas, void* stream);
 
 /* K8: SparseReduceScatter, owner side.  The holders' wgrads already pushed their partial
  * gradients into this rank's staging slots (c_dest groups); here, per job

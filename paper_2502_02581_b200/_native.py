@@ -115,7 +115,7 @@ _SIGS = {
     "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],
     "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
-    "fssdp_gather_slots": [vp, i32, i64, i64, i64, vp, i32, i32, vp],
+    "fssdp_gather_slots": [vp, i32, i64, i64, i64, i64, vp, i32, i32, vp],
     "fssdp_sprs": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
     "fssdp_sprs_pull": [vp, i32, i64, i64, vp, i32, vp, vp],
     # launch timing (measurement)

@@ -1085,17 +1085,17 @@ constexpr int kTmaSub = 8 * 1024;
 constexpr int kTmaRing = 4;  // 32 KB of static smem per CTA -> several CTAs per SM
 __global__ void __launch_bounds__(32)
     spag_tma_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t src_off,
-                    int64_t dst_off, int64_t slot_bytes, const int32_t* __restrict__ copies,
-                    int64_t chunk) {
+                    int64_t dst_off, int64_t slot_bytes, int64_t copy_bytes,
+                    const int32_t* __restrict__ copies, int64_t chunk) {
   __shared__ __align__(128) uint8_t ring[kTmaRing][kTmaSub];
   __shared__ __align__(8) uint64_t bar[kTmaRing];
   const int job = blockIdx.y;
   const int64_t begin = static_cast<int64_t>(blockIdx.x) * chunk;
-  if (begin >= slot_bytes || threadIdx.x != 0) return;
+  if (begin >= copy_bytes || threadIdx.x != 0) return;
   const int src_rank = copies[3 * job];
   const int64_t src_slot = copies[3 * job + 1];
   const int64_t dst_slot = copies[3 * job + 2];
-  const int64_t bytes = imin64(chunk, slot_bytes - begin);
+  const int64_t bytes = imin64(chunk, copy_bytes - begin);
   const char* src = reinterpret_cast<const char*>(peer_bases[src_rank] + src_off) +
                     src_slot * slot_bytes + begin;
   char* dst = reinterpret_cast<char*>(peer_bases[rank] + dst_off) + dst_slot * slot_bytes + begin;
@@ -1626,10 +1626,11 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
 }
 
 int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off, int64_t dst_off,
-                       int64_t slot_bytes, const int32_t* copies, int32_t n_copies,
-                       int32_t max_ctas, void* stream) {
-  if (slot_bytes % 16 != 0) {
-    set_error("gather_slots: slot_bytes must be a multiple of 16");
+                       int64_t slot_bytes, int64_t copy_bytes, const int32_t* copies,
+                       int32_t n_copies, int32_t max_ctas, void* stream) {
+  if (copy_bytes == 0) copy_bytes = slot_bytes;
+  if (slot_bytes % 16 != 0 || copy_bytes % 16 != 0 || copy_bytes < 0 || copy_bytes > slot_bytes) {
+    set_error("gather_slots: slot_bytes / copy_bytes must be multiples of 16, copy <= slot");
     return kErrDimension;
   }
   if (n_copies <= 0) return kOk;
@@ -1637,20 +1638,20 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
     const char* v = getenv("FSSDP_SPAG_IMPL");
     return (v && strcmp(v, "ldg") == 0) ? 0 : 1;  // default: TMA-staged bulk copies
   }();
-  if (impl == 1 || src_off != dst_off) {
-    int64_t chunk = slot_bytes * n_copies / (2 * static_cast<int64_t>(num_sms()));
+  if (impl == 1 || src_off != dst_off || copy_bytes != slot_bytes) {
+    int64_t chunk = copy_bytes * n_copies / (2 * static_cast<int64_t>(num_sms()));
     chunk = (chunk + kTmaSub - 1) / kTmaSub * kTmaSub;
     if (chunk < 4 * kTmaSub) chunk = 4 * kTmaSub;
     if (chunk > (1 << 20)) chunk = 1 << 20;
     // a bounded footprint (max_ctas > 0): a copy running beside other kernels must leave
     // them SM slots — small latency-bound transfers stall behind a full-width copy
-    while (max_ctas > 0 && chunk < slot_bytes &&
-           ((slot_bytes + chunk - 1) / chunk) * n_copies > max_ctas)
+    while (max_ctas > 0 && chunk < copy_bytes &&
+           ((copy_bytes + chunk - 1) / chunk) * n_copies > max_ctas)
       chunk *= 2;
-    dim3 grid(static_cast<unsigned>((slot_bytes + chunk - 1) / chunk), n_copies);
+    dim3 grid(static_cast<unsigned>((copy_bytes + chunk - 1) / chunk), n_copies);
     timing_begin(as_stream(stream));
     spag_tma_kernel<<<grid, 32, 0, as_stream(stream)>>>(peer_bases, rank, src_off, dst_off,
-                                                        slot_bytes, copies, chunk);
+                                                        slot_bytes, copy_bytes, copies, chunk);
     return launch_status();
   }
   const int64_t chunk = coll_chunk_bytes(slot_bytes * n_copies, num_sms());
@@ -1663,8 +1664,8 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
 
 int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int64_t slot_bytes,
                const int32_t* copies, int32_t n_copies, void* stream) {
-  return fssdp_gather_slots(peer_bases, rank, param_off, param_off, slot_bytes, copies, n_copies,
-                            0, stream);
+  return fssdp_gather_slots(peer_bases, rank, param_off, param_off, slot_bytes, 0, copies,
+                            n_copies, 0, stream);
 }
 
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,

@@ -224,7 +224,8 @@ class FssdpMoE:
         self.pre_mask = None      # (E, D) replicas fetched early this iteration, or None
         self.pre_mask_ptr = None
         self.pre_tables = None
-        self._pre_done = None     # event on the side stream after the early SpAG
+        self._pre_done = None     # event on the side stream after the early SpAG (W1 parts)
+        self._pre_w2 = None       # ... and after its W2 parts (fwd2 waits for it)
         self._pre_staged = None   # event after the H2D of pre_host (before it is rewritten)
         self.decision = None
         self.tables = None
@@ -346,6 +347,7 @@ class FssdpMoE:
 
     def phase_prefetch(self) -> None:
         self.pre_mask, self.pre_mask_ptr, self.pre_tables, self._pre_done = None, None, None, None
+        self._pre_w2 = None
         self._pre_launch = False
         if not self.PREFETCH:
             return
@@ -389,9 +391,16 @@ class FssdpMoE:
         side = self._side_stream()
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side)
+            # fwd1 reads only W1 (W13) of a replica: that part first, its own event, then
+            # W2 — which crosses NVLink while fwd1 runs (fwd2 waits for it)
+            n1b = self.g.n1 * self.g.d_model * 2
+            self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side, 0, n1b)
             self._pre_done = torch.cuda.Event()
             self._pre_done.record(side)
+            self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side, n1b,
+                              self.g.slot_param_bytes - n1b)
+            self._pre_w2 = torch.cuda.Event()
+            self._pre_w2.record(side)
 
     # the early SpAG runs beside the count readback, the host planning and the table upload:
     # a bounded grid (one CTA per SM by default, FSSDP_SPAG_PRE_CTAS; 0 = full width) keeps
@@ -399,15 +408,17 @@ class FssdpMoE:
     # ~20 us, the step from 1.874 to 1.844 ms; N=2 unchanged — profiles/r1_spag_pre_ctas.txt)
     SPAG_PRE_CTAS = int(os.environ.get("FSSDP_SPAG_PRE_CTAS", "-1"))
 
-    def _spag_launch(self, key, blob_dev, tables, stream) -> None:
+    def _spag_launch(self, key, blob_dev, tables, stream, part_off=0, part_bytes=0) -> None:
+        """SpAG copies of `tables`; part_off / part_bytes (0 = whole slot) select a part of
+        every slot (W1 or W2)."""
         spag = C.c_void_p(blob_dev.data_ptr() + tables.offsets["spag"])
-        off = self.off["params"]
+        off = self.off["params"] + part_off
         cap = 0
         if key == "spag_pre":
             cap = self.SPAG_PRE_CTAS if self.SPAG_PRE_CTAS >= 0 else N.LIB.fssdp_num_sms()
         self._timed(key, lambda: N.call(
             "fssdp_gather_slots", self._pb(), self.rank, off, off, self.g.slot_param_bytes,
-            spag, tables.n_spag, cap, C.c_void_p(stream.cuda_stream)))
+            part_bytes, spag, tables.n_spag, cap, C.c_void_p(stream.cuda_stream)))
 
     def phase_gate(self, x: torch.Tensor) -> None:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.g.d_model:
@@ -561,7 +572,7 @@ class FssdpMoE:
         self._reshard_pending = None
         self.phase_barrier(BAR_RESHARD)  # every old owner has staged its shards
         self._call("fssdp_gather_slots", self._pb(), self.rank, self.off["reshard"],
-                   self.off["params"], self.g.slot_param_bytes, ops._ptr(copies),
+                   self.off["params"], self.g.slot_param_bytes, 0, ops._ptr(copies),
                    copies.shape[0], 0, self._stream())
 
     def phase_dispatch(self, n_zero: int | None = None) -> None:
@@ -641,6 +652,9 @@ class FssdpMoE:
         f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1
         self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.gprime, n1, self.epi_fwd1,
                    c2=self.h)
+        if self._pre_w2 is not None:  # the early replicas' W2 parts
+            torch.cuda.current_stream(self.dev).wait_event(self._pre_w2)
+            self._pre_w2 = None
         self._gemm("fwd2", self.h, False, self.w2_view, False, self.y_e, d, ops.EPI_BF16)
 
     def phase_barrier(self, which: int) -> None:

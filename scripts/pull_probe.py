@@ -48,7 +48,7 @@ def main():
 
     def spag():
         with torch.cuda.stream(side):
-            N.call("fssdp_gather_slots", pb, rank, poff, poff, S, C.c_void_p(copies.data_ptr()),
+            N.call("fssdp_gather_slots", pb, rank, poff, poff, S, 0, C.c_void_p(copies.data_ptr()),
                    n_copies, 0, C.c_void_p(side.cuda_stream))
 
     transports = {
