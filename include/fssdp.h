@@ -336,20 +336,24 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
                    uint32_t* grid_counter, void* stream);
 
 /* K6: combine.  y[t] = sum_j w[t, j] * Y_{dest}[pos]  (fp32, j ascending) -> bf16.
- * Y rows are pulled from peer heaps (offset y_off). */
+ * Y rows are pulled from peer heaps (offset y_off).  y_slots (nullable, bf16 [T*k, d_model]):
+ * the gathered rows are also stored there in slot order, so the backward's <dy, Y> reads
+ * them from local HBM instead of pulling them over NVLink a second time. */
 int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float* topk_w,
                   int64_t T, int32_t d_model, int32_t k, const uint64_t* peer_bases, int64_t y_off,
-                  void* y_out, void* stream);
+                  void* y_out, void* y_slots, void* stream);
 
 /* K7 (token side of backward): for every slot, g[t, j] = <dy_t, Y_slot> (fp32) and
  * bf16(w[t, j] * dy_t) is pushed to the slot's destination dY receive buffer
- * (heap offset dy_recv_off).  Zeroes own padding rows, ends with a device barrier. */
+ * (heap offset dy_recv_off).  Y_slot comes from y_slots (the forward combine's copy) when
+ * non-null, else from the peer heaps (offset y_off).  Zeroes own padding rows, ends with a
+ * device barrier. */
 int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
                         const float* topk_w, int64_t T, int32_t d_model, int32_t k,
-                        const uint64_t* peer_bases, int64_t y_off, int64_t dy_recv_off,
-                        float* slot_grad, const int32_t* zero_rows, int32_t n_zero,
-                        int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
-                        uint32_t epoch, uint32_t* grid_counter, void* stream);
+                        const uint64_t* peer_bases, int64_t y_off, const void* y_slots,
+                        int64_t dy_recv_off, float* slot_grad, const int32_t* zero_rows,
+                        int32_t n_zero, int64_t flags_off, int32_t rank, int32_t world,
+                        int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter, void* stream);
 
 /* K7 (gate + combine side of backward):
  *   dlogit[t, j] = w_j (g_j - sum_i w_i g_i)            (renormalised top-k softmax)

@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(256)
     combine_kernel(const int32_t* __restrict__ slot_dest, const int32_t* __restrict__ slot_pos,
                    const float* __restrict__ topk_w, int64_t T, int d_model,
                    const uint64_t* __restrict__ peer_bases, int64_t y_off,
-                   __nv_bfloat16* __restrict__ y_out) {
+                   __nv_bfloat16* __restrict__ y_out, __nv_bfloat16* __restrict__ y_slots) {
   constexpr int TB = kTokBatch;  // tokens per warp batch (TB * K <= 32)
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -753,6 +753,9 @@ __global__ void __launch_bounds__(256)
         w[j] = __shfl_sync(0xffffffffu, sw, src);
       }
       int4* out = reinterpret_cast<int4*>(y_out + (base + i) * d_model);
+      // the K gathered rows, kept token-local for dispatch_grad's <dy, Y> (slot order)
+      int4* keep = y_slots == nullptr ? nullptr
+                                      : reinterpret_cast<int4*>(y_slots + (base + i) * K * d_model);
       for (int c0 = 0; c0 < n16; c0 += kRowBlk) {
         int4 v[K][4];
 #pragma unroll
@@ -762,6 +765,15 @@ __global__ void __launch_bounds__(256)
             const int c = c0 + lane + 32 * u;
             v[j][u] = c < n16 ? ld_nc_v4(rows[j] + c) : make_int4(0, 0, 0, 0);
           }
+        if (keep != nullptr) {
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int c = c0 + lane + 32 * u;
+              if (c < n16) st_v4(keep + j * n16 + c, v[j][u]);
+            }
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + lane + 32 * u;
@@ -788,7 +800,8 @@ __global__ void __launch_bounds__(256)
     dispatch_grad_kernel(const __nv_bfloat16* __restrict__ dy, const int32_t* __restrict__ slot_dest,
                          const int32_t* __restrict__ slot_pos, const float* __restrict__ topk_w,
                          int64_t T, int d_model, int k, const uint64_t* __restrict__ peer_bases,
-                         int64_t y_off, int64_t dy_recv_off, float* __restrict__ slot_grad,
+                         int64_t y_off, const __nv_bfloat16* __restrict__ y_slots,
+                         int64_t dy_recv_off, float* __restrict__ slot_grad,
                          const int32_t* __restrict__ zero_rows, int n_zero, int64_t flags_off,
                          int rank, int world, int bar_slot, uint32_t epoch,
                          uint32_t* grid_counter) {
@@ -815,8 +828,11 @@ __global__ void __launch_bounds__(256)
       const int dst = __shfl_sync(0xffffffffu, sd, i);
       const int64_t pos = __shfl_sync(0xffffffffu, sp, i);
       const float w = __shfl_sync(0xffffffffu, sw, i);
-      const int4* yrow = reinterpret_cast<const int4*>(
-          reinterpret_cast<const char*>(peer_bases[dst] + y_off) + pos * row_bytes);
+      const int4* yrow =
+          y_slots != nullptr
+              ? reinterpret_cast<const int4*>(y_slots + (base + i) * d_model)
+              : reinterpret_cast<const int4*>(
+                    reinterpret_cast<const char*>(peer_bases[dst] + y_off) + pos * row_bytes);
       const int4* grow = reinterpret_cast<const int4*>(dy + t * d_model);
       int4* out = reinterpret_cast<int4*>(reinterpret_cast<char*>(peer_bases[dst] + dy_recv_off) +
                                           pos * row_bytes);
@@ -1541,7 +1557,7 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
 
 int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float* topk_w, int64_t T,
                   int32_t d_model, int32_t k, const uint64_t* peer_bases, int64_t y_off,
-                  void* y_out, void* stream) {
+                  void* y_out, void* y_slots, void* stream) {
   if (d_model % 8 != 0 || k <= 0 || k > kGateMaxK) {
     set_error("combine: bad shape");
     return kErrDimension;
@@ -1550,16 +1566,17 @@ int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float
   const int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
   timing_begin(as_stream(stream));
   FSSDP_DISPATCH_K(k, combine_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_w, T,
-                   d_model, peer_bases, y_off, static_cast<__nv_bfloat16*>(y_out));
+                   d_model, peer_bases, y_off, static_cast<__nv_bfloat16*>(y_out),
+                   static_cast<__nv_bfloat16*>(y_slots));
   return launch_status();
 }
 
 int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
                         const float* topk_w, int64_t T, int32_t d_model, int32_t k,
-                        const uint64_t* peer_bases, int64_t y_off, int64_t dy_recv_off,
-                        float* slot_grad, const int32_t* zero_rows, int32_t n_zero,
-                        int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
-                        uint32_t epoch, uint32_t* grid_counter, void* stream) {
+                        const uint64_t* peer_bases, int64_t y_off, const void* y_slots,
+                        int64_t dy_recv_off, float* slot_grad, const int32_t* zero_rows,
+                        int32_t n_zero, int64_t flags_off, int32_t rank, int32_t world,
+                        int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter, void* stream) {
   if (d_model % 8 != 0 || world <= 0 || world > kMaxWorld || k > kGateMaxK) {
     set_error("dispatch_grad: bad shape");
     return kErrDimension;
@@ -1567,7 +1584,8 @@ int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t*
   timing_begin(as_stream(stream));
   dispatch_grad_kernel<<<grid_for_warps((T * k + kBatch - 1) / kBatch), 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(dy), slot_dest, slot_pos, topk_w, T, d_model, k,
-      peer_bases, y_off, dy_recv_off, slot_grad, zero_rows, n_zero, flags_off, rank, world,
+      peer_bases, y_off, static_cast<const __nv_bfloat16*>(y_slots), dy_recv_off, slot_grad,
+      zero_rows, n_zero, flags_off, rank, world,
       bar_slot, epoch, grid_counter);
   return launch_status();
 }

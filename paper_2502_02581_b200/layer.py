@@ -208,6 +208,10 @@ class FssdpMoE:
         self.slot_pos = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
         self.slot_grad = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
         self.dlogit = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
+        # token-local copy of the K gathered expert rows (combine -> dispatch_grad's <dy, Y>):
+        # the backward then pulls nothing over NVLink; one rank reads its own heap anyway
+        self.y_slots = (torch.empty(Tc * k, d, dtype=torch.bfloat16, device=self.dev)
+                        if self.world > 1 and self.KEEP_Y_SLOTS else None)
         wg_tiles = max(1, (Tc + WG_TILE - 1) // WG_TILE)
         self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
@@ -617,6 +621,7 @@ class FssdpMoE:
     # tile order per GEMM: N-fastest where the A operand (activations) is the big,
     # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
     N_FASTEST = {"fwd2": True, "dgrad1": True}
+    KEEP_Y_SLOTS = os.environ.get("FSSDP_KEEP_Y", "1") != "0"
     CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
 
     def _call(self, name, *args):
@@ -668,7 +673,7 @@ class FssdpMoE:
         y = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
         self._call("fssdp_combine", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
                ops._ptr(self.topk_w), self.T, self.g.d_model, self.g.top_k, self._pb(),
-               self.off["y"], ops._ptr(y), self._stream())
+               self.off["y"], ops._ptr(y), ops._ptr(self.y_slots), self._stream())
         return y
 
     # ------------------------------------------------------------ backward phases
@@ -680,7 +685,8 @@ class FssdpMoE:
         slot, epoch = self._bar(BAR_DGRAD)
         self._call("fssdp_dispatch_grad", ops._ptr(self.dy), ops._ptr(self.slot_dest),
                ops._ptr(self.slot_pos), ops._ptr(self.topk_w), self.T, self.g.d_model,
-               self.g.top_k, self._pb(), self.off["y"], self.off["dyrecv"],
+               self.g.top_k, self._pb(), self.off["y"], ops._ptr(self.y_slots),
+               self.off["dyrecv"],
                ops._ptr(self.slot_grad), self._tab("zero_rows"), t.n_zero,
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
