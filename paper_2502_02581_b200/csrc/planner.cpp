@@ -1255,7 +1255,9 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       }
       const int32_t st = static_cast<int32_t>(seg_start[rank][s]);
       const int32_t mt = static_cast<int32_t>(seg_pad[rank][s] / 128);
-      const int32_t kt = static_cast<int32_t>(seg_pad[rank][s] / 64);
+      // wgrad K = the segment's rows rounded up to one 64-row K block: the zero padding
+      // beyond it would only add exact zeros
+      const int32_t kt = static_cast<int32_t>((seg_rows[rank][s] + 63) / 64);
       fssdp_gemm_group& x = g[i];
       const int32_t w1r = static_cast<int32_t>(s * nm * f), w2r = static_cast<int32_t>(s * nm * d);
       switch (gi) {

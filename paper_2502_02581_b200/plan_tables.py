@@ -89,7 +89,7 @@ def n_tile_widths(d_ff: int, n_mats: int) -> tuple:
 
 
 def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None,
-                push=None, n_mats: int = 2):
+                push=None, n_mats: int = 2, seg_rows=None):
     """The six grouped-GEMM descriptor arrays of one rank (see gemm_sm100.cu).
 
     Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16 (GeLU, n_mats 2) or
@@ -103,12 +103,16 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     (n_shared, wgrad1_shared_tiles, wgrad2_shared_tiles).
 
     `push` (per segment: None, or (owner, staging index)): a replica's wgrad writes its
-    partial gradient into the owner's staging slot (c_dest = owner + 1) — the SpRS wire."""
+    partial gradient into the owner's staging slot (c_dest = owner + 1) — the SpRS wire.
+
+    `seg_rows` (real rows per segment): the wgrads' K stops at the first 64-row K block
+    boundary past them (the zero padding beyond would only add exact zeros)."""
     d, f, nm = d_model, d_ff, n_mats
     n1 = (nm - 1) * f
     bn1, bnf = n_tile_widths(f, nm)
     n = len(seg_start)
     shared = [False] * n if shared is None else [bool(x) for x in shared]
+    k_rows = seg_padded if seg_rows is None else (np.asarray(seg_rows, dtype=np.int64) + 63) // 64 * 64
     push = [None] * n if push is None else list(push)
     out = {}
     g = np.zeros(n, dtype=GROUP_DTYPE)
@@ -143,7 +147,7 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
             s = slot_of_seg[i]
             st = int(seg_start[i])
             dest, slot = (0, s) if push[i] is None else (push[i][0] + 1, push[i][1])
-            gw[j] = (rows // 128, 0, 0, st, 0, st, int(seg_padded[i] // 64), dest,
+            gw[j] = (rows // 128, 0, 0, st, 0, st, int(k_rows[i] // 64), dest,
                      slot * nm * f * d + extra)
         head, _, t_sh = _finalize(gw[:n_sh], n_t)
         tail, _, t_rest = _finalize(gw[n_sh:], n_t)
@@ -220,7 +224,8 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
     shared = [int(np.count_nonzero(target_mask[by_slot[s]])) > 1 for s in order]
     push = [None if int(base_owner[by_slot[s]]) == rank else
             (int(base_owner[by_slot[s]]), stage[(by_slot[s], rank)]) for s in order]
-    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared, push, n_mats)
+    groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared, push, n_mats,
+                                      seg_rows=rows)
     n_owned = sum(1 for e in slots if int(base_owner[e]) == rank)
     return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
                       seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),
