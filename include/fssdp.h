@@ -346,19 +346,23 @@ int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float
 /* K7 (token side of backward): for every slot, g[t, j] = <dy_t, Y_slot> (fp32) and
  * bf16(w[t, j] * dy_t) is pushed to the slot's destination dY receive buffer
  * (heap offset dy_recv_off).  Y_slot comes from y_slots (the forward combine's copy) when
- * non-null, else from the peer heaps (offset y_off).  Zeroes own padding rows, ends with a
- * device barrier. */
+ * non-null, else from the peer heaps (offset y_off).  dlogit_out (nullable, needs 4 % k == 0):
+ * the gate's dlogit [T*k] (as fssdp_combine_dx defines it) is written here too, so the gate
+ * backward can start before the dX combine.  Zeroes own padding rows, ends with a device
+ * barrier. */
 int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
                         const float* topk_w, int64_t T, int32_t d_model, int32_t k,
                         const uint64_t* peer_bases, int64_t y_off, const void* y_slots,
-                        int64_t dy_recv_off, float* slot_grad, const int32_t* zero_rows,
-                        int32_t n_zero, int64_t flags_off, int32_t rank, int32_t world,
-                        int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter, void* stream);
+                        int64_t dy_recv_off, float* slot_grad, float* dlogit_out,
+                        const int32_t* zero_rows, int32_t n_zero, int64_t flags_off,
+                        int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
+                        uint32_t* grid_counter, void* stream);
 
 /* K7 (gate + combine side of backward):
  *   dlogit[t, j] = w_j (g_j - sum_i w_i g_i)            (renormalised top-k softmax)
  *   dx[t] = sum_j dXe_{dest}[pos] + sum_j dlogit[t, j] * Wg[idx_j]     -> bf16
- * dXe rows are pulled from peer heaps (offset dxe_off).  dlogit_out [T*k] fp32. */
+ * dXe rows are pulled from peer heaps (offset dxe_off).  dlogit_out [T*k] fp32 (nullable:
+ * not written, e.g. when fssdp_dispatch_grad already wrote it). */
 int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const int32_t* topk_idx,
                      const float* topk_w, const float* slot_grad, const float* wg, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,

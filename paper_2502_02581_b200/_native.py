@@ -110,8 +110,8 @@ _SIGS = {
     "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
                        i64, i32, i32, u32, vp, vp],
     "fssdp_combine": [vp, vp, vp, i64, i32, i32, vp, i64, vp, vp, vp],
-    "fssdp_dispatch_grad": [vp, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp, vp, i32, i64,
-                            i32, i32, i32, u32, vp, vp],
+    "fssdp_dispatch_grad": [vp, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp, vp, vp, i32,
+                            i64, i32, i32, i32, u32, vp, vp],
     "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],
     "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],

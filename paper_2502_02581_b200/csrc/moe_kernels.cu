@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(256)
                          int64_t T, int d_model, int k, const uint64_t* __restrict__ peer_bases,
                          int64_t y_off, const __nv_bfloat16* __restrict__ y_slots,
                          int64_t dy_recv_off, float* __restrict__ slot_grad,
-                         const int32_t* __restrict__ zero_rows, int n_zero, int64_t flags_off,
+                         float* __restrict__ dlogit_out, const int32_t* __restrict__ zero_rows, int n_zero, int64_t flags_off,
                          int rank, int world, int bar_slot, uint32_t epoch,
                          uint32_t* grid_counter) {
   const int lane = threadIdx.x & 31;
@@ -865,6 +865,16 @@ __global__ void __launch_bounds__(256)
       if (lane == i) my_dot = dot;
     }
     if (lane < cnt) slot_grad[sl] = my_dot;
+    if (dlogit_out != nullptr) {
+      // whole tokens per batch (host guarantees kBatch % k == 0): the gate's dlogit here,
+      // in combine_dx's arithmetic, so the gate backward need not wait for the dX combine
+      const int first = (lane / k) * k;
+      float sg = 0.f;
+      for (int j = 0; j < k; ++j)
+        sg = fmaf(__shfl_sync(0xffffffffu, sw, (first + j) & 31),
+                  __shfl_sync(0xffffffffu, my_dot, (first + j) & 31), sg);
+      if (lane < cnt) dlogit_out[sl] = sw * (my_dot - sg);
+    }
   }
   warp_zero_rows(reinterpret_cast<char*>(peer_bases[rank] + dy_recv_off), zero_rows, n_zero,
                  row_bytes, warp_global, nwarps);
@@ -905,7 +915,7 @@ __global__ void __launch_bounds__(256)
       sg = fmaf(__shfl_sync(0xffffffffu, sw, (first + j) & 31),
                 __shfl_sync(0xffffffffu, sgr, (first + j) & 31), sg);
     const float dlv = sw * (sgr - sg);
-    if (own) dlogit_out[sl] = dlv;
+    if (own && dlogit_out != nullptr) dlogit_out[sl] = dlv;
     const int cnt = static_cast<int>(imin64(TB, T - base));
     for (int i = 0; i < cnt; ++i) {
       const int4* rows[K];
@@ -1574,10 +1584,12 @@ int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float
 int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
                         const float* topk_w, int64_t T, int32_t d_model, int32_t k,
                         const uint64_t* peer_bases, int64_t y_off, const void* y_slots,
-                        int64_t dy_recv_off, float* slot_grad, const int32_t* zero_rows,
-                        int32_t n_zero, int64_t flags_off, int32_t rank, int32_t world,
-                        int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter, void* stream) {
-  if (d_model % 8 != 0 || world <= 0 || world > kMaxWorld || k > kGateMaxK) {
+                        int64_t dy_recv_off, float* slot_grad, float* dlogit_out,
+                        const int32_t* zero_rows, int32_t n_zero, int64_t flags_off, int32_t rank,
+                        int32_t world, int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter,
+                        void* stream) {
+  if (d_model % 8 != 0 || world <= 0 || world > kMaxWorld || k <= 0 || k > kGateMaxK ||
+      (dlogit_out != nullptr && kBatch % k != 0)) {
     set_error("dispatch_grad: bad shape");
     return kErrDimension;
   }
@@ -1585,7 +1597,7 @@ int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t*
   dispatch_grad_kernel<<<grid_for_warps((T * k + kBatch - 1) / kBatch), 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(dy), slot_dest, slot_pos, topk_w, T, d_model, k,
       peer_bases, y_off, static_cast<const __nv_bfloat16*>(y_slots), dy_recv_off, slot_grad,
-      zero_rows, n_zero, flags_off, rank, world,
+      dlogit_out, zero_rows, n_zero, flags_off, rank, world,
       bar_slot, epoch, grid_counter);
   return launch_status();
 }

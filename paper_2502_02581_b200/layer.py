@@ -622,6 +622,14 @@ class FssdpMoE:
     # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
     N_FASTEST = {"fwd2": True, "dgrad1": True}
     KEEP_Y_SLOTS = os.environ.get("FSSDP_KEEP_Y", "1") != "0"
+    # dispatch_grad writes the gate's dlogit (whole tokens per 4-slot warp batch), so the
+    # gate backward runs on its own stream beside the expert GEMMs instead of after the
+    # dX combine at the end of the step
+    EARLY_GATE = os.environ.get("FSSDP_EARLY_GATE", "1") != "0"
+
+    @property
+    def _early_gate(self) -> bool:
+        return self.EARLY_GATE and 4 % self.g.top_k == 0
     CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
 
     def _call(self, name, *args):
@@ -687,7 +695,8 @@ class FssdpMoE:
                ops._ptr(self.slot_pos), ops._ptr(self.topk_w), self.T, self.g.d_model,
                self.g.top_k, self._pb(), self.off["y"], ops._ptr(self.y_slots),
                self.off["dyrecv"],
-               ops._ptr(self.slot_grad), self._tab("zero_rows"), t.n_zero,
+               ops._ptr(self.slot_grad), ops._ptr(self.dlogit if self._early_gate else None),
+               self._tab("zero_rows"), t.n_zero,
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
 
@@ -726,7 +735,8 @@ class FssdpMoE:
         self._call("fssdp_combine_dx", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
                ops._ptr(self.topk_idx), ops._ptr(self.topk_w), ops._ptr(self.slot_grad),
                ops._ptr(self.wg), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,
-               self._pb(), self.off["dxe"], ops._ptr(self.dlogit), ops._ptr(dx), self._stream())
+               self._pb(), self.off["dxe"], ops._ptr(None if self._early_gate else self.dlogit),
+               ops._ptr(dx), self._stream())
         return dx
 
     def phase_gate_wgrad(self) -> None:
@@ -791,6 +801,12 @@ class FssdpMoE:
 
     def _backward(self, dy: torch.Tensor, rematerialize: bool | None) -> torch.Tensor:
         self.phase_dispatch_grad(dy)
+        main = torch.cuda.current_stream(self.dev)
+        if self._early_gate:
+            gs = self._gate_stream()
+            gs.wait_stream(main)
+            with self._on(gs):
+                self.phase_gate_wgrad()
         remat = self.planner.policy.rematerialize if rematerialize is None else rematerialize
         if remat:
             self.phase_spag(refetch_early=True)
@@ -801,7 +817,6 @@ class FssdpMoE:
         # (disjoint buffers).  The decision is global (same plan on every rank), so every
         # rank joins the same barriers.
         replicas = self.decision.target != self.decision.base
-        main = torch.cuda.current_stream(self.dev)
         self.phase_bwd_shared()
         if replicas:
             side = self._side_stream()
@@ -816,9 +831,12 @@ class FssdpMoE:
         with self._on(dxs):
             self.phase_barrier(BAR_DX)
             self.phase_combine_dx(dx)
-            self.phase_gate_wgrad()
+            if not self._early_gate:
+                self.phase_gate_wgrad()
         self.phase_wgrad_rest()
         main.wait_stream(dxs)
+        if self._early_gate:
+            main.wait_stream(self._gate_stream())
         if replicas:
             main.wait_stream(side)
         self.phase_barrier(BAR_END)
@@ -839,6 +857,11 @@ class FssdpMoE:
         if getattr(self, "_dxs", None) is None:
             self._dxs = torch.cuda.Stream(device=self.dev)
         return self._dxs
+
+    def _gate_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_gs", None) is None:
+            self._gs = torch.cuda.Stream(device=self.dev)
+        return self._gs
 
     def _side_stream(self) -> torch.cuda.Stream:
         if getattr(self, "_side", None) is None:
