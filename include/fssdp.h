@@ -254,7 +254,8 @@ typedef struct fssdp_gemm_group {
  * (A: [K][M], B: [K][N]).  N (= n_tiles * 256) is shared by every group.
  * C (and C2 / aux) is a row-major [c_rows][ldc] tensor (bf16, or fp32 for
  * FSSDP_EPI_F32); a group's C origin is element c_off (a multiple of ldc).
- * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum.
+ * groups_dev: device array of num_groups descriptors; total_tiles must equal their sum,
+ * or -1: read on the device from the last group (tile_start + m_tiles * n_tiles).
  * c_dest_maps (nullable): device array of 128-byte tensor maps made by
  * fssdp_epilogue_tmap, the destinations of groups with c_dest > 0 — a wgrad pushes a
  * replica's partial gradient into its owner's staging slot over NVLink this way.
@@ -334,6 +335,15 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
                    int64_t recv_off, const int32_t* zero_rows, int32_t n_zero,
                    int64_t flags_off, int32_t rank, int32_t bar_slot, uint32_t epoch,
                    uint32_t* grid_counter, void* stream);
+
+/* Single rank (N = 1): the six grouped-GEMM tables of the fssdp_tables_layout(E, 1) blob at
+ * local_tables, written on the device from this rank's expert totals (the counts row at
+ * heap offset table_off, as fssdp_gate_route wrote it) — identical to what
+ * fssdp_build_rank_tables writes for one rank, so the forward GEMMs (launched with
+ * total_tiles = -1) need not wait for the host plan. */
+int fssdp_local_gemm_tables(const uint64_t* peer_bases, int32_t rank, int64_t table_off,
+                            int32_t E, int32_t d_model, int32_t d_ff, int32_t n_mats,
+                            void* local_tables, void* stream);
 
 /* K6: combine.  y[t] = sum_j w[t, j] * Y_{dest}[pos]  (fp32, j ascending) -> bf16.
  * Y rows are pulled from peer heaps (offset y_off).  y_slots (nullable, bf16 [T*k, d_model]):

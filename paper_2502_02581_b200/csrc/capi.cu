@@ -198,7 +198,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
                        int32_t total_tiles, void* c, void* c2, const void* aux,
                        const void* c_dest_maps, int64_t ldc, int64_t c_rows, int32_t flags,
                        void* stream) {
-  if (num_groups <= 0 || n_tiles <= 0 || total_tiles < 0 || c == nullptr || c_rows <= 0) {
+  if (num_groups <= 0 || n_tiles <= 0 || total_tiles < -1 || c == nullptr || c_rows <= 0) {
     set_error("grouped_gemm: bad arguments");
     return kErrDimension;
   }

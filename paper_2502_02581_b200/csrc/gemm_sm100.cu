@@ -243,7 +243,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const GemmGroup* __restrict__ groups = args.groups;
-  const int total = args.total_tiles / CG;
+  // total_tiles = -1: the tables were written on the device (fssdp_local_gemm_tables)
+  const int total =
+      (args.total_tiles >= 0
+           ? args.total_tiles
+           : args.groups[args.num_groups - 1].tile_start +
+                 args.groups[args.num_groups - 1].m_tiles * args.n_tiles) / CG;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -599,7 +604,8 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
       return kErrCuda;
     configured = true;
   }
-  const int units = args.total_tiles / CG;  // tiles of CG*128 rows
+  // tiles of CG*128 rows; a device-side total (-1) gets the full persistent grid
+  const int units = args.total_tiles >= 0 ? args.total_tiles / CG : num_sms();
   int grid = CG * (units < num_sms() / CG ? units : num_sms() / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -682,7 +688,7 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
                         int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                         int64_t c_rows, const GemmLaunch& args, cudaStream_t stream) {
   const int BN = args.bn == 128 ? 128 : 256;
-  if (args.total_tiles <= 0) return kOk;
+  if (args.total_tiles == 0) return kOk;
   if (args.ldc % 32 != 0) return kErrDimension;
   const int cg = args.cta_group == 2 ? 2 : 1;
   CUtensorMap ma, mb, mc, mx;

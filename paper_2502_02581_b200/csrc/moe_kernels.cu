@@ -300,6 +300,60 @@ __global__ void gate_local_tables_kernel(const uint64_t* peer_bases, int rank, i
                        E, local);
 }
 
+// Single rank, N = 1: the six grouped-GEMM descriptor tables of fssdp_build_rank_tables
+// (planner.cpp), written on the device from the gate's expert totals — every expert is an
+// owned slot (ascending), segments padded to 256 rows, no replica, no SpRS push; the wgrads
+// list the slots longest-first (stable), as the host builder does.  The forward GEMMs can
+// then be queued before the host plan exists (fssdp_grouped_gemm total_tiles = -1).
+__global__ void local_gemm_tables_kernel(const uint64_t* __restrict__ peer_bases, int rank,
+                                         int64_t table_off, int E, int64_t d, int64_t f, int nm,
+                                         fssdp_gemm_group* __restrict__ gemm0, int64_t stride) {
+  __shared__ int32_t s_start[kGateMaxE], s_pad[kGateMaxE], s_rows[kGateMaxE], s_order[kGateMaxE];
+  if (threadIdx.x == 0) {
+    const int32_t* tot = reinterpret_cast<const int32_t*>(peer_bases[rank] + table_off) + rank * E;
+    int32_t row = 0;
+    for (int e = 0; e < E; ++e) {
+      const int32_t c = __ldcg(tot + e), pad = (c + 255) / 256 * 256;
+      s_start[e] = row;
+      s_rows[e] = c;
+      s_pad[e] = pad;
+      row += pad;
+      int j = e;  // stable insertion by padded rows, descending
+      while (j > 0 && s_pad[s_order[j - 1]] < pad) {
+        s_order[j] = s_order[j - 1];
+        --j;
+      }
+      s_order[j] = e;
+    }
+  }
+  __syncthreads();
+  const int gi = threadIdx.x;
+  if (gi >= 6) return;
+  const int64_t n1 = (nm - 1) * f;
+  const int64_t bnf = f % 256 == 0 ? 256 : 128, bn1 = nm == 3 ? 256 : bnf;
+  const int64_t n_tiles[6] = {n1 / bn1, d / 256, f / bnf, d / 256, d / 256, f / bnf};
+  fssdp_gemm_group* g = reinterpret_cast<fssdp_gemm_group*>(
+      reinterpret_cast<uint8_t*>(gemm0) + gi * stride);
+  int32_t tile = 0;
+  for (int i = 0; i < E; ++i) {
+    const int s = gi >= 4 ? s_order[i] : i;
+    const int32_t st = s_start[s], mt = s_pad[s] / 128, kt = (s_rows[s] + 63) / 64;
+    const int32_t w1r = static_cast<int32_t>(s * nm * f), w2r = static_cast<int32_t>(s * nm * d);
+    fssdp_gemm_group x;
+    switch (gi) {
+      case 0: x = {mt, 0, st, 0, w1r, 0, static_cast<int32_t>(d / 64), 0, st * n1}; break;
+      case 1: x = {mt, 0, st, 0, w2r, 0, static_cast<int32_t>(f / 64), 0, st * d}; break;
+      case 2: x = {mt, 0, st, 0, 0, w2r, static_cast<int32_t>(d / 64), 0, st * n1}; break;
+      case 3: x = {mt, 0, st, 0, 0, w1r, static_cast<int32_t>(n1 / 64), 0, st * d}; break;
+      case 4: x = {static_cast<int32_t>(n1 / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d}; break;
+      default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d + n1 * d}; break;
+    }
+    x.tile_start = tile;
+    tile += x.m_tiles * static_cast<int32_t>(n_tiles[gi]);
+    g[i] = x;
+  }
+}
+
 __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ tile_counts,
                                 int32_t* __restrict__ tile_prefix, int32_t* __restrict__ ws,
                                 const uint64_t* __restrict__ peer_bases, int64_t table_off,
@@ -1562,6 +1616,24 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
       static_cast<const __nv_bfloat16*>(x), topk_idx, slot_rank, tile_prefix, T, d_model, E, k,
       world, route_cum, recv_base, slot_dest, slot_pos, peer_bases, recv_off, zero_rows, n_zero,
       flags_off, rank, bar_slot, epoch, grid_counter);
+  return launch_status();
+}
+
+int fssdp_local_gemm_tables(const uint64_t* peer_bases, int32_t rank, int64_t table_off,
+                            int32_t E, int32_t d_model, int32_t d_ff, int32_t n_mats,
+                            void* local_tables, void* stream) {
+  if (E <= 0 || E > kGateMaxE || d_model % 256 != 0 || d_ff % 128 != 0 || n_mats < 2 ||
+      n_mats > 3 || local_tables == nullptr) {
+    set_error("local_gemm_tables: unsupported shape");
+    return kErrDimension;
+  }
+  int64_t off[FSSDP_TAB_NSECTIONS], total = 0;
+  fssdp_tables_layout(E, 1, off, &total);
+  uint8_t* blob = static_cast<uint8_t*>(local_tables);
+  local_gemm_tables_kernel<<<1, 32, 0, as_stream(stream)>>>(
+      peer_bases, rank, table_off, E, d_model, d_ff, n_mats,
+      reinterpret_cast<fssdp_gemm_group*>(blob + off[FSSDP_TAB_GEMM0]),
+      off[FSSDP_TAB_GEMM0 + 1] - off[FSSDP_TAB_GEMM0]);
   return launch_status();
 }
 

@@ -191,6 +191,7 @@ class FssdpMoE:
               "wgrad2": bnf}
         pair = {k: self.CTA_PAIR for k in bn}
         pair["wgrad1"] = self.CTA_PAIR and (n1 // 128) % 2 == 0
+        self._bn = bn
         self._gemm_flags = {k: (ops.GEMM_BN128 if bn[k] == 128 else 0) |
                                (ops.GEMM_CTA_PAIR if pair[k] else 0) for k in bn}
         Tc = geom.max_tokens
@@ -353,6 +354,7 @@ class FssdpMoE:
         self.pre_mask, self.pre_mask_ptr, self.pre_tables, self._pre_done = None, None, None, None
         self._pre_w2 = None
         self._pre_launch = False
+        self._pre_w2_pending = False
         if not self.PREFETCH:
             return
         if self._base_owner is not None and not np.array_equal(
@@ -401,6 +403,24 @@ class FssdpMoE:
             self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side, 0, n1b)
             self._pre_done = torch.cuda.Event()
             self._pre_done.record(side)
+        self._pre_w2_pending = True
+        if not self.PRE_W2_AFTER_DISPATCH:
+            self._launch_prefetch_w2()
+
+    # experiment (off): start the early SpAG's W2 part once the dispatch is done.  The
+    # dispatch then has NVLink to itself (N=4: 105 -> 48 us) but the step is not faster
+    # (1.792 vs 1.800 ms, interleaved A/B): W2 then lands during fwd1, which it slows
+    PRE_W2_AFTER_DISPATCH = os.environ.get("FSSDP_PRE_W2_AFTER_DISPATCH", "0") == "1"
+
+    def _launch_prefetch_w2(self) -> None:
+        if not getattr(self, "_pre_w2_pending", False):
+            return
+        self._pre_w2_pending = False
+        side = self._side_stream()
+        if self.PRE_W2_AFTER_DISPATCH:
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            n1b = self.g.n1 * self.g.d_model * 2
             self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side, n1b,
                               self.g.slot_param_bytes - n1b)
             self._pre_w2 = torch.cuda.Event()
@@ -663,6 +683,7 @@ class FssdpMoE:
 
     def phase_experts_fwd(self) -> None:
         f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1
+        self._launch_prefetch_w2()  # after the dispatch (and any late SpAG) in stream order
         self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.gprime, n1, self.epi_fwd1,
                    c2=self.h)
         if self._pre_w2 is not None:  # the early replicas' W2 parts
@@ -768,6 +789,11 @@ class FssdpMoE:
     # single rank: the gate writes the dispatch tables itself (the placement cannot change),
     # so the dispatch runs while the host plans (FSSDP_LOCAL_DISPATCH=0 disables)
     LOCAL_DISPATCH = os.environ.get("FSSDP_LOCAL_DISPATCH", "1") != "0"
+    # experiment (off): the gate's totals also give the forward GEMM tables on the device
+    # (fssdp_local_gemm_tables), so fwd1/fwd2 are queued before the host plan.  Device time
+    # is unchanged (1.5094 vs 1.5072 ms, interleaved A/B) — the host plan already finishes
+    # while the dispatch runs — and e2e loses 3 % (its copies are issued after the plan)
+    LOCAL_GEMM_TABLES = os.environ.get("FSSDP_LOCAL_GEMM", "0") == "1"
 
     def _forward(self, x: torch.Tensor) -> torch.Tensor:
         self.phase_prefetch()
@@ -777,17 +803,31 @@ class FssdpMoE:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
             self.gap_events.append((e0, None))  # closed after the table upload
+        fwd_queued = False
         if self.LOCAL_DISPATCH and self.world == 1:
             self._push_counts()
             self.phase_dispatch(n_zero=self.g.num_experts)  # one {row, count} per expert
+            if self.LOCAL_GEMM_TABLES:
+                # the GEMM tables too come from the device: the forward GEMMs are queued
+                # before the host plan (which then overlaps them instead of preceding them)
+                self._call("fssdp_local_gemm_tables", self._pb(), self.rank, self.off["counts"],
+                           self.g.num_experts, self.g.d_model, self.g.d_ff, self.g.n_mats,
+                           C.c_void_p(self.blob_dev_ptr), self._stream())
+                E = self.g.num_experts
+                self.gemm = dict(getattr(self, "gemm", None) or {})
+                self.gemm["fwd1"] = (E, self.g.n1 // self._bn["fwd1"], -1)
+                self.gemm["fwd2"] = (E, self.g.d_model // 256, -1)
+                self.phase_experts_fwd()
+                fwd_queued = True
             self.phase_plan(pushed=True)
         else:
             self.phase_plan(dispatch=True)
             if not self._dispatched:
                 self.phase_dispatch()
         self._mark("dispatch_launched")
-        self.phase_spag()  # only fwd1 reads the replicas: the dispatch overlaps the early SpAG
-        self.phase_experts_fwd()
+        if not fwd_queued:
+            self.phase_spag()  # only fwd1 reads the replicas: the dispatch overlaps the early SpAG
+            self.phase_experts_fwd()
         self._finish_plan()  # Python bookkeeping of the plan, once the GEMMs are queued
         self.phase_barrier(BAR_Y)
         return self.phase_combine()

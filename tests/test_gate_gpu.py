@@ -107,3 +107,16 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
     assert np.array_equal(sec("recv_base", E).reshape(E, 1), host.recv_base)
     zr = sec("zero_rows", 2 * E).reshape(E, 2)
     assert np.array_equal(zr[zr[:, 1] > 0], host.zero_rows)
+    # ... and the six grouped-GEMM tables fssdp_local_gemm_tables writes from those totals
+    # == the host builder's, byte for byte (the forward GEMMs run on them before the plan)
+    for dm, dff, nm in ((1024, 4096, 2), (2048, 1408, 3), (256, 1024, 2)):
+        blob.zero_()
+        N.call("fssdp_local_gemm_tables", pb, 0, off, E, dm, dff, nm, ops._ptr(blob), s)
+        torch.cuda.synchronize()
+        dev = blob.cpu().numpy()
+        host = NativeTables(0, np.zeros(E, np.int32), np.ones((E, 1), np.uint8),
+                            counts[None, :, None], dm, dff, n_mats=nm)
+        for name in ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2"):
+            want_g = host.groups(name)
+            got = dev[offs[name]:offs[name] + want_g.nbytes]
+            assert got.tobytes() == want_g.tobytes(), (name, dm, dff, nm)
