@@ -330,8 +330,8 @@ __global__ void local_gemm_tables_kernel(const uint64_t* __restrict__ peer_bases
   const int gi = threadIdx.x;
   if (gi >= 6) return;
   const int64_t n1 = (nm - 1) * f;
-  const int64_t bnf = f % 256 == 0 ? 256 : 128, bn1 = nm == 3 ? 256 : bnf;
-  const int64_t n_tiles[6] = {n1 / bn1, d / 256, f / bnf, d / 256, d / 256, f / bnf};
+  const int64_t bnf = f % 256 == 0 ? 256 : 128, bn1 = nm == 3 ? 256 : bnf, nf = (f + 255) / 256;
+  const int64_t n_tiles[6] = {n1 / bn1, d / 256, nf, d / 256, d / 256, nf};
   fssdp_gemm_group* g = reinterpret_cast<fssdp_gemm_group*>(
       reinterpret_cast<uint8_t*>(gemm0) + gi * stride);
   int32_t tile = 0;

@@ -1237,10 +1237,13 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
   // n1 = fwd1's N.  N tiles of width f use 128 columns when f % 256 != 0; SwiGLU's fwd1
   // always uses 256 (an a1|a3 block pair per tile)
   const int64_t d = d_model, f = d_ff, nm = n_mats, n1 = (nm - 1) * f;
+  // dgrad2 / wgrad2 (N = f, B read N-contiguous): 256-wide tiles, the last one ragged (TMA
+  // zero-fills B past f and clips the stores) — plan_tables.n_tile_widths
   const int64_t bnf = f % 256 == 0 ? 256 : 128, bn1 = nm == 3 ? 256 : bnf;
+  const int64_t nf = (f + 255) / 256;
   const int n_tiles[6] = {static_cast<int>(n1 / bn1), static_cast<int>(d / 256),
-                          static_cast<int>(f / bnf), static_cast<int>(d / 256),
-                          static_cast<int>(d / 256), static_cast<int>(f / bnf)};
+                          static_cast<int>(nf), static_cast<int>(d / 256),
+                          static_cast<int>(d / 256), static_cast<int>(nf)};
   int ints = 7;
   int32_t shared_tiles[2] = {0, 0};
   for (int gi = 0; gi < 6; ++gi) {

@@ -82,10 +82,18 @@ def _finalize(groups: np.ndarray, n_tiles: int):
 
 
 def n_tile_widths(d_ff: int, n_mats: int) -> tuple:
-    """(N tile of fwd1, N tile of the GEMMs whose N = d_ff): 128 when d_ff % 256 != 0;
-    SwiGLU's fwd1 always 256 (an a1|a3 block pair per tile) — fssdp_gemm_group docs."""
+    """(N tile of fwd1, N tile of dgrad2 / wgrad2, whose N = d_ff).  fwd1: 128 when
+    d_ff % 256 != 0 (its B rows past d_ff belong to the next matrix); SwiGLU's fwd1 always
+    256 (an a1|a3 block pair per tile) — fssdp_gemm_group docs.  dgrad2 / wgrad2 read B
+    N-contiguous (MN-major, inner extent d_ff): always 256-wide, the last tile ragged — TMA
+    zero-fills its B columns past d_ff and clips its stores there (cfg4's 1408 = 5.5 x 256)."""
     bnf = 256 if d_ff % 256 == 0 else 128
-    return (256 if n_mats == 3 else bnf), bnf
+    return (256 if n_mats == 3 else bnf), 256
+
+
+def n_tiles_f(d_ff: int) -> int:
+    """N tiles of dgrad2 / wgrad2 (256 wide, the last one ragged)."""
+    return (d_ff + 255) // 256
 
 
 def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None,
@@ -130,7 +138,7 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
         s = slot_of_seg[i]
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * d, d // 64, 0, st * n1)
-    out["dgrad2"] = _finalize(g.copy(), f // bnf)
+    out["dgrad2"] = _finalize(g.copy(), n_tiles_f(f))
     for i in range(n):  # dXe = dA . W1  (B = W1 / W13 [K=n1][N=d], MN-major)
         s = slot_of_seg[i]
         st = int(seg_start[i])
@@ -141,7 +149,7 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
              sorted([i for i in range(n) if not shared[i]], key=lambda i: -int(seg_padded[i])))
     n_sh = sum(shared)
     split = [n_sh]
-    for name, rows, n_t, extra in (("wgrad1", n1, d // 256, 0), ("wgrad2", d, f // bnf, n1 * d)):
+    for name, rows, n_t, extra in (("wgrad1", n1, d // 256, 0), ("wgrad2", d, n_tiles_f(f), n1 * d)):
         gw = np.zeros(n, dtype=GROUP_DTYPE)
         for j, i in enumerate(order):  # dW1 = dA^T X, dW2 = dY^T H (K = the segment's tokens)
             s = slot_of_seg[i]
