@@ -642,14 +642,15 @@ class FssdpMoE:
     # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
     N_FASTEST = {"fwd2": True, "dgrad1": True}
     KEEP_Y_SLOTS = os.environ.get("FSSDP_KEEP_Y", "1") != "0"
-    # dispatch_grad writes the gate's dlogit (whole tokens per 4-slot warp batch), so the
-    # gate backward runs on its own stream beside the expert GEMMs instead of after the
-    # dX combine at the end of the step
+    # N > 1: dispatch_grad writes the gate's dlogit (whole tokens per 4-slot warp batch), so
+    # the gate backward runs on its own stream beside the expert GEMMs instead of after the
+    # dX combine at the end of the step (N=4: 1.816 -> 1.805 ms).  One rank keeps it beside
+    # the last wgrads (interleaved A/B at N=1: 0.3-0.5 % faster there, cfg2 and cfg4)
     EARLY_GATE = os.environ.get("FSSDP_EARLY_GATE", "1") != "0"
 
     @property
     def _early_gate(self) -> bool:
-        return self.EARLY_GATE and 4 % self.g.top_k == 0
+        return self.EARLY_GATE and 4 % self.g.top_k == 0 and self.world > 1
     CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
 
     def _call(self, name, *args):
