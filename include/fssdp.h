@@ -213,6 +213,40 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
                             double* doubles_out, int32_t* flags_out, uint8_t* blob,
                             int64_t blob_bytes, int32_t* header_out, void* blob_dev, void* stream);
 
+/* Arguments of the dispatch fssdp_plan_layer_dispatch launches (fssdp_dispatch's, minus the
+ * three plan-table pointers, n_zero and the stream, which come from the plan call). */
+typedef struct fssdp_dispatch_launch {
+  const void* x;
+  const int32_t* topk_idx;
+  const int32_t* slot_rank;
+  const int32_t* tile_prefix;
+  int64_t T;
+  int32_t d_model, E, k, world;
+  int32_t* slot_dest;
+  int32_t* slot_pos;
+  const uint64_t* peer_bases;
+  int64_t recv_off;
+  int64_t flags_off;
+  int32_t rank, bar_slot;
+  uint32_t epoch;
+  uint32_t* grid_counter;
+} fssdp_dispatch_launch;
+
+/* The whole planning critical path of one layer-iteration with no Python in it: wait for
+ * the counts readback flag (fssdp_host_wait), fssdp_plan_layer_tables, then — if disp and
+ * blob_dev — fssdp_dispatch on the uploaded tables (route_cum / recv_base / zero_rows
+ * sections of blob_dev, n_zero = header_out[3]) on the same stream. */
+int fssdp_plan_layer_dispatch(const uint32_t* counts_flag, uint32_t counts_epoch,
+                              double timeout_s, int32_t num_experts, const int32_t* base_owner,
+                              const double* est, const int32_t* counts,
+                              const fssdp_topology* topo, const fssdp_layer_knobs* knobs,
+                              int32_t rank, const uint8_t* pre_mask, int32_t d_model,
+                              int32_t d_ff, int32_t n_mats, const int64_t* limits,
+                              uint8_t* target_out, int32_t* added_out, int64_t* route_out,
+                              double* doubles_out, int32_t* flags_out, uint8_t* blob,
+                              int64_t blob_bytes, int32_t* header_out, void* blob_dev,
+                              void* stream, const fssdp_dispatch_launch* disp);
+
 /* The estimate-based, adoption-gated materialization alone (engine.py:497-501 with
  * _adopt_materialization engine.py:406-429): depends only on the load history, so its
  * SparseAllGather can start before the gate.  fssdp_plan_layer's final target is either

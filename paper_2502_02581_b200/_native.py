@@ -67,6 +67,18 @@ class GemmGroup(C.Structure):
 
 P_topo = C.POINTER(Topology)
 
+
+class DispatchLaunch(C.Structure):
+    """fssdp_dispatch_launch (include/fssdp.h)."""
+    _fields_ = [
+        ("x", C.c_void_p), ("topk_idx", C.c_void_p), ("slot_rank", C.c_void_p),
+        ("tile_prefix", C.c_void_p), ("T", C.c_int64), ("d_model", C.c_int32),
+        ("E", C.c_int32), ("k", C.c_int32), ("world", C.c_int32), ("slot_dest", C.c_void_p),
+        ("slot_pos", C.c_void_p), ("peer_bases", C.c_void_p), ("recv_off", C.c_int64),
+        ("flags_off", C.c_int64), ("rank", C.c_int32), ("bar_slot", C.c_int32),
+        ("epoch", C.c_uint32), ("grid_counter", C.c_void_p),
+    ]
+
 # name -> argtypes (every function returns int status unless listed in _RESTYPE)
 _SIGS = {
     "fssdp_version": [],
@@ -97,6 +109,10 @@ _SIGS = {
     "fssdp_plan_layer_tables": [i32, P_i32, P_f64, P_i32, P_topo, C.POINTER(LayerKnobs), i32,
                                 P_u8, i32, i32, i32, P_i64, P_u8, P_i32, P_i64, P_f64, P_i32, vp,
                                 i64, P_i32, vp, vp],
+    "fssdp_plan_layer_dispatch": [vp, u32, f64, i32, P_i32, P_f64, P_i32, P_topo,
+                                  C.POINTER(LayerKnobs), i32, P_u8, i32, i32, i32, P_i64, P_u8,
+                                  P_i32, P_i64, P_f64, P_i32, vp, i64, P_i32, vp, vp,
+                                  C.POINTER(DispatchLaunch)],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
                            vp, vp, i64, i64, i32, vp],
@@ -184,6 +200,7 @@ def check(status: int, what: str) -> None:
 KERNELS_PER_CALL = {
     "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
     "fssdp_route_scan_allgather": 1, "fssdp_gate_route": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1, "fssdp_local_gemm_tables": 1,
+    "fssdp_plan_layer_dispatch": 2,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
     "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
     "fssdp_gather_slots": 1,

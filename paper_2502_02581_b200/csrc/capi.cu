@@ -191,6 +191,36 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
   return fssdp_pull_host(blob_dev, blob, (total + 15) / 16 * 16, stream);
 }
 
+int fssdp_plan_layer_dispatch(const uint32_t* counts_flag, uint32_t counts_epoch,
+                              double timeout_s, int32_t num_experts, const int32_t* base_owner,
+                              const double* est, const int32_t* counts,
+                              const fssdp_topology* topo, const fssdp_layer_knobs* knobs,
+                              int32_t rank, const uint8_t* pre_mask, int32_t d_model,
+                              int32_t d_ff, int32_t n_mats, const int64_t* limits,
+                              uint8_t* target_out, int32_t* added_out, int64_t* route_out,
+                              double* doubles_out, int32_t* flags_out, uint8_t* blob,
+                              int64_t blob_bytes, int32_t* header_out, void* blob_dev,
+                              void* stream, const fssdp_dispatch_launch* disp) {
+  int rc = fssdp_host_wait(counts_flag, counts_epoch, timeout_s);
+  if (rc != kOk) return rc;
+  rc = fssdp_plan_layer_tables(num_experts, base_owner, est, counts, topo, knobs, rank, pre_mask,
+                               d_model, d_ff, n_mats, limits, target_out, added_out, route_out,
+                               doubles_out, flags_out, blob, blob_bytes, header_out, blob_dev,
+                               stream);
+  if (rc != kOk || disp == nullptr || blob_dev == nullptr) return rc;
+  const int32_t D = topo->nodes * topo->devices_per_node;
+  int64_t offs[FSSDP_TAB_NSECTIONS], total = 0;
+  fssdp_tables_layout(num_experts, D, offs, &total);
+  uint8_t* dev = static_cast<uint8_t*>(blob_dev);
+  auto sec = [&](int i) { return reinterpret_cast<int32_t*>(dev + offs[i]); };
+  return fssdp_dispatch(disp->x, disp->topk_idx, disp->slot_rank, disp->tile_prefix, disp->T,
+                        disp->d_model, disp->E, disp->k, disp->world, sec(FSSDP_TAB_ROUTE_CUM),
+                        sec(FSSDP_TAB_RECV_BASE), disp->slot_dest, disp->slot_pos,
+                        disp->peer_bases, disp->recv_off, sec(FSSDP_TAB_ZERO_ROWS),
+                        header_out[3], disp->flags_off, disp->rank, disp->bar_slot, disp->epoch,
+                        disp->grid_counter, stream);
+}
+
 
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,

@@ -342,24 +342,38 @@ class FssdpPlanner:
         the planning critical path (fssdp_plan_layer_tables).  `counts` is the (D, E) int32
         host array at counts_ptr.  decide=False defers the LayerDecision to
         last_decision(layer) (callable until this layer is planned again)."""
+        args = self.plan_call_args(layer, counts.shape, counts_ptr, rank, pre_ptr, d_model, d_ff,
+                                   blob, blob_ptr, header_ptr, blob_dev_ptr, stream, limits_ptr,
+                                   n_mats)
+        self.plan_counts(layer, counts)
+        N.check(N.LIB_RAW.fssdp_plan_layer_tables(*args), "plan_layer_tables")
+        return self.last_decision(layer) if decide else None
+
+    def plan_call_args(self, layer: int, counts_shape, counts_ptr: int, rank: int, pre_ptr,
+                       d_model: int, d_ff: int, blob, blob_ptr: int, header_ptr: int,
+                       blob_dev_ptr, stream, limits_ptr=None, n_mats: int = 2) -> tuple:
+        """The fssdp_plan_layer_tables argument list of this layer's plan — everything that
+        does not need the counts, so it can be built before they arrive.  Call
+        plan_counts(layer, counts) once the counts are in."""
         if self._step is None:
             self.begin_iteration()
             self._step = [None] * self.config.layers
         base = self.shards.per_layer[layer]
         E, D = base.num_chunks, base.num_devices
-        if counts.shape != (D, E):
-            raise TraceMismatchError(f"counts {counts.shape} do not match {D} devices x {E} experts")
-        self._step[layer] = counts.astype(np.int64)
+        if tuple(counts_shape) != (D, E):
+            raise TraceMismatchError(f"counts {tuple(counts_shape)} do not match {D} devices x {E} experts")
         sc = self._scratch(layer)
         knobs, est_ptr = self._layer_knobs(layer)
-        N.check(N.LIB_RAW.fssdp_plan_layer_tables(
-            E, self._owners_ptr(layer), est_ptr, counts_ptr, sc.topo_ref(self._topo_c),
-            N.C.byref(knobs), rank, pre_ptr, d_model, d_ff, n_mats, limits_ptr, sc.p_target,
-            sc.p_added,
-            sc.p_route, sc.p_dbl, sc.p_flags, blob_ptr, len(blob), header_ptr, blob_dev_ptr,
-            stream), "plan_layer_tables")
+        self._knobs_keep = knobs  # alive until the native call has read it
         self.last_target_ptr, self.last_route_ptr = sc.p_target, sc.p_route
-        return self._decision(base, sc) if decide else None
+        return (E, self._owners_ptr(layer), est_ptr, counts_ptr, sc.topo_ref(self._topo_c),
+                N.C.byref(knobs), rank, pre_ptr, d_model, d_ff, n_mats, limits_ptr, sc.p_target,
+                sc.p_added, sc.p_route, sc.p_dbl, sc.p_flags, blob_ptr, len(blob), header_ptr,
+                blob_dev_ptr, stream)
+
+    def plan_counts(self, layer: int, counts) -> None:
+        """Record this iteration's (D, E) counts of `layer` (history push at the end)."""
+        self._step[layer] = np.asarray(counts).astype(np.int64)
 
     def last_decision(self, layer: int) -> LayerDecision:
         """The LayerDecision of the layer's most recent plan_with_tables(decide=False)."""

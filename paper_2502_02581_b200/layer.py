@@ -497,6 +497,47 @@ class FssdpMoE:
         if self.timers is not None:
             self.timers.setdefault("host_plan_s", []).append(time.perf_counter() - t_host)
 
+    # N > 1: counts wait, plan, tables, upload and the dispatch launch in ONE native call
+    # with its arguments built before the counts arrive (no Python on the critical path).
+    # The instrumented passes (phase timers, gap probe) keep the separate calls.
+    FUSED_PLAN = os.environ.get("FSSDP_FUSED_PLAN", "1") != "0"
+
+    def _fused_plan_ok(self) -> bool:
+        return (self.FUSED_PLAN and self.timers is None and self.gap_events is None and
+                self.planner.policy.reshard_interval == 0 and self._reshard_pending is None)
+
+    def phase_plan_dispatch(self) -> None:
+        self._push_counts()
+        E, D = self.g.num_experts, self.world
+        args = self.planner.plan_call_args(
+            self.layer, (D, E), self.counts_host_ptr, self.rank, self.pre_mask_ptr,
+            self.g.d_model, self.g.d_ff, self.blob_host_np, self.blob_host_ptr,
+            NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
+            self.g.n_mats)
+        dl = self._dispatch_launch
+        if dl is None:
+            dl = self._dispatch_launch = N.DispatchLaunch(
+                0, self.topk_idx.data_ptr(), self.slot_rank.data_ptr(),
+                self.tile_prefix.data_ptr(), 0, self.g.d_model, E, self.g.top_k, self.world,
+                self.slot_dest.data_ptr(), self.slot_pos.data_ptr(), self.group.peer_bases.data_ptr(),
+                self.off["xrecv"], self.flags_off, self.rank, 0, 0, self.grid_counter.data_ptr())
+        dl.x = self.x.data_ptr()
+        dl.T = self.T
+        dl.bar_slot, dl.epoch = self._bar(BAR_DISPATCH)
+        N.check(N.LIB_RAW.fssdp_plan_layer_dispatch(
+            self.counts_flag_ptr, self._counts_epoch, 60.0, *args, C.byref(dl)),
+            "plan_layer_dispatch")
+        N.launch_count += N.KERNELS_PER_CALL["fssdp_plan_layer_dispatch"]
+        self._mark("dispatch_issued")
+        self.planner.plan_counts(self.layer, self.counts_host_np)
+        self._dispatched = True
+        tables = NativeTables.from_header(E, D, self.blob_host_np)
+        self.tables = self.packed = tables
+        self.gemm = tables.gemm
+        self._plan_pending = True
+
+    _dispatch_launch = None
+
     def _plan_tables(self, counts, dispatch: bool = False) -> None:
         # plan + this rank's tables + their upload (boundary #2), capacity-checked: one native
         # call; the Python-side decision object is built after the dispatch is launched
@@ -821,6 +862,8 @@ class FssdpMoE:
                 self.phase_experts_fwd()
                 fwd_queued = True
             self.phase_plan(pushed=True)
+        elif self._fused_plan_ok():
+            self.phase_plan_dispatch()
         else:
             self.phase_plan(dispatch=True)
             if not self._dispatched:
