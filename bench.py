@@ -272,10 +272,23 @@ def cpu_oracle_rate(sample_tokens: int, budget_s: float):
                                            "threads": OracleWorkload.threads()}
 
 
+_THREAD_LIMITS = None
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # every host core (torchrun sets OMP_NUM_THREADS=1 for each rank; the BLAS pool of the
+    # numpy port is raised back here)
+    global _THREAD_LIMITS
+    try:
+        import numpy  # noqa: F401  (the BLAS library must be loaded to be re-limited)
+        from threadpoolctl import threadpool_limits
+
+        _THREAD_LIMITS = threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:
+        pass
     sample = cpu_sample_tokens(2048)
     wl = OracleWorkload(sample)
     for _ in range(args.warmup):
