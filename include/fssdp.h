@@ -213,6 +213,10 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
                             double* doubles_out, int32_t* flags_out, uint8_t* blob,
                             int64_t blob_bytes, int32_t* header_out, void* blob_dev, void* stream);
 
+/* A copy-engine transfer (cudaMemcpyAsync, any pair of local / peer-heap addresses): moves
+ * bytes over NVLink without occupying SMs, e.g. replica parts that land beside a GEMM. */
+int fssdp_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Arguments of the dispatch fssdp_plan_layer_dispatch launches (fssdp_dispatch's, minus the
  * three plan-table pointers, n_zero and the stream, which come from the plan call). */
 typedef struct fssdp_dispatch_launch {

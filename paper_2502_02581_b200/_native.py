@@ -109,6 +109,7 @@ _SIGS = {
     "fssdp_plan_layer_tables": [i32, P_i32, P_f64, P_i32, P_topo, C.POINTER(LayerKnobs), i32,
                                 P_u8, i32, i32, i32, P_i64, P_u8, P_i32, P_i64, P_f64, P_i32, vp,
                                 i64, P_i32, vp, vp],
+    "fssdp_copy_async": [vp, vp, i64, vp],
     "fssdp_plan_layer_dispatch": [vp, u32, f64, i32, P_i32, P_f64, P_i32, P_topo,
                                   C.POINTER(LayerKnobs), i32, P_u8, i32, i32, i32, P_i64, P_u8,
                                   P_i32, P_i64, P_f64, P_i32, vp, i64, P_i32, vp, vp,

@@ -191,6 +191,18 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
   return fssdp_pull_host(blob_dev, blob, (total + 15) / 16 * 16, stream);
 }
 
+int fssdp_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (dst == nullptr || src == nullptr))) {
+    set_error("copy_async: bad arguments");
+    return kErrDimension;
+  }
+  if (bytes == 0) return kOk;
+  return cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
+                         static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? kOk
+             : kErrCuda;
+}
+
 int fssdp_plan_layer_dispatch(const uint32_t* counts_flag, uint32_t counts_epoch,
                               double timeout_s, int32_t num_experts, const int32_t* base_owner,
                               const double* est, const int32_t* counts,

@@ -404,7 +404,7 @@ class FssdpMoE:
             self._pre_done = torch.cuda.Event()
             self._pre_done.record(side)
         self._pre_w2_pending = True
-        if not self.PRE_W2_AFTER_DISPATCH:
+        if not (self.PRE_W2_AFTER_DISPATCH or self.PRE_W2_CE):
             self._launch_prefetch_w2()
 
     # experiment (off): start the early SpAG's W2 part once the dispatch is done.  The
@@ -412,10 +412,35 @@ class FssdpMoE:
     # (1.792 vs 1.800 ms, interleaved A/B): W2 then lands during fwd1, which it slows
     PRE_W2_AFTER_DISPATCH = os.environ.get("FSSDP_PRE_W2_AFTER_DISPATCH", "0") == "1"
 
+    # the early SpAG's W2 parts by the copy engines, once the dispatch is done: they cross
+    # NVLink beside fwd1 without taking its SMs (an SM copy kernel cannot co-reside with the
+    # GEMM's 227 KB CTAs and delays them), and the dispatch has NVLink to itself
+    # (N=4, interleaved A/B: dispatch 103 -> 48 us, step 1.799 -> 1.756 ms)
+    PRE_W2_CE = os.environ.get("FSSDP_PRE_W2_CE", "1") != "0"
+
+    def _launch_prefetch_w2_ce(self) -> None:
+        ce = getattr(self, "_ce", None)
+        if ce is None:
+            ce = self._ce = torch.cuda.Stream(device=self.dev)
+        ce.wait_stream(torch.cuda.current_stream(self.dev))
+        n1b = self.g.n1 * self.g.d_model * 2
+        sb = self.g.slot_param_bytes
+        off = self.off["params"] + n1b
+        bases = self.group.bases
+        s = C.c_void_p(ce.cuda_stream)
+        for src_rank, src_slot, dst_slot in self.pre_tables.spag_copies.tolist():
+            N.call_raw("fssdp_copy_async", C.c_void_p(bases[self.rank] + off + dst_slot * sb),
+                       C.c_void_p(bases[src_rank] + off + src_slot * sb), sb - n1b, s)
+        self._pre_w2 = torch.cuda.Event()
+        self._pre_w2.record(ce)
+
     def _launch_prefetch_w2(self) -> None:
         if not getattr(self, "_pre_w2_pending", False):
             return
         self._pre_w2_pending = False
+        if self.PRE_W2_CE:
+            self._launch_prefetch_w2_ce()
+            return
         side = self._side_stream()
         if self.PRE_W2_AFTER_DISPATCH:
             side.wait_stream(torch.cuda.current_stream(self.dev))
