@@ -384,7 +384,7 @@ class FssdpMoE:
             self._pre_staged = torch.cuda.Event()
             self._pre_staged.record(side)
         self._pre_launch = True  # the copies themselves start at PREFETCH_AT
-        if self.PREFETCH_AT == "gate":
+        if self.PREFETCH_AT == "gate" or self.PRE_W1_CE:
             self._launch_prefetch()
 
     def _launch_prefetch(self) -> None:
@@ -393,6 +393,20 @@ class FssdpMoE:
         if not getattr(self, "_pre_launch", False):
             return
         self._pre_launch = False
+        if self.PRE_W1_CE:
+            self._pre_done = self._ce_copies(0, self.g.n1 * self.g.d_model * 2)
+        else:
+            self._launch_prefetch_w1()
+        self._pre_w2_pending = True
+        if not (self.PRE_W2_AFTER_DISPATCH or self.PRE_W2_CE):
+            self._launch_prefetch_w2()
+
+    # the early SpAG's W1 parts by the copy engines too, started with the gate (an SM copy
+    # kernel there slowed the gate; the copy engines take no SMs) — N=4, interleaved A/B:
+    # 1.794 -> 1.787 ms.  FSSDP_PRE_W1_CE=0: the bounded-grid SM kernel at PREFETCH_AT
+    PRE_W1_CE = os.environ.get("FSSDP_PRE_W1_CE", "1") != "0"
+
+    def _launch_prefetch_w1(self) -> None:
         main = torch.cuda.current_stream(self.dev)
         side = self._side_stream()
         side.wait_stream(main)
@@ -403,9 +417,6 @@ class FssdpMoE:
             self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, side, 0, n1b)
             self._pre_done = torch.cuda.Event()
             self._pre_done.record(side)
-        self._pre_w2_pending = True
-        if not (self.PRE_W2_AFTER_DISPATCH or self.PRE_W2_CE):
-            self._launch_prefetch_w2()
 
     # experiment (off): start the early SpAG's W2 part once the dispatch is done.  The
     # dispatch then has NVLink to itself (N=4: 105 -> 48 us) but the step is not faster
@@ -419,20 +430,26 @@ class FssdpMoE:
     PRE_W2_CE = os.environ.get("FSSDP_PRE_W2_CE", "1") != "0"
 
     def _launch_prefetch_w2_ce(self) -> None:
+        n1b = self.g.n1 * self.g.d_model * 2
+        self._pre_w2 = self._ce_copies(n1b, self.g.slot_param_bytes - n1b)
+
+    def _ce_copies(self, part_off: int, part_bytes: int) -> torch.cuda.Event:
+        """The early SpAG's copies of one part of every slot, by the copy engines on their
+        own stream (after the current stream's work); returns their completion event."""
         ce = getattr(self, "_ce", None)
         if ce is None:
             ce = self._ce = torch.cuda.Stream(device=self.dev)
         ce.wait_stream(torch.cuda.current_stream(self.dev))
-        n1b = self.g.n1 * self.g.d_model * 2
         sb = self.g.slot_param_bytes
-        off = self.off["params"] + n1b
+        off = self.off["params"] + part_off
         bases = self.group.bases
         s = C.c_void_p(ce.cuda_stream)
         for src_rank, src_slot, dst_slot in self.pre_tables.spag_copies.tolist():
             N.call_raw("fssdp_copy_async", C.c_void_p(bases[self.rank] + off + dst_slot * sb),
-                       C.c_void_p(bases[src_rank] + off + src_slot * sb), sb - n1b, s)
-        self._pre_w2 = torch.cuda.Event()
-        self._pre_w2.record(ce)
+                       C.c_void_p(bases[src_rank] + off + src_slot * sb), part_bytes, s)
+        ev = torch.cuda.Event()
+        ev.record(ce)
+        return ev
 
     def _launch_prefetch_w2(self) -> None:
         if not getattr(self, "_pre_w2_pending", False):
