@@ -543,7 +543,11 @@ def run_ours(args):
             "nvlink_peer_gbs_ref": NVLINK_PEER_GBS,
             "a2a": a2a_stats(dec, allp, keys, world),
             "note": "SpRS wire is fp32 partials pushed by the wgrad epilogue's TMA stores "
-                    "(2x the reference's expert_bytes pricing); sprs_ms is the local reduce"}
+                    "(2x the reference's expert_bytes pricing); sprs_ms is the local reduce. "
+                    "The early SpAG runs on the copy engines in two windows (W1 parts with the "
+                    "gate, W2 parts beside fwd1 — sharing NVLink with the dispatch / GEMM "
+                    "traffic); spag_ms sums both windows. Standalone SpAG / SpRS kernel "
+                    "bandwidth: profiles/r1_sparse_sweep.txt"}
 
     # end to end through the public API with host buffers: inputs are copied H2D on a copy
     # stream one step ahead (double buffered), dx is copied D2H behind the compute.

@@ -444,9 +444,16 @@ class FssdpMoE:
         off = self.off["params"] + part_off
         bases = self.group.bases
         s = C.c_void_p(ce.cuda_stream)
-        for src_rank, src_slot, dst_slot in self.pre_tables.spag_copies.tolist():
+        copies = self.pre_tables.spag_copies.tolist()
+        if self.timers is not None and copies:  # bench: the copies' window on their stream
+            t0, t1 = N.NativeEvent(), N.NativeEvent()
+            t0.record(ce)
+        for src_rank, src_slot, dst_slot in copies:
             N.call_raw("fssdp_copy_async", C.c_void_p(bases[self.rank] + off + dst_slot * sb),
                        C.c_void_p(bases[src_rank] + off + src_slot * sb), part_bytes, s)
+        if self.timers is not None and copies:
+            t1.record(ce)
+            self.timers.setdefault("spag_pre", []).append((t0, t1))
         ev = torch.cuda.Event()
         ev.record(ce)
         return ev
