@@ -89,6 +89,7 @@ __device__ __forceinline__ void grid_done_then_barrier(uint32_t* grid_counter,
 
 __global__ void barrier_kernel(const uint64_t* peer_bases, int64_t flags_off, int rank, int world,
                                int slot, uint32_t epoch) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched with PDL (launch_pdl)
   __threadfence_system();
   world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
 }
@@ -778,6 +779,8 @@ __global__ void __launch_bounds__(256)
                    const float* __restrict__ topk_w, int64_t T, int d_model,
                    const uint64_t* __restrict__ peer_bases, int64_t y_off,
                    __nv_bfloat16* __restrict__ y_out, __nv_bfloat16* __restrict__ y_slots) {
+  // launched with PDL (launch_pdl): scheduled during the producing GEMM tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int TB = kTokBatch;  // tokens per warp batch (TB * K <= 32)
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -942,6 +945,8 @@ __global__ void __launch_bounds__(256)
                       const float* __restrict__ slot_grad, const float* __restrict__ wg, int64_t T,
                       int d_model, const uint64_t* __restrict__ peer_bases, int64_t dxe_off,
                       float* __restrict__ dlogit_out, __nv_bfloat16* __restrict__ dx_out) {
+  // launched with PDL (launch_pdl): scheduled during the producing GEMM tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int TB = kTokBatch;
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1393,16 +1398,40 @@ static int launch_status() {
 }
 
 // K-templated launch for the token gathers (K = top-k <= kGateMaxK = 8)
-#define FSSDP_DISPATCH_K(k, KERNEL, GRID, STREAM, ...)               \
-  switch (k) {                                                        \
-    case 1: KERNEL<1><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    case 2: KERNEL<2><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    case 3: KERNEL<3><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    case 4: KERNEL<4><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    case 5: KERNEL<5><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    case 6: KERNEL<6><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    case 7: KERNEL<7><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;  \
-    default: KERNEL<8><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break; \
+// Programmatic dependent launch (FSSDP_TOKEN_PDL, default on; "0" disables): the kernel may
+// be scheduled while the previous kernel in the stream drains (the grouped GEMM triggers
+// launch_dependents after its mainloop); every kernel launched this way executes
+// griddepcontrol.wait before its first global-memory access, so ordering is unchanged.
+template <typename... P, typename... A>
+static void launch_pdl(void (*kern)(P...), unsigned grid, unsigned block, cudaStream_t stream,
+                       A&&... args) {
+  static const bool pdl = [] {
+    const char* v = getenv("FSSDP_TOKEN_PDL");
+    return v == nullptr || v[0] != '0';
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<P>(args)...);
+}
+
+#define FSSDP_DISPATCH_K(k, KERNEL, GRID, STREAM, ...)                    \
+  switch (k) {                                                             \
+    case 1: launch_pdl(KERNEL<1>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    case 2: launch_pdl(KERNEL<2>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    case 3: launch_pdl(KERNEL<3>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    case 4: launch_pdl(KERNEL<4>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    case 5: launch_pdl(KERNEL<5>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    case 6: launch_pdl(KERNEL<6>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    case 7: launch_pdl(KERNEL<7>, GRID, 256, STREAM, __VA_ARGS__); break;  \
+    default: launch_pdl(KERNEL<8>, GRID, 256, STREAM, __VA_ARGS__); break; \
   }
 
 static int grid_for_warps(int64_t work_items) {
@@ -1594,8 +1623,8 @@ int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, i
     return kErrDimension;
   }
   timing_begin(as_stream(stream));
-  barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(peer_bases, flags_off, rank, world, bar_slot,
-                                                   epoch);
+  launch_pdl(barrier_kernel, 1, 32, as_stream(stream), peer_bases, flags_off, rank, world,
+             bar_slot, epoch);
   return launch_status();
 }
 
