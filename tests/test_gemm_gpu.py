@@ -415,3 +415,73 @@ def test_bn128_wgrad_fp32():
         ref = At[k0:k0 + s_].float().T @ Bt[k0:k0 + s_].float()
         _close(C[g * M:(g + 1) * M], ref, rel=2e-3, abs_=1e-4)
         k0 += s_
+
+
+@pytest.mark.parametrize("K,N,b_mn,pair", [(4096, 1024, False, True), (4096, 1024, True, True),
+                                           (14336, 4096, False, True), (14336, 512, True, False),
+                                           (2048, 1408, False, True)])
+def test_long_k_against_fp32(K, N, b_mn, pair):
+    """The BASELINE contraction lengths: K = d_ff 4096 (cfg2 fwd2 / dgrad1), 14 336 (cfg3),
+    2048 (cfg4 d_model) with a ragged N = 1408 — bf16 out within one bf16 ulp of the fp32
+    product (|Δ| <= 2^-7·|ref| + 1e-3·max|ref|)."""
+    ops = _ops()
+    dev = "cuda"
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.manual_seed(K + N)
+    m_tiles = [2, 4]
+    R = sum(m_tiles) * 128
+    G = len(m_tiles)
+    A = torch.randn(R, K, device=dev).bfloat16()
+    B = ((torch.randn(G * K, N, device=dev) if b_mn else torch.randn(G * N, K, device=dev))
+         / K ** 0.5).bfloat16()
+    C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    bn = 128 if N % 256 else 256
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, 0 if b_mn else g * N, g * K if b_mn else 0, K // 64, r0 * N))
+        r0 += mt * 128
+    n_tiles = -(-N // bn)
+    gd, ng, total = _groups(ops, rows, n_tiles, dev)
+    ops.grouped_gemm(A, False, B, b_mn, gd, ng, n_tiles, total, C, N, cta_pair=pair,
+                     bn128=bn == 128)
+    torch.cuda.synchronize()
+    r0 = 0
+    for g, mt in enumerate(m_tiles):
+        sl = slice(r0, r0 + mt * 128)
+        b = B[g * K:(g + 1) * K].float() if b_mn else B[g * N:(g + 1) * N].float().T
+        ref = A[sl].float() @ b
+        err = (C[sl].float() - ref).abs()
+        bound = 2.0 ** -7 * ref.abs() + 1e-3 * ref.abs().max()
+        assert (err <= bound).all(), f"max excess {(err - bound).max().item():.3g}"
+        r0 += mt * 128
+
+
+@pytest.mark.parametrize("segs,pair", [([16384, 4096], True), ([24576], True),
+                                       ([11264, 0, 5120], False)])
+def test_wgrad_long_token_k(segs, pair):
+    """wgrad with the token axis as K at bench scale (cfg2's hottest expert holds ~11k
+    rows; 24 576 = a whole rank's worth at N = 1): fp32 out vs the fp32 product,
+    accumulation order only (1e-4·max|ref|: both sides sum ~24k fp32 products)."""
+    ops = _ops()
+    dev = "cuda"
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.manual_seed(sum(segs))
+    M, N = 1024, 512
+    G = len(segs)
+    Rt = sum(segs)
+    At = torch.randn(Rt, M, device=dev).bfloat16()
+    Bt = torch.randn(Rt, N, device=dev).bfloat16()
+    C = torch.full((G * M, N), 9.0, device=dev)
+    rows, k0 = [], 0
+    for g, s_ in enumerate(segs):
+        rows.append((M // 128, 0, k0, 0, k0, s_ // 64, g * M * N))
+        k0 += s_
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    ops.grouped_gemm(At, True, Bt, True, gd, ng, N // 256, total, C, N, epilogue=ops.EPI_F32,
+                     cta_pair=pair)
+    torch.cuda.synchronize()
+    k0 = 0
+    for g, s_ in enumerate(segs):
+        ref = At[k0:k0 + s_].float().T @ Bt[k0:k0 + s_].float()
+        _close(C[g * M:(g + 1) * M], ref, rel=1e-4, abs_=0.0 if s_ else 1e-30)
+        k0 += s_

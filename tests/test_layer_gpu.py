@@ -88,10 +88,10 @@ def test_single_rank_matches_oracle(f, activation):
     close(f32(dx), ref["dx"], what="dx")
     for e in range(E):
         grads = ly.expert_grad(e)
-        close(f32(grads[0]), ref["dW1"][e], abs_=1e-5, what=f"dW1[{e}]")
-        close(f32(grads[-1]), ref["dW2"][e], abs_=1e-5, what=f"dW2[{e}]")
+        close(f32(grads[0]), ref["dW1"][e], rel=1e-2, abs_=1e-5, what=f"dW1[{e}]")
+        close(f32(grads[-1]), ref["dW2"][e], rel=1e-2, abs_=1e-5, what=f"dW2[{e}]")
         if activation == "swiglu":
-            close(f32(grads[1]), ref["dW3"][e], abs_=1e-5, what=f"dW3[{e}]")
+            close(f32(grads[1]), ref["dW3"][e], rel=1e-2, abs_=1e-5, what=f"dW3[{e}]")
     close(ly.dwg.cpu().numpy(), ref["dWg"], rel=1e-3, abs_=1e-5, what="dWg")
     # padding rows of the receive buffers are zero (wgrad K blocks rely on it)
     t = ly.tables

@@ -1,0 +1,273 @@
+"""Parity at the exact BASELINE.json shapes (configs[1..3]) — the workloads bench.py measures.
+
+cfg2 (the metric's line): E=16, top-2, d_model 1024, d_ff 4096 GeLU, 16 384 tokens/GPU,
+Zipf(1.2) gate, FSSDP t=8 / m=4.  cfg4: E=64, d_model 2048, d_ff 1408 SwiGLU, 16 384
+tokens, Zipf(1.2), re-materialization on.  cfg3: Mixtral-shaped E=8, d_model 4096, d_ff
+14 336 SwiGLU at full width (2048 tokens: the GEMMs' K and N are the real ones, only the
+token count is cut so the fp32 checker stays fast).
+
+Three kinds of checks, all on the second iteration (history-driven planning active):
+
+1. token-side kernels BIT-EXACT: dispatch rows (x_recv[pos] == x), combine
+   (y == bf16(w0·Y0 + w1·Y1) in fp32), dispatch_grad (dy_recv[pos] == bf16(w·dy)), zeroed
+   padding rows;
+2. every GEMM stage against ONE fp32 contraction of the device's own inputs
+   (tests/_torch_ref.py stage_*): bf16 outputs within 1 bf16 ulp of the fp32 result
+   (|Δ| <= 2^-7·|ref| + ABS_STAGE·max|ref|, the small absolute term absorbs tanh.approx /
+   __expf near zero crossings); fp32 weight gradients within STAGE_F32 = 1e-4·max|ref|
+   (accumulation order only; K up to 16 384 token rows);
+3. the whole layer against the independent torch mirror of the oracle's rounding points
+   (E2E_* bounds, max-norm relative) and against plain fp32 (no bf16 intermediates):
+   the bf16 drift of the product path, bounded by DRIFT_*.
+
+Set FSSDP_PARITY_LOG=<path> to append the measured errors as JSON lines.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_02581_b200 as F
+from paper_2502_02581_b200.comm import HeapLayout, emulated_group
+from paper_2502_02581_b200.layer import (FssdpMoE, LayerGeometry, default_slots,
+                                         run_lockstep_backward, run_lockstep_forward)
+
+from _torch_ref import bf16, layer as ref_layer, rel_err, stage_dgrad2, stage_fwd1
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "cfg2": dict(E=16, d=1024, f=4096, T=16384, act="gelu", zipf=1.2, t=8, m=4, remat=False),
+    "cfg4": dict(E=64, d=2048, f=1408, T=16384, act="swiglu", zipf=1.2, t=16, m=4, remat=True),
+    "cfg3": dict(E=8, d=4096, f=14336, T=2048, act="swiglu", zipf=1.0, t=2, m=1, remat=False),
+}
+
+ULP = 2.0 ** -7          # one bf16 ulp, relative (8 significant bits)
+ABS_STAGE = 2e-3         # absolute floor of the bf16 stage checks, x max|ref|
+STAGE_F32 = 1e-4         # fp32 wgrad vs fp32 contraction of the same bf16 inputs
+E2E_Y, E2E_DX, E2E_DW = 1.5e-2, 1e-2, 1e-2  # device vs rounding-point mirror (max-norm rel)
+DRIFT = 3e-2             # device vs plain fp32 (max-norm rel): the bf16 drift bound
+
+
+def _log(rec):
+    path = os.environ.get("FSSDP_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(rec) + "\n")
+
+
+def zipf_bias(E, s, seed):
+    p = 1.0 / np.arange(1, E + 1) ** s
+    p = p[np.random.default_rng(seed).permutation(E)]
+    return torch.tensor(np.log(p / p.sum()), dtype=torch.float32, device="cuda")
+
+
+def build(world, c, policy, T, seed=1):
+    m = policy.capacity_override if policy.capacity_override is not None else c["E"]
+    geom = LayerGeometry(c["d"], c["f"], c["E"], 2, T, world, default_slots(c["E"], world, m),
+                         c["act"])
+    layout = HeapLayout()
+    geom.add_regions(layout, "L0.")
+    groups = emulated_group(layout, world)
+    topo = F.ClusterTopology.for_nvswitch(world)
+    cfg = F.ModelConfig(1, c["E"], geom.expert_bytes, 2 * c["d"], 1e-3,
+                        2.0 * geom.n_mats * c["d"] * c["f"] / 1381.7e12)
+    bias = zipf_bias(c["E"], c["zipf"], 5)
+    layers = []
+    for r in range(world):
+        ly = FssdpMoE(geom, groups[r], F.FssdpPlanner(cfg, topo, policy), 0, seed)
+        ly.gate_bias.copy_(bias)
+        layers.append(ly)
+    return layers
+
+
+def _inputs(c, it, T):
+    g = torch.Generator(device="cuda").manual_seed(100 + it)
+    x = torch.randn(T, c["d"], device="cuda", generator=g).bfloat16()
+    dy = (torch.randn(T, c["d"], device="cuda", generator=g) * 0.05).bfloat16()
+    return x, dy
+
+
+@pytest.fixture(scope="module", params=sorted(CASES))
+def run(request):
+    """Two iterations of one rank at the config's full shape; keeps the second."""
+    name = request.param
+    c = CASES[name]
+    torch.backends.cuda.matmul.allow_tf32 = False
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=c["t"], capacity_override=c["m"],
+                   rematerialize=c["remat"])
+    (ly,) = build(1, c, pol, c["T"])
+    for it in range(2):
+        x, dy = _inputs(c, it, c["T"])
+        y = ly.forward(x)
+        dx = ly.backward(dy)
+        ly.planner.finish()
+    torch.cuda.synchronize()
+    yield name, c, ly, x, dy, y, dx
+    del ly
+    torch.cuda.empty_cache()
+
+
+def _slot(ly, s):
+    """(W13 or W1 [n1, d], W2 [d, f]) params and fp32 grads of local slot s."""
+    d, f, n1 = ly.g.d_model, ly.g.d_ff, ly.g.n1
+    p, gr = ly.params[s], ly.grads[s]
+    return (p[:n1 * d].view(n1, d), p[n1 * d:].view(d, f),
+            gr[:n1 * d].view(n1, d), gr[n1 * d:].view(d, f))
+
+
+def _ulp_check(out, ref, what, name):
+    out, ref = out.float(), ref.float()
+    bound = ULP * ref.abs() + ABS_STAGE * ref.abs().max()
+    excess = ((out - ref).abs() - bound).max().item()
+    _log(dict(config=name, check=what, rel_err=rel_err(out, ref),
+              frac_ne=(out != ref).float().mean().item()))
+    assert excess <= 0, f"{name} {what}: {excess:.3g} beyond 1 ulp + {ABS_STAGE}·max"
+
+
+def test_token_side_bit_exact(run):
+    name, c, ly, x, dy, y, dx = run
+    T, k = c["T"], 2
+    pos = ly.slot_pos[:T].long()
+    assert torch.equal(ly.slot_dest[:T], torch.zeros_like(ly.slot_dest[:T]))
+    # dispatch: the receive row of every token-slot is the token's x row
+    for j in range(k):
+        assert torch.equal(ly.xrecv[pos[:, j]], x), f"{name}: dispatch row of slot {j}"
+    # combine, fp32 j-ascending, no FMA (the kernel's order)
+    w = ly.topk_w[:T]
+    acc = torch.zeros(T, c["d"], device="cuda")
+    for j in range(k):
+        acc = acc + w[:, j:j + 1] * ly.y_e[pos[:, j]].float()
+    assert torch.equal(y, acc.bfloat16()), f"{name}: combine"
+    # dispatch_grad: w·dy pushed to the expert rows (fp32 multiply, bf16 round)
+    for j in range(k):
+        assert torch.equal(ly.dyrecv[pos[:, j]], (w[:, j:j + 1] * dy.float()).bfloat16()), \
+            f"{name}: dispatch_grad row of slot {j}"
+    # <dy, Y> per slot (the gate's backward input): fp32 dot of the same bf16 rows
+    g_ref = torch.einsum("td,tkd->tk", dy.float(), ly.y_e[pos].float())
+    assert rel_err(ly.slot_grad[:T], g_ref) <= 1e-5
+    # padding rows of every receive segment are zero (wgrad's K blocks rely on it)
+    t = ly.tables
+    for s in range(len(t.seg_start)):
+        a, b = int(t.seg_start[s] + t.seg_rows[s]), int(t.seg_start[s] + t.seg_padded[s])
+        assert not ly.xrecv[a:b].any() and not ly.dyrecv[a:b].any()
+    # every routed slot landed in its expert's segment
+    assert int(t.seg_rows.sum()) == T * k
+
+
+def test_gemm_stages_against_fp32(run):
+    """fwd1, fwd2, dgrad2, dgrad1, wgrad1, wgrad2 of every slot, each from the device's
+    own inputs; K = d_model (fwd1, dgrad2), d_ff (fwd2, dgrad1: 4096 / 1408 / 14336) and
+    the slot's token rows (wgrads: up to ~11k at cfg2's hottest expert)."""
+    name, c, ly, x, dy, y, dx = run
+    sw = c["act"] == "swiglu"
+    f = c["f"]
+    t = ly.tables
+    worst = {}
+    max_rows = 0
+    for s in range(len(t.seg_start)):
+        r0, n = int(t.seg_start[s]), int(t.seg_rows[s])
+        if n == 0:
+            continue
+        max_rows = max(max_rows, n)
+        w13, w2, dw13, dw2 = _slot(ly, s)
+        sl = slice(r0, r0 + n)
+        xr, dyr = ly.xrecv[sl], ly.dyrecv[sl]
+        saved, h = stage_fwd1(xr, w13, sw)
+        _ulp_check(ly.gprime[sl, :saved.shape[1]], saved, f"fwd1.saved[s{s}]", name)
+        _ulp_check(ly.h[sl], h, f"fwd1.h[s{s}]", name)
+        _ulp_check(ly.y_e[sl], bf16(ly.h[sl].float() @ w2.float().T), f"fwd2[s{s}]", name)
+        da = stage_dgrad2(dyr, w2, ly.gprime[sl, :saved.shape[1]], sw)
+        _ulp_check(ly.da[sl, :da.shape[1]], da, f"dgrad2[s{s}]", name)
+        _ulp_check(ly.dxe[sl], bf16(ly.da[sl, :da.shape[1]].float() @ w13.float()),
+                   f"dgrad1[s{s}]", name)
+        for what, out, ref in (
+                ("wgrad1", dw13, ly.da[sl, :da.shape[1]].float().T @ xr.float()),
+                ("wgrad2", dw2, dyr.float().T @ ly.h[sl].float())):
+            e = rel_err(out, ref)
+            worst[what] = max(worst.get(what, 0.0), e)
+            assert e <= STAGE_F32, f"{name} {what}[s{s}] rel {e:.3g} > {STAGE_F32}"
+    _log(dict(config=name, check="wgrad", worst=worst, max_segment_rows=max_rows))
+    assert max_rows > 0
+
+
+def test_layer_against_mirror_and_plain_fp32(run):
+    name, c, ly, x, dy, y, dx = run
+    T = c["T"]
+    idx, w = ly.topk_idx[:T], ly.topk_w[:T]
+    experts = {e: tuple(m.clone() for m in ly.expert_weight(e)) for e in range(c["E"])}
+    rec = dict(config=name)
+    for plain in (False, True):
+        ref = ref_layer(x, idx, w, ly.wg, experts, dy, plain=plain)
+        ey, edx = rel_err(y, ref["y"]), rel_err(dx, ref["dx"])
+        edw = max(rel_err(g, r) for e in range(c["E"])
+                  for g, r in zip(ly.expert_grad(e), ref["dW"][e]))
+        edwg = rel_err(ly.dwg, ref["dWg"])
+        tag = "plain_fp32" if plain else "mirror"
+        rec[tag] = dict(y=ey, dx=edx, dW=edw, dWg=edwg)
+        if plain:
+            assert max(ey, edx, edw) <= DRIFT, f"{name}: bf16 drift {rec[tag]} > {DRIFT}"
+        else:
+            assert ey <= E2E_Y and edx <= E2E_DX and edw <= E2E_DW, f"{name}: {rec[tag]}"
+            assert edwg <= 1e-2, f"{name}: dWg {edwg}"
+    _log(rec)
+
+
+def test_gate_routing_full_shape(run):
+    """Top-k selection at the full shape: equal to the selection on fp64 logits wherever
+    the k-th / (k+1)-th logit margin exceeds the fp32 logit error (1e-4)."""
+    name, c, ly, x, dy, y, dx = run
+    T, k = c["T"], 2
+    logits = (x.double() @ ly.wg.double().T) + ly.gate_bias.double()
+    top = torch.topk(logits, k + 1, dim=1)
+    clear = (top.values[:, k - 1] - top.values[:, k]) > 1e-4
+    sel = torch.sort(ly.topk_idx[:T].long(), dim=1).values
+    ref = torch.sort(top.indices[:, :k], dim=1).values
+    assert clear.float().mean() > 0.99
+    assert torch.equal(sel[clear], ref[clear]), f"{name}: top-k selection differs"
+    counts = torch.bincount(ly.topk_idx[:T].reshape(-1).long(), minlength=c["E"]).int()
+    assert torch.equal(ly.counts_table[0], counts)
+    # weights: softmax over the selected logits
+    lsel = torch.gather(logits, 1, ly.topk_idx[:T].long())
+    wref = torch.softmax(lsel, dim=1)
+    assert rel_err(ly.topk_w[:T], wref) <= 1e-4
+
+
+def test_cfg2_four_ranks_equal_one_rank():
+    """cfg2 at full shape over 4 emulated ranks (the FSSDP path of bench --gpus 4: early
+    SpAG, calibration, token A2A, push-SpRS) equals one rank on the same 65 536 tokens:
+    y and dx bit-exact, SpRS-reduced owner gradients within fp32 reordering (1e-4)."""
+    c = CASES["cfg2"]
+    torch.backends.cuda.matmul.allow_tf32 = False
+    D, Tr = 4, c["T"]
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=c["t"], capacity_override=c["m"])
+    multi = build(D, c, pol, Tr)
+    single = build(1, c, F.Policy(F.PolicyKind.EP), D * Tr)[0]
+    replicas = prefetched = 0
+    for it in range(3):
+        x, dy = _inputs(c, it, D * Tr)
+        ys = run_lockstep_forward(multi, list(x.split(Tr)))
+        dxs = run_lockstep_backward(multi, list(dy.split(Tr)))
+        for ly in multi:
+            ly.planner.finish()
+        y1 = single.forward(x)
+        dx1 = single.backward(dy)
+        single.planner.finish()
+        torch.cuda.synchronize()
+        dec = multi[0].decision
+        replicas += len(dec.target.entries) - c["E"]
+        prefetched += sum(ly.pre_tables.n_spag for ly in multi if ly.pre_tables is not None)
+        assert torch.equal(torch.cat(ys), y1), f"y differs (it {it})"
+        assert torch.equal(torch.cat(dxs), dx1), f"dx differs (it {it})"
+        worst = 0.0
+        for e in range(c["E"]):
+            o = dec.base.owner(e)
+            for gm, gs in zip(multi[o].expert_grad(e), single.expert_grad(e)):
+                worst = max(worst, rel_err(gm, gs))
+        assert worst <= 1e-4, f"SpRS-reduced grads rel {worst} (it {it})"
+        _log(dict(config="cfg2_n4", it=it, sprs_rel=worst,
+                  replicas=len(dec.target.entries) - c["E"]))
+    assert replicas > 0 and prefetched > 0
