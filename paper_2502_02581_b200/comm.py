@@ -19,7 +19,7 @@ from . import _native as N
 from .errors import DeviceError
 
 ALIGN = 4096
-FLAG_SLOTS = 64
+FLAG_SLOTS = 72  # 8 barrier slots per layer (<= 8 layers) + the standalone collectives'
 MAX_WORLD = 32
 
 

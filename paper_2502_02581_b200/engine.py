@@ -459,3 +459,16 @@ class FssdpPlanner:
     def memory(self, decisions) -> MemoryBreakdown:
         mode = "rematerialize" if self.policy.rematerialize else "retain"
         return memory_report(self.shards, [d.materialization for d in decisions], self.config, mode)
+
+
+def make_policy_state(config: ModelConfig, topology, policy: Policy) -> FssdpPlanner:
+    """Drop-in for moesim's make_policy_state (engine.py:751-758) on the executed path:
+    the FSSDP (or EP) control state.  `run_iteration(step)` advances it by one iteration of
+    gate counts exactly like FssdpState / EPState (engine.py:457-557) and returns the
+    per-layer LayerDecisions the kernels execute (placement, route, priced SpAG/SpRS
+    latencies) instead of the simulator's IterationTimeline; `memory(decisions)` gives
+    the iteration's MemoryBreakdown.  The simulated comparison policies are not executed."""
+    kind = getattr(policy, "kind", None)
+    if kind not in (PolicyKind.FSSDP, PolicyKind.EP):
+        raise ConfigError(f"unknown policy kind {kind!r}")
+    return FssdpPlanner(config, topology, policy)
