@@ -359,6 +359,17 @@ int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int3
 int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, int32_t world,
                   int32_t bar_slot, uint32_t epoch, void* stream);
 
+/* Barrier-protocol self-test (test infrastructure for the multi-rank path on ONE GPU): world
+ * emulated ranks (heaps at peer_bases) as the CTAs of one cooperative launch; `rounds`
+ * rounds of peer stores -> world barrier (bar_slot, epochs epoch0 ..) -> check.  Each heap
+ * needs FSSDP_SELFTEST_BYTES at data_off.  *errors (device int) += mismatched words.
+ * bar_slot < 0 skips the barrier: the negative control (stale words expected). */
+#define FSSDP_SELFTEST_THREADS 256
+#define FSSDP_SELFTEST_BYTES (2 * 32 * FSSDP_SELFTEST_THREADS * 4)
+int fssdp_barrier_selftest(const uint64_t* peer_bases, int64_t flags_off, int64_t data_off,
+                           int32_t world, int32_t rounds, int32_t bar_slot, uint32_t epoch0,
+                           int32_t* errors, void* stream);
+
 /* K4: dispatch.  For token-slot (t, j) with expert e and global rank r within
  * (this source, e) [tile_prefix + slot_rank], the destination d is the first with
  * route_cum[e*(D+1) + d + 1] > r and the row lands at recv_base[e*D + d] + r - route_cum[..d].

@@ -124,6 +124,7 @@ _SIGS = {
                          i32, i32, i32, C.c_uint32, vp, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
+    "fssdp_barrier_selftest": [vp, i64, i64, i32, i32, i32, u32, vp, vp],
     "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
                        i64, i32, i32, u32, vp, vp],
     "fssdp_combine": [vp, vp, vp, i64, i32, i32, vp, i64, vp, vp, vp],
@@ -204,7 +205,7 @@ KERNELS_PER_CALL = {
     "fssdp_plan_layer_dispatch": 2,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
     "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
-    "fssdp_gather_slots": 1,
+    "fssdp_gather_slots": 1, "fssdp_barrier_selftest": 1,
 }
 launch_count = 0
 

@@ -5,8 +5,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <string>
+#include <utility>
 
 #include "fssdp_internal.h"
 
@@ -19,6 +21,20 @@ void set_error(const char* msg) { g_last_error = msg ? msg : ""; }
 LaunchTiming& launch_timing() {
   static thread_local LaunchTiming t;
   return t;
+}
+
+cudaError_t ensure_dynamic_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> opted;  // (func, device) -> bytes
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = opted[std::make_pair(func, dev)];
+  if (have >= bytes) return cudaSuccess;
+  err = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err == cudaSuccess) have = bytes;
+  return err;
 }
 
 int num_sms() {

@@ -45,6 +45,10 @@ struct GemmLaunch {
 
 int num_sms();
 void set_error(const char* msg);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) raised to at least `bytes` for `func` on
+// the CURRENT device (the attribute is per device), at most once per (func, device, size):
+// thread-safe, and cheap on the launch path after the first call.
+cudaError_t ensure_dynamic_smem(const void* func, int bytes);
 
 // Launch timing windows (fssdp_timing_arm): the events a caller armed are recorded right
 // around the next entry point's kernel launches — after its host-side setup — so the

@@ -601,13 +601,8 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
                           const CUtensorMap& mx, const GemmLaunch& args, cudaStream_t stream) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI, CG>;
   const int smem = GemmSmem<BN, EPI, CG>::kDynamic;
-  static bool configured = false;  // per template instance
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return kErrCuda;
-    configured = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem) != cudaSuccess)
+    return kErrCuda;
   // tiles of CG*128 rows; a device-side total (-1) gets the full persistent grid
   const int units = args.total_tiles >= 0 ? args.total_tiles / CG : num_sms();
   int grid = CG * (units < num_sms() / CG ? units : num_sms() / CG);

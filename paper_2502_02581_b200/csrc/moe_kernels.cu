@@ -31,6 +31,7 @@
 namespace fssdp {
 
 constexpr int kMaxWorld = 32;
+constexpr int kSelftestThreads = FSSDP_SELFTEST_THREADS;
 constexpr int kGateTile = FSSDP_GATE_TILE;
 constexpr int kGateThreads = 256;
 constexpr int kGateChunk = 128;
@@ -92,6 +93,45 @@ __global__ void barrier_kernel(const uint64_t* peer_bases, int64_t flags_off, in
   asm volatile("griddepcontrol.wait;" ::: "memory");  // launched with PDL (launch_pdl)
   __threadfence_system();
   world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
+}
+
+// Barrier protocol self-test: `world` emulated ranks in ONE cooperative launch (CTA r is
+// rank r, all CTAs co-resident), so ranks that wait on each other never depend on the
+// scheduler (separate spinning launches on one GPU are not guaranteed to run together).
+// Round k: every rank stores a stamp block into every peer's heap (plain peer stores,
+// like the dispatch / SpRS pushes), makes them visible the way the product kernels do
+// (__syncthreads + __threadfence_system), joins world_barrier_warp with epoch0 + k, then
+// checks every writer's block in its own heap.  Blocks alternate between two buffers, so a
+// rank one round ahead never overwrites a block a peer is still checking.
+__device__ __forceinline__ uint32_t selftest_stamp(int round, int writer, int i) {
+  return (static_cast<uint32_t>(round) * 2654435761u) ^ (static_cast<uint32_t>(writer) << 20) ^
+         static_cast<uint32_t>(i);
+}
+
+__global__ void barrier_selftest_kernel(const uint64_t* __restrict__ peer_bases,
+                                        int64_t flags_off, int64_t data_off, int world,
+                                        int rounds, int slot, uint32_t epoch0, int* errors) {
+  const int rank = blockIdx.x;
+  const int n = blockDim.x;
+  int bad = 0;
+  for (int k = 0; k < rounds; ++k) {
+    const int64_t blk = (static_cast<int64_t>(k & 1) * kMaxWorld + rank) * n + threadIdx.x;
+    for (int p = 0; p < world; ++p)
+      reinterpret_cast<uint32_t*>(peer_bases[p] + data_off)[blk] =
+          selftest_stamp(k, rank, threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < 32)
+      world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch0 + static_cast<uint32_t>(k));
+    __syncthreads();
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(peer_bases[rank] + data_off);
+    for (int w = 0; w < world; ++w) {
+      const int64_t at = (static_cast<int64_t>(k & 1) * kMaxWorld + w) * n + threadIdx.x;
+      if (mine[at] != selftest_stamp(k, w, threadIdx.x)) ++bad;
+    }
+  }
+  if (bad) atomicAdd(errors, bad);
 }
 
 // ------------------------------------------------------------------ K1 gate
@@ -1462,20 +1502,9 @@ static int gate_mma_launch(const __nv_bfloat16* x, const float* wg, const float*
   auto go = [&](auto kern, int threads) {
     const size_t dyn = sw ? wsm : 0;
     // static + dynamic above 48 KB needs the opt-in; raised once per kernel (all the
-    // instantiations share one function-pointer type, so key by address)
-    static const void* fn_seen[32];
-    static size_t fn_opted[32];
-    int slot_i = 0;
-    while (slot_i < 31 && fn_seen[slot_i] != nullptr &&
-           fn_seen[slot_i] != reinterpret_cast<const void*>(kern))
-      ++slot_i;
-    fn_seen[slot_i] = reinterpret_cast<const void*>(kern);
-    if (dyn > fn_opted[slot_i]) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(dyn)) != cudaSuccess)
-        return;  // reported by launch_status()
-      fn_opted[slot_i] = dyn;
-    }
+    if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), static_cast<int>(dyn)) !=
+        cudaSuccess)
+      return;  // reported by launch_status()
     timing_begin(stream);
     kern<<<tiles, threads, dyn, stream>>>(x, wg, bias, T, d, E, k, logits, topk_idx, topk_w,
                                           slot_rank, tile_counts, tile_prefix, ws, peer_bases,
@@ -1527,8 +1556,8 @@ int fssdp_gate_topk(const void* x, const float* wg, const float* bias, int64_t T
   auto launch = [&](auto kern) -> int {
     const size_t max_smem = kGateTile * sizeof(__nv_bfloat16) * (kGateChunk + 8) +
                             kGateMaxE * sizeof(float) * (kGateChunk + 4);
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(max_smem)) != cudaSuccess)
+    if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), static_cast<int>(max_smem)) !=
+        cudaSuccess)
       return launch_status();
     timing_begin(as_stream(stream));
     kern<<<tiles, kGateThreads, smem, as_stream(stream)>>>(
@@ -1625,6 +1654,34 @@ int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, i
   timing_begin(as_stream(stream));
   launch_pdl(barrier_kernel, 1, 32, as_stream(stream), peer_bases, flags_off, rank, world,
              bar_slot, epoch);
+  return launch_status();
+}
+
+int fssdp_barrier_selftest(const uint64_t* peer_bases, int64_t flags_off, int64_t data_off,
+                           int32_t world, int32_t rounds, int32_t bar_slot, uint32_t epoch0,
+                           int32_t* errors, void* stream) {
+  if (world <= 0 || world > kMaxWorld || rounds <= 0) {
+    set_error("barrier_selftest: bad world/rounds");
+    return kErrDimension;
+  }
+  int coop = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) {
+    set_error("barrier_selftest: device cannot launch cooperative kernels");
+    return kErrCuda;
+  }
+  int threads = kSelftestThreads;
+  void* args[] = {&peer_bases, &flags_off, &data_off, &world, &rounds, &bar_slot, &epoch0, &errors};
+  timing_begin(as_stream(stream));
+  const cudaError_t err = cudaLaunchCooperativeKernel(
+      reinterpret_cast<const void*>(barrier_selftest_kernel), dim3(world), dim3(threads), args,
+      0, as_stream(stream));
+  timing_end();
+  if (err != cudaSuccess) {
+    set_error(cudaGetErrorString(err));
+    return kErrCuda;
+  }
   return launch_status();
 }
 
@@ -1734,13 +1791,10 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
   const int n_tiles = static_cast<int>((T + tok_per_cta - 1) / tok_per_cta);
   if (n_tiles > 0) {
     const int smem = E * kWgThreads * static_cast<int>(sizeof(float4));
-    static int configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      if (cudaFuncSetAttribute(gate_wgrad_partial_kernel,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-        return launch_status();
-      configured = smem;
-    }
+    if (smem > 48 * 1024 &&
+        ensure_dynamic_smem(reinterpret_cast<const void*>(gate_wgrad_partial_kernel), smem) !=
+            cudaSuccess)
+      return launch_status();
     dim3 grid(col_blocks, n_tiles);
     timing_begin(as_stream(stream));
     gate_wgrad_partial_kernel<<<grid, kWgThreads, smem, as_stream(stream)>>>(
@@ -1833,10 +1887,8 @@ int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
   }
   if (n_jobs <= 0) return kOk;
   constexpr int kSmem = kPullRing * kPullSub;
-  static const bool attr_ok = cudaFuncSetAttribute(sprs_pull_kernel,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kSmem) == cudaSuccess;
-  if (!attr_ok) {
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(sprs_pull_kernel), kSmem) !=
+      cudaSuccess) {
     set_error("sprs_pull: cannot reserve the TMA ring");
     return kErrCuda;
   }

@@ -18,7 +18,7 @@ sums in registers).  No NCCL call is made on either collective.
 Slot convention (`chunk_slots`), identical on every rank so no table is exchanged: the
 partition's chunks on a device (ascending id) first, then the device's other chunks of the
 non-partition placement (ascending id) — the layout FssdpMoE uses for owned + replica
-slots (plan_tables.slot_maps).  Under SpAG the pre slots are a prefix of the post slots;
+slots (csrc/planner.cpp fssdp_build_rank_tables).  Under SpAG the pre slots are a prefix of the post slots;
 under SpRS the post (owned) slots are a prefix of the pre slots.
 """
 

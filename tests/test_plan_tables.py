@@ -6,7 +6,8 @@ import numpy as np
 
 import paper_2502_02581_b200 as F
 from oracle import tensor_oracle as TO
-from paper_2502_02581_b200.plan_tables import ROW_ALIGN, build_rank_tables
+from oracle.plan_tables_oracle import build_rank_tables
+from paper_2502_02581_b200.plan_tables import ROW_ALIGN
 
 
 def _random_plan(rng, D, E, T, k):
@@ -56,7 +57,7 @@ def test_positions_tile_receive_segments_exactly():
 
 
 def test_native_tables_equal_python_tables():
-    """The C++ twin (product path) builds exactly the tables of plan_tables.py."""
+    """The C++ twin (product path) builds exactly the tables of oracle/plan_tables_oracle.py."""
     from paper_2502_02581_b200.plan_tables import GEMM_NAMES, NativeTables
 
     rng = np.random.default_rng(3)
