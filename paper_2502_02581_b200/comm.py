@@ -38,17 +38,29 @@ def view_bytes(ptr: int, nbytes: int, device) -> torch.Tensor:
 
 
 class HeapLayout:
-    """Deterministic bump allocator of heap offsets (identical on every rank)."""
+    """Deterministic bump allocator of heap offsets (identical on every rank).
 
-    def __init__(self):
+    guard > 0 (tests; compute-sanitizer is closed on the GPU pool) puts `guard` canary
+    bytes after every region: Heap.fill_guards / check_guards then catch any kernel that
+    writes past the end of a heap buffer — a peer's or its own."""
+
+    GUARD_BYTE = 0xA5
+
+    def __init__(self, guard: int = 0):
         self.size = 0
+        self.guard = (int(guard) + ALIGN - 1) // ALIGN * ALIGN
         self.regions: dict[str, tuple[int, int]] = {}
+        self.guards: list[tuple[str, int, int]] = []
         self.add("flags", FLAG_SLOTS * MAX_WORLD * 4)
 
     def add(self, name: str, nbytes: int) -> int:
         off = (self.size + ALIGN - 1) // ALIGN * ALIGN
         self.regions[name] = (off, int(nbytes))
         self.size = off + int(nbytes)
+        if self.guard:
+            g = (self.size + ALIGN - 1) // ALIGN * ALIGN
+            self.guards.append((name, g, self.guard))
+            self.size = g + self.guard
         return off
 
     def offset(self, name: str) -> int:
@@ -70,6 +82,15 @@ class Heap:
     def tensor(self, offset: int, shape, dtype: torch.dtype) -> torch.Tensor:
         n = int(np.prod(shape)) * torch.empty(0, dtype=dtype).element_size()
         return self._bytes[offset:offset + n].view(dtype).view(*shape)
+
+    def fill_guards(self, layout: HeapLayout) -> None:
+        for _, off, n in layout.guards:
+            self._bytes[off:off + n].fill_(HeapLayout.GUARD_BYTE)
+
+    def check_guards(self, layout: HeapLayout) -> list:
+        """Names of the regions whose trailing canary was overwritten."""
+        return [name for name, off, n in layout.guards
+                if not bool((self._bytes[off:off + n] == HeapLayout.GUARD_BYTE).all())]
 
     def ipc_handle(self) -> bytes:
         buf = (C.c_uint8 * 64)()
