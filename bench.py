@@ -69,7 +69,23 @@ CFG2 = CFG  # the metric's configuration
 POLICY = CFG["policy"]
 ZIPF_S = CFG["zipf_s"]
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def _nvlink_peak():
+    """Per-direction NVLink peak measured on this pool's B200s by scripts/nvlink_probe.py
+    (inbound user bytes of one GPU pulling from every peer, best of SM kernel / copy
+    engines), committed under profiles/; else B200_PROFILING.md's 770 GB/s peer copy."""
+    f = ROOT / "profiles" / "r2_nvlink_peak_n4.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["nvlink_gbs"]), f"measured ({f.name})"
+        except (KeyError, ValueError):
+            pass
+    return 770.0, "fallback (B200_PROFILING.md peer copy)"
+
+
+NVLINK_PEER_GBS, NVLINK_PEAK_SRC = _nvlink_peak()
+INPUT_POOL = 8  # distinct (x, dy) batches cycled through the steps: routing varies per step
 
 
 def parse():
@@ -368,13 +384,20 @@ def run_ours(args):
     p = 1.0 / np.arange(1, E + 1) ** ZIPF_S
     p = p[np.random.default_rng(42).permutation(E)]
     layer.gate_bias.copy_(torch.tensor(np.log(p / p.sum()), dtype=torch.float32))
+    # a pool of distinct token batches cycled through the steps: every step routes fresh
+    # tokens, so counts, plans and the early-SpAG candidate change from step to step
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    x = torch.randn(T, CFG2["d_model"], device=dev, generator=gen).bfloat16()
-    dy = (torch.randn(T, CFG2["d_model"], device=dev, generator=gen) * 0.05).bfloat16()
+    xs = [torch.randn(T, CFG2["d_model"], device=dev, generator=gen).bfloat16()
+          for _ in range(INPUT_POOL)]
+    dys = [(torch.randn(T, CFG2["d_model"], device=dev, generator=gen) * 0.05).bfloat16()
+           for _ in range(INPUT_POOL)]
+    it = [0]
 
-    def step(xin, dyin):
-        layer.forward(xin)
-        dx = layer.backward(dyin)
+    def step():
+        i = it[0] % INPUT_POOL
+        it[0] += 1
+        layer.forward(xs[i])
+        dx = layer.backward(dys[i])
         layer.reduce_gate_grad()
         layer.planner.finish()
         return dx
@@ -385,26 +408,28 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     for _ in range(max(3, args.warmup)):
-        step(x, dy)
+        step()
     barrier()
     layer.timers = None  # the timed region runs uninstrumented
+    layer.reset_plan_stats()
     NAT.launch_count = 0
     start, end = torch.cuda.Event(True), torch.cuda.Event(True)
     with ClockSampler(local) as clocks:
         barrier()
         start.record()
         for _ in range(args.steps):
-            step(x, dy)
+            step()
         end.record()
         barrier()
     launches = NAT.launch_count
+    plan_stats = dict(layer.plan_stats)
     ms = start.elapsed_time(end) / args.steps
     # the GPU-side planning gap (count all-gather done -> tables uploaded, dispatch next),
     # probed with just two events per step
     layer.gap_events = []
     barrier()
     for _ in range(args.steps):
-        step(x, dy)
+        step()
     barrier()
     plan_gap_ms = sum(a.elapsed_time(b) for a, b in layer.gap_events) / max(1, len(layer.gap_events))
     layer.gap_events = None
@@ -415,14 +440,14 @@ def run_ours(args):
     # of warm-up steps — so its kernel times describe the kernels of the timed region.
     time.sleep(0.3)
     for _ in range(max(3, args.warmup)):
-        step(x, dy)
+        step()
     layer.timers = {}
     barrier()
     ref = NAT.NativeEvent()  # timeline origin for the per-kernel launch-timing windows
     ref.record(torch.cuda.current_stream(dev))
     with ClockSampler(local) as inst_clocks:
         for _ in range(args.steps):
-            step(x, dy)
+            step()
         barrier()
     timers = layer.timers
     marks = timers.pop("marks", [])
@@ -483,7 +508,11 @@ def run_ours(args):
                    sprs_reduce_bytes, rows_rank, float(t.recv_rows), float(t.n_slots)])
     peaks, peak_src = load_peaks()
     achieved = allr[:, 1].sum() / (allr[:, 0].sum() * 1e-3) / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
+    # the GEMMs run inside a ~1.5 ms step at max SM clock: the burst GEMM peak is the
+    # denominator (the sustained figure is the seconds-long, power-capped loop's)
+    peak = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+    peak_sustained = float(peaks.get("bf16_tflops_sustained",
+                                     PEAKS_FALLBACK["bf16_tflops_sustained"]))
     traffic, traffic_src = None, None
     tfiles = sorted((ROOT / "profiles").glob("*gemm_traffic.json"))
     if tfiles:  # DRAM bytes of the step's GEMM launches from the committed ncu --set full capture
@@ -495,7 +524,9 @@ def run_ours(args):
                 "kernel": "fssdp grouped_gemm_kernel (tcgen05), all 6 GEMMs of the step",
                 "algorithmic_flops": "3 x 2 x routed_rows x n_mats x d_model x d_ff per rank "
                                      "(n_mats 2 GeLU, 3 SwiGLU)",
-                "peak_source": f"{peak_src}, sustained bf16 (kernels timed inside a long step)",
+                "peak_source": f"{peak_src}, burst bf16 (cuBLAS 8192^3 best of 10; the "
+                               f"GEMMs run at max SM clock inside a short step)",
+                "frac_of_sustained": achieved / peak_sustained,
                 "gemm_ms_per_step_per_rank": [round(v, 4) for v in allr[:, 0]],
                 "gemm_tflops_per_rank": [round(f / (g * 1e-3) / 1e12, 1)
                                          for g, f in zip(allr[:, 0], allr[:, 1])],
@@ -540,7 +571,9 @@ def run_ours(args):
             "spag_inbound_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 4], allr[:, 2])],
             "sprs_pushed_in_bytes_per_rank": [float(b) for b in allr[:, 5]],
             "sprs_local_reduce_gbs_per_rank": [gbs(b, m) for b, m in zip(allr[:, 8], allr[:, 3])],
-            "nvlink_peer_gbs_ref": NVLINK_PEER_GBS,
+            "nvlink_peak_gbs": NVLINK_PEER_GBS, "nvlink_peak_source": NVLINK_PEAK_SRC,
+            "spag_bottleneck_frac_of_nvlink": (gbs(rep.bottleneck_bytes, spag_max) or 0.0)
+                                              / NVLINK_PEER_GBS,
             "a2a": a2a_stats(dec, allp, keys, world),
             "note": "SpRS wire is fp32 partials pushed by the wgrad epilogue's TMA stores "
                     "(2x the reference's expert_bytes pricing); sprs_ms is the local reduce. "
@@ -549,34 +582,38 @@ def run_ours(args):
                     "traffic); spag_ms sums both windows. Standalone SpAG / SpRS kernel "
                     "bandwidth: profiles/r1_sparse_sweep.txt"}
 
-    # end to end through the public API with host buffers: inputs are copied H2D on a copy
-    # stream one step ahead (double buffered), dx is copied D2H behind the compute.
+    # end to end through the public API with host buffers: each step's (x, dy) is copied
+    # H2D from pinned host memory on a copy stream one step ahead (double buffered); its y
+    # and dx are copied D2H behind the compute (y once the forward is done).
     e2e = None
     if not args.no_e2e:
-        xh = x.cpu().pin_memory()
-        dyh = dy.cpu().pin_memory()
-        dxh = [torch.empty_like(xh).pin_memory() for _ in range(2)]
-        xb = [torch.empty_like(x) for _ in range(2)]
-        dyb = [torch.empty_like(dy) for _ in range(2)]
+        HP = 2  # distinct pinned host batches (the device pool's first two)
+        xh = [xs[i].cpu().pin_memory() for i in range(HP)]
+        dyh = [dys[i].cpu().pin_memory() for i in range(HP)]
+        dxh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
+        yh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
+        xb = [torch.empty_like(xs[0]) for _ in range(2)]
+        dyb = [torch.empty_like(dys[0]) for _ in range(2)]
         copy_s = torch.cuda.Stream(device=dev)   # H2D
         d2h_s = torch.cuda.Stream(device=dev)    # D2H: PCIe is full duplex
         main_s = torch.cuda.current_stream(dev)
         in_ev = [torch.cuda.Event() for _ in range(2)]
         done_ev = [torch.cuda.Event() for _ in range(2)]
+        fwd_ev = [torch.cuda.Event() for _ in range(2)]
 
         def prefetch(i):
             b = i % 2
             with torch.cuda.stream(copy_s):
                 copy_s.wait_event(done_ev[b])  # step i-2 finished with buffer b
-                xb[b].copy_(xh, non_blocking=True)
-                dyb[b].copy_(dyh, non_blocking=True)
+                xb[b].copy_(xh[i % HP], non_blocking=True)
+                dyb[b].copy_(dyh[i % HP], non_blocking=True)
                 in_ev[b].record(copy_s)
 
-        def d2h(dx, b):
+        def d2h(t, host, ev):
             with torch.cuda.stream(d2h_s):
-                d2h_s.wait_event(done_ev[b])
-                dxh[b].copy_(dx, non_blocking=True)
-                dx.record_stream(d2h_s)
+                d2h_s.wait_event(ev)
+                host.copy_(t, non_blocking=True)
+                t.record_stream(d2h_s)
 
         def run(n):
             # The bulk copies are issued once the step's forward has been planned (the
@@ -590,16 +627,18 @@ def run_ours(args):
             for i in range(n):
                 b = i % 2
                 main_s.wait_event(in_ev[b])
-                layer.forward(xb[b])
+                y = layer.forward(xb[b])
+                fwd_ev[b].record(main_s)
                 if i + 1 < n:  # next inputs stream in while this step computes
                     prefetch(i + 1)
-                if prev is not None:  # the previous step's result streams out
+                if prev is not None:  # the previous step's dx streams out
                     d2h(*prev)
+                d2h(y, yh[b], fwd_ev[b])  # this step's y, behind its forward
                 dx = layer.backward(dyb[b])
                 layer.reduce_gate_grad()
                 layer.planner.finish()
                 done_ev[b].record(main_s)
-                prev = (dx, b)
+                prev = (dx, dxh[b], done_ev[b])
             d2h(*prev)
             main_s.wait_stream(copy_s)
             main_s.wait_stream(d2h_s)
@@ -621,11 +660,11 @@ def run_ours(args):
             e2e_ms = float(t.item())
         nb = T * CFG2["d_model"] * 2
         e2e = {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s",
-               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": nb, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "ms_per_step": e2e_ms,
                "planning_gap_gpu_ms": round(e2e_gap_ms, 4),
-               "pipeline": "H2D of step i+1 and D2H of step i-1 on two copy streams (PCIe full "
-                           "duplex), issued after step i's forward is planned, overlapped with "
-                           "its compute (FssdpMoE.forward/backward)"}
+               "pipeline": "x, dy of step i+1 H2D and y of step i, dx of step i-1 D2H on two "
+                           "copy streams (PCIe full duplex), overlapped with step i's compute "
+                           "(FssdpMoE.forward/backward); two distinct host batches alternate"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -639,10 +678,17 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (seeded N(0,1) tokens, random-init experts, Zipf gate bias)",
+                "data": f"synthetic (seeded N(0,1) tokens, {INPUT_POOL} distinct batches cycled "
+                        f"per rank, random-init experts, Zipf gate bias)",
                 "config": _config(args, world), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
                 "phase_ms_per_step": breakdown,
+                "early_spag": {**plan_stats, "hit_rate": plan_stats["early_hit"] /
+                               max(1, plan_stats["early"]),
+                               "note": "timed steps: early = an estimate-based candidate was "
+                                       "fetched before the gate; hit = the final plan equals "
+                                       "it; extended = calibration added replicas (late "
+                                       "SpAG); fallback = dropped to the bare partition"},
                 "host_plan_path_us": {k: round(v, 1) for k, v in host_us.items()}}
         if sparse:
             line["sparse_collectives"] = sparse

@@ -247,7 +247,13 @@ class FssdpMoE:
         self._owned_expert_ids = None
         self._base_owner = None      # owner per expert of the partition the params follow
         self._reshard_pending = None  # device copy list of a re-shard gather, or None
+        self.reset_plan_stats()
         self.init_parameters(seed)
+
+    def reset_plan_stats(self) -> None:
+        """Counters of the early (estimate-based) SpAG against the final plan, per forward."""
+        self.plan_stats = {"plans": 0, "early": 0, "early_hit": 0, "early_extended": 0,
+                           "early_fallback": 0, "late_copies": 0}
 
     # ------------------------------------------------------------ parameters
     def owned_experts(self) -> list:
@@ -628,6 +634,17 @@ class FssdpMoE:
             if np.any(target > dec.base.mask):
                 raise InternalError("final placement is neither a superset of the early one "
                                     "nor the bare partition")
+        st = self.plan_stats
+        st["plans"] += 1
+        st["late_copies"] += int(tables.n_spag)
+        if pre is not None:
+            st["early"] += 1
+            if np.array_equal(pre, target):
+                st["early_hit"] += 1          # the final plan is exactly the early one
+            elif not np.any(target > dec.base.mask):
+                st["early_fallback"] += 1     # dropped: the bare partition (fallback)
+            else:
+                st["early_extended"] += 1     # calibration added replicas (late SpAG)
         if tables.n_owned != self._n_owned or (
                 self.planner.last_reshard_moves and
                 list(tables.slot_expert[:tables.n_owned]) != self._owned_expert_ids):
