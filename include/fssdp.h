@@ -471,6 +471,27 @@ int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
                     int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
                     const int32_t* pull_srcs, void* stream);
 
+/* ================================================================== training step */
+/* AdamW over n fp32 elements (n % 4 == 0): exp_avg / exp_avg_sq / master updated in place
+ * from grads (bias corrections of `step` >= 1, decoupled weight decay), then params_bf16
+ * (nullable: the master IS the parameter) = bf16(master).  The owner's expert shards keep
+ * master / moments in the symmetric heap so a re-shard moves them with the parameters
+ * (params + 6x state = the 7x expert_bytes of engine.py:233, 444-453).  Replaces nothing in
+ * the reference (it prices the optimizer state, it has no optimizer). */
+int fssdp_adam_step(void* params_bf16, float* master, float* exp_avg, float* exp_avg_sq,
+                    const float* grads, int64_t n, float lr, float beta1, float beta2, float eps,
+                    float weight_decay, int64_t step, void* stream);
+
+/* Owner-update epochs (flag pad slot `slot`, entry [slot][rank] of each rank's own pad):
+ * fssdp_publish_epoch stores `epoch` (system-scope release) after every earlier write of the
+ * stream — an owner's optimizer step — so peers may read its shards; fssdp_wait_epochs
+ * blocks its stream until every rank < world published >= epoch (the early SpAG's copy
+ * engines start reading owners' shards before any barrier of the step). */
+int fssdp_publish_epoch(const uint64_t* peer_bases, int64_t flags_off, int32_t slot, int32_t rank,
+                        uint32_t epoch, void* stream);
+int fssdp_wait_epochs(const uint64_t* peer_bases, int64_t flags_off, int32_t slot, int32_t world,
+                      uint32_t epoch, void* stream);
+
 /* ================================================================== symmetric heap */
 /* cudaMalloc'd, zero-initialised heap (bytes rounded up to 2 MiB). */
 int fssdp_heap_alloc(size_t bytes, void** ptr_out);

@@ -137,6 +137,11 @@ _SIGS = {
     "fssdp_gather_slots": [vp, i32, i64, i64, i64, i64, vp, i32, i32, vp],
     "fssdp_sprs": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
     "fssdp_sprs_pull": [vp, i32, i64, i64, vp, i32, vp, vp],
+    # training step
+    "fssdp_adam_step": [vp, vp, vp, vp, vp, i64, C.c_float, C.c_float, C.c_float, C.c_float,
+                        C.c_float, i64, vp],
+    "fssdp_publish_epoch": [vp, i64, i32, i32, u32, vp],
+    "fssdp_wait_epochs": [vp, i64, i32, i32, u32, vp],
     # launch timing (measurement)
     "fssdp_event_create": [C.POINTER(C.c_void_p)],
     "fssdp_event_destroy": [vp],
@@ -205,7 +210,8 @@ KERNELS_PER_CALL = {
     "fssdp_plan_layer_dispatch": 2,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
     "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
-    "fssdp_gather_slots": 1, "fssdp_barrier_selftest": 1,
+    "fssdp_gather_slots": 1, "fssdp_barrier_selftest": 1, "fssdp_adam_step": 1,
+    "fssdp_publish_epoch": 1, "fssdp_wait_epochs": 1,
 }
 launch_count = 0
 

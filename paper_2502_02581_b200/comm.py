@@ -19,7 +19,8 @@ from . import _native as N
 from .errors import DeviceError
 
 ALIGN = 4096
-FLAG_SLOTS = 72  # 8 barrier slots per layer (<= 8 layers) + the standalone collectives'
+FLAG_SLOTS = 80  # 8 barrier slots per layer (<= 8 layers), 64: standalone collectives,
+#                  72 + layer: owner-update epochs
 MAX_WORLD = 32
 
 

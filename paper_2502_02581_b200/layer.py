@@ -39,6 +39,7 @@ GROUP_BYTES = N.C.sizeof(N.GemmGroup)  # fssdp_gemm_group
 
 # barrier slots (flag pads) used by one layer; layer i uses base + 8*i
 BAR_COUNTS, BAR_DISPATCH, BAR_Y, BAR_DGRAD, BAR_DX, BAR_END, BAR_RESHARD, BAR_SPRS = range(8)
+EPOCH_SLOT0 = 72  # + layer index: the owner-update epoch of the layer (comm.FLAG_SLOTS)
 
 
 @dataclass(frozen=True)
@@ -53,6 +54,7 @@ class LayerGeometry:
     activation: str = "gelu"  # "gelu": [W1 | W2];  "swiglu": [W13 | W2] (Mixtral/DeepSeek)
     owned_max: int = 0        # max experts of this layer a rank owns (0: ceil(E / world))
     reshard: bool = False     # heterogeneous re-sharding enabled: a staging region for moves
+    optimizer: bool = False   # AdamW state (fp32 master, m, v) of the owned shards in the heap
 
     @property
     def n_mats(self) -> int:  # expert matrices per slot
@@ -78,6 +80,11 @@ class LayerGeometry:
     @property
     def expert_bytes(self) -> int:
         return self.slot_param_bytes
+
+    @property
+    def owned_cap(self) -> int:
+        """Most experts of this layer one rank can own (optimizer-state slots)."""
+        return self.owned_max or -(-self.num_experts // self.world)
 
     @property
     def stage_slots(self) -> int:
@@ -113,6 +120,11 @@ class LayerGeometry:
         layout.add(prefix + "stage", max(1, self.stage_slots) * self.slot_grad_elems * 4)
         # re-shard staging: the old owned shards, pulled by their new owners
         layout.add(prefix + "reshard", (self.slots if self.reshard else 1) * self.slot_param_bytes)
+        if self.optimizer:  # fp32 master / exp_avg / exp_avg_sq of the owned slots (+ staging)
+            n = self.owned_cap * self.slot_grad_elems * 4
+            for k in ("opt_master", "opt_m", "opt_v"):
+                layout.add(prefix + k, n)
+            layout.add(prefix + "reshard_opt", 3 * n if self.reshard else 16)
 
 
 def default_slots(num_experts: int, world: int, m: int) -> int:
@@ -143,6 +155,15 @@ class FssdpMoE:
         self.off = {k: L.offset(prefix + k) for k in
                     ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage",
                      "reshard")}
+        self.opt_state = None  # {"master", "m", "v"}: [owned_cap, slot elems] fp32 heap views
+        if geom.optimizer:
+            for k in ("opt_master", "opt_m", "opt_v", "reshard_opt"):
+                self.off[k] = L.offset(prefix + k)
+            self.opt_state = {k: heap.tensor(self.off["opt_" + k],
+                                             (geom.owned_cap, geom.n_mats * d * f), torch.float32)
+                              for k in ("master", "m", "v")}
+        self.epoch_slot = EPOCH_SLOT0 + layer_index
+        self._fwd_epoch = 0
         self.flags_off = L.offset("flags")
         self.params = heap.tensor(self.off["params"], (geom.slots, geom.n_mats * d * f),
                                   torch.bfloat16)
@@ -352,9 +373,29 @@ class FssdpMoE:
     # load history, so its replicas are pulled on a side stream while the gate, the
     # count all-gather and the host planner run; the final plan (a superset after
     # calibration, or the bare partition after fallback) then copies only the rest.
-    # Owned shards must not change between the end of backward and the next forward
-    # (peers read them early) — put a barrier after an optimizer step that updates them.
+    # Peers read an owner's shards early, before any barrier of the step: every forward
+    # first publishes an owner-update epoch (phase_publish, after the caller's optimizer
+    # step in stream order) and the early copies wait for every owner's (_ce_copies).
     PREFETCH = os.environ.get("FSSDP_PREFETCH", "1") != "0"
+
+    # FSSDP_EPOCHS=0 drops the owner-update epochs (negative control of
+    # scripts/dist_train_check.py: the early copies then race the owners' optimizer step)
+    EPOCHS = os.environ.get("FSSDP_EPOCHS", "1") != "0"
+
+    def _epochs_live(self) -> bool:
+        """Owner-update epochs guard the early copy-engine SpAG between processes (emulated
+        ranks run in lockstep on one stream: nothing to guard)."""
+        return (self.EPOCHS and self.group.mode == "dist" and self.world > 1 and self.PREFETCH
+                and self.PRE_W1_CE)
+
+    def phase_publish(self) -> None:
+        """Owner-update epoch: this rank's owned shards are final for forward #e — stream-
+        ordered after whatever the caller ran before this forward (its optimizer step), so
+        a peer's early SpAG (which starts before any barrier of the step) may read them."""
+        self._fwd_epoch += 1
+        if self._epochs_live():
+            self._call("fssdp_publish_epoch", self._pb(), self.flags_off, self.epoch_slot,
+                       self.rank, C.c_uint32(self._fwd_epoch & 0xFFFFFFFF), self._stream())
 
     def phase_prefetch(self) -> None:
         self.pre_mask, self.pre_mask_ptr, self.pre_tables, self._pre_done = None, None, None, None
@@ -441,11 +482,17 @@ class FssdpMoE:
 
     def _ce_copies(self, part_off: int, part_bytes: int) -> torch.cuda.Event:
         """The early SpAG's copies of one part of every slot, by the copy engines on their
-        own stream (after the current stream's work); returns their completion event."""
+        own stream (after the current stream's work); returns their completion event.
+        The W1 part starts before any barrier of the step: it first waits until every
+        owner published this forward's epoch (its shards are final — phase_publish)."""
         ce = getattr(self, "_ce", None)
         if ce is None:
             ce = self._ce = torch.cuda.Stream(device=self.dev)
         ce.wait_stream(torch.cuda.current_stream(self.dev))
+        if part_off == 0 and self._epochs_live():
+            N.call_raw("fssdp_wait_epochs", self._pb(), self.flags_off, self.epoch_slot,
+                       self.world, C.c_uint32(self._fwd_epoch & 0xFFFFFFFF),
+                       C.c_void_p(ce.cuda_stream))
         sb = self.g.slot_param_bytes
         off = self.off["params"] + part_off
         bases = self.group.bases
@@ -671,9 +718,10 @@ class FssdpMoE:
     # owned shards follow it: every rank copies its old owned slots into its staging region
     # (planning phase), then — after a device barrier — every rank pulls its new owned
     # experts, in slot order, from their old owners' staging (dispatch phase, before the
-    # dispatch's own barrier, so no replica is pulled from a shard still in flight).  Only
-    # parameters move: this layer keeps no optimizer state (the reference prices 7×S per
-    # moved expert, engine.py:233, for parameters + Adam state).
+    # dispatch's own barrier, so no replica is pulled from a shard still in flight).  With
+    # an optimizer (geometry optimizer=True) its fp32 master and both moments move the same
+    # way: params + 6x state = the 7x expert_bytes per moved expert the reference prices
+    # (engine.py:233, 444-453).
     def _reshard_stage(self) -> None:
         new_owner = np.asarray(self.planner.shards.per_layer[self.layer].owners())
         if np.array_equal(new_owner, self._base_owner):
@@ -685,6 +733,12 @@ class FssdpMoE:
         if nb:
             stage = self.group.local.tensor(self.off["reshard"], (nb,), torch.uint8)
             stage.copy_(self.params.view(torch.uint8).view(-1)[:nb])
+        if self.opt_state is not None and self._n_owned:  # the Adam state moves with them
+            ost = self.group.local.tensor(self.off["reshard_opt"],
+                                          (3, self.g.owned_cap, self.g.slot_grad_elems),
+                                          torch.float32)
+            for i, k in enumerate(("master", "m", "v")):
+                ost[i, :self._n_owned].copy_(self.opt_state[k][:self._n_owned])
         old_owner = self._base_owner
         old_slots = {r: sorted(int(e) for e in np.flatnonzero(old_owner == r))
                      for r in range(self.world)}
@@ -705,6 +759,12 @@ class FssdpMoE:
         self._call("fssdp_gather_slots", self._pb(), self.rank, self.off["reshard"],
                    self.off["params"], self.g.slot_param_bytes, 0, ops._ptr(copies),
                    copies.shape[0], 0, self._stream())
+        if self.opt_state is not None:  # fp32 master / exp_avg / exp_avg_sq: 6x expert_bytes
+            sb = self.g.slot_grad_elems * 4
+            for i, k in enumerate(("opt_master", "opt_m", "opt_v")):
+                self._call("fssdp_gather_slots", self._pb(), self.rank,
+                           self.off["reshard_opt"] + i * self.g.owned_cap * sb, self.off[k], sb,
+                           0, ops._ptr(copies), copies.shape[0], 0, self._stream())
 
     def phase_dispatch(self, n_zero: int | None = None) -> None:
         """K4 — first launch after the host plan: its arguments are mostly prebuilt (the
@@ -904,6 +964,7 @@ class FssdpMoE:
     LOCAL_GEMM_TABLES = os.environ.get("FSSDP_LOCAL_GEMM", "0") == "1"
 
     def _forward(self, x: torch.Tensor) -> torch.Tensor:
+        self.phase_publish()
         self.phase_prefetch()
         self.phase_gate(x)
         self.phase_counts()
@@ -1030,15 +1091,17 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
                  policy, *, rank: int = 0, world: int = 1, device="cuda", seed: int = 0,
                  peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
                  per_token_expert_time: float | None = None, pg=None,
-                 activation: str = "gelu", record_trace: bool = False) -> FssdpMoE:
-    """One rank per process: heap layout, IPC peer group (world > 1), planner, layer."""
+                 activation: str = "gelu", record_trace: bool = False,
+                 optimizer: bool = False) -> FssdpMoE:
+    """One rank per process: heap layout, IPC peer group (world > 1), planner, layer.
+    optimizer=True reserves the owned shards' AdamW state in the heap (optim.FssdpAdam)."""
     from .engine import ModelConfig
     from .topology import ClusterTopology
 
     m = policy.capacity_override if policy.capacity_override is not None else num_experts
     geom = LayerGeometry(d_model, d_ff, num_experts, top_k, max_tokens, world,
                          default_slots(num_experts, world, m), activation, 0,
-                         policy.reshard_interval > 0)
+                         policy.reshard_interval > 0, optimizer)
     layout = HeapLayout()
     geom.add_regions(layout, "L0.")
     group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
@@ -1051,7 +1114,8 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
 
 
 def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
-                     max_tokens: int, m: int, activation: str = "gelu") -> list:
+                     max_tokens: int, m: int, activation: str = "gelu",
+                     optimizer: bool = False) -> list:
     """Per-layer geometry under the planner's current ShardPlan (even or heterogeneous):
     slot capacity = the most experts any rank owns in that layer + m replica slots.  With
     re-sharding on, a layer may later own up to a device's whole share across layers
@@ -1064,7 +1128,8 @@ def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
         if reshard:
             owned_max = min(E, max(owned_max, -(-(E * len(planner.shards.per_layer)) // D)))
         geoms.append(LayerGeometry(d_model, d_ff, E, top_k, max_tokens, D,
-                                   min(E, owned_max + max(0, m)), activation, owned_max, reshard))
+                                   min(E, owned_max + max(0, m)), activation, owned_max, reshard,
+                                   optimizer))
     return geoms
 
 
@@ -1072,7 +1137,8 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
                  max_tokens: int, policy, *, rank: int = 0, world: int = 1, device="cuda",
                  seed: int = 0, peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
                  per_token_expert_time: float | None = None, pg=None,
-                 activation: str = "gelu", load_profile=None, record_trace: bool = False) -> list:
+                 activation: str = "gelu", load_profile=None, record_trace: bool = False,
+                 optimizer: bool = False) -> list:
     """num_layers FSSDP MoE layers sharing one planner (one iteration = every layer's
     forward, then backward in reverse, then planner.finish()) and one symmetric heap.
     load_profile [L, E] (expected per-expert loads): the initial ShardPlan comes from
@@ -1094,7 +1160,7 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
     if load_profile is not None:
         planner.shards = heterogeneous_sharding(
             GlobalLoadProfile(np.asarray(load_profile, dtype=np.float64)), planner.t, topo)
-    geoms = layer_geometries(planner, d_model, d_ff, top_k, max_tokens, m, activation)
+    geoms = layer_geometries(planner, d_model, d_ff, top_k, max_tokens, m, activation, optimizer)
     layout = HeapLayout()
     for li, geom in enumerate(geoms):
         geom.add_regions(layout, f"L{li}.")
@@ -1121,6 +1187,8 @@ class FssdpMoEFunction(torch.autograd.Function):
 
 def run_lockstep_forward(layers: list, xs: list) -> list:
     """Emulated multi-rank forward: every phase on every logical rank before the next."""
+    for ly in layers:
+        ly.phase_publish()
     for ly in layers:
         ly.phase_prefetch()
     for ly, x in zip(layers, xs):

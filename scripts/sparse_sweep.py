@@ -34,6 +34,12 @@ from paper_2502_02581_b200.comm import HeapLayout, PeerGroup  # noqa: E402
 from paper_2502_02581_b200.plan_tables import NativeTables  # noqa: E402
 
 
+_PEAK_FILE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                          "profiles", "r2_nvlink_peak_n4.json")
+NVLINK_PEAK = (json.load(open(_PEAK_FILE))["nvlink_gbs"] if os.path.exists(_PEAK_FILE)
+               else 770.0)  # measured inbound peer peak (scripts/nvlink_probe.py)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
@@ -153,7 +159,13 @@ def main():
                         "sprs_pull_gbs_bottleneck_fp32":
                             2 * rep.bottleneck_bytes / (res["sprs_pull"] * 1e-3) / 1e9,
                         "sprs_pull_gbs_inbound_max_fp32": 2 * max_in / (res["sprs_pull"] * 1e-3) / 1e9,
-                        "nvlink_peer_gbs_ref": 770.0,
+                        "nvlink_peak_gbs": NVLINK_PEAK,
+                        "spag_frac_of_peak": rep.bottleneck_bytes / (res["spag"] * 1e-3) / 1e9
+                                             / NVLINK_PEAK,
+                        # the reference's bottleneck bytes (costmodel.py:75-84; sprs_traffic is
+                        # spag_traffic transposed), fp32 wire
+                        "sprs_pull_frac_of_peak": 2 * rep.bottleneck_bytes
+                                                  / (res["sprs_pull"] * 1e-3) / 1e9 / NVLINK_PEAK,
                     }
                     print("SWEEP " + json.dumps(line), flush=True)
     dist.barrier()

@@ -24,3 +24,17 @@ def test_dist_fssdp_matches_single_rank(n):
            os.path.join(ROOT, "scripts", "dist_check.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0 and "DIST OK" in res.stdout, res.stdout[-3000:] + res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_dist_training_loop_owner_epochs(n):
+    """AdamW on the owned shards with one rank's update delayed: every replica pulled by
+    the early copy-engine SpAG equals its owner's UPDATED shard (scripts/dist_train_check.py;
+    with FSSDP_EPOCHS=0 the same run reports stale replicas — profiles/r2_train_check.txt)."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + n),
+           os.path.join(ROOT, "scripts", "dist_train_check.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0 and "TRAIN OK" in res.stdout, res.stdout[-3000:] + res.stderr[-3000:]
