@@ -176,6 +176,10 @@ int fssdp_shard_score(int32_t layers, int32_t experts, const int32_t* owner, con
  * slots whose expert has other holders (the SpRS inputs) first, as a separately launchable
  * prefix; the remaining groups restart tile_start at 0, so a wgrad runs as two launches
  * (shared prefix, then the rest) and SpRS can start between them.
+ * slot_layout (nullable): where a local slot's PARAMETERS live.  Null: the layer's own
+ * contiguous region, slot s at index s.  {owned_base, replica_base}: a model-level region —
+ * owned slot i at owned_base + i, replica j at replica_base + j (the SpAG copy list and the
+ * GEMM B offsets use these indices; gradients and staging stay per-layer, owned slots only).
  * Layout semantics: plan_tables.py. */
 #define FSSDP_TAB_HEADER_INTS 29
 #define FSSDP_TAB_ROUTE_CUM 0   /* int32 [E][D+1] */
@@ -197,14 +201,17 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
 int fssdp_build_rank_tables(int32_t rank, int32_t num_devices, int32_t num_experts,
                             const int32_t* base_owner, const uint8_t* target_mask,
                             const uint8_t* pre_mask, const int64_t* route, int32_t d_model,
-                            int32_t d_ff, int32_t n_mats, uint8_t* blob, int64_t blob_bytes,
-                            int32_t* header_out);
+                            int32_t d_ff, int32_t n_mats, const int64_t* slot_layout,
+                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out);
 
 /* The planning critical path in one call: fssdp_plan_layer on this rank's all-gathered
  * int32 counts [D*E], then fssdp_build_rank_tables for `rank` into the pinned `blob`, then
- * (if blob_dev) its upload on `stream`.  Outputs as the two calls'.  limits (nullable):
- * {slot capacity, receive-row capacity, staging-slot capacity} of this rank's buffers; a
- * plan exceeding one returns FSSDP_ERR_INFEASIBLE before anything is uploaded. */
+ * (if blob_dev) its upload on `stream`.  Outputs as the two calls'.  limits (nullable,
+ * 6 entries): {slot capacity, receive-row capacity, staging-slot capacity, owned_base,
+ * replica_base, replica-slot capacity} of this rank's buffers; owned_base < 0 = the
+ * per-layer parameter region (slot_layout null), else the model-level one (slot_layout =
+ * limits + 3; slot capacity then counts owned slots only).  A plan exceeding a capacity
+ * returns FSSDP_ERR_INFEASIBLE before anything is uploaded. */
 int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, const double* est,
                             const int32_t* counts, const fssdp_topology* topo,
                             const fssdp_layer_knobs* knobs, int32_t rank, const uint8_t* pre_mask,
@@ -363,12 +370,13 @@ int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, i
  * emulated ranks (heaps at peer_bases) as the CTAs of one cooperative launch; `rounds`
  * rounds of peer stores -> world barrier (bar_slot, epochs epoch0 ..) -> check.  Each heap
  * needs FSSDP_SELFTEST_BYTES at data_off.  *errors (device int) += mismatched words.
- * bar_slot < 0 skips the barrier: the negative control (stale words expected). */
+ * bar_slot < 0 skips the barrier: the negative control (stale words expected); skew_ns > 0
+ * delays rank r's stores by r * skew_ns each round (makes a missing barrier visible). */
 #define FSSDP_SELFTEST_THREADS 256
 #define FSSDP_SELFTEST_BYTES (2 * 32 * FSSDP_SELFTEST_THREADS * 4)
 int fssdp_barrier_selftest(const uint64_t* peer_bases, int64_t flags_off, int64_t data_off,
                            int32_t world, int32_t rounds, int32_t bar_slot, uint32_t epoch0,
-                           int32_t* errors, void* stream);
+                           int32_t skew_ns, int32_t* errors, void* stream);
 
 /* K4: dispatch.  For token-slot (t, j) with expert e and global rank r within
  * (this source, e) [tile_prefix + slot_rank], the destination d is the first with

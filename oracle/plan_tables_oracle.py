@@ -74,7 +74,7 @@ def _finalize(groups: np.ndarray, n_tiles: int):
 
 
 def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, shared=None,
-                push=None, n_mats: int = 2, seg_rows=None):
+                push=None, n_mats: int = 2, seg_rows=None, param_slots=None):
     """The six grouped-GEMM descriptor arrays of one rank (see gemm_sm100.cu).
 
     Slot s of the parameter region holds [W1 (f x d) | W2 (d x f)] bf16 (GeLU, n_mats 2) or
@@ -91,7 +91,11 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     partial gradient into the owner's staging slot (c_dest = owner + 1) — the SpRS wire.
 
     `seg_rows` (real rows per segment): the wgrads' K stops at the first 64-row K block
-    boundary past them (the zero padding beyond would only add exact zeros)."""
+    boundary past them (the zero padding beyond would only add exact zeros).
+
+    `param_slots` (per segment, default slot_of_seg): the parameter slot B is read from
+    (a model-level parameter region, fssdp_build_rank_tables slot_layout); gradient slots
+    stay slot_of_seg."""
     d, f, nm = d_model, d_ff, n_mats
     n1 = (nm - 1) * f
     bn1, bnf = n_tile_widths(f, nm)
@@ -99,25 +103,26 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     shared = [False] * n if shared is None else [bool(x) for x in shared]
     k_rows = seg_padded if seg_rows is None else (np.asarray(seg_rows, dtype=np.int64) + 63) // 64 * 64
     push = [None] * n if push is None else list(push)
+    pslot = list(slot_of_seg) if param_slots is None else list(param_slots)
     out = {}
     g = np.zeros(n, dtype=GROUP_DTYPE)
     for i in range(n):
-        s = slot_of_seg[i]
+        s = pslot[i]
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * f, 0, d // 64, 0, st * n1)
     out["fwd1"] = _finalize(g.copy(), n1 // bn1)
     for i in range(n):
-        s = slot_of_seg[i]
+        s = pslot[i]
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * d, 0, f // 64, 0, st * d)
     out["fwd2"] = _finalize(g.copy(), d // 256)
     for i in range(n):  # dH = dY . W2  (B = W2 [K=d][N=f], MN-major)
-        s = slot_of_seg[i]
+        s = pslot[i]
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * d, d // 64, 0, st * n1)
     out["dgrad2"] = _finalize(g.copy(), n_tiles_f(f))
     for i in range(n):  # dXe = dA . W1  (B = W1 / W13 [K=n1][N=d], MN-major)
-        s = slot_of_seg[i]
+        s = pslot[i]
         st = int(seg_start[i])
         g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * f, n1 // 64, 0, st * d)
     out["dgrad1"] = _finalize(g.copy(), d // 256)
@@ -143,8 +148,9 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
 
 def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray,
                       route: np.ndarray, d_model: int, d_ff: int, pre_mask=None,
-                      n_mats: int = 2) -> RankTables:
-    """`pre_mask` (E, D): replicas already fetched by an earlier SpAG (same slots, no copy)."""
+                      n_mats: int = 2, slot_layout=None) -> RankTables:
+    """`pre_mask` (E, D): replicas already fetched by an earlier SpAG (same slots, no copy).
+    `slot_layout` (owned_base, replica_base): parameter slots in a model-level region."""
     E, D = target_mask.shape
     if route.shape != (D, E, D):
         raise InternalError(f"route shape {route.shape} != {(D, E, D)}")
@@ -166,12 +172,19 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
             if padded[s] > rows[s]]
     zero_rows = np.array(zero, dtype=np.int32).reshape(-1, 2)
 
+    n_own = sum(1 for e in slots if int(base_owner[e]) == rank)
+
+    def pslot(s, owned):
+        if slot_layout is None:
+            return s
+        return slot_layout[0] + s if s < owned else slot_layout[1] + (s - owned)
+
     # SpAG: replicas this rank materializes, pulled from the owner's slot
     copies = []
     for e, s in sorted(slots.items(), key=lambda kv: kv[1]):
         o = int(base_owner[e])
         if o != rank and not (pre_mask is not None and pre_mask[e, rank]):
-            copies.append((o, maps[o][e], s))
+            copies.append((o, pslot(maps[o][e], E), pslot(s, n_own)))
     spag = np.array(copies, dtype=np.int32).reshape(-1, 3)
 
     # SpRS by push: staging index of (expert, holder) on the expert's owner — the owner's
@@ -210,7 +223,7 @@ def build_rank_tables(rank: int, base_owner: np.ndarray, target_mask: np.ndarray
     push = [None if int(base_owner[by_slot[s]]) == rank else
             (int(base_owner[by_slot[s]]), stage[(by_slot[s], rank)]) for s in order]
     groups, wgrad_split = gemm_groups(start, padded, order, d_model, d_ff, shared, push, n_mats,
-                                      seg_rows=rows)
+                                      seg_rows=rows, param_slots=[pslot(s, n_own) for s in order])
     n_owned = sum(1 for e in slots if int(base_owner[e]) == rank)
     return RankTables(rank=rank, world=D, slots=slots, n_owned=n_owned, seg_start=start,
                       seg_rows=rows, seg_padded=padded, recv_rows=int(padded.sum()),

@@ -103,8 +103,8 @@ _SIGS = {
                          P_i64, P_f64, P_i32],
     "fssdp_shard_score": [i32, i32, P_i32, P_f64, P_topo, P_f64],
     "fssdp_tables_layout": [i32, i32, P_i64, P_i64],
-    "fssdp_build_rank_tables": [i32, i32, i32, P_i32, P_u8, P_u8, P_i64, i32, i32, i32, vp, i64,
-                                P_i32],
+    "fssdp_build_rank_tables": [i32, i32, i32, P_i32, P_u8, P_u8, P_i64, i32, i32, i32, vp, vp,
+                                i64, P_i32],
     "fssdp_plan_candidate": [i32, P_i32, P_f64, P_topo, C.POINTER(LayerKnobs), P_u8, P_i32],
     "fssdp_plan_layer_tables": [i32, P_i32, P_f64, P_i32, P_topo, C.POINTER(LayerKnobs), i32,
                                 P_u8, i32, i32, i32, P_i64, P_u8, P_i32, P_i64, P_f64, P_i32, vp,
@@ -124,7 +124,7 @@ _SIGS = {
                          i32, i32, i32, C.c_uint32, vp, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
-    "fssdp_barrier_selftest": [vp, i64, i64, i32, i32, i32, u32, vp, vp],
+    "fssdp_barrier_selftest": [vp, i64, i64, i32, i32, i32, u32, i32, vp, vp],
     "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
                        i64, i32, i32, u32, vp, vp],
     "fssdp_combine": [vp, vp, vp, i64, i32, i32, vp, i64, vp, vp, vp],

@@ -184,18 +184,23 @@ int fssdp_plan_layer_tables(int32_t num_experts, const int32_t* base_owner, cons
   int rc = fssdp_plan_layer(num_experts, base_owner, est, actual, topo, knobs, target_out,
                             added_out, route_out, doubles_out, flags_out);
   if (rc != kOk) return rc;
+  // limits[3] >= 0: a model-level parameter region {owned_base, replica_base} (limits[3..4])
+  const bool split = limits != nullptr && limits[3] >= 0;
   rc = fssdp_build_rank_tables(rank, static_cast<int32_t>(D), num_experts, base_owner, target_out,
-                               pre_mask, route_out, d_model, d_ff, n_mats, blob, blob_bytes,
-                               header_out);
+                               pre_mask, route_out, d_model, d_ff, n_mats,
+                               split ? limits + 3 : nullptr, blob, blob_bytes, header_out);
   if (rc != kOk) return rc;
   if (limits != nullptr) {  // header: [0] slots, [2] receive rows, [28] staging slots
-    const int64_t need[3] = {header_out[0], header_out[2], header_out[28]};
-    static const char* what[3] = {"expert slots", "receive rows", "staging slots"};
-    for (int i = 0; i < 3; ++i)
-      if (need[i] > limits[i]) {
+    // split layout: [0] is the owned-slot capacity, limits[5] the replica-slot capacity
+    const int64_t need[4] = {split ? header_out[1] : header_out[0], header_out[2], header_out[28],
+                             split ? header_out[0] - header_out[1] : 0};
+    static const char* what[4] = {"expert slots", "receive rows", "staging slots",
+                                  "replica slots"};
+    for (int i = 0; i < (split ? 4 : 3); ++i)
+      if (need[i] > limits[i == 3 ? 5 : i]) {
         char msg[160];
         snprintf(msg, sizeof(msg), "plan needs %lld %s > capacity %lld", (long long)need[i],
-                 what[i], (long long)limits[i]);
+                 what[i], (long long)limits[i == 3 ? 5 : i]);
         set_error(msg);
         return FSSDP_ERR_INFEASIBLE;
       }

@@ -110,11 +110,13 @@ __device__ __forceinline__ uint32_t selftest_stamp(int round, int writer, int i)
 
 __global__ void barrier_selftest_kernel(const uint64_t* __restrict__ peer_bases,
                                         int64_t flags_off, int64_t data_off, int world,
-                                        int rounds, int slot, uint32_t epoch0, int* errors) {
+                                        int rounds, int slot, uint32_t epoch0, int skew_ns,
+                                        int* errors) {
   const int rank = blockIdx.x;
   const int n = blockDim.x;
   int bad = 0;
   for (int k = 0; k < rounds; ++k) {
+    if (skew_ns > 0) __nanosleep(static_cast<unsigned>(rank) * static_cast<unsigned>(skew_ns));
     const int64_t blk = (static_cast<int64_t>(k & 1) * kMaxWorld + rank) * n + threadIdx.x;
     for (int p = 0; p < world; ++p)
       reinterpret_cast<uint32_t*>(peer_bases[p] + data_off)[blk] =
@@ -1659,7 +1661,7 @@ int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, i
 
 int fssdp_barrier_selftest(const uint64_t* peer_bases, int64_t flags_off, int64_t data_off,
                            int32_t world, int32_t rounds, int32_t bar_slot, uint32_t epoch0,
-                           int32_t* errors, void* stream) {
+                           int32_t skew_ns, int32_t* errors, void* stream) {
   if (world <= 0 || world > kMaxWorld || rounds <= 0) {
     set_error("barrier_selftest: bad world/rounds");
     return kErrDimension;
@@ -1672,7 +1674,8 @@ int fssdp_barrier_selftest(const uint64_t* peer_bases, int64_t flags_off, int64_
     return kErrCuda;
   }
   int threads = kSelftestThreads;
-  void* args[] = {&peer_bases, &flags_off, &data_off, &world, &rounds, &bar_slot, &epoch0, &errors};
+  void* args[] = {&peer_bases, &flags_off, &data_off, &world,   &rounds,
+                  &bar_slot,   &epoch0,    &skew_ns,  &errors};
   timing_begin(as_stream(stream));
   const cudaError_t err = cudaLaunchCooperativeKernel(
       reinterpret_cast<const void*>(barrier_selftest_kernel), dim3(world), dim3(threads), args,

@@ -1093,7 +1093,8 @@ int fssdp_tables_layout(int32_t num_experts, int32_t num_devices, int64_t* offse
 int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* base_owner,
                             const uint8_t* target_mask, const uint8_t* pre_mask,
                             const int64_t* route, int32_t d_model, int32_t d_ff, int32_t n_mats,
-                            uint8_t* blob, int64_t blob_bytes, int32_t* header_out) {
+                            const int64_t* slot_layout, uint8_t* blob, int64_t blob_bytes,
+                            int32_t* header_out) {
   // pre_mask (nullable): replicas already fetched by the early, estimate-based SpAG.  They
   // take the first replica slots (ascending expert id) and get no SpAG copy here.
   auto pre = [&](int e, int d) {
@@ -1160,19 +1161,26 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       zero[2 * n_zero + 1] = static_cast<int32_t>(seg_pad[rank][s] - seg_rows[rank][s]);
       ++n_zero;
     }
+  // parameter slot of local slot s (owned slots first, then replicas): the layer's own
+  // contiguous region (slot_layout null) or, in a model-level parameter region, owned slot i
+  // at owned_base + i and replica j at replica_base + j — replicas of every layer may share
+  // one region (re-materialization keeps only one layer's replicas resident)
+  int n_owned = 0;
+  for (int s = 0; s < n_slots; ++s) n_owned += base_owner[slot_expert[rank][s]] == rank;
+  auto pslot = [&](int s, int owned) -> int32_t {
+    if (slot_layout == nullptr) return s;
+    return static_cast<int32_t>(s < owned ? slot_layout[0] + s : slot_layout[1] + (s - owned));
+  };
   int32_t* spag = reinterpret_cast<int32_t*>(blob + off[FSSDP_TAB_SPAG]);
-  int n_spag = 0, n_owned = 0;
+  int n_spag = 0;
   for (int s = 0; s < n_slots; ++s) {
     const int e = slot_expert[rank][s];
     const int o = base_owner[e];
-    if (o == rank) {
-      ++n_owned;
-      continue;
-    }
+    if (o == rank) continue;
     if (pre(e, rank)) continue;  // fetched early
     spag[3 * n_spag] = o;
-    spag[3 * n_spag + 1] = slot_of[o][e];
-    spag[3 * n_spag + 2] = s;
+    spag[3 * n_spag + 1] = pslot(slot_of[o][e], E);  // an owned slot on the owner
+    spag[3 * n_spag + 2] = pslot(s, n_owned);
     ++n_spag;
   }
   // SpRS by push: a holder's wgrad epilogue writes its partial of a replica straight into
@@ -1262,7 +1270,8 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
       // beyond it would only add exact zeros
       const int32_t kt = static_cast<int32_t>((seg_rows[rank][s] + 63) / 64);
       fssdp_gemm_group& x = g[i];
-      const int32_t w1r = static_cast<int32_t>(s * nm * f), w2r = static_cast<int32_t>(s * nm * d);
+      const int64_t ps = pslot(s, n_owned);
+      const int32_t w1r = static_cast<int32_t>(ps * nm * f), w2r = static_cast<int32_t>(ps * nm * d);
       switch (gi) {
         case 0: x = {mt, 0, st, 0, w1r, 0, static_cast<int32_t>(d / 64), 0, st * n1}; break;
         case 1: x = {mt, 0, st, 0, w2r, 0, static_cast<int32_t>(f / 64), 0, st * d}; break;

@@ -105,7 +105,9 @@ class MemoryBreakdown:
 def memory_report(plan: ShardPlan, materializations, config: ModelConfig,
                   mode: str = "retain") -> MemoryBreakdown:
     """Expert memory per device; retain = Σ layers' replicas, rematerialize = max
-    (engine.py:188-226).  Sizes the replica buffers of the device layer."""
+    (engine.py:188-226).  The device layer reserves the worst case of it: m replica slots
+    per layer (retain) or one shared set of m for all layers (rematerialize) —
+    layer.model_regions / replica_region_bytes."""
     if mode not in ("retain", "rematerialize"):
         raise ConfigError(f"unknown memory mode {mode!r}")
     D = plan.num_devices

@@ -30,7 +30,7 @@ import torch
 from . import _native as N
 from . import ops
 from .comm import HeapLayout, PeerGroup
-from .engine import FssdpPlanner
+from .engine import FssdpPlanner, PolicyKind
 from .errors import DimensionError, InternalError
 from .plan_tables import NativeTables, _layout, n_tile_widths
 
@@ -55,6 +55,12 @@ class LayerGeometry:
     owned_max: int = 0        # max experts of this layer a rank owns (0: ceil(E / world))
     reshard: bool = False     # heterogeneous re-sharding enabled: a staging region for moves
     optimizer: bool = False   # AdamW state (fp32 master, m, v) of the owned shards in the heap
+    # model-level parameter region (model_regions): this layer's owned slots start at
+    # owned_base, its replica slots at replica_base (shared by every layer under
+    # re-materialization); -1: the layer's own contiguous [owned | replica] region
+    owned_base: int = -1
+    replica_base: int = -1
+    param_slots_total: int = 0  # slots of the model-level region (its TMA extent)
 
     @property
     def n_mats(self) -> int:  # expert matrices per slot
@@ -80,6 +86,15 @@ class LayerGeometry:
     @property
     def expert_bytes(self) -> int:
         return self.slot_param_bytes
+
+    @property
+    def split(self) -> bool:
+        return self.owned_base >= 0
+
+    @property
+    def replica_cap(self) -> int:
+        """Replica slots this layer may fill in one iteration."""
+        return max(0, self.slots - self.owned_cap)
 
     @property
     def owned_cap(self) -> int:
@@ -110,8 +125,12 @@ class LayerGeometry:
 
     def add_regions(self, layout: HeapLayout, prefix: str) -> None:
         d, R = self.d_model, self.recv_cap
-        layout.add(prefix + "params", self.slots * self.slot_param_bytes)
-        layout.add(prefix + "grads", self.slots * self.slot_grad_elems * 4)
+        if not self.split:
+            layout.add(prefix + "params", self.slots * self.slot_param_bytes)
+        # gradients: a replica's partial goes straight to its owner's staging slot (the
+        # wgrad epilogue's c_dest stores), so the split layout keeps owned slots only
+        grad_slots = self.owned_cap if self.split and self.world > 1 else self.slots
+        layout.add(prefix + "grads", grad_slots * self.slot_grad_elems * 4)
         layout.add(prefix + "xrecv", R * d * 2)
         layout.add(prefix + "y", R * d * 2)
         layout.add(prefix + "dyrecv", R * d * 2)
@@ -129,6 +148,50 @@ class LayerGeometry:
 
 def default_slots(num_experts: int, world: int, m: int) -> int:
     return min(num_experts, -(-num_experts // world) + max(0, m))
+
+
+def model_regions(layout: HeapLayout, geoms: list, rematerialize: bool,
+                  prefix: str = "L{}.") -> list:
+    """The model-level parameter region plus every layer's own regions; returns the
+    geometries with their slot bases.  Owned slots of every layer persist (they ARE the
+    shards); replica slots follow moesim's memory model (memory_report, engine.py:188-226):
+    retain = each layer keeps its replicas from forward to backward (Σ over layers),
+    rematerialize = ONE replica region shared by every layer (max over layers) — a layer's
+    backward re-gathers its replicas (FssdpMoE.backward, phase_spag(refetch_early=True))."""
+    from dataclasses import replace
+
+    if not geoms:
+        return []
+    sb = {g.slot_param_bytes for g in geoms}
+    if len(sb) != 1:
+        raise DimensionError("layers of one model need equal expert shapes")
+    owned_bases, ob = [], 0
+    for g in geoms:
+        owned_bases.append(ob)
+        ob += g.owned_cap
+    rep_bases, rb = [], ob
+    for g in geoms:
+        rep_bases.append(ob if rematerialize else rb)
+        rb += 0 if rematerialize else g.replica_cap
+    total = ob + (max(g.replica_cap for g in geoms) if rematerialize else rb - ob)
+    layout.add("params", max(1, total) * sb.pop())
+    out = []
+    for li, g in enumerate(geoms):
+        ng = replace(g, owned_base=owned_bases[li], replica_base=rep_bases[li],
+                     param_slots_total=total)
+        ng.add_regions(layout, prefix.format(li))
+        out.append(ng)
+    return out
+
+
+def replica_region_bytes(geoms: list) -> int:
+    """Bytes of replica parameter slots the heap holds for these (split) geometries."""
+    if not geoms or not geoms[0].split:
+        return sum(g.replica_cap * g.slot_param_bytes for g in geoms)
+    bases = {g.replica_base for g in geoms}
+    if len(bases) == 1 and len(geoms) > 1:  # shared (re-materialization)
+        return max(g.replica_cap for g in geoms) * geoms[0].slot_param_bytes
+    return sum(g.replica_cap for g in geoms) * geoms[0].slot_param_bytes
 
 
 class FssdpMoE:
@@ -153,8 +216,17 @@ class FssdpMoE:
         heap = group.local
         d, f, E, R = geom.d_model, geom.d_ff, geom.num_experts, geom.recv_cap
         self.off = {k: L.offset(prefix + k) for k in
-                    ("params", "grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage",
-                     "reshard")}
+                    ("grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage", "reshard")}
+        # parameter slots: "params" = the region the plan tables' slot indices address
+        # (model-level in the split layout), "owned" = this layer's first owned slot
+        sb = geom.slot_param_bytes
+        if geom.split:
+            self.off["params"] = L.offset("params")
+            self.off["owned"] = self.off["params"] + geom.owned_base * sb
+            n_param_slots = geom.param_slots_total
+        else:
+            self.off["params"] = self.off["owned"] = L.offset(prefix + "params")
+            n_param_slots = geom.slots
         self.opt_state = None  # {"master", "m", "v"}: [owned_cap, slot elems] fp32 heap views
         if geom.optimizer:
             for k in ("opt_master", "opt_m", "opt_v", "reshard_opt"):
@@ -165,9 +237,19 @@ class FssdpMoE:
         self.epoch_slot = EPOCH_SLOT0 + layer_index
         self._fwd_epoch = 0
         self.flags_off = L.offset("flags")
-        self.params = heap.tensor(self.off["params"], (geom.slots, geom.n_mats * d * f),
-                                  torch.bfloat16)
-        self.grads = heap.tensor(self.off["grads"], (geom.slots, geom.n_mats * d * f),
+        # params: this layer's slots from its first owned one — in the split layout only the
+        # owned slots (replicas: self.replicas, see slot_params)
+        self.param_region = heap.tensor(self.off["params"], (n_param_slots, geom.n_mats * d * f),
+                                        torch.bfloat16)
+        if geom.split:
+            self.params = self.param_region[geom.owned_base:geom.owned_base + geom.owned_cap]
+            self.replicas = self.param_region[geom.replica_base:
+                                              geom.replica_base + geom.replica_cap]
+        else:
+            self.params = self.param_region
+            self.replicas = None
+        grad_slots = geom.owned_cap if geom.split and self.world > 1 else geom.slots
+        self.grads = heap.tensor(self.off["grads"], (grad_slots, geom.n_mats * d * f),
                                  torch.float32)
         self.xrecv = heap.tensor(self.off["xrecv"], (R, d), torch.bfloat16)
         self.y_e = heap.tensor(self.off["y"], (R, d), torch.bfloat16)
@@ -195,9 +277,9 @@ class FssdpMoE:
             self.dest_maps[name] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.dev)
         # 2-D TMA views of the parameter region (nm = matrices per slot, n1 = (nm-1) f)
         nm, n1 = geom.n_mats, geom.n1
-        flat = self.params.view(-1)
-        self.w1_view = flat.view(geom.slots * nm * f, d)              # W1/W13 of slot s: rows s*nm*f..
-        self.w2_view = flat[n1 * d:].view(geom.slots * nm * d - (nm - 1) * d, f)  # W2: rows s*nm*d..
+        flat = self.param_region.view(-1)
+        self.w1_view = flat.view(n_param_slots * nm * f, d)           # W1/W13 of slot s: rows s*nm*f..
+        self.w2_view = flat[n1 * d:].view(n_param_slots * nm * d - (nm - 1) * d, f)  # W2: rows s*nm*d..
         # local activations (capacity-sized once, so plans never reallocate): fwd1 saves
         # gelu'(a) (GeLU) or the pre-activations [a1|a3] (SwiGLU) for dgrad2's epilogue
         self.gprime = torch.empty(R, n1, dtype=torch.bfloat16, device=self.dev)
@@ -257,7 +339,12 @@ class FssdpMoE:
         self.tables = None
         self._cs = None  # launching stream during forward()/backward()
         self._plan_pending = False
-        self._limits = np.array([geom.slots, geom.recv_cap, geom.stage_slots], dtype=np.int64)
+        # plan capacity limits + the parameter slot layout (fssdp_plan_layer_tables)
+        self._slot_layout = (geom.owned_base, geom.replica_base) if geom.split else None
+        self._limits = np.array(
+            [geom.owned_cap if geom.split else geom.slots, geom.recv_cap, geom.stage_slots,
+             geom.owned_base if geom.split else -1, geom.replica_base, geom.replica_cap],
+            dtype=np.int64)
         self._limits_ptr = self._limits.ctypes.data
         self._tab_ptrs = None
         self._dispatch_args = None
@@ -333,6 +420,14 @@ class FssdpMoE:
             return buf[s, : f * d].view(f, d), w2
         w1, w3 = self.unpack_w13(buf[s, : n1 * d].view(n1, d))
         return w1, w3, w2
+
+    def slot_params(self, s: int) -> torch.Tensor:
+        """Parameters of local slot s of the current plan (owned slots first, then the
+        replicas SpAG materialized) — a view into the parameter region."""
+        n_owned = self.tables.n_owned if self.tables is not None else self._n_owned
+        if self.replicas is None or s < n_owned:
+            return self.params[s]
+        return self.replicas[s - n_owned]
 
     def expert_weight(self, e: int):
         """(W1 [f,d], W2 [d,f]) of an owned expert (views into the heap); SwiGLU: (W1, W3,
@@ -416,8 +511,9 @@ class FssdpMoE:
         E, D = pre.shape
         tables = NativeTables(self.rank, base_owner, pre, np.zeros((D, E, D), dtype=np.int64),
                               self.g.d_model, self.g.d_ff, out_bytes=self.pre_host_np,
-                              n_mats=self.g.n_mats)
-        if tables.n_slots > self.g.slots:
+                              n_mats=self.g.n_mats, slot_layout=self._slot_layout)
+        n_rep, rep_cap = tables.n_slots - tables.n_owned, self.g.slots - self.g.owned_cap
+        if tables.n_slots > self.g.slots or (self.g.split and n_rep > rep_cap):
             raise InternalError(f"early plan needs {tables.n_slots} slots > capacity {self.g.slots}")
         self.pre_mask, self.pre_mask_ptr, self.pre_tables = pre, pre.ctypes.data, tables
         if tables.n_spag == 0:
@@ -709,6 +805,8 @@ class FssdpMoE:
             main.wait_event(self._pre_done)
             self._pre_done = None
         if refetch_early and self.pre_tables is not None and self.pre_tables.n_spag:
+            if self._pre_staged is not None:  # pre_dev was uploaded on the side stream
+                main.wait_event(self._pre_staged)
             self._spag_launch("spag_pre", self.pre_dev, self.pre_tables, main)
         if self.tables.n_spag:
             self._spag_launch("spag", self.blob_dev, self.tables, main)
@@ -757,7 +855,7 @@ class FssdpMoE:
         self._reshard_pending = None
         self.phase_barrier(BAR_RESHARD)  # every old owner has staged its shards
         self._call("fssdp_gather_slots", self._pb(), self.rank, self.off["reshard"],
-                   self.off["params"], self.g.slot_param_bytes, 0, ops._ptr(copies),
+                   self.off["owned"], self.g.slot_param_bytes, 0, ops._ptr(copies),
                    copies.shape[0], 0, self._stream())
         if self.opt_state is not None:  # fp32 master / exp_avg / exp_avg_sq: 6x expert_bytes
             sb = self.g.slot_grad_elems * 4
@@ -1095,22 +1193,22 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
                  optimizer: bool = False) -> FssdpMoE:
     """One rank per process: heap layout, IPC peer group (world > 1), planner, layer.
     optimizer=True reserves the owned shards' AdamW state in the heap (optim.FssdpAdam)."""
-    from .engine import ModelConfig
-    from .topology import ClusterTopology
+    (layer,) = create_model(1, d_model, d_ff, num_experts, top_k, max_tokens, policy, rank=rank,
+                            world=world, device=device, seed=seed, peer_bw=peer_bw,
+                            attn_fwd_time=attn_fwd_time,
+                            per_token_expert_time=per_token_expert_time, pg=pg,
+                            activation=activation, record_trace=record_trace,
+                            optimizer=optimizer)
+    return layer
 
-    m = policy.capacity_override if policy.capacity_override is not None else num_experts
-    geom = LayerGeometry(d_model, d_ff, num_experts, top_k, max_tokens, world,
-                         default_slots(num_experts, world, m), activation, 0,
-                         policy.reshard_interval > 0, optimizer)
-    layout = HeapLayout()
-    geom.add_regions(layout, "L0.")
-    group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
-    topo = ClusterTopology.for_nvswitch(world, peer_bw)
-    if per_token_expert_time is None:  # fwd expert time per token-slot at the sustained bf16 peak
-        per_token_expert_time = 2.0 * geom.n_mats * d_model * d_ff / 1381.7e12
-    cfg = ModelConfig(1, num_experts, geom.expert_bytes, 2 * d_model, attn_fwd_time,
-                      per_token_expert_time)
-    return FssdpMoE(geom, group, FssdpPlanner(cfg, topo, policy, record_trace), 0, seed)
+
+def replica_slots(planner: FssdpPlanner) -> int:
+    """Replica slots per layer and rank: the planner's m (capacity_override, else
+    free_bytes_per_device // expert_bytes, else every expert — engine.py:389-402); none for
+    EP or when nothing can be fetched (t or m <= 0: FSSDP degenerates to EP)."""
+    if planner.policy.kind != PolicyKind.FSSDP or planner.t <= 0 or planner.m <= 0:
+        return 0
+    return int(planner.m)
 
 
 def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
@@ -1148,7 +1246,6 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
     from .topology import ClusterTopology
 
     nm = 3 if activation == "swiglu" else 2
-    m = policy.capacity_override if policy.capacity_override is not None else num_experts
     topo = ClusterTopology.for_nvswitch(world, peer_bw)
     if per_token_expert_time is None:
         per_token_expert_time = 2.0 * nm * d_model * d_ff / 1381.7e12
@@ -1160,10 +1257,11 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
     if load_profile is not None:
         planner.shards = heterogeneous_sharding(
             GlobalLoadProfile(np.asarray(load_profile, dtype=np.float64)), planner.t, topo)
-    geoms = layer_geometries(planner, d_model, d_ff, top_k, max_tokens, m, activation, optimizer)
+    geoms = layer_geometries(planner, d_model, d_ff, top_k, max_tokens, replica_slots(planner),
+                             activation, optimizer)
     layout = HeapLayout()
-    for li, geom in enumerate(geoms):
-        geom.add_regions(layout, f"L{li}.")
+    # owned slots per layer; replica slots per layer (retain) or one shared set (remat)
+    geoms = model_regions(layout, geoms, policy.rematerialize)
     group = PeerGroup(layout, rank, world, device, "dist", pg=pg)
     return [FssdpMoE(geom, group, planner, li, seed, prefix=f"L{li}.")
             for li, geom in enumerate(geoms)]

@@ -69,7 +69,7 @@ class NativeTables:
     _hdr_ptr = _hdr.ctypes.data
 
     def __init__(self, rank, base_owner, target_mask, route, d_model, d_ff, out_bytes=None,
-                 pre_mask=None, n_mats=2):
+                 pre_mask=None, n_mats=2, slot_layout=None):
         E, D = target_mask.shape
         _, nbytes = _layout(E, D)
         blob = out_bytes if out_bytes is not None else np.zeros(nbytes, dtype=np.uint8)
@@ -77,18 +77,19 @@ class NativeTables:
         mask = np.ascontiguousarray(target_mask, dtype=np.uint8)
         rt = np.ascontiguousarray(route, dtype=np.int64)
         pre = None if pre_mask is None else np.ascontiguousarray(pre_mask, dtype=np.uint8)
+        lay = None if slot_layout is None else np.ascontiguousarray(slot_layout, dtype=np.int64)
         self._build(rank, E, D, owner.ctypes.data, mask.ctypes.data,
                     None if pre is None else pre.ctypes.data, rt.ctypes.data, d_model, d_ff,
-                    blob, blob.ctypes.data, n_mats)
+                    blob, blob.ctypes.data, n_mats, None if lay is None else lay.ctypes.data)
 
     @classmethod
     def from_pointers(cls, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff,
-                      blob, blob_ptr, n_mats=2) -> "NativeTables":
+                      blob, blob_ptr, n_mats=2, layout_ptr=None) -> "NativeTables":
         """Planning critical path: inputs already in place (FssdpPlanner scratch buffers),
         addresses resolved by the caller."""
         obj = cls.__new__(cls)
         obj._build(rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
-                   blob_ptr, n_mats)
+                   blob_ptr, n_mats, layout_ptr)
         return obj
 
     @classmethod
@@ -112,7 +113,7 @@ class NativeTables:
         self.n_stage = h[28]
 
     def _build(self, rank, E, D, owner_ptr, mask_ptr, pre_ptr, route_ptr, d_model, d_ff, blob,
-               blob_ptr, n_mats=2) -> None:
+               blob_ptr, n_mats=2, layout_ptr=None) -> None:
         from . import _native as N
 
         self.E, self.D = E, D
@@ -121,8 +122,9 @@ class NativeTables:
         if len(blob) < self.nbytes:
             raise InternalError("plan tables exceed the staging buffer")
         N.check(N.LIB_RAW.fssdp_build_rank_tables(rank, D, E, owner_ptr, mask_ptr, pre_ptr,
-                                                  route_ptr, d_model, d_ff, n_mats, blob_ptr,
-                                                  self.nbytes, self._hdr_ptr), "build_rank_tables")
+                                                  route_ptr, d_model, d_ff, n_mats, layout_ptr,
+                                                  blob_ptr, self.nbytes, self._hdr_ptr),
+                "build_rank_tables")
         self._parse_header()
 
     def section(self, name, dtype, count):

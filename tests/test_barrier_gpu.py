@@ -33,7 +33,7 @@ def test_world_barrier_orders_peer_stores(world):
     epoch = 1
     for rounds in (1, 257, 2000):  # epochs keep growing across launches, never reset
         N.call("fssdp_barrier_selftest", pb, flags, off, world, rounds, 5, C.c_uint32(epoch),
-               C.c_void_p(errors.data_ptr()), stream)
+               2000 if rounds == 257 else 0, C.c_void_p(errors.data_ptr()), stream)
         epoch += rounds
         torch.cuda.synchronize()
         assert int(errors.item()) == 0, f"{errors.item()} stale words at world {world}"
@@ -44,14 +44,14 @@ def test_world_barrier_orders_peer_stores(world):
 
 
 def test_selftest_detects_a_missing_barrier():
-    """Negative control: the same rounds with the barrier skipped (slot -1) must read stale
-    stamps — the check above is live."""
+    """Negative control: the same rounds with the barrier skipped (slot -1) and the ranks'
+    stores skewed by 2 us per rank must read stale stamps — the check above is live."""
     layout = HeapLayout()
     off = layout.add("selftest", SELFTEST_BYTES)
     g = emulated_group(layout, 8)[0]
     errors = torch.zeros(1, dtype=torch.int32, device="cuda")
     N.call("fssdp_barrier_selftest", C.c_void_p(g.peer_bases.data_ptr()), layout.offset("flags"),
-           off, 8, 2000, -1, C.c_uint32(1), C.c_void_p(errors.data_ptr()),
+           off, 8, 500, -1, C.c_uint32(1), 2000, C.c_void_p(errors.data_ptr()),
            C.c_void_p(torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     assert int(errors.item()) > 0
@@ -63,5 +63,5 @@ def test_selftest_rejects_bad_arguments():
     g = emulated_group(layout, 2)[0]
     with pytest.raises(Exception):
         N.call("fssdp_barrier_selftest", C.c_void_p(g.peer_bases.data_ptr()),
-               layout.offset("flags"), 0, 33, 1, 0, C.c_uint32(1), None,
+               layout.offset("flags"), 0, 33, 1, 0, C.c_uint32(1), 0, None,
                C.c_void_p(torch.cuda.current_stream().cuda_stream))

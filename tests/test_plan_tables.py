@@ -67,9 +67,13 @@ def test_native_tables_equal_python_tables():
         d, f, nm = shapes[it % len(shapes)]
         dec, _ = _random_plan(rng, D, E, 300, 2)
         owner = dec.base.owners()
+        # every other case: a model-level parameter region (owned_base, replica_base)
+        lay = None if it % 2 == 0 else (int(rng.integers(0, 40)), int(rng.integers(40, 90)))
         for r in range(D):
-            py = build_rank_tables(r, owner, dec.target.mask, dec.route, d, f, n_mats=nm)
-            nt = NativeTables(r, owner, dec.target.mask, dec.route, d, f, n_mats=nm)
+            py = build_rank_tables(r, owner, dec.target.mask, dec.route, d, f, n_mats=nm,
+                                   slot_layout=lay)
+            nt = NativeTables(r, owner, dec.target.mask, dec.route, d, f, n_mats=nm,
+                              slot_layout=lay)
             assert nt.slots == py.slots and nt.n_owned == py.n_owned
             assert nt.recv_rows == py.recv_rows
             for name in ("seg_start", "seg_rows", "seg_padded", "route_cum", "recv_base",
