@@ -53,7 +53,7 @@ def main():
         early += layer.pre_tables.n_spag if layer.pre_tables is not None else 0
         # every replica slot vs its owner's current shard
         t = layer.tables
-        mine = {int(e): digest(layer.params[s]) for s, e in enumerate(t.slot_expert)}
+        mine = {int(e): digest(layer.slot_params(s)) for s, e in enumerate(t.slot_expert)}
         allm = [None] * world
         dist.all_gather_object(allm, mine)
         dec = layer.decision
