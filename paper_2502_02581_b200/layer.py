@@ -913,6 +913,11 @@ class FssdpMoE:
     # the last wgrads (interleaved A/B at N=1: 0.3-0.5 % faster there, cfg2 and cfg4)
     EARLY_GATE = os.environ.get("FSSDP_EARLY_GATE", "1") != "0"
 
+    # experiment: where the dX combine and (N = 1) the gate backward run — "overlap" (dx
+    # stream beside the remaining wgrads), "gate_end" (gate backward after them on the main
+    # stream), "serial" (both after them)
+    DX_MODE = os.environ.get("FSSDP_DX_MODE", "overlap")
+
     @property
     def _early_gate(self) -> bool:
         return self.EARLY_GATE and 4 % self.g.top_k == 0 and self.world > 1
@@ -1137,12 +1142,19 @@ class FssdpMoE:
         dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
         dxs = self._dx_stream()
         dxs.wait_stream(main)
-        with self._on(dxs):
+        mode = self.DX_MODE
+        if mode != "serial":
+            with self._on(dxs):
+                self.phase_barrier(BAR_DX)
+                self.phase_combine_dx(dx)
+                if not self._early_gate and mode != "gate_end":
+                    self.phase_gate_wgrad()
+        self.phase_wgrad_rest()
+        if mode == "serial":
             self.phase_barrier(BAR_DX)
             self.phase_combine_dx(dx)
-            if not self._early_gate:
-                self.phase_gate_wgrad()
-        self.phase_wgrad_rest()
+        if not self._early_gate and mode in ("serial", "gate_end"):
+            self.phase_gate_wgrad()
         main.wait_stream(dxs)
         if self._early_gate:
             main.wait_stream(self._gate_stream())
