@@ -350,13 +350,21 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
  * whose dispatch sections are filled from the counts — route_cum, recv_base and zero_rows
  * with one {row, count >= 0} entry per expert (pass n_zero = E to fssdp_dispatch) — equal to
  * what fssdp_build_rank_tables derives for a single device, so the dispatch can be
- * launched before the host plan. */
+ * launched before the host plan.  local_d_ff > 0 (with local_tables): the six GEMM tables
+ * too (fssdp_local_gemm_tables for d_model = d, local_d_ff, local_n_mats), so the forward
+ * GEMMs (total_tiles = -1) can be queued before the host plan.  counts_host (nullable):
+ * host boundary #1 in the same
+ * launch — after the count barrier the whole D x E table (counts_bytes, a multiple of 16)
+ * is copied to this mapped pinned buffer and *flag_host := flag_value (system-scope
+ * release), what fssdp_push_host would do as a separate kernel. */
 int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
                      int32_t E, int32_t k, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
                      int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
                      const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
                      int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
-                     int32_t* local_tables, void* stream);
+                     int32_t* local_tables, int32_t local_d_ff, int32_t local_n_mats,
+                     void* counts_host, int64_t counts_bytes, uint32_t* flag_host,
+                     uint32_t flag_value, void* stream);
 int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,

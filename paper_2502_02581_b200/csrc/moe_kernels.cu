@@ -320,6 +320,17 @@ struct GateLocalTables {
   int32_t* route_cum;
   int32_t* recv_base;
   int32_t* zero_rows;
+  // host boundary #1 folded into the tail (nullable): after the count barrier, the whole
+  // all-gathered counts table (n16 x 16 B) to mapped pinned host memory, then the flag
+  int4* host_counts;
+  int host_n16;
+  uint32_t* host_flag;
+  uint32_t host_flag_value;
+  // (nullable) the six grouped-GEMM tables of the same single-rank blob, also written from
+  // the totals, so the forward GEMMs need not wait for the host plan (fssdp_local_gemm_tables)
+  fssdp_gemm_group* gemm0;
+  int64_t gemm_stride;  // bytes between the six GEMM sections
+  int32_t d_model, d_ff, n_mats;
 };
 
 __device__ void write_local_tables(const int32_t* totals, int E, GateLocalTables local) {
@@ -344,57 +355,64 @@ __global__ void gate_local_tables_kernel(const uint64_t* peer_bases, int rank, i
 }
 
 // Single rank, N = 1: the six grouped-GEMM descriptor tables of fssdp_build_rank_tables
-// (planner.cpp), written on the device from the gate's expert totals — every expert is an
-// owned slot (ascending), segments padded to 256 rows, no replica, no SpRS push; the wgrads
-// list the slots longest-first (stable), as the host builder does.  The forward GEMMs can
-// then be queued before the host plan exists (fssdp_grouped_gemm total_tiles = -1).
-__global__ void local_gemm_tables_kernel(const uint64_t* __restrict__ peer_bases, int rank,
-                                         int64_t table_off, int E, int64_t d, int64_t f, int nm,
-                                         fssdp_gemm_group* __restrict__ gemm0, int64_t stride) {
-  __shared__ int32_t s_start[kGateMaxE], s_pad[kGateMaxE], s_rows[kGateMaxE], s_order[kGateMaxE];
-  if (threadIdx.x == 0) {
-    const int32_t* tot = reinterpret_cast<const int32_t*>(peer_bases[rank] + table_off) + rank * E;
-    int32_t row = 0;
-    for (int e = 0; e < E; ++e) {
-      const int32_t c = __ldcg(tot + e), pad = (c + 255) / 256 * 256;
-      s_start[e] = row;
-      s_rows[e] = c;
-      s_pad[e] = pad;
-      row += pad;
-      int j = e;  // stable insertion by padded rows, descending
-      while (j > 0 && s_pad[s_order[j - 1]] < pad) {
-        s_order[j] = s_order[j - 1];
-        --j;
-      }
-      s_order[j] = e;
-    }
-  }
-  __syncthreads();
-  const int gi = threadIdx.x;
-  if (gi >= 6) return;
+// (planner.cpp), written on the device from the expert totals — every expert is an owned
+// slot (ascending), segments padded to 256 rows, no replica, no SpRS push; the wgrads list
+// the slots longest-first (stable), as the host builder does.  The forward GEMMs can then be
+// queued before the host plan exists (fssdp_grouped_gemm total_tiles = -1).  Thread e < E
+// derives expert e's entries in O(E) (prefix of the padded rows, its rank in the wgrad
+// order), so one block writes every table in a few hundred cycles.
+__device__ void write_local_gemm_groups(const int32_t* __restrict__ tot, int E, int64_t d,
+                                        int64_t f, int nm, fssdp_gemm_group* gemm0,
+                                        int64_t stride) {
+  const int e = threadIdx.x;
+  if (e >= E) return;
   const int64_t n1 = (nm - 1) * f;
   const int64_t bnf = f % 256 == 0 ? 256 : 128, bn1 = nm == 3 ? 256 : bnf, nf = (f + 255) / 256;
   const int64_t n_tiles[6] = {n1 / bn1, d / 256, nf, d / 256, d / 256, nf};
-  fssdp_gemm_group* g = reinterpret_cast<fssdp_gemm_group*>(
-      reinterpret_cast<uint8_t*>(gemm0) + gi * stride);
-  int32_t tile = 0;
-  for (int i = 0; i < E; ++i) {
-    const int s = gi >= 4 ? s_order[i] : i;
-    const int32_t st = s_start[s], mt = s_pad[s] / 128, kt = (s_rows[s] + 63) / 64;
-    const int32_t w1r = static_cast<int32_t>(s * nm * f), w2r = static_cast<int32_t>(s * nm * d);
+  const int32_t c = tot[e], pad = (c + 255) / 256 * 256;
+  int32_t st = 0, before_tiles = 0, rank_w = 0, before_w = 0;
+  for (int q = 0; q < E; ++q) {
+    const int32_t pq = (tot[q] + 255) / 256 * 256;
+    if (q < e) {
+      st += pq;
+      before_tiles += pq / 128;
+    }
+    if (pq > pad || (pq == pad && q < e)) {  // stable, padded rows descending
+      ++rank_w;
+      before_w += pq / 128;
+    }
+  }
+  const int32_t mt = pad / 128, kt = (c + 63) / 64;
+  const int32_t w1r = static_cast<int32_t>(e * nm * f), w2r = static_cast<int32_t>(e * nm * d);
+  for (int gi = 0; gi < 6; ++gi) {
     fssdp_gemm_group x;
     switch (gi) {
       case 0: x = {mt, 0, st, 0, w1r, 0, static_cast<int32_t>(d / 64), 0, st * n1}; break;
       case 1: x = {mt, 0, st, 0, w2r, 0, static_cast<int32_t>(f / 64), 0, st * d}; break;
       case 2: x = {mt, 0, st, 0, 0, w2r, static_cast<int32_t>(d / 64), 0, st * n1}; break;
       case 3: x = {mt, 0, st, 0, 0, w1r, static_cast<int32_t>(n1 / 64), 0, st * d}; break;
-      case 4: x = {static_cast<int32_t>(n1 / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d}; break;
-      default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d + n1 * d}; break;
+      case 4: x = {static_cast<int32_t>(n1 / 128), 0, 0, st, 0, st, kt, 0, e * nm * f * d}; break;
+      default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, e * nm * f * d + n1 * d}; break;
     }
-    x.tile_start = tile;
-    tile += x.m_tiles * static_cast<int32_t>(n_tiles[gi]);
-    g[i] = x;
+    const bool wgrad = gi >= 4;
+    // m_tiles of a wgrad group = its output rows / 128 (the same for every expert)
+    x.tile_start = static_cast<int32_t>((wgrad ? static_cast<int64_t>(rank_w) * x.m_tiles
+                                               : before_tiles) * n_tiles[gi]);
+    fssdp_gemm_group* g = reinterpret_cast<fssdp_gemm_group*>(
+        reinterpret_cast<uint8_t*>(gemm0) + gi * stride);
+    g[wgrad ? rank_w : e] = x;
   }
+  (void)before_w;
+}
+
+__global__ void local_gemm_tables_kernel(const uint64_t* __restrict__ peer_bases, int rank,
+                                         int64_t table_off, int E, int64_t d, int64_t f, int nm,
+                                         fssdp_gemm_group* __restrict__ gemm0, int64_t stride) {
+  __shared__ int32_t s_tot[kGateMaxE];
+  const int32_t* tot = reinterpret_cast<const int32_t*>(peer_bases[rank] + table_off) + rank * E;
+  if (threadIdx.x < E) s_tot[threadIdx.x] = __ldcg(tot + threadIdx.x);
+  __syncthreads();
+  write_local_gemm_groups(s_tot, E, d, f, nm, gemm0, stride);
 }
 
 __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ tile_counts,
@@ -433,6 +451,9 @@ __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ 
   }
   __syncthreads();
   if (local.route_cum != nullptr && threadIdx.x == 0) write_local_tables(s_tot, E, local);
+  if (local.gemm0 != nullptr)
+    write_local_gemm_groups(s_tot, E, local.d_model, local.d_ff, local.n_mats, local.gemm0,
+                            local.gemm_stride);
   if (active) {
     int32_t run = csum[threadIdx.x];
     for (int t = t0; t < t1; ++t) {
@@ -446,6 +467,17 @@ __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ 
     if (threadIdx.x == 0) __threadfence_system();
     __syncwarp();
     world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
+  }
+  if (local.host_counts != nullptr) {  // every rank's row is in (barrier): push the table
+    __syncthreads();
+    const int4* src = reinterpret_cast<const int4*>(peer_bases[rank] + table_off);
+    for (int i = threadIdx.x; i < local.host_n16; i += blockDim.x)
+      local.host_counts[i] = __ldcv(src + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(local.host_flag, local.host_flag_value);
+    }
   }
 }
 
@@ -1428,6 +1460,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// the two-kernel gate path's counts push (the fused gate does it in its tail)
+__global__ void __launch_bounds__(256)
+    push_counts_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t table_off,
+                       GateLocalTables local) {
+  const int4* src = reinterpret_cast<const int4*>(peer_bases[rank] + table_off);
+  for (int i = threadIdx.x; i < local.host_n16; i += blockDim.x) local.host_counts[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(local.host_flag, local.host_flag_value);
+  }
+}
+
 __global__ void __launch_bounds__(256)
     pull_host_kernel(const int4* src_host, int4* __restrict__ dst, int n16) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
@@ -1609,11 +1654,15 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
                      int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
                      const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
                      int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
-                     int32_t* local_tables, void* stream) {
+                     int32_t* local_tables, int32_t local_d_ff, int32_t local_n_mats,
+                     void* counts_host, int64_t counts_bytes, uint32_t* flag_host,
+                     uint32_t flag_value, void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
       k > E || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world ||
-      (local_tables != nullptr && world != 1)) {
-    set_error("gate_route: unsupported shape (local tables need world == 1)");
+      (local_tables != nullptr && world != 1) ||
+      (counts_host != nullptr && (counts_bytes % 16 != 0 || flag_host == nullptr))) {
+    set_error("gate_route: unsupported shape (local tables need world == 1; counts push "
+              "needs 16-byte multiples and a flag)");
     return kErrDimension;
   }
   const int tiles = static_cast<int>((T + kGateTile - 1) / kGateTile);
@@ -1624,7 +1673,26 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
     auto sec = [&](int i) {
       return reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(local_tables) + off[i]);
     };
-    local = {sec(FSSDP_TAB_ROUTE_CUM), sec(FSSDP_TAB_RECV_BASE), sec(FSSDP_TAB_ZERO_ROWS)};
+    local.route_cum = sec(FSSDP_TAB_ROUTE_CUM);
+    local.recv_base = sec(FSSDP_TAB_RECV_BASE);
+    local.zero_rows = sec(FSSDP_TAB_ZERO_ROWS);
+    if (local_d_ff > 0) {  // + the six GEMM tables (fssdp_local_gemm_tables' work)
+      if (d % 256 != 0 || local_d_ff % 128 != 0 || local_n_mats < 2 || local_n_mats > 3) {
+        set_error("gate_route: local GEMM tables need d % 256, d_ff % 128, n_mats 2 or 3");
+        return kErrDimension;
+      }
+      local.gemm0 = reinterpret_cast<fssdp_gemm_group*>(sec(FSSDP_TAB_GEMM0));
+      local.gemm_stride = off[FSSDP_TAB_GEMM0 + 1] - off[FSSDP_TAB_GEMM0];
+      local.d_model = d;
+      local.d_ff = local_d_ff;
+      local.n_mats = local_n_mats;
+    }
+  }
+  if (counts_host != nullptr) {
+    local.host_counts = static_cast<int4*>(counts_host);
+    local.host_n16 = static_cast<int>(counts_bytes / 16);
+    local.host_flag = flag_host;
+    local.host_flag_value = flag_value;
   }
   if (!gate_mma_ok(d, E) || tiles == 0) {  // the two-kernel path (+ the local tables)
     int rc = fssdp_gate_topk(x, wg, bias, T, d, E, k, nullptr, topk_idx, topk_w, slot_rank,
@@ -1632,9 +1700,22 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
     if (rc != kOk) return rc;
     rc = fssdp_route_scan_allgather(tile_counts, tiles, E, tile_prefix, peer_bases, table_off,
                                     flags_off, rank, world, bar_slot, epoch, stream);
-    if (rc != kOk || local_tables == nullptr) return rc;
-    gate_local_tables_kernel<<<1, 32, 0, as_stream(stream)>>>(peer_bases, rank, table_off, E,
-                                                             local);
+    if (rc != kOk) return rc;
+    if (local_tables != nullptr) {
+      gate_local_tables_kernel<<<1, 32, 0, as_stream(stream)>>>(peer_bases, rank, table_off, E,
+                                                               local);
+      rc = launch_status();
+      if (rc != kOk) return rc;
+      if (local.gemm0 != nullptr) {
+        local_gemm_tables_kernel<<<1, kGateMaxE, 0, as_stream(stream)>>>(
+            peer_bases, rank, table_off, E, local.d_model, local.d_ff, local.n_mats, local.gemm0,
+            local.gemm_stride);
+        rc = launch_status();
+        if (rc != kOk) return rc;
+      }
+    }
+    if (counts_host == nullptr) return kOk;
+    push_counts_kernel<<<1, 256, 0, as_stream(stream)>>>(peer_bases, rank, table_off, local);
     return launch_status();
   }
   const int rc = gate_mma_launch(static_cast<const __nv_bfloat16*>(x), wg, bias, T, d, E, k,
@@ -1732,7 +1813,7 @@ int fssdp_local_gemm_tables(const uint64_t* peer_bases, int32_t rank, int64_t ta
   int64_t off[FSSDP_TAB_NSECTIONS], total = 0;
   fssdp_tables_layout(E, 1, off, &total);
   uint8_t* blob = static_cast<uint8_t*>(local_tables);
-  local_gemm_tables_kernel<<<1, 32, 0, as_stream(stream)>>>(
+  local_gemm_tables_kernel<<<1, kGateMaxE, 0, as_stream(stream)>>>(
       peer_bases, rank, table_off, E, d_model, d_ff, n_mats,
       reinterpret_cast<fssdp_gemm_group*>(blob + off[FSSDP_TAB_GEMM0]),
       off[FSSDP_TAB_GEMM0 + 1] - off[FSSDP_TAB_GEMM0]);

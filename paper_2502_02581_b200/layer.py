@@ -654,18 +654,33 @@ class FssdpMoE:
         # K1 + K2 fused: the gate's last CTA scans the tile counts, all-gathers this rank's
         # totals and joins the count barrier
         slot, epoch = self._bar(BAR_COUNTS)
+        # host boundary #1 inside the same launch (after the count barrier the table is
+        # complete) — not under lockstep emulation, whose ranks' gates run one after another
+        fused = self.FUSED_PUSH and (self.group.mode == "dist" or self.world == 1)
+        self._pushed_with_gate = fused
+        if fused:
+            self._counts_epoch = (self._counts_epoch + 1) & 0xFFFFFFFF
         self._call("fssdp_gate_route", ops._ptr(self.x), ops._ptr(self.wg),
                    ops._ptr(self.gate_bias), T, self.g.d_model, E, k, ops._ptr(self.topk_idx),
                    ops._ptr(self.topk_w), ops._ptr(self.slot_rank), ops._ptr(self.tile_counts),
                    ops._ptr(self.tile_prefix), ops._ptr(self.gate_ws), self._pb(),
                    self.off["counts"], self.flags_off, self.rank, self.world, slot, epoch,
                    C.c_void_p(self.blob_dev_ptr) if self.LOCAL_DISPATCH and self.world == 1
-                   else None, self._stream())
+                   else None,
+                   self.g.d_ff if self._local_gemm else 0, self.g.n_mats,
+                   C.c_void_p(self.counts_host_ptr if fused else 0), self.counts_nbytes,
+                   C.c_void_p(self.counts_flag_ptr if fused else 0),
+                   C.c_uint32(self._counts_epoch), self._stream())
 
     def phase_counts(self) -> None:
         """The counts are all-gathered by the gate launch; the early SpAG may start now."""
         if self.PREFETCH_AT == "counts":
             self._launch_prefetch()
+
+    # the gate launch also pushes the counts to the host (FSSDP_FUSED_PUSH=0: a separate
+    # push_host kernel after it)
+    FUSED_PUSH = os.environ.get("FSSDP_FUSED_PUSH", "1") != "0"
+    _pushed_with_gate = False
 
     # where the early SpAG starts: with the gate ("gate"), after the count all-gather
     # ("counts"), or once the counts readback has left ("push")
@@ -675,10 +690,11 @@ class FssdpMoE:
         """Host boundary #1: the all-gathered counts to mapped pinned memory + a flag, by the
         SMs (a copy-engine transfer would queue behind the caller's bulk copies)."""
         self._mark("readback")
-        self._counts_epoch = (self._counts_epoch + 1) & 0xFFFFFFFF
-        self._timed("push_host", lambda: N.check(N.LIB_RAW.fssdp_push_host(
-            self.counts_dev_ptr, self.counts_host_ptr, self.counts_nbytes, self.counts_flag_ptr,
-            self._counts_epoch, self._stream()), "counts readback"))
+        if not self._pushed_with_gate:
+            self._counts_epoch = (self._counts_epoch + 1) & 0xFFFFFFFF
+            self._timed("push_host", lambda: N.check(N.LIB_RAW.fssdp_push_host(
+                self.counts_dev_ptr, self.counts_host_ptr, self.counts_nbytes,
+                self.counts_flag_ptr, self._counts_epoch, self._stream()), "counts readback"))
         if self.PREFETCH_AT == "push":
             self._launch_prefetch()
 
@@ -1060,11 +1076,16 @@ class FssdpMoE:
     # single rank: the gate writes the dispatch tables itself (the placement cannot change),
     # so the dispatch runs while the host plans (FSSDP_LOCAL_DISPATCH=0 disables)
     LOCAL_DISPATCH = os.environ.get("FSSDP_LOCAL_DISPATCH", "1") != "0"
-    # experiment (off): the gate's totals also give the forward GEMM tables on the device
-    # (fssdp_local_gemm_tables), so fwd1/fwd2 are queued before the host plan.  Device time
-    # is unchanged (1.5094 vs 1.5072 ms, interleaved A/B) — the host plan already finishes
-    # while the dispatch runs — and e2e loses 3 % (its copies are issued after the plan)
-    LOCAL_GEMM_TABLES = os.environ.get("FSSDP_LOCAL_GEMM", "0") == "1"
+    # single rank: the gate's last CTA also writes the six GEMM tables from its totals
+    # (byte-equal to the host builder's), so fwd1/fwd2 are queued before the host plan
+    # instead of waiting for it (device timeline: fwd1 started 34 us after the dispatch,
+    # waiting for the plan's table upload; as a separate single-thread kernel the tables
+    # themselves took 17 us).  FSSDP_LOCAL_GEMM=0: the GEMMs wait for the host tables
+    LOCAL_GEMM_TABLES = os.environ.get("FSSDP_LOCAL_GEMM", "1") != "0"
+
+    @property
+    def _local_gemm(self) -> bool:
+        return self.LOCAL_GEMM_TABLES and self.LOCAL_DISPATCH and self.world == 1
 
     def _forward(self, x: torch.Tensor) -> torch.Tensor:
         self.phase_publish()
@@ -1079,12 +1100,9 @@ class FssdpMoE:
         if self.LOCAL_DISPATCH and self.world == 1:
             self._push_counts()
             self.phase_dispatch(n_zero=self.g.num_experts)  # one {row, count} per expert
-            if self.LOCAL_GEMM_TABLES:
-                # the GEMM tables too come from the device: the forward GEMMs are queued
-                # before the host plan (which then overlaps them instead of preceding them)
-                self._call("fssdp_local_gemm_tables", self._pb(), self.rank, self.off["counts"],
-                           self.g.num_experts, self.g.d_model, self.g.d_ff, self.g.n_mats,
-                           C.c_void_p(self.blob_dev_ptr), self._stream())
+            if self._local_gemm:
+                # the GEMM tables too came from the device (the gate wrote them): the forward
+                # GEMMs are queued before the host plan (which then overlaps them)
                 E = self.g.num_experts
                 self.gemm = dict(getattr(self, "gemm", None) or {})
                 self.gemm["fwd1"] = (E, self.g.n1 // self._bn["fwd1"], -1)

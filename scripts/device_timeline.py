@@ -1,0 +1,84 @@
+"""Device-side kernel timeline of the bench workload (torch.profiler / CUPTI activity
+records: GPU timestamps of every kernel, no CUDA events in the stream).
+
+    python scripts/device_timeline.py [--config cfg2] [--steps 3] [--out gpurun_out/tl.json]
+
+Prints, for the last profiled step, every kernel (start/end relative to the step's first
+kernel, µs) and the GPU idle gaps on the critical stream, plus totals."""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    bench.select_config(args.config)
+    import paper_2502_02581_b200 as F
+    from paper_2502_02581_b200.layer import create_layer
+
+    C = bench.CFG2
+    T = C["tokens_per_gpu"]
+    dev = torch.device("cuda", 0)
+    layer = create_layer(C["d_model"], C["d_ff"], C["num_experts"], C["top_k"], T,
+                         F.Policy(F.PolicyKind.FSSDP, **bench.POLICY), device=dev, seed=1234,
+                         activation=C["activation"])
+    E = C["num_experts"]
+    p = 1.0 / np.arange(1, E + 1) ** bench.ZIPF_S
+    p = p[np.random.default_rng(42).permutation(E)]
+    layer.gate_bias.copy_(torch.tensor(np.log(p / p.sum()), dtype=torch.float32))
+    g = torch.Generator(device=dev).manual_seed(1000)
+    xs = [torch.randn(T, C["d_model"], device=dev, generator=g).bfloat16() for _ in range(4)]
+    dys = [(torch.randn(T, C["d_model"], device=dev, generator=g) * 0.05).bfloat16()
+           for _ in range(4)]
+
+    def step(i):
+        layer.forward(xs[i % 4])
+        layer.backward(dys[i % 4])
+        layer.planner.finish()
+
+    for i in range(5):
+        step(i)
+    torch.cuda.synchronize()
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(args.steps):
+            step(i)
+        torch.cuda.synchronize()
+    evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    ks = sorted(((e.time_range.start, e.time_range.end, e.name) for e in evs), key=lambda t: t[0])
+    # split into steps at each gate launch
+    starts = [i for i, k in enumerate(ks) if "gate_topk" in k[2]]
+    last = ks[starts[-1]:] if starts else ks
+    t0 = last[0][0]
+    rows = [(round(a - t0, 2), round(b - t0, 2), n[:70]) for a, b, n in last]
+    busy_end, gaps = rows[0][0], 0.0
+    for a, b, n in rows:
+        if a > busy_end:
+            gaps += a - busy_end
+        busy_end = max(busy_end, b)
+    step_us = (ks[starts[-1]][0] - ks[starts[-2]][0]) if len(starts) > 1 else None
+    for a, b, n in rows:
+        print(f"{a:9.2f} {b:9.2f} {b - a:8.2f}  {n}")
+    print(json.dumps({"step_us": step_us, "idle_gaps_us": round(gaps, 2),
+                      "kernels": len(rows)}))
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump({"rows": rows, "step_us": step_us, "idle_gaps_us": gaps}, fh)
+
+
+if __name__ == "__main__":
+    main()

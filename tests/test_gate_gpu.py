@@ -86,13 +86,20 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
     for local in (False, True):
         out = [torch.empty_like(t) for t in (idx, w, rank, tc, prefix)]
         table.zero_()
+        host = torch.zeros(((E * 4 + 15) // 16 * 16) // 4 + 4, dtype=torch.int32,
+                           pin_memory=True)
+        flag_ptr = host.data_ptr() + (E * 4 + 15) // 16 * 16
         N.call("fssdp_gate_route", ops._ptr(x), ops._ptr(wg), ops._ptr(bias), T, d, E, k,
                *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0,
-               ops._ptr(blob) if local else None, s)
+               ops._ptr(blob) if local else None, 512 if local and d % 256 == 0 else 0, 2,
+               C.c_void_p(host.data_ptr() if local else 0), (E * 4 + 15) // 16 * 16,
+               C.c_void_p(flag_ptr if local else 0), C.c_uint32(7), s)
         torch.cuda.synchronize()
         for a, b in zip(want, [t.cpu() for t in out] + [table.cpu()]):
             assert torch.equal(a, b)
         assert not ws.any()
+        if local:  # the counts row pushed to the mapped host buffer, then the flag
+            assert torch.equal(host[:E], want[5].reshape(-1)[:E]) and int(host[-4]) == 7
     assert int(want[5].sum()) == T * k
     # the single-rank dispatch tables the gate wrote == the host builder's for one device
     counts = want[5].numpy().astype(np.int64)
@@ -107,6 +114,12 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
     assert np.array_equal(sec("recv_base", E).reshape(E, 1), host.recv_base)
     zr = sec("zero_rows", 2 * E).reshape(E, 2)
     assert np.array_equal(zr[zr[:, 1] > 0], host.zero_rows)
+    if d % 256 == 0:  # the gate's tail wrote the GEMM tables too (local_d_ff = 512)
+        ht = NativeTables(0, np.zeros(E, np.int32), np.ones((E, 1), np.uint8),
+                          counts[None, :, None], d, 512)
+        for name in ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2"):
+            want_g = ht.groups(name).tobytes()
+            assert dev[offs[name]:offs[name] + len(want_g)].tobytes() == want_g, name
     # ... and the six grouped-GEMM tables fssdp_local_gemm_tables writes from those totals
     # == the host builder's, byte for byte (the forward GEMMs run on them before the plan)
     for dm, dff, nm in ((1024, 4096, 2), (2048, 1408, 3), (256, 1024, 2)):
