@@ -351,7 +351,8 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
  * with one {row, count >= 0} entry per expert (pass n_zero = E to fssdp_dispatch) — equal to
  * what fssdp_build_rank_tables derives for a single device, so the dispatch can be
  * launched before the host plan.  local_d_ff > 0 (with local_tables): the six GEMM tables
- * too (fssdp_local_gemm_tables for d_model = d, local_d_ff, local_n_mats), so the forward
+ * too (fssdp_local_gemm_tables for d_model = d, local_d_ff, local_n_mats,
+ * local_param_base), so the forward
  * GEMMs (total_tiles = -1) can be queued before the host plan.  counts_host (nullable):
  * host boundary #1 in the same
  * launch — after the count barrier the whole D x E table (counts_bytes, a multiple of 16)
@@ -363,8 +364,8 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
                      const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
                      int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
                      int32_t* local_tables, int32_t local_d_ff, int32_t local_n_mats,
-                     void* counts_host, int64_t counts_bytes, uint32_t* flag_host,
-                     uint32_t flag_value, void* stream);
+                     int32_t local_param_base, void* counts_host, int64_t counts_bytes,
+                     uint32_t* flag_host, uint32_t flag_value, void* stream);
 int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
@@ -404,11 +405,12 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
 /* Single rank (N = 1): the six grouped-GEMM tables of the fssdp_tables_layout(E, 1) blob at
  * local_tables, written on the device from this rank's expert totals (the counts row at
  * heap offset table_off, as fssdp_gate_route wrote it) — identical to what
- * fssdp_build_rank_tables writes for one rank, so the forward GEMMs (launched with
- * total_tiles = -1) need not wait for the host plan. */
+ * fssdp_build_rank_tables writes for one rank (param_base: the parameter slot of expert 0,
+ * the slot_layout owned_base; 0 for a per-layer region), so the forward GEMMs (launched
+ * with total_tiles = -1) need not wait for the host plan. */
 int fssdp_local_gemm_tables(const uint64_t* peer_bases, int32_t rank, int64_t table_off,
                             int32_t E, int32_t d_model, int32_t d_ff, int32_t n_mats,
-                            void* local_tables, void* stream);
+                            int32_t param_base, void* local_tables, void* stream);
 
 /* K6: combine.  y[t] = sum_j w[t, j] * Y_{dest}[pos]  (fp32, j ascending) -> bf16.
  * Y rows are pulled from peer heaps (offset y_off).  y_slots (nullable, bf16 [T*k, d_model]):

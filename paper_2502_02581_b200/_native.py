@@ -121,15 +121,15 @@ _SIGS = {
     "fssdp_gate_topk": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "fssdp_gate_route": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i64,
-                         i32, i32, i32, C.c_uint32, vp, i32, i32, vp, i64, vp, C.c_uint32,
-                         vp],
+                         i32, i32, i32, C.c_uint32, vp, i32, i32, i32, vp, i64, vp,
+                         C.c_uint32, vp],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier_selftest": [vp, i64, i64, i32, i32, i32, u32, i32, vp, vp],
     "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
                        i64, i32, i32, u32, vp, vp],
     "fssdp_combine": [vp, vp, vp, i64, i32, i32, vp, i64, vp, vp, vp],
-    "fssdp_local_gemm_tables": [vp, i32, i64, i32, i32, i32, i32, vp, vp],
+    "fssdp_local_gemm_tables": [vp, i32, i64, i32, i32, i32, i32, i32, vp, vp],
     "fssdp_dispatch_grad": [vp, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp, vp, vp, i32,
                             i64, i32, i32, i32, u32, vp, vp],
     "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],

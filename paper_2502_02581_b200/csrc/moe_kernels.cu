@@ -67,6 +67,36 @@ __device__ __forceinline__ void world_barrier_warp(const uint64_t* __restrict__ 
   __syncwarp();
 }
 
+// The two halves of world_barrier_warp, for a caller with work to overlap in between:
+// every lane < world publishes this rank's arrival on that peer; later, the same lanes
+// wait for every peer's arrival here (30 s bound, as above).
+__device__ __forceinline__ void world_barrier_arrive(const uint64_t* __restrict__ peer_bases,
+                                                     int64_t flags_off, int rank, int world,
+                                                     int slot, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  if (slot < 0 || lane >= world) return;
+  uint32_t* remote = reinterpret_cast<uint32_t*>(peer_bases[lane] + flags_off) +
+                     slot * kMaxWorld + rank;
+  st_release_sys(remote, epoch);
+}
+__device__ __forceinline__ void world_barrier_wait(const uint64_t* __restrict__ peer_bases,
+                                                   int64_t flags_off, int rank, int world,
+                                                   int slot, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  if (slot >= 0 && lane < world) {
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(peer_bases[rank] + flags_off) +
+                           slot * kMaxWorld + lane;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 30ull * 1000000000ull) __trap();
+    }
+  }
+  __syncwarp();
+}
+
 // Grid-wide "all CTAs done" followed by the world barrier, run by the last CTA.
 __device__ __forceinline__ void grid_done_then_barrier(uint32_t* grid_counter,
                                                        const uint64_t* __restrict__ peer_bases,
@@ -331,6 +361,7 @@ struct GateLocalTables {
   fssdp_gemm_group* gemm0;
   int64_t gemm_stride;  // bytes between the six GEMM sections
   int32_t d_model, d_ff, n_mats;
+  int32_t param_base;   // parameter slot of expert 0 (a model-level parameter region)
 };
 
 __device__ void write_local_tables(const int32_t* totals, int E, GateLocalTables local) {
@@ -363,7 +394,7 @@ __global__ void gate_local_tables_kernel(const uint64_t* peer_bases, int rank, i
 // order), so one block writes every table in a few hundred cycles.
 __device__ void write_local_gemm_groups(const int32_t* __restrict__ tot, int E, int64_t d,
                                         int64_t f, int nm, fssdp_gemm_group* gemm0,
-                                        int64_t stride) {
+                                        int64_t stride, int param_base) {
   const int e = threadIdx.x;
   if (e >= E) return;
   const int64_t n1 = (nm - 1) * f;
@@ -383,7 +414,8 @@ __device__ void write_local_gemm_groups(const int32_t* __restrict__ tot, int E, 
     }
   }
   const int32_t mt = pad / 128, kt = (c + 63) / 64;
-  const int32_t w1r = static_cast<int32_t>(e * nm * f), w2r = static_cast<int32_t>(e * nm * d);
+  const int64_t ps = param_base + e;  // expert e's parameter slot (gradients: slot e)
+  const int32_t w1r = static_cast<int32_t>(ps * nm * f), w2r = static_cast<int32_t>(ps * nm * d);
   for (int gi = 0; gi < 6; ++gi) {
     fssdp_gemm_group x;
     switch (gi) {
@@ -407,21 +439,54 @@ __device__ void write_local_gemm_groups(const int32_t* __restrict__ tot, int E, 
 
 __global__ void local_gemm_tables_kernel(const uint64_t* __restrict__ peer_bases, int rank,
                                          int64_t table_off, int E, int64_t d, int64_t f, int nm,
-                                         fssdp_gemm_group* __restrict__ gemm0, int64_t stride) {
+                                         fssdp_gemm_group* __restrict__ gemm0, int64_t stride,
+                                         int param_base) {
   __shared__ int32_t s_tot[kGateMaxE];
   const int32_t* tot = reinterpret_cast<const int32_t*>(peer_bases[rank] + table_off) + rank * E;
   if (threadIdx.x < E) s_tot[threadIdx.x] = __ldcg(tot + threadIdx.x);
   __syncthreads();
-  write_local_gemm_groups(s_tot, E, d, f, nm, gemm0, stride);
+  write_local_gemm_groups(s_tot, E, d, f, nm, gemm0, stride, param_base);
 }
 
 __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ tile_counts,
                                 int32_t* __restrict__ tile_prefix, int32_t* __restrict__ ws,
                                 const uint64_t* __restrict__ peer_bases, int64_t table_off,
                                 int64_t flags_off, int rank, int world, int slot, uint32_t epoch,
-                                GateLocalTables local) {
+                                GateLocalTables local, int32_t* s_stage, int stage_ints) {
   __shared__ int32_t csum[512];
   __shared__ int32_t s_tot[kGateMaxE];
+  // 1. this rank's totals (accumulated by every CTA's atomics) into every rank's count
+  //    table, then the barrier ARRIVAL: peers can proceed while the scan below runs
+  if (threadIdx.x < E) {
+    const int32_t total = __ldcg(ws + 1 + threadIdx.x);
+    for (int p = 0; p < world; ++p)
+      reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + threadIdx.x] = total;
+    ws[1 + threadIdx.x] = 0;  // ready for the next call (stream order)
+    s_tot[threadIdx.x] = total;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncwarp();
+    world_barrier_arrive(peer_bases, flags_off, rank, world, slot, epoch);
+  }
+  if (local.route_cum != nullptr && threadIdx.x == 0) write_local_tables(s_tot, E, local);
+  if (local.gemm0 != nullptr)
+    write_local_gemm_groups(s_tot, E, local.d_model, local.d_ff, local.n_mats, local.gemm0,
+                            local.gemm_stride, local.param_base);
+  // 2. the tile counts into shared memory in one coalesced pass (the gate's staged weights
+  //    are dead by now), then the exclusive scan over tiles from there
+  const int n = n_tiles * E;
+  const bool staged = s_stage != nullptr && n <= stage_ints && (n % 4) == 0;
+  if (staged) {
+    const int4* src = reinterpret_cast<const int4*>(tile_counts);
+    for (int i = threadIdx.x; i < n / 4; i += blockDim.x)
+      reinterpret_cast<int4*>(s_stage)[i] = __ldcg(src + i);
+    __syncthreads();
+  }
+  auto cnt = [&](int t, int e) {
+    return staged ? s_stage[t * E + e] : __ldcg(tile_counts + static_cast<int64_t>(t) * E + e);
+  };
   const int nthr = blockDim.x;
   const int chunks = (nthr < 512 ? nthr : 512) / E;
   const int per = (n_tiles + chunks - 1) / chunks;
@@ -429,10 +494,10 @@ __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ 
   const int c = threadIdx.x / E;
   const bool active = c < chunks;
   const int t0 = c * per, t1 = min(n_tiles, t0 + per);
-  int32_t sum = 0;
   if (active) {
+    int32_t sum = 0;
 #pragma unroll 8
-    for (int t = t0; t < t1; ++t) sum += __ldcg(tile_counts + static_cast<int64_t>(t) * E + e);
+    for (int t = t0; t < t1; ++t) sum += cnt(t, e);
     csum[threadIdx.x] = sum;
   }
   __syncthreads();
@@ -443,31 +508,18 @@ __device__ void gate_route_tail(int n_tiles, int E, const int32_t* __restrict__ 
       csum[q * E + threadIdx.x] = run;
       run += v;
     }
-    const int32_t total = __ldcg(ws + 1 + threadIdx.x);
-    for (int p = 0; p < world; ++p)
-      reinterpret_cast<int32_t*>(peer_bases[p] + table_off)[rank * E + threadIdx.x] = total;
-    ws[1 + threadIdx.x] = 0;  // ready for the next call (stream order)
-    s_tot[threadIdx.x] = total;
   }
   __syncthreads();
-  if (local.route_cum != nullptr && threadIdx.x == 0) write_local_tables(s_tot, E, local);
-  if (local.gemm0 != nullptr)
-    write_local_gemm_groups(s_tot, E, local.d_model, local.d_ff, local.n_mats, local.gemm0,
-                            local.gemm_stride);
   if (active) {
     int32_t run = csum[threadIdx.x];
     for (int t = t0; t < t1; ++t) {
       tile_prefix[static_cast<int64_t>(t) * E + e] = run;
-      run += __ldcg(tile_counts + static_cast<int64_t>(t) * E + e);
+      run += cnt(t, e);
     }
   }
   if (threadIdx.x == 0) ws[0] = 0;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) __threadfence_system();
-    __syncwarp();
-    world_barrier_warp(peer_bases, flags_off, rank, world, slot, epoch);
-  }
+  // 3. every peer's arrival (their rows of the count table are in)
+  if (threadIdx.x < 32) world_barrier_wait(peer_bases, flags_off, rank, world, slot, epoch);
   if (local.host_counts != nullptr) {  // every rank's row is in (barrier): push the table
     __syncthreads();
     const int4* src = reinterpret_cast<const int4*>(peer_bases[rank] + table_off);
@@ -650,7 +702,8 @@ __global__ void __launch_bounds__(128 * KS)
   __syncthreads();
   if (!is_last) return;
   gate_route_tail(gridDim.x, E, tile_counts, tile_prefix, ws, peer_bases, table_off, flags_off,
-                  rank, world, slot, epoch, local);
+                  rank, world, slot, epoch, local,
+                  SW ? reinterpret_cast<int32_t*>(gate_wsm) : nullptr, SW ? E * wrow / 4 : 0);
 }
 
 __global__ void __launch_bounds__(kGateThreads)
@@ -1655,8 +1708,8 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
                      const uint64_t* peer_bases, int64_t table_off, int64_t flags_off,
                      int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
                      int32_t* local_tables, int32_t local_d_ff, int32_t local_n_mats,
-                     void* counts_host, int64_t counts_bytes, uint32_t* flag_host,
-                     uint32_t flag_value, void* stream) {
+                     int32_t local_param_base, void* counts_host, int64_t counts_bytes,
+                     uint32_t* flag_host, uint32_t flag_value, void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
       k > E || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world ||
       (local_tables != nullptr && world != 1) ||
@@ -1686,6 +1739,7 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
       local.d_model = d;
       local.d_ff = local_d_ff;
       local.n_mats = local_n_mats;
+      local.param_base = local_param_base;
     }
   }
   if (counts_host != nullptr) {
@@ -1709,7 +1763,7 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
       if (local.gemm0 != nullptr) {
         local_gemm_tables_kernel<<<1, kGateMaxE, 0, as_stream(stream)>>>(
             peer_bases, rank, table_off, E, local.d_model, local.d_ff, local.n_mats, local.gemm0,
-            local.gemm_stride);
+            local.gemm_stride, local.param_base);
         rc = launch_status();
         if (rc != kOk) return rc;
       }
@@ -1804,7 +1858,7 @@ int fssdp_dispatch(const void* x, const int32_t* topk_idx, const int32_t* slot_r
 
 int fssdp_local_gemm_tables(const uint64_t* peer_bases, int32_t rank, int64_t table_off,
                             int32_t E, int32_t d_model, int32_t d_ff, int32_t n_mats,
-                            void* local_tables, void* stream) {
+                            int32_t param_base, void* local_tables, void* stream) {
   if (E <= 0 || E > kGateMaxE || d_model % 256 != 0 || d_ff % 128 != 0 || n_mats < 2 ||
       n_mats > 3 || local_tables == nullptr) {
     set_error("local_gemm_tables: unsupported shape");
@@ -1816,7 +1870,7 @@ int fssdp_local_gemm_tables(const uint64_t* peer_bases, int32_t rank, int64_t ta
   local_gemm_tables_kernel<<<1, kGateMaxE, 0, as_stream(stream)>>>(
       peer_bases, rank, table_off, E, d_model, d_ff, n_mats,
       reinterpret_cast<fssdp_gemm_group*>(blob + off[FSSDP_TAB_GEMM0]),
-      off[FSSDP_TAB_GEMM0 + 1] - off[FSSDP_TAB_GEMM0]);
+      off[FSSDP_TAB_GEMM0 + 1] - off[FSSDP_TAB_GEMM0], param_base);
   return launch_status();
 }
 

@@ -668,6 +668,7 @@ class FssdpMoE:
                    C.c_void_p(self.blob_dev_ptr) if self.LOCAL_DISPATCH and self.world == 1
                    else None,
                    self.g.d_ff if self._local_gemm else 0, self.g.n_mats,
+                   max(0, self.g.owned_base),
                    C.c_void_p(self.counts_host_ptr if fused else 0), self.counts_nbytes,
                    C.c_void_p(self.counts_flag_ptr if fused else 0),
                    C.c_uint32(self._counts_epoch), self._stream())
@@ -757,10 +758,13 @@ class FssdpMoE:
         # call; the Python-side decision object is built after the dispatch is launched
         E, D = self.g.num_experts, self.world
         # (timed as "pull_host": the native window covers only the table upload kernel)
+        # single rank with device-written tables (the gate's tail): the device blob already
+        # holds every section the kernels read, byte-equal — no upload
+        dev_blob = None if self._local_gemm else self.blob_dev_ptr
         self._timed("pull_host", lambda: self.planner.plan_with_tables(
             self.layer, counts, self.counts_host_ptr, self.rank, self.pre_mask_ptr,
             self.g.d_model, self.g.d_ff, self.blob_host_np, self.blob_host_ptr,
-            NativeTables._hdr_ptr, self.blob_dev_ptr, self._stream(), self._limits_ptr,
+            NativeTables._hdr_ptr, dev_blob, self._stream(), self._limits_ptr,
             decide=False, n_mats=self.g.n_mats))
         self._mark("planned")
         if self.gap_events is not None:
@@ -1004,7 +1008,7 @@ class FssdpMoE:
                self.g.top_k, self._pb(), self.off["y"], ops._ptr(self.y_slots),
                self.off["dyrecv"],
                ops._ptr(self.slot_grad), ops._ptr(self.dlogit if self._early_gate else None),
-               self._tab("zero_rows"), t.n_zero,
+               self._tab("zero_rows"), self.g.num_experts if self._local_gemm else t.n_zero,
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
 

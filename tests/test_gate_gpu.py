@@ -91,7 +91,7 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
         flag_ptr = host.data_ptr() + (E * 4 + 15) // 16 * 16
         N.call("fssdp_gate_route", ops._ptr(x), ops._ptr(wg), ops._ptr(bias), T, d, E, k,
                *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0,
-               ops._ptr(blob) if local else None, 512 if local and d % 256 == 0 else 0, 2,
+               ops._ptr(blob) if local else None, 512 if local and d % 256 == 0 else 0, 2, 0,
                C.c_void_p(host.data_ptr() if local else 0), (E * 4 + 15) // 16 * 16,
                C.c_void_p(flag_ptr if local else 0), C.c_uint32(7), s)
         torch.cuda.synchronize()
@@ -122,13 +122,16 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
             assert dev[offs[name]:offs[name] + len(want_g)].tobytes() == want_g, name
     # ... and the six grouped-GEMM tables fssdp_local_gemm_tables writes from those totals
     # == the host builder's, byte for byte (the forward GEMMs run on them before the plan)
-    for dm, dff, nm in ((1024, 4096, 2), (2048, 1408, 3), (256, 1024, 2)):
+    # (base > 0: the layer's owned slots start at that slot of a model-level region)
+    for dm, dff, nm, base in ((1024, 4096, 2, 0), (2048, 1408, 3, 0), (256, 1024, 2, 0),
+                              (1024, 4096, 2, 2 * E)):
         blob.zero_()
-        N.call("fssdp_local_gemm_tables", pb, 0, off, E, dm, dff, nm, ops._ptr(blob), s)
+        N.call("fssdp_local_gemm_tables", pb, 0, off, E, dm, dff, nm, base, ops._ptr(blob), s)
         torch.cuda.synchronize()
         dev = blob.cpu().numpy()
         host = NativeTables(0, np.zeros(E, np.int32), np.ones((E, 1), np.uint8),
-                            counts[None, :, None], dm, dff, n_mats=nm)
+                            counts[None, :, None], dm, dff, n_mats=nm,
+                            slot_layout=(base, base + E) if base else None)
         for name in ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2"):
             want_g = host.groups(name)
             got = dev[offs[name]:offs[name] + want_g.nbytes]
