@@ -304,7 +304,11 @@ typedef struct fssdp_gemm_group {
  * c_dest_maps (nullable): device array of 128-byte tensor maps made by
  * fssdp_epilogue_tmap, the destinations of groups with c_dest > 0 — a wgrad pushes a
  * replica's partial gradient into its owner's staging slot over NVLink this way.
- * flags: FSSDP_GEMM_N_FASTEST orders a group's tiles N-fastest (A tile shared in L2). */
+ * flags: FSSDP_GEMM_N_FASTEST orders a group's tiles N-fastest (A tile shared in L2).
+ * tile_sched (nullable): device int32[2], zero before the first launch and left zero after
+ * each — the persistent CTAs then take tiles dynamically in list order from this counter
+ * (CTAs that start late or share their SM with another kernel take fewer); null = a static
+ * snake order.  Not shared by launches that may run concurrently. */
 #define FSSDP_GEMM_N_FASTEST 1
 /* CTA-pair (tcgen05 cta_group::2) 256 x 256 tiles; requires every group's m_tiles even. */
 #define FSSDP_GEMM_CTA_PAIR 2
@@ -315,7 +319,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
                        int32_t total_tiles, void* c, void* c2, const void* aux,
                        const void* c_dest_maps, int64_t ldc, int64_t c_rows, int32_t flags,
-                       void* stream);
+                       int32_t* tile_sched, void* stream);
 /* The epilogue tensor map fssdp_grouped_gemm builds for C = [rows][ldc] at `base` with
  * this epilogue (128 bytes into map_out, host memory); upload it for c_dest_maps. */
 int fssdp_epilogue_tmap(int32_t epilogue, const void* base, int64_t ldc, int64_t rows,

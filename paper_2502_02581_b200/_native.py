@@ -116,7 +116,7 @@ _SIGS = {
                                   C.POINTER(DispatchLaunch)],
     # device data plane (device pointers as void*)
     "fssdp_grouped_gemm": [i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i32, i32, i32, vp, vp,
-                           vp, vp, i64, i64, i32, vp],
+                           vp, vp, i64, i64, i32, vp, vp],
     "fssdp_epilogue_tmap": [i32, vp, i64, i64, vp],
     "fssdp_gate_topk": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp],
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],

@@ -95,18 +95,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
-def build_gemm_profile() -> Path:
-    out = ROOT / "build" / "fssdp_prof"
+def build_variant(lib: Path, defines: tuple, tag: str) -> Path:
+    """A diagnostic / experiment build of the same sources with extra -D defines (selected
+    at run time with FSSDP_LIB=<path>)."""
+    out = ROOT / "build" / tag
     out.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
-        objs = list(pool.map(lambda s: _compile(s, False, out, ("-DFSSDP_GEMM_PROFILE",)), srcs))
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB_PROF), *map(str, objs),
+        objs = list(pool.map(lambda s: _compile(s, False, out, defines), srcs))
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),
            "-lstdc++"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
-    return LIB_PROF
+    return lib
+
+
+def build_gemm_profile() -> Path:
+    return build_variant(LIB_PROF, ("-DFSSDP_GEMM_PROFILE",), "fssdp_prof")
 
 
 def main() -> None:
@@ -115,10 +121,16 @@ def main() -> None:
     ap.add_argument("--verbose", action="store_true", help="print ptxas resource usage")
     ap.add_argument("--gemm-profile", action="store_true",
                     help="also build the diagnostic GEMM role-wait counter variant")
+    ap.add_argument("--variant", nargs=2, metavar=("LIB", "DEFINES"),
+                    help="an experiment build: output .so path and comma-separated defines")
     args = ap.parse_args()
     print(build(force=args.force, verbose=args.verbose))
     if args.gemm_profile:
         print(build_gemm_profile())
+    if args.variant:
+        lib, defs = args.variant
+        print(build_variant(Path(lib).resolve(), tuple("-D" + d for d in defs.split(",") if d),
+                            Path(lib).stem))
 
 
 if __name__ == "__main__":

@@ -260,7 +260,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,
                        int32_t total_tiles, void* c, void* c2, const void* aux,
                        const void* c_dest_maps, int64_t ldc, int64_t c_rows, int32_t flags,
-                       void* stream) {
+                       int32_t* tile_sched, void* stream) {
   if (num_groups <= 0 || n_tiles <= 0 || total_tiles < -1 || c == nullptr || c_rows <= 0) {
     set_error("grouped_gemm: bad arguments");
     return kErrDimension;
@@ -288,6 +288,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.c2 = c2;
   args.aux = static_cast<const __nv_bfloat16*>(aux);
   args.c_dest_maps = c_dest_maps;
+  args.sched = tile_sched;
   int rc = grouped_gemm_launch(a_mn, b_mn, epilogue, a, a_inner, a_outer, b, b_inner, b_outer,
                                c_rows, args, reinterpret_cast<cudaStream_t>(stream));
   if (rc == kErrCuda && g_last_error.empty()) set_error("grouped_gemm launch failed");

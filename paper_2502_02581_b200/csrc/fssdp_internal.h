@@ -41,6 +41,7 @@ struct GemmLaunch {
   void* c2;         // second output (GeLU: post-activation)
   const __nv_bfloat16* aux;  // DGeLU: pre-activation, same layout as c
   const void* c_dest_maps;   // device CUtensorMap[] for groups with c_dest > 0 (nullable)
+  int* sched;                // device int32[2] tile / exit counters, zero (nullable: static order)
 };
 
 int num_sms();

@@ -64,6 +64,11 @@ constexpr int gemm_threads() {
   return 64 + 32 * epi_warps<EPI>();
 }
 constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store box)
+// Dynamic tile scheduling (GemmLaunch.sched != null): the (leader) producer takes the next
+// tile from a global counter and hands its id to the MMA issuer, the epilogue warps and
+// the peer CTA through a ring of kSched entries — CTA (pairs) that start late, or whose
+// SMs are shared with a co-running kernel, simply take fewer tiles.
+constexpr int kSched = 8;
 
 template <int BN, int EPI, int CG>
 struct GemmSmem {
@@ -84,14 +89,17 @@ struct GemmSmem {
   static constexpr int kEpiWarpBytes = (kCBufs + kAuxBufs * kAuxTiles) * kBufBytes;
   // as many mainloop stages (up to 6) as the 227 KB budget leaves
   static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
-  static constexpr int kBarBytes = (2 * 6 + 4 + 4 * kEpiWarps) * 8 + 16;
+  // dynamic tile scheduler ring (kSched entries): full / empty mbarriers + the tile ids
+  static constexpr int kSchedBytes = 2 * kSched * 8 + kSched * 8;
+  static constexpr int kBarBytes = (2 * 6 + 4 + 4 * kEpiWarps) * 8 + 16 + kSchedBytes;
   static constexpr int kFit = (232448 - 1024 - kBarBytes - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kFit < 6 ? kFit : 6;
   static_assert(kStages >= 2, "shared memory budget exceeded");
   static constexpr int kEpiOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], aux[kEpiWarps][4], tmem base slot
-  static constexpr int kTotal = kBarOffset + (2 * kStages + 4 + 4 * kEpiWarps) * 8 + 16;
+  static constexpr int kTotal =
+      kBarOffset + (2 * kStages + 4 + 4 * kEpiWarps) * 8 + 16 + kSchedBytes;
   static constexpr int kDynamic = kTotal + 1024;  // slack for 1024-B alignment
   static_assert(kDynamic <= 232448, "shared memory budget exceeded");
 };
@@ -204,7 +212,10 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* aux_bar = tempty_bar + 2;
   constexpr int kEpiWarps = S::kEpiWarps;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4 * kEpiWarps);
+  uint64_t* sched_full = aux_bar + 4 * kEpiWarps;
+  uint64_t* sched_empty = sched_full + kSched;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_empty + kSched);
+  int32_t* sched_tile = reinterpret_cast<int32_t*>(tmem_slot + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -226,6 +237,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       mbar_init(&tempty_bar[a], kEpiWarps * CG);  // one arrival per epilogue warp of the pair
     }
     for (int a = 0; a < 4 * kEpiWarps; ++a) mbar_init(&aux_bar[a], 1);
+    // sched_empty (used on the leader): its MMA issuer, every epilogue warp of the pair
+    // and the peer's producer release an entry
+    for (int i = 0; i < kSched; ++i) {
+      mbar_init(&sched_full[i], 1);
+      mbar_init(&sched_empty[i], 1 + CG * kEpiWarps + (CG - 1));
+      sched_tile[2 * i] = -1;  // round tag of an entry never published
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -253,13 +271,97 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
            : args.groups[args.num_groups - 1].tile_start +
                  args.groups[args.num_groups - 1].m_tiles * args.n_tiles) / CG;
 
+  const bool dyn = args.sched != nullptr;
+  // consumer side of the scheduler ring: entry `it` -> tile id (-1: no more work); the
+  // entry is released on the leader (remote arrive from the follower CTA)
+  auto sched_take = [&](int it) -> int {
+    const int slot = it % kSched;
+    // CTA-scope wait (a cluster-scope acquire here, in every consumer warp, cost ~3 % of
+    // the step: the epilogue-heavy GEMMs slowed by 15 %), then the entry's round tag is
+    // checked, so a value from another CTA is never used before it has landed
+    mbar_wait(&sched_full[slot], static_cast<uint32_t>(it / kSched) & 1u);
+    int2 v;
+    do {
+      v = ld_volatile_shared_v2(&sched_tile[2 * slot]);
+    } while (v.x != it);
+    const int t = v.y;
+    if (CG == 2 && !leader)
+      mbar_arrive_leader(&sched_empty[slot]);
+    else
+      mbar_arrive(&sched_empty[slot]);
+    return t;
+  };
+  // the tile of round `it` for a role: static snake order, or the ring
+  auto next_tile = [&](int it) -> int {
+    if (!dyn) {
+      const int t = snake_tile(it, unit, units);
+      return t < total ? t : -1;
+    }
+    return sched_take(it);
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       // ===================== TMA producer (both CTAs stage their own halves)
       PROF_T0(tp0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
+      // The pair's scheduler (leader producer): entry it + 1 is published while tile `it`
+      // is being loaded, so the peer CTA's producer never waits for a tile id at a tile
+      // boundary, and one atomic is always in flight (its round trip overlaps the loads).
+      int cur = -1, pending = 0;
+      bool done = !(dyn && leader);
+      auto sched_exit = [&]() {  // once per pair, on its first fetch past the end
+        // the last pair to run dry resets the counters for the next launch (stream order,
+        // or PDL's griddepcontrol.wait, keeps the next grid behind this one)
+        if (atomicAdd(args.sched + 1, 1) == units - 1) {
+          atomicExch(args.sched, 0);
+          atomicExch(args.sched + 1, 0);
+        }
+      };
+      auto publish = [&](int it, int t) {
+        const int slot = it % kSched;
+        if (it >= kSched)
+          mbar_wait(&sched_empty[slot], static_cast<uint32_t>(it / kSched - 1) & 1u);
+        // entry = {round, tile}: the round tag lets a consumer verify the value it read
+        st_volatile_shared_v2(&sched_tile[2 * slot], it, t);
+        mbar_arrive(&sched_full[slot]);
+        if (CG == 2) {
+          st_cluster_v2(cluster_map(&sched_tile[2 * slot], 1u), static_cast<uint32_t>(it),
+                        static_cast<uint32_t>(t));
+          mbar_arrive_cluster(cluster_map(&sched_full[slot], 1u));
+        }
+      };
+      if (!done) {
+        cur = atomicAdd(args.sched, 1);
+        if (cur >= total) {
+          cur = -1;
+          sched_exit();
+        }
+        publish(0, cur);
+        done = cur < 0;
+        if (!done) pending = atomicAdd(args.sched, 1);
+      }
+      for (int it = 0;; ++it) {
+        int tile;
+        if (dyn && leader) {
+          tile = cur;
+          if (!done) {
+            int t = pending;
+            if (t >= total) {
+              t = -1;
+              sched_exit();
+              done = true;
+            } else {
+              pending = atomicAdd(args.sched, 1);
+            }
+            publish(it + 1, t);
+            cur = t;
+          }
+        } else {
+          tile = next_tile(it);
+        }
+        if (tile < 0) break;
         const TileCoord tc =
             locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const GemmGroup& g = groups[tc.group];
@@ -323,7 +425,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
+      for (int it = 0;; ++it) {
+        const int tile = next_tile(it);
+        if (tile < 0) break;
         const TileCoord tc =
             locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
         const int kblocks = groups[tc.group].k_blocks;
@@ -400,7 +504,11 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     PROF_T0(tep0);
     // aux / output column of f-space column j in the interleaved [a1|a3] layout (SwiGLU)
     auto a13_col = [](int j) { return 256 * (j >> 7) + (j & 127); };
-    for (int it = 0, tile = unit; tile < total; tile = snake_tile(++it, unit, units)) {
+    for (int it = 0;; ++it) {
+      int tile = 0;
+      if (lane == 0) tile = next_tile(it);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile < 0) break;
       const TileCoord tc =
           locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
       const GemmGroup& g = groups[tc.group];

@@ -319,6 +319,10 @@ class FssdpMoE:
         wg_tiles = max(1, (Tc + WG_TILE - 1) // WG_TILE)
         self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
+        # dynamic tile scheduler counters of this layer's GEMMs (all on the main stream, in
+        # order; each launch leaves them zero) — used with FSSDP_GEMM_DYN=1
+        self.gemm_sched = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        self._gemm_sched_ptr = C.c_void_p(self.gemm_sched.data_ptr() if self.GEMM_DYN else 0)
         self.gate_ws = torch.zeros(1 + E, dtype=torch.int32, device=self.dev)  # ticket, totals
         self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
         self.blob_host_np = self.blob_host.numpy()
@@ -942,6 +946,10 @@ class FssdpMoE:
     def _early_gate(self) -> bool:
         return self.EARLY_GATE and 4 % self.g.top_k == 0 and self.world > 1
     CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
+    # dynamic tile scheduling of the grouped GEMMs (FSSDP_GEMM_DYN=1): measured neutral in
+    # isolation (cfg2 shapes within +-1.5 %) and 1.7 % slower per step than the static snake
+    # order (interleaved A/B, N=1), so off by default
+    GEMM_DYN = os.environ.get("FSSDP_GEMM_DYN", "0") == "1"
 
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
@@ -970,7 +978,8 @@ class FssdpMoE:
         self._timed("gemm." + name, lambda: N.call(
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
             ops._ptr(b), b.shape[1], b.shape[0], tab, ng, n_tiles, total, ops._ptr(c),
-            ops._ptr(c2), ops._ptr(aux), maps, ldc, c.numel() // ldc, flags, self._stream()))
+            ops._ptr(c2), ops._ptr(aux), maps, ldc, c.numel() // ldc, flags,
+            self._gemm_sched_ptr, self._stream()))
 
     def phase_experts_fwd(self) -> None:
         f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1

@@ -60,12 +60,13 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
                  epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
                  aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
                  cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None,
-                 bn128: bool = False) -> None:
+                 bn128: bool = False, dynamic: bool = True) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
     aux) the whole output tensor, viewed as [numel // ldc, ldc].  c_dest_maps: device
-    uint8 tensor of 128-byte tensor maps (epilogue_tmap) for groups with c_dest > 0."""
+    uint8 tensor of 128-byte tensor maps (epilogue_tmap) for groups with c_dest > 0.
+    dynamic: tiles taken from a device counter (else the static snake order)."""
     for t, nm in ((a, "A"), (b, "B")):
         _need(t, torch.bfloat16, nm)
         if t.dim() != 2:
@@ -76,7 +77,19 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
            a.shape[0], _ptr(b), b.shape[1], b.shape[0], _ptr(groups_dev), num_groups, n_tiles,
            total_tiles, _ptr(c), _ptr(c2), _ptr(aux), _ptr(c_dest_maps), ldc, c.numel() // ldc,
            (GEMM_N_FASTEST if n_fastest else 0) | (GEMM_CTA_PAIR if cta_pair else 0) |
-           (GEMM_BN128 if bn128 else 0), _stream(stream))
+           (GEMM_BN128 if bn128 else 0), _sched(a.device) if dynamic else None, _stream(stream))
+
+
+_SCHED: dict = {}
+
+
+def _sched(device) -> C.c_void_p:
+    """Per-device tile-scheduler counters for grouped_gemm (left zero by every launch)."""
+    key = torch.device(device).index
+    t = _SCHED.get(key)
+    if t is None:
+        t = _SCHED[key] = torch.zeros(2, dtype=torch.int32, device=device)
+    return C.c_void_p(t.data_ptr())
 
 
 def epilogue_tmap(epilogue: int, base_ptr: int, ldc: int, rows: int) -> bytes:

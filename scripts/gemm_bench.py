@@ -1,4 +1,5 @@
-"""Quick tcgen05 grouped-GEMM throughput probe (CUDA events), cfg2 fwd1/fwd2/dgrad/wgrad shapes."""
+"""Quick tcgen05 grouped-GEMM throughput probe (CUDA events), cfg2 fwd1/fwd2/dgrad/wgrad shapes.
+DYN=0: the static snake tile order instead of the dynamic tile scheduler."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -40,6 +41,9 @@ Y = torch.empty(R, d, device="cuda").bfloat16()
 dW1 = torch.empty(G * f, d, device="cuda")
 flop_one = 2 * R * d * f
 res = {}
+DYN = os.environ.get("DYN", "1") != "0"
+_gg = ops.grouped_gemm
+ops.grouped_gemm = lambda *a, **k: _gg(*a, **k, dynamic=DYN)
 gd = groups([(Mg // 128, g * Mg, 0, g * f, 0, d // 64, g * Mg * f) for g in range(G)], f // 256)
 res["fwd1_gelu"] = timeit(lambda: ops.grouped_gemm(X, False, W1, False, *gd[:2], f // 256, gd[2], A, f, ops.EPI_GELU, c2=Hout))
 gd2 = groups([(Mg // 128, g * Mg, 0, g * d, 0, f // 64, g * Mg * d) for g in range(G)], d // 256)
@@ -54,4 +58,4 @@ Xf = X.view(G, Mg, d)
 W1v = W1.view(G, f, d)
 res["torch_bmm_fwd1"] = timeit(lambda: torch.bmm(Xf, W1v.transpose(1, 2)))
 for k, v in res.items():
-    print(f"{k:20s} {v*1e3:9.1f} us  {flop_one / (v * 1e-3) / 1e12:8.1f} TFLOP/s")
+    print(f"dyn={int(DYN)} {k:20s} {v*1e3:9.1f} us  {flop_one / (v * 1e-3) / 1e12:8.1f} TFLOP/s")

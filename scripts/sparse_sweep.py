@@ -83,7 +83,7 @@ def main():
             N.call("fssdp_grouped_gemm", 1, 1, ops.EPI_F32, ops._ptr(a), a_w, 64, ops._ptr(b),
                    b_w, 64, C.c_void_p(blob.data_ptr() + tab.offsets[name]), n_sh,
                    tab.gemm[name][1], tiles, ops._ptr(grads), None, None, ops._ptr(maps[name]),
-                   ldc, grads.numel() // ldc, 2, sp)
+                   ldc, grads.numel() // ldc, 2, None, sp)
     pb = C.c_void_p(group.peer_bases.data_ptr())
     E = world
     base = F.make_even_partition(E, topo)

@@ -485,3 +485,33 @@ def test_wgrad_long_token_k(segs, pair):
         ref = At[k0:k0 + s_].float().T @ Bt[k0:k0 + s_].float()
         _close(C[g * M:(g + 1) * M], ref, rel=1e-4, abs_=0.0 if s_ else 1e-30)
         k0 += s_
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_dynamic_tile_scheduler_equals_static_order(pair):
+    """Tiles taken from the device counter (default) or in the static snake order: the
+    same bits (each tile is computed the same way whoever takes it), and every launch
+    leaves the counters zero for the next."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(11)
+    K, N = 512, 1024
+    m_tiles = [2, 6, 0, 4, 2, 8]
+    R = sum(m_tiles) * 128
+    G = len(m_tiles)
+    A = torch.randn(R, K, device=dev).bfloat16()
+    B = (torch.randn(G * N, K, device=dev) / K ** 0.5).bfloat16()
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, g * N, 0, K // 64, r0 * N))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    outs = []
+    for dynamic in (True, False, True):
+        C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+        ops.grouped_gemm(A, False, B, False, gd, ng, N // 256, total, C, N, cta_pair=pair,
+                         dynamic=dynamic)
+        torch.cuda.synchronize()
+        outs.append(C)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert not ops._SCHED[torch.device(dev).index or 0].any()
