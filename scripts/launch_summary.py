@@ -11,6 +11,16 @@ import sys
 path = sys.argv[1]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 per_step = int(sys.argv[3]) if len(sys.argv) > 3 else 15
+OURS = ("gate_", "dispatch", "combine", "grouped_gemm", "spag", "sprs", "push_host",
+        "pull_host", "barrier", "local_gemm", "route_scan", "adam", "epoch")
+
+
+def _ours(name: str) -> bool:
+    """This framework's kernels (ncu prints them with or without the fssdp:: namespace)."""
+    base = name.replace("void ", "").replace("fssdp::", "").split("(")[0]
+    return base.startswith(OURS) or "fssdp::" in name
+
+
 rows = list(csv.reader(open(path)))
 hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 h = rows[hdr]
@@ -18,7 +28,7 @@ data = [dict(zip(h, r)) for r in rows[hdr + 1:] if len(r) == len(h)]
 unit = data[0]["Metric Unit"] if data else "ns"
 to_us = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3}[unit]
 seq = [(d["Kernel Name"].split("(")[0].replace("void ", "")[:58], float(d["Metric Value"]) * to_us)
-       for d in data if d["Metric Name"] == "gpu__time_duration.sum" and "fssdp::" in d["Kernel Name"]]
+       for d in data if d["Metric Name"] == "gpu__time_duration.sum" and _ours(d["Kernel Name"])]
 last = seq[-per_step * steps:]
 agg = collections.OrderedDict()
 for nm, v in last:
