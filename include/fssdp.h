@@ -369,7 +369,12 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
                      int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
                      int32_t* local_tables, int32_t local_d_ff, int32_t local_n_mats,
                      int32_t local_param_base, void* counts_host, int64_t counts_bytes,
-                     uint32_t* flag_host, uint32_t flag_value, void* stream);
+                     uint32_t* flag_host, uint32_t flag_value, void* gemm_ws,
+                     int64_t gemm_ws_bytes, void* stream);
+/* Workspace bytes of the tensor-core gate path of fssdp_gate_route (gemm_ws, device
+ * memory): the logits x . [hi(Wg); lo(Wg)] as one tcgen05 grouped-GEMM launch (fp32 C of
+ * T x 128), then the selection / count kernel.  E <= 64, d % 64 == 0. */
+int64_t fssdp_gate_gemm_ws_bytes(int64_t T, int32_t d);
 int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int32_t E,
                                int32_t* tile_prefix, const uint64_t* peer_bases, int64_t table_off,
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,

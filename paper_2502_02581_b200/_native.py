@@ -122,7 +122,8 @@ _SIGS = {
     "fssdp_topk_from_logits": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "fssdp_gate_route": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i64,
                          i32, i32, i32, C.c_uint32, vp, i32, i32, i32, vp, i64, vp,
-                         C.c_uint32, vp],
+                         C.c_uint32, vp, i64, vp],
+    "fssdp_gate_gemm_ws_bytes": [i64, i32],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier_selftest": [vp, i64, i64, i32, i32, i32, u32, i32, vp, vp],
@@ -160,13 +161,14 @@ _SIGS = {
     "fssdp_host_wait": [vp, u32, f64],
     "fssdp_pull_host": [vp, vp, i64, vp],
 }
-_RESTYPE = {"fssdp_version": C.c_char_p, "fssdp_last_error": C.c_char_p}
+_RESTYPE = {"fssdp_version": C.c_char_p, "fssdp_last_error": C.c_char_p,
+            "fssdp_gate_gemm_ws_bytes": C.c_int64}
 
 
 def header_symbols() -> list[str]:
     """Every function the public header declares (for the export check)."""
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(fssdp_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char\*)\s+(fssdp_\w+)\s*\(", text, re.M)))
 
 
 def _load() -> C.CDLL:

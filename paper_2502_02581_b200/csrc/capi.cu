@@ -8,6 +8,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <utility>
 
 #include "fssdp_internal.h"
@@ -70,8 +71,46 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Encoded tensor maps are cached by their arguments: the layer launches the same few
+// GEMM operand / output maps every step, and an encode costs microseconds of host time on
+// the launch path.  (A map only holds the address and extents, never the data.)
+struct TmapKey {
+  const void* base;
+  int64_t inner, outer;
+  int box_inner, box_outer, dtype, swizzle;
+  bool operator<(const TmapKey& o) const {
+    return std::tie(base, inner, outer, box_inner, box_outer, dtype, swizzle) <
+           std::tie(o.base, o.inner, o.outer, o.box_inner, o.box_outer, o.dtype, o.swizzle);
+  }
+};
+static int make_tmap_2d_uncached(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
+                                 int box_inner, int box_outer, int dtype, int swizzle_bytes);
+
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_inner,
                  int box_outer, int dtype, int swizzle_bytes) {
+  static std::mutex mu;
+  static std::map<TmapKey, CUtensorMap> cache;
+  const TmapKey key{base, inner, outer, box_inner, box_outer, dtype, swizzle_bytes};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *map = it->second;
+      return kOk;
+    }
+  }
+  const int rc = make_tmap_2d_uncached(map, base, inner, outer, box_inner, box_outer, dtype,
+                                       swizzle_bytes);
+  if (rc == kOk) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 4096) cache.clear();  // bound it (buffers come and go in tests)
+    cache[key] = *map;
+  }
+  return rc;
+}
+
+static int make_tmap_2d_uncached(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
+                                 int box_inner, int box_outer, int dtype, int swizzle_bytes) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");

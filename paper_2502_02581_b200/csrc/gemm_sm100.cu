@@ -55,6 +55,9 @@ constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
 #ifndef FSSDP_GELU_EPI_WARPS
 #define FSSDP_GELU_EPI_WARPS 4
 #endif
+#ifndef FSSDP_F32_SETS
+#define FSSDP_F32_SETS 2
+#endif
 template <int EPI>
 constexpr int epi_warps() {
   return EPI == FSSDP_EPI_GELU ? FSSDP_GELU_EPI_WARPS : 4;
@@ -82,7 +85,10 @@ struct GemmSmem {
   // staged): C; C + C2 (GeLU); a1 + a3 + h (SwiGLU); da1 + da3 (SwiGLU backward)
   static constexpr int kOutTiles = EPI == kEpiGelu ? 2 : EPI == kEpiSwiglu ? 3
                                    : EPI == kEpiDSwiglu ? 2 : 1;
-  static constexpr int kCBufs = 2 * kOutTiles;
+  // staging sets per epilogue warp: chunk c uses set c % kSets and may reuse it once the
+  // TMA store issued kSets chunks earlier has read it (fp32 outputs: FSSDP_F32_SETS)
+  static constexpr int kSets = EPI == kEpiF32 ? FSSDP_F32_SETS : 2;
+  static constexpr int kCBufs = kSets * kOutTiles;
   // aux-tile prefetch ring (dgrad2): entries of one tile (GeLU') or two (a1, a3)
   static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : EPI == kEpiDSwiglu ? 2 : 0;
   static constexpr int kAuxTiles = EPI == kEpiDSwiglu ? 2 : 1;
@@ -542,7 +548,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 #pragma unroll 1
       for (int ci = 0; ci < kCW; ++ci, ++gchunk) {
         const int c = cbase + ci;
-        const int b = gchunk & 1;
+        const int b = static_cast<int>(gchunk % S::kSets);
         uint32_t r[32], r3[32];
         const uint32_t tm = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                             static_cast<uint32_t>(acc * BN + c * kEpiCols);
@@ -583,8 +589,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                   *reinterpret_cast<const int4*>(ab + S::kBufBytes + sw64(lane, j));
           }
         }
-        // the staging set b was last used two chunks ago: its TMA stores must have read it
-        if (lane == 0) bulk_wait_read<1>();
+        // the staging set b was last used kSets chunks ago: its TMA stores must have read it
+        if (lane == 0) bulk_wait_read<S::kSets - 1>();
         __syncwarp();
         uint8_t* cb = cbuf0 + b * kOT * S::kBufBytes;
         auto stage_bf16 = [&](uint8_t* dst, const __nv_bfloat162 (&v)[16]) {
@@ -762,8 +768,8 @@ static int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb,
       if constexpr (kFull || (!A_MN && B_MN))
         return launch_variant<A_MN, B_MN, BN, kEpiDGelu, CG>(ma, mb, mc, mx, args, stream);
       break;
-    case kEpiF32:
-      if constexpr (kFull || (A_MN && B_MN))
+    case kEpiF32:  // BN 128: the weight gradients (MN / MN) and the tensor-core gate logits
+      if constexpr (kFull || (A_MN == B_MN))
         return launch_variant<A_MN, B_MN, BN, kEpiF32, CG>(ma, mb, mc, mx, args, stream);
       break;
     case kEpiSwiglu:

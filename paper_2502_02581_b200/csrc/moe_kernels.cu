@@ -706,6 +706,81 @@ __global__ void __launch_bounds__(128 * KS)
                   SW ? reinterpret_cast<int32_t*>(gate_wsm) : nullptr, SW ? E * wrow / 4 : 0);
 }
 
+// ------------------------------------------------------------------ K1 on tcgen05
+// The gate logits as one grouped-GEMM launch on the 5th-generation tensor cores: x [T, d]
+// (K-major) times B = [hi(Wg); lo(Wg); 0] (kGateN x d bf16: the fp32 gate weights split
+// into two bf16 halves, ~16 mantissa bits) into fp32 C [T, kGateN]; then
+// logits[t, e] = (C[t, e] + C[t, E + e]) + bias[e].  The GEMM streams x through TMA at HBM
+// rate (the mma.sync gate kernel above is bound by the latency of its register loads).
+constexpr int kGateN = 128;  // the GEMM's N tile: hi and lo of up to 64 experts
+
+__global__ void __launch_bounds__(256)
+    gate_gemm_prep_kernel(const float* __restrict__ wg, int E, int d,
+                          __nv_bfloat16* __restrict__ b, GemmGroup* __restrict__ group,
+                          int m_tiles) {
+  const int64_t n = static_cast<int64_t>(kGateN) * d;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / d);
+    const int64_t c = i % d;
+    float v = 0.f;
+    if (row < E) {
+      v = wg[static_cast<int64_t>(row) * d + c];
+    } else if (row < 2 * E) {
+      const float w = wg[static_cast<int64_t>(row - E) * d + c];
+      v = w - __bfloat162float(__float2bfloat16_rn(w));
+    }
+    b[i] = __float2bfloat16_rn(v);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    *group = GemmGroup{m_tiles, 0, 0, 0, 0, 0, d / 64, 0, 0};
+}
+
+__global__ void __launch_bounds__(kGateThreads)
+    gate_select_kernel(const float* __restrict__ c, const float* __restrict__ bias, int64_t T,
+                       int E, int k, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                       int32_t* __restrict__ slot_rank, int32_t* __restrict__ tile_counts,
+                       int32_t* __restrict__ tile_prefix, int32_t* __restrict__ ws,
+                       const uint64_t* __restrict__ peer_bases, int64_t table_off,
+                       int64_t flags_off, int rank, int world, int slot, uint32_t epoch,
+                       GateLocalTables local, int stage_ints) {
+  __shared__ float lg[kGateTile][kGateMaxE + 1];
+  __shared__ int32_t s_idx[kGateTile * kGateMaxK];
+  __shared__ int32_t s_cnt[kGateMaxE];
+  __shared__ int is_last;
+  const int tile = blockIdx.x;
+  const int64_t t0 = static_cast<int64_t>(tile) * kGateTile;
+  for (int i = threadIdx.x; i < kGateTile * E; i += blockDim.x) {
+    const int r = i / E, e = i % E;
+    if (t0 + r < T) {
+      const float* row = c + (t0 + r) * kGateN;
+      const float v = __fadd_rn(__ldcs(row + e), __ldcs(row + E + e));
+      lg[r][e] = bias != nullptr ? __fadd_rn(v, bias[e]) : v;
+    }
+  }
+  __syncthreads();
+  gate_select_tile(&lg[0][0], kGateMaxE + 1, tile, T, E, k, s_idx, s_cnt, topk_idx, topk_w,
+                   slot_rank, tile_counts);
+  if (ws == nullptr) return;
+  // fused K2, as in gate_topk_mma_kernel: publish this tile's counts, the last CTA scans /
+  // all-gathers them
+  __syncthreads();
+  if (threadIdx.x < E) atomicAdd(ws + 1 + threadIdx.x, s_cnt[threadIdx.x]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int ticket = atomicAdd(ws, 1);
+    is_last = ticket == static_cast<int>(gridDim.x) - 1;
+    if (is_last) __threadfence();
+  }
+  __syncthreads();
+  if (!is_last) return;
+  extern __shared__ __align__(16) int32_t sel_stage[];  // the tail's tile-count staging
+  gate_route_tail(gridDim.x, E, tile_counts, tile_prefix, ws, peer_bases, table_off, flags_off,
+                  rank, world, slot, epoch, local, stage_ints > 0 ? sel_stage : nullptr,
+                  stage_ints);
+}
+
 __global__ void __launch_bounds__(kGateThreads)
     topk_from_logits_kernel(const float* __restrict__ logits, int64_t T, int E, int k,
                             int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
@@ -1702,6 +1777,11 @@ int fssdp_topk_from_logits(const float* logits, int64_t T, int32_t E, int32_t k,
   return launch_status();
 }
 
+int64_t fssdp_gate_gemm_ws_bytes(int64_t T, int32_t d) {
+  const int64_t rows = (T + 255) / 256 * 256;
+  return 1024 + (static_cast<int64_t>(kGateN) * d * 2 + 1023) / 1024 * 1024 + rows * kGateN * 4;
+}
+
 int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t T, int32_t d,
                      int32_t E, int32_t k, int32_t* topk_idx, float* topk_w, int32_t* slot_rank,
                      int32_t* tile_counts, int32_t* tile_prefix, int32_t* ws,
@@ -1709,7 +1789,8 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
                      int32_t rank, int32_t world, int32_t bar_slot, uint32_t epoch,
                      int32_t* local_tables, int32_t local_d_ff, int32_t local_n_mats,
                      int32_t local_param_base, void* counts_host, int64_t counts_bytes,
-                     uint32_t* flag_host, uint32_t flag_value, void* stream) {
+                     uint32_t* flag_host, uint32_t flag_value, void* gemm_ws,
+                     int64_t gemm_ws_bytes, void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E <= 0 || E > kGateMaxE || k <= 0 || k > kGateMaxK ||
       k > E || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world ||
       (local_tables != nullptr && world != 1) ||
@@ -1747,6 +1828,48 @@ int fssdp_gate_route(const void* x, const float* wg, const float* bias, int64_t 
     local.host_n16 = static_cast<int>(counts_bytes / 16);
     local.host_flag = flag_host;
     local.host_flag_value = flag_value;
+  }
+  if (gemm_ws != nullptr && tiles > 0) {  // the logits on tcgen05 (gate_gemm_prep_kernel)
+    if (E > kGateN / 2 || d % 64 != 0 || gemm_ws_bytes < fssdp_gate_gemm_ws_bytes(T, d)) {
+      set_error("gate_route: tensor-core gate needs E <= 64, d % 64 == 0 and "
+                "fssdp_gate_gemm_ws_bytes of workspace");
+      return kErrDimension;
+    }
+    uint8_t* w8 = static_cast<uint8_t*>(gemm_ws);
+    GemmGroup* group = reinterpret_cast<GemmGroup*>(w8);
+    __nv_bfloat16* bmat = reinterpret_cast<__nv_bfloat16*>(w8 + 1024);
+    float* cmat = reinterpret_cast<float*>(w8 + 1024 + (static_cast<int64_t>(kGateN) * d * 2 + 1023) /
+                                                          1024 * 1024);
+    const int m_tiles = static_cast<int>(2 * ((T + 255) / 256));  // 128-row units, pairs
+    const int64_t nb = static_cast<int64_t>(kGateN) * d;
+    const int pb = static_cast<int>((nb + 255) / 256 < 2 * num_sms() ? (nb + 255) / 256 : 2 * num_sms());
+    timing_begin(as_stream(stream));
+    gate_gemm_prep_kernel<<<pb, 256, 0, as_stream(stream)>>>(wg, E, d, bmat, group, m_tiles);
+    int rc = launch_check();
+    if (rc != kOk) return rc;
+    GemmLaunch args = {};
+    args.groups = group;
+    args.num_groups = 1;
+    args.n_tiles = 1;
+    args.total_tiles = m_tiles;
+    args.n_fast = 0;
+    args.cta_group = 2;
+    args.bn = kGateN;
+    args.ldc = kGateN;
+    args.c = cmat;
+    rc = grouped_gemm_launch(0, 0, kEpiF32, x, d, T, bmat, d, kGateN,
+                             static_cast<int64_t>(m_tiles) * 128, args, as_stream(stream));
+    if (rc != kOk) return rc;
+    // dynamic smem for the last CTA's tile-count staging (the tail's scan)
+    const int stage_bytes = tiles * E * 4 <= 96 * 1024 ? tiles * E * 4 : 0;
+    if (stage_bytes > 48 * 1024 &&
+        ensure_dynamic_smem(reinterpret_cast<const void*>(gate_select_kernel), stage_bytes) !=
+            cudaSuccess)
+      return launch_status();
+    gate_select_kernel<<<tiles, kGateThreads, stage_bytes, as_stream(stream)>>>(
+        cmat, bias, T, E, k, topk_idx, topk_w, slot_rank, tile_counts, tile_prefix, ws,
+        peer_bases, table_off, flags_off, rank, world, bar_slot, epoch, local, stage_bytes / 4);
+    return launch_status();
   }
   if (!gate_mma_ok(d, E) || tiles == 0) {  // the two-kernel path (+ the local tables)
     int rc = fssdp_gate_topk(x, wg, bias, T, d, E, k, nullptr, topk_idx, topk_w, slot_rank,

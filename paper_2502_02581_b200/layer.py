@@ -301,6 +301,18 @@ class FssdpMoE:
         k = geom.top_k
         tiles = (Tc + ops.GATE_TILE - 1) // ops.GATE_TILE
         self.wg = torch.empty(E, d, dtype=torch.float32, device=self.dev)
+        # the gate logits on tcgen05 (one grouped-GEMM launch + selection): its workspace
+        self._gate_gemm_bytes = 0
+        self.gate_gemm_ws = None
+        # default: only where the mma.sync gate cannot stage its split weights in shared
+        # memory (E x (4 d + 16) > 80 KB, e.g. cfg4's 64 x 2048: 126 us there); at cfg2 the
+        # staged mma.sync gate is as fast in isolation and 0.3 % faster per step
+        gate_gemm = (self.GATE_GEMM if self.GATE_GEMM is not None
+                     else E * (4 * d + 16) > 80 * 1024)
+        if gate_gemm and E <= 64 and d % 64 == 0:
+            self._gate_gemm_bytes = int(N.LIB.fssdp_gate_gemm_ws_bytes(geom.max_tokens, d))
+            self.gate_gemm_ws = torch.empty(self._gate_gemm_bytes, dtype=torch.uint8,
+                                            device=self.dev)
         self.gate_bias = torch.zeros(E, dtype=torch.float32, device=self.dev)
         self.dwg = torch.zeros(E, d, dtype=torch.float32, device=self.dev)
         self.topk_idx = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
@@ -675,7 +687,10 @@ class FssdpMoE:
                    max(0, self.g.owned_base),
                    C.c_void_p(self.counts_host_ptr if fused else 0), self.counts_nbytes,
                    C.c_void_p(self.counts_flag_ptr if fused else 0),
-                   C.c_uint32(self._counts_epoch), self._stream())
+                   C.c_uint32(self._counts_epoch),
+                   ops._ptr(self.gate_gemm_ws), self._gate_gemm_bytes, self._stream())
+        if self.gate_gemm_ws is not None:
+            N.launch_count += 2  # + the weight-split and GEMM launches
 
     def phase_counts(self) -> None:
         """The counts are all-gathered by the gate launch; the early SpAG may start now."""
@@ -946,6 +961,9 @@ class FssdpMoE:
     def _early_gate(self) -> bool:
         return self.EARLY_GATE and 4 % self.g.top_k == 0 and self.world > 1
     CTA_PAIR = True  # tcgen05 cta_group::2 256x256 tiles (segments are 256-row aligned)
+    # the gate logits as a tcgen05 GEMM: FSSDP_GATE_GEMM=1 always, =0 never, unset: where
+    # the mma.sync gate cannot stage its weights (see __init__)
+    GATE_GEMM = {"0": False, "1": True}.get(os.environ.get("FSSDP_GATE_GEMM", ""))
     # dynamic tile scheduling of the grouped GEMMs (FSSDP_GEMM_DYN=1): measured neutral in
     # isolation (cfg2 shapes within +-1.5 %) and 1.7 % slower per step than the static snake
     # order (interleaved A/B, N=1), so off by default

@@ -59,3 +59,15 @@ W1v = W1.view(G, f, d)
 res["torch_bmm_fwd1"] = timeit(lambda: torch.bmm(Xf, W1v.transpose(1, 2)))
 for k, v in res.items():
     print(f"dyn={int(DYN)} {k:20s} {v*1e3:9.1f} us  {flop_one / (v * 1e-3) / 1e12:8.1f} TFLOP/s")
+
+# cfg4-shaped wgrad1 (64 experts x 512 token rows, M = n1 = 2 x 1408, N = d = 2048, fp32 out)
+G4, M4, d4, n14 = 64, 512, 2048, 2816
+dA4 = torch.randn(G4 * M4, n14, device="cuda").bfloat16()
+X4 = torch.randn(G4 * M4, d4, device="cuda").bfloat16()
+dW4 = torch.empty(G4 * n14, d4, device="cuda")
+gd5 = groups([(n14 // 128, 0, g * M4, 0, g * M4, M4 // 64, g * n14 * d4) for g in range(G4)], d4 // 256)
+t4 = timeit(lambda: ops.grouped_gemm(dA4, True, X4, True, *gd5[:2], d4 // 256, gd5[2], dW4, d4,
+                                     ops.EPI_F32, cta_pair=False), iters=10)
+fl4 = 2 * G4 * M4 * n14 * d4
+print(f"dyn={int(DYN)} cfg4_wgrad1_fp32     {t4*1e3:9.1f} us  {fl4 / (t4 * 1e-3) / 1e12:8.1f} TFLOP/s  "
+      f"{G4 * n14 * d4 * 4 / (t4 * 1e-3) / 1e9:7.0f} GB/s out")

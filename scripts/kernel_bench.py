@@ -76,6 +76,8 @@ def main():
     gws = torch.zeros(1 + E, dtype=torch.int32, device=dev)
     blob = torch.zeros(_layout(E, 1)[1], dtype=torch.uint8, device=dev)
     host = torch.zeros(32, dtype=torch.int32, pin_memory=True)
+    gws = torch.empty(int(N.LIB.fssdp_gate_gemm_ws_bytes(T, d)), dtype=torch.uint8, device=dev)
+    tc_gate = [False]
     ep = [0]
 
     def route():
@@ -85,9 +87,13 @@ def main():
                ops._ptr(gws), C.c_void_p(grp.peer_bases.data_ptr()), layout.offset("counts"),
                layout.offset("flags"), 0, 1, -1, 0, ops._ptr(blob), 4096, 2, 0,
                C.c_void_p(host.data_ptr()), 64, C.c_void_p(host.data_ptr() + 64),
-               C.c_uint32(ep[0]), stream)
+               C.c_uint32(ep[0]), ops._ptr(gws) if tc_gate[0] else None,
+               gws.numel() if tc_gate[0] else 0, stream)
     res["gate_route_cold_us"] = timeit(route)
     res["gate_route_warm_us"] = timeit(route, cold=False)
+    tc_gate[0] = True  # the tensor-core gate path
+    res["gate_route_tc_cold_us"] = timeit(route)
+    res["gate_route_tc_warm_us"] = timeit(route, cold=False)
     res["gate_topk_warm_us"] = timeit(lambda: ops.gate_topk(x, wg, k, bias=bias), cold=False)
     res["gate_wgrad_us"] = timeit(lambda: N.call(
         "fssdp_gate_wgrad", ops._ptr(x), ops._ptr(idx), ops._ptr(dlogit), T, d, E, k,

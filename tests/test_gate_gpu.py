@@ -93,7 +93,7 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
                *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0,
                ops._ptr(blob) if local else None, 512 if local and d % 256 == 0 else 0, 2, 0,
                C.c_void_p(host.data_ptr() if local else 0), (E * 4 + 15) // 16 * 16,
-               C.c_void_p(flag_ptr if local else 0), C.c_uint32(7), s)
+               C.c_void_p(flag_ptr if local else 0), C.c_uint32(7), None, 0, s)
         torch.cuda.synchronize()
         for a, b in zip(want, [t.cpu() for t in out] + [table.cpu()]):
             assert torch.equal(a, b)
@@ -136,3 +136,57 @@ def test_gate_route_fused_equals_two_kernels(T, d, E, k):
             want_g = host.groups(name)
             got = dev[offs[name]:offs[name] + want_g.nbytes]
             assert got.tobytes() == want_g.tobytes(), (name, dm, dff, nm)
+
+
+@pytest.mark.parametrize("T,d,E,k", [(16384, 1024, 16, 2), (16384, 2048, 64, 2), (1000, 256, 8, 2),
+                                     (777, 4096, 8, 2), (130, 192, 16, 4)])
+def test_tensor_core_gate_route(T, d, E, k):
+    """The tcgen05 gate path of fssdp_gate_route (logits = x . [hi(Wg); lo(Wg)] as one
+    grouped-GEMM launch, then selection + the count tail): logits within 1e-4 of the fp64
+    product, selection / weights / ranks / tile counts / prefixes bit-exact with
+    fssdp_topk_from_logits applied to those same logits, totals all-gathered, workspace
+    left zero."""
+    import ctypes as C
+
+    from paper_2502_02581_b200 import _native as N
+    from paper_2502_02581_b200 import ops
+    from paper_2502_02581_b200.comm import HeapLayout, emulated_group
+
+    g = torch.Generator().manual_seed(T + d + E)
+    x = torch.randn(T, d, generator=g).bfloat16().cuda()
+    wg = (torch.randn(E, d, generator=g) / d ** 0.5).cuda()
+    bias = torch.linspace(-1, 1, E).cuda()
+    layout = HeapLayout()
+    layout.add("counts", 4 * E * 4)
+    (grp,) = emulated_group(layout, 1)
+    pb, off, flags = C.c_void_p(grp.peer_bases.data_ptr()), layout.offset("counts"), layout.offset("flags")
+    table = grp.local.tensor(off, (E,), torch.int32)
+    tiles = (T + ops.GATE_TILE - 1) // ops.GATE_TILE
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nbytes = int(N.LIB.fssdp_gate_gemm_ws_bytes(T, d))
+    gws = torch.full((nbytes,), 0x7F, dtype=torch.uint8, device="cuda")  # garbage: no init needed
+    ws = torch.zeros(1 + E, dtype=torch.int32, device="cuda")
+    out = [torch.empty(T, k, dtype=torch.int32, device="cuda"),
+           torch.empty(T, k, dtype=torch.float32, device="cuda"),
+           torch.empty(T, k, dtype=torch.int32, device="cuda"),
+           torch.empty(tiles, E, dtype=torch.int32, device="cuda"),
+           torch.empty(tiles, E, dtype=torch.int32, device="cuda")]
+    for _ in range(2):
+        table.zero_()
+        N.call("fssdp_gate_route", ops._ptr(x), ops._ptr(wg), ops._ptr(bias), T, d, E, k,
+               *[ops._ptr(t) for t in out], ops._ptr(ws), pb, off, flags, 0, 1, -1, 0, None, 0,
+               2, 0, None, 0, None, C.c_uint32(0), ops._ptr(gws), nbytes, s)
+        torch.cuda.synchronize()
+        assert not ws.any()
+    # the logits the selection used: C [rows, 128] fp32 after the 1 KB header and B
+    cm_off = 1024 + (128 * d * 2 + 1023) // 1024 * 1024
+    cmat = gws[cm_off:cm_off + T * 128 * 4].view(torch.float32).view(T, 128)
+    logits = (cmat[:, :E] + cmat[:, E:2 * E]) + bias
+    ref = (x.double() @ wg.double().T) + bias.double()
+    assert (logits.double() - ref).abs().max().item() <= 1e-4 * ref.abs().max().item()
+    idx, w, rank, tc = ops.topk_from_logits(logits.contiguous(), k)
+    assert torch.equal(out[0], idx) and torch.equal(out[1], w)
+    assert torch.equal(out[2], rank) and torch.equal(out[3], tc)
+    prefix = torch.cumsum(tc, 0) - tc
+    assert torch.equal(out[4], prefix.int())
+    assert torch.equal(table, tc.sum(0).int())
