@@ -942,9 +942,13 @@ class FssdpMoE:
         else:
             N.timed_launch(self.timers, key, fn)
 
-    # tile order per GEMM: N-fastest where the A operand (activations) is the big,
-    # re-read one (N = d_model: 4 tiles share each A tile), M-fastest elsewhere
-    N_FASTEST = {"fwd2": True, "dgrad1": True}
+    # tile order per GEMM: N-fastest (neighbouring CTAs share the A tile: the activation
+    # rows) for the forward / dgrad GEMMs, M-fastest (sharing the B tile) for the wgrads
+    # (fwd1 / dgrad2 N-fastest too: 0.4 % per step, interleaved A/B at N = 1)
+    N_FASTEST = {"fwd2": True, "dgrad1": True, "fwd1": True, "dgrad2": True}
+    for _k in os.environ.get("FSSDP_NFAST", "").split(","):  # experiments: extra N-fastest GEMMs
+        if _k:
+            N_FASTEST[_k] = True
     KEEP_Y_SLOTS = os.environ.get("FSSDP_KEEP_Y", "1") != "0"
     # N > 1: dispatch_grad writes the gate's dlogit (whole tokens per 4-slot warp batch), so
     # the gate backward runs on its own stream beside the expert GEMMs instead of after the
