@@ -174,10 +174,13 @@ struct TileCoord {
 template <int CG>
 __device__ __forceinline__ TileCoord locate_tile(const GemmGroup* __restrict__ groups,
                                                  int num_groups, int n_tiles, int n_fast,
-                                                 int tile) {
-  int g = 0;
-  // groups are few (<= experts per device + replica slots); a linear scan is cheapest
+                                                 int tile, int& cursor) {
+  // A role's tiles come in increasing order (snake rounds, or the scheduler's counter), so
+  // the group search resumes from the previous tile's group: a scan from group 0 is a chain
+  // of dependent loads as long as the group index (64+ groups at cfg4), at every tile.
+  int g = groups[cursor].tile_start / CG <= tile ? cursor : 0;
   while (g + 1 < num_groups && groups[g + 1].tile_start / CG <= tile) ++g;
+  cursor = g;
   const int local = tile - groups[g].tile_start / CG;
   const int mt = groups[g].m_tiles / CG;
   TileCoord tc;
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       PROF_T0(tp0);
       int stage = 0;
       uint32_t phase = 0;
+      int gcur = 0;  // group cursor (locate_tile)
       // The pair's scheduler (leader producer): entry it + 1 is published while tile `it`
       // is being loaded, so the peer CTA's producer never waits for a tile id at a tile
       // boundary, and one atomic is always in flight (its round trip overlaps the loads).
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         }
         if (tile < 0) break;
         const TileCoord tc =
-            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
+            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur);
         const GemmGroup& g = groups[tc.group];
         const int m0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * kBM;
         const int n0 = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * kBNc;
@@ -431,11 +435,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int gcur = 0;
       for (int it = 0;; ++it) {
         const int tile = next_tile(it);
         if (tile < 0) break;
         const TileCoord tc =
-            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
+            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur);
         const int kblocks = groups[tc.group].k_blocks;
         PROF_T0(te);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -507,6 +512,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t gchunk = 0;  // running chunk counter (selects the staging set)
+    int gcur = 0;
     PROF_T0(tep0);
     // aux / output column of f-space column j in the interleaved [a1|a3] layout (SwiGLU)
     auto a13_col = [](int j) { return 256 * (j >> 7) + (j & 127); };
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile < 0) break;
       const TileCoord tc =
-          locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile);
+          locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur);
       const GemmGroup& g = groups[tc.group];
       const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM) +
                        static_cast<int>(rank) * kBM + q * 32;
@@ -598,6 +604,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<int4*>(dst + sw64(lane, j)) = *reinterpret_cast<const int4*>(&v[4 * j]);
         };
+#ifdef FSSDP_EXP_EPI_NOSTS  // experiment: accumulators read, nothing staged or stored
+        if (true) {
+          if (r[0] == 0x7fc00001u && lane == 0) cb[0] = 1;  // keep the TMEM load live
+          continue;
+        }
+#endif
         if (EPI == kEpiF32) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -665,6 +677,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
+#ifdef FSSDP_EXP_EPI_NOSTORE  // experiment: staged in shared memory, never stored
+        if (true) continue;
+#endif
         if (lane == 0) {
           if (EPI == kEpiSwiglu) {
             const int j = col0 + c * kEpiCols;  // a1 column in the interleaved 2f layout

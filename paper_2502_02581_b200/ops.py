@@ -60,13 +60,14 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
                  epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
                  aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
                  cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None,
-                 bn128: bool = False, dynamic: bool = True) -> None:
+                 bn128: bool = False, dynamic: bool = False) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
     aux) the whole output tensor, viewed as [numel // ldc, ldc].  c_dest_maps: device
     uint8 tensor of 128-byte tensor maps (epilogue_tmap) for groups with c_dest > 0.
-    dynamic: tiles taken from a device counter (else the static snake order)."""
+    dynamic: tiles taken from a device counter (default: the static snake order, as the
+    layer runs)."""
     for t, nm in ((a, "A"), (b, "B")):
         _need(t, torch.bfloat16, nm)
         if t.dim() != 2:

@@ -1,5 +1,5 @@
 """Quick tcgen05 grouped-GEMM throughput probe (CUDA events), cfg2 fwd1/fwd2/dgrad/wgrad shapes.
-DYN=0: the static snake tile order instead of the dynamic tile scheduler."""
+DYN=1: the dynamic tile scheduler instead of the static snake order."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -41,7 +41,7 @@ Y = torch.empty(R, d, device="cuda").bfloat16()
 dW1 = torch.empty(G * f, d, device="cuda")
 flop_one = 2 * R * d * f
 res = {}
-DYN = os.environ.get("DYN", "1") != "0"
+DYN = os.environ.get("DYN", "0") != "0"
 _gg = ops.grouped_gemm
 ops.grouped_gemm = lambda *a, **k: _gg(*a, **k, dynamic=DYN)
 gd = groups([(Mg // 128, g * Mg, 0, g * f, 0, d // 64, g * Mg * f) for g in range(G)], f // 256)

@@ -84,3 +84,16 @@ profile("wgrad1", lambda: ops.grouped_gemm(H, True, X, True, *gd4[:2], d // 256,
 gd6 = groups([(d // 128, 0, g * Mg, 0, g * Mg, Mg // 64, g * f * d) for g in range(G)], f // 256)
 profile("wgrad2", lambda: ops.grouped_gemm(Y, True, H, True, *gd6[:2], f // 256, gd6[2], dW2, f,
                                            ops.EPI_F32, cta_pair=True))
+
+# cfg4-shaped wgrad1: 64 groups of 512 token rows (short K: 8 k-blocks per tile)
+G4, M4, d4, n14 = 64, 512, 2048, 2816
+dA4 = torch.randn(G4 * M4, n14, device="cuda").bfloat16()
+X4 = torch.randn(G4 * M4, d4, device="cuda").bfloat16()
+dW4 = torch.empty(G4 * n14, d4, device="cuda")
+dW4h = torch.empty(G4 * n14, d4, device="cuda").bfloat16()
+gd7 = groups([(n14 // 128, 0, g * M4, 0, g * M4, M4 // 64, g * n14 * d4) for g in range(G4)],
+             d4 // 256)
+profile("cfg4_wgrad1", lambda: ops.grouped_gemm(dA4, True, X4, True, *gd7[:2], d4 // 256, gd7[2],
+                                                dW4, d4, ops.EPI_F32, cta_pair=True))
+profile("cfg4_wgrad1_bf", lambda: ops.grouped_gemm(dA4, True, X4, True, *gd7[:2], d4 // 256,
+                                                   gd7[2], dW4h, d4, ops.EPI_BF16, cta_pair=True))
