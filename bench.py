@@ -98,6 +98,8 @@ def parse():
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default: config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--grad-dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="weight-gradient buffers (bf16: the reference's grad bytes = param bytes)")
     return ap.parse_args()
 
 
@@ -333,7 +335,7 @@ def _config(args, world):
             "experts": CFG2["num_experts"], "top_k": CFG2["top_k"], "d_model": CFG2["d_model"],
             "d_ff": CFG2["d_ff"], "tokens_per_gpu": args.tokens,
             "global_batch_tokens": args.tokens * world, "parallelism": f"fssdp{world}",
-            "policy": POLICY, "zipf_s": ZIPF_S,
+            "policy": POLICY, "zipf_s": ZIPF_S, "grad_dtype": args.grad_dtype,
             "l2": "per-step working set > 1 GB exceeds the 126 MB L2 (no explicit flush)"}
 
 
@@ -379,7 +381,7 @@ def run_ours(args):
     pol = F.Policy(F.PolicyKind.FSSDP, **POLICY)
     layer = create_layer(CFG2["d_model"], CFG2["d_ff"], CFG2["num_experts"], CFG2["top_k"], T,
                          pol, rank=rank, world=world, device=dev, seed=1234,
-                         activation=CFG["activation"])
+                         activation=CFG["activation"], grad_dtype=args.grad_dtype)
     E = CFG2["num_experts"]
     p = 1.0 / np.arange(1, E + 1) ** ZIPF_S
     p = p[np.random.default_rng(42).permutation(E)]

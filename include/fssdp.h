@@ -482,32 +482,35 @@ int fssdp_gather_slots(const uint64_t* peer_bases, int32_t rank, int64_t src_off
  * gradients into this rank's staging slots (c_dest groups); here, per job
  * jobs[n * 3] = {dst_slot, src_begin, src_count} with srcs[* 2] = {rank, idx} in ascending
  * rank order (owner included):  grads[dst_slot] = sum over srcs (fp32, listed order) of
- * (rank == this rank ? grads[idx] : stage[idx]).  Local memory only; slot_elems fp32 per
- * slot; grads / stage at heap offsets grad_off / stage_off. */
+ * (rank == this rank ? grads[idx] : stage[idx]).  Local memory only; slot_elems elements
+ * of elem_bytes per slot — 4: fp32, 2: bf16 (summed in fp32, rounded once; the reference's
+ * grad_bytes = param bytes, engine.py:223) — grads / stage at heap offsets grad_off /
+ * stage_off. */
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,
-               int64_t slot_elems, const int32_t* jobs, int32_t n_jobs, const int32_t* srcs,
-               void* stream);
+               int64_t slot_elems, int32_t elem_bytes, const int32_t* jobs, int32_t n_jobs,
+               const int32_t* srcs, void* stream);
 /* K8, pull variant — the standalone SparseReduceScatter (sprs_traffic's schedule,
  * costmodel.py:111-132): every holder's partial stays in its own grads slot and the owner
  * pulls them over NVLink through a TMA ring, summing in listed (ascending-rank) order:
  * grads[dst_slot] = sum over pull_srcs {r, slot} of rank r's grads[slot] (the
- * FSSDP_TAB_SPRS_PULL section; the owner's own entry is local).  The caller orders it after
- * every holder's partials are complete (device barrier) and keeps the holders' replica
- * grads intact until it has finished. */
+ * FSSDP_TAB_SPRS_PULL section; the owner's own entry is local; elem_bytes as fssdp_sprs).
+ * The caller orders it after every holder's partials are complete (device barrier) and
+ * keeps the holders' replica grads intact until it has finished. */
 int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
-                    int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
+                    int64_t slot_elems, int32_t elem_bytes, const int32_t* jobs, int32_t n_jobs,
                     const int32_t* pull_srcs, void* stream);
 
 /* ================================================================== training step */
 /* AdamW over n fp32 elements (n % 4 == 0): exp_avg / exp_avg_sq / master updated in place
- * from grads (bias corrections of `step` >= 1, decoupled weight decay), then params_bf16
+ * from grads (fp32, or bf16 when grads_bf16 != 0; bias corrections of `step` >= 1, decoupled
+ * weight decay), then params_bf16
  * (nullable: the master IS the parameter) = bf16(master).  The owner's expert shards keep
  * master / moments in the symmetric heap so a re-shard moves them with the parameters
  * (params + 6x state = the 7x expert_bytes of engine.py:233, 444-453).  Replaces nothing in
  * the reference (it prices the optimizer state, it has no optimizer). */
 int fssdp_adam_step(void* params_bf16, float* master, float* exp_avg, float* exp_avg_sq,
-                    const float* grads, int64_t n, float lr, float beta1, float beta2, float eps,
-                    float weight_decay, int64_t step, void* stream);
+                    const void* grads, int32_t grads_bf16, int64_t n, float lr, float beta1,
+                    float beta2, float eps, float weight_decay, int64_t step, void* stream);
 
 /* Owner-update epochs (flag pad slot `slot`, entry [slot][rank] of each rank's own pad):
  * fssdp_publish_epoch stores `epoch` (system-scope release) after every earlier write of the

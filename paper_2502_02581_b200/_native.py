@@ -137,10 +137,10 @@ _SIGS = {
     "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
     "fssdp_gather_slots": [vp, i32, i64, i64, i64, i64, vp, i32, i32, vp],
-    "fssdp_sprs": [vp, i32, i64, i64, i64, vp, i32, vp, vp],
-    "fssdp_sprs_pull": [vp, i32, i64, i64, vp, i32, vp, vp],
+    "fssdp_sprs": [vp, i32, i64, i64, i64, i32, vp, i32, vp, vp],
+    "fssdp_sprs_pull": [vp, i32, i64, i64, i32, vp, i32, vp, vp],
     # training step
-    "fssdp_adam_step": [vp, vp, vp, vp, vp, i64, C.c_float, C.c_float, C.c_float, C.c_float,
+    "fssdp_adam_step": [vp, vp, vp, vp, vp, i32, i64, C.c_float, C.c_float, C.c_float, C.c_float,
                         C.c_float, i64, vp],
     "fssdp_publish_epoch": [vp, i64, i32, i32, u32, vp],
     "fssdp_wait_epochs": [vp, i64, i32, i32, u32, vp],

@@ -1425,57 +1425,92 @@ __global__ void __launch_bounds__(32)
   bulk_wait<0>();
 }
 
+// Gradient elements in 16-byte vectors: 4 fp32, or 8 bf16 summed in fp32 (one rounding
+// after the last holder) — grad_dtype of the layer.
+template <bool BF16>
+struct GradVec {
+  static constexpr int kElems = BF16 ? 8 : 4;
+  float v[kElems];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < kElems; ++i) v[i] = 0.f;
+  }
+  __device__ __forceinline__ void add(const int4 raw) {  // v += raw, element by element
+    const uint32_t w[4] = {static_cast<uint32_t>(raw.x), static_cast<uint32_t>(raw.y),
+                           static_cast<uint32_t>(raw.z), static_cast<uint32_t>(raw.w)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (BF16) {
+        v[2 * i] = __fadd_rn(v[2 * i], __uint_as_float(w[i] << 16));
+        v[2 * i + 1] = __fadd_rn(v[2 * i + 1], __uint_as_float(w[i] & 0xffff0000u));
+      } else {
+        v[i] = __fadd_rn(v[i], __uint_as_float(w[i]));
+      }
+    }
+  }
+  __device__ __forceinline__ int4 pack() const {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (BF16) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+      } else {
+        w[i] = __float_as_uint(v[i]);
+      }
+    }
+    return make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]), static_cast<int>(w[2]),
+                     static_cast<int>(w[3]));
+  }
+};
+
 // Owner-side SpRS reduction (the holders' partials were pushed into the local staging
 // slots by their wgrad epilogues): local HBM reads only.  Persistent over (chunk, job)
 // units so the launcher can bound the SMs it occupies beside the backward GEMMs.
+// slot_bytes / chunk in bytes; BF16: bf16 gradient slots (GradVec).
+template <bool BF16>
 __global__ void __launch_bounds__(256)
     sprs_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
-                int64_t stage_off, int64_t slot_elems, const int32_t* __restrict__ jobs,
+                int64_t stage_off, int64_t slot_bytes, const int32_t* __restrict__ jobs,
                 const int32_t* __restrict__ srcs, int64_t chunk, int n_chunks, int n_units) {
   __shared__ const int4* s_src[kMaxWorld];
-  const int64_t chunk_elems = chunk / 4;
+  const int64_t slot_vecs = slot_bytes / 16;
+  const int64_t chunk_vecs = chunk / 16;
   for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
     const int job = unit / n_chunks;
     const int64_t dst_slot = jobs[3 * job];
     const int src_begin = jobs[3 * job + 1];
     const int src_count = jobs[3 * job + 2];
-    const int64_t begin = static_cast<int64_t>(unit % n_chunks) * chunk_elems;
+    const int64_t begin = static_cast<int64_t>(unit % n_chunks) * chunk_vecs;
     __syncthreads();  // previous unit's readers of s_src are done
     if (threadIdx.x < src_count) {  // own grads slot, or the staging slot a holder pushed
       const int r = srcs[2 * (src_begin + threadIdx.x)];
       const int64_t idx = srcs[2 * (src_begin + threadIdx.x) + 1];
       const int64_t off = r == rank ? grad_off : stage_off;
-      s_src[threadIdx.x] = reinterpret_cast<const int4*>(
-          reinterpret_cast<const float*>(peer_bases[rank] + off) + idx * slot_elems + begin);
+      s_src[threadIdx.x] =
+          reinterpret_cast<const int4*>(peer_bases[rank] + off) + idx * slot_vecs + begin;
     }
     __syncthreads();
-    const int64_t n = imin64(chunk_elems, slot_elems - begin);
-    const int n4 = static_cast<int>(n / 4);
-    float4* dst = reinterpret_cast<float4*>(
-        reinterpret_cast<float*>(peer_bases[rank] + grad_off) + dst_slot * slot_elems + begin);
-    // U float4 per thread per pass: U * src_count 128-bit loads in flight; each element is
+    const int n4 = static_cast<int>(imin64(chunk_vecs, slot_vecs - begin));
+    int4* dst = reinterpret_cast<int4*>(peer_bases[rank] + grad_off) + dst_slot * slot_vecs + begin;
+    // U vectors per thread per pass: U * src_count 128-bit loads in flight; each element is
     // still summed over the holders in ascending-rank order (bit-exact vs the oracle).
     constexpr int U = 4;
     for (int i0 = threadIdx.x; i0 < n4; i0 += U * 256) {
-      float4 acc[U];
+      GradVec<BF16> acc[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < U; ++u) acc[u].zero();
       for (int q = 0; q < src_count; ++q) {
         int4 raw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u)
           raw[u] = (i0 + u * 256 < n4) ? ld_nc_v4(s_src[q] + i0 + u * 256) : make_int4(0, 0, 0, 0);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          acc[u].x = __fadd_rn(acc[u].x, __int_as_float(raw[u].x));
-          acc[u].y = __fadd_rn(acc[u].y, __int_as_float(raw[u].y));
-          acc[u].z = __fadd_rn(acc[u].z, __int_as_float(raw[u].z));
-          acc[u].w = __fadd_rn(acc[u].w, __int_as_float(raw[u].w));
-        }
+        for (int u = 0; u < U; ++u) acc[u].add(raw[u]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (i0 + u * 256 < n4) dst[i0 + u * 256] = acc[u];
+        if (i0 + u * 256 < n4) dst[i0 + u * 256] = acc[u].pack();
     }
   }
 }
@@ -1489,10 +1524,11 @@ __global__ void __launch_bounds__(256)
 // its sources arrive one ring stage each.
 constexpr int kPullSub = 8 * 1024;
 constexpr int kPullRing = 8;   // 64 KB of dynamic smem per CTA: 3 CTAs per SM
-constexpr int kPullWarps = 4;  // 128 consumer threads x 4 float4 = one sub-chunk
+constexpr int kPullWarps = 4;  // 128 consumer threads x 4 vectors = one sub-chunk
+template <bool BF16>
 __global__ void __launch_bounds__(32 * (kPullWarps + 1))
     sprs_pull_kernel(const uint64_t* __restrict__ peer_bases, int rank, int64_t grad_off,
-                     int64_t slot_elems, const int32_t* __restrict__ jobs,
+                     int64_t slot_bytes, const int32_t* __restrict__ jobs,
                      const int32_t* __restrict__ srcs, int64_t chunk, int n_chunks, int n_units) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kPullRing], empty[kPullRing];
@@ -1504,7 +1540,6 @@ __global__ void __launch_bounds__(32 * (kPullWarps + 1))
     fence_barrier_init();
   }
   __syncthreads();
-  const int64_t slot_bytes = slot_elems * 4;
   const int warp = threadIdx.x / 32;
   if (warp == 0) {
     if (threadIdx.x != 0) return;
@@ -1542,32 +1577,26 @@ __global__ void __launch_bounds__(32 * (kPullWarps + 1))
     char* dst = reinterpret_cast<char*>(peer_bases[rank] + grad_off) + dst_slot * slot_bytes + begin;
     for (int64_t c = 0; c < bytes; c += kPullSub) {
       const int n16 = static_cast<int>(imin64(kPullSub, bytes - c) / 16);
-      float4 acc[4];
+      GradVec<BF16> acc[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < 4; ++u) acc[u].zero();
       for (int q = 0; q < src_count; ++q, ++it) {
         const uint32_t st = it % kPullRing;
         mbar_wait(&full[st], (it / kPullRing) & 1u);
-        const float4* buf = reinterpret_cast<const float4*>(ring + st * kPullSub);
+        const int4* buf = reinterpret_cast<const int4*>(ring + st * kPullSub);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = t + u * 32 * kPullWarps;
-          if (i < n16) {
-            const float4 v = buf[i];
-            acc[u].x = __fadd_rn(acc[u].x, v.x);
-            acc[u].y = __fadd_rn(acc[u].y, v.y);
-            acc[u].z = __fadd_rn(acc[u].z, v.z);
-            acc[u].w = __fadd_rn(acc[u].w, v.w);
-          }
+          if (i < n16) acc[u].add(buf[i]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
       }
-      float4* out = reinterpret_cast<float4*>(dst + c);
+      int4* out = reinterpret_cast<int4*>(dst + c);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = t + u * 32 * kPullWarps;
-        if (i < n16) out[i] = acc[u];
+        if (i < n16) out[i] = acc[u].pack();
       }
     }
   }
@@ -2128,12 +2157,13 @@ int fssdp_spag(const uint64_t* peer_bases, int32_t rank, int64_t param_off, int6
 }
 
 int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64_t stage_off,
-               int64_t slot_elems, const int32_t* jobs, int32_t n_jobs, const int32_t* srcs,
-               void* stream) {
-  if (slot_elems % 4 != 0) {
-    set_error("sprs: slot_elems must be a multiple of 4");
+               int64_t slot_elems, int32_t elem_bytes, const int32_t* jobs, int32_t n_jobs,
+               const int32_t* srcs, void* stream) {
+  if ((elem_bytes != 2 && elem_bytes != 4) || (slot_elems * elem_bytes) % 16 != 0) {
+    set_error("sprs: elem_bytes must be 2 (bf16) or 4 (fp32) and a slot whole 16-byte vectors");
     return kErrDimension;
   }
+  const int64_t slot_bytes = slot_elems * elem_bytes;
   if (n_jobs <= 0) return kOk;
   // CTA budget (FSSDP_SPRS_CTAS, default one per SM): SpRS runs beside the backward GEMMs
   // and a full 4-per-SM grid slows them more than it speeds the reduction (measured, N=4)
@@ -2141,28 +2171,35 @@ int fssdp_sprs(const uint64_t* peer_bases, int32_t rank, int64_t grad_off, int64
     const char* v = getenv("FSSDP_SPRS_CTAS");
     return v ? atoi(v) : num_sms();
   }();
-  const int64_t chunk = coll_chunk_bytes(slot_elems * 4 * n_jobs, num_sms());
-  const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
+  const int64_t chunk = coll_chunk_bytes(slot_bytes * n_jobs, num_sms());
+  const int n_chunks = static_cast<int>((slot_bytes + chunk - 1) / chunk);
   const int n_units = n_chunks * n_jobs;
   const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
   timing_begin(as_stream(stream));
-  sprs_kernel<<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, stage_off,
-                                                   slot_elems, jobs, srcs, chunk, n_chunks,
-                                                   n_units);
+  if (elem_bytes == 2)
+    sprs_kernel<true><<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off, stage_off,
+                                                           slot_bytes, jobs, srcs, chunk, n_chunks,
+                                                           n_units);
+  else
+    sprs_kernel<false><<<ctas, 256, 0, as_stream(stream)>>>(peer_bases, rank, grad_off,
+                                                            stage_off, slot_bytes, jobs, srcs,
+                                                            chunk, n_chunks, n_units);
   return launch_status();
 }
 
 int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
-                    int64_t slot_elems, const int32_t* jobs, int32_t n_jobs,
+                    int64_t slot_elems, int32_t elem_bytes, const int32_t* jobs, int32_t n_jobs,
                     const int32_t* pull_srcs, void* stream) {
-  if (slot_elems % 4 != 0) {
-    set_error("sprs_pull: slot_elems must be a multiple of 4");
+  if ((elem_bytes != 2 && elem_bytes != 4) || (slot_elems * elem_bytes) % 16 != 0) {
+    set_error("sprs_pull: elem_bytes must be 2 (bf16) or 4 (fp32) and a slot whole 16-byte "
+              "vectors");
     return kErrDimension;
   }
   if (n_jobs <= 0) return kOk;
+  const int64_t slot_bytes = slot_elems * elem_bytes;
   constexpr int kSmem = kPullRing * kPullSub;
-  if (ensure_dynamic_smem(reinterpret_cast<const void*>(sprs_pull_kernel), kSmem) !=
-      cudaSuccess) {
+  auto kern = elem_bytes == 2 ? sprs_pull_kernel<true> : sprs_pull_kernel<false>;
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), kSmem) != cudaSuccess) {
     set_error("sprs_pull: cannot reserve the TMA ring");
     return kErrCuda;
   }
@@ -2172,16 +2209,16 @@ int fssdp_sprs_pull(const uint64_t* peer_bases, int32_t rank, int64_t grad_off,
     const char* v = getenv("FSSDP_SPRS_PULL_CTAS");
     return v ? atoi(v) : 3 * num_sms();
   }();
-  int64_t chunk = slot_elems * 4 * n_jobs / (3 * static_cast<int64_t>(num_sms()));
+  int64_t chunk = slot_bytes * n_jobs / (3 * static_cast<int64_t>(num_sms()));
   chunk = (chunk + kPullSub - 1) / kPullSub * kPullSub;
   if (chunk < 4 * kPullSub) chunk = 4 * kPullSub;
   if (chunk > (1 << 20)) chunk = 1 << 20;
-  const int n_chunks = static_cast<int>((slot_elems * 4 + chunk - 1) / chunk);
+  const int n_chunks = static_cast<int>((slot_bytes + chunk - 1) / chunk);
   const int n_units = n_chunks * n_jobs;
   const int ctas = budget > 0 ? (budget < n_units ? budget : n_units) : n_units;
   timing_begin(as_stream(stream));
-  sprs_pull_kernel<<<ctas, 32 * (kPullWarps + 1), kSmem, as_stream(stream)>>>(
-      peer_bases, rank, grad_off, slot_elems, jobs, pull_srcs, chunk, n_chunks, n_units);
+  kern<<<ctas, 32 * (kPullWarps + 1), kSmem, as_stream(stream)>>>(
+      peer_bases, rank, grad_off, slot_bytes, jobs, pull_srcs, chunk, n_chunks, n_units);
   return launch_status();
 }
 

@@ -3,7 +3,8 @@
 //   adam_kernel           AdamW on an owner's shards: fp32 master / m / v in the symmetric
 //                         heap (they move with re-shards: params + 6x state = the 7x
 //                         expert_bytes the reference prices, engine.py:233, 444-453), bf16
-//                         working copy rewritten from the master.  HBM-bound: 30 B/param.
+//                         working copy rewritten from the master; fp32 or bf16 gradients.
+//                         HBM-bound: 30 B/param (fp32 grads), 28 (bf16).
 //   publish_epoch_kernel  an owner announces "my shards are final for forward #e"
 //   wait_epochs_kernel    a reader (the early SpAG's copy-engine stream) waits until every
 //                         owner announced forward #e before it pulls their shards
@@ -21,18 +22,25 @@ namespace {
 constexpr int kAdamThreads = 256;
 constexpr int kFlagWorld = 32;  // flag pad row width (kMaxWorld of moe_kernels.cu)
 
+template <bool BF16G>
 __global__ void __launch_bounds__(kAdamThreads)
     adam_kernel(__nv_bfloat16* __restrict__ params, float* __restrict__ master,
-                float* __restrict__ m1, float* __restrict__ m2, const float* __restrict__ grads,
+                float* __restrict__ m1, float* __restrict__ m2, const void* __restrict__ grads,
                 int64_t n4, float lr, float beta1, float beta2, float eps, float weight_decay,
                 float bc1, float bc2) {
-  const float4* g4 = reinterpret_cast<const float4*>(grads);
   float4* w4 = reinterpret_cast<float4*>(master);
   float4* a4 = reinterpret_cast<float4*>(m1);
   float4* b4 = reinterpret_cast<float4*>(m2);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float4 g = g4[i];
+    float4 g;
+    if (BF16G) {  // 4 bf16 gradients: the high halves of their fp32 bit patterns
+      const uint2 raw = reinterpret_cast<const uint2*>(grads)[i];
+      g = make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xffff0000u),
+                      __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xffff0000u));
+    } else {
+      g = reinterpret_cast<const float4*>(grads)[i];
+    }
     float4 w = w4[i], a = a4[i], b = b4[i];
     float gv[4] = {g.x, g.y, g.z, g.w}, wv[4] = {w.x, w.y, w.z, w.w};
     float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
@@ -102,8 +110,8 @@ using namespace fssdp;
 extern "C" {
 
 int fssdp_adam_step(void* params_bf16, float* master, float* exp_avg, float* exp_avg_sq,
-                    const float* grads, int64_t n, float lr, float beta1, float beta2, float eps,
-                    float weight_decay, int64_t step, void* stream) {
+                    const void* grads, int32_t grads_bf16, int64_t n, float lr, float beta1,
+                    float beta2, float eps, float weight_decay, int64_t step, void* stream) {
   if (n < 0 || n % 4 != 0 || step < 1) {
     set_error("adam_step: n must be a non-negative multiple of 4 and step >= 1");
     return kErrDimension;
@@ -117,7 +125,8 @@ int fssdp_adam_step(void* params_bf16, float* master, float* exp_avg, float* exp
   if (blocks > cap) blocks = cap;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   timing_begin(s);
-  adam_kernel<<<static_cast<unsigned>(blocks), kAdamThreads, 0, s>>>(
+  auto kern = grads_bf16 ? adam_kernel<true> : adam_kernel<false>;
+  kern<<<static_cast<unsigned>(blocks), kAdamThreads, 0, s>>>(
       static_cast<__nv_bfloat16*>(params_bf16), master, exp_avg, exp_avg_sq, grads, n4, lr, beta1,
       beta2, eps, weight_decay, bc1, bc2);
   timing_end();

@@ -61,6 +61,11 @@ class LayerGeometry:
     owned_base: int = -1
     replica_base: int = -1
     param_slots_total: int = 0  # slots of the model-level region (its TMA extent)
+    # weight-gradient buffers (grads, SpRS staging): "bf16" — the reference's memory and
+    # traffic model (grad_bytes = param bytes, engine.py:223; SpRS priced at expert_bytes,
+    # engine.py:536-538): the wgrad GEMMs accumulate in fp32 (TMEM) and round once on store,
+    # the SpRS sums the holders' partials in fp32 and rounds once — or "fp32"
+    grad_dtype: str = "bf16"
 
     @property
     def n_mats(self) -> int:  # expert matrices per slot
@@ -80,8 +85,12 @@ class LayerGeometry:
         return 2 * self.n_mats * self.d_model * self.d_ff
 
     @property
-    def slot_grad_elems(self) -> int:       # the same matrices in fp32
+    def slot_grad_elems(self) -> int:       # the same matrices (grad_dtype elements)
         return self.n_mats * self.d_model * self.d_ff
+
+    @property
+    def grad_elem_bytes(self) -> int:
+        return 2 if self.grad_dtype == "bf16" else 4
 
     @property
     def expert_bytes(self) -> int:
@@ -118,6 +127,8 @@ class LayerGeometry:
     def validate(self) -> None:
         if self.d_model % 256 or self.d_ff % 128:
             raise DimensionError("d_model must be a multiple of 256 and d_ff of 128 (GEMM tiles)")
+        if self.grad_dtype not in ("bf16", "fp32"):
+            raise DimensionError(f"grad_dtype must be 'bf16' or 'fp32', not {self.grad_dtype!r}")
         if self.activation not in ("gelu", "swiglu"):
             raise DimensionError(f"unknown expert activation {self.activation!r}")
         if not 1 <= self.top_k <= min(8, self.num_experts) or self.num_experts > 64:
@@ -130,13 +141,14 @@ class LayerGeometry:
         # gradients: a replica's partial goes straight to its owner's staging slot (the
         # wgrad epilogue's c_dest stores), so the split layout keeps owned slots only
         grad_slots = self.owned_cap if self.split and self.world > 1 else self.slots
-        layout.add(prefix + "grads", grad_slots * self.slot_grad_elems * 4)
+        layout.add(prefix + "grads", grad_slots * self.slot_grad_elems * self.grad_elem_bytes)
         layout.add(prefix + "xrecv", R * d * 2)
         layout.add(prefix + "y", R * d * 2)
         layout.add(prefix + "dyrecv", R * d * 2)
         layout.add(prefix + "dxe", R * d * 2)
         layout.add(prefix + "counts", (self.world * self.num_experts * 4 + 15) // 16 * 16)
-        layout.add(prefix + "stage", max(1, self.stage_slots) * self.slot_grad_elems * 4)
+        layout.add(prefix + "stage",
+                   max(1, self.stage_slots) * self.slot_grad_elems * self.grad_elem_bytes)
         # re-shard staging: the old owned shards, pulled by their new owners
         layout.add(prefix + "reshard", (self.slots if self.reshard else 1) * self.slot_param_bytes)
         if self.optimizer:  # fp32 master / exp_avg / exp_avg_sq of the owned slots (+ staging)
@@ -250,7 +262,8 @@ class FssdpMoE:
             self.replicas = None
         grad_slots = geom.owned_cap if geom.split and self.world > 1 else geom.slots
         self.grads = heap.tensor(self.off["grads"], (grad_slots, geom.n_mats * d * f),
-                                 torch.float32)
+                                 torch.bfloat16 if geom.grad_dtype == "bf16" else torch.float32)
+        self.epi_wgrad = ops.EPI_BF16 if geom.grad_dtype == "bf16" else ops.EPI_F32
         self.xrecv = heap.tensor(self.off["xrecv"], (R, d), torch.bfloat16)
         self.y_e = heap.tensor(self.off["y"], (R, d), torch.bfloat16)
         self.dyrecv = heap.tensor(self.off["dyrecv"], (R, d), torch.bfloat16)
@@ -272,7 +285,7 @@ class FssdpMoE:
         stage_elems = max(1, geom.stage_slots) * geom.slot_grad_elems
         self.dest_maps = {}
         for name, ldc in (("wgrad1", d), ("wgrad2", f)):
-            blob = b"".join(ops.epilogue_tmap(ops.EPI_F32, base + self.off["stage"], ldc,
+            blob = b"".join(ops.epilogue_tmap(self.epi_wgrad, base + self.off["stage"], ldc,
                                               stage_elems // ldc) for base in group.bases)
             self.dest_maps[name] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.dev)
         # 2-D TMA views of the parameter region (nm = matrices per slot, n1 = (nm-1) f)
@@ -451,8 +464,8 @@ class FssdpMoE:
         return self._slot_mats(self.params, e)
 
     def expert_grad(self, e: int):
-        """(dW1, dW2) [SwiGLU: (dW1, dW3, dW2)] fp32 of an owned expert after backward
-        (SpRS-reduced)."""
+        """(dW1, dW2) [SwiGLU: (dW1, dW3, dW2)] of an owned expert after backward
+        (SpRS-reduced; grad_dtype)."""
         return self._slot_mats(self.grads, e)
 
     # ------------------------------------------------------------ helpers
@@ -1053,8 +1066,9 @@ class FssdpMoE:
         self._gemm("dgrad2", self.dyrecv, False, self.w2_view, True, self.da, n1, self.epi_dgrad2,
                    aux=self.gprime)
         grads2d = self.grads.view(-1)
-        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32, part="shared")
-        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32,
+        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, self.epi_wgrad,
+                   part="shared")
+        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, self.epi_wgrad,
                    part="shared")
 
     def phase_bwd_rest(self) -> None:
@@ -1069,8 +1083,10 @@ class FssdpMoE:
     def phase_wgrad_rest(self) -> None:
         f, d = self.g.d_ff, self.g.d_model
         grads2d = self.grads.view(-1)
-        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, ops.EPI_F32, part="rest")
-        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, ops.EPI_F32, part="rest")
+        self._gemm("wgrad1", self.da, True, self.xrecv, True, grads2d, d, self.epi_wgrad,
+                   part="rest")
+        self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, self.epi_wgrad,
+                   part="rest")
 
     def phase_combine_dx(self, dx: torch.Tensor | None = None) -> torch.Tensor:
         if dx is None:
@@ -1093,7 +1109,8 @@ class FssdpMoE:
             return
         self._timed("sprs", lambda: N.call(
             "fssdp_sprs", self._pb(), self.rank, self.off["grads"], self.off["stage"],
-            self.g.slot_grad_elems, self._tab("sprs_jobs"), n, self._tab("sprs_srcs"),
+            self.g.slot_grad_elems, self.g.grad_elem_bytes, self._tab("sprs_jobs"), n,
+            self._tab("sprs_srcs"),
             self._stream()))
 
     # ------------------------------------------------------------ one rank per process
@@ -1255,15 +1272,16 @@ def create_layer(d_model: int, d_ff: int, num_experts: int, top_k: int, max_toke
                  peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
                  per_token_expert_time: float | None = None, pg=None,
                  activation: str = "gelu", record_trace: bool = False,
-                 optimizer: bool = False) -> FssdpMoE:
+                 optimizer: bool = False, grad_dtype: str = "bf16") -> FssdpMoE:
     """One rank per process: heap layout, IPC peer group (world > 1), planner, layer.
-    optimizer=True reserves the owned shards' AdamW state in the heap (optim.FssdpAdam)."""
+    optimizer=True reserves the owned shards' AdamW state in the heap (optim.FssdpAdam);
+    grad_dtype "bf16" / "fp32" weight-gradient buffers (LayerGeometry.grad_dtype)."""
     (layer,) = create_model(1, d_model, d_ff, num_experts, top_k, max_tokens, policy, rank=rank,
                             world=world, device=device, seed=seed, peer_bw=peer_bw,
                             attn_fwd_time=attn_fwd_time,
                             per_token_expert_time=per_token_expert_time, pg=pg,
                             activation=activation, record_trace=record_trace,
-                            optimizer=optimizer)
+                            optimizer=optimizer, grad_dtype=grad_dtype)
     return layer
 
 
@@ -1278,7 +1296,7 @@ def replica_slots(planner: FssdpPlanner) -> int:
 
 def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
                      max_tokens: int, m: int, activation: str = "gelu",
-                     optimizer: bool = False) -> list:
+                     optimizer: bool = False, grad_dtype: str = "bf16") -> list:
     """Per-layer geometry under the planner's current ShardPlan (even or heterogeneous):
     slot capacity = the most experts any rank owns in that layer + m replica slots.  With
     re-sharding on, a layer may later own up to a device's whole share across layers
@@ -1292,7 +1310,7 @@ def layer_geometries(planner: FssdpPlanner, d_model: int, d_ff: int, top_k: int,
             owned_max = min(E, max(owned_max, -(-(E * len(planner.shards.per_layer)) // D)))
         geoms.append(LayerGeometry(d_model, d_ff, E, top_k, max_tokens, D,
                                    min(E, owned_max + max(0, m)), activation, owned_max, reshard,
-                                   optimizer))
+                                   optimizer, grad_dtype=grad_dtype))
     return geoms
 
 
@@ -1301,9 +1319,10 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
                  seed: int = 0, peer_bw: float = 770e9, attn_fwd_time: float = 1e-3,
                  per_token_expert_time: float | None = None, pg=None,
                  activation: str = "gelu", load_profile=None, record_trace: bool = False,
-                 optimizer: bool = False) -> list:
+                 optimizer: bool = False, grad_dtype: str = "bf16") -> list:
     """num_layers FSSDP MoE layers sharing one planner (one iteration = every layer's
     forward, then backward in reverse, then planner.finish()) and one symmetric heap.
+    grad_dtype: "bf16" (default; the reference's grad_bytes = param bytes) or "fp32".
     load_profile [L, E] (expected per-expert loads): the initial ShardPlan comes from
     heterogeneous_sharding (Alg. 2, planner.py:302-385) instead of the even split."""
     from .engine import ModelConfig
@@ -1323,7 +1342,7 @@ def create_model(num_layers: int, d_model: int, d_ff: int, num_experts: int, top
         planner.shards = heterogeneous_sharding(
             GlobalLoadProfile(np.asarray(load_profile, dtype=np.float64)), planner.t, topo)
     geoms = layer_geometries(planner, d_model, d_ff, top_k, max_tokens, replica_slots(planner),
-                             activation, optimizer)
+                             activation, optimizer, grad_dtype)
     layout = HeapLayout()
     # owned slots per layer; replica slots per layer (retain) or one shared set (remat)
     geoms = model_regions(layout, geoms, policy.rematerialize)

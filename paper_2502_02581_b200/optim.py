@@ -47,7 +47,8 @@ class FssdpAdam:
         b1, b2 = self.betas
         N.call("fssdp_adam_step", C.c_void_p(0 if params is None else params.data_ptr()),
                C.c_void_p(master.data_ptr()), C.c_void_p(m.data_ptr()),
-               C.c_void_p(v.data_ptr()), C.c_void_p(grads.data_ptr()), n, self.lr, b1, b2,
+               C.c_void_p(v.data_ptr()), C.c_void_p(grads.data_ptr()),
+               int(grads.dtype == torch.bfloat16), n, self.lr, b1, b2,
                self.eps, self.weight_decay, self.step_count, stream)
 
     @torch.no_grad()

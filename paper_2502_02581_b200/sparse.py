@@ -6,8 +6,8 @@ The reference's contract is a pair of ChunkPlacements:
 * SpAG(pre, post): `pre` is a partition, pre ⊆ post (validate_spag_pair,
   placement.py:200-204); every (chunk, device) in post − pre receives the owner's copy.
 * SpRS(pre, post): `post` is a partition, post ⊆ pre (validate_sprs_pair,
-  placement.py:207-211); every owner in post ends with the fp32 sum of all pre holders'
-  partials, in ascending device order.
+  placement.py:207-211); every owner in post ends with the sum of all pre holders'
+  partials, in ascending device order (fp32 chunks, or bf16 chunks summed in fp32).
 
 Here they move real bytes: chunks live in a `ChunkBuffer` — `slots` chunk-sized slots at
 the same offset of every rank's symmetric heap (comm.py) — and the transfers are the
@@ -159,20 +159,23 @@ def sparse_all_gather(pre: ChunkPlacement, post: ChunkPlacement, buf: ChunkBuffe
 
 
 def sparse_reduce_scatter(pre: ChunkPlacement, post: ChunkPlacement, buf: ChunkBuffer, *,
-                          stream=None, fence: bool = True) -> SparsityReport:
+                          stream=None, fence: bool = True,
+                          dtype: torch.dtype = torch.float32) -> SparsityReport:
     """SpRS(pre → post) on this rank: for every chunk this rank owns in post, its slot
-    becomes the fp32 sum of every pre holder's partial (ascending device order; the
-    owner's own partial included).  Chunks are fp32 (chunk_bytes / 4 elements).
+    becomes the sum of every pre holder's partial (ascending device order; the owner's own
+    partial included).  dtype: the chunks' elements — float32, or bfloat16 (summed in fp32,
+    rounded once: the layer's bf16 gradients).
 
     Raises InvalidPairError when (pre, post) violates the SpRS contract.  fence: barriers
     before (every holder's partial complete) and after (holders may reuse their slots).
-    Returns the reference's SparsityReport (sprs_traffic, fp32 bytes of this buffer)."""
+    Returns the reference's SparsityReport (sprs_traffic, bytes of this buffer)."""
     sprs_traffic(pre, post, 1)  # the pair contract first (costmodel.py:120-121)
     _dims(pre, post, buf)
     report = sprs_traffic(pre, post, buf.chunk_bytes)[1]
     _slots_fit(pre, post, buf, post)
-    if buf.chunk_bytes % 16:
-        raise DimensionError("fp32 chunks must be whole 16-byte vectors")
+    if dtype not in (torch.float32, torch.bfloat16):
+        raise DimensionError(f"SpRS chunks are float32 or bfloat16, not {dtype}")
+    esize = 4 if dtype == torch.float32 else 2
     g = buf.group
     st = _stream(stream, g.device)
     s = C.c_void_p(st.cuda_stream)
@@ -182,7 +185,7 @@ def sparse_reduce_scatter(pre: ChunkPlacement, post: ChunkPlacement, buf: ChunkB
     if len(jobs):
         tj, ts = _upload(jobs, st), _upload(srcs, st)
         N.call("fssdp_sprs_pull", C.c_void_p(g.peer_bases.data_ptr()), g.rank, buf.offset,
-               buf.chunk_bytes // 4, C.c_void_p(tj.data_ptr()), len(jobs),
+               buf.chunk_bytes // esize, esize, C.c_void_p(tj.data_ptr()), len(jobs),
                C.c_void_p(ts.data_ptr()), s)
     if fence:
         _barrier(g, s)

@@ -75,17 +75,23 @@ def main():
             torch.cuda.synchronize()
             same_y = torch.equal(torch.cat(ys), y1)
             same_dx = torch.equal(torch.cat(dxs), dx1)
-            worst = 0.0
+            worst, grads_ok = 0.0, True
             for e in range(E):
                 g1, g2 = single.expert_grad(e)
-                ref = torch.cat([g1.reshape(-1), g2.reshape(-1)])
-                err = (grads[e] - ref).abs().max().item() / (ref.abs().max().item() + 1e-12)
+                ref = torch.cat([g1.reshape(-1), g2.reshape(-1)]).float()
+                diff = (grads[e] - ref).abs()
+                err = diff.max().item() / (ref.abs().max().item() + 1e-12)
                 worst = max(worst, err)
+                if g1.dtype == torch.bfloat16:  # partials and sum rounded (tests/_torch_ref)
+                    bound = 2.0 ** -6 * ref.abs() + 2.0 ** -8 * ref.abs().max()
+                    grads_ok = grads_ok and bool((diff <= bound).all())
+                else:
+                    grads_ok = grads_ok and err < 1e-4
             dwg_ok = torch.allclose(layer.dwg, single.dwg, rtol=1e-4, atol=1e-6)
             print(f"iter {it}: y bit-exact {same_y}, dx bit-exact {same_dx}, worst grad rel err "
                   f"{worst:.2e}, dWg ok {dwg_ok}, replicas {len(layer.decision.target.entries) - E}",
                   flush=True)
-            ok = ok and same_y and same_dx and worst < 1e-4 and dwg_ok
+            ok = ok and same_y and same_dx and grads_ok and dwg_ok
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, src=0)
     if rank == 0:

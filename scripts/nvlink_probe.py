@@ -141,7 +141,7 @@ def main():
     for d in range(n):
         bufs[d][:S].view(torch.float32).fill_(1.0)
     rec("sprs_pull_all", (n - 1) * S, timed(
-        lambda: N.call("fssdp_sprs_pull", C.c_void_p(pb.data_ptr()), 0, 0, S // 4,
+        lambda: N.call("fssdp_sprs_pull", C.c_void_p(pb.data_ptr()), 0, 0, S // 4, 4,
                        C.c_void_p(jobs.data_ptr()), 1, C.c_void_p(srcs.data_ptr()), sp),
         args.iters))
 

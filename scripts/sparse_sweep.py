@@ -6,8 +6,9 @@ E = N experts, even single-owner partition; the post-placement adds expert e to 
 (e+1 .. e+r-1) mod N (balanced ring: every GPU pulls (r-1)·S in SpAG and its owner pulls
 (r-1)·S_grad in SpRS).  A "hot" variant materializes expert 0 on r devices only.  Times are
 CUDA events around the kernel, max over ranks; GB/s = per-GPU inbound bytes / time
-(SpAG) and the reference's bottleneck bytes / time (costmodel.py:75-84).  SpRS moves fp32
-gradients (S_grad = 2·S) the way the layer does: the shared-prefix wgrad launches push each
+(SpAG) and the reference's bottleneck bytes / time (costmodel.py:75-84).  SpRS moves the
+layer's gradients (--grad-dtype bf16: S_grad = S, the reference's expert_bytes pricing;
+fp32: S_grad = 2·S) the way the layer does: the shared-prefix wgrad launches push each
 holder's partial into its owner's staging slot through the epilogue's TMA stores (run
 here with K = 0, i.e. the store path alone), then a barrier and the owner's local
 reduction.  "sprs_pull" times the pull transport alone: the partials already sit in the
@@ -44,7 +45,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--grad-dtype", default="bf16", choices=["bf16", "fp32"])
     args = ap.parse_args()
+    gbytes = 2 if args.grad_dtype == "bf16" else 4
+    gdt = torch.bfloat16 if gbytes == 2 else torch.float32
+    epi = ops.EPI_BF16 if gbytes == 2 else ops.EPI_F32
+    wire = gbytes / 2  # gradient bytes per parameter byte
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -64,12 +70,12 @@ def main():
     bar_epoch = [0]
     heap = group.local
     heap.tensor(poff, (slots * smax // 2,), torch.bfloat16).normal_()
-    heap.tensor(goff, (slots * smax // 2,), torch.float32).normal_()
+    heap.tensor(goff, (slots * smax // 2,), gdt).normal_()
     topo = F.ClusterTopology.for_nvswitch(world)
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)
     flags_off = layout.offset("flags")
-    grads = heap.tensor(goff, (slots * smax // 2,), torch.float32)
+    grads = heap.tensor(goff, (slots * smax // 2,), gdt)
 
     def push(tab, blob, maps, d_, f_):
         """The shared-prefix wgrad launches with K = 0: replica partials (zeros) stored
@@ -80,7 +86,7 @@ def main():
                 continue
             a = dummy[:, :a_w]
             b = dummy[:, :b_w]
-            N.call("fssdp_grouped_gemm", 1, 1, ops.EPI_F32, ops._ptr(a), a_w, 64, ops._ptr(b),
+            N.call("fssdp_grouped_gemm", 1, 1, epi, ops._ptr(a), a_w, 64, ops._ptr(b),
                    b_w, 64, C.c_void_p(blob.data_ptr() + tab.offsets[name]), n_sh,
                    tab.gemm[name][1], tiles, ops._ptr(grads), None, None, ops._ptr(maps[name]),
                    ldc, grads.numel() // ldc, 2, None, sp)
@@ -103,7 +109,7 @@ def main():
                 blob = torch.from_numpy(tab.blob[:tab.nbytes].copy()).to(dev)
                 maps = {}
                 for name, ldc in (("wgrad1", d_), ("wgrad2", f_)):
-                    raw = b"".join(ops.epilogue_tmap(ops.EPI_F32, b + soff, ldc,
+                    raw = b"".join(ops.epilogue_tmap(epi, b + soff, ldc,
                                                      (world - 1) * 2 * d_ * f_ // ldc)
                                    for b in group.bases)
                     maps[name] = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
@@ -127,12 +133,13 @@ def main():
                             N.call("fssdp_barrier", pb, flags_off, rank, world, 0,
                                    C.c_uint32(bar_epoch[0]), sp)
                             if tab.n_sprs_jobs:
-                                N.call("fssdp_sprs", pb, rank, goff, soff, S // 2, jobs_t,
+                                N.call("fssdp_sprs", pb, rank, goff, soff, S // 2, gbytes,
+                                       jobs_t,
                                        tab.n_sprs_jobs, srcs_t, sp)
                         if kind == "sprs_pull" and tab.n_sprs_jobs:
                             # partials already in the holders' own grads slots (a wgrad
                             # without c_dest writes them there): the owners' pull + sum alone
-                            N.call("fssdp_sprs_pull", pb, rank, goff, S // 2, jobs_t,
+                            N.call("fssdp_sprs_pull", pb, rank, goff, S // 2, gbytes, jobs_t,
                                    tab.n_sprs_jobs, pull_t, sp)
                         e.record()
                         torch.cuda.synchronize()
@@ -153,18 +160,19 @@ def main():
                         "spag_bottleneck_bytes": rep.bottleneck_bytes,
                         "spag_gbs_bottleneck": rep.bottleneck_bytes / (res["spag"] * 1e-3) / 1e9,
                         "spag_gbs_inbound_max": max_in / (res["spag"] * 1e-3) / 1e9,
-                        "sprs_gbs_bottleneck_fp32": 2 * rep.bottleneck_bytes / (res["sprs"] * 1e-3) / 1e9,
+                        "grad_dtype": args.grad_dtype,
+                        "sprs_gbs_bottleneck": wire * rep.bottleneck_bytes / (res["sprs"] * 1e-3) / 1e9,
                         "sprs_path": "wgrad epilogue TMA-store push (K=0) + barrier + local reduce",
                         "sprs_pull_ms": res["sprs_pull"],
-                        "sprs_pull_gbs_bottleneck_fp32":
-                            2 * rep.bottleneck_bytes / (res["sprs_pull"] * 1e-3) / 1e9,
-                        "sprs_pull_gbs_inbound_max_fp32": 2 * max_in / (res["sprs_pull"] * 1e-3) / 1e9,
+                        "sprs_pull_gbs_bottleneck":
+                            wire * rep.bottleneck_bytes / (res["sprs_pull"] * 1e-3) / 1e9,
+                        "sprs_pull_gbs_inbound_max": wire * max_in / (res["sprs_pull"] * 1e-3) / 1e9,
                         "nvlink_peak_gbs": NVLINK_PEAK,
                         "spag_frac_of_peak": rep.bottleneck_bytes / (res["spag"] * 1e-3) / 1e9
                                              / NVLINK_PEAK,
                         # the reference's bottleneck bytes (costmodel.py:75-84; sprs_traffic is
-                        # spag_traffic transposed), fp32 wire
-                        "sprs_pull_frac_of_peak": 2 * rep.bottleneck_bytes
+                        # spag_traffic transposed) x gradient bytes per parameter byte
+                        "sprs_pull_frac_of_peak": wire * rep.bottleneck_bytes
                                                   / (res["sprs_pull"] * 1e-3) / 1e9 / NVLINK_PEAK,
                     }
                     print("SWEEP " + json.dumps(line), flush=True)

@@ -142,3 +142,19 @@ def rel_err(out: torch.Tensor, ref: torch.Tensor) -> float:
     den = ref.abs().max().item()
     num = (out - ref).abs().max().item()
     return num / den if den > 0 else num
+
+
+def grad_excess(gm: torch.Tensor, gs: torch.Tensor) -> float:
+    """A sharded run's SpRS-reduced weight gradient gm against the single-rank gs: the
+    largest excess over the bound (<= 0 passes).  fp32 gradients: 1e-4·max|gs| (summation
+    order only).  bf16 gradients: each holder's partial and the reduced sum are rounded to
+    bf16 (one ulp = 2^-7 relative at worst), so 2 ulps of the element plus 2^-8·max|gs| for
+    partials that cancel."""
+    bf = gs.dtype == torch.bfloat16
+    gm, gs = gm.double(), gs.double()
+    peak = gs.abs().max().item()
+    if bf:
+        bound = 2.0 ** -6 * gs.abs() + 2.0 ** -8 * peak
+    else:
+        bound = torch.full_like(gs, 1e-4 * peak + 1e-6)
+    return ((gm - gs).abs() - bound).max().item()

@@ -15,6 +15,7 @@ import pytest
 import torch
 
 import paper_2502_02581_b200 as F
+from _torch_ref import grad_excess
 from oracle import tensor_oracle as TO
 from paper_2502_02581_b200.comm import HeapLayout, emulated_group
 from paper_2502_02581_b200.layer import (FssdpMoE, layer_geometries, run_lockstep_backward,
@@ -92,8 +93,7 @@ def compare(world, L, E, d, f, k, Tr, policy, activation, profile=None, bias=Non
             for e in range(E):  # owners hold the SpRS-reduced gradients
                 o = dec.base.owner(e)
                 for gm, gs in zip(multi[li][o].expert_grad(e), single[li][0].expert_grad(e)):
-                    gm, gs = gm.double(), gs.double()
-                    assert (gm - gs).abs().max() <= 1e-4 * gs.abs().max() + 1e-6
+                    assert grad_excess(gm, gs) <= 0, f"layer {li} expert {e} grad (it {it})"
     if oracle:  # the single-rank run of the first layer against the numpy restatement
         ly = single[0][0]
         T = world * Tr

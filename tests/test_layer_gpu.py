@@ -15,6 +15,7 @@ import pytest
 import torch
 
 import paper_2502_02581_b200 as F
+from _torch_ref import grad_excess
 from oracle import tensor_oracle as TO
 from paper_2502_02581_b200.comm import HeapLayout, emulated_group
 from paper_2502_02581_b200.layer import (FssdpMoE, LayerGeometry, default_slots,
@@ -23,9 +24,10 @@ from paper_2502_02581_b200.layer import (FssdpMoE, LayerGeometry, default_slots,
 pytestmark = pytest.mark.gpu
 
 
-def build(world, E, d, f, k, T, policy, seed=0, bias=None, activation="gelu"):
+def build(world, E, d, f, k, T, policy, seed=0, bias=None, activation="gelu", grad_dtype="bf16"):
     m = policy.capacity_override if policy.capacity_override is not None else E
-    geom = LayerGeometry(d, f, E, k, T, world, default_slots(E, world, m), activation)
+    geom = LayerGeometry(d, f, E, k, T, world, default_slots(E, world, m), activation,
+                         grad_dtype=grad_dtype)
     layout = HeapLayout()
     geom.add_regions(layout, "L0.")
     groups = emulated_group(layout, world)
@@ -58,14 +60,17 @@ def zipf_bias(E, s=1.2, seed=0):
     return torch.tensor(np.log(p / p.sum()), dtype=torch.float32, device="cuda")
 
 
-@pytest.mark.parametrize("f,activation", [(1024, "gelu"), (384, "gelu"), (384, "swiglu"),
-                                          (512, "swiglu")])
-def test_single_rank_matches_oracle(f, activation):
+@pytest.mark.parametrize("f,activation,grad_dtype", [
+    (1024, "gelu", "bf16"), (1024, "gelu", "fp32"), (384, "gelu", "bf16"), (384, "swiglu", "bf16"),
+    (512, "swiglu", "fp32")])
+def test_single_rank_matches_oracle(f, activation, grad_dtype):
     """GeLU and SwiGLU experts; d_ff = 384 exercises 128-wide N tiles (and, for GeLU, the
-    single-CTA wgrad1: d_ff / 128 is odd)."""
+    single-CTA wgrad1: d_ff / 128 is odd); bf16 and fp32 weight gradients."""
     E, d, k, T = 8, 256, 2, 1000
     pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2)
-    (ly,) = build(1, E, d, f, k, T, pol, seed=3, bias=zipf_bias(E), activation=activation)
+    (ly,) = build(1, E, d, f, k, T, pol, seed=3, bias=zipf_bias(E), activation=activation,
+                  grad_dtype=grad_dtype)
+    assert ly.grads.dtype == (torch.bfloat16 if grad_dtype == "bf16" else torch.float32)
     g = torch.Generator(device="cuda").manual_seed(5)
     x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
     dy = (torch.randn(T, d, device="cuda", generator=g) * 0.1).bfloat16()
@@ -101,25 +106,28 @@ def test_single_rank_matches_oracle(f, activation):
         assert not xr[a:b].any()
 
 
-@pytest.mark.parametrize("world,E,policy_kw,f,activation", [
-    (4, 8, dict(overlap_override=8, capacity_override=2), 512, "gelu"),
-    (2, 16, dict(overlap_override=4, capacity_override=3, rematerialize=True), 512, "gelu"),
-    (8, 16, dict(overlap_override=6, capacity_override=2), 512, "gelu"),
-    (4, 8, dict(kind=F.PolicyKind.EP), 512, "gelu"),
-    (4, 8, dict(overlap_override=8, capacity_override=2, rematerialize=True), 384, "swiglu"),
-    (8, 16, dict(overlap_override=6, capacity_override=2), 384, "gelu"),
+@pytest.mark.parametrize("world,E,policy_kw,f,activation,grad_dtype", [
+    (4, 8, dict(overlap_override=8, capacity_override=2), 512, "gelu", "bf16"),
+    (4, 8, dict(overlap_override=8, capacity_override=2), 512, "gelu", "fp32"),
+    (2, 16, dict(overlap_override=4, capacity_override=3, rematerialize=True), 512, "gelu", "bf16"),
+    (8, 16, dict(overlap_override=6, capacity_override=2), 512, "gelu", "bf16"),
+    (4, 8, dict(kind=F.PolicyKind.EP), 512, "gelu", "bf16"),
+    (4, 8, dict(overlap_override=8, capacity_override=2, rematerialize=True), 384, "swiglu",
+     "bf16"),
+    (8, 16, dict(overlap_override=6, capacity_override=2), 384, "gelu", "fp32"),
 ])
-def test_multi_rank_equals_single_rank(world, E, policy_kw, f, activation):
+def test_multi_rank_equals_single_rank(world, E, policy_kw, f, activation, grad_dtype):
     """FSSDP over N emulated ranks == the same tokens on one rank (y, dx bit-exact;
-    SpRS-reduced owner grads within fp32 tolerance), over 3 iterations so history-driven
-    adoption and calibration both act."""
+    SpRS-reduced owner grads within the gradient dtype's tolerance: grad_excess), over 3
+    iterations so history-driven adoption and calibration both act."""
     d, k, Tr = 256, 2, 384
     kind = policy_kw.pop("kind", F.PolicyKind.FSSDP)
     pol = F.Policy(kind, **policy_kw)
     bias = zipf_bias(E, 1.3, seed=world)
-    multi = build(world, E, d, f, k, Tr, pol, seed=7, bias=bias, activation=activation)
+    multi = build(world, E, d, f, k, Tr, pol, seed=7, bias=bias, activation=activation,
+                  grad_dtype=grad_dtype)
     single = build(1, E, d, f, k, Tr * world, F.Policy(F.PolicyKind.EP), seed=7, bias=bias,
-                   activation=activation)[0]
+                   activation=activation, grad_dtype=grad_dtype)[0]
     g = torch.Generator(device="cuda").manual_seed(11)
     replicas_seen = prefetched = 0
     for it in range(3):
@@ -148,7 +156,7 @@ def test_multi_rank_equals_single_rank(world, E, policy_kw, f, activation):
         for e in range(E):
             owner = dec.base.owner(e)
             for j, (gm, gs) in enumerate(zip(multi[owner].expert_grad(e), single.expert_grad(e))):
-                close(f32(gm), f32(gs), rel=1e-4, abs_=1e-6, what=f"grad{j}[{e}] it{it}")
+                assert grad_excess(gm, gs) <= 0, f"grad{j}[{e}] it{it}"
         dwg = sum(ly.dwg.double() for ly in multi)
         close(dwg.cpu().numpy(), single.dwg.double().cpu().numpy(), rel=1e-4, abs_=1e-6,
               what="dWg")

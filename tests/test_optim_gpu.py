@@ -19,7 +19,8 @@ from paper_2502_02581_b200.layer import (FssdpMoE, layer_geometries, run_lockste
 pytestmark = pytest.mark.gpu
 
 
-def test_adam_kernel_matches_torch_adamw():
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])
+def test_adam_kernel_matches_torch_adamw(gdt):
     torch.manual_seed(0)
     n = 1 << 20
     master = torch.randn(n, device="cuda")
@@ -29,15 +30,17 @@ def test_adam_kernel_matches_torch_adamw():
     lr, b1, b2, eps, wd, step = 3e-3, 0.9, 0.95, 1e-8, 0.1, 7
     refs = (master.clone(), m.clone(), v.clone())
     for s in range(step, step + 3):
-        g = torch.randn(n, device="cuda")
+        g = torch.randn(n, device="cuda").to(gdt)
         rw, rm, rv = refs
-        rm.mul_(b1).add_((1 - b1) * g)
-        rv.mul_(b2).add_((1 - b2) * g * g)
+        g32 = g.float()
+        rm.mul_(b1).add_((1 - b1) * g32)
+        rv.mul_(b2).add_((1 - b2) * g32 * g32)
         bc1, bc2 = 1 - b1 ** s, 1 - b2 ** s
         rw.sub_(lr * wd * rw)
         rw.sub_(lr * (rm / bc1) / ((rv / bc2).sqrt() + eps))
         N.call("fssdp_adam_step", C.c_void_p(params.data_ptr()), C.c_void_p(master.data_ptr()),
-               C.c_void_p(m.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(g.data_ptr()), n,
+               C.c_void_p(m.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(g.data_ptr()),
+               int(gdt == torch.bfloat16), n,
                lr, b1, b2, eps, wd, s, C.c_void_p(torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     for name, got, ref in (("master", master, refs[0]), ("m", m, refs[1]), ("v", v, refs[2])):
@@ -46,12 +49,13 @@ def test_adam_kernel_matches_torch_adamw():
     assert torch.equal(params, master.bfloat16())  # the working copy is the rounded master
 
 
-def _model(world, pol, L, E, d, f, Tr, bias):
+def _model(world, pol, L, E, d, f, Tr, bias, grad_dtype="bf16"):
     topo = F.ClusterTopology.for_nvswitch(world)
     cfg = F.ModelConfig(L, E, 2 * 2 * d * f, 2 * d, 1e-3, 1e-6)
     planners = [F.FssdpPlanner(cfg, topo, pol) for _ in range(world)]
     m = pol.capacity_override if pol.capacity_override is not None else E
-    geoms = layer_geometries(planners[0], d, f, 2, Tr, m, "gelu", optimizer=True)
+    geoms = layer_geometries(planners[0], d, f, 2, Tr, m, "gelu", optimizer=True,
+                             grad_dtype=grad_dtype)
     layout = HeapLayout()
     for li, g in enumerate(geoms):
         g.add_regions(layout, f"L{li}.")
@@ -76,7 +80,11 @@ def _owner_state(model, li, e, opts):
     raise AssertionError(f"expert {e} of layer {li} has no owner")
 
 
-def test_optimizer_state_moves_with_reshard_and_replicas_follow_updates():
+@pytest.mark.parametrize("grad_dtype,drift", [("fp32", 0.05), ("bf16", 0.15)])
+def test_optimizer_state_moves_with_reshard_and_replicas_follow_updates(grad_dtype, drift):
+    """drift: bound on |Δ update| / |update| between the sharded and the single-rank run.
+    Adam's first steps are ~lr·sign(g): an element whose holders' partials nearly cancel can
+    flip sign under reduction-order (fp32) or partial-rounding (bf16 gradients) noise."""
     world, L, E, d, f, Tr = 4, 2, 8, 256, 512, 256
     pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2,
                    reshard_interval=2)
@@ -86,8 +94,9 @@ def test_optimizer_state_moves_with_reshard_and_replicas_follow_updates():
         p = 1.0 / np.arange(1, E + 1) ** (1.0 + li)
         bias.append(torch.tensor(np.log(p[rng.permutation(E)] / p.sum()), dtype=torch.float32,
                                  device="cuda"))
-    multi, opts, planners = _model(world, pol, L, E, d, f, Tr, bias)
-    single, sopts, _ = _model(1, F.Policy(F.PolicyKind.EP), L, E, d, f, world * Tr, bias)
+    multi, opts, planners = _model(world, pol, L, E, d, f, Tr, bias, grad_dtype)
+    single, sopts, _ = _model(1, F.Policy(F.PolicyKind.EP), L, E, d, f, world * Tr, bias,
+                              grad_dtype)
     gen = torch.Generator(device="cuda").manual_seed(8)
     moved = replicas = 0
     init = {(li, e): _owner_state(single, li, e, sopts)[1] for li in range(L) for e in range(E)}
@@ -130,6 +139,7 @@ def test_optimizer_state_moves_with_reshard_and_replicas_follow_updates():
                 _, ms, _, _ = _owner_state(single, li, e, sopts)  # compare the updates' norms
                 upd = (ms - init[(li, e)]).norm().item()
                 assert (mm - ms).abs().max().item() <= 2.5 * lr * (it + 1), f"it {it} L{li} e{e}"
-                assert (mm - ms).norm().item() <= 0.05 * upd, f"it {it} L{li} e{e}: update differs"
+                assert (mm - ms).norm().item() <= drift * upd, \
+                    f"it {it} L{li} e{e}: update differs"
     assert moved > 0, "the per-layer skews should trigger a re-shard"
     assert replicas > 0

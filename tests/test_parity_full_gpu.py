@@ -35,7 +35,8 @@ from paper_2502_02581_b200.comm import HeapLayout, emulated_group
 from paper_2502_02581_b200.layer import (FssdpMoE, LayerGeometry, default_slots,
                                          run_lockstep_backward, run_lockstep_forward)
 
-from _torch_ref import bf16, layer as ref_layer, rel_err, stage_dgrad2, stage_fwd1
+from _torch_ref import (bf16, grad_excess, layer as ref_layer, rel_err, stage_dgrad2,
+                        stage_fwd1)
 
 pytestmark = pytest.mark.gpu
 
@@ -189,7 +190,10 @@ def test_gemm_stages_against_fp32(run):
                 ("wgrad2", dw2, dyr.float().T @ ly.h[sl].float())):
             e = rel_err(out, ref)
             worst[what] = max(worst.get(what, 0.0), e)
-            assert e <= STAGE_F32, f"{name} {what}[s{s}] rel {e:.3g} > {STAGE_F32}"
+            if out.dtype == torch.bfloat16:  # bf16 gradients: the fp32 sum rounded once
+                _ulp_check(out, ref, f"{what}[s{s}]", name)
+            else:
+                assert e <= STAGE_F32, f"{name} {what}[s{s}] rel {e:.3g} > {STAGE_F32}"
     _log(dict(config=name, check="wgrad", worst=worst, max_segment_rows=max_rows))
     assert max_rows > 0
 
@@ -262,12 +266,13 @@ def test_cfg2_four_ranks_equal_one_rank():
         prefetched += sum(ly.pre_tables.n_spag for ly in multi if ly.pre_tables is not None)
         assert torch.equal(torch.cat(ys), y1), f"y differs (it {it})"
         assert torch.equal(torch.cat(dxs), dx1), f"dx differs (it {it})"
-        worst = 0.0
+        worst, excess = 0.0, -1.0
         for e in range(c["E"]):
             o = dec.base.owner(e)
             for gm, gs in zip(multi[o].expert_grad(e), single.expert_grad(e)):
                 worst = max(worst, rel_err(gm, gs))
-        assert worst <= 1e-4, f"SpRS-reduced grads rel {worst} (it {it})"
+                excess = max(excess, grad_excess(gm, gs))
+        assert excess <= 0, f"SpRS-reduced grads rel {worst} (it {it})"
         _log(dict(config="cfg2_n4", it=it, sprs_rel=worst,
                   replicas=len(dec.target.entries) - c["E"]))
     assert replicas > 0 and prefetched > 0

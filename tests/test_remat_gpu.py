@@ -10,6 +10,7 @@ import pytest
 import torch
 
 import paper_2502_02581_b200 as F
+from _torch_ref import grad_excess
 from paper_2502_02581_b200.comm import HeapLayout, emulated_group
 from paper_2502_02581_b200.layer import (FssdpMoE, layer_geometries, model_regions,
                                          replica_region_bytes, replica_slots,
@@ -84,6 +85,5 @@ def test_shared_replica_region_remat_matches_single_rank(remat):
             for e in range(E):
                 o = dec.base.owner(e)
                 for gm, gs_ in zip(multi[li][o].expert_grad(e), single[li][0].expert_grad(e)):
-                    gm, gs_ = gm.double(), gs_.double()
-                    assert (gm - gs_).abs().max() <= 1e-4 * gs_.abs().max() + 1e-7
+                    assert grad_excess(gm, gs_) <= 0, f"it {it} layer {li} expert {e} grad"
     assert replicas > 0

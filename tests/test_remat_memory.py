@@ -42,6 +42,11 @@ def test_replica_region_equals_memory_report(remat, L, E, D, m):
     layout = HeapLayout()
     geoms = model_regions(layout, layer_geometries(planner, d, f, 2, 256, m), remat)
     grads = sum(layout.regions[f"L{li}.grads"][1] for li in range(L))
+    assert grads == rep.param_bytes.max()  # bf16: the reference's grad bytes = param bytes
+    layout = HeapLayout()
+    geoms = model_regions(layout, layer_geometries(planner, d, f, 2, 256, m, grad_dtype="fp32"),
+                          remat)
+    grads = sum(layout.regions[f"L{li}.grads"][1] for li in range(L))
     assert grads == 2 * rep.param_bytes.max()  # fp32 = 2x the bf16 expert bytes
 
 

@@ -3,8 +3,8 @@ emulated on one GPU (separate symmetric heaps, real cross-heap addressing).
 
 SpAG: every replica slot becomes a bit-exact copy of its owner's shard.  SpRS (push's
 owner-local reduce and the pull kernel): each owned slot becomes the fp32 sum, in listed
-(ascending-rank) order, of the holders' partials — checked BIT-EXACTLY against a numpy
-float32 sequential sum.  Schedules come from the product tables (build_rank_tables) of
+(ascending-rank) order, of the holders' partials — checked BIT-EXACTLY against a float32
+sequential sum (bf16 gradients: of the partials widened to fp32, rounded once at the end).  Schedules come from the product tables (build_rank_tables) of
 ring and hot-expert placements (sparse sweep shapes) and random ones; slot sizes include
 ragged ones (not a multiple of the kernels' 8 KB sub-chunks).
 """
@@ -45,7 +45,7 @@ def setup(world, E, slot_elems, kind, seed=0):
     n_stage = max(1, max(t.n_stage for t in tabs))
     layout = HeapLayout()
     layout.add("params", slots * slot_elems * 2)
-    layout.add("grads", slots * slot_elems * 4)
+    layout.add("grads", slots * slot_elems * 4)  # fp32-sized: either gradient dtype fits
     layout.add("stage", n_stage * slot_elems * 4)
     groups = emulated_group(layout, world)
     return base, post, tabs, layout, groups, slots, n_stage
@@ -74,19 +74,21 @@ def test_spag_copies_owner_shards(world, E, kind, slot_elems):
             assert torch.equal(params[r][s], params[o][tabs[o].slots[e]]), (r, e)
 
 
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("pull", [False, True])
 @pytest.mark.parametrize("world,E,kind,slot_elems", [
-    (2, 2, "ring", 1 << 20), (4, 4, "ring", 3 * 2048 + 500), (4, 8, "hot", 1 << 18),
-    (8, 8, "ring", 12345 * 4), (8, 16, "random", 77777 * 4)])
-def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull):
+    (2, 2, "ring", 1 << 20), (4, 4, "ring", 3 * 2048 + 504), (4, 8, "hot", 1 << 18),
+    (8, 8, "ring", 12345 * 8), (8, 16, "random", 77777 * 8)])
+def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull, dt):
     """Partials sit where the transport expects them — push: the owner's staging slots;
     pull: the holders' own grads slots — and the owner's grads slot ends up holding the
-    ascending-rank fp32 sum (bit-exact)."""
+    ascending-rank fp32 sum (bit-exact; bf16 slots: rounded once)."""
     base, post, tabs, layout, groups, slots, n_stage = setup(world, E, slot_elems, kind, seed=3)
     goff, soff = layout.offset("grads"), layout.offset("stage")
     g = torch.Generator(device="cuda").manual_seed(2)
-    grads = [grp.local.tensor(goff, (slots, slot_elems), torch.float32) for grp in groups]
-    stage = [grp.local.tensor(soff, (n_stage, slot_elems), torch.float32) for grp in groups]
+    grads = [grp.local.tensor(goff, (slots, slot_elems), dt) for grp in groups]
+    stage = [grp.local.tensor(soff, (n_stage, slot_elems), dt) for grp in groups]
+    eb = 4 if dt == torch.float32 else 2
     partial = {}  # (expert, holder) -> its partial
     for r, t in enumerate(tabs):
         grads[r].copy_(torch.randn(slots, slot_elems, generator=g, device="cuda"))
@@ -107,11 +109,11 @@ def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull):
     for r, t in enumerate(tabs):
         pb, jobs = C.c_void_p(groups[r].peer_bases.data_ptr()), t.offsets["sprs_jobs"]
         if pull:
-            N.call("fssdp_sprs_pull", pb, r, goff, slot_elems,
+            N.call("fssdp_sprs_pull", pb, r, goff, slot_elems, eb,
                    C.c_void_p(blobs[r].data_ptr() + jobs), t.n_sprs_jobs,
                    C.c_void_p(blobs[r].data_ptr() + t.offsets["sprs_pull"]), stream)
         else:
-            N.call("fssdp_sprs", pb, r, goff, soff, slot_elems,
+            N.call("fssdp_sprs", pb, r, goff, soff, slot_elems, eb,
                    C.c_void_p(blobs[r].data_ptr() + jobs), t.n_sprs_jobs,
                    C.c_void_p(blobs[r].data_ptr() + t.offsets["sprs_srcs"]), stream)
     torch.cuda.synchronize()
@@ -121,13 +123,13 @@ def test_sprs_sums_partials_in_rank_order(world, E, kind, slot_elems, pull):
             if base.owner(e) != r:
                 continue
             holders = [d for d in range(world) if post.mask[e, d]]
-            want = np.zeros(slot_elems, dtype=np.float32)
+            want = torch.zeros(slot_elems, dtype=torch.float32)
             for h in holders:
-                want = want + partial[(e, h)].cpu().numpy()   # float32, ascending rank
-            got = grads[r][s].cpu().numpy()
+                want = want + partial[(e, h)].cpu().float()   # float32, ascending rank
+            got = grads[r][s].cpu()
             if len(holders) > 1:
                 reduced += 1
-                assert np.array_equal(got, want), (r, e)
+                assert torch.equal(got, want.to(dt)), (r, e)
             else:
-                assert np.array_equal(got, partial[(e, r)].cpu().numpy())
+                assert torch.equal(got, partial[(e, r)].cpu())
     assert reduced > 0
