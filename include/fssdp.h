@@ -461,6 +461,14 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
 int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, float* workspace, float* dwg_out,
                      void* stream);
+/* The same dWg on the tensor cores: the logit gradient as a dense bf16 [T, hi | lo] matrix
+ * (~16 mantissa bits of the fp32 dlogit), one split-T grouped-GEMM launch of x^T times it,
+ * and a fixed-order reduction of the splits (deterministic for a given T and SM count).
+ * E <= 64, d_model % 256 == 0; ws: fssdp_gate_wgrad_tc_ws_bytes(T, d_model) device bytes. */
+int64_t fssdp_gate_wgrad_tc_ws_bytes(int64_t T, int32_t d_model);
+int fssdp_gate_wgrad_tc(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
+                        int32_t d_model, int32_t E, int32_t k, void* ws, int64_t ws_bytes,
+                        float* dwg_out, void* stream);
 
 /* K3: SparseAllGather.  copies[n * 3] = {src_rank, src_slot, dst_slot}: pull
  * slot_bytes from peer src_rank's heap (offset param_off + src_slot * slot_bytes) into

@@ -135,6 +135,8 @@ _SIGS = {
                             i64, i32, i32, i32, u32, vp, vp],
     "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],
     "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
+    "fssdp_gate_wgrad_tc_ws_bytes": [i64, i32],
+    "fssdp_gate_wgrad_tc": [vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp],
     "fssdp_spag": [vp, i32, i64, i64, vp, i32, vp],
     "fssdp_gather_slots": [vp, i32, i64, i64, i64, i64, vp, i32, i32, vp],
     "fssdp_sprs": [vp, i32, i64, i64, i64, i32, vp, i32, vp, vp],
@@ -162,7 +164,7 @@ _SIGS = {
     "fssdp_pull_host": [vp, vp, i64, vp],
 }
 _RESTYPE = {"fssdp_version": C.c_char_p, "fssdp_last_error": C.c_char_p,
-            "fssdp_gate_gemm_ws_bytes": C.c_int64}
+            "fssdp_gate_gemm_ws_bytes": C.c_int64, "fssdp_gate_wgrad_tc_ws_bytes": C.c_int64}
 
 
 def header_symbols() -> list[str]:
@@ -212,6 +214,7 @@ KERNELS_PER_CALL = {
     "fssdp_route_scan_allgather": 1, "fssdp_gate_route": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1, "fssdp_local_gemm_tables": 1,
     "fssdp_plan_layer_dispatch": 2,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
+    "fssdp_gate_wgrad_tc": 3,
     "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
     "fssdp_gather_slots": 1, "fssdp_barrier_selftest": 1, "fssdp_adam_step": 1,
     "fssdp_publish_epoch": 1, "fssdp_wait_epochs": 1,

@@ -706,13 +706,79 @@ __global__ void __launch_bounds__(128 * KS)
                   SW ? reinterpret_cast<int32_t*>(gate_wsm) : nullptr, SW ? E * wrow / 4 : 0);
 }
 
+// ------------------------------------------------------------------ gate backward on tcgen05
+// dWg^T [d, 2E] = x^T [d, T] . G [T, 2E], G = the gate's logit gradient as a dense bf16
+// matrix (row t: hi(dlogit) at column e, lo = bf16(dlogit - hi) at column E + e for each of
+// its k experts, zeros elsewhere — ~16 mantissa bits of the fp32 gradient), split along T
+// into `splits` groups so one wave of CTA pairs covers it; then
+// dWg[e, c] = sum over splits, in order, of (C_s[c, e] + C_s[c, E + e]).  Replaces the
+// SIMT gate_wgrad partials (their E x 512-column accumulators cannot co-reside with a GEMM
+// CTA, so at E = 64 they stretch over the backward's last GEMMs).
+constexpr int kGateN = 128;  // the gate GEMMs' N tile: hi and lo of up to 64 experts
+static int gate_wgrad_splits(int64_t T, int d) {
+  const int pair_tiles = d / 256;                      // M tiles of one split
+  int s = (num_sms() / 2 + pair_tiles - 1) / pair_tiles;  // ~one wave of CTA pairs
+  const int64_t kb = (T + 63) / 64;                    // at least 4 K blocks per split
+  if (s > kb / 4) s = static_cast<int>(kb / 4);
+  return s > 0 ? s : 1;
+}
+
+__global__ void __launch_bounds__(256)
+    gate_wgrad_prep_kernel(const int32_t* __restrict__ topk_idx, const float* __restrict__ dlogit,
+                           int64_t T, int64_t rows, int E, int k, int d, int splits, int64_t ks,
+                           __nv_bfloat16* __restrict__ g, GemmGroup* __restrict__ groups) {
+  // one thread per 8 columns (16 bytes) of G
+  const int64_t n16 = rows * kGateN / 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (kGateN / 8);
+    const int c0 = static_cast<int>(i % (kGateN / 8)) * 8;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (t < T && c0 < 2 * E) {
+      for (int j = 0; j < k; ++j) {
+        const int e = topk_idx[t * k + j];
+        const float w = dlogit[t * k + j];
+        const float hi = __bfloat162float(__float2bfloat16_rn(w));
+        if (e >= c0 && e < c0 + 8) v[e - c0] = hi;
+        if (E + e >= c0 && E + e < c0 + 8) v[E + e - c0] = w - hi;
+      }
+    }
+    __nv_bfloat162 o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    reinterpret_cast<int4*>(g)[i] = *reinterpret_cast<const int4*>(o);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < splits) {
+    const int s = threadIdx.x;
+    const int64_t k0 = s * ks;
+    const int64_t kn = k0 >= rows ? 0 : (rows - k0 < ks ? rows - k0 : ks);
+    const int mt = d / 128;
+    groups[s] = GemmGroup{mt, s * mt, 0, static_cast<int>(k0), 0, static_cast<int>(k0),
+                          static_cast<int>(kn / 64), 0, static_cast<int64_t>(s) * d * kGateN};
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    gate_wgrad_tc_reduce_kernel(const float* __restrict__ c, int splits, int d, int E,
+                                float* __restrict__ dwg) {
+  // thread i: expert i % E of column i / E (neighbouring threads read one C row)
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(E) * d) return;
+  const int e = static_cast<int>(i % E), col = static_cast<int>(i / E);
+  float acc = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float* row = c + (static_cast<int64_t>(s) * d + col) * kGateN;
+    acc = __fadd_rn(acc, __fadd_rn(row[e], row[E + e]));
+  }
+  dwg[static_cast<int64_t>(e) * d + col] = acc;
+}
+
 // ------------------------------------------------------------------ K1 on tcgen05
 // The gate logits as one grouped-GEMM launch on the 5th-generation tensor cores: x [T, d]
 // (K-major) times B = [hi(Wg); lo(Wg); 0] (kGateN x d bf16: the fp32 gate weights split
 // into two bf16 halves, ~16 mantissa bits) into fp32 C [T, kGateN]; then
 // logits[t, e] = (C[t, e] + C[t, E + e]) + bias[e].  The GEMM streams x through TMA at HBM
 // rate (the mma.sync gate kernel above is bound by the latency of its register loads).
-constexpr int kGateN = 128;  // the GEMM's N tile: hi and lo of up to 64 experts
 
 __global__ void __launch_bounds__(256)
     gate_gemm_prep_kernel(const float* __restrict__ wg, int E, int d,
@@ -2110,6 +2176,60 @@ int fssdp_gate_wgrad(const void* x, const int32_t* topk_idx, const float* dlogit
   timing_begin(as_stream(stream));
   gate_wgrad_reduce_kernel<<<static_cast<unsigned>((n_out + 31) / 32), 256, 0, as_stream(stream)>>>(
       workspace, n_tiles, d_model, E, dwg_out);
+  return launch_status();
+}
+
+int64_t fssdp_gate_wgrad_tc_ws_bytes(int64_t T, int32_t d) {
+  const int64_t rows = (T + 63) / 64 * 64;
+  const int splits = gate_wgrad_splits(T, d);
+  return 4096 + rows * kGateN * 2 + static_cast<int64_t>(splits) * d * kGateN * 4;
+}
+
+int fssdp_gate_wgrad_tc(const void* x, const int32_t* topk_idx, const float* dlogit, int64_t T,
+                        int32_t d_model, int32_t E, int32_t k, void* ws, int64_t ws_bytes,
+                        float* dwg_out, void* stream) {
+  if (E <= 0 || E > kGateN / 2 || k <= 0 || k > kGateMaxK || k > E || d_model <= 0 ||
+      d_model % 256 != 0 || T < 0 || ws_bytes < fssdp_gate_wgrad_tc_ws_bytes(T, d_model)) {
+    set_error("gate_wgrad_tc: needs E <= 64, d_model % 256 == 0 and "
+              "fssdp_gate_wgrad_tc_ws_bytes of workspace");
+    return kErrDimension;
+  }
+  const int64_t rows = (T + 63) / 64 * 64;
+  const int splits = gate_wgrad_splits(T, d_model);
+  const int64_t ks = (rows / 64 + splits - 1) / splits * 64;  // K rows per split
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  GemmGroup* groups = reinterpret_cast<GemmGroup*>(w8);
+  __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(w8 + 4096);
+  float* c = reinterpret_cast<float*>(w8 + 4096 + rows * kGateN * 2);
+  cudaStream_t s = as_stream(stream);
+  const int64_t n16 = rows * kGateN / 8;
+  const int pb = static_cast<int>((n16 + 255) / 256 < 2 * num_sms() ? (n16 + 255) / 256
+                                                                     : 2 * num_sms());
+  timing_begin(s);
+  gate_wgrad_prep_kernel<<<pb > 0 ? pb : 1, 256, 0, s>>>(topk_idx, dlogit, T, rows, E, k,
+                                                       d_model, splits, ks, g, groups);
+  int rc = launch_check();
+  if (rc != kOk) return rc;
+  if (T > 0) {
+    GemmLaunch args = {};
+    args.groups = groups;
+    args.num_groups = splits;
+    args.n_tiles = 1;
+    args.total_tiles = splits * (d_model / 128);
+    args.n_fast = 0;
+    args.cta_group = 2;
+    args.bn = kGateN;
+    args.ldc = kGateN;
+    args.c = c;
+    // A = x [T][d] read M-contiguous (MN-major), B = G [rows][kGateN] (MN-major)
+    rc = grouped_gemm_launch(1, 1, kEpiF32, x, d_model, T, g, kGateN, rows,
+                             static_cast<int64_t>(splits) * d_model, args, s);
+    if (rc != kOk) return rc;
+  }
+  const int64_t n_out = static_cast<int64_t>(E) * d_model;
+  timing_begin(s);
+  gate_wgrad_tc_reduce_kernel<<<static_cast<unsigned>((n_out + 255) / 256), 256, 0, s>>>(
+      c, T > 0 ? splits : 0, d_model, E, dwg_out);
   return launch_status();
 }
 

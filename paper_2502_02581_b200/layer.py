@@ -341,13 +341,19 @@ class FssdpMoE:
         # the backward then pulls nothing over NVLink; one rank reads its own heap anyway
         self.y_slots = (torch.empty(Tc * k, d, dtype=torch.bfloat16, device=self.dev)
                         if self.world > 1 and self.KEEP_Y_SLOTS else None)
-        wg_tiles = max(1, (Tc + WG_TILE - 1) // WG_TILE)
-        self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
+        # the gate backward: on the tensor cores (fssdp_gate_wgrad_tc) unless FSSDP_GATE_WGRAD_TC=0
+        self._wg_tc = self.GATE_WGRAD_TC and E <= 64 and d % 256 == 0
+        if self._wg_tc:
+            self.wg_ws = torch.empty(int(N.LIB.fssdp_gate_wgrad_tc_ws_bytes(Tc, d)),
+                                     dtype=torch.uint8, device=self.dev)
+        else:
+            wg_tiles = max(1, (Tc + WG_TILE - 1) // WG_TILE)
+            self.wg_ws = torch.empty(wg_tiles * E * d, dtype=torch.float32, device=self.dev)
         self.grid_counter = torch.zeros(4, dtype=torch.int32, device=self.dev)
         # dynamic tile scheduler counters of this layer's GEMMs (all on the main stream, in
         # order; each launch leaves them zero) — used with FSSDP_GEMM_DYN=1
         self.gemm_sched = torch.zeros(2, dtype=torch.int32, device=self.dev)
-        self._gemm_sched_ptr = C.c_void_p(self.gemm_sched.data_ptr() if self.GEMM_DYN else 0)
+        self._gemm_sched_ptr = C.c_void_p(self.gemm_sched.data_ptr())
         self.gate_ws = torch.zeros(1 + E, dtype=torch.int32, device=self.dev)  # ticket, totals
         self.blob_host = torch.empty(1 << 20, dtype=torch.uint8, pin_memory=True)
         self.blob_host_np = self.blob_host.numpy()
@@ -973,6 +979,7 @@ class FssdpMoE:
     # stream beside the remaining wgrads), "gate_end" (gate backward after them on the main
     # stream), "serial" (both after them)
     DX_MODE = os.environ.get("FSSDP_DX_MODE", "overlap")
+    GATE_WGRAD_TC = os.environ.get("FSSDP_GATE_WGRAD_TC", "1") == "1"
 
     @property
     def _early_gate(self) -> bool:
@@ -984,7 +991,10 @@ class FssdpMoE:
     # dynamic tile scheduling of the grouped GEMMs (FSSDP_GEMM_DYN=1): measured neutral in
     # isolation (cfg2 shapes within +-1.5 %) and 1.7 % slower per step than the static snake
     # order (interleaved A/B, N=1), so off by default
-    GEMM_DYN = os.environ.get("FSSDP_GEMM_DYN", "0") == "1"
+    # (FSSDP_GEMM_DYN=name,name: only those GEMMs)
+    _dyn = os.environ.get("FSSDP_GEMM_DYN", "0")
+    GEMM_DYN = (set(("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2")) if _dyn == "1"
+                else set() if _dyn == "0" else set(_dyn.split(",")))
 
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
@@ -1014,7 +1024,7 @@ class FssdpMoE:
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],
             ops._ptr(b), b.shape[1], b.shape[0], tab, ng, n_tiles, total, ops._ptr(c),
             ops._ptr(c2), ops._ptr(aux), maps, ldc, c.numel() // ldc, flags,
-            self._gemm_sched_ptr, self._stream()))
+            self._gemm_sched_ptr if name in self.GEMM_DYN else None, self._stream()))
 
     def phase_experts_fwd(self) -> None:
         f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1
@@ -1099,6 +1109,12 @@ class FssdpMoE:
         return dx
 
     def phase_gate_wgrad(self) -> None:
+        if self._wg_tc:
+            self._call("fssdp_gate_wgrad_tc", ops._ptr(self.x), ops._ptr(self.topk_idx),
+                       ops._ptr(self.dlogit), self.T, self.g.d_model, self.g.num_experts,
+                       self.g.top_k, ops._ptr(self.wg_ws), self.wg_ws.numel(),
+                       ops._ptr(self.dwg), self._stream())
+            return
         self._call("fssdp_gate_wgrad", ops._ptr(self.x), ops._ptr(self.topk_idx),
                ops._ptr(self.dlogit), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,
                ops._ptr(self.wg_ws), ops._ptr(self.dwg), self._stream())

@@ -50,7 +50,32 @@ def wgrad(G, K, M, N, epi, pair, bn=256):
     return t, fl / (t * 1e-3) / 1e12, G * M * N * out.element_size() / (t * 1e-3) / 1e9
 
 
+def wgrad_ragged(Ks, M, N, epi, dynamic):
+    """Groups of different token rows (descending, as the layer lists them)."""
+    Ks = sorted(Ks, reverse=True)
+    a = torch.randn(sum(Ks), M, device="cuda").bfloat16()
+    b = torch.randn(sum(Ks), N, device="cuda").bfloat16()
+    out = torch.empty(len(Ks) * M, N, device="cuda",
+                      dtype=torch.float32 if epi == ops.EPI_F32 else torch.bfloat16)
+    nt = N // 256
+    offs = np.concatenate([[0], np.cumsum(Ks)[:-1]])
+    gd = groups([(M // 128, 0, int(o), 0, int(o), k // 64, g * M * N)
+                 for g, (k, o) in enumerate(zip(Ks, offs))], nt)
+    t = timeit(lambda: ops.grouped_gemm(a, True, b, True, *gd[:2], nt, gd[2], out, N, epi,
+                                        cta_pair=True, dynamic=dynamic))
+    return t, 2 * sum(Ks) * M * N / (t * 1e-3) / 1e12
+
+
 print(f"lib={os.environ.get('FSSDP_LIB', 'default')}")
+if os.environ.get("RAGGED"):
+    p = 1.0 / np.arange(1, 17) ** 1.2
+    Ks = [max(64, int(round(32768 * x / p.sum() / 64)) * 64) for x in p]
+    for name, ks in (("zipf", Ks), ("uniform", [2048] * 16)):
+        for dyn in (False, True):
+            t, tf = wgrad_ragged(ks, 4096, 1024, ops.EPI_BF16, dyn)
+            print(f"cfg2 wgrad1 {name:8s} dyn={int(dyn)} {t * 1e3:8.1f} us {tf:7.1f} TFLOP/s "
+                  f"rows {sum(ks)}", flush=True)
+    sys.exit(0)
 for name, G, K, M, N in (("cfg4 wgrad1", 64, 512, 2816, 2048), ("cfg4 wgrad2", 64, 512, 2048, 1408),
                          ("cfg4 wgrad1 K2048", 16, 2048, 2816, 2048),
                          ("cfg2 wgrad1", 16, 2048, 4096, 1024)):

@@ -190,3 +190,44 @@ def test_tensor_core_gate_route(T, d, E, k):
     prefix = torch.cumsum(tc, 0) - tc
     assert torch.equal(out[4], prefix.int())
     assert torch.equal(table, tc.sum(0).int())
+
+
+@pytest.mark.parametrize("T,d,E,k", [(1000, 256, 8, 2), (16384, 1024, 16, 2), (3000, 2048, 64, 2),
+                                     (130, 512, 16, 4), (0, 256, 8, 2)])
+def test_tensor_core_gate_wgrad(T, d, E, k):
+    """fssdp_gate_wgrad_tc (dlogit as bf16 hi/lo, split-T tcgen05 GEMM, fixed-order reduce)
+    against an fp64 sum and the SIMT fssdp_gate_wgrad; deterministic across calls."""
+    import ctypes as C
+
+    from paper_2502_02581_b200 import _native as N
+
+    g = torch.Generator().manual_seed(T + d + E)
+    x = torch.randn(max(T, 1), d, generator=g).bfloat16()[:T]
+    idx = torch.stack([torch.randperm(E, generator=g)[:k] for _ in range(T)]) if T else \
+        torch.zeros(0, k, dtype=torch.int64)
+    dl = torch.randn(T, k, generator=g) * 0.1
+    ref = torch.zeros(E, d, dtype=torch.float64)
+    ref.index_add_(0, idx.reshape(-1), (dl.double()[:, :, None] * x.double()[:, None, :])
+                   .reshape(-1, d))
+    xd, idd, dld = x.cuda(), idx.int().cuda(), dl.float().cuda()
+    ws = torch.empty(int(N.LIB.fssdp_gate_wgrad_tc_ws_bytes(T, d)), dtype=torch.uint8,
+                     device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    outs = []
+    for _ in range(2):
+        dwg = torch.full((E, d), float("nan"), device="cuda")
+        N.call("fssdp_gate_wgrad_tc", C.c_void_p(xd.data_ptr()), C.c_void_p(idd.data_ptr()),
+               C.c_void_p(dld.data_ptr()), T, d, E, k, C.c_void_p(ws.data_ptr()), ws.numel(),
+               C.c_void_p(dwg.data_ptr()), st)
+        outs.append(dwg)
+    wsimt = torch.empty(max(1, (T + 63) // 64) * E * d, device="cuda")
+    simt = torch.empty(E, d, device="cuda")
+    N.call("fssdp_gate_wgrad", C.c_void_p(xd.data_ptr()), C.c_void_p(idd.data_ptr()),
+           C.c_void_p(dld.data_ptr()), T, d, E, k, C.c_void_p(wsimt.data_ptr()),
+           C.c_void_p(simt.data_ptr()), st)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])  # deterministic
+    got = outs[0].double().cpu()
+    scale = max(ref.abs().max().item(), 1e-30)
+    assert (got - ref).abs().max().item() <= 1e-5 * scale + 1e-7, "tensor-core dWg vs fp64"
+    assert (simt.double().cpu() - got).abs().max().item() <= 2e-5 * scale + 1e-7
