@@ -2138,7 +2138,13 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
     return kErrDimension;
   }
   if (T == 0) return kOk;
-  const int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
+  // CTA cap (FSSDP_COMBINE_DX_CTAS, experiments): it runs beside the weight-gradient GEMMs
+  static const int cap = [] {
+    const char* v = getenv("FSSDP_COMBINE_DX_CTAS");
+    return v ? atoi(v) : 0;
+  }();
+  int grid = grid_for_warps((T + kTokBatch - 1) / kTokBatch);
+  if (cap > 0 && grid > cap) grid = cap;
   timing_begin(as_stream(stream));
   FSSDP_DISPATCH_K(k, combine_dx_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_idx,
                    topk_w, slot_grad, wg, T, d_model, peer_bases, dxe_off, dlogit_out,

@@ -9,8 +9,8 @@ timeout 600 $B > gpurun_out/p_plain.log 2>&1 &&
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv \
     --log-file gpurun_out/p_launches.csv $B > gpurun_out/p_ncu1.log 2>&1
 echo launches=$?
-# one step = 13 launches at N = 1; skip the 3 warm-up steps
-timeout 1500 ncu --set full --clock-control none --import-source on -k "$K" -s 39 -c 13 \
+# one step = 14 launches at N = 1; skip the 3 warm-up steps
+timeout 1500 ncu --set full --clock-control none --import-source on -k "$K" -s 42 -c 14 \
     -o gpurun_out/p_step_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/p_ncu2.log 2>&1
 echo full=$?

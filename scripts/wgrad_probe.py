@@ -70,11 +70,15 @@ print(f"lib={os.environ.get('FSSDP_LIB', 'default')}")
 if os.environ.get("RAGGED"):
     p = 1.0 / np.arange(1, 17) ** 1.2
     Ks = [max(64, int(round(32768 * x / p.sum() / 64)) * 64) for x in p]
-    for name, ks in (("zipf", Ks), ("uniform", [2048] * 16)):
-        for dyn in (False, True):
-            t, tf = wgrad_ragged(ks, 4096, 1024, ops.EPI_BF16, dyn)
-            print(f"cfg2 wgrad1 {name:8s} dyn={int(dyn)} {t * 1e3:8.1f} us {tf:7.1f} TFLOP/s "
-                  f"rows {sum(ks)}", flush=True)
+    p4 = 1.0 / np.arange(1, 65) ** 1.2
+    Ks4 = [max(64, int(round(32768 * x / p4.sum() / 64)) * 64) for x in p4]
+    for cfg, M, N_, cases in (("cfg2", 4096, 1024, (("zipf", Ks), ("uniform", [2048] * 16))),
+                              ("cfg4", 2816, 2048, (("zipf", Ks4), ("uniform", [512] * 64)))):
+        for name, ks in cases:
+            for dyn in (False, True):
+                t, tf = wgrad_ragged(ks, M, N_, ops.EPI_BF16, dyn)
+                print(f"{cfg} wgrad1 {name:8s} dyn={int(dyn)} {t * 1e3:8.1f} us {tf:7.1f} "
+                      f"TFLOP/s rows {sum(ks)} max K {max(ks)}", flush=True)
     sys.exit(0)
 for name, G, K, M, N in (("cfg4 wgrad1", 64, 512, 2816, 2048), ("cfg4 wgrad2", 64, 512, 2048, 1408),
                          ("cfg4 wgrad1 K2048", 16, 2048, 2816, 2048),
