@@ -314,6 +314,10 @@ typedef struct fssdp_gemm_group {
 #define FSSDP_GEMM_CTA_PAIR 2
 /* 128-wide N tiles (N % 256 != 0, e.g. d_ff = 1408); not with FSSDP_EPI_SWIGLU. */
 #define FSSDP_GEMM_BN128 4
+/* With CTA_PAIR and N_FASTEST, 256-wide N tiles, an even n_tiles and no tile_sched:
+ * clusters of two CTA pairs on N tiles (2j, 2j+1) of one M tile; the A tile is loaded once
+ * and multicast into both pairs (half the A operand's L2 -> SM traffic). */
+#define FSSDP_GEMM_MULTICAST 8
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,

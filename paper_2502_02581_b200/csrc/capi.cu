@@ -317,6 +317,15 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.total_tiles = total_tiles;
   args.n_fast = (flags & FSSDP_GEMM_N_FASTEST) ? 1 : 0;
   args.cta_group = (flags & FSSDP_GEMM_CTA_PAIR) ? 2 : 1;
+  if (flags & FSSDP_GEMM_MULTICAST) {
+    if (args.cta_group != 2 || !(flags & FSSDP_GEMM_N_FASTEST) || (flags & FSSDP_GEMM_BN128) ||
+        n_tiles % 2 != 0 || tile_sched != nullptr) {
+      set_error("grouped_gemm: MULTICAST needs CTA_PAIR, N_FASTEST, 256-wide N tiles, an even "
+                "n_tiles and the static order");
+      return kErrDimension;
+    }
+    args.cta_group = 4;
+  }
   args.bn = (flags & FSSDP_GEMM_BN128) ? 128 : 256;
   if (args.bn == 128 && epilogue == kEpiSwiglu) {
     set_error("grouped_gemm: the SwiGLU epilogue needs 256-wide N tiles");

@@ -171,23 +171,27 @@ struct TileCoord {
 
 // Tiles are enumerated in units of (CG*128 rows) x BN columns; groups carry m_tiles and
 // tile_start in 128-row units (both even when CG == 2).
-template <int CG>
+// CL = 2: a cluster of two CTA pairs takes N tiles (2 n2, 2 n2 + 1) of the same M tile
+// (N-fastest order only); `pair` selects this pair's one.
+template <int CG, int CL = 1>
 __device__ __forceinline__ TileCoord locate_tile(const GemmGroup* __restrict__ groups,
                                                  int num_groups, int n_tiles, int n_fast,
-                                                 int tile, int& cursor) {
+                                                 int tile, int& cursor, int pair = 0) {
   // A role's tiles come in increasing order (snake rounds, or the scheduler's counter), so
   // the group search resumes from the previous tile's group: a scan from group 0 is a chain
   // of dependent loads as long as the group index (64+ groups at cfg4), at every tile.
-  int g = groups[cursor].tile_start / CG <= tile ? cursor : 0;
-  while (g + 1 < num_groups && groups[g + 1].tile_start / CG <= tile) ++g;
+  constexpr int U = CG * CL;
+  int g = groups[cursor].tile_start / U <= tile ? cursor : 0;
+  while (g + 1 < num_groups && groups[g + 1].tile_start / U <= tile) ++g;
   cursor = g;
-  const int local = tile - groups[g].tile_start / CG;
+  const int local = tile - groups[g].tile_start / U;
   const int mt = groups[g].m_tiles / CG;
+  const int nt = n_tiles / CL;
   TileCoord tc;
   tc.group = g;
   if (n_fast) {  // neighbouring CTAs share the A tile (activation rows) in L2
-    tc.n_tile = local % n_tiles;
-    tc.m_tile = local / n_tiles;
+    tc.n_tile = (local % nt) * CL + pair;
+    tc.m_tile = local / nt;
   } else {  // neighbouring CTAs share the B tile (weights) in L2
     tc.m_tile = local % mt;
     tc.n_tile = local / mt;
@@ -203,12 +207,18 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) {  // 128-byte rows, SWI
   return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
 }
 
-template <bool A_MN, bool B_MN, int BN, int EPI, int CG>
+// CGX: 1 = one CTA per 128x256 tile, 2 = a CTA pair per 256x256 tile (cta_group::2),
+// 4 = clusters of two pairs on neighbouring N tiles of one M tile: the A tile is loaded
+// once per cluster and multicast into both pairs (TMA .multicast::cluster), halving the
+// A operand's L2 -> SM traffic.
+template <bool A_MN, bool B_MN, int BN, int EPI, int CGX>
 __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
                         const __grid_constant__ CUtensorMap map_x, GemmLaunch args) {
+  constexpr int CG = CGX == 4 ? 2 : CGX;  // CTAs per tile
+  constexpr int CL = CGX == 4 ? 2 : 1;    // tiles (pairs) per cluster
   using S = GemmSmem<BN, EPI, CG>;
   constexpr int kStages = S::kStages;
   constexpr int kBNc = BN / CG;  // B columns staged by this CTA
@@ -228,10 +238,15 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank & 1u;  // position in the pair
+  const int pair = static_cast<int>(crank >> 1);  // pair in the cluster (CL = 2)
   const bool leader = rank == 0;
-  const int unit = CG == 2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
-  const int units = CG == 2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+  const int unit = static_cast<int>(blockIdx.x) / (CG * CL);
+  const int units = static_cast<int>(gridDim.x) / (CG * CL);
+  // tfull commits go to this pair's two CTAs; a stage is free once every pair consumed it
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pair));
+  const uint16_t stage_mask = CL == 2 ? static_cast<uint16_t>(0xF) : static_cast<uint16_t>(3);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -239,7 +254,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     tma_prefetch_desc(&map_c);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], CL);  // one MMA commit per pair sharing the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -278,9 +293,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       (args.total_tiles >= 0
            ? args.total_tiles
            : args.groups[args.num_groups - 1].tile_start +
-                 args.groups[args.num_groups - 1].m_tiles * args.n_tiles) / CG;
+                 args.groups[args.num_groups - 1].m_tiles * args.n_tiles) / (CG * CL);
 
-  const bool dyn = args.sched != nullptr;
+  const bool dyn = CL == 1 && args.sched != nullptr;
   // consumer side of the scheduler ring: entry `it` -> tile id (-1: no more work); the
   // entry is released on the leader (remote arrive from the follower CTA)
   auto sched_take = [&](int it) -> int {
@@ -373,7 +388,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         }
         if (tile < 0) break;
         const TileCoord tc =
-            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur);
+            locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
+                                pair);
         const GemmGroup& g = groups[tc.group];
         const int m0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * kBM;
         const int n0 = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * kBNc;
@@ -387,7 +403,19 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           const int ka = g.a_k + kb * kBK;
           const int kbb = g.b_k + kb * kBK;
           if (CG == 2) {
-            if (A_MN) {
+            if (CL == 2) {  // the first pair loads A for both: CTA r -> CTAs r and r + 2
+              if (pair == 0) {
+                const uint16_t mc = static_cast<uint16_t>(0x5u << rank);
+                if (A_MN) {
+#pragma unroll
+                  for (int j = 0; j < kBM / 64; ++j)
+                    tma_load_2d_pair_mc(sa + j * (kBK * 128), &map_a, &full_bar[stage],
+                                        m0 + 64 * j, ka, mc);
+                } else {
+                  tma_load_2d_pair_mc(sa, &map_a, &full_bar[stage], ka, m0, mc);
+                }
+              }
+            } else if (A_MN) {
 #pragma unroll
               for (int j = 0; j < kBM / 64; ++j)
                 tma_load_2d_pair(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
@@ -440,7 +468,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         const int tile = next_tile(it);
         if (tile < 0) break;
         const TileCoord tc =
-            locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur);
+            locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
+                                pair);
         const int kblocks = groups[tc.group].k_blocks;
         PROF_T0(te);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -471,9 +500,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             else
               umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
           }
-          // frees the smem slot (in both CTAs) when these MMAs finish
+          // frees the smem slot (in both CTAs; CL = 2: in all four) when these MMAs finish
           if (CG == 2)
-            umma_commit_pair(&empty_bar[stage]);
+            umma_commit_pair(&empty_bar[stage], stage_mask);
           else
             umma_commit(&empty_bar[stage]);
           if (++stage == kStages) {
@@ -482,7 +511,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           }
         }
         if (CG == 2)  // accumulator ready for both CTAs' epilogues
-          umma_commit_pair(&tfull_bar[acc]);
+          umma_commit_pair(&tfull_bar[acc], pair_mask);
         else
           umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
@@ -522,7 +551,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile < 0) break;
       const TileCoord tc =
-          locate_tile<CG>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur);
+          locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
+                                pair);
       const GemmGroup& g = groups[tc.group];
       const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM) +
                        static_cast<int>(rank) * kBM + q * 32;
@@ -725,16 +755,45 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 
 // ------------------------------------------------------------------ host side
 
-template <bool A_MN, bool B_MN, int BN, int EPI, int CG>
+template <bool A_MN, bool B_MN, int BN, int EPI, int CGX>
 static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                           const CUtensorMap& mx, const GemmLaunch& args, cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI, CG>;
+  constexpr int CG = CGX == 4 ? 2 : CGX;
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI, CGX>;
   const int smem = GemmSmem<BN, EPI, CG>::kDynamic;
   if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem) != cudaSuccess)
     return kErrCuda;
-  // tiles of CG*128 rows; a device-side total (-1) gets the full persistent grid
-  const int units = args.total_tiles >= 0 ? args.total_tiles / CG : num_sms();
-  int grid = CG * (units < num_sms() / CG ? units : num_sms() / CG);
+  // work units: tiles of CG*128 rows (CGX = 4: pairs of N tiles); a device-side total (-1)
+  // gets the full persistent grid.  Clusters of 4 need 4 SMs of one GPC each: the grid is
+  // what fits co-resident (cudaOccupancyMaxActiveClusters, once per device).
+  int max_units = num_sms() / CGX;
+  if (CGX == 4) {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cached[dev & 63] == 0) {
+      cudaLaunchConfig_t oc = {};
+      oc.gridDim = dim3(num_sms());
+      oc.blockDim = dim3(gemm_threads<EPI>());
+      oc.dynamicSmemBytes = smem;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = 4;
+      ca[0].val.clusterDim.y = 1;
+      ca[0].val.clusterDim.z = 1;
+      oc.attrs = ca;
+      oc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(kern), &oc) !=
+              cudaSuccess ||
+          n <= 0)
+        n = num_sms() / 4;
+      cached[dev & 63] = n;
+    }
+    max_units = cached[dev & 63];
+  }
+  const int units = args.total_tiles >= 0 ? args.total_tiles / CGX : num_sms();
+  int grid = CGX * (units < max_units ? units : max_units);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(gemm_threads<EPI>());
@@ -746,7 +805,7 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   }();
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CGX;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   // programmatic dependent launch: this GEMM's CTAs may start their prologue while the
@@ -827,12 +886,14 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   const int BN = args.bn == 128 ? 128 : 256;
   if (args.total_tiles == 0) return kOk;
   if (args.ldc % 32 != 0) return kErrDimension;
-  const int cg = args.cta_group == 2 ? 2 : 1;
+  const int cg = args.cta_group == 4 ? 4 : args.cta_group == 2 ? 2 : 1;
+  if (cg == 4 && (BN != 256 || !args.n_fast || args.n_tiles % 2 != 0 || args.sched != nullptr))
+    return kErrDimension;  // A multicast: N-fastest pairs of 256-wide N tiles, static order
   CUtensorMap ma, mb, mc, mx;
   // K-major operand: box = {64 K elems, rows};  MN-major: box = {64 MN elems, 64 K rows}
   int rc = make_tmap_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM, kDtBF16, 128);
   if (rc != kOk) return rc;
-  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / cg, kDtBF16, 128);
+  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / (cg == 4 ? 2 : cg), kDtBF16, 128);
   if (rc != kOk) return rc;
   rc = epilogue_tmap(epi, args.c, args.ldc, c_rows, &mc);
   if (rc != kOk) return rc;
@@ -848,6 +909,7 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
     if (cg == 2) return dispatch_major<128, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
     return dispatch_major<128, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
   }
+  if (cg == 4) return dispatch_major<256, 4>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
   if (cg == 2) return dispatch_major<256, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
   return dispatch_major<256, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
 }

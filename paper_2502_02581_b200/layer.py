@@ -995,6 +995,9 @@ class FssdpMoE:
     _dyn = os.environ.get("FSSDP_GEMM_DYN", "0")
     GEMM_DYN = (set(("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2")) if _dyn == "1"
                 else set() if _dyn == "0" else set(_dyn.split(",")))
+    # A-tile multicast across two CTA pairs (FSSDP_GEMM_MULTICAST): these GEMMs, where
+    # eligible (N-fastest, CTA pairs, 256-wide N tiles, even n_tiles)
+    GEMM_MC = set(x for x in os.environ.get("FSSDP_GEMM_MC", "").split(",") if x)
 
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
@@ -1019,6 +1022,9 @@ class FssdpMoE:
         if total == 0:
             return
         flags = (1 if self.N_FASTEST.get(name, False) else 0) | self._gemm_flags[name]
+        if name in self.GEMM_MC and flags & 1 and flags & ops.GEMM_CTA_PAIR and \
+                not flags & ops.GEMM_BN128 and n_tiles % 2 == 0 and name not in self.GEMM_DYN:
+            flags |= ops.GEMM_MULTICAST
         maps = ops._ptr(self.dest_maps.get(name))
         self._timed("gemm." + name, lambda: N.call(
             "fssdp_grouped_gemm", int(a_mn), int(b_mn), epi, ops._ptr(a), a.shape[1], a.shape[0],

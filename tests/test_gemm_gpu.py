@@ -515,3 +515,51 @@ def test_dynamic_tile_scheduler_equals_static_order(pair):
         outs.append(C)
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     assert not ops._SCHED[torch.device(dev).index or 0].any()
+
+
+@pytest.mark.parametrize("case", ["bf16", "gelu", "dgelu_mnB", "bf16_mnB", "swiglu", "dswiglu"])
+def test_multicast_clusters_equal_pairs(case):
+    """FSSDP_GEMM_MULTICAST (clusters of two CTA pairs sharing the A tile through TMA
+    multicast) computes every tile the same way as the plain pair kernel: bit-identical
+    outputs, over groups of different M (incl. empty ones) and an odd number of cluster
+    tiles per group row."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(13)
+    K = 512
+    N = 1536 if case in ("bf16", "bf16_mnB") else 1024  # 6 / 4 N tiles
+    m_tiles = [2, 6, 0, 4, 2, 10]
+    R = sum(m_tiles) * 128
+    G = len(m_tiles)
+    A = torch.randn(R, K, device=dev).bfloat16()
+    b_mn = case in ("dgelu_mnB", "bf16_mnB", "dswiglu")
+    if b_mn:  # B [G*K, N]: N contiguous (dgrad-style)
+        B = (torch.randn(G * K, N, device=dev) / K ** 0.5).bfloat16()
+    else:
+        B = (torch.randn(G * N, K, device=dev) / K ** 0.5).bfloat16()
+    cw = 2 * N if case == "dswiglu" else N  # dSwiGLU writes [da1 | da3] (2 x the GEMM's N)
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        if b_mn:
+            rows.append((mt, r0, 0, 0, g * K, K // 64, r0 * cw))
+        else:
+            rows.append((mt, r0, 0, g * N, 0, K // 64, r0 * cw))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    epi = {"bf16": ops.EPI_BF16, "bf16_mnB": ops.EPI_BF16, "gelu": ops.EPI_GELU,
+           "dgelu_mnB": ops.EPI_DGELU, "swiglu": ops.EPI_SWIGLU, "dswiglu": ops.EPI_DSWIGLU}[case]
+    aux = torch.randn(R, cw, device=dev).bfloat16() if case in ("dgelu_mnB", "dswiglu") else None
+    outs = []
+    for mc in (False, True, True):
+        C = torch.zeros(R, cw, device=dev, dtype=torch.bfloat16)
+        C2 = (torch.zeros(R, N // 2 if case == "swiglu" else N, device=dev, dtype=torch.bfloat16)
+              if case in ("gelu", "swiglu") else None)
+        ops.grouped_gemm(A, False, B, b_mn, gd, ng, N // 256, total, C, cw, epilogue=epi, c2=C2,
+                         aux=aux, n_fastest=True, cta_pair=True, multicast=mc)
+        torch.cuda.synchronize()
+        outs.append((C, C2))
+    for C, C2 in outs[1:]:
+        assert torch.equal(C, outs[0][0])
+        if C2 is not None:
+            assert torch.equal(C2, outs[0][1])
+    assert outs[0][0].abs().sum() > 0
