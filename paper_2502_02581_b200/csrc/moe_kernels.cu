@@ -766,7 +766,18 @@ __global__ void __launch_bounds__(256)
   if (i >= static_cast<int64_t>(E) * d) return;
   const int e = static_cast<int>(i % E), col = static_cast<int>(i / E);
   float acc = 0.f;
-  for (int s = 0; s < splits; ++s) {
+  int s = 0;
+  for (; s + 6 <= splits; s += 6) {  // 12 independent loads in flight, summed in order
+    float v[6];
+#pragma unroll
+    for (int u = 0; u < 6; ++u) {
+      const float* row = c + (static_cast<int64_t>(s + u) * d + col) * kGateN;
+      v[u] = __fadd_rn(__ldcs(row + e), __ldcs(row + E + e));
+    }
+#pragma unroll
+    for (int u = 0; u < 6; ++u) acc = __fadd_rn(acc, v[u]);
+  }
+  for (; s < splits; ++s) {
     const float* row = c + (static_cast<int64_t>(s) * d + col) * kGateN;
     acc = __fadd_rn(acc, __fadd_rn(row[e], row[E + e]));
   }
@@ -2209,8 +2220,9 @@ int fssdp_gate_wgrad_tc(const void* x, const int32_t* topk_idx, const float* dlo
   float* c = reinterpret_cast<float*>(w8 + 4096 + rows * kGateN * 2);
   cudaStream_t s = as_stream(stream);
   const int64_t n16 = rows * kGateN / 8;
-  const int pb = static_cast<int>((n16 + 255) / 256 < 2 * num_sms() ? (n16 + 255) / 256
-                                                                     : 2 * num_sms());
+  // one 16-byte vector per thread: every thread's two dependent loads in flight at once
+  const int pb = static_cast<int>((n16 + 255) / 256 < 16 * num_sms() ? (n16 + 255) / 256
+                                                                      : 16 * num_sms());
   timing_begin(s);
   gate_wgrad_prep_kernel<<<pb > 0 ? pb : 1, 256, 0, s>>>(topk_idx, dlogit, T, rows, E, k,
                                                        d_model, splits, ks, g, groups);

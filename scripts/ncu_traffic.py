@@ -26,7 +26,8 @@ def main(path, out_path):
             "dram_bytes": float(r[rd].replace(",", "")) * scale[units[rd]] +
                           float(r[wr].replace(",", "")) * scale[units[wr]],
             "us": float(r[t].replace(",", "")) * tscale[units[t]]})
-    gemm = [x for x in kernels if "grouped_gemm" in x["kernel"]]
+    # the expert GEMMs (not the gate's tcgen05 GEMMs: fp32 epilogue with 128-wide N tiles)
+    gemm = [x for x in kernels if "grouped_gemm" in x["kernel"] and ", 128, 3," not in x["kernel"]]
     out = {"source": path, "kernels": kernels,
            "gemm_dram_bytes_per_step": sum(x["dram_bytes"] for x in gemm),
            "gemm_launches": len(gemm)}

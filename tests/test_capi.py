@@ -41,3 +41,18 @@ def test_errors_map_to_reference_taxonomy():
         assert "num_devices > 0" in str(exc)
     else:
         raise AssertionError("expected DimensionError")
+
+
+def test_binding_argument_counts_match_the_header():
+    """Every ctypes signature in _native.py has exactly the header's parameter count (an
+    ABI change on one side only would pass garbage through the boundary)."""
+    import re
+
+    text = re.sub(r"/\*.*?\*/", "", N.HEADER.read_text(), flags=re.S)
+    decls = re.findall(r"^\s*(?:int64_t|int|const char\*)\s+(fssdp_\w+)\s*\(([^;]*?)\)\s*;",
+                       text, re.M | re.S)
+    assert len(decls) >= 30
+    for name, params in decls:
+        p = params.strip()
+        n = 0 if p in ("", "void") else p.count(",") + 1
+        assert len(N._SIGS[name]) == n, f"{name}: header {n} params, binding {len(N._SIGS[name])}"
