@@ -318,6 +318,10 @@ typedef struct fssdp_gemm_group {
  * clusters of two CTA pairs on N tiles (2j, 2j+1) of one M tile; the A tile is loaded once
  * and multicast into both pairs (half the A operand's L2 -> SM traffic). */
 #define FSSDP_GEMM_MULTICAST 8
+/* Static order with CTA pairs and 256-wide N tiles (not the SwiGLU epilogues): when the
+ * last round of tiles would leave more than half the CTA pairs idle, its tiles run as two
+ * 256 x 128 halves each (same results; the short round takes half a tile's time). */
+#define FSSDP_GEMM_SPLIT_TAIL 16
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,

@@ -317,6 +317,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.total_tiles = total_tiles;
   args.n_fast = (flags & FSSDP_GEMM_N_FASTEST) ? 1 : 0;
   args.cta_group = (flags & FSSDP_GEMM_CTA_PAIR) ? 2 : 1;
+  args.split_tail = (flags & FSSDP_GEMM_SPLIT_TAIL) ? 1 : 0;
   if (flags & FSSDP_GEMM_MULTICAST) {
     if (args.cta_group != 2 || !(flags & FSSDP_GEMM_N_FASTEST) || (flags & FSSDP_GEMM_BN128) ||
         n_tiles % 2 != 0 || tile_sched != nullptr) {

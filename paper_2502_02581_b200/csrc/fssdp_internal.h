@@ -42,6 +42,7 @@ struct GemmLaunch {
   const __nv_bfloat16* aux;  // DGeLU: pre-activation, same layout as c
   const void* c_dest_maps;   // device CUtensorMap[] for groups with c_dest > 0 (nullable)
   int* sched;                // device int32[2] tile / exit counters, zero (nullable: static order)
+  int split_tail;            // static order: a short last round runs as 256 x 128 half tiles
 };
 
 int num_sms();

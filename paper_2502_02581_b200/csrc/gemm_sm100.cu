@@ -296,6 +296,25 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                  args.groups[args.num_groups - 1].m_tiles * args.n_tiles) / (CG * CL);
 
   const bool dyn = CL == 1 && args.sched != nullptr;
+  // Tail split (args.split_tail): when the static order's last round would leave most CTA
+  // pairs idle (0 < total % units <= units / 2 — e.g. cfg2's fwd2: 544 tiles on 74 pairs),
+  // each of its tiles runs as two 256 x 128 halves spread over the idle pairs, so the last
+  // round takes half a tile's time.  Work item i < split_from is tile i; after it, items
+  // come in (half 0, half 1) pairs of one tile.
+  constexpr bool kSplitOk =
+      CG == 2 && CL == 1 && BN == 256 && EPI != kEpiSwiglu && EPI != kEpiDSwiglu;
+  const int rem = units > 0 ? total % units : 0;
+  const bool split = kSplitOk && args.split_tail != 0 && !dyn && rem > 0 && 2 * rem <= units;
+  const int split_from = split ? total - rem : total;
+  const int n_items = split ? total + rem : total;
+  auto item_tile = [&](int item, int& half) -> int {
+    if (item < split_from) {
+      half = -1;
+      return item;
+    }
+    half = (item - split_from) & 1;
+    return split_from + ((item - split_from) >> 1);
+  };
   // consumer side of the scheduler ring: entry `it` -> tile id (-1: no more work); the
   // entry is released on the leader (remote arrive from the follower CTA)
   auto sched_take = [&](int it) -> int {
@@ -319,7 +338,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   auto next_tile = [&](int it) -> int {
     if (!dyn) {
       const int t = snake_tile(it, unit, units);
-      return t < total ? t : -1;
+      return t < n_items ? t : -1;
     }
     return sched_take(it);
   };
@@ -387,12 +406,16 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           tile = next_tile(it);
         }
         if (tile < 0) break;
+        int half;
+        const int tl = item_tile(tile, half);
         const TileCoord tc =
-            locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
+            locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tl, gcur,
                                 pair);
         const GemmGroup& g = groups[tc.group];
         const int m0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * kBM;
-        const int n0 = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * kBNc;
+        // a half tile's MMA reads the first kBNc / 2 staged B rows of each CTA
+        const int n0 = g.b_n + tc.n_tile * BN + (half > 0 ? BN / 2 : 0) +
+                       static_cast<int>(rank) * (half >= 0 ? kBNc / 2 : kBNc);
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           PROF_T0(tw);
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -459,14 +482,19 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       PROF_T0(tm0);
       constexpr uint32_t idesc =
           make_idesc_bf16(CG * kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+      constexpr uint32_t idesc_half =
+          make_idesc_bf16(CG * kBM, BN / 2, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       int gcur = 0;
       for (int it = 0;; ++it) {
-        const int tile = next_tile(it);
-        if (tile < 0) break;
+        const int item = next_tile(it);
+        if (item < 0) break;
+        int half;
+        const int tile = item_tile(item, half);
+        const uint32_t tdesc = half >= 0 ? idesc_half : idesc;
         const TileCoord tc =
             locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
                                 pair);
@@ -496,9 +524,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             else
               bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
             if (CG == 2)
-              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
+              umma_bf16_pair(d_tmem, adesc, bdesc, tdesc, (kb | kk) ? 1u : 0u);
             else
-              umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
+              umma_bf16(d_tmem, adesc, bdesc, tdesc, (kb | kk) ? 1u : 0u);
           }
           // frees the smem slot (in both CTAs; CL = 2: in all four) when these MMAs finish
           if (CG == 2)
@@ -550,13 +578,17 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       if (lane == 0) tile = next_tile(it);
       tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile < 0) break;
+      int half;
+      const int tl = item_tile(tile, half);
       const TileCoord tc =
-          locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
+          locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tl, gcur,
                                 pair);
       const GemmGroup& g = groups[tc.group];
       const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM) +
                        static_cast<int>(rank) * kBM + q * 32;
-      const int col0 = tc.n_tile * BN;
+      const int col0 = tc.n_tile * BN + (half > 0 ? BN / 2 : 0);
+      // chunks this warp drains: a half tile has kChunks / 2 (in its first TMEM columns)
+      const int cw_end = half < 0 ? kCW : min(kCW, max(0, kChunks / 2 - cbase));
       const bool zero = g.k_blocks == 0;
       // destination: C, or (c_dest > 0) a tensor map in global memory — e.g. a peer's
       // staging slot, so the store itself is the NVLink transfer
@@ -575,14 +607,24 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       };
       if (kAux && lane == 0) {  // prefetch the first aux tiles of this tile
         fence_proxy_async_smem();
-        for (int p = 0; p < kAB - 1 && p < kCW; ++p) aux_load((gchunk + p) % kAB, cbase + p);
+        for (int p = 0; p < kAB - 1 && p < cw_end; ++p) aux_load((gchunk + p) % kAB, cbase + p);
       }
       PROF_T0(ta);
       mbar_wait(&tfull_bar[acc], acc_phase);
       if (ew == 0 && lane == 0) PROF_ADD(5, ta);
       tc_fence_after();
+      if (cw_end == 0) {  // nothing of this half tile to drain: release TMEM right away
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2 && !leader)
+            mbar_arrive_leader(&tempty_bar[acc]);
+          else
+            mbar_arrive(&tempty_bar[acc]);
+        }
+      }
 #pragma unroll 1
-      for (int ci = 0; ci < kCW; ++ci, ++gchunk) {
+      for (int ci = 0; ci < cw_end; ++ci, ++gchunk) {
         const int c = cbase + ci;
         const int b = static_cast<int>(gchunk % S::kSets);
         uint32_t r[32], r3[32];
@@ -596,7 +638,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = r3[i] = 0u;
         }
-        if (ci == kCW - 1) {  // this warp's share of the accumulator read: release TMEM
+        if (ci == cw_end - 1) {  // this warp's share of the accumulator read: release TMEM
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -608,7 +650,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         }
         __nv_bfloat162 pre[16], pre3[16];
         if (kAux) {
-          if (lane == 0 && ci + kAB - 1 < kCW) {  // keep kAB-1 aux entries in flight
+          if (lane == 0 && ci + kAB - 1 < cw_end) {  // keep kAB-1 aux entries in flight
             fence_proxy_async_smem();
             aux_load((gchunk + kAB - 1) % kAB, c + kAB - 1);
           }

@@ -998,6 +998,9 @@ class FssdpMoE:
     # A-tile multicast across two CTA pairs (FSSDP_GEMM_MULTICAST): these GEMMs, where
     # eligible (N-fastest, CTA pairs, 256-wide N tiles, even n_tiles)
     GEMM_MC = set(x for x in os.environ.get("FSSDP_GEMM_MC", "").split(",") if x)
+    # short last rounds as half tiles (FSSDP_GEMM_SPLIT_TAIL; the kernel applies it only
+    # where eligible and useful)
+    SPLIT_TAIL = set(x for x in os.environ.get("FSSDP_SPLIT_TAIL", "").split(",") if x)
 
     def _call(self, name, *args):
         """One device entry point, CUDA-event-timed under its own name when profiling."""
@@ -1022,6 +1025,8 @@ class FssdpMoE:
         if total == 0:
             return
         flags = (1 if self.N_FASTEST.get(name, False) else 0) | self._gemm_flags[name]
+        if name in self.SPLIT_TAIL:
+            flags |= ops.GEMM_SPLIT_TAIL
         if name in self.GEMM_MC and flags & 1 and flags & ops.GEMM_CTA_PAIR and \
                 not flags & ops.GEMM_BN128 and n_tiles % 2 == 0 and name not in self.GEMM_DYN:
             flags |= ops.GEMM_MULTICAST

@@ -18,7 +18,7 @@ from .errors import DimensionError
 GATE_TILE = 64
 BM, BN, BK = 128, 256, 64
 EPI_BF16, EPI_GELU, EPI_DGELU, EPI_F32, EPI_SWIGLU, EPI_DSWIGLU = 0, 1, 2, 3, 4, 5
-GEMM_N_FASTEST, GEMM_CTA_PAIR, GEMM_BN128, GEMM_MULTICAST = 1, 2, 4, 8  # fssdp_grouped_gemm flags
+GEMM_N_FASTEST, GEMM_CTA_PAIR, GEMM_BN128, GEMM_MULTICAST, GEMM_SPLIT_TAIL = 1, 2, 4, 8, 16
 
 
 def _stream(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
@@ -60,7 +60,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
                  epilogue: int = EPI_BF16, c2: torch.Tensor | None = None,
                  aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
                  cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None,
-                 bn128: bool = False, dynamic: bool = False, multicast: bool = False) -> None:
+                 bn128: bool = False, dynamic: bool = False, multicast: bool = False,
+                 split_tail: bool = False) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
@@ -68,7 +69,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
     uint8 tensor of 128-byte tensor maps (epilogue_tmap) for groups with c_dest > 0.
     dynamic: tiles taken from a device counter (default: the static snake order, as the
     layer runs).  multicast: clusters of two CTA pairs sharing the A tile (needs cta_pair,
-    n_fastest, an even n_tiles)."""
+    n_fastest, an even n_tiles).  split_tail: a short last round of tiles runs as 256x128
+    halves (FSSDP_GEMM_SPLIT_TAIL)."""
     for t, nm in ((a, "A"), (b, "B")):
         _need(t, torch.bfloat16, nm)
         if t.dim() != 2:
@@ -79,7 +81,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
            a.shape[0], _ptr(b), b.shape[1], b.shape[0], _ptr(groups_dev), num_groups, n_tiles,
            total_tiles, _ptr(c), _ptr(c2), _ptr(aux), _ptr(c_dest_maps), ldc, c.numel() // ldc,
            (GEMM_N_FASTEST if n_fastest else 0) | (GEMM_CTA_PAIR if cta_pair else 0) |
-           (GEMM_BN128 if bn128 else 0) | (GEMM_MULTICAST if multicast else 0),
+           (GEMM_BN128 if bn128 else 0) | (GEMM_MULTICAST if multicast else 0) |
+           (GEMM_SPLIT_TAIL if split_tail else 0),
            _sched(a.device) if dynamic else None, _stream(stream))
 
 

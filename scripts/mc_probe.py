@@ -77,10 +77,11 @@ offs = np.concatenate([[0], np.cumsum(pad)[:-1]])
 Rp = int(sum(pad))
 Hp = torch.randn(Rp, f, device="cuda").bfloat16()
 Yp = torch.empty(Rp, d, device="cuda").bfloat16()
-for bn in (256, 128):
+for bn, st in ((256, False), (256, True), (128, False)):
     gz = groups([(pd // 128, int(o), 0, g * d, 0, f // 64, int(o) * d)
                  for g, (pd, o) in enumerate(zip(pad, offs))], d // bn)
     t = timeit(lambda: ops.grouped_gemm(Hp, False, W2, False, *gz[:2], d // bn, gz[2], Yp, d,
-                                        n_fastest=True, cta_pair=True, bn128=bn == 128))
-    print(f"fwd2 zipf-padded rows {Rp} BN {bn}: {t * 1e3:7.1f} us "
+                                        n_fastest=True, cta_pair=True, bn128=bn == 128,
+                                        split_tail=st))
+    print(f"fwd2 zipf-padded rows {Rp} BN {bn} split_tail {int(st)}: {t * 1e3:7.1f} us "
           f"{2 * sum(rows) * d * f / t / 1e9:7.1f} TF/s (routed)", flush=True)

@@ -563,3 +563,50 @@ def test_multicast_clusters_equal_pairs(case):
         if C2 is not None:
             assert torch.equal(C2, outs[0][1])
     assert outs[0][0].abs().sum() > 0
+
+
+@pytest.mark.parametrize("case", ["bf16", "gelu", "dgelu_mnB", "bf16_mnB"])
+def test_split_tail_equals_full_tiles(case):
+    """FSSDP_GEMM_SPLIT_TAIL: the short last round as 256x128 half tiles gives the same bits
+    as full tiles (shapes chosen so total pair tiles % pairs is in (0, pairs / 2] on a
+    148-SM B200)."""
+    from paper_2502_02581_b200 import _native as N
+
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(17)
+    K = 512
+    N_ = 2048 if case == "gelu" else 1024
+    m_tiles = [6, 8, 0, 4, 6] if case == "gelu" else [10, 14, 0, 16, 10]
+    pairs = int(N.LIB.fssdp_num_sms()) // 2
+    total_pairs = sum(m_tiles) // 2 * (N_ // 256)
+    assert 0 < total_pairs % pairs <= pairs // 2, (total_pairs, pairs)
+    R = sum(m_tiles) * 128
+    G = len(m_tiles)
+    A = torch.randn(R, K, device=dev).bfloat16()
+    b_mn = case in ("dgelu_mnB", "bf16_mnB")
+    if b_mn:
+        B = (torch.randn(G * K, N_, device=dev) / K ** 0.5).bfloat16()
+    else:
+        B = (torch.randn(G * N_, K, device=dev) / K ** 0.5).bfloat16()
+    rows, r0 = [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, 0 if b_mn else g * N_, g * K if b_mn else 0, K // 64, r0 * N_))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N_ // 256, dev)
+    epi = {"bf16": ops.EPI_BF16, "bf16_mnB": ops.EPI_BF16, "gelu": ops.EPI_GELU,
+           "dgelu_mnB": ops.EPI_DGELU}[case]
+    aux = torch.randn(R, N_, device=dev).bfloat16() if case == "dgelu_mnB" else None
+    outs = []
+    for st in (False, True, True):
+        C = torch.zeros(R, N_, device=dev, dtype=torch.bfloat16)
+        C2 = torch.zeros(R, N_, device=dev, dtype=torch.bfloat16) if case == "gelu" else None
+        ops.grouped_gemm(A, False, B, b_mn, gd, ng, N_ // 256, total, C, N_, epilogue=epi,
+                         c2=C2, aux=aux, n_fastest=True, cta_pair=True, split_tail=st)
+        torch.cuda.synchronize()
+        outs.append((C, C2))
+    for C, C2 in outs[1:]:
+        assert torch.equal(C, outs[0][0])
+        if C2 is not None:
+            assert torch.equal(C2, outs[0][1])
+    assert outs[0][0].abs().sum() > 0
