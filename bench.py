@@ -502,9 +502,10 @@ def run_ours(args):
     # SpRS: partials pushed into this rank's staging slots by the holders' wgrad epilogues
     # (NVLink, inside the GEMMs); the "sprs" kernel is the owner-side local reduction, which
     # reads every holder's partial (own slot + staging) and writes the sum
-    sprs_in = float(t.n_stage * layer.g.slot_grad_elems * 4)
+    gb = layer.g.grad_elem_bytes  # bf16 (default) or fp32 weight gradients
+    sprs_in = float(t.n_stage * layer.g.slot_grad_elems * gb)
     sprs_reduce_bytes = float(sum(int(c) + 1 for _, _, c in t.sprs_jobs) *
-                              layer.g.slot_grad_elems * 4)
+                              layer.g.slot_grad_elems * gb)
     host_ms = 1e3 * sum(timers.get("host_plan_s", [])) / args.steps
     allr = gather([gemm_ms, flops_rank, spag_ms, sprs_ms, spag_in, sprs_in, host_ms, ms,
                    sprs_reduce_bytes, rows_rank, float(t.recv_rows), float(t.n_slots)])
@@ -577,8 +578,9 @@ def run_ours(args):
             "spag_bottleneck_frac_of_nvlink": (gbs(rep.bottleneck_bytes, spag_max) or 0.0)
                                               / NVLINK_PEER_GBS,
             "a2a": a2a_stats(dec, allp, keys, world),
-            "note": "SpRS wire is fp32 partials pushed by the wgrad epilogue's TMA stores "
-                    "(2x the reference's expert_bytes pricing); sprs_ms is the local reduce. "
+            "note": f"SpRS wire is {layer.g.grad_dtype} partials pushed by the wgrad "
+                    "epilogue's TMA stores (bf16 = the reference's expert_bytes pricing); "
+                    "sprs_ms is the local reduce. "
                     "The early SpAG runs on the copy engines in two windows (W1 parts with the "
                     "gate, W2 parts beside fwd1 — sharing NVLink with the dispatch / GEMM "
                     "traffic); spag_ms sums both windows. Standalone SpAG / SpRS kernel "
