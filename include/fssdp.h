@@ -279,6 +279,9 @@ typedef struct fssdp_gemm_group {
   int32_t k_blocks;   /* number of 64-wide K blocks (0 => C tile written as zeros) */
   int32_t c_dest;     /* 0: C;  r + 1: the tensor c_dest_maps[r] (e.g. a peer's staging) */
   int64_t c_off;      /* element offset of the group's C[0, 0] in its destination */
+  int32_t rows;       /* real rows along M (0 = all m_tiles * 128): with
+                         FSSDP_GEMM_SWAP_TAIL the last M tile's padding is not computed */
+  int32_t reserved;   /* 0 */
 } fssdp_gemm_group;
 
 #define FSSDP_EPI_BF16 0  /* C = bf16(acc) */
@@ -322,6 +325,12 @@ typedef struct fssdp_gemm_group {
  * last round of tiles would leave more than half the CTA pairs idle, its tiles run as two
  * 256 x 128 halves each (same results; the short round takes half a tile's time). */
 #define FSSDP_GEMM_SPLIT_TAIL 16
+/* Token-side GEMMs (A K-major, CTA pairs, 256-wide N tiles; bf16, GeLU and dGeLU
+ * epilogues): a group's last M tile whose real rows (fssdp_gemm_group.rows) end within 192
+ * rows is computed with swapped operands (D^T = B^T A^T, N' = rows rounded up to 64), so
+ * the segment padding to 256 rows costs at most 63 rows of MMA work; rows past N' are not
+ * written. */
+#define FSSDP_GEMM_SWAP_TAIL 32
 int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void* a, int64_t a_inner,
                        int64_t a_outer, const void* b, int64_t b_inner, int64_t b_outer,
                        const fssdp_gemm_group* groups_dev, int32_t num_groups, int32_t n_tiles,

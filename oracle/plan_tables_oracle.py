@@ -102,6 +102,7 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     n = len(seg_start)
     shared = [False] * n if shared is None else [bool(x) for x in shared]
     k_rows = seg_padded if seg_rows is None else (np.asarray(seg_rows, dtype=np.int64) + 63) // 64 * 64
+    real = seg_padded if seg_rows is None else seg_rows  # token GEMMs: the real rows
     push = [None] * n if push is None else list(push)
     pslot = list(slot_of_seg) if param_slots is None else list(param_slots)
     out = {}
@@ -109,22 +110,26 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
     for i in range(n):
         s = pslot[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * f, 0, d // 64, 0, st * n1)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * f, 0, d // 64, 0, st * n1,
+                int(real[i]), 0)
     out["fwd1"] = _finalize(g.copy(), n1 // bn1)
     for i in range(n):
         s = pslot[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * d, 0, f // 64, 0, st * d)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, s * nm * d, 0, f // 64, 0, st * d,
+                int(real[i]), 0)
     out["fwd2"] = _finalize(g.copy(), d // 256)
     for i in range(n):  # dH = dY . W2  (B = W2 [K=d][N=f], MN-major)
         s = pslot[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * d, d // 64, 0, st * n1)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * d, d // 64, 0, st * n1,
+                int(real[i]), 0)
     out["dgrad2"] = _finalize(g.copy(), n_tiles_f(f))
     for i in range(n):  # dXe = dA . W1  (B = W1 / W13 [K=n1][N=d], MN-major)
         s = pslot[i]
         st = int(seg_start[i])
-        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * f, n1 // 64, 0, st * d)
+        g[i] = (int(seg_padded[i] // 128), 0, st, 0, 0, s * nm * f, n1 // 64, 0, st * d,
+                int(real[i]), 0)
     out["dgrad1"] = _finalize(g.copy(), d // 256)
     # each part longest-first (stable): the GEMM's snake tile order is then close to LPT
     order = (sorted([i for i in range(n) if shared[i]], key=lambda i: -int(seg_padded[i])) +
@@ -138,7 +143,7 @@ def gemm_groups(seg_start, seg_padded, slot_of_seg, d_model: int, d_ff: int, sha
             st = int(seg_start[i])
             dest, slot = (0, s) if push[i] is None else (push[i][0] + 1, push[i][1])
             gw[j] = (rows // 128, 0, 0, st, 0, st, int(k_rows[i] // 64), dest,
-                     slot * nm * f * d + extra)
+                     slot * nm * f * d + extra, 0, 0)
         head, _, t_sh = _finalize(gw[:n_sh], n_t)
         tail, _, t_rest = _finalize(gw[n_sh:], n_t)
         out[name] = (np.concatenate([head, tail]), n_t, t_sh + t_rest)

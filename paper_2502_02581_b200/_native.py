@@ -62,6 +62,8 @@ class GemmGroup(C.Structure):
         ("k_blocks", C.c_int32),
         ("c_dest", C.c_int32),
         ("c_off", C.c_int64),
+        ("rows", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

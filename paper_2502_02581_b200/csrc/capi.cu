@@ -310,7 +310,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
     set_error("grouped_gemm: epilogue needs c2/aux");
     return kErrDimension;
   }
-  GemmLaunch args;
+  GemmLaunch args = {};
   args.groups = groups_dev;
   args.num_groups = num_groups;
   args.n_tiles = n_tiles;
@@ -318,6 +318,7 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.n_fast = (flags & FSSDP_GEMM_N_FASTEST) ? 1 : 0;
   args.cta_group = (flags & FSSDP_GEMM_CTA_PAIR) ? 2 : 1;
   args.split_tail = (flags & FSSDP_GEMM_SPLIT_TAIL) ? 1 : 0;
+  args.swap_tail = (flags & FSSDP_GEMM_SWAP_TAIL) ? 1 : 0;
   if (flags & FSSDP_GEMM_MULTICAST) {
     if (args.cta_group != 2 || !(flags & FSSDP_GEMM_N_FASTEST) || (flags & FSSDP_GEMM_BN128) ||
         n_tiles % 2 != 0 || tile_sched != nullptr) {

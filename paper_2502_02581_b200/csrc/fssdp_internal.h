@@ -43,6 +43,8 @@ struct GemmLaunch {
   const void* c_dest_maps;   // device CUtensorMap[] for groups with c_dest > 0 (nullable)
   int* sched;                // device int32[2] tile / exit counters, zero (nullable: static order)
   int split_tail;            // static order: a short last round runs as 256 x 128 half tiles
+  int swap_tail;             // a group's short last M tile as a swapped-operand tile
+  CUtensorMap map_a32;       // swap_tail: A with 32-row boxes (only the tail's rows staged)
 };
 
 int num_sms();

@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
-                        const __grid_constant__ CUtensorMap map_x, GemmLaunch args) {
+                        const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ GemmLaunch args) {
   constexpr int CG = CGX == 4 ? 2 : CGX;  // CTAs per tile
   constexpr int CL = CGX == 4 ? 2 : 1;    // tiles (pairs) per cluster
   using S = GemmSmem<BN, EPI, CG>;
@@ -314,6 +315,21 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     }
     half = (item - split_from) & 1;
     return split_from + ((item - split_from) >> 1);
+  };
+  // Swapped tail tiles (args.swap_tail, token-side GEMMs: A = the token rows, K-major): the
+  // last M tile of a group whose real rows (GemmGroup.rows) end within its first 192 rows
+  // is computed as D^T = W . X^T — M' = the tile's 256 weight columns (the pair's B halves,
+  // staged in the A slots), N' = the real rows rounded up to 64 (staged in the B slots,
+  // N'/2 per CTA) — so the 256-row padding of the segment costs at most 63 rows of MMA
+  // work.  The epilogue stores the transposed accumulator through the same 32x32 boxes.
+  constexpr bool kSwapOk = CG == 2 && CL == 1 && !A_MN && BN == 256 && kEpiWarps == 4 &&
+                           (EPI == kEpiBF16 || EPI == kEpiGelu || EPI == kEpiDGelu);
+  auto swap_rows = [&](const TileCoord& tc, const GemmGroup& g, int half) -> int {
+    if (!kSwapOk || !args.swap_tail || half >= 0 || g.rows <= 0) return 0;
+    if (tc.m_tile != g.m_tiles / CG - 1) return 0;
+    const int tail = g.rows - tc.m_tile * (CG * kBM);
+    const int np = (tail + 63) / 64 * 64;
+    return tail > 0 && np <= 192 ? np : 0;
   };
   // consumer side of the scheduler ring: entry `it` -> tile id (-1: no more work); the
   // entry is released on the leader (remote arrive from the follower CTA)
@@ -416,16 +432,33 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         // a half tile's MMA reads the first kBNc / 2 staged B rows of each CTA
         const int n0 = g.b_n + tc.n_tile * BN + (half > 0 ? BN / 2 : 0) +
                        static_cast<int>(rank) * (half >= 0 ? kBNc / 2 : kBNc);
+        const int sw = swap_rows(tc, g, half);
+        // swapped: this CTA's N'/2 token rows of the tile (into its B slot)
+        const int sm0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * (sw / 2);
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           PROF_T0(tw);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           PROF_ADD(1, tw);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * S::kStageBytes);
+          // swapped tail: the weights fill the A slots, only N' token rows the B slots
+          if (leader)
+            mbar_arrive_expect_tx(&full_bar[stage], (kSwapOk && sw > 0)
+                                                        ? CG * S::kABytes + sw * kBK * 2
+                                                        : CG * S::kStageBytes);
           const int ka = g.a_k + kb * kBK;
           const int kbb = g.b_k + kb * kBK;
-          if (CG == 2) {
+          if (kSwapOk && sw > 0) {  // weights -> A slot, token rows -> B slot
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < kBNc / 64; ++j)
+                tma_load_2d_pair(sa + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
+            } else {
+              tma_load_2d_pair(sa, &map_b, &full_bar[stage], kbb, n0);
+            }
+            for (int j = 0; j < sw / 64; ++j)  // this CTA's sw / 2 rows, 32 per box
+              tma_load_2d_pair(sb + j * 32 * 128, &args.map_a32, &full_bar[stage], ka, sm0 + 32 * j);
+          } else if (CG == 2) {
             if (CL == 2) {  // the first pair loads A for both: CTA r -> CTAs r and r + 2
               if (pair == 0) {
                 const uint16_t mc = static_cast<uint16_t>(0x5u << rank);
@@ -494,11 +527,15 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         if (item < 0) break;
         int half;
         const int tile = item_tile(item, half);
-        const uint32_t tdesc = half >= 0 ? idesc_half : idesc;
         const TileCoord tc =
             locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
                                 pair);
         const int kblocks = groups[tc.group].k_blocks;
+        const int sw = swap_rows(tc, groups[tc.group], half);
+        // swapped: A' = the weights (B's majorness), B' = the token rows (K-major), N' = sw
+        const uint32_t tdesc = sw > 0 ? make_idesc_bf16(CG * kBM, static_cast<uint32_t>(sw),
+                                                        B_MN ? 1u : 0u, 0u)
+                               : half >= 0 ? idesc_half : idesc;
         PROF_T0(te);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         PROF_ADD(3, te);
@@ -523,6 +560,11 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               bdesc = make_sdesc_sw128(b_base + kk * 2048, kBK * 128, 1024);
             else
               bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
+            if (kSwapOk && sw > 0) {  // the A slot holds B's operand and vice versa
+              adesc = B_MN ? make_sdesc_sw128(a_base + kk * 2048, kBK * 128, 1024)
+                           : make_sdesc_sw128(a_base + kk * 32, 16, 1024);
+              bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
+            }
             if (CG == 2)
               umma_bf16_pair(d_tmem, adesc, bdesc, tdesc, (kb | kk) ? 1u : 0u);
             else
@@ -605,6 +647,92 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           tma_load_2d(dst, &map_x, &abar[entry], col0 + c * kEpiCols, row0);
         }
       };
+      const int sw = swap_rows(tc, g, half);
+      if (kSwapOk && sw > 0) {
+        // swapped tail tile: TMEM lane = output column wcol + lane, TMEM column = token row;
+        // each 32-row chunk is staged transposed ([row][col] as the normal path) and stored
+        // through the same 32x32 boxes
+        const int wcol = tc.n_tile * BN + static_cast<int>(rank) * kBNc + q * 32;
+        const int trow = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM);
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const int nch = sw / 32;
+#pragma unroll 1
+        for (int ci = 0; ci < nch; ++ci, ++gchunk) {
+          const int b = static_cast<int>(gchunk % S::kSets);
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                 static_cast<uint32_t>(acc * BN + ci * 32),
+                             r);
+          tmem_ld_wait();
+          if (ci == nch - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (!leader)
+                mbar_arrive_leader(&tempty_bar[acc]);
+              else
+                mbar_arrive(&tempty_bar[acc]);
+            }
+          }
+          float pre[32];
+          if (EPI == kEpiDGelu) {  // the saved gelu' box of these rows / columns
+            const int entry = static_cast<int>(gchunk % kAB);
+            uint8_t* ab = abuf0 + entry * kAT * S::kBufBytes;
+            if (lane == 0) {
+              fence_proxy_async_smem();
+              mbar_arrive_expect_tx(&abar[entry], S::kBufBytes);
+              tma_load_2d(ab, &map_x, &abar[entry], wcol, trow + ci * 32);
+            }
+            mbar_wait(&abar[entry], (aux_phase >> entry) & 1u);
+            aux_phase ^= 1u << entry;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              pre[j] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+                  ab + (static_cast<uint32_t>(sw64(j, lane >> 3)) + (lane & 7) * 2)));
+          }
+          if (lane == 0) bulk_wait_read<S::kSets - 1>();
+          __syncwarp();
+          uint8_t* cb = cbuf0 + b * kOT * S::kBufBytes;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float a0 = __uint_as_float(r[j]), a1 = __uint_as_float(r[j + 1]);
+            __nv_bfloat162 o, act;
+            if (EPI == kEpiGelu) {
+              uint64_t g2, d2;
+              gelu_and_grad2(f2_pack(a0, a1), g2, d2);
+              const float2 gf = f2_unpack(g2), df = f2_unpack(d2);
+              act = __floats2bfloat162_rn(gf.x, gf.y);
+              o = __floats2bfloat162_rn(df.x, df.y);
+            } else if (EPI == kEpiDGelu) {
+              const float2 v = f2_unpack(f2_mul(f2_pack(a0, a1), f2_pack(pre[j], pre[j + 1])));
+              o = __floats2bfloat162_rn(v.x, v.y);
+            } else {
+              o = __floats2bfloat162_rn(a0, a1);
+            }
+            const uint32_t o0 = static_cast<uint32_t>(sw64(j, lane >> 3)) + (lane & 7) * 2;
+            const uint32_t o1 = static_cast<uint32_t>(sw64(j + 1, lane >> 3)) + (lane & 7) * 2;
+            *reinterpret_cast<__nv_bfloat16*>(cb + o0) = o.x;
+            *reinterpret_cast<__nv_bfloat16*>(cb + o1) = o.y;
+            if (EPI == kEpiGelu) {
+              *reinterpret_cast<__nv_bfloat16*>(cb + S::kBufBytes + o0) = act.x;
+              *reinterpret_cast<__nv_bfloat16*>(cb + S::kBufBytes + o1) = act.y;
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(cmap, cb, wcol, trow + ci * 32);
+            if (EPI == kEpiGelu) tma_store_2d(&map_x, cb + S::kBufBytes, wcol, trow + ci * 32);
+            bulk_commit();
+          }
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       if (kAux && lane == 0) {  // prefetch the first aux tiles of this tile
         fence_proxy_async_smem();
         for (int p = 0; p < kAB - 1 && p < cw_end; ++p) aux_load((gchunk + p) % kAB, cbase + p);
@@ -935,6 +1063,11 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   // K-major operand: box = {64 K elems, rows};  MN-major: box = {64 MN elems, 64 K rows}
   int rc = make_tmap_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM, kDtBF16, 128);
   if (rc != kOk) return rc;
+  GemmLaunch la = args;
+  if (la.swap_tail && !a_mn) {  // 32-row boxes: a swapped tail stages only its rows
+    rc = make_tmap_2d(&la.map_a32, a, a_inner, a_outer, 64, 32, kDtBF16, 128);
+    if (rc != kOk) return rc;
+  }
   rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / (cg == 4 ? 2 : cg), kDtBF16, 128);
   if (rc != kOk) return rc;
   rc = epilogue_tmap(epi, args.c, args.ldc, c_rows, &mc);
@@ -948,12 +1081,12 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
                     epi == kEpiF32 ? 128 : 64);
   if (rc != kOk) return rc;
   if (BN == 128) {
-    if (cg == 2) return dispatch_major<128, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
-    return dispatch_major<128, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+    if (cg == 2) return dispatch_major<128, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
+    return dispatch_major<128, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
   }
-  if (cg == 4) return dispatch_major<256, 4>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
-  if (cg == 2) return dispatch_major<256, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
-  return dispatch_major<256, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, args, stream);
+  if (cg == 4) return dispatch_major<256, 4>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
+  if (cg == 2) return dispatch_major<256, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
+  return dispatch_major<256, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
 }
 
 #ifdef FSSDP_GEMM_PROFILE

@@ -427,6 +427,7 @@ __device__ void write_local_gemm_groups(const int32_t* __restrict__ tot, int E, 
       default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, e * nm * f * d + n1 * d}; break;
     }
     const bool wgrad = gi >= 4;
+    if (!wgrad) x.rows = c;  // the real rows (the last M tile's padding: FSSDP_GEMM_SWAP_TAIL)
     // m_tiles of a wgrad group = its output rows / 128 (the same for every expert)
     x.tile_start = static_cast<int32_t>((wgrad ? static_cast<int64_t>(rank_w) * x.m_tiles
                                                : before_tiles) * n_tiles[gi]);

@@ -1280,6 +1280,7 @@ int fssdp_build_rank_tables(int32_t rank, int32_t D, int32_t E, const int32_t* b
         case 4: x = {static_cast<int32_t>(n1 / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d}; break;
         default: x = {static_cast<int32_t>(d / 128), 0, 0, st, 0, st, kt, 0, s * nm * f * d + n1 * d}; break;
       }
+      if (!wgrad) x.rows = static_cast<int32_t>(seg_rows[rank][s]);  // the real rows
       if (wgrad) {  // a replica's partial goes to its owner's staging slot
         const int e = slot_expert[rank][s];
         const int o = base_owner[e];

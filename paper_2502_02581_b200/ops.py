@@ -19,6 +19,7 @@ GATE_TILE = 64
 BM, BN, BK = 128, 256, 64
 EPI_BF16, EPI_GELU, EPI_DGELU, EPI_F32, EPI_SWIGLU, EPI_DSWIGLU = 0, 1, 2, 3, 4, 5
 GEMM_N_FASTEST, GEMM_CTA_PAIR, GEMM_BN128, GEMM_MULTICAST, GEMM_SPLIT_TAIL = 1, 2, 4, 8, 16
+GEMM_SWAP_TAIL = 32
 
 
 def _stream(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
@@ -44,7 +45,7 @@ def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
 # fssdp_gemm_group (include/fssdp.h): c_dest 0 = C, r + 1 = c_dest_maps[r]
 GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
                         ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("c_dest", "<i4"),
-                        ("c_off", "<i8")])
+                        ("c_off", "<i8"), ("rows", "<i4"), ("reserved", "<i4")])
 
 
 def finalize_groups(groups_cpu: np.ndarray, n_tiles: int) -> int:
@@ -61,7 +62,7 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
                  aux: torch.Tensor | None = None, stream=None, n_fastest: bool = False,
                  cta_pair: bool = False, c_dest_maps: torch.Tensor | None = None,
                  bn128: bool = False, dynamic: bool = False, multicast: bool = False,
-                 split_tail: bool = False) -> None:
+                 split_tail: bool = False, swap_tail: bool = False) -> None:
     """C_g = A_g · B_g for every group (tcgen05 kernel, gemm_sm100.cu).
 
     a, b: 2-D bf16 tensors (the TMA view: [outer, inner], inner contiguous); c (and c2,
@@ -70,7 +71,8 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
     dynamic: tiles taken from a device counter (default: the static snake order, as the
     layer runs).  multicast: clusters of two CTA pairs sharing the A tile (needs cta_pair,
     n_fastest, an even n_tiles).  split_tail: a short last round of tiles runs as 256x128
-    halves (FSSDP_GEMM_SPLIT_TAIL)."""
+    halves (FSSDP_GEMM_SPLIT_TAIL).  swap_tail: a group's short last M tile (the `rows`
+    field) as a swapped-operand tile (FSSDP_GEMM_SWAP_TAIL)."""
     for t, nm in ((a, "A"), (b, "B")):
         _need(t, torch.bfloat16, nm)
         if t.dim() != 2:
@@ -82,7 +84,7 @@ def grouped_gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, group
            total_tiles, _ptr(c), _ptr(c2), _ptr(aux), _ptr(c_dest_maps), ldc, c.numel() // ldc,
            (GEMM_N_FASTEST if n_fastest else 0) | (GEMM_CTA_PAIR if cta_pair else 0) |
            (GEMM_BN128 if bn128 else 0) | (GEMM_MULTICAST if multicast else 0) |
-           (GEMM_SPLIT_TAIL if split_tail else 0),
+           (GEMM_SPLIT_TAIL if split_tail else 0) | (GEMM_SWAP_TAIL if swap_tail else 0),
            _sched(a.device) if dynamic else None, _stream(stream))
 
 

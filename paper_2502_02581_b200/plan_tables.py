@@ -21,7 +21,7 @@ from .errors import InternalError
 ROW_ALIGN = 256  # = the CTA-pair GEMM M tile (two 128-row halves)
 GROUP_DTYPE = np.dtype([("m_tiles", "<i4"), ("tile_start", "<i4"), ("a_m", "<i4"), ("a_k", "<i4"),
                         ("b_n", "<i4"), ("b_k", "<i4"), ("k_blocks", "<i4"), ("c_dest", "<i4"),
-                        ("c_off", "<i8")])
+                        ("c_off", "<i8"), ("rows", "<i4"), ("reserved", "<i4")])
 GEMM_NAMES = ("fwd1", "fwd2", "dgrad2", "dgrad1", "wgrad1", "wgrad2")
 
 
