@@ -319,6 +319,11 @@ int fssdp_grouped_gemm(int32_t a_mn, int32_t b_mn, int32_t epilogue, const void*
   args.cta_group = (flags & FSSDP_GEMM_CTA_PAIR) ? 2 : 1;
   args.split_tail = (flags & FSSDP_GEMM_SPLIT_TAIL) ? 1 : 0;
   args.swap_tail = (flags & FSSDP_GEMM_SWAP_TAIL) ? 1 : 0;
+  static const int tail_last = [] {  // experiment: swapped tails after every full tile
+    const char* v = getenv("FSSDP_GEMM_TAIL_LAST");
+    return v != nullptr && v[0] == '1' ? 1 : 0;
+  }();
+  args.tail_last = tail_last;
   if (flags & FSSDP_GEMM_MULTICAST) {
     if (args.cta_group != 2 || !(flags & FSSDP_GEMM_N_FASTEST) || (flags & FSSDP_GEMM_BN128) ||
         n_tiles % 2 != 0 || tile_sched != nullptr) {

@@ -44,6 +44,7 @@ struct GemmLaunch {
   int* sched;                // device int32[2] tile / exit counters, zero (nullable: static order)
   int split_tail;            // static order: a short last round runs as 256 x 128 half tiles
   int swap_tail;             // a group's short last M tile as a swapped-operand tile
+  int tail_last;             // swap_tail: the tail tiles after every full tile (experiment)
   CUtensorMap map_a32;       // swap_tail: A with 32-row boxes (only the tail's rows staged)
 };
 

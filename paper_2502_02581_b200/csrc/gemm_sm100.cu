@@ -324,12 +324,69 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   // work.  The epilogue stores the transposed accumulator through the same 32x32 boxes.
   constexpr bool kSwapOk = CG == 2 && CL == 1 && !A_MN && BN == 256 && kEpiWarps == 4 &&
                            (EPI == kEpiBF16 || EPI == kEpiGelu || EPI == kEpiDGelu);
-  auto swap_rows = [&](const TileCoord& tc, const GemmGroup& g, int half) -> int {
-    if (!kSwapOk || !args.swap_tail || half >= 0 || g.rows <= 0) return 0;
-    if (tc.m_tile != g.m_tiles / CG - 1) return 0;
-    const int tail = g.rows - tc.m_tile * (CG * kBM);
+  auto tail_rows = [&](const GemmGroup& g) -> int {  // N' of the group's tail, 0: none
+    if (!kSwapOk || !args.swap_tail || g.rows <= 0 || g.m_tiles < CG) return 0;
+    const int tail = g.rows - (g.m_tiles / CG - 1) * (CG * kBM);
     const int np = (tail + 63) / 64 * 64;
     return tail > 0 && np <= 192 ? np : 0;
+  };
+  auto swap_rows = [&](const TileCoord& tc, const GemmGroup& g, int half) -> int {
+    if (!kSwapOk || half >= 0 || tc.m_tile != g.m_tiles / CG - 1) return 0;
+    return tail_rows(g);
+  };
+  // Tails last (args.tail_last, static order with swapped tails): every group's full tiles
+  // first (group order, N-fastest inside a group), then the groups' tail tiles, so the
+  // order's last round(s) are the cheap tail tiles.  Measured 0.5 % SLOWER per step at cfg2
+  // (each tail re-reads its weight tiles long after the group's other tiles), neutral at
+  // cfg4: off by default (FSSDP_GEMM_TAIL_LAST=1).
+  const bool tail_order = kSwapOk && args.swap_tail != 0 && args.tail_last != 0 && !dyn && !split;
+  int n_tail_tiles = 0;
+  if (tail_order) {  // every warp counts (all threads are here)
+    int c = 0;
+    for (int i = lane; i < args.num_groups; i += 32) c += tail_rows(groups[i]) > 0 ? 1 : 0;
+    n_tail_tiles = __reduce_add_sync(0xffffffffu, c) * args.n_tiles;
+  }
+  const int total_full = total - n_tail_tiles;
+  struct TailCursor {
+    int g = 0, base = 0, gt = 0, tbase = 0;
+  };
+  // tile id -> coordinates (and N' of a swapped tile) in either order; ids increase per role
+  auto locate = [&](int tl, int half, int& gcur, TailCursor& tcur, int& sw) -> TileCoord {
+    if (!tail_order) {
+      const TileCoord tc = locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles,
+                                               args.n_fast, tl, gcur, pair);
+      sw = swap_rows(tc, groups[tc.group], half);
+      return tc;
+    }
+    const int nt = args.n_tiles;
+    TileCoord tc;
+    if (tl < total_full) {
+      for (;;) {
+        const GemmGroup& gg = groups[tcur.g];
+        const int ft = (gg.m_tiles / CG - (tail_rows(gg) > 0 ? 1 : 0)) * nt;
+        if (tl < tcur.base + ft) break;
+        tcur.base += ft;
+        ++tcur.g;
+      }
+      const int local = tl - tcur.base;
+      tc.group = tcur.g;
+      tc.m_tile = local / nt;
+      tc.n_tile = local % nt;
+      sw = 0;
+    } else {
+      const int u = tl - total_full;
+      for (;;) {
+        const int tt = tail_rows(groups[tcur.gt]) > 0 ? nt : 0;
+        if (u < tcur.tbase + tt) break;
+        tcur.tbase += tt;
+        ++tcur.gt;
+      }
+      tc.group = tcur.gt;
+      tc.m_tile = groups[tcur.gt].m_tiles / CG - 1;
+      tc.n_tile = u - tcur.tbase;
+      sw = tail_rows(groups[tcur.gt]);
+    }
+    return tc;
   };
   // consumer side of the scheduler ring: entry `it` -> tile id (-1: no more work); the
   // entry is released on the leader (remote arrive from the follower CTA)
@@ -366,6 +423,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       int gcur = 0;  // group cursor (locate_tile)
+      TailCursor tcur;
       // The pair's scheduler (leader producer): entry it + 1 is published while tile `it`
       // is being loaded, so the peer CTA's producer never waits for a tile id at a tile
       // boundary, and one atomic is always in flight (its round trip overlaps the loads).
@@ -424,15 +482,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         if (tile < 0) break;
         int half;
         const int tl = item_tile(tile, half);
-        const TileCoord tc =
-            locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tl, gcur,
-                                pair);
+        int sw;
+        const TileCoord tc = locate(tl, half, gcur, tcur, sw);
         const GemmGroup& g = groups[tc.group];
         const int m0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * kBM;
         // a half tile's MMA reads the first kBNc / 2 staged B rows of each CTA
         const int n0 = g.b_n + tc.n_tile * BN + (half > 0 ? BN / 2 : 0) +
                        static_cast<int>(rank) * (half >= 0 ? kBNc / 2 : kBNc);
-        const int sw = swap_rows(tc, g, half);
         // swapped: this CTA's N'/2 token rows of the tile (into its B slot)
         const int sm0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * (sw / 2);
         for (int kb = 0; kb < g.k_blocks; ++kb) {
@@ -522,16 +578,15 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int gcur = 0;
+      TailCursor tcur;
       for (int it = 0;; ++it) {
         const int item = next_tile(it);
         if (item < 0) break;
         int half;
         const int tile = item_tile(item, half);
-        const TileCoord tc =
-            locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tile, gcur,
-                                pair);
+        int sw;
+        const TileCoord tc = locate(tile, half, gcur, tcur, sw);
         const int kblocks = groups[tc.group].k_blocks;
-        const int sw = swap_rows(tc, groups[tc.group], half);
         // swapped: A' = the weights (B's majorness), B' = the token rows (K-major), N' = sw
         const uint32_t tdesc = sw > 0 ? make_idesc_bf16(CG * kBM, static_cast<uint32_t>(sw),
                                                         B_MN ? 1u : 0u, 0u)
@@ -612,6 +667,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     uint32_t acc_phase = 0;
     uint32_t gchunk = 0;  // running chunk counter (selects the staging set)
     int gcur = 0;
+    TailCursor tcur;
     PROF_T0(tep0);
     // aux / output column of f-space column j in the interleaved [a1|a3] layout (SwiGLU)
     auto a13_col = [](int j) { return 256 * (j >> 7) + (j & 127); };
@@ -622,9 +678,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       if (tile < 0) break;
       int half;
       const int tl = item_tile(tile, half);
-      const TileCoord tc =
-          locate_tile<CG, CL>(groups, args.num_groups, args.n_tiles, args.n_fast, tl, gcur,
-                                pair);
+      int sw;
+      const TileCoord tc = locate(tl, half, gcur, tcur, sw);
       const GemmGroup& g = groups[tc.group];
       const int row0 = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM) +
                        static_cast<int>(rank) * kBM + q * 32;
@@ -647,7 +702,6 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           tma_load_2d(dst, &map_x, &abar[entry], col0 + c * kEpiCols, row0);
         }
       };
-      const int sw = swap_rows(tc, g, half);
       if (kSwapOk && sw > 0) {
         // swapped tail tile: TMEM lane = output column wcol + lane, TMEM column = token row;
         // each 32-row chunk is staged transposed ([row][col] as the normal path) and stored
