@@ -977,7 +977,8 @@ class FssdpMoE:
 
     # experiment: where the dX combine and (N = 1) the gate backward run — "overlap" (dx
     # stream beside the remaining wgrads), "gate_end" (gate backward after them on the main
-    # stream), "serial" (both after them)
+    # stream), "serial" (both after them), "dx_first" (the dX combine on the main stream
+    # before them, the gate backward beside them)
     DX_MODE = os.environ.get("FSSDP_DX_MODE", "overlap")
     GATE_WGRAD_TC = os.environ.get("FSSDP_GATE_WGRAD_TC", "1") == "1"
 
@@ -1248,7 +1249,14 @@ class FssdpMoE:
         dxs = self._dx_stream()
         dxs.wait_stream(main)
         mode = self.DX_MODE
-        if mode != "serial":
+        if mode == "dx_first":  # dX combine on the main stream, the gate backward beside
+            self.phase_barrier(BAR_DX)
+            self.phase_combine_dx(dx)
+            if not self._early_gate:
+                dxs.wait_stream(main)
+                with self._on(dxs):
+                    self.phase_gate_wgrad()
+        elif mode != "serial":
             with self._on(dxs):
                 self.phase_barrier(BAR_DX)
                 self.phase_combine_dx(dx)
