@@ -607,19 +607,23 @@ class FssdpMoE:
     # (N=4, interleaved A/B: dispatch 103 -> 48 us, step 1.799 -> 1.756 ms)
     PRE_W2_CE = os.environ.get("FSSDP_PRE_W2_CE", "1") != "0"
 
-    def _launch_prefetch_w2_ce(self) -> None:
+    def _launch_prefetch_w2_ce(self, after=None) -> None:
         n1b = self.g.n1 * self.g.d_model * 2
-        self._pre_w2 = self._ce_copies(n1b, self.g.slot_param_bytes - n1b)
+        self._pre_w2 = self._ce_copies(n1b, self.g.slot_param_bytes - n1b, after)
 
-    def _ce_copies(self, part_off: int, part_bytes: int) -> torch.cuda.Event:
+    def _ce_copies(self, part_off: int, part_bytes: int, after=None) -> torch.cuda.Event:
         """The early SpAG's copies of one part of every slot, by the copy engines on their
-        own stream (after the current stream's work); returns their completion event.
-        The W1 part starts before any barrier of the step: it first waits until every
-        owner published this forward's epoch (its shards are final — phase_publish)."""
+        own stream (after the current stream's work, or after the event `after`); returns
+        their completion event.  The W1 part starts before any barrier of the step: it
+        first waits until every owner published this forward's epoch (its shards are final
+        — phase_publish)."""
         ce = getattr(self, "_ce", None)
         if ce is None:
             ce = self._ce = torch.cuda.Stream(device=self.dev)
-        ce.wait_stream(torch.cuda.current_stream(self.dev))
+        if after is not None:
+            ce.wait_event(after)
+        else:
+            ce.wait_stream(torch.cuda.current_stream(self.dev))
         if part_off == 0 and self._epochs_live():
             N.call_raw("fssdp_wait_epochs", self._pb(), self.flags_off, self.epoch_slot,
                        self.world, C.c_uint32(self._fwd_epoch & 0xFFFFFFFF),
@@ -642,12 +646,12 @@ class FssdpMoE:
         ev.record(ce)
         return ev
 
-    def _launch_prefetch_w2(self) -> None:
+    def _launch_prefetch_w2(self, after=None) -> None:
         if not getattr(self, "_pre_w2_pending", False):
             return
         self._pre_w2_pending = False
         if self.PRE_W2_CE:
-            self._launch_prefetch_w2_ce()
+            self._launch_prefetch_w2_ce(after)
             return
         side = self._side_stream()
         if self.PRE_W2_AFTER_DISPATCH:
@@ -1046,11 +1050,24 @@ class FssdpMoE:
             ops._ptr(c2), ops._ptr(aux), maps, ldc, c.numel() // ldc, flags,
             self._gemm_sched_ptr if name in self.GEMM_DYN else None, self._stream()))
 
+    # fwd1 is launched before the host issues the early SpAG's W2 copies (they still start
+    # after the dispatch: an event recorded before fwd1): issuing the copies first delayed
+    # fwd1's launch by the host time of the copy calls (N=4: a ~30 us GPU gap)
+    W2_AFTER_FWD1_LAUNCH = os.environ.get("FSSDP_W2_AFTER_FWD1_LAUNCH", "1") != "0"
+
     def phase_experts_fwd(self) -> None:
         f, d, n1 = self.g.d_ff, self.g.d_model, self.g.n1
-        self._launch_prefetch_w2()  # after the dispatch (and any late SpAG) in stream order
+        late = (self.W2_AFTER_FWD1_LAUNCH and self.PRE_W2_CE and
+                getattr(self, "_pre_w2_pending", False))
+        if late:
+            after = torch.cuda.Event()
+            after.record(torch.cuda.current_stream(self.dev))  # the dispatch (+ late SpAG)
+        else:
+            self._launch_prefetch_w2()  # after the dispatch (and any late SpAG) in stream order
         self._gemm("fwd1", self.xrecv, False, self.w1_view, False, self.gprime, n1, self.epi_fwd1,
                    c2=self.h)
+        if late:
+            self._launch_prefetch_w2(after)
         if self._pre_w2 is not None:  # the early replicas' W2 parts
             torch.cuda.current_stream(self.dev).wait_event(self._pre_w2)
             self._pre_w2 = None

@@ -34,15 +34,21 @@ def main():
 
     C = bench.CFG2
     T = C["tokens_per_gpu"]
-    dev = torch.device("cuda", 0)
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    if world > 1:  # torchrun: one rank per GPU, each profiles its own device
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
     layer = create_layer(C["d_model"], C["d_ff"], C["num_experts"], C["top_k"], T,
-                         F.Policy(F.PolicyKind.FSSDP, **bench.POLICY), device=dev, seed=1234,
-                         activation=C["activation"])
+                         F.Policy(F.PolicyKind.FSSDP, **bench.POLICY), rank=rank, world=world,
+                         device=dev, seed=1234, activation=C["activation"])
     E = C["num_experts"]
     p = 1.0 / np.arange(1, E + 1) ** bench.ZIPF_S
     p = p[np.random.default_rng(42).permutation(E)]
     layer.gate_bias.copy_(torch.tensor(np.log(p / p.sum()), dtype=torch.float32))
-    g = torch.Generator(device=dev).manual_seed(1000)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
     xs = [torch.randn(T, C["d_model"], device=dev, generator=g).bfloat16() for _ in range(4)]
     dys = [(torch.randn(T, C["d_model"], device=dev, generator=g) * 0.05).bfloat16()
            for _ in range(4)]
@@ -50,6 +56,7 @@ def main():
     def step(i):
         layer.forward(xs[i % 4])
         layer.backward(dys[i % 4])
+        layer.reduce_gate_grad()
         layer.planner.finish()
 
     if args.e2e:  # the bench's e2e pipeline (bench.py run_ours, e2e section)
@@ -120,10 +127,14 @@ def main():
             gaps += a - busy_end
         busy_end = max(busy_end, b)
     step_us = (ks[starts[-1]][0] - ks[starts[-2]][0]) if len(starts) > 1 else None
-    for a, b, n in rows:
-        print(f"{a:9.2f} {b:9.2f} {b - a:8.2f}  {n}")
-    print(json.dumps({"step_us": step_us, "idle_gaps_us": round(gaps, 2),
-                      "kernels": len(rows)}))
+    lines = [f"{a:9.2f} {b:9.2f} {b - a:8.2f}  {n}" for a, b, n in rows]
+    lines.append(json.dumps({"rank": rank, "step_us": step_us, "idle_gaps_us": round(gaps, 2),
+                             "kernels": len(rows)}))
+    if world == 1:
+        print("\n".join(lines))
+    else:  # one file per rank (gpurun_out/tl_dev_n{world}_r{rank}.txt)
+        with open(f"gpurun_out/tl_dev_n{world}_r{rank}.txt", "w") as fh:
+            fh.write("\n".join(lines) + "\n")
     if args.out:
         with open(args.out, "w") as fh:
             json.dump({"rows": rows, "step_us": step_us, "idle_gaps_us": gaps}, fh)

@@ -85,3 +85,17 @@ for bn, st in ((256, False), (256, True), (128, False)):
                                         split_tail=st))
     print(f"fwd2 zipf-padded rows {Rp} BN {bn} split_tail {int(st)}: {t * 1e3:7.1f} us "
           f"{2 * sum(rows) * d * f / t / 1e9:7.1f} TF/s (routed)", flush=True)
+
+# fwd1's shape (K = d = 1024, N = f = 4096) with each epilogue: what the GeLU outputs cost
+if os.environ.get("EPI_PROBE"):
+    for name, epi, c2 in (("bf16 (1 output)", ops.EPI_BF16, None), ("gelu (2 outputs)", ops.EPI_GELU, Hout),
+                          ("f32 (1 fp32 output)", ops.EPI_F32, None)):
+        Cf = torch.empty(R, f, device="cuda") if epi == ops.EPI_F32 else A
+        t = timeit(lambda: ops.grouped_gemm(X, False, W1, False, *gd1[:2], f // 256, gd1[2], Cf, f,
+                                            epi, c2=c2, n_fastest=True, cta_pair=True))
+        print(f"fwd1 shape, epilogue {name:20s} {t * 1e3:7.1f} us {flop / t / 1e9:7.1f} TF/s",
+              flush=True)
+    # and fwd2's shape (K = f = 4096, N = d = 1024), bf16
+    t = timeit(lambda: ops.grouped_gemm(H, False, W2, False, *gd2[:2], d // 256, gd2[2], Y, d,
+                                        n_fastest=True, cta_pair=True))
+    print(f"fwd2 shape, epilogue bf16 {t * 1e3:7.1f} us {flop / t / 1e9:7.1f} TF/s", flush=True)
