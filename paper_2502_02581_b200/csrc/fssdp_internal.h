@@ -46,6 +46,9 @@ struct GemmLaunch {
   int swap_tail;             // a group's short last M tile as a swapped-operand tile
   int tail_last;             // swap_tail: the tail tiles after every full tile (experiment)
   CUtensorMap map_a32;       // swap_tail: A with 32-row boxes (only the tail's rows staged)
+  int wide_store;            // BF16 / GeLU epilogues: 32 x 64 store boxes (128-byte rows)
+  CUtensorMap map_c64;       // wide_store: C with 32 x 64 boxes (SWIZZLE_128B)
+  CUtensorMap map_x64;       // wide_store, GeLU: the second output, same boxes
 };
 
 int num_sms();

@@ -58,6 +58,9 @@ constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
 #ifndef FSSDP_F32_SETS
 #define FSSDP_F32_SETS 2
 #endif
+#ifndef FSSDP_GELU_SETS
+#define FSSDP_GELU_SETS 2
+#endif
 template <int EPI>
 constexpr int epi_warps() {
   return EPI == FSSDP_EPI_GELU ? FSSDP_GELU_EPI_WARPS : 4;
@@ -87,7 +90,7 @@ struct GemmSmem {
                                    : EPI == kEpiDSwiglu ? 2 : 1;
   // staging sets per epilogue warp: chunk c uses set c % kSets and may reuse it once the
   // TMA store issued kSets chunks earlier has read it (fp32 outputs: FSSDP_F32_SETS)
-  static constexpr int kSets = EPI == kEpiF32 ? FSSDP_F32_SETS : 2;
+  static constexpr int kSets = EPI == kEpiF32 ? FSSDP_F32_SETS : EPI == kEpiGelu ? FSSDP_GELU_SETS : 2;
   static constexpr int kCBufs = kSets * kOutTiles;
   // aux-tile prefetch ring (dgrad2): entries of one tile (GeLU') or two (a1, a3)
   static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : EPI == kEpiDSwiglu ? 2 : 0;
@@ -324,6 +327,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   // work.  The epilogue stores the transposed accumulator through the same 32x32 boxes.
   constexpr bool kSwapOk = CG == 2 && CL == 1 && !A_MN && BN == 256 && kEpiWarps == 4 &&
                            (EPI == kEpiBF16 || EPI == kEpiGelu || EPI == kEpiDGelu);
+  constexpr bool kWideOk = (EPI == kEpiBF16 || EPI == kEpiGelu) && kEpiWarps == 4 &&
+                           S::kSets * S::kOutTiles * S::kBufBytes >= 4096 * S::kOutTiles;
   auto tail_rows = [&](const GemmGroup& g) -> int {  // N' of the group's tail, 0: none
     if (!kSwapOk || !args.swap_tail || g.rows <= 0 || g.m_tiles < CG) return 0;
     const int tail = g.rows - (g.m_tiles / CG - 1) * (CG * kBM);
@@ -666,6 +671,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t gchunk = 0;  // running chunk counter (selects the staging set)
+    bool wide_out = false;  // lane 0: a wide store may still be reading the staging sets
     int gcur = 0;
     TailCursor tcur;
     PROF_T0(tep0);
@@ -687,6 +693,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
       // chunks this warp drains: a half tile has kChunks / 2 (in its first TMEM columns)
       const int cw_end = half < 0 ? kCW : min(kCW, max(0, kChunks / 2 - cbase));
       const bool zero = g.k_blocks == 0;
+      // wide stores (args.wide_store): BF16 / GeLU outputs leave through 32 x 64 boxes of
+      // 128-byte rows — half the TMA store requests of the 32 x 32 boxes
+      const bool wide = kWideOk && args.wide_store != 0 && g.c_dest == 0 && (cw_end & 1) == 0;
       // destination: C, or (c_dest > 0) a tensor map in global memory — e.g. a peer's
       // staging slot, so the store itself is the NVLink transfer
       const CUtensorMap* cmap =
@@ -745,7 +754,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               pre[j] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
                   ab + (static_cast<uint32_t>(sw64(j, lane >> 3)) + (lane & 7) * 2)));
           }
-          if (lane == 0) bulk_wait_read<S::kSets - 1>();
+          if (lane == 0) {
+            if (wide_out)
+              bulk_wait_read<0>();
+            else
+              bulk_wait_read<S::kSets - 1>();
+          }
+          wide_out = false;
           __syncwarp();
           uint8_t* cb = cbuf0 + b * kOT * S::kBufBytes;
 #pragma unroll
@@ -850,8 +865,17 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           }
         }
         // the staging set b was last used kSets chunks ago: its TMA stores must have read it
-        if (lane == 0) bulk_wait_read<S::kSets - 1>();
-        __syncwarp();
+        // (wide stores: one 32 x 64 buffer per output, waited for below, after the math)
+        if (!wide) {
+          if (lane == 0) {
+            if (wide_out)  // a wide store (spanning both sets) may still be reading
+              bulk_wait_read<0>();
+            else
+              bulk_wait_read<S::kSets - 1>();
+          }
+          wide_out = false;
+          __syncwarp();
+        }
         uint8_t* cb = cbuf0 + b * kOT * S::kBufBytes;
         auto stage_bf16 = [&](uint8_t* dst, const __nv_bfloat162 (&v)[16]) {
 #pragma unroll
@@ -899,14 +923,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           stage_bf16(cb, d1);
           stage_bf16(cb + S::kBufBytes, d3);
         } else {
-          __nv_bfloat162 out[16];
+          __nv_bfloat162 out[16], act[16];
           if (EPI == kEpiBF16) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               out[i] = __floats2bfloat162_rn(__uint_as_float(r[2 * i]),
                                              __uint_as_float(r[2 * i + 1]));
           } else if (EPI == kEpiGelu) {
-            __nv_bfloat162 act[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {  // one tanh feeds both GeLU and GeLU'
               uint64_t g2, d2;
@@ -916,7 +939,6 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               act[i] = __floats2bfloat162_rn(gf.x, gf.y);
               out[i] = __floats2bfloat162_rn(df.x, df.y);
             }
-            stage_bf16(cb + S::kBufBytes, act);
           } else {  // kEpiDGelu: out = acc * gelu'(pre-activation), gelu' saved by fwd1
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -927,7 +949,26 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               out[i] = __floats2bfloat162_rn(o.x, o.y);
             }
           }
-          stage_bf16(cb, out);
+          if (wide) {
+            // chunk pair (2 p, 2 p + 1) fills one 128-byte-row box per output: its first
+            // chunk waits until the previous pair's stores have read the buffers
+            if ((ci & 1) == 0) {
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+            }
+            const int h = (ci & 1) * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              *reinterpret_cast<int4*>(cbuf0 + sw128(lane, h + j)) =
+                  *reinterpret_cast<const int4*>(&out[4 * j]);
+              if (EPI == kEpiGelu)
+                *reinterpret_cast<int4*>(cbuf0 + 2 * S::kBufBytes + sw128(lane, h + j)) =
+                    *reinterpret_cast<const int4*>(&act[4 * j]);
+            }
+          } else {
+            if (EPI == kEpiGelu) stage_bf16(cb + S::kBufBytes, act);
+            stage_bf16(cb, out);
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -944,6 +985,14 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             const int a1 = a13_col(col0 + c * kEpiCols);
             tma_store_2d(cmap, cb, a1, row0);
             tma_store_2d(cmap, cb + S::kBufBytes, a1 + 128, row0);
+          } else if (wide) {
+            wide_out = true;
+            if (ci & 1) {
+              tma_store_2d(&args.map_c64, cbuf0, col0 + (c - 1) * kEpiCols, row0);
+              if (EPI == kEpiGelu)
+                tma_store_2d(&args.map_x64, cbuf0 + 2 * S::kBufBytes, col0 + (c - 1) * kEpiCols,
+                             row0);
+            }
           } else {
             tma_store_2d(cmap, cb, col0 + c * kEpiCols, row0);
             if (EPI == kEpiGelu)
@@ -1134,6 +1183,22 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   rc = make_tmap_2d(&mx, xptr, xld, c_rows, kEpiCols, 32, epi == kEpiF32 ? kDtF32 : kDtBF16,
                     epi == kEpiF32 ? 128 : 64);
   if (rc != kOk) return rc;
+  // wide stores: the GeLU epilogue by default (fwd1 standalone -2 %, cfg2 step -0.3 %,
+  // interleaved A/B); FSSDP_GEMM_WIDE_STORE=0 never, =2 also the BF16 epilogue (neutral
+  // standalone, 0.5 % slower per cfg4 step)
+  static const int wide = [] {
+    const char* v = getenv("FSSDP_GEMM_WIDE_STORE");
+    return v == nullptr ? 1 : v[0] - '0';
+  }();
+  if (((wide >= 1 && epi == kEpiGelu) || (wide >= 2 && epi == kEpiBF16)) && args.ldc % 64 == 0) {
+    rc = make_tmap_2d(&la.map_c64, args.c, args.ldc, c_rows, 2 * kEpiCols, 32, kDtBF16, 128);
+    if (rc != kOk) return rc;
+    if (epi == kEpiGelu) {
+      rc = make_tmap_2d(&la.map_x64, args.c2, args.ldc, c_rows, 2 * kEpiCols, 32, kDtBF16, 128);
+      if (rc != kOk) return rc;
+    }
+    la.wide_store = 1;
+  }
   if (BN == 128) {
     if (cg == 2) return dispatch_major<128, 2>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
     return dispatch_major<128, 1>(a_mn, b_mn, epi, ma, mb, mc, mx, la, stream);
