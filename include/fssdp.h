@@ -449,9 +449,10 @@ int fssdp_combine(const int32_t* slot_dest, const int32_t* slot_pos, const float
 /* K7 (token side of backward): for every slot, g[t, j] = <dy_t, Y_slot> (fp32) and
  * bf16(w[t, j] * dy_t) is pushed to the slot's destination dY receive buffer
  * (heap offset dy_recv_off).  Y_slot comes from y_slots (the forward combine's copy) when
- * non-null, else from the peer heaps (offset y_off).  dlogit_out (nullable, needs 4 % k == 0):
- * the gate's dlogit [T*k] (as fssdp_combine_dx defines it) is written here too, so the gate
- * backward can start before the dX combine.  Zeroes own padding rows, ends with a device
+ * non-null, else from the peer heaps (offset y_off).  slot_grad may be NULL: the dots are
+ * then left to fssdp_combine_dx_dots.  dlogit_out (nullable, needs 4 % k == 0 and
+ * slot_grad): the gate's dlogit [T*k] (as fssdp_combine_dx defines it) is written here too,
+ * so the gate backward can start before the dX combine.  Zeroes own padding rows, ends with a device
  * barrier. */
 int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t* slot_pos,
                         const float* topk_w, int64_t T, int32_t d_model, int32_t k,
@@ -470,6 +471,17 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
                      const float* topk_w, const float* slot_grad, const float* wg, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
                      int64_t dxe_off, float* dlogit_out, void* dx_out, void* stream);
+/* The same, with the gate's per-slot <dy_t, Y_slot> computed here instead of in
+ * fssdp_dispatch_grad (call that with slot_grad = NULL: it then only scatters w * dy, the
+ * part on the critical path).  Y rows: y_slots [T*k, d] (combine's token-local copy) or,
+ * when NULL, the expert-order rows at peer heap offset y_off.  Bit-identical dots (same
+ * per-lane order); slot_grad_out [T*k] fp32 (nullable). */
+int fssdp_combine_dx_dots(const int32_t* slot_dest, const int32_t* slot_pos,
+                          const int32_t* topk_idx, const float* topk_w, const void* dy,
+                          const void* y_slots, int64_t y_off, const float* wg, int64_t T,
+                          int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
+                          int64_t dxe_off, float* slot_grad_out, float* dlogit_out, void* dx_out,
+                          void* stream);
 
 /* Gate weight gradient dWg[e] = sum_t dlogit[t, e] x[t]  (fixed order; fp32 [E*d]).
  * workspace: fp32 [ceil(T / FSSDP_WG_TILE) * E * d] (per-token-tile partials, reduced in

@@ -136,6 +136,8 @@ _SIGS = {
     "fssdp_dispatch_grad": [vp, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp, vp, vp, i32,
                             i64, i32, i32, i32, u32, vp, vp],
     "fssdp_combine_dx": [vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp, vp],
+    "fssdp_combine_dx_dots": [vp, vp, vp, vp, vp, vp, i64, vp, i64, i32, i32, i32, vp, i64, vp,
+                              vp, vp, vp],
     "fssdp_gate_wgrad": [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp],
     "fssdp_gate_wgrad_tc_ws_bytes": [i64, i32],
     "fssdp_gate_wgrad_tc": [vp, vp, vp, i64, i32, i32, i32, vp, i64, vp, vp],
@@ -215,7 +217,7 @@ KERNELS_PER_CALL = {
     "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
     "fssdp_route_scan_allgather": 1, "fssdp_gate_route": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1, "fssdp_local_gemm_tables": 1,
     "fssdp_plan_layer_dispatch": 2,
-    "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
+    "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_combine_dx_dots": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
     "fssdp_gate_wgrad_tc": 3,
     "fssdp_sprs": 1, "fssdp_sprs_pull": 1, "fssdp_push_host": 1, "fssdp_pull_host": 1,
     "fssdp_gather_slots": 1, "fssdp_barrier_selftest": 1, "fssdp_adam_step": 1,

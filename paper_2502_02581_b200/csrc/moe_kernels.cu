@@ -1192,7 +1192,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + lane + 32 * u;
-          vy[u] = c < n16 ? ld_nc_v4(yrow + c) : make_int4(0, 0, 0, 0);
+          // slot_grad null: the dots are left to combine_dx (off the critical path)
+          vy[u] = c < n16 && slot_grad != nullptr ? ld_nc_v4(yrow + c) : make_int4(0, 0, 0, 0);
           vg[u] = c < n16 ? ld_nc_v4(grow + c) : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
@@ -1214,7 +1215,7 @@ __global__ void __launch_bounds__(256)
       for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
       if (lane == i) my_dot = dot;
     }
-    if (lane < cnt) slot_grad[sl] = my_dot;
+    if (lane < cnt && slot_grad != nullptr) slot_grad[sl] = my_dot;
     if (dlogit_out != nullptr) {
       // whole tokens per batch (host guarantees kBatch % k == 0): the gate's dlogit here,
       // in combine_dx's arithmetic, so the gate backward need not wait for the dX combine
@@ -1237,7 +1238,9 @@ __global__ void __launch_bounds__(256)
                       const int32_t* __restrict__ topk_idx, const float* __restrict__ topk_w,
                       const float* __restrict__ slot_grad, const float* __restrict__ wg, int64_t T,
                       int d_model, const uint64_t* __restrict__ peer_bases, int64_t dxe_off,
-                      float* __restrict__ dlogit_out, __nv_bfloat16* __restrict__ dx_out) {
+                      float* __restrict__ dlogit_out, __nv_bfloat16* __restrict__ dx_out,
+                      const __nv_bfloat16* __restrict__ dy, int64_t y_off,
+                      const __nv_bfloat16* __restrict__ y_slots, float* __restrict__ slot_grad_out) {
   // launched with PDL (launch_pdl): scheduled during the producing GEMM tail
   asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int TB = kTokBatch;
@@ -1257,7 +1260,47 @@ __global__ void __launch_bounds__(256)
       sp = slot_pos[sl];
       se = topk_idx[sl];
       sw = topk_w[sl];
-      sgr = slot_grad[sl];
+      if (dy == nullptr) sgr = slot_grad[sl];
+    }
+    if (dy != nullptr) {
+      // <dy, Y> of every slot of the batch, here instead of in dispatch_grad (which then
+      // only scatters w * dy on the critical path): the same per-lane fma order and
+      // butterfly as dispatch_grad, so the values are bit-identical
+      const int nsl = static_cast<int>(imin64(TB, T - base)) * K;
+      for (int i = 0; i < nsl; ++i) {
+        const int dst = __shfl_sync(0xffffffffu, sd, i);
+        const int64_t pos = __shfl_sync(0xffffffffu, sp, i);
+        const int4* yrow =
+            y_slots != nullptr
+                ? reinterpret_cast<const int4*>(y_slots + (base * K + i) * d_model)
+                : reinterpret_cast<const int4*>(
+                      reinterpret_cast<const char*>(peer_bases[dst] + y_off) + pos * row_bytes);
+        const int4* grow = reinterpret_cast<const int4*>(dy + (base + i / K) * d_model);
+        float dot = 0.f;
+        for (int c0 = 0; c0 < n16; c0 += kRowBlk) {
+          int4 vy[4], vg[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + lane + 32 * u;
+            vy[u] = c < n16 ? ld_nc_v4(yrow + c) : make_int4(0, 0, 0, 0);
+            vg[u] = c < n16 ? ld_nc_v4(grow + c) : make_int4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + lane + 32 * u;
+            if (c >= n16) break;
+            float fy[8], fg[8];
+            bf16x8_to_f32(vy[u], fy);
+            bf16x8_to_f32(vg[u], fg);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dot = fmaf(fg[q], fy[q], dot);
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+        if (lane == i) sgr = dot;
+      }
+      if (own && slot_grad_out != nullptr) slot_grad_out[sl] = sgr;
     }
     // dlogit of this lane's slot: w_j (g_j - sum_i w_i g_i), the sum over its token's slots
     const int first = (lane / K) * K;
@@ -2128,7 +2171,7 @@ int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t*
                         int32_t world, int32_t bar_slot, uint32_t epoch, uint32_t* grid_counter,
                         void* stream) {
   if (d_model % 8 != 0 || world <= 0 || world > kMaxWorld || k <= 0 || k > kGateMaxK ||
-      (dlogit_out != nullptr && kBatch % k != 0)) {
+      (dlogit_out != nullptr && (kBatch % k != 0 || slot_grad == nullptr))) {
     set_error("dispatch_grad: bad shape");
     return kErrDimension;
   }
@@ -2141,10 +2184,47 @@ int fssdp_dispatch_grad(const void* dy, const int32_t* slot_dest, const int32_t*
   return launch_status();
 }
 
+static int combine_dx_launch(const int32_t* slot_dest, const int32_t* slot_pos,
+                             const int32_t* topk_idx, const float* topk_w, const float* slot_grad,
+                             const float* wg, int64_t T, int32_t d_model, int32_t E, int32_t k,
+                             const uint64_t* peer_bases, int64_t dxe_off, float* dlogit_out,
+                             void* dx_out, const void* dy, int64_t y_off, const void* y_slots,
+                             float* slot_grad_out, void* stream);
+
 int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const int32_t* topk_idx,
                      const float* topk_w, const float* slot_grad, const float* wg, int64_t T,
                      int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
                      int64_t dxe_off, float* dlogit_out, void* dx_out, void* stream) {
+  if (slot_grad == nullptr && T > 0) {
+    set_error("combine_dx: slot_grad is required (fssdp_combine_dx_dots computes it)");
+    return kErrDimension;
+  }
+  return combine_dx_launch(slot_dest, slot_pos, topk_idx, topk_w, slot_grad, wg, T, d_model, E, k,
+                           peer_bases, dxe_off, dlogit_out, dx_out, nullptr, 0, nullptr, nullptr,
+                           stream);
+}
+
+int fssdp_combine_dx_dots(const int32_t* slot_dest, const int32_t* slot_pos,
+                          const int32_t* topk_idx, const float* topk_w, const void* dy,
+                          const void* y_slots, int64_t y_off, const float* wg, int64_t T,
+                          int32_t d_model, int32_t E, int32_t k, const uint64_t* peer_bases,
+                          int64_t dxe_off, float* slot_grad_out, float* dlogit_out, void* dx_out,
+                          void* stream) {
+  if (dy == nullptr && T > 0) {
+    set_error("combine_dx_dots: dy is required");
+    return kErrDimension;
+  }
+  return combine_dx_launch(slot_dest, slot_pos, topk_idx, topk_w, nullptr, wg, T, d_model, E, k,
+                           peer_bases, dxe_off, dlogit_out, dx_out, dy, y_off, y_slots,
+                           slot_grad_out, stream);
+}
+
+static int combine_dx_launch(const int32_t* slot_dest, const int32_t* slot_pos,
+                             const int32_t* topk_idx, const float* topk_w, const float* slot_grad,
+                             const float* wg, int64_t T, int32_t d_model, int32_t E, int32_t k,
+                             const uint64_t* peer_bases, int64_t dxe_off, float* dlogit_out,
+                             void* dx_out, const void* dy, int64_t y_off, const void* y_slots,
+                             float* slot_grad_out, void* stream) {
   if (d_model % 8 != 0 || k <= 0 || k > kGateMaxK || E > kGateMaxE) {
     set_error("combine_dx: bad shape");
     return kErrDimension;
@@ -2160,7 +2240,8 @@ int fssdp_combine_dx(const int32_t* slot_dest, const int32_t* slot_pos, const in
   timing_begin(as_stream(stream));
   FSSDP_DISPATCH_K(k, combine_dx_kernel, grid, as_stream(stream), slot_dest, slot_pos, topk_idx,
                    topk_w, slot_grad, wg, T, d_model, peer_bases, dxe_off, dlogit_out,
-                   static_cast<__nv_bfloat16*>(dx_out));
+                   static_cast<__nv_bfloat16*>(dx_out), static_cast<const __nv_bfloat16*>(dy),
+                   y_off, static_cast<const __nv_bfloat16*>(y_slots), slot_grad_out);
   return launch_status();
 }
 

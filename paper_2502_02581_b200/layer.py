@@ -985,6 +985,17 @@ class FssdpMoE:
     # before them, the gate backward beside them)
     DX_MODE = os.environ.get("FSSDP_DX_MODE", "overlap")
     GATE_WGRAD_TC = os.environ.get("FSSDP_GATE_WGRAD_TC", "1") == "1"
+    # experiment (FSSDP_LATE_DOTS=1): the gate's <dy, Y> dots in the dX combine (beside
+    # the wgrads) instead of in dispatch_grad, which then only scatters w * dy on the
+    # critical path — where the gate backward follows the dX combine anyway (no early
+    # gate).  Bit-identical (test); measured 0.5 % SLOWER per step at N=1 (interleaved
+    # A/B: the 100 MB of extra reads slow the wgrads they run beside more than
+    # dispatch_grad gains), so off by default
+    LATE_DOTS = os.environ.get("FSSDP_LATE_DOTS", "0") == "1"
+
+    @property
+    def _late_dots(self) -> bool:
+        return self.LATE_DOTS and not self._early_gate
 
     @property
     def _early_gate(self) -> bool:
@@ -1098,7 +1109,8 @@ class FssdpMoE:
                ops._ptr(self.slot_pos), ops._ptr(self.topk_w), self.T, self.g.d_model,
                self.g.top_k, self._pb(), self.off["y"], ops._ptr(self.y_slots),
                self.off["dyrecv"],
-               ops._ptr(self.slot_grad), ops._ptr(self.dlogit if self._early_gate else None),
+               ops._ptr(None if self._late_dots else self.slot_grad),
+               ops._ptr(self.dlogit if self._early_gate else None),
                self._tab("zero_rows"), self.g.num_experts if self._local_gemm else t.n_zero,
                self.flags_off, self.rank, self.world, slot, C.c_uint32(epoch),
                C.c_void_p(self.grid_counter.data_ptr() + 4), self._stream())
@@ -1138,6 +1150,14 @@ class FssdpMoE:
     def phase_combine_dx(self, dx: torch.Tensor | None = None) -> torch.Tensor:
         if dx is None:
             dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
+        if self._late_dots:
+            self._call("fssdp_combine_dx_dots", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
+                       ops._ptr(self.topk_idx), ops._ptr(self.topk_w), ops._ptr(self.dy),
+                       ops._ptr(self.y_slots), self.off["y"], ops._ptr(self.wg), self.T,
+                       self.g.d_model, self.g.num_experts, self.g.top_k, self._pb(),
+                       self.off["dxe"], ops._ptr(self.slot_grad), ops._ptr(self.dlogit),
+                       ops._ptr(dx), self._stream())
+            return dx
         self._call("fssdp_combine_dx", ops._ptr(self.slot_dest), ops._ptr(self.slot_pos),
                ops._ptr(self.topk_idx), ops._ptr(self.topk_w), ops._ptr(self.slot_grad),
                ops._ptr(self.wg), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,

@@ -174,3 +174,32 @@ def test_multi_rank_equals_single_rank(world, E, policy_kw, f, activation, grad_
     else:
         assert replicas_seen == 0 and prefetched == 0
 
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_late_dots_bit_identical(world, monkeypatch):
+    """The gate's <dy, Y> dots computed in the dX combine (fssdp_combine_dx_dots, the
+    default wherever the gate backward follows the dX combine) equal the dispatch_grad ones
+    bit for bit, and so do dlogit, dx and dWg."""
+    E, d, f, k, T = 8, 256, 512, 2, 777
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    xs = [torch.randn(T, d, device="cuda", generator=g).bfloat16() for _ in range(world)]
+    dys = [(torch.randn(T, d, device="cuda", generator=g) * 0.1).bfloat16() for _ in range(world)]
+    out = {}
+    for late in (False, True):
+        monkeypatch.setattr(FssdpMoE, "LATE_DOTS", late)
+        monkeypatch.setattr(FssdpMoE, "EARLY_GATE", False)
+        layers = build(world, E, d, f, k, T, pol, seed=2, bias=zipf_bias(E))
+        assert all(ly._late_dots == late for ly in layers)
+        ys = run_lockstep_forward(layers, xs) if world > 1 else [layers[0].forward(xs[0])]
+        dxs = (run_lockstep_backward(layers, dys) if world > 1
+               else [layers[0].backward(dys[0])])
+        torch.cuda.synchronize()
+        out[late] = [(y.clone(), dx.clone(), ly.slot_grad[:T].clone(), ly.dlogit[:T].clone(),
+                      ly.dwg.clone()) for y, dx, ly in zip(ys, dxs, layers)]
+        for ly in layers:
+            ly.planner.finish()
+    for a, b in zip(out[False], out[True]):
+        for u, v in zip(a, b):
+            assert torch.equal(u, v)
