@@ -601,7 +601,8 @@ def run_ours(args):
         copy_s = torch.cuda.Stream(device=dev)   # H2D
         d2h_s = torch.cuda.Stream(device=dev)    # D2H: PCIe is full duplex
         main_s = torch.cuda.current_stream(dev)
-        in_ev = [torch.cuda.Event() for _ in range(2)]
+        in_ev = [torch.cuda.Event() for _ in range(2)]     # x of the step landed
+        in_dy_ev = [torch.cuda.Event() for _ in range(2)]  # dy landed (the backward waits)
         done_ev = [torch.cuda.Event() for _ in range(2)]
         fwd_ev = [torch.cuda.Event() for _ in range(2)]
 
@@ -610,8 +611,9 @@ def run_ours(args):
             with torch.cuda.stream(copy_s):
                 copy_s.wait_event(done_ev[b])  # step i-2 finished with buffer b
                 xb[b].copy_(xh[i % HP], non_blocking=True)
-                dyb[b].copy_(dyh[i % HP], non_blocking=True)
                 in_ev[b].record(copy_s)
+                dyb[b].copy_(dyh[i % HP], non_blocking=True)
+                in_dy_ev[b].record(copy_s)
 
         def d2h(t, host, ev):
             with torch.cuda.stream(d2h_s):
@@ -638,6 +640,7 @@ def run_ours(args):
                 if prev is not None:  # the previous step's dx streams out
                     d2h(*prev)
                 d2h(y, yh[b], fwd_ev[b])  # this step's y, behind its forward
+                main_s.wait_event(in_dy_ev[b])  # the forward only needed x
                 dx = layer.backward(dyb[b])
                 layer.reduce_gate_grad()
                 layer.planner.finish()
@@ -668,7 +671,8 @@ def run_ours(args):
                "planning_gap_gpu_ms": round(e2e_gap_ms, 4),
                "pipeline": "x, dy of step i+1 H2D and y of step i, dx of step i-1 D2H on two "
                            "copy streams (PCIe full duplex), overlapped with step i's compute "
-                           "(FssdpMoE.forward/backward); two distinct host batches alternate"}
+                           "(FssdpMoE.forward/backward; the forward waits for x only, the "
+                           "backward for dy); two distinct host batches alternate"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
