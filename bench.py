@@ -652,15 +652,12 @@ def run_ours(args):
 
         run(2)
         barrier()
-        layer.gap_events = []  # the planning gap under the bulk PCIe copies (2 events/step)
         s2, e2 = torch.cuda.Event(True), torch.cuda.Event(True)
         s2.record()
         run(args.steps)
         e2.record()
         barrier()
         e2e_ms = s2.elapsed_time(e2) / args.steps
-        e2e_gap_ms = sum(a.elapsed_time(b) for a, b in layer.gap_events) / max(1, len(layer.gap_events))
-        layer.gap_events = None
         if world > 1:
             t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -668,7 +665,6 @@ def run_ours(args):
         nb = T * CFG2["d_model"] * 2
         e2e = {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "ms_per_step": e2e_ms,
-               "planning_gap_gpu_ms": round(e2e_gap_ms, 4),
                "pipeline": "x, dy of step i+1 H2D and y of step i, dx of step i-1 D2H on two "
                            "copy streams (PCIe full duplex), overlapped with step i's compute "
                            "(FssdpMoE.forward/backward; the forward waits for x only, the "
