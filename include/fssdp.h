@@ -397,6 +397,13 @@ int fssdp_route_scan_allgather(const int32_t* tile_counts, int32_t n_tiles, int3
                                int64_t flags_off, int32_t rank, int32_t world, int32_t bar_slot,
                                uint32_t epoch, void* stream);
 
+/* Dense all-reduce of a small replicated gradient over P2P, to run after a world barrier:
+ * out[i] = sum over ranks p = 0..world-1 (in rank order, fp32) of rank p's partial at heap
+ * offset src_off (n floats, n % 4 == 0, 16-byte aligned) — the same bits on every rank.
+ * Replaces the NCCL all-reduce of the gate's dWg (replicated gate, data-parallel grad). */
+int fssdp_sum_peers(const uint64_t* peer_bases, int32_t world, int64_t src_off, int64_t n,
+                    float* out, void* stream);
+
 /* Device barrier across the world (system-scope release/acquire on flag pads). */
 int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, int32_t world,
                   int32_t bar_slot, uint32_t epoch, void* stream);

@@ -128,6 +128,7 @@ _SIGS = {
     "fssdp_gate_gemm_ws_bytes": [i64, i32],
     "fssdp_route_scan_allgather": [vp, i32, i32, vp, vp, i64, i64, i32, i32, i32, u32, vp],
     "fssdp_barrier": [vp, i64, i32, i32, i32, u32, vp],
+    "fssdp_sum_peers": [vp, i32, i64, i64, vp, vp],
     "fssdp_barrier_selftest": [vp, i64, i64, i32, i32, i32, u32, i32, vp, vp],
     "fssdp_dispatch": [vp, vp, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32,
                        i64, i32, i32, u32, vp, vp],
@@ -215,7 +216,8 @@ def check(status: int, what: str) -> None:
 # kernels launched per successful call of each device entry point (launch accounting)
 KERNELS_PER_CALL = {
     "fssdp_grouped_gemm": 1, "fssdp_gate_topk": 1, "fssdp_topk_from_logits": 1,
-    "fssdp_route_scan_allgather": 1, "fssdp_gate_route": 1, "fssdp_barrier": 1, "fssdp_dispatch": 1, "fssdp_combine": 1, "fssdp_local_gemm_tables": 1,
+    "fssdp_route_scan_allgather": 1, "fssdp_gate_route": 1, "fssdp_barrier": 1,
+    "fssdp_sum_peers": 1, "fssdp_dispatch": 1, "fssdp_combine": 1, "fssdp_local_gemm_tables": 1,
     "fssdp_plan_layer_dispatch": 2,
     "fssdp_dispatch_grad": 1, "fssdp_combine_dx": 1, "fssdp_combine_dx_dots": 1, "fssdp_gate_wgrad": 2, "fssdp_spag": 1,
     "fssdp_gate_wgrad_tc": 3,

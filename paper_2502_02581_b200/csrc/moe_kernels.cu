@@ -1062,6 +1062,29 @@ __device__ __forceinline__ int4 f32_to_bf16x8(const float (&f)[8]) {
   return v;
 }
 
+// Dense all-reduce of a small replicated gradient over P2P (the gate's dWg): after a world
+// barrier (every rank's partial is final), out = sum over ranks p = 0..world-1, in rank
+// order, of rank p's fp32 partial at heap offset src_off — bit-identical on every rank.
+// The loads go through L2 (__ldcg): the partials were released before the barrier.
+__global__ void __launch_bounds__(256)
+    sum_peers_kernel(const uint64_t* __restrict__ peer_bases, int world, int64_t src_off,
+                     int64_t n4, float4* __restrict__ out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched behind the barrier (PDL)
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = __ldcg(reinterpret_cast<const float4*>(peer_bases[0] + src_off) + i);
+#pragma unroll 4
+    for (int p = 1; p < world; ++p) {  // independent loads: the unrolled ones are in flight
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(peer_bases[p] + src_off) + i);
+      a.x = __fadd_rn(a.x, v.x);
+      a.y = __fadd_rn(a.y, v.y);
+      a.z = __fadd_rn(a.z, v.z);
+      a.w = __fadd_rn(a.w, v.w);
+    }
+    out[i] = a;
+  }
+}
+
 // Row chunks: a warp walks a row in blocks of 128 x 16 B; a lane holds 4 of them, and the
 // loads of all K rows of a token are issued before any use (one memory latency per token).
 constexpr int kRowBlk = 128;
@@ -2077,6 +2100,23 @@ int fssdp_barrier(const uint64_t* peer_bases, int64_t flags_off, int32_t rank, i
   timing_begin(as_stream(stream));
   launch_pdl(barrier_kernel, 1, 32, as_stream(stream), peer_bases, flags_off, rank, world,
              bar_slot, epoch);
+  return launch_status();
+}
+
+int fssdp_sum_peers(const uint64_t* peer_bases, int32_t world, int64_t src_off, int64_t n,
+                    float* out, void* stream) {
+  if (world <= 0 || world > kMaxWorld || n < 0 || (n % 4) != 0 || (src_off % 16) != 0 ||
+      (reinterpret_cast<uintptr_t>(out) & 15) != 0) {
+    set_error("sum_peers: bad world / n (multiple of 4) / alignment");
+    return kErrDimension;
+  }
+  if (n == 0) return kOk;
+  const int64_t n4 = n / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
+  timing_begin(as_stream(stream));
+  launch_pdl(sum_peers_kernel, static_cast<int>(blocks), 256, as_stream(stream), peer_bases,
+             world, src_off, n4, reinterpret_cast<float4*>(out));
   return launch_status();
 }
 

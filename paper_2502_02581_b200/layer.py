@@ -147,6 +147,8 @@ class LayerGeometry:
         layout.add(prefix + "dyrecv", R * d * 2)
         layout.add(prefix + "dxe", R * d * 2)
         layout.add(prefix + "counts", (self.world * self.num_experts * 4 + 15) // 16 * 16)
+        # the gate's dWg partials (two, by step parity), summed over P2P after the end barrier
+        layout.add(prefix + "dwgp", 2 * self.num_experts * d * 4)
         layout.add(prefix + "stage",
                    max(1, self.stage_slots) * self.slot_grad_elems * self.grad_elem_bytes)
         # re-shard staging: the old owned shards, pulled by their new owners
@@ -228,7 +230,8 @@ class FssdpMoE:
         heap = group.local
         d, f, E, R = geom.d_model, geom.d_ff, geom.num_experts, geom.recv_cap
         self.off = {k: L.offset(prefix + k) for k in
-                    ("grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage", "reshard")}
+                    ("grads", "xrecv", "y", "dyrecv", "dxe", "counts", "stage", "reshard",
+                     "dwgp")}
         # parameter slots: "params" = the region the plan tables' slot indices address
         # (model-level in the split layout), "owned" = this layer's first owned slot
         sb = geom.slot_param_bytes
@@ -328,6 +331,9 @@ class FssdpMoE:
                                             device=self.dev)
         self.gate_bias = torch.zeros(E, dtype=torch.float32, device=self.dev)
         self.dwg = torch.zeros(E, d, dtype=torch.float32, device=self.dev)
+        self.dwg_part = [heap.tensor(self.off["dwgp"] + i * E * d * 4, (E, d), torch.float32)
+                         for i in range(2)]
+        self._gpar = 0  # parity of the dWg partial the last gate backward wrote
         self.topk_idx = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
         self.topk_w = torch.empty(Tc, k, dtype=torch.float32, device=self.dev)
         self.slot_rank = torch.empty(Tc, k, dtype=torch.int32, device=self.dev)
@@ -1165,16 +1171,43 @@ class FssdpMoE:
                ops._ptr(dx), self._stream())
         return dx
 
+    # dWg all-reduce (the gate is replicated, its gradient data-parallel): the partials in
+    # the heap, summed in rank order over P2P right after the step's end barrier
+    # (fssdp_sum_peers: bit-identical on every rank, no NCCL call in the step).
+    # FSSDP_P2P_GATE_REDUCE=0: the NCCL all-reduce in reduce_gate_grad() instead
+    P2P_GATE_REDUCE = os.environ.get("FSSDP_P2P_GATE_REDUCE", "1") != "0"
+    P2P_GATE_REDUCE_EMULATED = False  # tests: the same over emulated ranks (lockstep)
+
+    @property
+    def _p2p_gate_reduce(self) -> bool:
+        return self.P2P_GATE_REDUCE and self.world > 1 and (
+            self.group.mode == "dist" or self.P2P_GATE_REDUCE_EMULATED)
+
     def phase_gate_wgrad(self) -> None:
+        out = self.dwg
+        if self._p2p_gate_reduce:
+            self._gpar ^= 1
+            out = self.dwg_part[self._gpar]
         if self._wg_tc:
             self._call("fssdp_gate_wgrad_tc", ops._ptr(self.x), ops._ptr(self.topk_idx),
                        ops._ptr(self.dlogit), self.T, self.g.d_model, self.g.num_experts,
                        self.g.top_k, ops._ptr(self.wg_ws), self.wg_ws.numel(),
-                       ops._ptr(self.dwg), self._stream())
+                       ops._ptr(out), self._stream())
             return
         self._call("fssdp_gate_wgrad", ops._ptr(self.x), ops._ptr(self.topk_idx),
                ops._ptr(self.dlogit), self.T, self.g.d_model, self.g.num_experts, self.g.top_k,
-               ops._ptr(self.wg_ws), ops._ptr(self.dwg), self._stream())
+               ops._ptr(self.wg_ws), ops._ptr(out), self._stream())
+
+    def phase_gate_reduce(self) -> None:
+        """dWg = sum over ranks of the partials (after a barrier that every rank's gate
+        backward precedes).  The parity double buffer keeps a fast rank's next partial off
+        the one its peers may still be reading."""
+        if not self._p2p_gate_reduce:
+            return
+        E, d = self.g.num_experts, self.g.d_model
+        self._call("fssdp_sum_peers", self._pb(), self.world,
+                   self.off["dwgp"] + self._gpar * E * d * 4, E * d, ops._ptr(self.dwg),
+                   self._stream())
 
     def phase_sprs(self) -> None:
         n = self.tables.n_sprs_jobs
@@ -1311,6 +1344,7 @@ class FssdpMoE:
         if replicas:
             main.wait_stream(side)
         self.phase_barrier(BAR_END)
+        self.phase_gate_reduce()
         return dx
 
     @contextlib.contextmanager
@@ -1340,8 +1374,9 @@ class FssdpMoE:
         return self._side
 
     def reduce_gate_grad(self, pg=None) -> None:
-        """dWg is data-parallel (the gate is replicated): one small NCCL all-reduce."""
-        if self.world > 1 and self.group.mode == "dist":
+        """dWg is data-parallel (the gate is replicated).  By default the backward already
+        summed it over P2P (phase_gate_reduce); else one small NCCL all-reduce."""
+        if self.world > 1 and self.group.mode == "dist" and not self._p2p_gate_reduce:
             import torch.distributed as dist
 
             dist.all_reduce(self.dwg, group=pg)
@@ -1482,6 +1517,8 @@ def run_lockstep_backward(layers: list, dys: list, rematerialize: bool = False) 
     dxs = [ly.phase_combine_dx() for ly in layers]
     for ly in layers:
         ly.phase_gate_wgrad()
+    for ly in layers:
+        ly.phase_gate_reduce()
     for ly in layers:
         ly.phase_sprs()
     return dxs

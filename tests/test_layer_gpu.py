@@ -203,3 +203,37 @@ def test_late_dots_bit_identical(world, monkeypatch):
     for a, b in zip(out[False], out[True]):
         for u, v in zip(a, b):
             assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_gate_reduce(world, monkeypatch):
+    """dWg summed over P2P (fssdp_sum_peers after the end barrier, the default at N > 1
+    in a real process group): every rank gets the same bits — the rank-order fp32 sum of
+    the gate partials — and it matches the single-rank dWg of the same tokens."""
+    monkeypatch.setattr(FssdpMoE, "P2P_GATE_REDUCE_EMULATED", True)
+    E, d, f, k, Tr = 8, 256, 512, 2, 300
+    pol = F.Policy(F.PolicyKind.FSSDP, overlap_override=4, capacity_override=2)
+    bias = zipf_bias(E)
+    multi = build(world, E, d, f, k, Tr, pol, seed=4, bias=bias)
+    single = build(1, E, d, f, k, Tr * world, F.Policy(F.PolicyKind.EP), seed=4, bias=bias)[0]
+    assert all(ly._p2p_gate_reduce for ly in multi) and not single._p2p_gate_reduce
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for it in range(3):  # both parities of the partial buffers
+        x = torch.randn(world * Tr, d, device="cuda", generator=g).bfloat16()
+        dy = (torch.randn(world * Tr, d, device="cuda", generator=g) * 0.1).bfloat16()
+        run_lockstep_forward(multi, list(x.split(Tr)))
+        run_lockstep_backward(multi, list(dy.split(Tr)))
+        for ly in multi:
+            ly.planner.finish()
+        single.forward(x)
+        single.backward(dy)
+        single.planner.finish()
+        torch.cuda.synchronize()
+        parts = [ly.dwg_part[ly._gpar] for ly in multi]
+        ref = parts[0].clone()
+        for p in parts[1:]:
+            ref = ref + p
+        for ly in multi:
+            assert torch.equal(ly.dwg, ref), f"it{it}: rank {ly.rank}"
+        close(multi[0].dwg.double().cpu().numpy(), single.dwg.double().cpu().numpy(),
+              rel=1e-4, abs_=1e-6, what="dWg")
