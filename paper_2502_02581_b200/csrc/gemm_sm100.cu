@@ -168,6 +168,16 @@ __device__ __forceinline__ void gelu_and_grad2(uint64_t x, uint64_t& g, uint64_t
   dg = f2_fma(half, f2_add(one, t), f2_mul(f2_mul(hx, q), w));
 }
 
+// SwiGLU backward of one element from the fp32 dh and the saved bf16 a1, a3 (both the
+// normal and the swapped-tail epilogue use this one expression: bit-identical results):
+//   s = sigmoid(a1), d1 = dh a3 s (1 + a1 (1 - s)), d3 = dh silu(a1)
+__device__ __forceinline__ void dswiglu1(float dh, float a1, float a3, float& d1, float& d3) {
+  const float sg = __frcp_rn(1.f + __expf(-a1));
+  const float ds = sg * (1.f + a1 * (1.f - sg));
+  d1 = dh * a3 * ds;
+  d3 = dh * a1 * sg;
+}
+
 struct TileCoord {
   int group, m_tile, n_tile;  // m_tile in units of CG * 128 rows
 };
@@ -326,7 +336,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   // N'/2 per CTA) — so the 256-row padding of the segment costs at most 63 rows of MMA
   // work.  The epilogue stores the transposed accumulator through the same 32x32 boxes.
   constexpr bool kSwapOk = CG == 2 && CL == 1 && !A_MN && BN == 256 && kEpiWarps == 4 &&
-                           (EPI == kEpiBF16 || EPI == kEpiGelu || EPI == kEpiDGelu);
+                           (EPI == kEpiBF16 || EPI == kEpiGelu || EPI == kEpiDGelu ||
+                            EPI == kEpiDSwiglu);
   constexpr bool kWideOk = (EPI == kEpiBF16 || EPI == kEpiGelu) && kEpiWarps == 4 &&
                            S::kSets * S::kOutTiles * S::kBufBytes >= 4096 * S::kOutTiles;
   auto tail_rows = [&](const GemmGroup& g) -> int {  // N' of the group's tail, 0: none
@@ -738,21 +749,31 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                 mbar_arrive(&tempty_bar[acc]);
             }
           }
-          float pre[32];
-          if (EPI == kEpiDGelu) {  // the saved gelu' box of these rows / columns
+          float pre[32], pre3[32];
+          if (kAux) {  // the saved gelu' (dSwiGLU: a1 and a3) box of these rows / columns
             const int entry = static_cast<int>(gchunk % kAB);
             uint8_t* ab = abuf0 + entry * kAT * S::kBufBytes;
             if (lane == 0) {
               fence_proxy_async_smem();
-              mbar_arrive_expect_tx(&abar[entry], S::kBufBytes);
-              tma_load_2d(ab, &map_x, &abar[entry], wcol, trow + ci * 32);
+              mbar_arrive_expect_tx(&abar[entry], kAT * S::kBufBytes);
+              if (EPI == kEpiDSwiglu) {
+                const int a1c = a13_col(wcol);
+                tma_load_2d(ab, &map_x, &abar[entry], a1c, trow + ci * 32);
+                tma_load_2d(ab + S::kBufBytes, &map_x, &abar[entry], a1c + 128, trow + ci * 32);
+              } else {
+                tma_load_2d(ab, &map_x, &abar[entry], wcol, trow + ci * 32);
+              }
             }
             mbar_wait(&abar[entry], (aux_phase >> entry) & 1u);
             aux_phase ^= 1u << entry;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              pre[j] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-                  ab + (static_cast<uint32_t>(sw64(j, lane >> 3)) + (lane & 7) * 2)));
+            for (int j = 0; j < 32; ++j) {
+              const uint32_t o = static_cast<uint32_t>(sw64(j, lane >> 3)) + (lane & 7) * 2;
+              pre[j] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(ab + o));
+              if (EPI == kEpiDSwiglu)
+                pre3[j] = __bfloat162float(
+                    *reinterpret_cast<const __nv_bfloat16*>(ab + S::kBufBytes + o));
+            }
           }
           if (lane == 0) {
             if (wide_out)
@@ -776,6 +797,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             } else if (EPI == kEpiDGelu) {
               const float2 v = f2_unpack(f2_mul(f2_pack(a0, a1), f2_pack(pre[j], pre[j + 1])));
               o = __floats2bfloat162_rn(v.x, v.y);
+            } else if (EPI == kEpiDSwiglu) {  // o = d1, act = d3 of rows j, j + 1
+              float d1a, d3a, d1b, d3b;
+              dswiglu1(a0, pre[j], pre3[j], d1a, d3a);
+              dswiglu1(a1, pre[j + 1], pre3[j + 1], d1b, d3b);
+              o = __floats2bfloat162_rn(d1a, d1b);
+              act = __floats2bfloat162_rn(d3a, d3b);
             } else {
               o = __floats2bfloat162_rn(a0, a1);
             }
@@ -783,7 +810,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             const uint32_t o1 = static_cast<uint32_t>(sw64(j + 1, lane >> 3)) + (lane & 7) * 2;
             *reinterpret_cast<__nv_bfloat16*>(cb + o0) = o.x;
             *reinterpret_cast<__nv_bfloat16*>(cb + o1) = o.y;
-            if (EPI == kEpiGelu) {
+            if (EPI == kEpiGelu || EPI == kEpiDSwiglu) {
               *reinterpret_cast<__nv_bfloat16*>(cb + S::kBufBytes + o0) = act.x;
               *reinterpret_cast<__nv_bfloat16*>(cb + S::kBufBytes + o1) = act.y;
             }
@@ -791,8 +818,14 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(cmap, cb, wcol, trow + ci * 32);
-            if (EPI == kEpiGelu) tma_store_2d(&map_x, cb + S::kBufBytes, wcol, trow + ci * 32);
+            if (EPI == kEpiDSwiglu) {  // da1, da3 columns of the interleaved [a1 | a3] layout
+              const int a1c = a13_col(wcol);
+              tma_store_2d(cmap, cb, a1c, trow + ci * 32);
+              tma_store_2d(cmap, cb + S::kBufBytes, a1c + 128, trow + ci * 32);
+            } else {
+              tma_store_2d(cmap, cb, wcol, trow + ci * 32);
+              if (EPI == kEpiGelu) tma_store_2d(&map_x, cb + S::kBufBytes, wcol, trow + ci * 32);
+            }
             bulk_commit();
           }
         }
@@ -914,11 +947,11 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {  // dH (fp32) with the saved bf16 a1, a3
             const float2 a1 = __bfloat1622float2(pre[i]), a3 = __bfloat1622float2(pre3[i]);
-            const float dh0 = __uint_as_float(r[2 * i]), dh1 = __uint_as_float(r[2 * i + 1]);
-            const float s0 = __frcp_rn(1.f + __expf(-a1.x)), s1 = __frcp_rn(1.f + __expf(-a1.y));
-            const float ds0 = s0 * (1.f + a1.x * (1.f - s0)), ds1 = s1 * (1.f + a1.y * (1.f - s1));
-            d1[i] = __floats2bfloat162_rn(dh0 * a3.x * ds0, dh1 * a3.y * ds1);
-            d3[i] = __floats2bfloat162_rn(dh0 * a1.x * s0, dh1 * a1.y * s1);
+            float d1a, d3a, d1b, d3b;
+            dswiglu1(__uint_as_float(r[2 * i]), a1.x, a3.x, d1a, d3a);
+            dswiglu1(__uint_as_float(r[2 * i + 1]), a1.y, a3.y, d1b, d3b);
+            d1[i] = __floats2bfloat162_rn(d1a, d1b);
+            d3[i] = __floats2bfloat162_rn(d3a, d3b);
           }
           stage_bf16(cb, d1);
           stage_bf16(cb + S::kBufBytes, d3);

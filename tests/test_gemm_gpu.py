@@ -612,7 +612,7 @@ def test_split_tail_equals_full_tiles(case):
     assert outs[0][0].abs().sum() > 0
 
 
-@pytest.mark.parametrize("case", ["bf16", "bf16_mnB", "gelu", "dgelu_mnB"])
+@pytest.mark.parametrize("case", ["bf16", "bf16_mnB", "gelu", "dgelu_mnB", "dswiglu_mnB"])
 def test_swap_tail_equals_full_tiles(case):
     """FSSDP_GEMM_SWAP_TAIL: a group's last M tile whose real rows end within 192 rows runs
     as D^T = W X^T with N' = rows rounded up to 64.  Every REAL row equals the full-tile
@@ -632,7 +632,9 @@ def test_swap_tail_equals_full_tiles(case):
     for r, p in zip(rows, pad):
         A[r0:r0 + r] = torch.randn(r, K, device=dev).bfloat16()
         r0 += p
-    b_mn = case in ("dgelu_mnB", "bf16_mnB")
+    b_mn = case in ("dgelu_mnB", "bf16_mnB", "dswiglu_mnB")
+    # dSwiGLU: N = d_ff (h space), C and aux = the interleaved [a1 | a3] layout, 2 N wide
+    W = 2 * N_ if case == "dswiglu_mnB" else N_
     if b_mn:
         B = (torch.randn(G * K, N_, device=dev) / K ** 0.5).bfloat16()
     else:
@@ -642,18 +644,19 @@ def test_swap_tail_equals_full_tiles(case):
     for i, (r, p) in enumerate(zip(rows, pad)):
         g["m_tiles"][i], g["a_m"][i], g["k_blocks"][i] = p // 128, r0, K // 64
         g["b_n"][i], g["b_k"][i] = (0, i * K) if b_mn else (i * N_, 0)
-        g["c_off"][i], g["rows"][i] = r0 * N_, r
+        g["c_off"][i], g["rows"][i] = r0 * W, r
         r0 += p
     total = ops.finalize_groups(g, N_ // 256)
     gd = torch.from_numpy(g.view(np.uint8).copy()).to(dev)
     epi = {"bf16": ops.EPI_BF16, "bf16_mnB": ops.EPI_BF16, "gelu": ops.EPI_GELU,
-           "dgelu_mnB": ops.EPI_DGELU}[case]
-    aux = torch.randn(R, N_, device=dev).bfloat16() if case == "dgelu_mnB" else None
+           "dgelu_mnB": ops.EPI_DGELU, "dswiglu_mnB": ops.EPI_DSWIGLU}[case]
+    aux = (torch.randn(R, W, device=dev).bfloat16()
+           if case in ("dgelu_mnB", "dswiglu_mnB") else None)
     outs = []
     for st in (False, True, True):
-        C = torch.full((R, N_), 7.0, device=dev, dtype=torch.bfloat16)
+        C = torch.full((R, W), 7.0, device=dev, dtype=torch.bfloat16)
         C2 = torch.full((R, N_), 7.0, device=dev, dtype=torch.bfloat16) if case == "gelu" else None
-        ops.grouped_gemm(A, False, B, b_mn, gd, G, N_ // 256, total, C, N_, epilogue=epi,
+        ops.grouped_gemm(A, False, B, b_mn, gd, G, N_ // 256, total, C, W, epilogue=epi,
                          c2=C2, aux=aux, n_fastest=True, cta_pair=True, swap_tail=st)
         torch.cuda.synchronize()
         outs.append((C, C2))
