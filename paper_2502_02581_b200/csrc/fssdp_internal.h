@@ -49,6 +49,7 @@ struct GemmLaunch {
   int wide_store;            // BF16 / GeLU epilogues: 32 x 64 store boxes (128-byte rows)
   CUtensorMap map_c64;       // wide_store: C with 32 x 64 boxes (SWIZZLE_128B)
   CUtensorMap map_x64;       // wide_store, GeLU: the second output, same boxes
+  CUtensorMap map_b64;       // swap_tail, SwiGLU: B with 64-row boxes (a1 / a3 unit halves)
 };
 
 int num_sms();

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
   // work.  The epilogue stores the transposed accumulator through the same 32x32 boxes.
   constexpr bool kSwapOk = CG == 2 && CL == 1 && !A_MN && BN == 256 && kEpiWarps == 4 &&
                            (EPI == kEpiBF16 || EPI == kEpiGelu || EPI == kEpiDGelu ||
-                            EPI == kEpiDSwiglu);
+                            EPI == kEpiDSwiglu || (EPI == kEpiSwiglu && !B_MN));
   constexpr bool kWideOk = (EPI == kEpiBF16 || EPI == kEpiGelu) && kEpiWarps == 4 &&
                            S::kSets * S::kOutTiles * S::kBufBytes >= 4096 * S::kOutTiles;
   auto tail_rows = [&](const GemmGroup& g) -> int {  // N' of the group's tail, 0: none
@@ -521,7 +521,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           const int ka = g.a_k + kb * kBK;
           const int kbb = g.b_k + kb * kBK;
           if (kSwapOk && sw > 0) {  // weights -> A slot, token rows -> B slot
-            if (B_MN) {
+            if (EPI == kEpiSwiglu) {
+              // a1 units [rank * 64, +64) and the same a3 units: h pairs them in one CTA
+              const int nu = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * 64;
+              tma_load_2d_pair(sa, &args.map_b64, &full_bar[stage], kbb, nu);
+              tma_load_2d_pair(sa + 64 * 128, &args.map_b64, &full_bar[stage], kbb, nu + BN / 2);
+            } else if (B_MN) {
 #pragma unroll
               for (int j = 0; j < kBNc / 64; ++j)
                 tma_load_2d_pair(sa + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
@@ -731,6 +736,82 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const int nch = sw / 32;
+        if constexpr (EPI == kEpiSwiglu) {
+          // TMEM lanes 0-63: a1 of units u1 + 0..63, lanes 64-127: a3 of the same units
+          // (u1 = the tile's first unit + rank * 64); warp q < 2 holds a1 of units
+          // u1 + 32 q + lane, warp q + 2 their a3.  Per 32-row chunk the a3 warp hands its
+          // fp32 values to the a1 warp through shared memory (double-buffered by chunk
+          // parity, one 64-thread named barrier per chunk), which computes h as the normal
+          // path does; each warp stores its own a1 / a3 box, the a1 warps the h box.
+          const int u = tc.n_tile * (BN / 2) + static_cast<int>(rank) * 64 + (q & 1) * 32;
+          const int ocol = a13_col(u) + (q >= 2 ? BN / 2 : 0);
+          const int trow = static_cast<int>(g.c_off / args.ldc) + tc.m_tile * (CG * kBM);
+          // staging: the a1 warps 2 tiles per set (a1, h), the a3 warps 1 (a3), which leaves
+          // 8 KB of the a3 warp's region for the exchange buffers
+          static_assert(S::kEpiWarpBytes >= 6 * S::kBufBytes, "SwiGLU swap: staging space");
+          float* xch = reinterpret_cast<float*>(smem + S::kEpiOffset + (q & 1) * S::kEpiWarpBytes +
+                                                2 * S::kBufBytes);
+          const int ot = q < 2 ? 2 : 1;
+          // the staging layout differs from the normal path's: no older store may still read
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll 1
+          for (int ci = 0; ci < nch; ++ci, ++gchunk) {
+            const int b = static_cast<int>(gchunk % S::kSets);
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(acc * BN + ci * 32),
+                               r);
+            tmem_ld_wait();
+            if (ci == nch - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if (!leader)
+                  mbar_arrive_leader(&tempty_bar[acc]);
+                else
+                  mbar_arrive(&tempty_bar[acc]);
+              }
+            }
+            float* xb = xch + (ci & 1) * 1024;  // [32 rows][32 units] fp32
+            if (q >= 2) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) xb[j * 32 + lane] = __uint_as_float(r[j]);
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + (q & 1)) : "memory");
+            if (lane == 0) bulk_wait_read<S::kSets - 1>();
+            __syncwarp();
+            uint8_t* cb = cbuf0 + b * ot * S::kBufBytes;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float a = __uint_as_float(r[j]);
+              const uint32_t o = static_cast<uint32_t>(sw64(j, lane >> 3)) + (lane & 7) * 2;
+              *reinterpret_cast<__nv_bfloat16*>(cb + o) = __float2bfloat16_rn(a);
+              if (q < 2) {  // h = silu(a1) a3 from the fp32 accumulators
+                const float a3 = xb[j * 32 + lane];
+                *reinterpret_cast<__nv_bfloat16*>(cb + S::kBufBytes + o) =
+                    __float2bfloat16_rn(__fdividef(a, 1.f + __expf(-a)) * a3);
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(cmap, cb, ocol, trow + ci * 32);
+              if (q < 2) tma_store_2d(&map_x, cb + S::kBufBytes, u, trow + ci * 32);
+              bulk_commit();
+            }
+          }
+          // back to the normal layout: this tile's stores have read their staging, and the
+          // a1 warp is done with the exchange buffers before the a3 warp reuses its region
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + (q & 1)) : "memory");
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+          continue;
+        }
 #pragma unroll 1
         for (int ci = 0; ci < nch; ++ci, ++gchunk) {
           const int b = static_cast<int>(gchunk % S::kSets);
@@ -1206,6 +1287,10 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   }
   rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / (cg == 4 ? 2 : cg), kDtBF16, 128);
   if (rc != kOk) return rc;
+  if (la.swap_tail && epi == kEpiSwiglu && !b_mn) {  // 64-row boxes: a1 / a3 unit halves
+    rc = make_tmap_2d(&la.map_b64, b, b_inner, b_outer, 64, 64, kDtBF16, 128);
+    if (rc != kOk) return rc;
+  }
   rc = epilogue_tmap(epi, args.c, args.ldc, c_rows, &mc);
   if (rc != kOk) return rc;
   // second tensor: GeLU's post-activation (same shape as C), SwiGLU's h (half the width of

@@ -612,7 +612,8 @@ def test_split_tail_equals_full_tiles(case):
     assert outs[0][0].abs().sum() > 0
 
 
-@pytest.mark.parametrize("case", ["bf16", "bf16_mnB", "gelu", "dgelu_mnB", "dswiglu_mnB"])
+@pytest.mark.parametrize("case", ["bf16", "bf16_mnB", "gelu", "dgelu_mnB", "dswiglu_mnB",
+                                  "swiglu"])
 def test_swap_tail_equals_full_tiles(case):
     """FSSDP_GEMM_SWAP_TAIL: a group's last M tile whose real rows end within 192 rows runs
     as D^T = W X^T with N' = rows rounded up to 64.  Every REAL row equals the full-tile
@@ -633,30 +634,34 @@ def test_swap_tail_equals_full_tiles(case):
         A[r0:r0 + r] = torch.randn(r, K, device=dev).bfloat16()
         r0 += p
     b_mn = case in ("dgelu_mnB", "bf16_mnB", "dswiglu_mnB")
-    # dSwiGLU: N = d_ff (h space), C and aux = the interleaved [a1 | a3] layout, 2 N wide
-    W = 2 * N_ if case == "dswiglu_mnB" else N_
+    # dSwiGLU: N = d_ff (h space), C and aux = the interleaved [a1 | a3] layout, 2 N wide;
+    # SwiGLU: N = 2 d_ff (the interleaved [a1 | a3] weight rows), C the same, C2 = h
+    W = 2 * N_ if case in ("dswiglu_mnB", "swiglu") else N_
+    NG = W if case == "swiglu" else N_  # the GEMM's N
     if b_mn:
-        B = (torch.randn(G * K, N_, device=dev) / K ** 0.5).bfloat16()
+        B = (torch.randn(G * K, NG, device=dev) / K ** 0.5).bfloat16()
     else:
-        B = (torch.randn(G * N_, K, device=dev) / K ** 0.5).bfloat16()
+        B = (torch.randn(G * NG, K, device=dev) / K ** 0.5).bfloat16()
     g = np.zeros(G, dtype=ops.GROUP_DTYPE)
     r0 = 0
     for i, (r, p) in enumerate(zip(rows, pad)):
         g["m_tiles"][i], g["a_m"][i], g["k_blocks"][i] = p // 128, r0, K // 64
-        g["b_n"][i], g["b_k"][i] = (0, i * K) if b_mn else (i * N_, 0)
+        g["b_n"][i], g["b_k"][i] = (0, i * K) if b_mn else (i * NG, 0)
         g["c_off"][i], g["rows"][i] = r0 * W, r
         r0 += p
-    total = ops.finalize_groups(g, N_ // 256)
+    total = ops.finalize_groups(g, NG // 256)
     gd = torch.from_numpy(g.view(np.uint8).copy()).to(dev)
     epi = {"bf16": ops.EPI_BF16, "bf16_mnB": ops.EPI_BF16, "gelu": ops.EPI_GELU,
-           "dgelu_mnB": ops.EPI_DGELU, "dswiglu_mnB": ops.EPI_DSWIGLU}[case]
+           "dgelu_mnB": ops.EPI_DGELU, "dswiglu_mnB": ops.EPI_DSWIGLU,
+           "swiglu": ops.EPI_SWIGLU}[case]
     aux = (torch.randn(R, W, device=dev).bfloat16()
            if case in ("dgelu_mnB", "dswiglu_mnB") else None)
     outs = []
     for st in (False, True, True):
         C = torch.full((R, W), 7.0, device=dev, dtype=torch.bfloat16)
-        C2 = torch.full((R, N_), 7.0, device=dev, dtype=torch.bfloat16) if case == "gelu" else None
-        ops.grouped_gemm(A, False, B, b_mn, gd, G, N_ // 256, total, C, W, epilogue=epi,
+        C2 = (torch.full((R, N_), 7.0, device=dev, dtype=torch.bfloat16)
+              if case in ("gelu", "swiglu") else None)
+        ops.grouped_gemm(A, False, B, b_mn, gd, G, NG // 256, total, C, W, epilogue=epi,
                          c2=C2, aux=aux, n_fastest=True, cta_pair=True, swap_tail=st)
         torch.cuda.synchronize()
         outs.append((C, C2))
