@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests/test_gemm_gpu.py -q -x -k swap 2>&1 | tail -3
-timeout 300 python scripts/swap_probe.py
-bash scripts/ab_env.sh "FSSDP_SWAP_TAIL=dgrad2,fwd2,dgrad1" "FSSDP_X=1" 4 --config cfg4
+for v in build/v_nohoist.so paper_2502_02581_b200/libfssdp.so build/v_nohoist.so paper_2502_02581_b200/libfssdp.so; do FSSDP_LIB=$v python scripts/kernel_bench.py 2>&1 | grep KBENCH | cut -c1-150; done
+bash scripts/ab_env.sh "FSSDP_LIB=build/v_nohoist.so" "FSSDP_X=1" 3
