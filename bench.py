@@ -629,7 +629,6 @@ def run_ours(args):
             for ev in done_ev:
                 ev.record(main_s)
             prefetch(0)
-            prev = None
             for i in range(n):
                 b = i % 2
                 main_s.wait_event(in_ev[b])
@@ -637,16 +636,15 @@ def run_ours(args):
                 fwd_ev[b].record(main_s)
                 if i + 1 < n:  # next inputs stream in while this step computes
                     prefetch(i + 1)
-                if prev is not None:  # the previous step's dx streams out
-                    d2h(*prev)
                 d2h(y, yh[b], fwd_ev[b])  # this step's y, behind its forward
                 main_s.wait_event(in_dy_ev[b])  # the forward only needed x
                 dx = layer.backward(dyb[b])
+                # dx is final once the dX combine ran (layer.dx_event), while the last
+                # wgrads still compute: it streams out from there
+                d2h(dx, dxh[b], layer.dx_event)
                 layer.reduce_gate_grad()
                 layer.planner.finish()
                 done_ev[b].record(main_s)
-                prev = (dx, dxh[b], done_ev[b])
-            d2h(*prev)
             main_s.wait_stream(copy_s)
             main_s.wait_stream(d2h_s)
 
@@ -665,10 +663,11 @@ def run_ours(args):
         nb = T * CFG2["d_model"] * 2
         e2e = {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "ms_per_step": e2e_ms,
-               "pipeline": "x, dy of step i+1 H2D and y of step i, dx of step i-1 D2H on two "
-                           "copy streams (PCIe full duplex), overlapped with step i's compute "
+               "pipeline": "x, dy of step i+1 H2D and y, dx of step i D2H on two copy "
+                           "streams (PCIe full duplex), overlapped with the compute "
                            "(FssdpMoE.forward/backward; the forward waits for x only, the "
-                           "backward for dy); two distinct host batches alternate"}
+                           "backward for dy; y streams out after the forward, dx after the "
+                           "dX combine, layer.dx_event); two distinct host batches alternate"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1153,7 +1153,19 @@ class FssdpMoE:
         self._gemm("wgrad2", self.dyrecv, True, self.h, True, grads2d, f, self.epi_wgrad,
                    part="rest")
 
+    # dx_event: recorded right after the dX combine on the stream that ran it — dx is final
+    # there, well before backward() returns (the remaining wgrads, SpRS and the end barrier
+    # follow): a caller can stream dx out (or into the previous layer's backward) from it
+    dx_event = None
+
     def phase_combine_dx(self, dx: torch.Tensor | None = None) -> torch.Tensor:
+        dx = self._combine_dx(dx)
+        if self.dx_event is None:
+            self.dx_event = torch.cuda.Event()
+        self.dx_event.record(torch.cuda.current_stream(self.dev))
+        return dx
+
+    def _combine_dx(self, dx: torch.Tensor | None = None) -> torch.Tensor:
         if dx is None:
             dx = torch.empty(self.T, self.g.d_model, dtype=torch.bfloat16, device=self.dev)
         if self._late_dots:
