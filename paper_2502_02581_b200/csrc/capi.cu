@@ -109,6 +109,47 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t oute
   return rc;
 }
 
+int make_tmap_mn3d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int nchunks) {
+  static std::mutex mu;
+  static std::map<TmapKey, CUtensorMap> cache;
+  const TmapKey key{base, inner, outer, -nchunks, 64, kDtBF16, 128};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *map = it->second;
+      return kOk;
+    }
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return kErrCuda;
+  }
+  if (inner <= 0 || outer <= 0 || inner % 64 != 0 || nchunks <= 0 ||
+      (reinterpret_cast<uintptr_t>(base) & 15) != 0) {
+    set_error("tensor map (3-D): bad extents or misaligned base");
+    return kErrDimension;
+  }
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(outer), static_cast<cuuint64_t>(inner / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * 2), 128};
+  cuuint32_t box[3] = {64, 64, static_cast<cuuint32_t>(nchunks)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (3-D) failed (%d)", static_cast<int>(r));
+    set_error(buf);
+    return kErrCuda;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *map;
+  return kOk;
+}
+
 static int make_tmap_2d_uncached(CUtensorMap* map, const void* base, int64_t inner, int64_t outer,
                                  int box_inner, int box_outer, int dtype, int swizzle_bytes) {
   EncodeTiledFn fn = encode_fn();

@@ -50,6 +50,8 @@ struct GemmLaunch {
   CUtensorMap map_c64;       // wide_store: C with 32 x 64 boxes (SWIZZLE_128B)
   CUtensorMap map_x64;       // wide_store, GeLU: the second output, same boxes
   CUtensorMap map_b64;       // swap_tail, SwiGLU: B with 64-row boxes (a1 / a3 unit halves)
+  int mn3d_a, mn3d_b;        // MN-major A / B staged by one 3-D load per stage (map_a3/b3)
+  CUtensorMap map_a3, map_b3;
 };
 
 int num_sms();
@@ -86,6 +88,9 @@ inline void timing_end() {
 constexpr int kDtBF16 = 0;
 constexpr int kDtF32 = 1;
 int epilogue_tmap(int epi, const void* base, int64_t ldc, int64_t rows, CUtensorMap* map);
+// MN-major bf16 operand [outer][inner] as {64, outer, inner / 64}: box {64, 64, nchunks},
+// SWIZZLE_128B — the smem image of nchunks consecutive 64 x 64 2-D boxes
+int make_tmap_mn3d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int nchunks);
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_inner,
                  int box_outer, int dtype, int swizzle_bytes);
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,

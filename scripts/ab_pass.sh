@@ -1,7 +1,8 @@
+FSSDP_GEMM_MN3D=1 timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_layer_gpu.py tests/test_configs_gpu.py -q -x 2>&1 | tail -2
 for i in 1 2 3; do for v in 0 1; do
-FSSDP_GEMM_WIDE_STORE=$v python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "
+FSSDP_GEMM_MN3D=$v python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); p=d['phase_ms_per_step']
-print('wide=$v', round(d['ms_per_step'],4), 'fwd1', p['gemm.fwd1'], 'fwd2', p['gemm.fwd2'], 'dgrad2', p['gemm.dgrad2'])"
+print('mn3d=$v', round(d['ms_per_step'],4), *[(k[5:], p[k]) for k in sorted(p) if k.startswith('gemm')])"
 done; done
-for v in 0 1; do FSSDP_GEMM_WIDE_STORE=$v TAG=wide$v python scripts/epi_probe.py | head -1; done
+bash scripts/ab_env.sh "FSSDP_GEMM_MN3D=0" "FSSDP_GEMM_MN3D=1" 2 --config cfg4
