@@ -110,9 +110,14 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t oute
 }
 
 int make_tmap_mn3d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int nchunks) {
+  return make_tmap_3d(map, base, inner, outer, 64, nchunks);
+}
+
+int make_tmap_3d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_rows,
+                 int nchunks) {
   static std::mutex mu;
   static std::map<TmapKey, CUtensorMap> cache;
-  const TmapKey key{base, inner, outer, -nchunks, 64, kDtBF16, 128};
+  const TmapKey key{base, inner, outer, -nchunks, box_rows, kDtBF16, 128};
   {
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
@@ -133,7 +138,7 @@ int make_tmap_mn3d(CUtensorMap* map, const void* base, int64_t inner, int64_t ou
   }
   cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(outer), static_cast<cuuint64_t>(inner / 64)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * 2), 128};
-  cuuint32_t box[3] = {64, 64, static_cast<cuuint32_t>(nchunks)};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(nchunks)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -52,6 +52,7 @@ struct GemmLaunch {
   CUtensorMap map_b64;       // swap_tail, SwiGLU: B with 64-row boxes (a1 / a3 unit halves)
   int mn3d_a, mn3d_b;        // MN-major A / B staged by one 3-D load per stage (map_a3/b3)
   CUtensorMap map_a3, map_b3;
+  CUtensorMap map_ak, map_bk;  // FSSDP_GEMM_BK = 128: K-major A / B, 2 K chunks per load
 };
 
 int num_sms();
@@ -91,6 +92,10 @@ int epilogue_tmap(int epi, const void* base, int64_t ldc, int64_t rows, CUtensor
 // MN-major bf16 operand [outer][inner] as {64, outer, inner / 64}: box {64, 64, nchunks},
 // SWIZZLE_128B — the smem image of nchunks consecutive 64 x 64 2-D boxes
 int make_tmap_mn3d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int nchunks);
+// the same with box {64, box_rows, nchunks}: a K-major operand's kBK = 64 * nchunks K block
+// (chunks of 64 K elements, each box_rows rows of 128 B), or an MN-major one's 128 K rows
+int make_tmap_3d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_rows,
+                 int nchunks);
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int box_inner,
                  int box_outer, int dtype, int swizzle_bytes);
 int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_inner,

@@ -48,7 +48,21 @@ __device__ unsigned long long g_gemm_prof[1024][8];
 #endif
 
 constexpr int kBM = 128;  // rows per CTA
-constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16
+// K per pipeline stage: 64 (one 128-byte swizzle atom of bf16) or 128 — two atoms staged by
+// ONE 3-D TMA load per operand (half the load instructions per byte; fewer, larger stages).
+// FSSDP_GEMM_BK: 0 = per GEMM (below), 64 / 128 = every CTA-pair GEMM (experiments).
+// 128 pays where B is MN-major and the epilogue leaves three 64 KB stages — dgrad1 (bf16)
+// and dgrad2 (dGeLU): cfg2 step -1.7 % (dgrad1 -10 %, dgrad2 -4 %), while the K-major and
+// the MN/MN GEMMs lose 1-3 % with half as many stages, and cfg4's SwiGLU epilogues (two
+// stages) 1 % per step (interleaved A/B).  Single-CTA tiles keep 64 (shared memory).
+#ifndef FSSDP_GEMM_BK
+#define FSSDP_GEMM_BK 0
+#endif
+constexpr int k_block(bool a_mn, bool b_mn, int epi, int cg) {
+  return cg < 2 ? 64
+         : FSSDP_GEMM_BK != 0 ? FSSDP_GEMM_BK
+         : (!a_mn && b_mn && (epi == FSSDP_EPI_BF16 || epi == FSSDP_EPI_DGELU)) ? 128 : 64;
+}
 // Epilogue warps: 4 (one per TMEM lane quarter), or 8 (two per quarter, column halves)
 // for the GeLU epilogue, whose per-element math otherwise outlasts a K = d_model mainloop
 // (the extra staging smem costs one mainloop stage).
@@ -76,9 +90,11 @@ constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store
 // SMs are shared with a co-running kernel, simply take fewer tiles.
 constexpr int kSched = 8;
 
-template <int BN, int EPI, int CG>
+template <int BN, int EPI, int CG, int BK = 64>
 struct GemmSmem {
   static constexpr int kEpiWarps = epi_warps<EPI>();
+  static constexpr int kBK = BK;             // K per stage
+  static constexpr int kKC = kBK / 64;       // 64-wide K chunks per stage
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -93,7 +109,8 @@ struct GemmSmem {
   static constexpr int kSets = EPI == kEpiF32 ? FSSDP_F32_SETS : EPI == kEpiGelu ? FSSDP_GELU_SETS : 2;
   static constexpr int kCBufs = kSets * kOutTiles;
   // aux-tile prefetch ring (dgrad2): entries of one tile (GeLU') or two (a1, a3)
-  static constexpr int kAuxBufs = EPI == kEpiDGelu ? (CG == 2 ? 4 : 2) : EPI == kEpiDSwiglu ? 2 : 0;
+  static constexpr int kAuxBufs =
+      EPI == kEpiDGelu ? (CG == 2 && BK == 64 ? 4 : 2) : EPI == kEpiDSwiglu ? 2 : 0;
   static constexpr int kAuxTiles = EPI == kEpiDSwiglu ? 2 : 1;
   static constexpr int kEpiWarpBytes = (kCBufs + kAuxBufs * kAuxTiles) * kBufBytes;
   // as many mainloop stages (up to 6) as the 227 KB budget leaves
@@ -233,8 +250,10 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                         const __grid_constant__ GemmLaunch args) {
   constexpr int CG = CGX == 4 ? 2 : CGX;  // CTAs per tile
   constexpr int CL = CGX == 4 ? 2 : 1;    // tiles (pairs) per cluster
-  using S = GemmSmem<BN, EPI, CG>;
+  using S = GemmSmem<BN, EPI, CG, k_block(A_MN, B_MN, EPI, CG)>;
   constexpr int kStages = S::kStages;
+  constexpr int kBK = S::kBK;
+  constexpr int kKC = S::kKC;
   constexpr int kBNc = BN / CG;  // B columns staged by this CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -507,7 +526,22 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                        static_cast<int>(rank) * (half >= 0 ? kBNc / 2 : kBNc);
         // swapped: this CTA's N'/2 token rows of the tile (into its B slot)
         const int sm0 = g.a_m + tc.m_tile * (CG * kBM) + static_cast<int>(rank) * (sw / 2);
-        for (int kb = 0; kb < g.k_blocks; ++kb) {
+        // K-major operand (rows x kBK): one 2-D load, or kKC chunks by one 3-D load
+        auto kmaj = [&](uint8_t* dst, const CUtensorMap* m2, const CUtensorMap* m3, int k, int row) {
+          if (kKC == 1) {
+            if (CG == 2)
+              tma_load_2d_pair(dst, m2, &full_bar[stage], k, row);
+            else
+              tma_load_2d(dst, m2, &full_bar[stage], k, row);
+          } else {
+            if (CG == 2)
+              tma_load_3d_pair(dst, m3, &full_bar[stage], 0, row, k / 64);
+            else
+              tma_load_3d(dst, m3, &full_bar[stage], 0, row, k / 64);
+          }
+        };
+        const int nkb = (g.k_blocks + kKC - 1) / kKC;
+        for (int kb = 0; kb < nkb; ++kb) {
           PROF_T0(tw);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           PROF_ADD(1, tw);
@@ -524,8 +558,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
             if (EPI == kEpiSwiglu) {
               // a1 units [rank * 64, +64) and the same a3 units: h pairs them in one CTA
               const int nu = g.b_n + tc.n_tile * BN + static_cast<int>(rank) * 64;
-              tma_load_2d_pair(sa, &args.map_b64, &full_bar[stage], kbb, nu);
-              tma_load_2d_pair(sa + 64 * 128, &args.map_b64, &full_bar[stage], kbb, nu + BN / 2);
+#pragma unroll
+              for (int c = 0; c < kKC; ++c) {
+                uint8_t* d = sa + c * (kBM * 128);
+                tma_load_2d_pair(d, &args.map_b64, &full_bar[stage], kbb + 64 * c, nu);
+                tma_load_2d_pair(d + 64 * 128, &args.map_b64, &full_bar[stage], kbb + 64 * c,
+                                 nu + BN / 2);
+              }
             } else if (B_MN) {
               if (args.mn3d_b) {
                 tma_load_3d_pair(sa, &args.map_b3, &full_bar[stage], 0, kbb, n0 / 64);
@@ -535,10 +574,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                   tma_load_2d_pair(sa + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
               }
             } else {
-              tma_load_2d_pair(sa, &map_b, &full_bar[stage], kbb, n0);
+              kmaj(sa, &map_b, &args.map_bk, kbb, n0);
             }
-            for (int j = 0; j < sw / 64; ++j)  // this CTA's sw / 2 rows, 32 per box
-              tma_load_2d_pair(sb + j * 32 * 128, &args.map_a32, &full_bar[stage], ka, sm0 + 32 * j);
+            for (int c = 0; c < kKC; ++c)
+              for (int j = 0; j < sw / 64; ++j)  // this CTA's sw / 2 rows, 32 per box
+                tma_load_2d_pair(sb + c * (sw / 2) * 128 + j * 32 * 128, &args.map_a32,
+                                 &full_bar[stage], ka + 64 * c, sm0 + 32 * j);
           } else if (CG == 2) {
             if (CL == 2) {  // the first pair loads A for both: CTA r -> CTAs r and r + 2
               if (pair == 0) {
@@ -549,7 +590,10 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                     tma_load_2d_pair_mc(sa + j * (kBK * 128), &map_a, &full_bar[stage],
                                         m0 + 64 * j, ka, mc);
                 } else {
-                  tma_load_2d_pair_mc(sa, &map_a, &full_bar[stage], ka, m0, mc);
+#pragma unroll
+                  for (int c = 0; c < kKC; ++c)
+                    tma_load_2d_pair_mc(sa + c * (kBM * 128), &map_a, &full_bar[stage],
+                                        ka + 64 * c, m0, mc);
                 }
               }
             } else if (A_MN) {
@@ -561,7 +605,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                   tma_load_2d_pair(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
               }
             } else {
-              tma_load_2d_pair(sa, &map_a, &full_bar[stage], ka, m0);
+              kmaj(sa, &map_a, &args.map_ak, ka, m0);
             }
             if (B_MN) {
               if (args.mn3d_b && half < 0) {
@@ -572,7 +616,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                   tma_load_2d_pair(sb + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
               }
             } else {
-              tma_load_2d_pair(sb, &map_b, &full_bar[stage], kbb, n0);
+              kmaj(sb, &map_b, &args.map_bk, kbb, n0);
             }
           } else {
             if (A_MN) {
@@ -580,14 +624,14 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               for (int j = 0; j < kBM / 64; ++j)
                 tma_load_2d(sa + j * (kBK * 128), &map_a, &full_bar[stage], m0 + 64 * j, ka);
             } else {
-              tma_load_2d(sa, &map_a, &full_bar[stage], ka, m0);
+              kmaj(sa, &map_a, &args.map_ak, ka, m0);
             }
             if (B_MN) {
 #pragma unroll
               for (int j = 0; j < kBNc / 64; ++j)
                 tma_load_2d(sb + j * (kBK * 128), &map_b, &full_bar[stage], n0 + 64 * j, kbb);
             } else {
-              tma_load_2d(sb, &map_b, &full_bar[stage], kbb, n0);
+              kmaj(sb, &map_b, &args.map_bk, kbb, n0);
             }
           }
           if (++stage == kStages) {
@@ -630,28 +674,38 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         PROF_INC(7);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        const int nkb = (kblocks + kKC - 1) / kKC;
+        for (int kb = 0; kb < nkb; ++kb) {
           PROF_T0(tf);
           mbar_wait(&full_bar[stage], phase);
           PROF_ADD(2, tf);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * S::kStageBytes);
           const uint32_t b_base = a_base + S::kABytes;
+          // a K block count that is not a multiple of kKC: the last stage's extra chunk
+          // (staged, possibly stale or zero) is not multiplied
+          const int kk_end = (kKC == 2 && kb == nkb - 1 && (kblocks & 1)) ? 4 : kBK / 16;
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
+            if (kk >= kk_end) break;
+            // K-major: 16 K elements = 32 B inside the 128-B swizzled row, chunk kk / 4 at
+            // (staged rows) * 128 B; MN-major: 16 K rows = 2048 B, MN chunks at kBK * 128 B
+            const uint32_t kofs = static_cast<uint32_t>((kk & 3) * 32);
+            const uint32_t kch = static_cast<uint32_t>(kk >> 2);
             uint64_t adesc, bdesc;
-            if (A_MN)  // 16 K rows = 2048 B per step; MN chunks of 64 at kBK*128 B
+            if (A_MN)
               adesc = make_sdesc_sw128(a_base + kk * 2048, kBK * 128, 1024);
-            else  // 16 K elements = 32 B inside the 128-B swizzled row
-              adesc = make_sdesc_sw128(a_base + kk * 32, 16, 1024);
+            else
+              adesc = make_sdesc_sw128(a_base + kch * (kBM * 128) + kofs, 16, 1024);
             if (B_MN)
               bdesc = make_sdesc_sw128(b_base + kk * 2048, kBK * 128, 1024);
             else
-              bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
+              bdesc = make_sdesc_sw128(b_base + kch * (kBNc * 128) + kofs, 16, 1024);
             if (kSwapOk && sw > 0) {  // the A slot holds B's operand and vice versa
               adesc = B_MN ? make_sdesc_sw128(a_base + kk * 2048, kBK * 128, 1024)
-                           : make_sdesc_sw128(a_base + kk * 32, 16, 1024);
-              bdesc = make_sdesc_sw128(b_base + kk * 32, 16, 1024);
+                           : make_sdesc_sw128(a_base + kch * (kBM * 128) + kofs, 16, 1024);
+              bdesc = make_sdesc_sw128(b_base + kch * static_cast<uint32_t>(sw / 2 * 128) + kofs,
+                                       16, 1024);
             }
             if (CG == 2)
               umma_bf16_pair(d_tmem, adesc, bdesc, tdesc, (kb | kk) ? 1u : 0u);
@@ -1159,7 +1213,7 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
                           const CUtensorMap& mx, const GemmLaunch& args, cudaStream_t stream) {
   constexpr int CG = CGX == 4 ? 2 : CGX;
   auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI, CGX>;
-  const int smem = GemmSmem<BN, EPI, CG>::kDynamic;
+  const int smem = GemmSmem<BN, EPI, CG, k_block(A_MN, B_MN, EPI, CG)>::kDynamic;
   if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem) != cudaSuccess)
     return kErrCuda;
   // work units: tiles of CG*128 rows (CGX = 4: pairs of N tiles); a device-side total (-1)
@@ -1290,15 +1344,25 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
     return kErrDimension;  // A multicast: N-fastest pairs of 256-wide N tiles, static order
   CUtensorMap ma, mb, mc, mx;
   // K-major operand: box = {64 K elems, rows};  MN-major: box = {64 MN elems, 64 K rows}
-  int rc = make_tmap_2d(&ma, a, a_inner, a_outer, 64, a_mn ? 64 : kBM, kDtBF16, 128);
+  // MN-major 2-D boxes: {64 MN, kBK K rows}
+  const int kBK = k_block(a_mn != 0, b_mn != 0, epi, cg), kKC = kBK / 64;
+  int rc = make_tmap_2d(&ma, a, a_inner, a_outer, 64, a_mn ? kBK : kBM, kDtBF16, 128);
   if (rc != kOk) return rc;
   GemmLaunch la = args;
+  if (kKC == 2 && !a_mn) {  // K-major A: kBM rows x 2 K chunks per load
+    rc = make_tmap_3d(&la.map_ak, a, a_inner, a_outer, kBM, kKC);
+    if (rc != kOk) return rc;
+  }
   if (la.swap_tail && !a_mn) {  // 32-row boxes: a swapped tail stages only its rows
     rc = make_tmap_2d(&la.map_a32, a, a_inner, a_outer, 64, 32, kDtBF16, 128);
     if (rc != kOk) return rc;
   }
-  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? 64 : BN / (cg == 4 ? 2 : cg), kDtBF16, 128);
+  rc = make_tmap_2d(&mb, b, b_inner, b_outer, 64, b_mn ? kBK : BN / (cg == 4 ? 2 : cg), kDtBF16, 128);
   if (rc != kOk) return rc;
+  if (kKC == 2 && !b_mn) {
+    rc = make_tmap_3d(&la.map_bk, b, b_inner, b_outer, BN / (cg == 4 ? 2 : cg), kKC);
+    if (rc != kOk) return rc;
+  }
   // MN-major operands (the wgrads' A and B, the dgrads' weights) staged by ONE 3-D load
   // per stage instead of one 2-D load per 64-wide chunk: half the TMA requests of those
   // operands — cfg2 step -1.3 % (wgrad1 -3.5 %, wgrad2 -4 %), cfg4 -1.5 % (interleaved
@@ -1309,12 +1373,12 @@ int grouped_gemm_launch(int a_mn, int b_mn, int epi, const void* a, int64_t a_in
   }();
   if (mn3d && cg == 2) {
     if (a_mn && a_inner % 64 == 0) {
-      rc = make_tmap_mn3d(&la.map_a3, a, a_inner, a_outer, kBM / 64);
+      rc = make_tmap_3d(&la.map_a3, a, a_inner, a_outer, kBK, kBM / 64);
       if (rc != kOk) return rc;
       la.mn3d_a = 1;
     }
     if (b_mn && BN / 2 >= 128 && b_inner % 64 == 0) {
-      rc = make_tmap_mn3d(&la.map_b3, b, b_inner, b_outer, (BN / 2) / 64);
+      rc = make_tmap_3d(&la.map_b3, b, b_inner, b_outer, kBK, (BN / 2) / 64);
       if (rc != kOk) return rc;
       la.mn3d_b = 1;
     }
