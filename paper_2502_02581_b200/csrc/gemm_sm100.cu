@@ -58,10 +58,18 @@ constexpr int kBM = 128;  // rows per CTA
 #ifndef FSSDP_GEMM_BK
 #define FSSDP_GEMM_BK 0
 #endif
+// MN/MN GEMMs (the wgrads): 64 (96 measured neutral: wgrad1 -2 %, wgrad2 +0.5 %; 128 — three
+// stages — slightly slower); FSSDP_GEMM_BK_MNMN overrides (any multiple of 16, MN-major
+// boxes take kBK K rows)
+#ifndef FSSDP_GEMM_BK_MNMN
+#define FSSDP_GEMM_BK_MNMN 64
+#endif
 constexpr int k_block(bool a_mn, bool b_mn, int epi, int cg) {
   return cg < 2 ? 64
          : FSSDP_GEMM_BK != 0 ? FSSDP_GEMM_BK
-         : (!a_mn && b_mn && (epi == FSSDP_EPI_BF16 || epi == FSSDP_EPI_DGELU)) ? 128 : 64;
+         : (!a_mn && b_mn && (epi == FSSDP_EPI_BF16 || epi == FSSDP_EPI_DGELU)) ? 128
+         : (a_mn && b_mn) ? FSSDP_GEMM_BK_MNMN
+                          : 64;
 }
 // Epilogue warps: 4 (one per TMEM lane quarter), or 8 (two per quarter, column halves)
 // for the GeLU epilogue, whose per-element math otherwise outlasts a K = d_model mainloop
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
               tma_load_3d(dst, m3, &full_bar[stage], 0, row, k / 64);
           }
         };
-        const int nkb = (g.k_blocks + kKC - 1) / kKC;
+        const int nkb = (g.k_blocks * 64 + kBK - 1) / kBK;
         for (int kb = 0; kb < nkb; ++kb) {
           PROF_T0(tw);
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -674,7 +682,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
         PROF_INC(7);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        const int nkb = (kblocks + kKC - 1) / kKC;
+        const int nkb = (kblocks * 64 + kBK - 1) / kBK;
         for (int kb = 0; kb < nkb; ++kb) {
           PROF_T0(tf);
           mbar_wait(&full_bar[stage], phase);
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
           const uint32_t b_base = a_base + S::kABytes;
           // a K block count that is not a multiple of kKC: the last stage's extra chunk
           // (staged, possibly stale or zero) is not multiplied
-          const int kk_end = (kKC == 2 && kb == nkb - 1 && (kblocks & 1)) ? 4 : kBK / 16;
+          const int kk_end = min(kBK / 16, (kblocks * 64 - kb * kBK) / 16);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             if (kk >= kk_end) break;
