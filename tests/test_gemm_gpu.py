@@ -679,3 +679,35 @@ def test_swap_tail_equals_full_tiles(case):
         ref = torch.cat([A[sum(pad[:i]):sum(pad[:i]) + pad[i]].float() @
                          B[i * N_:(i + 1) * N_].float().T for i in range(G)])
         _close(outs[1][0][real], ref[real], rel=1e-2, abs_=1e-2)
+
+
+@pytest.mark.parametrize("K", [64, 320, 448])
+@pytest.mark.parametrize("epi", ["bf16", "dgelu"])
+def test_deep_stages_odd_k_blocks(K, epi):
+    """dgrad-style GEMMs (K-major A, MN-major B, bf16 / dGeLU epilogue) run 128-deep K
+    stages: an odd number of 64-wide K blocks leaves the last stage's second chunk staged
+    (here B's rows of the NEXT group, non-zero) but not multiplied."""
+    ops = _ops()
+    dev = "cuda"
+    torch.manual_seed(23)
+    N = 512
+    m_tiles = [2, 4, 2]
+    G = len(m_tiles)
+    R = sum(m_tiles) * 128
+    A = torch.randn(R, K, device=dev).bfloat16()
+    B = (torch.randn(G * K, N, device=dev) / K ** 0.5).bfloat16()
+    C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    aux = torch.randn(R, N, device=dev).bfloat16() if epi == "dgelu" else None
+    rows, refs, r0 = [], [], 0
+    for g, mt in enumerate(m_tiles):
+        rows.append((mt, r0, 0, 0, g * K, K // 64, r0 * N))
+        refs.append((slice(r0, r0 + mt * 128),
+                     A[r0:r0 + mt * 128].float() @ B[g * K:(g + 1) * K].float()))
+        r0 += mt * 128
+    gd, ng, total = _groups(ops, rows, N // 256, dev)
+    ops.grouped_gemm(A, False, B, True, gd, ng, N // 256, total, C, N,
+                     epilogue=ops.EPI_DGELU if epi == "dgelu" else ops.EPI_BF16, aux=aux,
+                     n_fastest=True, cta_pair=True)
+    torch.cuda.synchronize()
+    for sl, ref in refs:
+        _close(C[sl], ref * aux[sl].float() if epi == "dgelu" else ref)
