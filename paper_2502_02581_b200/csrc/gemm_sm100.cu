@@ -83,13 +83,23 @@ constexpr int k_block(bool a_mn, bool b_mn, int epi, int cg) {
 #ifndef FSSDP_GELU_SETS
 #define FSSDP_GELU_SETS 2
 #endif
-template <int EPI>
+// The bf16-output MN/MN GEMMs (the weight gradients): 8 epilogue warps, two per TMEM lane
+// quarter on column halves — with K = one expert's token rows, short-K tiles outrun a
+// 4-warp epilogue (cfg4's 64 fine-grained experts), and their 2 KB staging tiles leave room
+// for 8 warps at 6 stages.  cfg4 step -5.3 % (wgrad1 517 -> 446 us, wgrad2 252 -> 215 us),
+// cfg2 -0.5 % (interleaved A/B).  FSSDP_WGRAD_EPI_WARPS=4 restores one warp per quarter
+#ifndef FSSDP_WGRAD_EPI_WARPS
+#define FSSDP_WGRAD_EPI_WARPS 8
+#endif
+template <int EPI, bool MNMN = false>
 constexpr int epi_warps() {
-  return EPI == FSSDP_EPI_GELU ? FSSDP_GELU_EPI_WARPS : 4;
+  return EPI == FSSDP_EPI_GELU ? FSSDP_GELU_EPI_WARPS
+         : (EPI == FSSDP_EPI_BF16 && MNMN) ? FSSDP_WGRAD_EPI_WARPS
+                                           : 4;
 }
-template <int EPI>
+template <int EPI, bool MNMN = false>
 constexpr int gemm_threads() {
-  return 64 + 32 * epi_warps<EPI>();
+  return 64 + 32 * epi_warps<EPI, MNMN>();
 }
 constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store box)
 // Dynamic tile scheduling (GemmLaunch.sched != null): the (leader) producer takes the next
@@ -98,9 +108,9 @@ constexpr int kEpiCols = 32;  // columns per epilogue chunk (one 32x32 TMA store
 // SMs are shared with a co-running kernel, simply take fewer tiles.
 constexpr int kSched = 8;
 
-template <int BN, int EPI, int CG, int BK = 64>
+template <int BN, int EPI, int CG, int BK = 64, int EW = epi_warps<EPI>()>
 struct GemmSmem {
-  static constexpr int kEpiWarps = epi_warps<EPI>();
+  static constexpr int kEpiWarps = EW;
   static constexpr int kBK = BK;             // K per stage
   static constexpr int kKC = kBK / 64;       // 64-wide K chunks per stage
   static constexpr int kABytes = kBM * kBK * 2;
@@ -250,7 +260,7 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) {  // 128-byte rows, SWI
 // once per cluster and multicast into both pairs (TMA .multicast::cluster), halving the
 // A operand's L2 -> SM traffic.
 template <bool A_MN, bool B_MN, int BN, int EPI, int CGX>
-__global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
+__global__ void __launch_bounds__(gemm_threads<EPI, A_MN && B_MN>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
                         const __grid_constant__ GemmLaunch args) {
   constexpr int CG = CGX == 4 ? 2 : CGX;  // CTAs per tile
   constexpr int CL = CGX == 4 ? 2 : 1;    // tiles (pairs) per cluster
-  using S = GemmSmem<BN, EPI, CG, k_block(A_MN, B_MN, EPI, CG)>;
+  using S = GemmSmem<BN, EPI, CG, k_block(A_MN, B_MN, EPI, CG), epi_warps<EPI, A_MN && B_MN>()>;
   constexpr int kStages = S::kStages;
   constexpr int kBK = S::kBK;
   constexpr int kKC = S::kKC;
@@ -1221,7 +1231,8 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
                           const CUtensorMap& mx, const GemmLaunch& args, cudaStream_t stream) {
   constexpr int CG = CGX == 4 ? 2 : CGX;
   auto kern = grouped_gemm_kernel<A_MN, B_MN, BN, EPI, CGX>;
-  const int smem = GemmSmem<BN, EPI, CG, k_block(A_MN, B_MN, EPI, CG)>::kDynamic;
+  const int smem =
+      GemmSmem<BN, EPI, CG, k_block(A_MN, B_MN, EPI, CG), epi_warps<EPI, A_MN && B_MN>()>::kDynamic;
   if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem) != cudaSuccess)
     return kErrCuda;
   // work units: tiles of CG*128 rows (CGX = 4: pairs of N tiles); a device-side total (-1)
@@ -1235,7 +1246,7 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (cached[dev & 63] == 0) {
       cudaLaunchConfig_t oc = {};
       oc.gridDim = dim3(num_sms());
-      oc.blockDim = dim3(gemm_threads<EPI>());
+      oc.blockDim = dim3(gemm_threads<EPI, A_MN && B_MN>());
       oc.dynamicSmemBytes = smem;
       cudaLaunchAttribute ca[1];
       ca[0].id = cudaLaunchAttributeClusterDimension;
@@ -1257,7 +1268,7 @@ static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   int grid = CGX * (units < max_units ? units : max_units);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(gemm_threads<EPI>());
+  cfg.blockDim = dim3(gemm_threads<EPI, A_MN && B_MN>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   static const bool pdl = [] {
