@@ -1,7 +1,2 @@
-FSSDP_LIB=build/v_wg8.so timeout 600 python -m pytest tests/test_gemm_gpu.py tests/test_layer_gpu.py -q -x 2>&1 | tail -1
-for cfg in cfg4 cfg2; do for i in 1 2; do for v in paper_2502_02581_b200/libfssdp.so build/v_wg8.so; do
-FSSDP_LIB=$v python bench.py --config $cfg --steps 20 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "
-import json,sys
-d=json.loads(sys.stdin.read()); p=d['phase_ms_per_step']
-print('$cfg $v'.ljust(40), round(d['ms_per_step'],4), *[(k[5:], p[k]) for k in sorted(p) if k.startswith('gemm.w')])"
-done; done; done
+timeout 900 python -m pytest tests/test_dist_gpu.py -q -x 2>&1 | tail -1
+NGPU=4 bash scripts/ab_env.sh "FSSDP_EARLY_GATE_REDUCE=0" "FSSDP_EARLY_GATE_REDUCE=1" 3
